@@ -1,0 +1,137 @@
+/* smoe.h — C ABI of the B200 speculative expert-prefetch MoE decode path.
+ *
+ * Drop-in boundary for the reference's decode-path API
+ * (/root/reference/proj/include/specmoe).  Plain pointers and sizes only; no
+ * CUDA or torch types.  Every function returns an int status:
+ *   0 = ok, 1 = invalid argument (the reference throws std::invalid_argument,
+ *   CLI exit 2), 2 = runtime / CUDA error (std::runtime_error, CLI exit 3);
+ * the message is available from smoe_last_error() on the calling thread.
+ * INTEGRATION.md shows the reference-side binding (a C++ shim rethrowing
+ * the matching exception, and a ctypes stub).
+ */
+#ifndef SMOE_H
+#define SMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct smoe_session smoe_session;
+
+/* ModelConfig (model.hpp:28-47).  gating: 0 softmax-topk-renorm, 1 topk-softmax. */
+typedef struct smoe_config {
+    int32_t layers, experts, top_k, hidden, expert_hidden, vocab, head_dim;
+    float eps;
+    uint64_t seed;
+    int32_t gating;
+} smoe_config;
+
+/* Session options.  cache_fraction caps the HBM slot pool per layer at
+ * max(top_k, ceil(cache_fraction * experts)) slots (NEW: the reference keeps
+ * exactly two k-expert buffers, executor.cpp:115-122).  copy_latency_us is
+ * ExecutorOptions::copy_latency_us (executor.hpp:23-29); deadlock_s the
+ * device-side wait limit (the reference's deadlock timeout, executor.cpp:124-128). */
+typedef struct smoe_options {
+    int32_t device;
+    float cache_fraction;
+    int32_t max_positions;
+    int32_t copy_latency_us;
+    double deadlock_s;
+} smoe_options;
+
+/* EstimatorConfig (estimator.hpp:20-39). */
+typedef struct smoe_estimator_config {
+    int32_t d, m, n, experts, layers;
+    float eps;
+} smoe_estimator_config;
+
+/* Predictor kinds (PredictorKind, speculation.hpp:64): -1 none,
+ * 0 baseline-s, 1 router-pf, 2 est-pf, 3 hybrid, 4 oracle. */
+enum { SMOE_PRED_NONE = -1, SMOE_PRED_BASELINE_S = 0, SMOE_PRED_ROUTER_PF = 1,
+       SMOE_PRED_EST_PF = 2, SMOE_PRED_HYBRID = 3, SMOE_PRED_ORACLE = 4 };
+/* OffloadMode (executor.hpp:18). */
+enum { SMOE_ON_DEMAND = 0, SMOE_PREFETCH = 1 };
+
+/* One copy-lane request (MeasuredEvent kCopy, executor.hpp:31-37, plus the
+ * cache outcome).  start/end are device-timed ms from the decode origin. */
+typedef struct smoe_copy_event {
+    int32_t seq, layer, step, hits, misses;
+    int64_t bytes;
+    double start_ms, end_ms;
+} smoe_copy_event;
+
+const char* smoe_last_error(void);
+
+/* Creates a session: allocates the pinned bf16 expert store, HBM slot pool,
+ * dense weights, streams and the copy-scheduler thread.  Replaces building a
+ * Model and the TwoLaneEngine (executor.cpp:41-216). */
+int smoe_session_create(const smoe_config* cfg, const smoe_options* opt, smoe_session** out);
+int smoe_session_destroy(smoe_session* s);
+
+/* build_model (model.cpp:112-158) generated on the GPU, every weight rounded
+ * to bf16 (RNE). */
+int smoe_init_weights_seeded(smoe_session* s);
+/* Loads one f32 tensor of a reference Model by its bundle name
+ * (model.cpp:194-254: "embedding", "layer3.wq", "layer0.expert5.w_down", ...);
+ * rounded to bf16 on the way in. */
+int smoe_load_tensor(smoe_session* s, const char* name, const float* data, int64_t count);
+/* DefaultVectorTable [L][E][H] (speculation.hpp:18-33). */
+int smoe_load_default_vectors(smoe_session* s, const float* d, int64_t count);
+/* EstimatorParams flat layout (estimator.hpp:41-72). */
+int smoe_load_estimator(smoe_session* s, const smoe_estimator_config* c, const float* flat,
+                        int64_t count);
+/* make_predictor (speculation.cpp:330-346).  hybrid_map: layers-1 kind codes
+ * (nullable -> all router-pf), only for SMOE_PRED_HYBRID. */
+int smoe_set_predictor(smoe_session* s, int32_t kind, const int32_t* hybrid_map);
+int smoe_set_cache_fraction(smoe_session* s, float cache_fraction);
+
+/* New decode sequence (DecodeState reset).  max_steps sizes the per-step
+ * record buffers; trace_full = 1 also records s, r, m, logits, gates and raw
+ * expert outputs per (step, layer) (LayerTraceRecord, model.hpp:94-103). */
+int smoe_reset(smoe_session* s, int32_t max_steps, int32_t trace_full);
+/* Prefill with true routing, one forward_decode per token (model.cpp:355-389). */
+int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n);
+/* n_steps greedy decode steps on the device (speculative_forward semantics in
+ * SMOE_PREFETCH mode, forward_decode in SMOE_ON_DEMAND mode). */
+int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph);
+/* run_offloaded_decode (executor.cpp:326-359): prefill + n_new-1 decode steps;
+ * out_tokens[n_new]; per_token_ms[n_new-1] (device-timed, nullable). */
+int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
+                              int32_t n_new, int32_t mode, int32_t* out_tokens,
+                              double* per_token_ms);
+/* One host-driven step: token in, logits[vocab] out, returns the argmax token
+ * through *next (end-to-end API: H2D of the token, D2H of the logits). */
+int smoe_step(smoe_session* s, int32_t mode, int32_t token, float* logits_out, int32_t* next);
+/* accumulate_default_vectors over random_token_stream(ntok, vocab, seed) with
+ * resets every seq_len tokens (speculation.cpp:23-83, trace.cpp:187-211), on
+ * the GPU; loads the table into the session and copies it out (nullable). */
+int smoe_calibrate(smoe_session* s, int64_t ntok, uint64_t seed, int32_t seq_len,
+                   float* d_out, int64_t* counts_out);
+
+/* Results. */
+int smoe_steps_done(smoe_session* s, int32_t* n);
+int smoe_read_tokens(smoe_session* s, int32_t* out, int32_t n);
+/* field: id_true, id_exec, id_pred ([steps][L][K] int32), g_true, g_exec,
+ * g_pred ([steps][L][K]), s, r, m ([steps][L][H]), lg_true, lg_pred
+ * ([steps][L][E]; lg_pred row l = prediction for layer l), y ([steps][L][K][H]),
+ * logits ([steps][vocab]). */
+int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n_elems);
+int smoe_token_ms(smoe_session* s, double* out, int32_t cap, int32_t* n);
+/* Per-layer cache hits/misses [L], total H2D bytes, summed copy-lane busy ms,
+ * number of copy requests. */
+int smoe_counters(smoe_session* s, int64_t* hits, int64_t* misses, int64_t* h2d_bytes,
+                  double* copy_ms, int32_t* requests);
+int smoe_copy_events(smoe_session* s, smoe_copy_event* out, int32_t cap, int32_t* n);
+/* Slots per layer actually allocated. */
+int smoe_cache_slots(smoe_session* s, int32_t* slots);
+/* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */
+int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMOE_H */

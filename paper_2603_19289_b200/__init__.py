@@ -1,0 +1,10 @@
+"""B200-native speculative expert-prefetch MoE decode path (arXiv 2603.19289).
+
+The product is libsmoe_b200.so (paper_2603_19289_b200/csrc, C ABI in
+include/smoe.h); this package only binds it.
+"""
+from .engine import (EXPORTS, GATING, MODE, PRED, CopyEvent, ModelConfig, Session, SmoeError,
+                     load_library)
+
+__all__ = ["EXPORTS", "GATING", "MODE", "PRED", "CopyEvent", "ModelConfig", "Session",
+           "SmoeError", "load_library"]

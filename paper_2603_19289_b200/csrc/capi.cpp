@@ -1,0 +1,233 @@
+// capi.cpp — extern "C" boundary (include/smoe.h) over the C++ Session.
+// Exceptions never cross the ABI: std::invalid_argument -> 1, others -> 2,
+// message kept in a thread-local string (the reference's exception
+// convention, SURVEY §8b "Errors").
+#include "../../include/smoe.h"
+
+#include "engine.h"
+
+#include <cstring>
+#include <string>
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    } catch (...) {
+        g_err = "unknown error";
+        return 2;
+    }
+}
+
+smoe::Session* S(smoe_session* s) {
+    if (!s) throw std::invalid_argument("null session");
+    return reinterpret_cast<smoe::Session*>(s);
+}
+}  // namespace
+
+extern "C" {
+
+const char* smoe_last_error(void) { return g_err.c_str(); }
+
+int smoe_session_create(const smoe_config* cfg, const smoe_options* opt, smoe_session** out) {
+    return guard([&] {
+        if (!cfg || !out) throw std::invalid_argument("null argument");
+        smoe::ModelCfg c{cfg->layers, cfg->experts, cfg->top_k, cfg->hidden, cfg->expert_hidden,
+                         cfg->vocab, cfg->head_dim, cfg->eps, cfg->seed, cfg->gating};
+        smoe::SessionOpts o;
+        if (opt) {
+            o.device = opt->device;
+            o.cache_fraction = opt->cache_fraction;
+            o.max_positions = opt->max_positions;
+            o.copy_latency_us = opt->copy_latency_us;
+            o.deadlock_s = opt->deadlock_s > 0 ? opt->deadlock_s : 10.0;
+        }
+        *out = reinterpret_cast<smoe_session*>(new smoe::Session(c, o));
+    });
+}
+
+int smoe_session_destroy(smoe_session* s) {
+    return guard([&] { delete S(s); });
+}
+
+int smoe_init_weights_seeded(smoe_session* s) {
+    return guard([&] { S(s)->init_weights_seeded(); });
+}
+
+int smoe_load_tensor(smoe_session* s, const char* name, const float* data, int64_t count) {
+    return guard([&] {
+        if (!name || !data) throw std::invalid_argument("null argument");
+        S(s)->load_tensor(name, data, count);
+    });
+}
+
+int smoe_load_default_vectors(smoe_session* s, const float* d, int64_t count) {
+    return guard([&] {
+        const auto& c = S(s)->cfg();
+        if (!d || count != static_cast<int64_t>(c.L) * c.E * c.H)
+            throw std::invalid_argument("default vectors must be [L][E][H]");
+        S(s)->load_default_vectors(d);
+    });
+}
+
+int smoe_load_estimator(smoe_session* s, const smoe_estimator_config* c, const float* flat,
+                        int64_t count) {
+    return guard([&] {
+        if (!c || !flat) throw std::invalid_argument("null argument");
+        if (c->m <= 1 || c->n <= 1 || c->d % c->m != 0)
+            throw std::invalid_argument("estimator: m and n must be > 1, d divisible by m");
+        const int64_t dm = c->d / c->m, mlp = dm * c->n;
+        const int64_t want = c->d * dm + static_cast<int64_t>(c->layers) * dm + 2 * mlp * dm +
+                             2 * dm + dm * c->experts;
+        if (count != want) throw std::invalid_argument("estimator: flat parameter count mismatch");
+        smoe::EstCfg e{c->d, c->m, c->n, c->experts, c->layers, c->eps};
+        S(s)->load_estimator(e, flat);
+    });
+}
+
+int smoe_set_predictor(smoe_session* s, int32_t kind, const int32_t* hybrid_map) {
+    return guard([&] { S(s)->set_predictor(kind, hybrid_map); });
+}
+
+int smoe_set_cache_fraction(smoe_session* s, float f) {
+    return guard([&] { S(s)->set_cache_fraction(f); });
+}
+
+int smoe_reset(smoe_session* s, int32_t max_steps, int32_t trace_full) {
+    return guard([&] {
+        if (max_steps < 0) throw std::invalid_argument("max_steps must be >= 0");
+        S(s)->reset(max_steps, trace_full);
+    });
+}
+
+int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n) {
+    return guard([&] {
+        if (!tokens && n > 0) throw std::invalid_argument("null tokens");
+        S(s)->prefill(tokens, n);
+    });
+}
+
+int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        S(s)->decode(mode, n_steps, use_graph);
+    });
+}
+
+int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
+                              int32_t n_new, int32_t mode, int32_t* out_tokens,
+                              double* per_token_ms) {
+    return guard([&] {
+        if (n_prompt < 1 || !prompt) throw std::invalid_argument("offloaded decode: empty prompt");
+        if (n_new < 1) throw std::invalid_argument("offloaded decode: n_new must be >= 1");
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        smoe::Session* ss = S(s);
+        ss->reset(n_prompt + n_new, 0);
+        ss->prefill(prompt, n_prompt);
+        ss->decode(mode, n_new - 1, 1);
+        std::vector<int> toks(n_prompt + n_new - 1);
+        ss->read_tokens(toks.data(), static_cast<int>(toks.size()));
+        for (int i = 0; i < n_new; ++i) out_tokens[i] = toks[n_prompt - 1 + i];
+        if (per_token_ms) {
+            auto v = ss->token_ms();
+            for (size_t i = 0; i < v.size() && i < static_cast<size_t>(n_new - 1); ++i) per_token_ms[i] = v[i];
+        }
+    });
+}
+
+int smoe_step(smoe_session* s, int32_t mode, int32_t token, float* logits_out, int32_t* next) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        const int t = S(s)->step_host(mode, token, logits_out);
+        if (next) *next = t;
+    });
+}
+
+int smoe_calibrate(smoe_session* s, int64_t ntok, uint64_t seed, int32_t seq_len, float* d_out,
+                   int64_t* counts_out) {
+    return guard([&] {
+        S(s)->calibrate(ntok, seed, seq_len, d_out, reinterpret_cast<long long*>(counts_out));
+    });
+}
+
+int smoe_steps_done(smoe_session* s, int32_t* n) {
+    return guard([&] { *n = S(s)->steps_done(); });
+}
+
+int smoe_read_tokens(smoe_session* s, int32_t* out, int32_t n) {
+    return guard([&] { S(s)->read_tokens(out, n); });
+}
+
+int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n) {
+    return guard([&] { S(s)->read_trace(field, out, n); });
+}
+
+int smoe_token_ms(smoe_session* s, double* out, int32_t cap, int32_t* n) {
+    return guard([&] {
+        auto v = S(s)->token_ms();
+        const int m = static_cast<int>(v.size()) < cap ? static_cast<int>(v.size()) : cap;
+        for (int i = 0; i < m; ++i) out[i] = v[i];
+        *n = static_cast<int32_t>(v.size());
+    });
+}
+
+int smoe_counters(smoe_session* s, int64_t* hits, int64_t* misses, int64_t* h2d_bytes,
+                  double* copy_ms, int32_t* requests) {
+    return guard([&] {
+        long long b = 0;
+        int req = 0;
+        double ms = 0;
+        S(s)->counters(reinterpret_cast<long long*>(hits), reinterpret_cast<long long*>(misses), &b,
+                       &ms, &req);
+        if (h2d_bytes) *h2d_bytes = b;
+        if (copy_ms) *copy_ms = ms;
+        if (requests) *requests = req;
+    });
+}
+
+int smoe_copy_events(smoe_session* s, smoe_copy_event* out, int32_t cap, int32_t* n) {
+    return guard([&] {
+        smoe::Session* ss = S(s);
+        ss->counters(nullptr, nullptr, nullptr, nullptr, nullptr);  // syncs both streams
+        auto recs = ss->copy_records();
+        int m = 0;
+        for (const auto& r : recs) {
+            if (m >= cap) break;
+            smoe_copy_event& e = out[m++];
+            e.seq = r.seq;
+            e.layer = r.layer;
+            e.step = r.step;
+            e.hits = r.hits;
+            e.misses = r.misses;
+            e.bytes = r.bytes;
+            e.start_ms = r.ev >= 0 ? ss->event_ms(r.ev, 0) : -1.0;
+            e.end_ms = r.ev >= 0 ? ss->event_ms(r.ev, 1) : -1.0;
+        }
+        *n = static_cast<int32_t>(recs.size());
+    });
+}
+
+int smoe_cache_slots(smoe_session* s, int32_t* slots) {
+    return guard([&] {
+        smoe::Session* ss = S(s);
+        const auto& c = ss->cfg();
+        (void)c;
+        *slots = ss->slots_per_layer();
+    });
+}
+
+int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
+    return guard([&] { S(s)->debug_state(out, cap); });
+}
+
+}  // extern "C"

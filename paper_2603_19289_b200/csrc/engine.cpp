@@ -1,0 +1,1161 @@
+// engine.cpp — host runtime (see engine.h).
+#include "engine.h"
+
+#include <cuda.h>
+#include <immintrin.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+namespace smoe {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " +
+                                 cudaGetErrorString(e));
+}
+
+// derive_seed (numerics.cpp:20-35): FNV-1a over the label, 2 splitmix rounds.
+uint64_t derive_seed(uint64_t seed, const std::string& label) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (unsigned char c : label) {
+        h ^= c;
+        h *= 0x100000001b3ull;
+    }
+    uint64_t z = seed ^ h;
+    for (int i = 0; i < 2; ++i) {
+        z += 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+    }
+    return z;
+}
+
+uint16_t f2bf(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+// Scatter a row-major f32 [R][C] tensor into a 32-row tiled bf16 buffer:
+// virtual row vr = r*mul + add + row_off, tile [vr/32][tile_cols][32].
+void tile_write_bf16(uint16_t* dst, const float* src, int R, int C, int tile_cols, int mul,
+                     int add, int row_off) {
+    for (int r = 0; r < R; ++r) {
+        const long long vr = static_cast<long long>(r) * mul + add + row_off;
+        uint16_t* base = dst + (vr / 32) * tile_cols * 32 + (vr % 32);
+        for (int c = 0; c < C; ++c) base[static_cast<long long>(c) * 32] = f2bf(src[static_cast<long long>(r) * C + c]);
+    }
+}
+
+void tile_write_f32(float* dst, const float* src, int R, int C) {
+    for (int r = 0; r < R; ++r) {
+        float* base = dst + static_cast<long long>(r / 32) * C * 32 + (r % 32);
+        for (int c = 0; c < C; ++c) base[static_cast<long long>(c) * 32] = src[static_cast<long long>(r) * C + c];
+    }
+}
+
+// cuStreamWriteValue32 through the runtime's driver entry point, so the
+// library does not link libcuda (it must load on GPU-less hosts too).
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValueFn write_value_fn() {
+    static WriteValueFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            throw std::runtime_error("cuStreamWriteValue32 entry point unavailable");
+        return reinterpret_cast<WriteValueFn>(p);
+    }();
+    return fn;
+}
+
+bool parse_layer(const std::string& name, int* l, std::string* rest) {
+    if (name.rfind("layer", 0) != 0) return false;
+    const size_t dot = name.find('.');
+    if (dot == std::string::npos) return false;
+    *l = std::stoi(name.substr(5, dot - 5));
+    *rest = name.substr(dot + 1);
+    return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ config --
+
+void ModelCfg::validate() const {
+    if (L < 1) throw std::invalid_argument("config: L must be >= 1");
+    if (E < 1) throw std::invalid_argument("config: E must be >= 1");
+    if (K < 1 || K > E) throw std::invalid_argument("config: k must satisfy 1 <= k <= E");
+    if (H < 1) throw std::invalid_argument("config: H must be >= 1");
+    if (Hm < 1) throw std::invalid_argument("config: H_moe must be >= 1");
+    if (V < 1) throw std::invalid_argument("config: vocab must be >= 1");
+    if (D < 1) throw std::invalid_argument("config: head_dim must be >= 1");
+    if (D % 2 != 0) throw std::invalid_argument("config: head_dim must be even for rotary pairs");
+    if (!(eps > 0.0f)) throw std::invalid_argument("config: eps must be > 0");
+    if (gating != 0 && gating != 1) throw std::invalid_argument("config: unknown gating order");
+    if (K > kMaxK) throw std::invalid_argument("config: k > 16 not supported on this path");
+    if (E > kMaxE) throw std::invalid_argument("config: E > 1024 not supported on this path");
+    if (D > kMaxD) throw std::invalid_argument("config: head_dim > 256 not supported on this path");
+    if (H > 16384) throw std::invalid_argument("config: hidden > 16384 not supported on this path");
+}
+
+// ------------------------------------------------------------ ExpertStore --
+
+ExpertStore::ExpertStore(long long n, long long elems) : n_(n), elems_(elems) {
+    const size_t bytes = static_cast<size_t>(n) * elems * 2;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&base_), bytes, cudaHostAllocPortable),
+       "cudaHostAlloc(expert store)");
+}
+
+ExpertStore::~ExpertStore() {
+    if (base_) cudaFreeHost(base_);
+}
+
+// -------------------------------------------------------------- SlotCache --
+
+SlotCache::SlotCache(int L, int E, int C)
+    : L_(L), E_(E), C_(C), expert_slot_(L, std::vector<int>(E, -1)),
+      slot_expert_(L, std::vector<int>(C, -1)), stamp_(L, std::vector<long long>(C, -1)),
+      hits_(L, 0), misses_(L, 0) {}
+
+void SlotCache::clear_stats() {
+    std::fill(hits_.begin(), hits_.end(), 0);
+    std::fill(misses_.begin(), misses_.end(), 0);
+}
+
+void SlotCache::invalidate() {
+    for (int l = 0; l < L_; ++l) {
+        std::fill(expert_slot_[l].begin(), expert_slot_[l].end(), -1);
+        std::fill(slot_expert_[l].begin(), slot_expert_[l].end(), -1);
+        std::fill(stamp_[l].begin(), stamp_[l].end(), -1);
+    }
+}
+
+// LRU within the layer's pool; never evicts an expert of the same request.
+std::vector<std::pair<int, int>> SlotCache::request(int layer, const int* ids, int n, int* hits,
+                                                    int* misses) {
+    if (layer < 0 || layer >= L_) throw std::runtime_error("copy request with bad layer");
+    std::vector<std::pair<int, int>> out;
+    *hits = *misses = 0;
+    const long long now = ++clock_;
+    auto& es = expert_slot_[layer];
+    auto& se = slot_expert_[layer];
+    auto& st = stamp_[layer];
+    for (int i = 0; i < n; ++i) {
+        const int e = ids[i];
+        if (e < 0 || e >= E_) throw std::runtime_error("copy request with bad expert id");
+        if (es[e] >= 0) {
+            st[es[e]] = now;
+            ++*hits;
+            continue;
+        }
+        int victim = -1;
+        for (int c = 0; c < C_; ++c) {
+            if (st[c] == now) continue;  // holds an expert of this request
+            if (victim < 0 || st[c] < st[victim]) victim = c;
+        }
+        if (victim < 0) throw std::runtime_error("slot pool smaller than the request");
+        if (se[victim] >= 0) es[se[victim]] = -1;
+        se[victim] = e;
+        es[e] = victim;
+        st[victim] = now;
+        out.emplace_back(victim, e);
+        ++*misses;
+    }
+    hits_[layer] += *hits;
+    misses_[layer] += *misses;
+    return out;
+}
+
+// ---------------------------------------------------------- CopyScheduler --
+
+CopyScheduler::CopyScheduler(Session* s) : s_(s) {}
+CopyScheduler::~CopyScheduler() { stop(); }
+
+void CopyScheduler::start() {
+    stop_ = false;
+    th_ = std::thread([this] { loop(); });
+}
+
+void CopyScheduler::stop() {
+    stop_ = true;
+    if (th_.joinable()) th_.join();
+}
+
+std::string CopyScheduler::error() {
+    std::lock_guard<std::mutex> g(mu_);
+    return err_;
+}
+
+std::vector<CopyRecord> CopyScheduler::records() {
+    std::lock_guard<std::mutex> g(mu_);
+    return recs_;
+}
+
+void CopyScheduler::clear_records() {
+    std::lock_guard<std::mutex> g(mu_);
+    recs_.clear();
+    ev_next_ = 0;
+}
+
+void CopyScheduler::loop() {
+    cudaSetDevice(s_->opts_.device);
+    auto idle_since = std::chrono::steady_clock::now();
+    while (!stop_.load(std::memory_order_relaxed)) {
+        MailboxEntry* e = &s_->h_mailbox_[next_seq_ % kMailboxRing];
+        const int seq = __atomic_load_n(const_cast<int*>(&e->seq), __ATOMIC_ACQUIRE);
+        ++polls;
+        if (seq != next_seq_) {
+            _mm_pause();
+            auto now = std::chrono::steady_clock::now();
+            if (now - idle_since > std::chrono::milliseconds(200))
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
+            continue;
+        }
+        MailboxEntry req;
+        std::memcpy(&req, e, sizeof req);
+        static const bool dbg = std::getenv("SMOE_DEBUG") != nullptr;
+        if (dbg)
+            std::fprintf(stderr, "[sched] t=%.3f ms seen seq %d layer %d\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(),
+                         req.seq, req.layer);
+        try {
+            handle(req);
+        } catch (const std::exception& ex) {
+            std::lock_guard<std::mutex> g(mu_);
+            if (err_.empty()) err_ = ex.what();
+            // unblock the device so it can observe the error instead of spinning
+            write_value_fn()(reinterpret_cast<CUstream>(s_->s_copy_),
+                                 reinterpret_cast<CUdeviceptr>(s_->ctl_.ready + req.layer),
+                                 static_cast<cuuint32_t>(req.seq), 0);
+        }
+        ++next_seq_;
+        idle_since = std::chrono::steady_clock::now();
+    }
+}
+
+// Alg. 1 "WaitAndPrefetch": stage the requested experts of one layer into
+// HBM slots (only cache misses move over PCIe), then publish the slot table
+// row and the layer's ready value on the same copy stream (FIFO, like the
+// reference's single copy worker, executor.cpp:138-198).
+void CopyScheduler::handle(const MailboxEntry& e) {
+    Session& s = *s_;
+    if (e.nids < 1 || e.nids > kMaxK) throw std::runtime_error("copy request with bad id count");
+    if (s.opts_.copy_latency_us > 0)
+        std::this_thread::sleep_for(std::chrono::microseconds(s.opts_.copy_latency_us));
+    int hits = 0, misses = 0;
+    auto copies = s.cache_->request(e.layer, e.ids, e.nids, &hits, &misses);
+    const int npairs = static_cast<int>(s.ev_copy_.size() / 2);
+    int ev = -1;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (ev_next_ < npairs) ev = ev_next_++;
+    }
+    if (ev >= 0) ck(cudaEventRecord(s.ev_copy_[2 * ev], s.s_copy_), "event record");
+    const long long bytes_per = s.store_->bytes_per_expert();
+    const int E = s.cfg_.E;
+    for (auto& [slot, expert] : copies) {
+        uint16_t* dst = s.d_slots_ + (static_cast<long long>(e.layer) * s.C_ + slot) * s.dm_.expert_elems;
+        const uint16_t* src = s.store_->expert(static_cast<long long>(e.layer) * E + expert);
+        ck(cudaMemcpyAsync(dst, src, bytes_per, cudaMemcpyHostToDevice, s.s_copy_), "H2D expert copy");
+    }
+    if (!copies.empty()) {
+        int* stage = s.h_stage_ + static_cast<long long>(stage_idx_ % 256) * E;
+        // the copy that last used this staging row is >=256 requests old and
+        // therefore complete: requests retire in FIFO order before the device
+        // can post more than a few new ones.
+        std::memcpy(stage, s.cache_->slot_row(e.layer).data(), sizeof(int) * E);
+        ck(cudaMemcpyAsync(s.d_slot_of_ + static_cast<long long>(e.layer) * E, stage, sizeof(int) * E,
+                           cudaMemcpyHostToDevice, s.s_copy_),
+           "slot table update");
+        ++stage_idx_;
+    }
+    if (ev >= 0) ck(cudaEventRecord(s.ev_copy_[2 * ev + 1], s.s_copy_), "event record");
+    static const int ready_mode = std::getenv("SMOE_READY_MODE") ? std::atoi(std::getenv("SMOE_READY_MODE")) : 0;
+    if (ready_mode == 2) {
+        int* flag = s.h_stage_ + 256LL * E + (stage_idx_ % 256);
+        *flag = e.seq;
+        ++stage_idx_;
+        ck(cudaMemcpyAsync(s.ctl_.ready + e.layer, flag, 4, cudaMemcpyHostToDevice, s.s_copy_), "ready flag");
+    } else {
+        const CUresult r = write_value_fn()(reinterpret_cast<CUstream>(s.s_copy_),
+                                            reinterpret_cast<CUdeviceptr>(s.ctl_.ready + e.layer),
+                                            static_cast<cuuint32_t>(e.seq),
+                                            ready_mode == 1 ? CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER : 0);
+        if (r != CUDA_SUCCESS) throw std::runtime_error("cuStreamWriteValue32 failed");
+    }
+    std::lock_guard<std::mutex> g(mu_);
+    recs_.push_back({e.seq, e.layer, e.step, hits, misses,
+                     static_cast<long long>(copies.size()) * bytes_per, ev});
+}
+
+// ---------------------------------------------------------------- Session --
+
+void* Session::dalloc(size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), "cudaMalloc");
+    ck(cudaMemset(p, 0, bytes < 256 ? 256 : bytes), "cudaMemset");
+    dev_allocs_.push_back(p);
+    return p;
+}
+
+Session::Session(const ModelCfg& cfg, const SessionOpts& opts) : cfg_(cfg), opts_(opts) {
+    cfg_.validate();
+    if (!(opts_.cache_fraction > 0.0f && opts_.cache_fraction <= 1.0f))
+        throw std::invalid_argument("cache_fraction must be in (0, 1]");
+    if (opts_.max_positions < 2) throw std::invalid_argument("max_positions must be >= 2");
+    ck(cudaSetDevice(opts_.device), "cudaSetDevice");
+    write_value_fn();
+    ck(preload_kernels(), "kernel preload");
+    try {
+        alloc();
+    } catch (...) {
+        free_all();
+        throw;
+    }
+    sched_ = std::make_unique<CopyScheduler>(this);
+    sched_->start();
+}
+
+Session::~Session() {
+    if (sched_) sched_->stop();
+    free_all();
+}
+
+void Session::free_all() {
+    drop_graphs();
+    if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_copy_) cudaStreamSynchronize(s_copy_);
+    for (void* p : dev_allocs_) cudaFree(p);
+    dev_allocs_.clear();
+    for (auto e : ev_copy_) cudaEventDestroy(e);
+    ev_copy_.clear();
+    for (auto e : ev_step_) cudaEventDestroy(e);
+    ev_step_.clear();
+    if (ev_origin_) cudaEventDestroy(ev_origin_);
+    ev_origin_ = nullptr;
+    if (h_mailbox_) cudaFreeHost(h_mailbox_);
+    if (h_stage_) cudaFreeHost(h_stage_);
+    if (h_token_) cudaFreeHost(h_token_);
+    if (h_logits_) cudaFreeHost(h_logits_);
+    h_mailbox_ = nullptr;
+    h_stage_ = nullptr;
+    h_token_ = nullptr;
+    h_logits_ = nullptr;
+    store_.reset();
+    if (s_comp_) cudaStreamDestroy(s_comp_);
+    if (s_copy_) cudaStreamDestroy(s_copy_);
+    s_comp_ = s_copy_ = nullptr;
+}
+
+void Session::drop_graphs() {
+    for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+    graphs_.clear();
+}
+
+void Session::alloc() {
+    const ModelCfg& c = cfg_;
+    const int L = c.L, E = c.E, K = c.K, H = c.H, D = c.D, V = c.V;
+    DevModel& m = dm_;
+    m.L = L; m.E = E; m.K = K; m.H = H; m.Hm = c.Hm; m.V = V; m.D = D;
+    m.eps = c.eps;
+    m.gating = c.gating;
+    m.Hmp = round_up(c.Hm, 16);
+    m.Hp = round_up(H, 32);
+    m.Ep = round_up(E, 32);
+    m.Vp = round_up(V, 32);
+    m.QKVp = round_up(3 * D, 32);
+    m.cap = opts_.max_positions;
+    m.inv_sqrt_d = 1.0f / std::sqrt(static_cast<float>(D));  // model.cpp:336
+    m.gu_elems = static_cast<long long>(m.Hmp) * H * 2;
+    m.expert_elems = m.gu_elems + static_cast<long long>(m.Hp) * m.Hmp;
+    C_ = static_cast<int>(std::ceil(static_cast<double>(opts_.cache_fraction) * E));
+    if (C_ < K) C_ = K;
+    if (C_ > E) C_ = E;
+    m.C = C_;
+
+    ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
+
+    d_emb_ = static_cast<uint16_t*>(dalloc(2ull * V * H));
+    d_unemb_ = static_cast<uint16_t*>(dalloc(2ull * m.Vp * H));
+    m.qkv_stride = static_cast<long long>(m.QKVp) * H;
+    m.wo_stride = static_cast<long long>(m.Hp) * D;
+    m.gate_stride = static_cast<long long>(m.Ep) * H;
+    d_wqkv_ = static_cast<uint16_t*>(dalloc(2ull * L * m.qkv_stride));
+    d_wo_ = static_cast<uint16_t*>(dalloc(2ull * L * m.wo_stride));
+    d_gate_ = static_cast<uint16_t*>(dalloc(2ull * L * m.gate_stride));
+    d_final_gain_ = static_cast<float*>(dalloc(4ull * H));
+    d_attn_gain_ = static_cast<float*>(dalloc(4ull * L * H));
+    d_moe_gain_ = static_cast<float*>(dalloc(4ull * L * H));
+    {
+        std::vector<float> ones(static_cast<size_t>(L) * H, 1.0f);  // model.cpp:126-131
+        ck(cudaMemcpy(d_final_gain_, ones.data(), 4ull * H, cudaMemcpyHostToDevice), "gain");
+        ck(cudaMemcpy(d_attn_gain_, ones.data(), 4ull * L * H, cudaMemcpyHostToDevice), "gain");
+        ck(cudaMemcpy(d_moe_gain_, ones.data(), 4ull * L * H, cudaMemcpyHostToDevice), "gain");
+    }
+    // RoPE table with the host libm, exactly model.cpp:311-316.
+    {
+        std::vector<float> rope(static_cast<size_t>(m.cap) * (D / 2) * 2);
+        for (int p = 0; p < m.cap; ++p)
+            for (int i = 0; i < D / 2; ++i) {
+                const double theta =
+                    std::pow(10000.0, -2.0 * static_cast<double>(i) / static_cast<double>(D));
+                const double angle = static_cast<double>(p) * theta;
+                rope[(static_cast<size_t>(p) * (D / 2) + i) * 2] = static_cast<float>(std::cos(angle));
+                rope[(static_cast<size_t>(p) * (D / 2) + i) * 2 + 1] = static_cast<float>(std::sin(angle));
+            }
+        d_rope_ = static_cast<float*>(dalloc(rope.size() * 4));
+        ck(cudaMemcpy(d_rope_, rope.data(), rope.size() * 4, cudaMemcpyHostToDevice), "rope");
+    }
+    d_slots_ = static_cast<uint16_t*>(dalloc(2ull * L * C_ * m.expert_elems));
+    d_slot_of_ = static_cast<int*>(dalloc(4ull * L * E));
+    ck(cudaMemset(d_slot_of_, 0xff, 4ull * L * E), "memset");
+    d_dv_ = static_cast<float*>(dalloc(4ull * L * E * H));
+    d_hybrid_ = static_cast<int*>(dalloc(4ull * L));
+    d_attn_scratch_ = static_cast<double*>(dalloc(16ull * m.cap));
+    d_prompt_tok_ = static_cast<int*>(dalloc(4ull * m.cap));
+
+    m.emb = d_emb_;
+    m.unemb = d_unemb_;
+    m.final_gain = d_final_gain_;
+    m.attn_gain = d_attn_gain_;
+    m.moe_gain = d_moe_gain_;
+    m.wqkv = d_wqkv_;
+    m.wo = d_wo_;
+    m.gate = d_gate_;
+    m.rope = d_rope_;
+    m.slots = d_slots_;
+    m.slot_of = d_slot_of_;
+    m.dv = d_dv_;
+    m.hybrid = d_hybrid_;
+
+    auto mk_state = [&](DevState& st) {
+        st.x = static_cast<float*>(dalloc(4ull * m.Hp));
+        st.r = static_cast<float*>(dalloc(4ull * L * m.Hp));
+        st.s = static_cast<float*>(dalloc(4ull * L * m.Hp));
+        st.m = static_cast<float*>(dalloc(4ull * L * m.Hp));
+        st.q = static_cast<float*>(dalloc(4ull * kMaxD));
+        st.ctx = static_cast<float*>(dalloc(4ull * kMaxD));
+        st.kc = static_cast<float*>(dalloc(4ull * L * m.cap * D));
+        st.vc = static_cast<float*>(dalloc(4ull * L * m.cap * D));
+        st.lg_true = static_cast<float*>(dalloc(4ull * L * E));
+        st.id_true = static_cast<int*>(dalloc(4ull * L * K));
+        st.g_true = static_cast<float*>(dalloc(4ull * L * K));
+        st.id_exec = static_cast<int*>(dalloc(4ull * L * K));
+        st.g_exec = static_cast<float*>(dalloc(4ull * L * K));
+        st.lg_pred = static_cast<float*>(dalloc(4ull * L * E));
+        st.id_pred = static_cast<int*>(dalloc(4ull * L * K));
+        st.g_pred = static_cast<float*>(dalloc(4ull * L * K));
+        st.quasi = static_cast<float*>(dalloc(4ull * m.Hp));
+        st.h = static_cast<float*>(dalloc(4ull * K * m.Hmp));
+        st.y = static_cast<float*>(dalloc(4ull * K * m.Hp));
+        st.logits = static_cast<float*>(dalloc(4ull * m.Vp));
+        st.pos = static_cast<int*>(dalloc(4));
+        st.token = static_cast<int*>(dalloc(4));
+        st.counters = static_cast<int*>(dalloc(4 * 64));
+        st.est_z = st.est_act = st.est_xn = nullptr;
+    };
+    mk_state(st_);
+    mk_state(sh_);
+
+    ctl_.req_counter = static_cast<int*>(dalloc(4));
+    ctl_.req_seq = static_cast<int*>(dalloc(4ull * L));
+    ctl_.ready = static_cast<int*>(dalloc(4ull * L));
+    ctl_.error = static_cast<int*>(dalloc(4));
+    ctl_.step = static_cast<int*>(dalloc(4));
+    ctl_.tokens_out = static_cast<int*>(dalloc(4ull * (m.cap + 1)));
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, opts_.device);
+    if (clk_khz <= 0) clk_khz = 2000000;
+    ctl_.spin_limit = static_cast<long long>(opts_.deadlock_s * clk_khz * 1e3);
+
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_mailbox_), sizeof(MailboxEntry) * kMailboxRing,
+                     cudaHostAllocMapped | cudaHostAllocPortable),
+       "mailbox");
+    std::memset(h_mailbox_, 0, sizeof(MailboxEntry) * kMailboxRing);
+    MailboxEntry* dmb = nullptr;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dmb), h_mailbox_, 0), "mailbox map");
+    ctl_.mailbox = dmb;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_stage_), 4ull * 256 * (E + 1), cudaHostAllocPortable), "stage");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_token_), 64, cudaHostAllocPortable), "token");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_logits_), 4ull * m.Vp, cudaHostAllocPortable), "logits");
+
+    ev_copy_.resize(2 * 8192);
+    for (auto& e : ev_copy_) ck(cudaEventCreate(&e), "event");
+    ev_step_.resize(2 * 4096);
+    for (auto& e : ev_step_) ck(cudaEventCreate(&e), "event");
+    ck(cudaEventCreate(&ev_origin_), "event");
+
+    store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * E, m.expert_elems);
+    cache_ = std::make_unique<SlotCache>(L, E, C_);
+    reset(0, 0);
+}
+
+void Session::set_cache_fraction(float frac) {
+    if (!(frac > 0.0f && frac <= 1.0f)) throw std::invalid_argument("cache_fraction must be in (0, 1]");
+    sync();
+    int C = static_cast<int>(std::ceil(static_cast<double>(frac) * cfg_.E));
+    if (C < cfg_.K) C = cfg_.K;
+    if (C > cfg_.E) C = cfg_.E;
+    if (C == C_) return;
+    // replace the slot pool
+    for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
+        if (*it == d_slots_) {
+            cudaFree(*it);
+            dev_allocs_.erase(it);
+            break;
+        }
+    opts_.cache_fraction = frac;
+    C_ = C;
+    dm_.C = C;
+    d_slots_ = static_cast<uint16_t*>(dalloc(2ull * cfg_.L * C_ * dm_.expert_elems));
+    dm_.slots = d_slots_;
+    ck(cudaMemset(d_slot_of_, 0xff, 4ull * cfg_.L * cfg_.E), "memset");
+    cache_ = std::make_unique<SlotCache>(cfg_.L, cfg_.E, C_);
+    drop_graphs();
+}
+
+// ------------------------------------------------------------- weights ------
+
+// build_model (model.cpp:112-158) on the GPU: every tensor from its labelled
+// counter-based stream, rounded to bf16 in the kernels' layouts.  Expert
+// blocks are generated into an HBM staging area and copied into the pinned
+// host store (they live off-device until the cache pulls them in).
+void Session::init_weights_seeded() {
+    sync();
+    const ModelCfg& c = cfg_;
+    DevModel& m = dm_;
+    const float stddev = 0.4f / std::sqrt(static_cast<float>(c.H));
+    cudaStream_t s = s_comp_;
+    auto gen = [&](const std::string& label, int R, int C, int tc, int layout, int which,
+                   int roff, uint16_t* out) {
+        ck(launch_gen_bf16(derive_seed(c.seed, label), stddev, R, C, tc, layout, which, roff, out, s),
+           "gen");
+    };
+    gen("embedding", c.V, c.H, c.H, kRowMajor, 0, 0, d_emb_);
+    gen("unembed", c.V, c.H, c.H, kRowTiled, 0, 0, d_unemb_);
+    for (int l = 0; l < c.L; ++l) {
+        const std::string p = "layer" + std::to_string(l) + ".";
+        uint16_t* qkv = d_wqkv_ + l * m.qkv_stride;
+        gen(p + "wq", c.D, c.H, c.H, kRowTiled, 0, 0, qkv);
+        gen(p + "wk", c.D, c.H, c.H, kRowTiled, 0, c.D, qkv);
+        gen(p + "wv", c.D, c.H, c.H, kRowTiled, 0, 2 * c.D, qkv);
+        gen(p + "wo", c.H, c.D, c.D, kRowTiled, 0, 0, d_wo_ + l * m.wo_stride);
+        gen(p + "gate", c.E, c.H, c.H, kRowTiled, 0, 0, d_gate_ + l * m.gate_stride);
+    }
+    // experts: batches through an HBM staging buffer
+    const long long per = m.expert_elems;
+    const long long total = static_cast<long long>(c.L) * c.E;
+    long long batch = (1ll << 30) / (per * 2);  // ~1 GiB staging
+    if (batch < 1) batch = 1;
+    if (batch > total) batch = total;
+    uint16_t* stage = nullptr;
+    ck(cudaMalloc(&stage, static_cast<size_t>(batch) * per * 2), "staging");
+    for (long long b0 = 0; b0 < total; b0 += batch) {
+        const long long nb = std::min(batch, total - b0);
+        ck(cudaMemsetAsync(stage, 0, static_cast<size_t>(nb) * per * 2, s), "memset");
+        for (long long i = 0; i < nb; ++i) {
+            const long long x = b0 + i;
+            const int l = static_cast<int>(x / c.E), e = static_cast<int>(x % c.E);
+            const std::string p = "layer" + std::to_string(l) + ".expert" + std::to_string(e) + ".";
+            uint16_t* blk = stage + i * per;
+            gen(p + "w_gate", c.Hm, c.H, c.H, kGateUp, 0, 0, blk);
+            gen(p + "w_up", c.Hm, c.H, c.H, kGateUp, 1, 0, blk);
+            gen(p + "w_down", c.H, c.Hm, m.Hmp, kRowTiled, 0, 0, blk + m.gu_elems);
+        }
+        ck(cudaMemcpyAsync(store_->expert(b0), stage, static_cast<size_t>(nb) * per * 2,
+                           cudaMemcpyDeviceToHost, s),
+           "D2H store");
+    }
+    ck(cudaStreamSynchronize(s), "init sync");
+    cudaFree(stage);
+    cache_->invalidate();
+    ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
+}
+
+void Session::load_tensor(const std::string& name, const float* data, long long n) {
+    sync();
+    const ModelCfg& c = cfg_;
+    DevModel& m = dm_;
+    auto need = [&](long long want) {
+        if (n != want) throw std::invalid_argument("load_tensor: " + name + " has wrong size");
+    };
+    auto upload16 = [&](uint16_t* dst, const std::vector<uint16_t>& v) {
+        ck(cudaMemcpy(dst, v.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
+    };
+    if (name == "embedding") {
+        need(static_cast<long long>(c.V) * c.H);
+        std::vector<uint16_t> v(n);
+        for (long long i = 0; i < n; ++i) v[i] = f2bf(data[i]);
+        upload16(d_emb_, v);
+        return;
+    }
+    if (name == "unembed") {
+        need(static_cast<long long>(c.V) * c.H);
+        std::vector<uint16_t> v(static_cast<size_t>(m.Vp) * c.H, 0);
+        tile_write_bf16(v.data(), data, c.V, c.H, c.H, 1, 0, 0);
+        upload16(d_unemb_, v);
+        return;
+    }
+    if (name == "final_norm_gain") {
+        need(c.H);
+        ck(cudaMemcpy(d_final_gain_, data, 4ull * c.H, cudaMemcpyHostToDevice), "upload");
+        return;
+    }
+    int l;
+    std::string rest;
+    if (!parse_layer(name, &l, &rest) || l < 0 || l >= c.L)
+        throw std::invalid_argument("load_tensor: unknown tensor " + name);
+    if (rest == "attn_norm_gain" || rest == "moe_norm_gain") {
+        need(c.H);
+        float* dst = (rest == "attn_norm_gain" ? d_attn_gain_ : d_moe_gain_) + static_cast<long long>(l) * c.H;
+        ck(cudaMemcpy(dst, data, 4ull * c.H, cudaMemcpyHostToDevice), "upload");
+        drop_graphs();
+        return;
+    }
+    if (rest == "wq" || rest == "wk" || rest == "wv") {
+        need(static_cast<long long>(c.D) * c.H);
+        std::vector<uint16_t> v(m.qkv_stride);
+        uint16_t* dst = d_wqkv_ + l * m.qkv_stride;
+        ck(cudaMemcpy(v.data(), dst, v.size() * 2, cudaMemcpyDeviceToHost), "download");
+        const int off = rest == "wq" ? 0 : rest == "wk" ? c.D : 2 * c.D;
+        tile_write_bf16(v.data(), data, c.D, c.H, c.H, 1, 0, off);
+        upload16(dst, v);
+        return;
+    }
+    if (rest == "wo") {
+        need(static_cast<long long>(c.H) * c.D);
+        std::vector<uint16_t> v(m.wo_stride, 0);
+        tile_write_bf16(v.data(), data, c.H, c.D, c.D, 1, 0, 0);
+        upload16(d_wo_ + l * m.wo_stride, v);
+        return;
+    }
+    if (rest == "gate") {
+        need(static_cast<long long>(c.E) * c.H);
+        std::vector<uint16_t> v(m.gate_stride, 0);
+        tile_write_bf16(v.data(), data, c.E, c.H, c.H, 1, 0, 0);
+        upload16(d_gate_ + l * m.gate_stride, v);
+        return;
+    }
+    int e;
+    char which[32];
+    if (std::sscanf(rest.c_str(), "expert%d.%31s", &e, which) == 2 && e >= 0 && e < c.E) {
+        uint16_t* blk = store_->expert(static_cast<long long>(l) * c.E + e);
+        const std::string w = which;
+        if (w == "w_gate" || w == "w_up") {
+            need(static_cast<long long>(c.Hm) * c.H);
+            tile_write_bf16(blk, data, c.Hm, c.H, c.H, 2, w == "w_up" ? 1 : 0, 0);
+        } else if (w == "w_down") {
+            need(static_cast<long long>(c.H) * c.Hm);
+            tile_write_bf16(blk + m.gu_elems, data, c.H, c.Hm, m.Hmp, 1, 0, 0);
+        } else {
+            throw std::invalid_argument("load_tensor: unknown tensor " + name);
+        }
+        // invalidate a resident copy of this expert
+        cache_->invalidate();
+        ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
+        return;
+    }
+    throw std::invalid_argument("load_tensor: unknown tensor " + name);
+}
+
+void Session::load_default_vectors(const float* d) {
+    sync();
+    ck(cudaMemcpy(d_dv_, d, 4ull * cfg_.L * cfg_.E * cfg_.H, cudaMemcpyHostToDevice), "dv upload");
+    have_dv_ = true;
+}
+
+// EstimatorParams flat layout (estimator.hpp:41-72) -> f32 row tiles.
+void Session::load_estimator(const EstCfg& e, const float* flat) {
+    sync();
+    if (e.d != cfg_.H) throw std::invalid_argument("estimator: d must equal the model hidden size");
+    if (e.E != cfg_.E) throw std::invalid_argument("estimator: E must equal the model expert count");
+    if (e.L != cfg_.L) throw std::invalid_argument("estimator: L must equal the model layer count");
+    if (e.m <= 1 || e.n <= 1 || e.d % e.m != 0) throw std::invalid_argument("estimator: bad m/n");
+    const int dm = e.d / e.m, mlp = dm * e.n;
+    const int dmp = round_up(dm, 32), mlpp = round_up(mlp, 32);
+    const long long a_off = 0, pos_off = static_cast<long long>(dm) * e.d,
+                    b_off = pos_off + static_cast<long long>(e.L) * dm,
+                    c_off = b_off + static_cast<long long>(mlp) * dm,
+                    g_off = c_off + static_cast<long long>(dm) * mlp, bias_off = g_off + dm,
+                    h_off = bias_off + dm;
+    const long long szA = static_cast<long long>(dmp) * e.d, szB = static_cast<long long>(mlpp) * dm,
+                    szC = static_cast<long long>(dmp) * mlp, szH = static_cast<long long>(dm_.Ep) * dm;
+    std::vector<float> buf(szA + szB + szC + szH + static_cast<long long>(e.L) * dm + 2 * dm, 0.0f);
+    float* A = buf.data();
+    float* B = A + szA;
+    float* Cc = B + szB;
+    float* Hd = Cc + szC;
+    float* P = Hd + szH;
+    float* G = P + static_cast<long long>(e.L) * dm;
+    float* Bi = G + dm;
+    tile_write_f32(A, flat + a_off, dm, e.d);
+    tile_write_f32(B, flat + b_off, mlp, dm);
+    tile_write_f32(Cc, flat + c_off, dm, mlp);
+    tile_write_f32(Hd, flat + h_off, e.E, dm);
+    std::memcpy(P, flat + pos_off, 4ull * e.L * dm);
+    std::memcpy(G, flat + g_off, 4ull * dm);
+    std::memcpy(Bi, flat + bias_off, 4ull * dm);
+    if (!d_est_ || est_.d != e.d || est_.m != e.m || est_.n != e.n) {
+        d_est_ = static_cast<float*>(dalloc(buf.size() * 4));
+        auto mk = [&](DevState& st) {
+            st.est_z = static_cast<float*>(dalloc(4ull * dmp));
+            st.est_act = static_cast<float*>(dalloc(4ull * mlpp));
+            st.est_xn = static_cast<float*>(dalloc(4ull * dmp));
+        };
+        mk(st_);
+        mk(sh_);
+    }
+    ck(cudaMemcpy(d_est_, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice), "est upload");
+    est_ = e;
+    DevModel& m = dm_;
+    m.est_d = e.d;
+    m.est_dm = dm;
+    m.est_mlp = mlp;
+    m.est_eps = e.eps;
+    m.est_a = d_est_;
+    m.est_b = d_est_ + (A - buf.data()) + szA;
+    m.est_c = d_est_ + (Cc - buf.data());
+    m.est_head = d_est_ + (Hd - buf.data());
+    m.est_pos = d_est_ + (P - buf.data());
+    m.est_gain = d_est_ + (G - buf.data());
+    m.est_bias = d_est_ + (Bi - buf.data());
+    have_est_ = true;
+    drop_graphs();
+}
+
+void Session::set_predictor(int kind, const int* hybrid_map) {
+    sync();
+    if (kind < kNone || kind > kOracle) throw std::invalid_argument("unknown predictor kind");
+    const int L = cfg_.L;
+    std::vector<int> map;
+    if (kind == kHybrid) {
+        map.assign(L, kRouterPF);
+        if (hybrid_map)
+            for (int l = 0; l < L - 1; ++l) {
+                const int k = hybrid_map[l];
+                if (k != kBaselineS && k != kRouterPF && k != kEstPF)
+                    throw std::invalid_argument("hybrid map: entries must be concrete predictors");
+                map[l] = k;
+            }
+    }
+    auto needs = [&](int k) {
+        if ((k == kRouterPF || k == kEstPF) && !have_dv_)
+            throw std::invalid_argument(std::string(k == kRouterPF ? "router-pf" : "est-pf") +
+                                        ": missing default-vector table");
+        if (k == kEstPF && !have_est_) throw std::invalid_argument("est-pf: missing estimator");
+    };
+    if (kind == kHybrid)
+        for (int l = 0; l < L - 1; ++l) needs(map[l]);
+    else
+        needs(kind);
+    pred_kind_ = kind;
+    hybrid_ = map;
+    drop_graphs();
+}
+
+// ------------------------------------------------------------- decode -------
+
+void Session::sync() {
+    static const bool dbg = std::getenv("SMOE_DEBUG") != nullptr;
+    if (dbg)
+        std::fprintf(stderr, "[main] t=%.3f ms sync begin\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
+    if (s_comp_) ck(cudaStreamSynchronize(s_comp_), "compute stream");
+    if (dbg)
+        std::fprintf(stderr, "[main] t=%.3f ms sync end\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
+    check_device_error();
+}
+
+void Session::check_device_error() {
+    int err = 0;
+    ck(cudaMemcpy(&err, ctl_.error, 4, cudaMemcpyDeviceToHost), "error flag");
+    const std::string se = sched_ ? sched_->error() : std::string();
+    if (!se.empty()) {
+        cudaMemset(ctl_.error, 0, 4);
+        throw std::runtime_error(se);
+    }
+    if (err != 0) {
+        cudaMemset(ctl_.error, 0, 4);
+        if (err >= 1000 && err < 2000)
+            throw std::runtime_error("deadlock suspected: compute waited " +
+                                     std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
+                                     " ms for layer " + std::to_string(err - 1000) + " expert copy");
+        throw std::runtime_error("expert read before readiness at layer " + std::to_string(err - 2000));
+    }
+}
+
+void Session::reset(int max_steps, int trace_full) {
+    sync();
+    const ModelCfg& c = cfg_;
+    int zero = 0;
+    for (DevState* st : {&st_, &sh_}) {
+        ck(cudaMemcpy(st->pos, &zero, 4, cudaMemcpyHostToDevice), "reset");
+        ck(cudaMemset(st->counters, 0, 256), "reset");
+    }
+    ck(cudaMemcpy(ctl_.step, &zero, 4, cudaMemcpyHostToDevice), "reset");
+    // trace buffers
+    if (max_steps != max_steps_ || trace_full != trace_full_ || !tr_.step) {
+        auto drop = [&](void* p) {
+            if (!p) return;
+            for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
+                if (*it == p) {
+                    cudaFree(p);
+                    dev_allocs_.erase(it);
+                    return;
+                }
+        };
+        for (void* p : {(void*)tr_.s, (void*)tr_.r, (void*)tr_.m, (void*)tr_.lg_true, (void*)tr_.g_true,
+                        (void*)tr_.g_exec, (void*)tr_.lg_pred, (void*)tr_.g_pred, (void*)tr_.y,
+                        (void*)tr_.logits, (void*)tr_.id_true, (void*)tr_.id_exec, (void*)tr_.id_pred,
+                        (void*)tr_.step})
+            drop(p);
+        tr_ = TraceDev{};
+        tr_.step = static_cast<int*>(dalloc(4));
+        tr_.cap = max_steps;
+        tr_.full = trace_full;
+        const long long S = max_steps > 0 ? max_steps : 1;
+        const long long LK = static_cast<long long>(c.L) * c.K;
+        tr_.id_true = static_cast<int*>(dalloc(4 * S * LK));
+        tr_.id_exec = static_cast<int*>(dalloc(4 * S * LK));
+        tr_.id_pred = static_cast<int*>(dalloc(4 * S * LK));
+        if (trace_full) {
+            const long long LH = static_cast<long long>(c.L) * c.H, LE = static_cast<long long>(c.L) * c.E;
+            tr_.g_true = static_cast<float*>(dalloc(4 * S * LK));
+            tr_.g_exec = static_cast<float*>(dalloc(4 * S * LK));
+            tr_.g_pred = static_cast<float*>(dalloc(4 * S * LK));
+            tr_.s = static_cast<float*>(dalloc(4 * S * LH));
+            tr_.r = static_cast<float*>(dalloc(4 * S * LH));
+            tr_.m = static_cast<float*>(dalloc(4 * S * LH));
+            tr_.lg_true = static_cast<float*>(dalloc(4 * S * LE));
+            tr_.lg_pred = static_cast<float*>(dalloc(4 * S * LE));
+            tr_.y = static_cast<float*>(dalloc(4 * S * LK * c.H));
+            tr_.logits = static_cast<float*>(dalloc(4 * S * c.V));
+        }
+        max_steps_ = max_steps;
+        trace_full_ = trace_full;
+        drop_graphs();
+    }
+    ck(cudaMemset(tr_.step, 0, 4), "reset");
+    if (max_steps > 0) {
+        const long long n = static_cast<long long>(max_steps) * c.L * c.K * 4;
+        ck(cudaMemset(tr_.id_pred, 0xff, n), "reset");
+    }
+    steps_ = 0;
+    n_step_events_ = 0;
+    ck(cudaEventRecord(ev_origin_, s_comp_), "event");
+    cache_->clear_stats();
+    sched_ ? sched_->clear_records() : void();
+}
+
+// One forward pass of `st` (forward_decode / speculative_forward structure,
+// model.cpp:355-389 / speculation.cpp:350-399, with Alg. 1's copy requests).
+void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating, int step_tag,
+                           int record, cudaStream_t s) {
+    (void)step_tag;
+    const ModelCfg& c = cfg_;
+    const bool is_main = (&st == &st_);
+    const bool prefetch = mode == 1 && use_pred && pred_kind_ != kNone;
+    auto kind_at = [&](int l) -> int {
+        if (l >= c.L - 1) return kNone;
+        return pred_kind_ == kHybrid ? hybrid_[l] : pred_kind_;
+    };
+    const DevState* shadow = pred_kind_ == kOracle ? &sh_ : nullptr;
+    for (int l = 0; l < c.L; ++l) {
+        ck(launch_qkv(dm_, st, l, s), "qkv");
+        ck(launch_attn(dm_, st, d_attn_scratch_, l, s), "attn");
+        ck(launch_wo(dm_, st, l, s), "wo");
+        if (!prefetch) {
+            RouterLaunch rl{l, 1, kNone, 0, 1, 0, step_tag};
+            ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
+        } else {
+            const int k = kind_at(l);
+            if (l == 0) {
+                RouterLaunch rl{0, 1, kNone, 0, 1, 0, step_tag};
+                ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
+                if (k != kNone) {
+                    RouterLaunch rp{0, 0, k, -1, 0, k != kEstPF, step_tag};
+                    ck(launch_router(dm_, st, ctl_, rp, shadow, s), "router");
+                }
+            } else {
+                RouterLaunch rl{l, 1, k, 1, 0, k != kNone && k != kEstPF, step_tag};
+                ck(launch_router(dm_, st, ctl_, rl, shadow, s), "router");
+            }
+            if (k == kEstPF) ck(launch_estimator(dm_, st, ctl_, l, 1, step_tag, s), "estimator");
+        }
+        ck(launch_ffn(dm_, st, ctl_, l, s), "ffn");
+        if (calibrating) ck(launch_dv_accum(dm_, st, d_dv_sums_, d_dv_counts_, l, s), "dv");
+        if (is_main && record && trace_full_ && tr_.cap > 0) ck(launch_trace_y(dm_, st, tr_, l, s), "trace");
+    }
+    ck(launch_final(dm_, st, ctl_, record && is_main, s), "final");
+    if (is_main && record && tr_.cap > 0) ck(launch_trace(dm_, st, tr_, s), "trace");
+}
+
+void Session::enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s) {
+    const int* tok_src = st_.token;
+    if (!is_prefill && mode == 1 && pred_kind_ == kOracle) {
+        // Oracle::begin_token (speculation.cpp:271-280): true path on the shadow state
+        ck(launch_embed(dm_, sh_, tok_src, s), "embed");
+        enqueue_pass(sh_, 0, 0, 0, -2, 0, s);
+    }
+    ck(launch_embed(dm_, st_, tok_src, s), "embed");
+    enqueue_pass(st_, is_prefill ? 0 : mode, is_prefill ? 0 : 1, calibrating, is_prefill ? -1 : 0,
+                 record, s);
+}
+
+void Session::set_token(int tok) {
+    // synchronous small upload (host-driven entry points only)
+    ck(cudaMemcpyAsync(st_.token, &tok, 4, cudaMemcpyHostToDevice, s_comp_), "token");
+    ck(cudaStreamSynchronize(s_comp_), "token");
+}
+
+void Session::prefill(const int* tokens, int n) {
+    if (n < 1) throw std::invalid_argument("generate: empty prompt");
+    sync();
+    for (int i = 0; i < n; ++i)
+        if (tokens[i] < 0 || tokens[i] >= cfg_.V) throw std::invalid_argument("forward_decode: token out of vocab");
+    int pos = 0;
+    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    if (pos + n >= dm_.cap) throw std::invalid_argument("prefill: KV capacity exceeded");
+    ck(cudaMemcpy(d_prompt_tok_, tokens, 4ull * n, cudaMemcpyHostToDevice), "prompt");
+    for (int i = 0; i < n; ++i) {
+        ck(launch_embed(dm_, st_, d_prompt_tok_ + i, s_comp_), "embed");
+        enqueue_pass(st_, 0, 0, 0, -1, 1, s_comp_);
+        if (pred_kind_ == kOracle) {  // Oracle::observe_prompt_token (speculation.cpp:266-269)
+            ck(launch_embed(dm_, sh_, d_prompt_tok_ + i, s_comp_), "embed");
+            enqueue_pass(sh_, 0, 0, 0, -2, 0, s_comp_);
+        }
+        ++steps_;
+    }
+    sync();
+}
+
+void Session::decode(int mode, int n_steps, int use_graph) {
+    if (n_steps < 0) throw std::invalid_argument("decode: n_steps must be >= 0");
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    sync();
+    int pos = 0;
+    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
+    cudaGraphExec_t exec = nullptr;
+    if (use_graph) {
+        const long long key = mode * 10 + 1;
+        auto it = graphs_.find(key);
+        if (it == graphs_.end()) {
+            cudaGraph_t g;
+            ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
+            enqueue_step(mode, 0, 1, 0, s_comp_);
+            ck(cudaStreamEndCapture(s_comp_, &g), "capture");
+            ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+            cudaGraphDestroy(g);
+            graphs_[key] = exec;
+        } else {
+            exec = it->second;
+        }
+    }
+    ck(cudaEventRecord(ev_origin_, s_comp_), "event");
+    for (int i = 0; i < n_steps; ++i) {
+        const int ev = n_step_events_ < static_cast<int>(ev_step_.size() / 2) ? n_step_events_++ : -1;
+        if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev], s_comp_), "event");
+        if (exec)
+            ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+        else
+            enqueue_step(mode, 0, 1, 0, s_comp_);
+        if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
+        ++steps_;
+    }
+    sync();
+}
+
+int Session::step_host(int mode, int token, float* logits_out) {
+    if (token < 0 || token >= cfg_.V) throw std::invalid_argument("forward_decode: token out of vocab");
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    const long long key = mode * 10 + 1;
+    auto it = graphs_.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (it == graphs_.end()) {
+        sync();
+        cudaGraph_t g;
+        ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
+        enqueue_step(mode, 0, 1, 0, s_comp_);
+        ck(cudaStreamEndCapture(s_comp_, &g), "capture");
+        ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+        cudaGraphDestroy(g);
+        graphs_[key] = exec;
+    } else {
+        exec = it->second;
+    }
+    h_token_[0] = token;
+    ck(cudaMemcpyAsync(st_.token, h_token_, 4, cudaMemcpyHostToDevice, s_comp_), "token H2D");
+    ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+    ck(cudaMemcpyAsync(h_logits_, st_.logits, 4ull * cfg_.V, cudaMemcpyDeviceToHost, s_comp_), "logits D2H");
+    ck(cudaMemcpyAsync(h_token_ + 1, st_.token, 4, cudaMemcpyDeviceToHost, s_comp_), "token D2H");
+    ck(cudaStreamSynchronize(s_comp_), "step");
+    ++steps_;
+    check_device_error();
+    if (logits_out) std::memcpy(logits_out, h_logits_, 4ull * cfg_.V);
+    return h_token_[1];
+}
+
+// accumulate_default_vectors over random_token_stream (trace.cpp:187-211,
+// speculation.cpp:23-58), true routing, state reset every seq_len tokens.
+void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out, long long* c_out) {
+    if (ntok < 1) throw std::invalid_argument("trace: empty workload");
+    if (seq_len < 1) throw std::invalid_argument("trace: seq_len must be >= 1");
+    if (seq_len + 1 >= dm_.cap) throw std::invalid_argument("calibrate: seq_len exceeds KV capacity");
+    sync();
+    const ModelCfg& c = cfg_;
+    const long long LE = static_cast<long long>(c.L) * c.E;
+    d_dv_sums_ = static_cast<double*>(dalloc(8ull * LE * c.H));
+    d_dv_counts_ = static_cast<long long*>(dalloc(8ull * LE));
+    std::vector<int> toks(ntok);
+    {
+        uint64_t st = derive_seed(seed, "token-stream");
+        for (long long i = 0; i < ntok; ++i) {
+            st += 0x9E3779B97F4A7C15ull;
+            uint64_t z = st;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z = z ^ (z >> 31);
+            toks[i] = static_cast<int>(z % static_cast<uint64_t>(c.V));
+        }
+    }
+    int* d_toks = static_cast<int*>(dalloc(4ull * ntok));
+    ck(cudaMemcpy(d_toks, toks.data(), 4ull * ntok, cudaMemcpyHostToDevice), "tokens");
+    int zero = 0;
+    for (long long i = 0; i < ntok; ++i) {
+        if (i % seq_len == 0) ck(cudaMemcpyAsync(st_.pos, &zero, 4, cudaMemcpyHostToDevice, s_comp_), "pos");
+        ck(launch_embed(dm_, st_, d_toks + i, s_comp_), "embed");
+        enqueue_pass(st_, 0, 0, 1, -3, 0, s_comp_);
+        if (i % 64 == 63) sync();
+    }
+    ck(launch_dv_freeze(d_dv_sums_, d_dv_counts_, d_dv_, LE, c.H, s_comp_), "freeze");
+    sync();
+    if (d_out) ck(cudaMemcpy(d_out, d_dv_, 4ull * LE * c.H, cudaMemcpyDeviceToHost), "dv");
+    if (c_out) ck(cudaMemcpy(c_out, d_dv_counts_, 8ull * LE, cudaMemcpyDeviceToHost), "counts");
+    for (void* p : {(void*)d_dv_sums_, (void*)d_dv_counts_, (void*)d_toks})
+        for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
+            if (*it == p) {
+                cudaFree(p);
+                dev_allocs_.erase(it);
+                break;
+            }
+    d_dv_sums_ = nullptr;
+    d_dv_counts_ = nullptr;
+    ck(cudaMemcpy(st_.pos, &zero, 4, cudaMemcpyHostToDevice), "pos");
+    have_dv_ = true;
+}
+
+// ------------------------------------------------------------- results ------
+
+int Session::steps_done() { return steps_; }
+
+// Diagnostics: [req_counter, error, host next_seq, n_records, polls, mailbox seq of
+// the next slot, then ready[0..L), req_seq[0..L)].
+void Session::debug_state(int* out, int cap) {
+    std::vector<int> v;
+    int x = 0;
+    cudaMemcpy(&x, ctl_.req_counter, 4, cudaMemcpyDeviceToHost);
+    v.push_back(x);
+    cudaMemcpy(&x, ctl_.error, 4, cudaMemcpyDeviceToHost);
+    v.push_back(x);
+    v.push_back(sched_->next_seq());
+    v.push_back(static_cast<int>(sched_->records().size()));
+    v.push_back(static_cast<int>(sched_->polls));
+    v.push_back(static_cast<int>(h_mailbox_[sched_->next_seq() % kMailboxRing].seq));
+    std::vector<int> r(cfg_.L), q(cfg_.L);
+    cudaMemcpy(r.data(), ctl_.ready, 4 * cfg_.L, cudaMemcpyDeviceToHost);
+    cudaMemcpy(q.data(), ctl_.req_seq, 4 * cfg_.L, cudaMemcpyDeviceToHost);
+    v.insert(v.end(), r.begin(), r.end());
+    v.insert(v.end(), q.begin(), q.end());
+    for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
+}
+
+void Session::read_tokens(int* out, int n) {
+    sync();
+    ck(cudaMemcpy(out, ctl_.tokens_out, 4ull * n, cudaMemcpyDeviceToHost), "tokens");
+}
+
+void Session::read_trace(const char* field, void* out, long long n) {
+    sync();
+    const std::string f = field;
+    const void* src = nullptr;
+    long long esz = 4;
+    if (f == "id_true") src = tr_.id_true;
+    else if (f == "id_exec") src = tr_.id_exec;
+    else if (f == "id_pred") src = tr_.id_pred;
+    else if (f == "g_true") src = tr_.g_true;
+    else if (f == "g_exec") src = tr_.g_exec;
+    else if (f == "g_pred") src = tr_.g_pred;
+    else if (f == "s") src = tr_.s;
+    else if (f == "r") src = tr_.r;
+    else if (f == "m") src = tr_.m;
+    else if (f == "lg_true") src = tr_.lg_true;
+    else if (f == "lg_pred") src = tr_.lg_pred;
+    else if (f == "y") src = tr_.y;
+    else if (f == "logits") src = tr_.logits;
+    else throw std::invalid_argument("read_trace: unknown field " + f);
+    if (!src) throw std::invalid_argument("read_trace: field not captured (trace_full=0?)");
+    ck(cudaMemcpy(out, src, n * esz, cudaMemcpyDeviceToHost), "trace");
+}
+
+std::vector<double> Session::token_ms() {
+    sync();
+    std::vector<double> v;
+    for (int i = 0; i < n_step_events_; ++i) {
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, ev_step_[2 * i], ev_step_[2 * i + 1]), "elapsed");
+        v.push_back(ms);
+    }
+    return v;
+}
+
+double Session::step_event_ms(int i, int which) {
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, ev_origin_, ev_step_[2 * i + which]), "elapsed");
+    return ms;
+}
+
+double Session::event_ms(int ev, int which) {
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, ev_origin_, ev_copy_[2 * ev + which]), "elapsed");
+    return ms;
+}
+
+void Session::counters(long long* hits, long long* misses, long long* bytes, double* copy_ms,
+                       int* requests) {
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    for (int l = 0; l < cfg_.L; ++l) {
+        if (hits) hits[l] = cache_->hits(l);
+        if (misses) misses[l] = cache_->misses(l);
+    }
+    long long b = 0;
+    double ms = 0.0;
+    auto recs = sched_->records();
+    for (const CopyRecord& r : recs) {
+        b += r.bytes;
+        if (r.ev >= 0 && r.bytes > 0) {
+            float t = 0.0f;
+            if (cudaEventElapsedTime(&t, ev_copy_[2 * r.ev], ev_copy_[2 * r.ev + 1]) == cudaSuccess) ms += t;
+        }
+    }
+    if (bytes) *bytes = b;
+    if (copy_ms) *copy_ms = ms;
+    if (requests) *requests = static_cast<int>(recs.size());
+}
+
+}  // namespace smoe

@@ -1,0 +1,218 @@
+// engine.h — host C++ runtime of the B200 speculative expert-prefetch decode
+// path.  Replaces the reference's TwoLaneEngine / offloaded_forward /
+// run_offloaded_decode (executor.cpp:41-359) with:
+//   * ExpertStore   — pinned host memory holding every expert as one
+//                     contiguous bf16 block in the kernels' tile layout;
+//   * SlotCache     — per-layer HBM slot pool capped at C slots, LRU
+//                     replacement, per-layer hit/miss table (NEW: the
+//                     reference double-buffers k experts, executor.cpp:115-122);
+//   * CopyScheduler — a host thread that polls a mapped-memory mailbox the
+//                     router kernel writes (predicted / routed ids), issues
+//                     cudaMemcpyAsync H2D for misses on the copy stream, then
+//                     publishes the slot table and a per-layer ready value
+//                     (cuStreamWriteValue32) the expert kernels wait on;
+//   * Session       — device weights, decode state, CUDA-graph-captured token
+//                     steps for on-demand and prefetch modes.
+#pragma once
+#include "kernels.h"
+#include "smoe_dev.h"
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace smoe {
+
+struct ModelCfg {
+    int L, E, K, H, Hm, V, D;
+    float eps;
+    uint64_t seed;
+    int gating;
+    void validate() const;  // model.cpp:25-37 invariants (+ this path's limits)
+};
+
+struct SessionOpts {
+    int device = 0;
+    float cache_fraction = 1.0f;  // HBM slots per layer = max(K, ceil(frac * E))
+    int max_positions = 4096;     // KV capacity
+    int copy_latency_us = 0;      // injected per copy request (ExecutorOptions parity)
+    double deadlock_s = 10.0;     // device spin limit before "deadlock suspected"
+};
+
+struct EstCfg {
+    int d, m, n, E, L;
+    float eps;
+};
+
+struct CopyRecord {  // one mailbox request as the copy lane saw it
+    int seq, layer, step, hits, misses;
+    long long bytes;
+    int ev;  // index into the event pool, -1 if none
+};
+
+class ExpertStore {
+public:
+    ExpertStore(long long n_experts, long long elems_per_expert);
+    ~ExpertStore();
+    uint16_t* expert(long long i) { return base_ + i * elems_; }
+    long long bytes_per_expert() const { return elems_ * 2; }
+
+private:
+    uint16_t* base_ = nullptr;
+    long long n_, elems_;
+};
+
+class SlotCache {
+public:
+    SlotCache(int L, int E, int C);
+    // Returns the (slot, expert) pairs that must be copied for this request.
+    std::vector<std::pair<int, int>> request(int layer, const int* ids, int n, int* hits,
+                                             int* misses);
+    const std::vector<int>& slot_row(int layer) const { return expert_slot_[layer]; }
+    int capacity() const { return C_; }
+    long long hits(int l) const { return hits_[l]; }
+    long long misses(int l) const { return misses_[l]; }
+    void clear_stats();
+    void invalidate();
+
+private:
+    int L_, E_, C_;
+    long long clock_ = 0;
+    std::vector<std::vector<int>> expert_slot_;   // [L][E] -> slot or -1
+    std::vector<std::vector<int>> slot_expert_;   // [L][C] -> expert or -1
+    std::vector<std::vector<long long>> stamp_;   // [L][C]
+    std::vector<long long> hits_, misses_;
+};
+
+class Session;
+
+class CopyScheduler {
+public:
+    explicit CopyScheduler(Session* s);
+    ~CopyScheduler();
+    void start();
+    void stop();
+    std::string error();  // first error seen by the thread ("" if none)
+    std::vector<CopyRecord> records();
+    void clear_records();
+    int next_seq() const { return next_seq_; }
+    long long polls = 0;
+
+private:
+    void loop();
+    void handle(const MailboxEntry& e);
+    Session* s_;
+    std::thread th_;
+    std::atomic<bool> stop_{false};
+    std::mutex mu_;
+    std::string err_;
+    std::vector<CopyRecord> recs_;
+    int next_seq_ = 1;
+    int stage_idx_ = 0;
+    int ev_next_ = 0;
+};
+
+class Session {
+public:
+    Session(const ModelCfg& cfg, const SessionOpts& opts);
+    ~Session();
+
+    // --- weights -------------------------------------------------------------
+    void init_weights_seeded();  // build_model (model.cpp:112-158) on the GPU, bf16
+    void load_tensor(const std::string& name, const float* data, long long n);  // from f32
+    void load_default_vectors(const float* d);  // [L][E][H]
+    void load_estimator(const EstCfg& c, const float* flat);
+    void set_predictor(int kind, const int* hybrid_map);
+    void set_cache_fraction(float frac);
+
+    // --- decode --------------------------------------------------------------
+    void reset(int max_steps, int trace_full);
+    void prefill(const int* tokens, int n);               // true routing per token
+    void decode(int mode, int n_steps, int use_graph);    // greedy, device-driven
+    int step_host(int mode, int token, float* logits_out);  // host token in, logits out
+    void calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out, long long* c_out);
+
+    // --- results -------------------------------------------------------------
+    int steps_done();
+    void read_tokens(int* out, int n);
+    void read_trace(const char* field, void* out, long long n_elems);
+    std::vector<double> token_ms();  // device-timed duration of each decode() step
+    void counters(long long* hits, long long* misses, long long* bytes, double* copy_ms,
+                  int* requests);
+    std::vector<CopyRecord> copy_records() { return sched_->records(); }
+    double event_ms(int ev_pair, int which);  // 0 start, 1 end; relative to run origin
+    double step_event_ms(int i, int which);
+
+    const ModelCfg& cfg() const { return cfg_; }
+    int slots_per_layer() const { return C_; }
+    void debug_state(int* out, int cap);
+
+    // used by the scheduler
+    friend class CopyScheduler;
+
+private:
+    void alloc();
+    void free_all();
+    void build_devmodel();
+    void enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s);
+    void enqueue_pass(DevState& st, int mode, int pred_kind_enabled, int calibrating,
+                      int step_tag, int record, cudaStream_t s);
+    void check_device_error();
+    void sync();
+    void set_token(int tok);
+
+    ModelCfg cfg_;
+    SessionOpts opts_;
+    int C_ = 0;
+    DevModel dm_{};
+    DevState st_{}, sh_{};
+    DevCtl ctl_{};
+    TraceDev tr_{};
+
+    // device allocations (owned)
+    std::vector<void*> dev_allocs_;
+    void* dalloc(size_t bytes);
+    uint16_t *d_emb_ = nullptr, *d_unemb_ = nullptr, *d_wqkv_ = nullptr, *d_wo_ = nullptr,
+             *d_gate_ = nullptr, *d_slots_ = nullptr;
+    float *d_final_gain_ = nullptr, *d_attn_gain_ = nullptr, *d_moe_gain_ = nullptr,
+          *d_rope_ = nullptr, *d_dv_ = nullptr;
+    int* d_slot_of_ = nullptr;
+    double* d_attn_scratch_ = nullptr;
+    double* d_dv_sums_ = nullptr;
+    long long* d_dv_counts_ = nullptr;
+    float* d_est_ = nullptr;
+    int* d_hybrid_ = nullptr;
+    int* d_prompt_tok_ = nullptr;
+
+    // host
+    std::unique_ptr<ExpertStore> store_;
+    std::unique_ptr<SlotCache> cache_;
+    std::unique_ptr<CopyScheduler> sched_;
+    MailboxEntry* h_mailbox_ = nullptr;
+    int* h_stage_ = nullptr;  // pinned slot-table staging ring [256][E]
+    int* h_token_ = nullptr;  // pinned token staging [2]
+    float* h_logits_ = nullptr;
+    cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
+    std::vector<cudaEvent_t> ev_copy_;  // pairs
+    std::vector<cudaEvent_t> ev_step_;  // pairs per decode step
+    cudaEvent_t ev_origin_ = nullptr;
+    int n_step_events_ = 0;
+
+    int pred_kind_ = kNone;
+    std::vector<int> hybrid_;
+    bool have_dv_ = false, have_est_ = false;
+    EstCfg est_{};
+    int max_steps_ = 0, trace_full_ = 0;
+    int steps_ = 0;
+
+    std::map<long long, cudaGraphExec_t> graphs_;
+    void drop_graphs();
+};
+
+}  // namespace smoe

@@ -1,0 +1,996 @@
+// kernels.cu — sm_100a kernels for the speculative expert-prefetch decode path.
+//
+// Arithmetic contract: every f32 dot product is the
+// reference's sequential `acc += w[c] * x[c]` (numerics.cpp:136-147) with a
+// separately rounded product (the file is compiled with --fmad=false; the
+// reference's x86-64 build emits no FMA).  One lane owns one output row and
+// walks the columns in order; parallelism comes from rows, experts and
+// layers, never from splitting a dot product.  Weights stream HBM -> smem
+// with cp.async.bulk (TMA bulk copies, SASS UBLKCP) into a per-warp
+// multi-stage ring guarded by mbarriers, so the sequential FADD chains run
+// at chain latency while the copy engine keeps bytes in flight.
+// f64 reductions (rms_norm sum of squares, softmax partition) are
+// tree-ordered; their ~1e-16 relative differences vanish in the f32
+// rounding of the result except at measure-zero midpoints (reported by the
+// parity tests as exact-match fractions).
+#include "kernels.h"
+
+#include <cstdio>
+
+namespace smoe {
+
+// ---------------------------------------------------------------- helpers --
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float bf2f(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+__device__ __forceinline__ float to_f(uint16_t b) { return bf2f(b); }
+__device__ __forceinline__ float to_f(float f) { return f; }
+
+// numerics.cpp:86-89 — silu in f64, rounded to f32.
+__device__ __forceinline__ float silu_ref(float x) {
+    const double xd = static_cast<double>(x);
+    return static_cast<float>(xd / (1.0 + exp(-xd)));
+}
+
+// Deterministic block reduction of a per-thread double (tree order fixed by
+// blockDim).  Returns the same value in every thread.
+__device__ double block_sum_d(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    __syncthreads();
+    return t;
+}
+
+__device__ float block_max_f(float v, float* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    float t = red[0];
+    for (int i = 1; i < nw; ++i) t = fmaxf(t, red[i]);
+    __syncthreads();
+    return t;
+}
+
+// rms_norm (numerics.cpp:72-84): out[i] = (v[i] * scale) * gain[i],
+// scale = f32(1 / sqrt(sum_f64(v^2) / n + eps)).  Whole block participates.
+__device__ void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
+                               double* red) {
+    double ss = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        ss += static_cast<double>(v[i]) * static_cast<double>(v[i]);
+    ss = block_sum_d(ss, red);
+    const float scale =
+        static_cast<float>(1.0 / sqrt(ss / static_cast<double>(n) + static_cast<double>(eps)));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v[i] * scale * gain[i];
+    __syncthreads();
+}
+
+// ------------------------------------------------------- warp tile stream --
+//
+// One warp computes 32 sequential dot products acc(lane) = sum_c W[c][lane]*x[c]
+// over a row tile [cols][32] in global memory.  Lane 0 keeps S chunks of CC
+// columns in flight with cp.async.bulk; every lane walks the columns in order.
+
+template <typename WT, int S, int CC>
+struct WarpPipe {
+    static constexpr int kChunkElems = CC * 32;
+    static constexpr int kBytes = S * kChunkElems * static_cast<int>(sizeof(WT)) + S * 8;
+    uint64_t* full;  // [S]
+    WT* buf;         // [S][CC*32]
+    int ctr;         // chunks consumed so far (phase tracking)
+
+    __device__ void init(unsigned char* smem) {  // call with the owning warp; then syncwarp
+        buf = reinterpret_cast<WT*>(smem);
+        full = reinterpret_cast<uint64_t*>(smem + S * kChunkElems * sizeof(WT));
+        ctr = 0;
+        if ((threadIdx.x & 31) == 0) {
+            for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+    }
+
+    __device__ void issue(const WT* tile, int cols, int n, int g) {
+        const int st = g % S;
+        const int c0 = n * CC;
+        const int cn = min(CC, cols - c0);
+        const uint32_t bytes = static_cast<uint32_t>(cn) * 32u * sizeof(WT);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
+    }
+
+    // Returns this lane's dot product.  xs: shared-memory f32 vector [cols].
+    __device__ float run(const WT* tile, int cols, const float* xs) {
+        const int lane = threadIdx.x & 31;
+        const int nch = (cols + CC - 1) / CC;
+        if (lane == 0)
+            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        float acc = 0.0f;
+        for (int n = 0; n < nch; ++n) {
+            const int g = ctr + n;
+            const int st = g % S;
+            mbar_wait(&full[st], static_cast<uint32_t>((g / S) & 1));
+            const WT* b = buf + st * kChunkElems + lane;
+            const float* xc = xs + n * CC;
+            const int cn = min(CC, cols - n * CC);
+            if (cn == CC) {
+#pragma unroll 16
+                for (int c = 0; c < CC; ++c) acc = acc + to_f(b[c * 32]) * xc[c];
+            } else {
+                for (int c = 0; c < cn; ++c) acc = acc + to_f(b[c * 32]) * xc[c];
+            }
+            __syncwarp();
+            if (lane == 0 && n + S < nch) issue(tile, cols, n + S, g + S);
+        }
+        ctr += nch;
+        return acc;
+    }
+};
+
+constexpr int kS = 4;       // stages per warp
+constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
+constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
+constexpr int kCCd = 64;    // down-projection columns per chunk (4 KB)
+using PipeB = WarpPipe<uint16_t, kS, kCCb>;
+using PipeF = WarpPipe<float, kS, kCCf>;
+using PipeD = WarpPipe<uint16_t, kS, kCCd>;
+
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+    return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+extern __shared__ __align__(128) unsigned char g_smem[];
+
+// "Last CTA done" gate: returns true in every thread of the last CTA to arrive.
+__device__ bool last_cta(int* counter, int total) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(counter, 1);
+        s_last = (prev == total - 1);
+        if (s_last) *counter = 0;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}
+
+// -------------------------------------------------------------- decision --
+//
+// make_decision (model.cpp:258-274) for one logits row, executed by warp 0.
+// softmax (numerics.cpp:37-54): f32 max, f64 exp, f64 partition summed in
+// index order by lane 0 (exactly the reference's order), f32 probabilities;
+// top_k (numerics.cpp:56-70): value desc, lower index first; gates renormalised
+// by an f32 sum in rank order.  topk-softmax: top_k on logits, softmax of the k.
+__device__ void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
+                              double* se /*smem E*/, int* ids, float* gates) {
+    const int lane = threadIdx.x & 31;
+    const float* v = logits;
+    if (gating == kSoftmaxTopK) {
+        float mx = -INFINITY;
+        for (int i = lane; i < E; i += 32) mx = fmaxf(mx, v[i]);
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int i = lane; i < E; i += 32)
+            se[i] = exp(static_cast<double>(v[i]) - static_cast<double>(mx));
+        __syncwarp();
+        double z = 0.0;
+        if (lane == 0)
+            for (int i = 0; i < E; ++i) z += se[i];
+        z = __shfl_sync(0xffffffffu, z, 0);
+        for (int i = lane; i < E; i += 32) sp[i] = static_cast<float>(se[i] / z);
+        __syncwarp();
+        v = sp;
+    }
+    // top-k by repeated warp argmax; selected entries marked in `taken` bits
+    unsigned taken_lo = 0;  // up to 32 elements per lane tracked by bit (E <= 1024)
+    int sel[kMaxK];
+    float val[kMaxK];
+    for (int t = 0; t < K; ++t) {
+        float bv = -INFINITY;
+        int bi = 0x7fffffff;
+        int j = 0;
+        for (int i = lane; i < E; i += 32, ++j) {
+            if (taken_lo & (1u << j)) continue;
+            const float x = v[i];
+            if (bi == 0x7fffffff || x > bv) {  // i increases: strict > keeps lower index
+                bv = x;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        sel[t] = bi;
+        val[t] = bv;
+        if ((bi & 31) == lane) taken_lo |= 1u << (bi >> 5);
+    }
+    if (lane == 0) {
+        if (gating == kSoftmaxTopK) {
+            float total = 0.0f;
+            for (int t = 0; t < K; ++t) total += val[t];
+            for (int t = 0; t < K; ++t) {
+                ids[t] = sel[t];
+                gates[t] = val[t] / total;
+            }
+        } else {
+            float mx = val[0];
+            for (int t = 0; t < K; ++t) mx = fmaxf(mx, val[t]);
+            double e[kMaxK], z = 0.0;
+            for (int t = 0; t < K; ++t) {
+                e[t] = exp(static_cast<double>(val[t]) - static_cast<double>(mx));
+                z += e[t];
+            }
+            for (int t = 0; t < K; ++t) {
+                ids[t] = sel[t];
+                gates[t] = static_cast<float>(e[t] / z);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Mailbox post (single thread): request copies of `ids` for `layer`.
+__device__ void post_request(const DevCtl& ctl, int layer, int step, const int* ids, int k) {
+    const int seq = *ctl.req_counter + 1;
+    *ctl.req_counter = seq;
+    ctl.req_seq[layer] = seq;
+    MailboxEntry* e = ctl.mailbox + (seq % kMailboxRing);
+    e->layer = layer;
+    e->step = step;
+    e->nids = k;
+    for (int i = 0; i < k; ++i) e->ids[i] = ids[i];
+    __threadfence_system();
+    e->seq = seq;
+    __threadfence_system();
+}
+
+// ------------------------------------------------------------- weight init --
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Rng::next_gaussian (numerics.cpp:10-14) for draw block n: 12 uniforms from
+// the counter-based splitmix64 stream, summed in order in f64, minus 6.
+__device__ __forceinline__ double gaussian_at(uint64_t seed, unsigned long long n) {
+    double s = 0.0;
+    uint64_t st = seed + (12ull * n) * 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+        st += 0x9E3779B97F4A7C15ull;
+        s = __dadd_rn(s, __dmul_rn(__ull2double_rn(mix64(st) >> 11), 0x1.0p-53));
+    }
+    return __dadd_rn(s, -6.0);
+}
+
+__device__ __forceinline__ uint16_t f2bf_rne(float x) {
+    uint32_t u = __float_as_uint(x);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+// Thread per destination element (coalesced writes).  Row-tiled layouts
+// cover rows [0, Rtile) x tile_cols; elements outside the tensor are left.
+__global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_cols,
+                           int layout, int which, int row_off, long long total, uint16_t* out) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; d < total;
+         d += stride) {
+        long long r, c;
+        if (layout == kRowMajor) {
+            r = d / C;
+            c = d % C;
+        } else {
+            const long long lane = d & 31;
+            const long long rest = d >> 5;
+            const long long rb = rest / tile_cols;
+            c = rest % tile_cols;
+            if (c >= C) continue;
+            const long long vr = rb * 32 + lane;
+            if (layout == kRowTiled) {
+                r = vr - row_off;
+            } else {  // kGateUp: virtual row 2r + which
+                if ((vr & 1) != which) continue;
+                r = vr >> 1;
+            }
+            if (r < 0 || r >= R) continue;
+        }
+        const double g = gaussian_at(seed, static_cast<unsigned long long>(r * C + c));
+        out[d] = f2bf_rne(static_cast<float>(__dmul_rn(g, stddev)));
+    }
+}
+
+// ------------------------------------------------------------- attention --
+
+__global__ void k_embed(DevModel m, DevState st, const int* token_src) {
+    const int tok = *token_src;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m.Hp; j += gridDim.x * blockDim.x)
+        st.x[j] = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
+}
+
+// q, k, v = W{q,k,v} . rms_norm(x, attn_gain) (model.cpp:325-333), RoPE on q
+// and k (model.cpp:309-321, cos/sin precomputed on the host with libm), k and v
+// appended to the layer's KV cache at `pos`.  One warp per 32-row tile.
+__global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) {
+    double* red = reinterpret_cast<double*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 64);
+    unsigned char* pipe_mem = align128(g_smem + 64 + m.H * 4);
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    block_rms_norm(st.x, m.attn_gain + static_cast<long long>(layer) * m.H, m.H, m.eps, xs, red);
+    const int rb = blockIdx.x;
+    const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * m.H * 32;
+    float acc = pipe.run(tile, m.H, xs);
+    const int lane = threadIdx.x & 31;
+    const int R = rb * 32 + lane;
+    const int D = m.D;
+    const int pos = *st.pos;
+    const float other = __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (R < 2 * D) {  // RoPE pair (2i, 2i+1) lives in lanes (2i', 2i'+1)
+        const int i = (R % D) >> 1;
+        const float c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
+        const float s = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2 + 1];
+        const bool even = (R & 1) == 0;
+        const float x0 = even ? acc : other, x1 = even ? other : acc;
+        acc = even ? (x0 * c - x1 * s) : (x0 * s + x1 * c);
+    }
+    const long long kv = (static_cast<long long>(layer) * m.cap + pos) * D;
+    if (R < D)
+        st.q[R] = acc;
+    else if (R < 2 * D)
+        st.kc[kv + R - D] = acc;
+    else if (R < 3 * D)
+        st.vc[kv + R - 2 * D] = acc;
+}
+
+// scores / softmax / context (model.cpp:335-351), one CTA.
+__global__ void __launch_bounds__(256) k_attn(DevModel m, DevState st, double* e, int layer) {
+    float* qs = reinterpret_cast<float*>(g_smem);           // [D]
+    float* red = qs + kMaxD;                                  // [32]
+    double* dred = reinterpret_cast<double*>(red + 32);       // [32]
+    const int D = m.D;
+    const int n = *st.pos + 1;
+    const long long base = static_cast<long long>(layer) * m.cap * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = st.q[i];
+    __syncthreads();
+    float* sc = reinterpret_cast<float*>(e + m.cap);  // scratch: doubles [cap] then floats [cap]
+    float lmax = -INFINITY;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const float* kj = st.kc + base + static_cast<long long>(j) * D;
+        float acc = 0.0f;
+        for (int i = 0; i < D; ++i) acc = acc + qs[i] * kj[i];
+        const float v = acc * m.inv_sqrt_d;
+        sc[j] = v;
+        lmax = fmaxf(lmax, v);
+    }
+    const float mx = block_max_f(lmax, red);
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
+    __syncthreads();
+    __shared__ double zs;
+    if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
+        double z = 0.0;
+        for (int j = 0; j < n; ++j) z += e[j];
+        zs = z;
+    }
+    __syncthreads();
+    const double z = zs;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) sc[j] = static_cast<float>(e[j] / z);
+    __syncthreads();
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+        float acc = 0.0f;
+        for (int j = 0; j < n; ++j) acc = acc + sc[j] * st.vc[base + static_cast<long long>(j) * D + i];
+        st.ctx[i] = acc;
+    }
+    (void)dred;
+}
+
+// attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
+__global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
+    float* xs = reinterpret_cast<float*>(g_smem);
+    unsigned char* pipe_mem = align128(g_smem + kMaxD * 4);
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    for (int i = threadIdx.x; i < m.D; i += blockDim.x) xs[i] = st.ctx[i];
+    __syncwarp();
+    const int rb = blockIdx.x;
+    const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
+    const float acc = pipe.run(tile, m.D, xs);
+    const int j = rb * 32 + (threadIdx.x & 31);
+    if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = st.x[j] + acc;
+}
+
+// ---------------------------------------------------------------- router --
+//
+// CTA groups: [0, nT) true-router row tiles of gate_l over s_l;
+// [nT, nT+nP) predictor row tiles of gate_{l+1} over the predictor input
+// (baseline-s: s_l; router-pf / est-pf: q_l = rms_norm(r_l + d_l, gain_{l+1})).
+// The last CTA turns logits into decisions, fixes the executed decision and
+// posts the copy requests.
+
+__device__ void compute_quasi(const DevModel& m, const DevState& st, int layer, int exec_from,
+                              float* qs, float* tmp, double* red) {
+    // layer_default (speculation.cpp:104-117) + quasi_hidden (speculation.cpp:119-121)
+    // over the decision executed at `layer` (pred_l when this launch also fixes exec).
+    const int H = m.H, K = m.K;
+    const int* ids = (exec_from == 1 ? st.id_pred : st.id_exec) + layer * K;
+    const float* gs = (exec_from == 1 ? st.g_pred : st.g_exec) + layer * K;
+    const float* r = st.r + static_cast<long long>(layer) * m.Hp;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        float d = 0.0f;
+        for (int i = 0; i < K; ++i)
+            d = d + gs[i] * m.dv[(static_cast<long long>(layer) * m.E + ids[i]) * H + j];
+        tmp[j] = r[j] + d;
+    }
+    __syncthreads();
+    block_rms_norm(tmp, m.moe_gain + static_cast<long long>(layer + 1) * H, H, m.eps, qs, red);
+}
+
+__global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl ctl,
+                                               RouterLaunch rl, DevState sh, int has_shadow) {
+    const int H = m.H, E = m.E, K = m.K, l = rl.layer;
+    double* red = reinterpret_cast<double*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 64);
+    float* tmp = xs + H;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(tmp + H));
+    const int nT = rl.do_true ? m.Ep / 32 : 0;
+    const bool gemv_pred = rl.pred_kind == kBaselineS || rl.pred_kind == kRouterPF;
+    const int nP = gemv_pred ? m.Ep / 32 : 0;
+    const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
+    const int b = blockIdx.x;
+    const float* r = st.r + static_cast<long long>(l) * m.Hp;
+    if (b < nT || (b < nT + nP && rl.pred_kind == kBaselineS)) {
+        block_rms_norm(r, m.moe_gain + static_cast<long long>(l) * H, H, m.eps, xs, red);
+        if (b == 0 && rl.do_true)
+            for (int j = threadIdx.x; j < H; j += blockDim.x) st.s[static_cast<long long>(l) * m.Hp + j] = xs[j];
+    } else if (b < nT + nP + nQ) {
+        compute_quasi(m, st, l, rl.exec_from, xs, tmp, red);
+        if (b == nT)
+            for (int j = threadIdx.x; j < H; j += blockDim.x) st.quasi[j] = xs[j];
+    }
+    if (b < nT + nP) {
+        PipeB pipe;
+        pipe.init(pipe_mem);
+        const bool is_true = b < nT;
+        const int rb = is_true ? b : b - nT;
+        const int gl = is_true ? l : l + 1;
+        const uint16_t* tile = m.gate + gl * m.gate_stride + static_cast<long long>(rb) * H * 32;
+        const float acc = pipe.run(tile, H, xs);
+        const int e = rb * 32 + (threadIdx.x & 31);
+        if (e < E) {
+            if (is_true)
+                st.lg_true[static_cast<long long>(l) * E + e] = acc;
+            else
+                st.lg_pred[static_cast<long long>(l + 1) * E + e] = acc;
+        }
+    }
+    if (!last_cta(st.counters + 0, gridDim.x)) return;
+    // ---- finalize (one CTA, warp 0) ----
+    double* se = reinterpret_cast<double*>(pipe_mem);            // [E]
+    float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);  // [E]
+    if (rl.do_true)
+        warp_decision(st.lg_true + static_cast<long long>(l) * E, E, K, m.gating, sp, se,
+                      st.id_true + l * K, st.g_true + l * K);
+    if (gemv_pred)
+        warp_decision(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, m.gating, sp, se,
+                      st.id_pred + (l + 1) * K, st.g_pred + (l + 1) * K);
+    if (threadIdx.x == 0) {
+        if (rl.pred_kind == kOracle && has_shadow) {  // Oracle: shadow true decisions (speculation.cpp:296-305)
+            for (int i = 0; i < K; ++i) {
+                st.id_pred[(l + 1) * K + i] = sh.id_true[(l + 1) * K + i];
+                st.g_pred[(l + 1) * K + i] = sh.g_true[(l + 1) * K + i];
+            }
+        }
+        if (rl.exec_from == 0) {
+            for (int i = 0; i < K; ++i) {
+                st.id_exec[l * K + i] = st.id_true[l * K + i];
+                st.g_exec[l * K + i] = st.g_true[l * K + i];
+            }
+        } else if (rl.exec_from == 1) {
+            for (int i = 0; i < K; ++i) {
+                st.id_exec[l * K + i] = st.id_pred[l * K + i];
+                st.g_exec[l * K + i] = st.g_pred[l * K + i];
+            }
+        }
+        if (rl.post_exec) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
+        if (rl.post_pred) post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+    }
+    if (rl.pred_kind == kOracle && has_shadow)
+        for (int e = threadIdx.x; e < E; e += blockDim.x)
+            st.lg_pred[static_cast<long long>(l + 1) * E + e] = sh.lg_true[static_cast<long long>(l + 1) * E + e];
+}
+
+// --------------------------------------------------------------- estimator --
+// estimator_forward<float> (estimator.cpp:94-161), f32 throughout; stage kernels:
+//  A: z = A.q + pos[l]   B: act = silu_f32(B.z)   C: h = z + C.act, LayerNorm
+//  head: logits = W_head.(gain*xhat + bias), decision, mailbox.
+
+// expf as glibc rounds it: f64 exp rounded to f32 (estimator.cpp:121 uses std::exp<float>).
+__device__ __forceinline__ float expf_ref(float x) {
+    return static_cast<float>(exp(static_cast<double>(x)));
+}
+
+__global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                  int stage, int post_pred, int step_tag) {
+    const int dm = m.est_dm, mlp = m.est_mlp;
+    float* xs = reinterpret_cast<float*>(g_smem);
+    int cols;
+    const float* in;
+    const float* tiles;
+    if (stage == 0) {
+        cols = m.est_d;
+        in = st.quasi;
+        tiles = m.est_a;
+    } else if (stage == 1) {
+        cols = dm;
+        in = st.est_z;
+        tiles = m.est_b;
+    } else if (stage == 2) {
+        cols = mlp;
+        in = st.est_act;
+        tiles = m.est_c;
+    } else {
+        cols = dm;
+        in = st.est_xn;
+        tiles = m.est_head;
+    }
+    for (int i = threadIdx.x; i < cols; i += blockDim.x) xs[i] = in[i];
+    __syncwarp();
+    unsigned char* pipe_mem = align128(g_smem + cols * 4);
+    PipeF pipe;
+    pipe.init(pipe_mem);
+    const int rb = blockIdx.x;
+    const float acc = pipe.run(tiles + static_cast<long long>(rb) * cols * 32, cols, xs);
+    const int row = rb * 32 + (threadIdx.x & 31);
+    if (stage == 0) {
+        if (row < dm) st.est_z[row] = acc + m.est_pos[static_cast<long long>(layer) * dm + row];
+    } else if (stage == 1) {
+        if (row < mlp) st.est_act[row] = acc / (1.0f + expf_ref(-acc));
+    } else if (stage == 2) {
+        if (row < dm) st.est_xn[row] = st.est_z[row] + acc;  // h (normalised below)
+    } else {
+        if (row < m.E) st.lg_pred[static_cast<long long>(layer + 1) * m.E + row] = acc;
+    }
+    if (stage == 0 || stage == 1) return;
+    if (!last_cta(st.counters + 1, gridDim.x)) return;
+    if (stage == 2) {  // LayerNorm, mean/var in f32 sequential (estimator.cpp:137-151)
+        if (threadIdx.x == 0) {
+            float* h = st.est_xn;
+            float mean = 0.0f;
+            for (int j = 0; j < dm; ++j) mean += h[j];
+            mean /= static_cast<float>(dm);
+            float var = 0.0f;
+            for (int j = 0; j < dm; ++j) {
+                const float c = h[j] - mean;
+                var += c * c;
+            }
+            var /= static_cast<float>(dm);
+            const float inv_std = 1.0f / sqrtf(var + m.est_eps);
+            for (int j = 0; j < dm; ++j) {
+                const float xhat = (h[j] - mean) * inv_std;
+                h[j] = m.est_gain[j] * xhat + m.est_bias[j];
+            }
+        }
+        return;
+    }
+    // stage 3: decision + mailbox
+    double* se = reinterpret_cast<double*>(pipe_mem);
+    float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);
+    warp_decision(st.lg_pred + static_cast<long long>(layer + 1) * m.E, m.E, m.K, m.gating, sp,
+                  se, st.id_pred + (layer + 1) * m.K, st.g_pred + (layer + 1) * m.K);
+    if (threadIdx.x == 0 && post_pred)
+        post_request(ctl, layer + 1, step_tag, st.id_pred + (layer + 1) * m.K, m.K);
+}
+
+// ------------------------------------------------------------- expert FFN --
+//
+// expert_ffn (model.cpp:283-288) for every executed expert, read from its HBM
+// slot.  gate/up: grid (Hmp/16, K), one warp per 16-row tile (lanes 2r, 2r+1
+// hold gate row r and up row r); h = silu(g) * u.
+
+__device__ void wait_ready(const DevCtl& ctl, int layer) {
+    if (threadIdx.x == 0) {
+        const int want = ctl.req_seq[layer];
+        const long long t0 = clock64();
+        while (ld_acquire(ctl.ready + layer) < want) {
+            if (*(volatile int*)ctl.error) break;
+            __nanosleep(128);
+            if (clock64() - t0 > ctl.spin_limit) {
+                atomicCAS(ctl.error, 0, 1000 + layer);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer) {
+    wait_ready(ctl, layer);
+    if (*(volatile int*)ctl.error) return;
+    const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
+    float* xs = reinterpret_cast<float*>(g_smem);
+    unsigned char* pipe_mem = align128(g_smem + H * 4);
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    const float* s = st.s + static_cast<long long>(layer) * m.Hp;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) xs[j] = s[j];
+    const int e = st.id_exec[layer * m.K + i];
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    if (slot < 0) {
+        if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+        return;
+    }
+    __syncwarp();
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
+                           static_cast<long long>(rb) * H * 32;
+    const float acc = pipe.run(tile, H, xs);
+    const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
+    const int lane = threadIdx.x & 31;
+    if ((lane & 1) == 0) {
+        const int row = rb * 16 + (lane >> 1);
+        st.h[static_cast<long long>(i) * m.Hmp + row] = silu_ref(acc) * up;
+    }
+}
+
+// down: grid Hp/32, K warps per CTA (warp i = i-th executed expert); then the
+// gate-weighted mixture in decision order (model.cpp:297-301) and the residual
+// x = r + m (model.cpp:386).
+__global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st, DevCtl ctl,
+                                                         int layer) {
+    if (*(volatile int*)ctl.error) return;
+    const int K = m.K, Hmp = m.Hmp, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* hs = reinterpret_cast<float*>(g_smem);          // [K][Hmp]
+    float* ys = hs + K * Hmp;                                // [K][32]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(ys + K * 32));
+    PipeD pipe;
+    pipe.init(pipe_mem + w * PipeD::kBytes);
+    for (int t = threadIdx.x; t < K * Hmp; t += blockDim.x) hs[t] = st.h[t];
+    __syncthreads();
+    const int e = st.id_exec[layer * K + w];
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    const int rb = blockIdx.x;
+    float acc = 0.0f;
+    if (slot >= 0) {
+        const uint16_t* tile = m.slots +
+                               (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
+                               m.gu_elems + static_cast<long long>(rb) * Hmp * 32;
+        acc = pipe.run(tile, m.Hm, hs + w * Hmp);
+    }
+    ys[w * 32 + lane] = acc;
+    const int j = rb * 32 + lane;
+    if (j < m.H) st.y[static_cast<long long>(w) * m.Hp + j] = acc;
+    __syncthreads();
+    if (w == 0 && j < m.H) {
+        float out = 0.0f;
+        for (int i = 0; i < K; ++i) out += st.g_exec[layer * K + i] * ys[i * 32 + lane];
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        st.x[j] = st.r[static_cast<long long>(layer) * m.Hp + j] + out;
+    }
+}
+
+// ------------------------------------------------------------ final / argmax --
+// h = rms_norm(x, final_gain); logits = unembed . h (model.cpp:388-389);
+// greedy argmax, first maximum (model.cpp:391-396).
+__global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ctl,
+                                              int record_token) {
+    double* red = reinterpret_cast<double*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 64);
+    unsigned char* pipe_mem = align128(g_smem + 64 + m.H * 4);
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    block_rms_norm(st.x, m.final_gain, m.H, m.eps, xs, red);
+    const int rb = blockIdx.x;
+    const float acc = pipe.run(m.unemb + static_cast<long long>(rb) * m.H * 32, m.H, xs);
+    const int v = rb * 32 + (threadIdx.x & 31);
+    if (v < m.V) st.logits[v] = acc;
+    if (!last_cta(st.counters + 2, gridDim.x)) return;
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int i = 1; i < m.V; ++i)
+            if (st.logits[i] > st.logits[best]) best = i;
+        *st.token = best;
+        *st.pos = *st.pos + 1;
+        if (record_token) {
+            const int s = *ctl.step;
+            ctl.tokens_out[s] = best;
+            *ctl.step = s + 1;
+        }
+    }
+}
+
+// ----------------------------------------------------------- calibration ----
+
+__global__ void k_dv_accum(DevModel m, DevState st, double* sums, long long* counts, int layer) {
+    const int K = m.K, H = m.H;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * H; t += gridDim.x * blockDim.x) {
+        const int i = t / H, j = t % H;
+        const int e = st.id_exec[layer * K + i];
+        sums[(static_cast<long long>(layer) * m.E + e) * H + j] += st.y[static_cast<long long>(i) * m.Hp + j];
+        if (j == 0) counts[static_cast<long long>(layer) * m.E + e] += 1;
+    }
+}
+
+__global__ void k_dv_freeze(const double* sums, const long long* counts, float* dv, long long LE,
+                            int H) {
+    const long long n = LE * H;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long c = counts[t / H];
+        dv[t] = c == 0 ? 0.0f : static_cast<float>(sums[t] / static_cast<double>(c));
+    }
+}
+
+// ----------------------------------------------------------------- trace ----
+
+__global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
+    const int step = *tr.step;
+    if (step >= tr.cap) return;
+    const int L = m.L, H = m.H, E = m.E, K = m.K, V = m.V, Hp = m.Hp;
+    const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long gs = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t = t0; t < static_cast<long long>(L) * K; t += gs) {
+        const long long o = static_cast<long long>(step) * L * K + t;
+        tr.id_true[o] = st.id_true[t];
+        tr.id_exec[o] = st.id_exec[t];
+        tr.id_pred[o] = st.id_pred[t];
+        if (tr.full) {
+            tr.g_true[o] = st.g_true[t];
+            tr.g_exec[o] = st.g_exec[t];
+            tr.g_pred[o] = st.g_pred[t];
+        }
+    }
+    if (!tr.full) {
+        __syncthreads();
+        if (t0 == 0) *tr.step = step + 1;  // single CTA launch in ids-only mode
+        return;
+    }
+    for (long long t = t0; t < static_cast<long long>(L) * H; t += gs) {
+        const long long l = t / H, j = t % H;
+        const long long o = static_cast<long long>(step) * L * H + t;
+        tr.s[o] = st.s[l * Hp + j];
+        tr.r[o] = st.r[l * Hp + j];
+        tr.m[o] = st.m[l * Hp + j];
+    }
+    for (long long t = t0; t < static_cast<long long>(L) * E; t += gs) {
+        const long long o = static_cast<long long>(step) * L * E + t;
+        tr.lg_true[o] = st.lg_true[t];
+        tr.lg_pred[o] = st.lg_pred[t];
+    }
+    for (long long t = t0; t < V; t += gs) tr.logits[static_cast<long long>(step) * V + t] = st.logits[t];
+}
+
+// Per-layer raw outputs are overwritten by the next layer, so the full trace
+// grabs them right after each layer's down projection.
+__global__ void k_trace_y(DevModel m, DevState st, TraceDev tr, int layer) {
+    const int step = *tr.step;
+    if (step >= tr.cap) return;
+    const int K = m.K, H = m.H, L = m.L;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * H; t += gridDim.x * blockDim.x) {
+        const int i = t / H, j = t % H;
+        tr.y[((static_cast<long long>(step) * L + layer) * K + i) * H + j] = st.y[static_cast<long long>(i) * m.Hp + j];
+    }
+}
+
+__global__ void k_trace_bump(TraceDev tr) {
+    if (*tr.step < tr.cap) *tr.step = *tr.step + 1;
+}
+
+// ============================================================== launchers ==
+
+namespace {
+inline int gen_blocks(long long n) {
+    long long b = (n + 255) / 256;
+    if (b > 148LL * 64) b = 148LL * 64;
+    return static_cast<int>(b < 1 ? 1 : b);
+}
+size_t qkv_smem(const DevModel& m) { return 64 + m.H * 4 + 128 + PipeB::kBytes; }
+size_t wo_smem(const DevModel&) { return kMaxD * 4 + 128 + PipeB::kBytes; }
+size_t router_smem(const DevModel& m) {
+    size_t a = 64 + 2 * m.H * 4 + 128 + PipeB::kBytes;
+    size_t b = 64 + 2 * m.H * 4 + 128 + kMaxE * 12;
+    return a > b ? a : b;
+}
+size_t est_smem(const DevModel& m) {
+    int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
+    cols = cols > kMaxE ? cols : kMaxE;
+    return static_cast<size_t>(cols) * 4 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
+}
+size_t gu_smem(const DevModel& m) { return m.H * 4 + 128 + PipeB::kBytes; }
+size_t down_smem(const DevModel& m) {
+    return static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 128 +
+           static_cast<size_t>(m.K) * PipeD::kBytes;
+}
+size_t final_smem(const DevModel& m) { return 64 + m.H * 4 + 128 + PipeB::kBytes; }
+
+cudaError_t set_smem(const void* fn, size_t bytes) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes));
+}
+}  // namespace
+
+int max_dynamic_smem_needed(const DevModel& m) {
+    size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m), est_smem(m), gu_smem(m), down_smem(m),
+                  final_smem(m)};
+    size_t mx = 0;
+    for (size_t x : v) mx = x > mx ? x : mx;
+    return static_cast<int>(mx);
+}
+
+cudaError_t launch_gen_bf16(uint64_t seed, float stddev, int R, int C, int tile_cols, int layout,
+                            int which, int row_off, uint16_t* out, cudaStream_t s) {
+    // total destination elements covered by this call
+    long long total;
+    if (layout == kRowMajor) {
+        total = static_cast<long long>(R) * C;
+    } else if (layout == kRowTiled) {
+        total = static_cast<long long>(round_up(R + row_off, 32)) * tile_cols;
+    } else {
+        total = static_cast<long long>(round_up(2 * R, 32)) * tile_cols;
+    }
+    k_gen_bf16<<<gen_blocks(total), 256, 0, s>>>(seed, static_cast<double>(stddev), R, C,
+                                                  tile_cols, layout, which, row_off, total, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
+                         cudaStream_t s) {
+    k_embed<<<(m.Hp + 255) / 256, 256, 0, s>>>(m, st, token_src);
+    return cudaGetLastError();
+}
+
+// Loads every kernel up front.  With CUDA lazy loading, the first launch of
+// a not-yet-loaded kernel synchronises the context; if that happens while an
+// expert kernel spins on a copy-ready flag the copy thread's API calls block
+// behind it (observed deadlock).  Session construction calls this once.
+cudaError_t preload_kernels() {
+    const void* fns[] = {(const void*)k_gen_bf16, (const void*)k_embed, (const void*)k_qkv,
+                         (const void*)k_attn, (const void*)k_wo, (const void*)k_router,
+                         (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
+                         (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
+                         (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump};
+    for (const void* f : fns) {
+        cudaFuncAttributes a;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaSuccess;
+    const void* big[] = {(const void*)k_qkv, (const void*)k_wo, (const void*)k_router,
+                         (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_final};
+    for (const void* f : big)
+        if ((e = set_smem(f, 200 * 1024)) != cudaSuccess) return e;
+    return set_smem((const void*)k_ffn_down, 220 * 1024);
+}
+
+cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
+    k_qkv<<<m.QKVp / 32, 32, qkv_smem(m), s>>>(m, st, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
+                        cudaStream_t s) {
+    k_attn<<<1, 256, kMaxD * 4 + 32 * 4 + 32 * 8, s>>>(m, st, scratch, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
+    k_wo<<<m.Hp / 32, 32, wo_smem(m), s>>>(m, st, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                          const RouterLaunch& rl, const DevState* shadow, cudaStream_t s) {
+    const int nT = rl.do_true ? m.Ep / 32 : 0;
+    const bool gemv_pred = rl.pred_kind == kBaselineS || rl.pred_kind == kRouterPF;
+    const int nP = gemv_pred ? m.Ep / 32 : 0;
+    const int nQ = rl.pred_kind == kEstPF ? 1 : 0;
+    int grid = nT + nP + nQ;
+    if (grid < 1) grid = 1;
+    DevState sh = shadow ? *shadow : st;
+    k_router<<<grid, 32, router_smem(m), s>>>(m, st, ctl, rl, sh, shadow ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                             int post_pred, int step_tag, cudaStream_t s) {
+    const size_t sm = est_smem(m);
+    k_est_stage<<<round_up(m.est_dm, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 0, 0, step_tag);
+    k_est_stage<<<round_up(m.est_mlp, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 1, 0, step_tag);
+    k_est_stage<<<round_up(m.est_dm, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 2, 0, step_tag);
+    k_est_stage<<<m.Ep / 32, 32, sm, s>>>(m, st, ctl, layer, 3, post_pred, step_tag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                       cudaStream_t s) {
+    k_ffn_gu<<<dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s>>>(m, st, ctl, layer);
+    k_ffn_down<<<m.Hp / 32, 32 * m.K, down_smem(m), s>>>(m, st, ctl, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                         int record_token, cudaStream_t s) {
+    k_final<<<m.Vp / 32, 32, final_smem(m), s>>>(m, st, ctl, record_token);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dv_accum(const DevModel& m, const DevState& st, double* sums,
+                            long long* counts, int layer, cudaStream_t s) {
+    k_dv_accum<<<(m.K * m.H + 255) / 256, 256, 0, s>>>(m, st, sums, counts, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dv_freeze(const double* sums, const long long* counts, float* dv,
+                             long long LE, int H, cudaStream_t s) {
+    k_dv_freeze<<<gen_blocks(LE * H), 256, 0, s>>>(sums, counts, dv, LE, H);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
+                         cudaStream_t s) {
+    if (!tr.full) {
+        k_trace<<<1, 256, 0, s>>>(m, st, tr);
+    } else {
+        k_trace<<<64, 256, 0, s>>>(m, st, tr);
+        k_trace_bump<<<1, 1, 0, s>>>(tr);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
+                           cudaStream_t s) {
+    k_trace_y<<<16, 256, 0, s>>>(m, st, tr, layer);
+    return cudaGetLastError();
+}
+
+}  // namespace smoe

@@ -1,0 +1,71 @@
+// kernels.h — host-callable launchers for the sm_100a kernels in kernels.cu.
+// Every launcher enqueues on the given stream and returns the launch error.
+// DevModel / DevState / DevCtl are passed by value (kernel parameters), so a
+// captured CUDA graph replays with the same pointers; all per-token dynamic
+// values (position, token, request numbers) live in device memory.
+#pragma once
+#include "smoe_dev.h"
+
+#include <cuda_runtime.h>
+
+namespace smoe {
+
+// Weight init (model.cpp:112-158 stream semantics, counter-based splitmix64):
+// element n of the reference's row-major [R][C] tensor is
+// f32(gaussian_n(seed) * f64(stddev)), rounded to bf16 (RNE) and written to
+// `out` in the given layout (row_offset shifts rows inside a row-tiled block
+// that packs several matrices, e.g. [wq; wk; wv]).
+enum GenLayout : int { kRowMajor = 0, kRowTiled = 1, kGateUp = 2 };
+cudaError_t launch_gen_bf16(uint64_t seed, float stddev, int R, int C, int tile_cols, int layout,
+                            int which, int row_offset, uint16_t* out, cudaStream_t s);
+
+struct RouterLaunch {
+    int layer;
+    int do_true;        // evaluate the true router of `layer`
+    int pred_kind;      // PredKind used to predict layer+1 (kNone = no prediction here)
+    int exec_from;      // 0: exec = true decision, 1: exec = pred decision of `layer`, -1: leave
+    int post_exec;      // post (layer, exec ids) to the mailbox
+    int post_pred;      // post (layer+1, pred ids) to the mailbox
+    int step_tag;       // mailbox step tag
+};
+
+cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
+                         cudaStream_t s);
+cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
+cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
+                        cudaStream_t s);
+cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
+cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                          const RouterLaunch& rl, const DevState* shadow, cudaStream_t s);
+cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                             int layer, int post_pred, int step_tag, cudaStream_t s);
+cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                       cudaStream_t s);
+cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                         int record_token, cudaStream_t s);
+
+// Default-vector calibration: f64 sums of raw expert outputs in token order
+// (speculation.cpp:28-42), frozen to f32 means (speculation.cpp:49-58).
+cudaError_t launch_dv_accum(const DevModel& m, const DevState& st, double* sums,
+                            long long* counts, int layer, cudaStream_t s);
+cudaError_t launch_dv_freeze(const double* sums, const long long* counts, float* dv,
+                             long long LE, int H, cudaStream_t s);
+
+// Per-step record capture (LayerTraceRecord, model.hpp:94-103).
+struct TraceDev {
+    int* step;          // device step counter
+    int cap;            // steps allocated
+    int full;           // 0: ids only (hit-rate history), 1: all fields
+    float *s, *r, *m, *lg_true, *g_true, *g_exec, *lg_pred, *g_pred, *y, *logits;
+    int *id_true, *id_exec, *id_pred;
+};
+cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
+                         cudaStream_t s);
+
+cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
+                           cudaStream_t s);
+
+int max_dynamic_smem_needed(const DevModel& m);
+cudaError_t preload_kernels();
+
+}  // namespace smoe

@@ -1,0 +1,127 @@
+// smoe_dev.h — device-side data layout shared by the host engine (engine.cpp)
+// and the sm_100a kernels (kernels.cu).  Plain C++ (no CUDA headers) so the
+// host engine can be compiled by g++.
+//
+// HBM layout:
+//   * every weight matrix the decode path streams is stored as *row tiles*:
+//     [R/32][cols][32] bf16 — 32 consecutive output rows interleaved per input
+//     column, so one warp (lane = output row) reads 64 contiguous bytes per
+//     column and a CTA stages a [chunk of columns x 32 rows] tile with one
+//     cp.async.bulk.  Each lane keeps the reference's *sequential* f32 dot
+//     product (numerics.cpp:136-147) for its row, so results are bit-identical.
+//   * an expert (l, e) is one contiguous block of expert_elems bf16:
+//       gate/up part  [Hmp/16][H][16][2]  (virtual row 2r = w_gate row r,
+//                                          2r+1 = w_up row r)
+//       down part     [Hp/32][Hmp][32]
+//     which is exactly one cudaMemcpyAsync between the pinned host store and
+//     an HBM slot.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace smoe {
+
+constexpr int kMaxK = 16;         // top-k limit
+constexpr int kMaxE = 1024;       // experts per layer limit
+constexpr int kMaxD = 256;        // head_dim limit
+constexpr int kRowTile = 32;      // rows per warp tile
+constexpr int kMailboxRing = 1024;
+
+enum PredKind : int { kBaselineS = 0, kRouterPF = 1, kEstPF = 2, kHybrid = 3, kOracle = 4, kNone = -1 };
+enum Gating : int { kSoftmaxTopK = 0, kTopKSoftmax = 1 };
+
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// One mailbox entry (pinned, mapped host memory).  Device writes the body,
+// __threadfence_system(), then `seq` last; the host scheduler polls `seq`.
+struct MailboxEntry {
+    volatile int seq;   // request number (monotonic, 1-based)
+    int layer;
+    int step;           // decode step (-1 prefill / shadow)
+    int nids;
+    int ids[kMaxK];
+    int pad[12];
+};
+
+struct DevModel {
+    int L, E, K, H, Hm, V, D;
+    float eps;
+    int gating;
+    int Hmp;            // Hm padded to 16 (gate/up tiles hold 16 rows x {gate,up})
+    int Hp;             // H padded to 32 (down / Wo row tiles)
+    int Ep, Vp, QKVp;   // router / unembed / qkv rows padded to 32
+    int cap;            // KV capacity (positions)
+    float inv_sqrt_d;   // 1.0f / sqrtf(D), computed on the host like model.cpp:336
+    const uint16_t* emb;      // [V][H] row-major bf16
+    const uint16_t* unemb;    // row tiles of unembed [V][H]
+    const float* final_gain;  // [H]
+    const float* attn_gain;   // [L][H]
+    const float* moe_gain;    // [L][H]
+    const uint16_t* wqkv;     // [L] x row tiles of [wq; wk; wv] (3D x H)
+    const uint16_t* wo;       // [L] x row tiles of wo (H x D)
+    const uint16_t* gate;     // [L] x row tiles of gate (E x H)
+    const float* rope;        // [cap][D/2][2] cos, sin (host libm, model.cpp:309-321)
+    long long qkv_stride, wo_stride, gate_stride;  // elements per layer
+    // expert cache
+    const uint16_t* slots;    // [L*C][expert_elems]
+    const int* slot_of;       // [L][E] -> slot index in layer, -1 = absent
+    int C;
+    long long expert_elems, gu_elems;
+    // speculation artifacts
+    const float* dv;          // [L][E][H] default vectors (f32)
+    // estimator (f32 row tiles): A (dm x d), B (mlp x dm), C (dm x mlp), W_head (E x dm)
+    int est_d, est_dm, est_mlp;
+    float est_eps;
+    const float* est_a;
+    const float* est_pos;     // [L][dm]
+    const float* est_b;
+    const float* est_c;
+    const float* est_gain;
+    const float* est_bias;
+    const float* est_head;
+    const int* hybrid;        // [L-1] predictor kind per layer
+};
+
+// Per-stream decode state (the main stream, and the Oracle's shadow stream).
+struct DevState {
+    float* x;          // [Hp] residual input of the current layer
+    float* r;          // [L][Hp]
+    float* s;          // [L][Hp]
+    float* m;          // [L][Hp]
+    float* q;          // [D]   attention query (after RoPE)
+    float* ctx;        // [D]
+    float* kc;         // [L][cap][D]
+    float* vc;         // [L][cap][D]
+    float* lg_true;    // [L][E]
+    int* id_true;      // [L][K]
+    float* g_true;     // [L][K]
+    int* id_exec;      // [L][K]
+    float* g_exec;     // [L][K]
+    float* lg_pred;    // [L][E]  index = predicted layer (l+1)
+    int* id_pred;      // [L][K]
+    float* g_pred;     // [L][K]
+    float* quasi;      // [Hp]  q_l of the last prediction (router-pf / est-pf)
+    float* est_z;      // [dm]
+    float* est_act;    // [mlp]
+    float* est_xn;     // [dm] gain*xhat + bias
+    float* h;          // [K][Hmp]
+    float* y;          // [K][Hp]  raw expert outputs (decision order)
+    float* logits;     // [V]
+    int* pos;          // position
+    int* token;        // current token
+    int* counters;     // last-CTA counters [64]
+};
+
+// Cross-stream control block (device memory unless noted).
+struct DevCtl {
+    MailboxEntry* mailbox;   // mapped pinned host memory, kMailboxRing entries
+    int* req_counter;        // requests issued so far
+    int* req_seq;            // [L] request number the next FFN at layer l waits for
+    int* ready;              // [L] last completed request number per layer (copy stream writes)
+    int* error;              // device-detected error code (deadlock etc.)
+    int* step;               // decode step counter
+    int* tokens_out;         // [max_steps]
+    long long spin_limit;    // clock64 cycles before declaring a deadlock
+};
+
+}  // namespace smoe

@@ -1,0 +1,245 @@
+"""ctypes binding of libsmoe_b200.so (include/smoe.h).
+
+This is the Python face of the C ABI, used by tests/ and bench.py.  It mirrors
+the reference's decode-path API (proj/include/specmoe): ``ModelConfig``,
+``ExecutorOptions`` / ``OffloadMode``, ``make_predictor`` kinds and
+``run_offloaded_decode``.  There is no CPU fallback: if the CUDA library is
+missing or no GPU is present, constructing a ``Session`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmoe_b200.so")
+
+PRED = {"none": -1, "baseline-s": 0, "router-pf": 1, "est-pf": 2, "hybrid": 3, "oracle": 4}
+MODE = {"on_demand": 0, "prefetch": 1}
+GATING = {"softmax-topk-renorm": 0, "topk-softmax": 1}
+
+# Symbols declared by include/smoe.h (checked by tests/test_capi.py).
+EXPORTS = [
+    "smoe_last_error", "smoe_session_create", "smoe_session_destroy", "smoe_init_weights_seeded",
+    "smoe_load_tensor", "smoe_load_default_vectors", "smoe_load_estimator", "smoe_set_predictor",
+    "smoe_set_cache_fraction", "smoe_reset", "smoe_prefill", "smoe_decode",
+    "smoe_run_offloaded_decode", "smoe_step", "smoe_calibrate", "smoe_steps_done",
+    "smoe_read_tokens", "smoe_read_trace", "smoe_token_ms", "smoe_counters", "smoe_copy_events",
+    "smoe_cache_slots",
+]
+
+
+class _Config(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("experts", C.c_int32), ("top_k", C.c_int32),
+                ("hidden", C.c_int32), ("expert_hidden", C.c_int32), ("vocab", C.c_int32),
+                ("head_dim", C.c_int32), ("eps", C.c_float), ("seed", C.c_uint64),
+                ("gating", C.c_int32)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("cache_fraction", C.c_float),
+                ("max_positions", C.c_int32), ("copy_latency_us", C.c_int32),
+                ("deadlock_s", C.c_double)]
+
+
+class _EstConfig(C.Structure):
+    _fields_ = [("d", C.c_int32), ("m", C.c_int32), ("n", C.c_int32), ("experts", C.c_int32),
+                ("layers", C.c_int32), ("eps", C.c_float)]
+
+
+class CopyEvent(C.Structure):
+    _fields_ = [("seq", C.c_int32), ("layer", C.c_int32), ("step", C.c_int32),
+                ("hits", C.c_int32), ("misses", C.c_int32), ("bytes", C.c_int64),
+                ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
+@dataclass
+class ModelConfig:
+    """ModelConfig (model.hpp:28-47)."""
+    layers: int
+    experts: int
+    top_k: int
+    hidden: int
+    expert_hidden: int
+    vocab: int
+    head_dim: int
+    eps: float = 1e-5
+    seed: int = 0
+    gating: str = "softmax-topk-renorm"
+
+    def _c(self):
+        return _Config(self.layers, self.experts, self.top_k, self.hidden, self.expert_hidden,
+                       self.vocab, self.head_dim, self.eps, self.seed, GATING[self.gating])
+
+    def expert_bytes_bf16(self) -> int:
+        return 3 * self.hidden * self.expert_hidden * 2
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build() first")
+        lib = C.CDLL(path)
+        lib.smoe_last_error.restype = C.c_char_p
+        for name in EXPORTS:
+            getattr(lib, name)  # raises AttributeError if not exported
+        _lib = lib
+    return _lib
+
+
+class SmoeError(RuntimeError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        msg = _lib.smoe_last_error().decode()
+        raise (ValueError if rc == 1 else SmoeError)(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Session:
+    """One model on one GPU: pinned expert store + HBM slot cache + decode state."""
+
+    def __init__(self, cfg: ModelConfig, device: int = 0, cache_fraction: float = 1.0,
+                 max_positions: int = 4096, copy_latency_us: int = 0, deadlock_s: float = 10.0):
+        lib = load_library()
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        opt = _Options(device, cache_fraction, max_positions, copy_latency_us, deadlock_s)
+        c = cfg._c()
+        _check(lib.smoe_session_create(C.byref(c), C.byref(opt), C.byref(self._h)))
+        self.lib = lib
+
+    def close(self):
+        if self._h:
+            _check(self.lib.smoe_session_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- weights / artifacts -------------------------------------------------
+    def init_weights_seeded(self):
+        _check(self.lib.smoe_init_weights_seeded(self._h))
+
+    def load_tensor(self, name: str, data: np.ndarray):
+        d = np.ascontiguousarray(data, np.float32).ravel()
+        _check(self.lib.smoe_load_tensor(self._h, name.encode(), _p(d), C.c_int64(d.size)))
+
+    def load_default_vectors(self, d: np.ndarray):
+        d = np.ascontiguousarray(d, np.float32).ravel()
+        _check(self.lib.smoe_load_default_vectors(self._h, _p(d), C.c_int64(d.size)))
+
+    def load_estimator(self, d, m, n, E, L, eps, flat):
+        f = np.ascontiguousarray(flat, np.float32).ravel()
+        c = _EstConfig(d, m, n, E, L, eps)
+        _check(self.lib.smoe_load_estimator(self._h, C.byref(c), _p(f), C.c_int64(f.size)))
+
+    def set_predictor(self, kind: str, hybrid=None):
+        hm = None
+        if hybrid is not None:
+            hm = np.ascontiguousarray([PRED[k] if isinstance(k, str) else k for k in hybrid],
+                                      np.int32)
+        _check(self.lib.smoe_set_predictor(self._h, PRED[kind], _p(hm)))
+
+    def set_cache_fraction(self, f: float):
+        _check(self.lib.smoe_set_cache_fraction(self._h, C.c_float(f)))
+
+    def cache_slots(self) -> int:
+        n = C.c_int32()
+        _check(self.lib.smoe_cache_slots(self._h, C.byref(n)))
+        return n.value
+
+    # -- decode ----------------------------------------------------------------
+    def reset(self, max_steps: int = 0, trace_full: bool = False):
+        _check(self.lib.smoe_reset(self._h, max_steps, int(trace_full)))
+
+    def prefill(self, tokens):
+        t = np.ascontiguousarray(tokens, np.int32)
+        _check(self.lib.smoe_prefill(self._h, _p(t), len(t)))
+
+    def decode(self, mode: str, n_steps: int, use_graph: bool = True):
+        _check(self.lib.smoe_decode(self._h, MODE[mode], n_steps, int(use_graph)))
+
+    def run_offloaded_decode(self, prompt, n_new: int, mode: str):
+        """run_offloaded_decode (executor.cpp:326-359): tokens + device-timed per-token ms."""
+        p = np.ascontiguousarray(prompt, np.int32)
+        toks = np.zeros(n_new, np.int32)
+        per = np.zeros(max(n_new - 1, 1), np.float64)
+        _check(self.lib.smoe_run_offloaded_decode(self._h, _p(p), len(p), n_new, MODE[mode],
+                                                  _p(toks), _p(per)))
+        return toks, per[: n_new - 1]
+
+    def step(self, mode: str, token: int, logits: np.ndarray | None = None) -> int:
+        nxt = C.c_int32()
+        _check(self.lib.smoe_step(self._h, MODE[mode], token, _p(logits), C.byref(nxt)))
+        return nxt.value
+
+    def calibrate(self, ntok: int, seed: int, seq_len: int):
+        c = self.cfg
+        d = np.zeros((c.layers, c.experts, c.hidden), np.float32)
+        cnt = np.zeros((c.layers, c.experts), np.int64)
+        _check(self.lib.smoe_calibrate(self._h, C.c_int64(ntok), C.c_uint64(seed), seq_len,
+                                       _p(d), _p(cnt)))
+        return d, cnt
+
+    # -- results ---------------------------------------------------------------
+    def steps_done(self) -> int:
+        n = C.c_int32()
+        _check(self.lib.smoe_steps_done(self._h, C.byref(n)))
+        return n.value
+
+    def tokens(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.int32)
+        _check(self.lib.smoe_read_tokens(self._h, _p(out), n))
+        return out
+
+    def trace(self, field: str, steps: int) -> np.ndarray:
+        c = self.cfg
+        L, K, H, E, V = c.layers, c.top_k, c.hidden, c.experts, c.vocab
+        shapes = {"id_true": (L, K), "id_exec": (L, K), "id_pred": (L, K), "g_true": (L, K),
+                  "g_exec": (L, K), "g_pred": (L, K), "s": (L, H), "r": (L, H), "m": (L, H),
+                  "lg_true": (L, E), "lg_pred": (L, E), "y": (L, K, H), "logits": (V,)}
+        dt = np.int32 if field.startswith("id_") else np.float32
+        out = np.zeros((steps,) + shapes[field], dt)
+        _check(self.lib.smoe_read_trace(self._h, field.encode(), _p(out), C.c_int64(out.size)))
+        return out
+
+    def token_ms(self) -> np.ndarray:
+        out = np.zeros(4096, np.float64)
+        n = C.c_int32()
+        _check(self.lib.smoe_token_ms(self._h, _p(out), len(out), C.byref(n)))
+        return out[: min(n.value, len(out))].copy()
+
+    def counters(self):
+        L = self.cfg.layers
+        hits = np.zeros(L, np.int64)
+        misses = np.zeros(L, np.int64)
+        b = C.c_int64()
+        ms = C.c_double()
+        req = C.c_int32()
+        _check(self.lib.smoe_counters(self._h, _p(hits), _p(misses), C.byref(b), C.byref(ms),
+                                      C.byref(req)))
+        return {"hits": hits, "misses": misses, "h2d_bytes": b.value, "copy_ms": ms.value,
+                "requests": req.value}
+
+    def copy_events(self, cap: int = 65536):
+        arr = (CopyEvent * cap)()
+        n = C.c_int32()
+        _check(self.lib.smoe_copy_events(self._h, arr, cap, C.byref(n)))
+        return [arr[i] for i in range(min(n.value, cap))]
