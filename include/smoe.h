@@ -127,6 +127,17 @@ int smoe_counters(smoe_session* s, int64_t* hits, int64_t* misses, int64_t* h2d_
 int smoe_copy_events(smoe_session* s, smoe_copy_event* out, int32_t cap, int32_t* n);
 /* Slots per layer actually allocated. */
 int smoe_cache_slots(smoe_session* s, int32_t* slots);
+/* Clears cache hit/miss counters, copy records and step timings (state kept). */
+int smoe_clear_stats(smoe_session* s);
+/* Average device time (us) per launch of each per-layer kernel, CUDA events on
+ * the compute stream over L back-to-back launches (one per layer, weights
+ * larger than L2), `reps` repetitions.  out_us[7]: qkv, attn, wo, router,
+ * ffn_gate_up, ffn_down, final.  Needs a completed decode step (resident experts). */
+int smoe_profile_kernels(smoe_session* s, int32_t reps, double* out_us);
+/* H2D GB/s of expert-sized copies from the pinned store into HBM. */
+int smoe_measure_link(smoe_session* s, int32_t n_copies, double* gbps);
+/* Kernel launches in one captured decode step (-1 before the first capture). */
+int smoe_kernels_per_step(smoe_session* s, int32_t mode, int32_t* n);
 /* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap);
 

@@ -107,6 +107,8 @@ class Ref(_Common):
         L.ref_last_error.restype = C.c_char_p
         L.ref_model_tensor.restype = C.c_int64
         L.ref_model_set_tensor.restype = C.c_int64
+        L.ref_model_set_tensor.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.ref_model_tensor.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         L.ref_derive_seed.restype = C.c_uint64
         L.ref_derive_seed.argtypes = [C.c_uint64, C.c_char_p]
         L.ref_silu.restype = C.c_float
@@ -133,6 +135,12 @@ class Ref(_Common):
     def build_model(self, cfg: Config, round_bf16: bool = True):
         h = C.c_void_p()
         self._check(self.lib.ref_build_model(*cfg.args(), int(round_bf16), C.byref(h)))
+        return RefModel(self, h, cfg)
+
+    def alloc_model(self, cfg: Config):
+        """Model with the reference's shapes and zero weights (fill with set_tensor)."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_alloc_model(*cfg.args(), C.byref(h)))
         return RefModel(self, h, cfg)
 
     def derive_seed(self, seed: int, label: str) -> int:

@@ -187,6 +187,49 @@ int ref_build_model(int L, int E, int K, int H, int Hm, int vocab, int hd, float
     });
 }
 
+// A Model with build_model's shapes (model.cpp:112-158) but zero weights, for
+// callers that fill the tensors themselves (the bench fills it with the
+// oracle's multithreaded generator; values are identical, tests pin that).
+int ref_alloc_model(int L, int E, int K, int H, int Hm, int vocab, int hd, float eps,
+                    std::uint64_t seed, int gating, void** out) {
+    return guard([&] {
+        ModelConfig c;
+        c.layers = L;
+        c.experts = E;
+        c.top_k = K;
+        c.hidden = H;
+        c.expert_hidden = Hm;
+        c.vocab = vocab;
+        c.head_dim = hd;
+        c.eps = eps;
+        c.seed = seed;
+        c.gating = gating == 0 ? GatingOrder::kSoftmaxThenTopK : GatingOrder::kTopKThenSoftmax;
+        c.validate();
+        auto* m = new Model();
+        m->config = c;
+        m->embedding = Mat(vocab, H);
+        m->unembed = Mat(vocab, H);
+        m->final_norm_gain.assign(H, 1.0f);
+        m->layers.resize(L);
+        for (LayerWeights& w : m->layers) {
+            w.attn_norm_gain.assign(H, 1.0f);
+            w.moe_norm_gain.assign(H, 1.0f);
+            w.wq = Mat(hd, H);
+            w.wk = Mat(hd, H);
+            w.wv = Mat(hd, H);
+            w.wo = Mat(H, hd);
+            w.gate = Mat(E, H);
+            w.experts.resize(E);
+            for (ExpertWeights& x : w.experts) {
+                x.w_gate = Mat(Hm, H);
+                x.w_up = Mat(Hm, H);
+                x.w_down = Mat(H, Hm);
+            }
+        }
+        *out = m;
+    });
+}
+
 // Returns the element count of a named tensor (0 if unknown); copies when out != null.
 std::int64_t ref_model_tensor(void* h, const char* name, float* out) {
     Model& m = *static_cast<Model*>(h);

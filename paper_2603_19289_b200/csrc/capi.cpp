@@ -230,4 +230,26 @@ int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->debug_state(out, cap); });
 }
 
+int smoe_clear_stats(smoe_session* s) {
+    return guard([&] { S(s)->clear_stats(); });
+}
+
+int smoe_profile_kernels(smoe_session* s, int32_t reps, double* out_us) {
+    return guard([&] {
+        if (reps < 1 || !out_us) throw std::invalid_argument("profile: reps >= 1 and out[7] required");
+        S(s)->profile_kernels(reps, out_us);
+    });
+}
+
+int smoe_measure_link(smoe_session* s, int32_t n_copies, double* gbps) {
+    return guard([&] {
+        if (n_copies < 1 || !gbps) throw std::invalid_argument("measure_link: n_copies >= 1");
+        *gbps = S(s)->measure_link(n_copies);
+    });
+}
+
+int smoe_kernels_per_step(smoe_session* s, int32_t mode, int32_t* n) {
+    return guard([&] { *n = S(s)->kernels_per_step(mode); });
+}
+
 }  // extern "C"

@@ -45,21 +45,26 @@ uint16_t f2bf(float x) {
     return static_cast<uint16_t>(u >> 16);
 }
 
-// Scatter a row-major f32 [R][C] tensor into a 32-row tiled bf16 buffer:
-// virtual row vr = r*mul + add + row_off, tile [vr/32][tile_cols][32].
+// Scatter a row-major f32 [R][C] tensor into the 32-row tile layout
+// (smoe_dev.h): virtual row vr = r*mul + add + row_off; tile [vr/32] of
+// tile_cols columns; inside a tile, columns in groups of G (16 bytes):
+// element (lane, c) at (c / G) * 32 * G + lane * G + c % G.
 void tile_write_bf16(uint16_t* dst, const float* src, int R, int C, int tile_cols, int mul,
                      int add, int row_off) {
     for (int r = 0; r < R; ++r) {
         const long long vr = static_cast<long long>(r) * mul + add + row_off;
-        uint16_t* base = dst + (vr / 32) * tile_cols * 32 + (vr % 32);
-        for (int c = 0; c < C; ++c) base[static_cast<long long>(c) * 32] = f2bf(src[static_cast<long long>(r) * C + c]);
+        uint16_t* base = dst + (vr / 32) * tile_cols * 32 + (vr % 32) * 8;
+        for (int c = 0; c < C; ++c)
+            base[static_cast<long long>(c / 8) * 256 + c % 8] = f2bf(src[static_cast<long long>(r) * C + c]);
     }
 }
 
 void tile_write_f32(float* dst, const float* src, int R, int C) {
+    const int tc = round_up(C, 4);
     for (int r = 0; r < R; ++r) {
-        float* base = dst + static_cast<long long>(r / 32) * C * 32 + (r % 32);
-        for (int c = 0; c < C; ++c) base[static_cast<long long>(c) * 32] = src[static_cast<long long>(r) * C + c];
+        float* base = dst + static_cast<long long>(r / 32) * tc * 32 + (r % 32) * 4;
+        for (int c = 0; c < C; ++c)
+            base[static_cast<long long>(c / 4) * 128 + c % 4] = src[static_cast<long long>(r) * C + c];
     }
 }
 
@@ -106,6 +111,8 @@ void ModelCfg::validate() const {
     if (E > kMaxE) throw std::invalid_argument("config: E > 1024 not supported on this path");
     if (D > kMaxD) throw std::invalid_argument("config: head_dim > 256 not supported on this path");
     if (H > 16384) throw std::invalid_argument("config: hidden > 16384 not supported on this path");
+    if (D % 8 != 0) throw std::invalid_argument("config: head_dim must be a multiple of 8 on this path");
+    if (H % 8 != 0) throw std::invalid_argument("config: hidden must be a multiple of 8 on this path");
 }
 
 // ------------------------------------------------------------ ExpertStore --
@@ -682,6 +689,7 @@ void Session::load_estimator(const EstCfg& e, const float* flat) {
     if (e.E != cfg_.E) throw std::invalid_argument("estimator: E must equal the model expert count");
     if (e.L != cfg_.L) throw std::invalid_argument("estimator: L must equal the model layer count");
     if (e.m <= 1 || e.n <= 1 || e.d % e.m != 0) throw std::invalid_argument("estimator: bad m/n");
+    if ((e.d / e.m) % 4 != 0) throw std::invalid_argument("estimator: latent width d/m must be a multiple of 4 on this path");
     const int dm = e.d / e.m, mlp = dm * e.n;
     const int dmp = round_up(dm, 32), mlpp = round_up(mlp, 32);
     const long long a_off = 0, pos_off = static_cast<long long>(dm) * e.d,
@@ -949,22 +957,7 @@ void Session::decode(int mode, int n_steps, int use_graph) {
     int pos = 0;
     ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
-    cudaGraphExec_t exec = nullptr;
-    if (use_graph) {
-        const long long key = mode * 10 + 1;
-        auto it = graphs_.find(key);
-        if (it == graphs_.end()) {
-            cudaGraph_t g;
-            ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
-            enqueue_step(mode, 0, 1, 0, s_comp_);
-            ck(cudaStreamEndCapture(s_comp_, &g), "capture");
-            ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
-            cudaGraphDestroy(g);
-            graphs_[key] = exec;
-        } else {
-            exec = it->second;
-        }
-    }
+    cudaGraphExec_t exec = use_graph ? get_graph(mode) : nullptr;
     ck(cudaEventRecord(ev_origin_, s_comp_), "event");
     for (int i = 0; i < n_steps; ++i) {
         const int ev = n_step_events_ < static_cast<int>(ev_step_.size() / 2) ? n_step_events_++ : -1;
@@ -983,21 +976,7 @@ int Session::step_host(int mode, int token, float* logits_out) {
     if (token < 0 || token >= cfg_.V) throw std::invalid_argument("forward_decode: token out of vocab");
     if (mode == 1 && pred_kind_ == kNone)
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
-    const long long key = mode * 10 + 1;
-    auto it = graphs_.find(key);
-    cudaGraphExec_t exec = nullptr;
-    if (it == graphs_.end()) {
-        sync();
-        cudaGraph_t g;
-        ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
-        enqueue_step(mode, 0, 1, 0, s_comp_);
-        ck(cudaStreamEndCapture(s_comp_, &g), "capture");
-        ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
-        cudaGraphDestroy(g);
-        graphs_[key] = exec;
-    } else {
-        exec = it->second;
-    }
+    cudaGraphExec_t exec = get_graph(mode);
     h_token_[0] = token;
     ck(cudaMemcpyAsync(st_.token, h_token_, 4, cudaMemcpyHostToDevice, s_comp_), "token H2D");
     ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
@@ -1062,6 +1041,129 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
 // ------------------------------------------------------------- results ------
 
 int Session::steps_done() { return steps_; }
+
+cudaGraphExec_t Session::get_graph(int mode) {
+    const long long key = mode * 10 + 1;
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) return it->second;
+    sync();
+    cudaGraph_t g;
+    cudaGraphExec_t exec = nullptr;
+    const long long before = launch_counter();
+    ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
+    enqueue_step(mode, 0, 1, 0, s_comp_);
+    ck(cudaStreamEndCapture(s_comp_, &g), "capture");
+    graph_kernels_[key] = static_cast<int>(launch_counter() - before);
+    ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+    cudaGraphDestroy(g);
+    graphs_[key] = exec;
+    return exec;
+}
+
+int Session::kernels_per_step(int mode) const {
+    auto it = graph_kernels_.find(mode * 10 + 1);
+    return it == graph_kernels_.end() ? -1 : it->second;
+}
+
+void Session::clear_stats() {
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    cache_->clear_stats();
+    sched_->clear_records();
+    n_step_events_ = 0;
+}
+
+void Session::profile_kernels(int reps, double* out) {
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    const int L = cfg_.L;
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    for (int k = 0; k < 7; ++k) {
+        // warm-up pass
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) ck(cudaEventRecord(a, s_comp_), "event");
+            const int R = pass == 0 ? 1 : reps;
+            for (int r = 0; r < R; ++r)
+                for (int l = 0; l < L; ++l) {
+                    switch (k) {
+                    case 0: ck(launch_qkv(dm_, st_, l, s_comp_), "qkv"); break;
+                    case 1: ck(launch_attn(dm_, st_, d_attn_scratch_, l, s_comp_), "attn"); break;
+                    case 2: ck(launch_wo(dm_, st_, l, s_comp_), "wo"); break;
+                    case 3: {
+                        RouterLaunch rl{l, 1, kNone, -1, 0, 0, -9};
+                        ck(launch_router(dm_, st_, ctl_, rl, nullptr, s_comp_), "router");
+                        break;
+                    }
+                    case 4:
+                    case 5: {
+                        // one of the two FFN kernels: launch the pair, subtract below
+                        ck(launch_ffn(dm_, st_, ctl_, l, s_comp_), "ffn");
+                        break;
+                    }
+                    case 6:
+                        if (l == 0) ck(launch_final(dm_, st_, ctl_, 0, s_comp_), "final");
+                        break;
+                    }
+                }
+            if (pass == 1) ck(cudaEventRecord(b, s_comp_), "event");
+        }
+        ck(cudaEventSynchronize(b), "event");
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        const double n = k == 6 ? reps : static_cast<double>(reps) * L;
+        out[k] = 1000.0 * ms / n;
+    }
+    // split the FFN pair with a gate/up-only and down-only timing
+    {
+        ck(cudaEventRecord(a, s_comp_), "event");
+        for (int r = 0; r < reps; ++r)
+            for (int l = 0; l < L; ++l) ck(launch_ffn_part(dm_, st_, ctl_, l, 0, s_comp_), "ffn");
+        ck(cudaEventRecord(b, s_comp_), "event");
+        ck(cudaEventSynchronize(b), "event");
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        out[4] = 1000.0 * ms / (static_cast<double>(reps) * L);
+        ck(cudaEventRecord(a, s_comp_), "event");
+        for (int r = 0; r < reps; ++r)
+            for (int l = 0; l < L; ++l) ck(launch_ffn_part(dm_, st_, ctl_, l, 1, s_comp_), "ffn");
+        ck(cudaEventRecord(b, s_comp_), "event");
+        ck(cudaEventSynchronize(b), "event");
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        out[5] = 1000.0 * ms / (static_cast<double>(reps) * L);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    sync();
+}
+
+double Session::measure_link(int n_copies) {
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    const long long bytes = store_->bytes_per_expert();
+    void* scratch = nullptr;
+    ck(cudaMalloc(&scratch, bytes), "scratch");
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    const long long nexp = static_cast<long long>(cfg_.L) * cfg_.E;
+    for (int i = 0; i < 4; ++i)
+        ck(cudaMemcpyAsync(scratch, store_->expert(i % nexp), bytes, cudaMemcpyHostToDevice, s_copy_), "warm");
+    ck(cudaEventRecord(a, s_copy_), "event");
+    for (int i = 0; i < n_copies; ++i)
+        ck(cudaMemcpyAsync(scratch, store_->expert((7919LL * i) % nexp), bytes, cudaMemcpyHostToDevice,
+                           s_copy_),
+           "link copy");
+    ck(cudaEventRecord(b, s_copy_), "event");
+    ck(cudaEventSynchronize(b), "event");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(scratch);
+    return static_cast<double>(bytes) * n_copies / (ms * 1e-3) / 1e9;
+}
 
 // Diagnostics: [req_counter, error, host next_seq, n_records, polls, mailbox seq of
 // the next slot, then ready[0..L), req_seq[0..L)].

@@ -152,6 +152,16 @@ public:
     const ModelCfg& cfg() const { return cfg_; }
     int slots_per_layer() const { return C_; }
     void debug_state(int* out, int cap);
+    void clear_stats();
+    // Average device time (us) per launch of each per-layer kernel, timed with
+    // CUDA events on the compute stream over L back-to-back launches (one per
+    // layer, so the streamed weights exceed L2), repeated `reps` times.
+    // out[7]: qkv, attn, wo, router, ffn_gate_up, ffn_down, final.
+    void profile_kernels(int reps, double* out);
+    // H2D GB/s of expert-sized copies from the pinned store (same allocation and
+    // copy size as the scheduler) into an HBM scratch block.
+    double measure_link(int n_copies);
+    int kernels_per_step(int mode) const;
 
     // used by the scheduler
     friend class CopyScheduler;
@@ -212,6 +222,8 @@ private:
     int steps_ = 0;
 
     std::map<long long, cudaGraphExec_t> graphs_;
+    std::map<long long, int> graph_kernels_;
+    cudaGraphExec_t get_graph(int mode);
     void drop_graphs();
 };
 

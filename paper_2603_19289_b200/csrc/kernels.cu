@@ -52,6 +52,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue (barrier init, static weight prefetch) while this one runs; every
+// kernel calls pdl_wait() before touching activations written upstream.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -107,24 +115,133 @@ __device__ void block_rms_norm(const float* v, const float* gain, int n, float e
     __syncthreads();
 }
 
+// ------------------------------------------------------------ smem stager --
+//
+// Stages a kernel's input vectors (activations, gains, default-vector rows,
+// expert hidden states) global -> shared with cp.async.bulk: thread 0 issues
+// one bulk copy per vector on a single mbarrier, so every vector is in flight
+// at once instead of one global-latency round trip per scalar load.  A
+// vector whose address/size is not 16-byte aligned falls back to a
+// block-strided copy.
+
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+struct Stager {
+    uint64_t* bar;
+    uint32_t phase;
+    __device__ void init(uint64_t* b) {  // whole block
+        bar = b;
+        phase = 0;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    // whole block; `bytes` is rounded up to 16 (buffers are padded)
+    __device__ void add(void* dst, const void* src, int bytes) {
+        const uint32_t b = static_cast<uint32_t>((bytes + 15) & ~15);
+        if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+            if (threadIdx.x == 0) {
+                mbar_expect(bar, b);
+                bulk_g2s(dst, src, b, bar);
+            }
+        } else {
+            const float* s = static_cast<const float*>(src);
+            float* d = static_cast<float*>(dst);
+            for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) d[i] = s[i];
+        }
+    }
+    __device__ void wait() {  // whole block
+        if (threadIdx.x == 0) mbar_arrive(bar);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        __syncthreads();
+    }
+};
+
 // ------------------------------------------------------- warp tile stream --
 //
 // One warp computes 32 sequential dot products acc(lane) = sum_c W[c][lane]*x[c]
 // over a row tile [cols][32] in global memory.  Lane 0 keeps S chunks of CC
 // columns in flight with cp.async.bulk; every lane walks the columns in order.
 
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// One 16-byte group of a lane's consecutive columns, in column order.
+__device__ __forceinline__ float chain_group(float acc, uint4 w, uint32_t xa, uint16_t) {
+    const float4 x0 = lds128f(xa), x1 = lds128f(xa + 16);
+    acc = acc + lo_bf(w.x) * x0.x;
+    acc = acc + hi_bf(w.x) * x0.y;
+    acc = acc + lo_bf(w.y) * x0.z;
+    acc = acc + hi_bf(w.y) * x0.w;
+    acc = acc + lo_bf(w.z) * x1.x;
+    acc = acc + hi_bf(w.z) * x1.y;
+    acc = acc + lo_bf(w.w) * x1.z;
+    acc = acc + hi_bf(w.w) * x1.w;
+    return acc;
+}
+__device__ __forceinline__ float chain_group(float acc, uint4 w, uint32_t xa, float) {
+    const float4 x0 = lds128f(xa);
+    acc = acc + __uint_as_float(w.x) * x0.x;
+    acc = acc + __uint_as_float(w.y) * x0.y;
+    acc = acc + __uint_as_float(w.z) * x0.z;
+    acc = acc + __uint_as_float(w.w) * x0.w;
+    return acc;
+}
+__device__ __forceinline__ float group_elem(uint4 w, int i, uint16_t) {
+    const uint32_t v = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
+    return (i & 1) ? hi_bf(v) : lo_bf(v);
+}
+__device__ __forceinline__ float group_elem(uint4 w, int i, float) {
+    return __uint_as_float(i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w);
+}
+
+// Row tile layout (smoe_dev.h): 32 rows, columns in groups of G = 16 B / sizeof(WT);
+// element (row lane, col c) at (c / G) * 32 * G + lane * G + c % G.  A chunk of
+// CC columns (CC % G == 0) is CC * 32 contiguous elements = one bulk copy; each
+// lane reads its G columns with one conflict-free ld.shared.v4.
 template <typename WT, int S, int CC>
 struct WarpPipe {
+    static constexpr int G = 16 / static_cast<int>(sizeof(WT));
     static constexpr int kChunkElems = CC * 32;
-    static constexpr int kBytes = S * kChunkElems * static_cast<int>(sizeof(WT)) + S * 8;
+    static constexpr int kChunkBytes = kChunkElems * static_cast<int>(sizeof(WT));
+    static constexpr int kBytes = S * kChunkBytes + S * 8;
+    static_assert(CC % G == 0, "chunk must hold whole column groups");
     uint64_t* full;  // [S]
     WT* buf;         // [S][CC*32]
+    uint32_t sbuf;   // shared-window address of buf
     int ctr;         // chunks consumed so far (phase tracking)
+    int primed;      // chunks already issued for the next run()
 
     __device__ void init(unsigned char* smem) {  // call with the owning warp; then syncwarp
         buf = reinterpret_cast<WT*>(smem);
-        full = reinterpret_cast<uint64_t*>(smem + S * kChunkElems * sizeof(WT));
+        sbuf = smem_u32(smem);
+        full = reinterpret_cast<uint64_t*>(smem + S * kChunkBytes);
         ctr = 0;
+        primed = 0;
         if ((threadIdx.x & 31) == 0) {
             for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
             fence_mbar_init();
@@ -135,31 +252,52 @@ struct WarpPipe {
     __device__ void issue(const WT* tile, int cols, int n, int g) {
         const int st = g % S;
         const int c0 = n * CC;
-        const int cn = min(CC, cols - c0);
+        const int cn = min(CC, round_up(cols, G) - c0);
         const uint32_t bytes = static_cast<uint32_t>(cn) * 32u * sizeof(WT);
         mbar_expect_tx(&full[st], bytes);
         bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
     }
 
-    // Returns this lane's dot product.  xs: shared-memory f32 vector [cols].
+    // Issue the first chunks of `tile` before the input vector exists (weights
+    // are independent of the activations), so the first wait finds data.
+    __device__ void prime(const WT* tile, int cols) {
+        const int nch = (cols + CC - 1) / CC;
+        if ((threadIdx.x & 31) == 0)
+            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        primed = 1;
+    }
+
+    // Returns this lane's dot product over the first `cols` columns, in
+    // column order.  xs: shared-memory f32 vector (16-byte aligned).
     __device__ float run(const WT* tile, int cols, const float* xs) {
         const int lane = threadIdx.x & 31;
         const int nch = (cols + CC - 1) / CC;
-        if (lane == 0)
+        if (lane == 0 && !primed)
             for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        primed = 0;
+        const uint32_t xbase = smem_u32(xs);
         float acc = 0.0f;
         for (int n = 0; n < nch; ++n) {
             const int g = ctr + n;
             const int st = g % S;
             mbar_wait(&full[st], static_cast<uint32_t>((g / S) & 1));
-            const WT* b = buf + st * kChunkElems + lane;
-            const float* xc = xs + n * CC;
+            const uint32_t wb = sbuf + st * kChunkBytes + lane * 16;
+            const uint32_t xb = xbase + n * CC * 4;
             const int cn = min(CC, cols - n * CC);
-            if (cn == CC) {
-#pragma unroll 16
-                for (int c = 0; c < CC; ++c) acc = acc + to_f(b[c * 32]) * xc[c];
+            const int ng = cn / G;
+            if (ng == CC / G) {
+#pragma unroll 4
+                for (int q = 0; q < CC / G; ++q)
+                    acc = chain_group(acc, lds128(wb + q * 512), xb + q * G * 4, WT{});
             } else {
-                for (int c = 0; c < cn; ++c) acc = acc + to_f(b[c * 32]) * xc[c];
+                for (int q = 0; q < ng; ++q)
+                    acc = chain_group(acc, lds128(wb + q * 512), xb + q * G * 4, WT{});
+                const int tail = cn - ng * G;
+                if (tail) {
+                    const uint4 w = lds128(wb + ng * 512);
+                    const float* xt = xs + n * CC + ng * G;
+                    for (int i = 0; i < tail; ++i) acc = acc + group_elem(w, i, WT{}) * xt[i];
+                }
             }
             __syncwarp();
             if (lane == 0 && n + S < nch) issue(tile, cols, n + S, g + S);
@@ -331,10 +469,10 @@ __global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_
             r = d / C;
             c = d % C;
         } else {
-            const long long lane = d & 31;
-            const long long rest = d >> 5;
-            const long long rb = rest / tile_cols;
-            c = rest % tile_cols;
+            const long long tile = static_cast<long long>(tile_cols) * 32;
+            const long long rb = d / tile, rem = d % tile;
+            const long long lane = (rem % 256) / 8;
+            c = (rem / 256) * 8 + (rem % 8);
             if (c >= C) continue;
             const long long vr = rb * 32 + lane;
             if (layout == kRowTiled) {
@@ -353,6 +491,8 @@ __global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_
 // ------------------------------------------------------------- attention --
 
 __global__ void k_embed(DevModel m, DevState st, const int* token_src) {
+    pdl_trigger();
+    pdl_wait();
     const int tok = *token_src;
     if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m.Hp; j += gridDim.x * blockDim.x)
@@ -363,14 +503,24 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src) {
 // and k (model.cpp:309-321, cos/sin precomputed on the host with libm), k and v
 // appended to the layer's KV cache at `pos`.  One warp per 32-row tile.
 __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) {
-    double* red = reinterpret_cast<double*>(g_smem);
-    float* xs = reinterpret_cast<float*>(g_smem + 64);
-    unsigned char* pipe_mem = align128(g_smem + 64 + m.H * 4);
-    PipeB pipe;
-    pipe.init(pipe_mem);
-    block_rms_norm(st.x, m.attn_gain + static_cast<long long>(layer) * m.H, m.H, m.eps, xs, red);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    double* red = reinterpret_cast<double*>(g_smem + 64);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    float* gs = xs + round_up(m.H, 32);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
+    pdl_trigger();
     const int rb = blockIdx.x;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * m.H * 32;
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    pipe.prime(tile, m.H);
+    Stager sg;
+    sg.init(bar);
+    pdl_wait();
+    sg.add(xs, st.x, m.H * 4);
+    sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);
+    sg.wait();
+    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
     float acc = pipe.run(tile, m.H, xs);
     const int lane = threadIdx.x & 31;
     const int R = rb * 32 + lane;
@@ -394,30 +544,83 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
         st.vc[kv + R - 2 * D] = acc;
 }
 
-// scores / softmax / context (model.cpp:335-351), one CTA.
-__global__ void __launch_bounds__(256) k_attn(DevModel m, DevState st, double* e, int layer) {
-    float* qs = reinterpret_cast<float*>(g_smem);           // [D]
-    float* red = qs + kMaxD;                                  // [32]
-    double* dred = reinterpret_cast<double*>(red + 32);       // [32]
+// scores / softmax / context (model.cpp:335-351), one CTA of kAttnThreads.
+// Keys, then values, stream through a 2-deep ring of kAttnChunk-position
+// tiles (cp.async.bulk); thread j owns position j's dot product (sequential
+// over head dims), thread i owns context dim i (sequential over positions).
+constexpr int kAttnChunk = 64;
+constexpr int kAttnThreads = 256;
+constexpr int kAttnSmemPositions = 4096;
+
+__global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, double* scratch,
+                                                        int layer) {
     const int D = m.D;
-    const int n = *st.pos + 1;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(g_smem);              // [3]
+    float* red = reinterpret_cast<float*>(g_smem + 32);                // [32]
+    float* qs = reinterpret_cast<float*>(g_smem + 256);                // [kMaxD]
+    float* tiles = qs + kMaxD;                                         // [2][chunk][D]
+    double* e = reinterpret_cast<double*>(tiles + 2 * kAttnChunk * D);  // [n] (smem when it fits)
+    float* sc = reinterpret_cast<float*>(e + m.cap);
+    if (m.cap > kAttnSmemPositions) {  // long contexts: f64/f32 scratch in global
+        e = scratch;
+        sc = reinterpret_cast<float*>(scratch + m.cap);
+    }
     const long long base = static_cast<long long>(layer) * m.cap * D;
-    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = st.q[i];
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
-    float* sc = reinterpret_cast<float*>(e + m.cap);  // scratch: doubles [cap] then floats [cap]
+    pdl_wait();
+    Stager sg;
+    sg.bar = &bars[2];
+    sg.phase = 0;
+    sg.add(qs, st.q, D * 4);
+    sg.wait();
+    const int n = *st.pos + 1;
+    const int nch = (n + kAttnChunk - 1) / kAttnChunk;
+    auto issue = [&](const float* src, int c) {  // thread 0
+        const int p0 = c * kAttnChunk;
+        const int pn = min(kAttnChunk, n - p0);
+        const uint32_t bytes = static_cast<uint32_t>(pn) * D * 4;
+        mbar_expect_tx(&bars[c & 1], bytes);
+        bulk_g2s(tiles + (c & 1) * kAttnChunk * D, src + base + static_cast<long long>(p0) * D, bytes,
+                 &bars[c & 1]);
+    };
+    uint32_t ph[2] = {0, 0};
+    // pass 1: scores
+    if (threadIdx.x == 0) {
+        issue(st.kc, 0);
+        if (nch > 1) issue(st.kc, 1);
+    }
     float lmax = -INFINITY;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const float* kj = st.kc + base + static_cast<long long>(j) * D;
-        float acc = 0.0f;
-        for (int i = 0; i < D; ++i) acc = acc + qs[i] * kj[i];
-        const float v = acc * m.inv_sqrt_d;
-        sc[j] = v;
-        lmax = fmaxf(lmax, v);
+    for (int c = 0; c < nch; ++c) {
+        mbar_wait(&bars[c & 1], ph[c & 1]);
+        ph[c & 1] ^= 1;
+        const float* t = tiles + (c & 1) * kAttnChunk * D;
+        const int p0 = c * kAttnChunk;
+        const int pn = min(kAttnChunk, n - p0);
+        for (int j = threadIdx.x; j < pn; j += blockDim.x) {
+            const float* kj = t + j * D;
+            float acc = 0.0f;
+            for (int i = 0; i < D; ++i) acc = acc + qs[i] * kj[i];
+            const float v = acc * m.inv_sqrt_d;
+            sc[p0 + j] = v;
+            lmax = fmaxf(lmax, v);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && c + 2 < nch) issue(st.kc, c + 2);
     }
     const float mx = block_max_f(lmax, red);
     for (int j = threadIdx.x; j < n; j += blockDim.x)
         e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
     __syncthreads();
+    // pass 2 prefetch overlaps the partition sum
+    if (threadIdx.x == 0) {
+        issue(st.vc, 0);
+        if (nch > 1) issue(st.vc, 1);
+    }
     __shared__ double zs;
     if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
         double z = 0.0;
@@ -428,27 +631,43 @@ __global__ void __launch_bounds__(256) k_attn(DevModel m, DevState st, double* e
     const double z = zs;
     for (int j = threadIdx.x; j < n; j += blockDim.x) sc[j] = static_cast<float>(e[j] / z);
     __syncthreads();
-    for (int i = threadIdx.x; i < D; i += blockDim.x) {
-        float acc = 0.0f;
-        for (int j = 0; j < n; ++j) acc = acc + sc[j] * st.vc[base + static_cast<long long>(j) * D + i];
-        st.ctx[i] = acc;
+    float acc = 0.0f;
+    const int i = threadIdx.x;
+    for (int c = 0; c < nch; ++c) {
+        mbar_wait(&bars[c & 1], ph[c & 1]);
+        ph[c & 1] ^= 1;
+        const float* t = tiles + (c & 1) * kAttnChunk * D;
+        const int p0 = c * kAttnChunk;
+        const int pn = min(kAttnChunk, n - p0);
+        if (i < D)
+            for (int j = 0; j < pn; ++j) acc = acc + sc[p0 + j] * t[j * D + i];
+        __syncthreads();
+        if (threadIdx.x == 0 && c + 2 < nch) issue(st.vc, c + 2);
     }
-    (void)dred;
+    if (i < D) st.ctx[i] = acc;
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
 __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
-    float* xs = reinterpret_cast<float*>(g_smem);
-    unsigned char* pipe_mem = align128(g_smem + kMaxD * 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    float* xr = xs + kMaxD;  // residual rows of this tile
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xr + 32));
+    pdl_trigger();
     PipeB pipe;
     pipe.init(pipe_mem);
-    for (int i = threadIdx.x; i < m.D; i += blockDim.x) xs[i] = st.ctx[i];
-    __syncwarp();
+    pipe.prime(m.wo + layer * m.wo_stride + static_cast<long long>(blockIdx.x) * m.D * 32, m.D);
+    Stager sg;
+    sg.init(bar);
+    pdl_wait();
+    sg.add(xs, st.ctx, m.D * 4);
+    sg.add(xr, st.x + blockIdx.x * 32, 32 * 4);
+    sg.wait();
     const int rb = blockIdx.x;
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
     const float acc = pipe.run(tile, m.D, xs);
     const int j = rb * 32 + (threadIdx.x & 31);
-    if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = st.x[j] + acc;
+    if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = xr[threadIdx.x & 31] + acc;
 }
 
 // ---------------------------------------------------------------- router --
@@ -459,53 +678,77 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
 // The last CTA turns logits into decisions, fixes the executed decision and
 // posts the copy requests.
 
+// layer_default (speculation.cpp:104-117) + quasi_hidden (speculation.cpp:119-121)
+// over the decision executed at `layer` (pred_l when this launch also fixes
+// exec).  r, the K default-vector rows and gain_{l+1} are staged in smem.
 __device__ void compute_quasi(const DevModel& m, const DevState& st, int layer, int exec_from,
-                              float* qs, float* tmp, double* red) {
-    // layer_default (speculation.cpp:104-117) + quasi_hidden (speculation.cpp:119-121)
-    // over the decision executed at `layer` (pred_l when this launch also fixes exec).
-    const int H = m.H, K = m.K;
-    const int* ids = (exec_from == 1 ? st.id_pred : st.id_exec) + layer * K;
-    const float* gs = (exec_from == 1 ? st.g_pred : st.g_exec) + layer * K;
-    const float* r = st.r + static_cast<long long>(layer) * m.Hp;
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
-        float d = 0.0f;
-        for (int i = 0; i < K; ++i)
-            d = d + gs[i] * m.dv[(static_cast<long long>(layer) * m.E + ids[i]) * H + j];
-        tmp[j] = r[j] + d;
+                              float* qs, float* rs, float* gs, float* dvs, double* red,
+                              Stager& sg) {
+    const int H = m.H, K = m.K, Hr = round_up(H, 32);
+    __shared__ int s_ids[kMaxK];
+    __shared__ float s_g[kMaxK];
+    if (threadIdx.x < K) {
+        s_ids[threadIdx.x] = (exec_from == 1 ? st.id_pred : st.id_exec)[layer * K + threadIdx.x];
+        s_g[threadIdx.x] = (exec_from == 1 ? st.g_pred : st.g_exec)[layer * K + threadIdx.x];
     }
     __syncthreads();
-    block_rms_norm(tmp, m.moe_gain + static_cast<long long>(layer + 1) * H, H, m.eps, qs, red);
+    sg.add(rs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
+    sg.add(gs, m.moe_gain + static_cast<long long>(layer + 1) * H, H * 4);
+    for (int i = 0; i < K; ++i)
+        sg.add(dvs + i * Hr, m.dv + (static_cast<long long>(layer) * m.E + s_ids[i]) * H, H * 4);
+    sg.wait();
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        float d = 0.0f;
+        for (int i = 0; i < K; ++i) d = d + s_g[i] * dvs[i * Hr + j];
+        rs[j] = rs[j] + d;
+    }
+    __syncthreads();
+    block_rms_norm(rs, gs, H, m.eps, qs, red);
 }
 
 __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl ctl,
                                                RouterLaunch rl, DevState sh, int has_shadow) {
-    const int H = m.H, E = m.E, K = m.K, l = rl.layer;
-    double* red = reinterpret_cast<double*>(g_smem);
-    float* xs = reinterpret_cast<float*>(g_smem + 64);
-    float* tmp = xs + H;
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(tmp + H));
+    const int H = m.H, E = m.E, K = m.K, l = rl.layer, Hr = round_up(H, 32);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    double* red = reinterpret_cast<double*>(g_smem + 64);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    float* rs = xs + Hr;
+    float* gs = rs + Hr;
+    float* dvs = gs + Hr;  // [K][Hr] (quasi CTAs only)
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(dvs + K * Hr));
     const int nT = rl.do_true ? m.Ep / 32 : 0;
     const bool gemv_pred = rl.pred_kind == kBaselineS || rl.pred_kind == kRouterPF;
     const int nP = gemv_pred ? m.Ep / 32 : 0;
     const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
     const int b = blockIdx.x;
-    const float* r = st.r + static_cast<long long>(l) * m.Hp;
+    pdl_trigger();
+    PipeB pipe;
+    const uint16_t* tile = nullptr;
+    if (b < nT + nP) {
+        const bool is_true = b < nT;
+        const int rb = is_true ? b : b - nT;
+        tile = m.gate + (is_true ? l : l + 1) * m.gate_stride + static_cast<long long>(rb) * H * 32;
+        pipe.init(pipe_mem);
+        pipe.prime(tile, H);
+    }
+    Stager sg;
+    sg.init(bar);
+    pdl_wait();
     if (b < nT || (b < nT + nP && rl.pred_kind == kBaselineS)) {
-        block_rms_norm(r, m.moe_gain + static_cast<long long>(l) * H, H, m.eps, xs, red);
+        sg.add(rs, st.r + static_cast<long long>(l) * m.Hp, H * 4);
+        sg.add(gs, m.moe_gain + static_cast<long long>(l) * H, H * 4);
+        sg.wait();
+        block_rms_norm(rs, gs, H, m.eps, xs, red);
         if (b == 0 && rl.do_true)
             for (int j = threadIdx.x; j < H; j += blockDim.x) st.s[static_cast<long long>(l) * m.Hp + j] = xs[j];
     } else if (b < nT + nP + nQ) {
-        compute_quasi(m, st, l, rl.exec_from, xs, tmp, red);
+        compute_quasi(m, st, l, rl.exec_from, xs, rs, gs, dvs, red, sg);
         if (b == nT)
             for (int j = threadIdx.x; j < H; j += blockDim.x) st.quasi[j] = xs[j];
     }
     if (b < nT + nP) {
-        PipeB pipe;
-        pipe.init(pipe_mem);
         const bool is_true = b < nT;
         const int rb = is_true ? b : b - nT;
-        const int gl = is_true ? l : l + 1;
-        const uint16_t* tile = m.gate + gl * m.gate_stride + static_cast<long long>(rb) * H * 32;
         const float acc = pipe.run(tile, H, xs);
         const int e = rb * 32 + (threadIdx.x & 31);
         if (e < E) {
@@ -585,12 +828,18 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
         in = st.est_xn;
         tiles = m.est_head;
     }
-    for (int i = threadIdx.x; i < cols; i += blockDim.x) xs[i] = in[i];
-    __syncwarp();
-    unsigned char* pipe_mem = align128(g_smem + cols * 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + round_up(cols, 32) * 4);
+    unsigned char* pipe_mem = align128(g_smem + round_up(cols, 32) * 4 + 64);
+    pdl_trigger();
+    const int rb = blockIdx.x;
     PipeF pipe;
     pipe.init(pipe_mem);
-    const int rb = blockIdx.x;
+    pipe.prime(tiles + static_cast<long long>(rb) * cols * 32, cols);
+    Stager sg;
+    sg.init(bar);
+    pdl_wait();
+    sg.add(xs, in, cols * 4);
+    sg.wait();
     const float acc = pipe.run(tiles + static_cast<long long>(rb) * cols * 32, cols, xs);
     const int row = rb * 32 + (threadIdx.x & 31);
     if (stage == 0) {
@@ -656,22 +905,26 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
 }
 
 __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer) {
+    pdl_trigger();
+    pdl_wait();
     wait_ready(ctl, layer);
     if (*(volatile int*)ctl.error) return;
     const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
-    float* xs = reinterpret_cast<float*>(g_smem);
-    unsigned char* pipe_mem = align128(g_smem + H * 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + round_up(H, 32)));
     PipeB pipe;
     pipe.init(pipe_mem);
-    const float* s = st.s + static_cast<long long>(layer) * m.Hp;
-    for (int j = threadIdx.x; j < H; j += blockDim.x) xs[j] = s[j];
+    Stager sg;
+    sg.init(bar);
+    sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
     const int e = st.id_exec[layer * m.K + i];
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     if (slot < 0) {
         if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
         return;
     }
-    __syncwarp();
+    sg.wait();
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
     const float acc = pipe.run(tile, H, xs);
@@ -688,15 +941,22 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
 // x = r + m (model.cpp:386).
 __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st, DevCtl ctl,
                                                          int layer) {
+    pdl_trigger();
+    pdl_wait();
     if (*(volatile int*)ctl.error) return;
     const int K = m.K, Hmp = m.Hmp, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* hs = reinterpret_cast<float*>(g_smem);          // [K][Hmp]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    float* hs = reinterpret_cast<float*>(g_smem + 128);    // [K][Hmp]
     float* ys = hs + K * Hmp;                                // [K][32]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(ys + K * 32));
+    float* rr = ys + K * 32;                                 // [32] residual rows
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(rr + 32));
     PipeD pipe;
     pipe.init(pipe_mem + w * PipeD::kBytes);
-    for (int t = threadIdx.x; t < K * Hmp; t += blockDim.x) hs[t] = st.h[t];
-    __syncthreads();
+    Stager sg;
+    sg.init(bar);
+    sg.add(hs, st.h, K * Hmp * 4);
+    sg.add(rr, st.r + static_cast<long long>(layer) * m.Hp + blockIdx.x * 32, 32 * 4);
+    sg.wait();
     const int e = st.id_exec[layer * K + w];
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     const int rb = blockIdx.x;
@@ -715,7 +975,7 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
         float out = 0.0f;
         for (int i = 0; i < K; ++i) out += st.g_exec[layer * K + i] * ys[i * 32 + lane];
         st.m[static_cast<long long>(layer) * m.Hp + j] = out;
-        st.x[j] = st.r[static_cast<long long>(layer) * m.Hp + j] + out;
+        st.x[j] = rr[lane] + out;
     }
 }
 
@@ -724,21 +984,46 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
 // greedy argmax, first maximum (model.cpp:391-396).
 __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ctl,
                                               int record_token) {
-    double* red = reinterpret_cast<double*>(g_smem);
-    float* xs = reinterpret_cast<float*>(g_smem + 64);
-    unsigned char* pipe_mem = align128(g_smem + 64 + m.H * 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    double* red = reinterpret_cast<double*>(g_smem + 64);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    float* gs = xs + round_up(m.H, 32);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
+    pdl_trigger();
     PipeB pipe;
     pipe.init(pipe_mem);
-    block_rms_norm(st.x, m.final_gain, m.H, m.eps, xs, red);
+    pipe.prime(m.unemb + static_cast<long long>(blockIdx.x) * m.H * 32, m.H);
+    Stager sg;
+    sg.init(bar);
+    pdl_wait();
+    sg.add(xs, st.x, m.H * 4);
+    sg.add(gs, m.final_gain, m.H * 4);
+    sg.wait();
+    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
     const int rb = blockIdx.x;
     const float acc = pipe.run(m.unemb + static_cast<long long>(rb) * m.H * 32, m.H, xs);
     const int v = rb * 32 + (threadIdx.x & 31);
     if (v < m.V) st.logits[v] = acc;
     if (!last_cta(st.counters + 2, gridDim.x)) return;
+    // argmax_token (model.cpp:391-396): first maximum, warp-parallel
+    int best = -1;
+    float bv = -INFINITY;
+    for (int i = threadIdx.x; i < m.V; i += 32) {
+        const float v = __ldcg(st.logits + i);
+        if (best < 0 || v > bv) {
+            bv = v;
+            best = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, best, o);
+        if (oi >= 0 && (best < 0 || ov > bv || (ov == bv && oi < best))) {
+            bv = ov;
+            best = oi;
+        }
+    }
     if (threadIdx.x == 0) {
-        int best = 0;
-        for (int i = 1; i < m.V; ++i)
-            if (st.logits[i] > st.logits[best]) best = i;
         *st.token = best;
         *st.pos = *st.pos + 1;
         if (record_token) {
@@ -752,6 +1037,8 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
 // ----------------------------------------------------------- calibration ----
 
 __global__ void k_dv_accum(DevModel m, DevState st, double* sums, long long* counts, int layer) {
+    pdl_trigger();
+    pdl_wait();
     const int K = m.K, H = m.H;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * H; t += gridDim.x * blockDim.x) {
         const int i = t / H, j = t % H;
@@ -774,6 +1061,8 @@ __global__ void k_dv_freeze(const double* sums, const long long* counts, float* 
 // ----------------------------------------------------------------- trace ----
 
 __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
+    pdl_trigger();
+    pdl_wait();
     const int step = *tr.step;
     if (step >= tr.cap) return;
     const int L = m.L, H = m.H, E = m.E, K = m.K, V = m.V, Hp = m.Hp;
@@ -813,6 +1102,8 @@ __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
 // Per-layer raw outputs are overwritten by the next layer, so the full trace
 // grabs them right after each layer's down projection.
 __global__ void k_trace_y(DevModel m, DevState st, TraceDev tr, int layer) {
+    pdl_trigger();
+    pdl_wait();
     const int step = *tr.step;
     if (step >= tr.cap) return;
     const int K = m.K, H = m.H, L = m.L;
@@ -823,10 +1114,41 @@ __global__ void k_trace_y(DevModel m, DevState st, TraceDev tr, int layer) {
 }
 
 __global__ void k_trace_bump(TraceDev tr) {
+    pdl_wait();
     if (*tr.step < tr.cap) *tr.step = *tr.step + 1;
 }
 
 // ============================================================== launchers ==
+
+static long long g_launches = 0;
+
+// Every decode-path kernel is launched with programmatic stream
+// serialization (PDL); captured into the step graph as programmatic edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+#define PDL(k, grid, block, smem, s, ...)                                   \
+    do {                                                                    \
+        cudaError_t e_ = launch_pdl(k, dim3(grid), dim3(block), smem, s, __VA_ARGS__); \
+        if (e_ != cudaSuccess) return e_;                                   \
+    } while (0)
+long long launch_counter() { return g_launches; }
+static inline cudaError_t counted(int n = 1) {
+    g_launches += n;
+    return cudaGetLastError();
+}
 
 namespace {
 inline int gen_blocks(long long n) {
@@ -834,24 +1156,28 @@ inline int gen_blocks(long long n) {
     if (b > 148LL * 64) b = 148LL * 64;
     return static_cast<int>(b < 1 ? 1 : b);
 }
-size_t qkv_smem(const DevModel& m) { return 64 + m.H * 4 + 128 + PipeB::kBytes; }
-size_t wo_smem(const DevModel&) { return kMaxD * 4 + 128 + PipeB::kBytes; }
+size_t vec_bytes(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
+size_t qkv_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t wo_smem(const DevModel&) { return 128 + kMaxD * 4 + 32 * 4 + 128 + PipeB::kBytes; }
 size_t router_smem(const DevModel& m) {
-    size_t a = 64 + 2 * m.H * 4 + 128 + PipeB::kBytes;
-    size_t b = 64 + 2 * m.H * 4 + 128 + kMaxE * 12;
-    return a > b ? a : b;
+    const size_t head = 128 + (3 + static_cast<size_t>(m.K)) * vec_bytes(m.H) + 128;
+    return head + (PipeB::kBytes > kMaxE * 12 ? PipeB::kBytes : kMaxE * 12);
 }
 size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
-    cols = cols > kMaxE ? cols : kMaxE;
-    return static_cast<size_t>(cols) * 4 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
+    return vec_bytes(cols) + 64 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
 }
-size_t gu_smem(const DevModel& m) { return m.H * 4 + 128 + PipeB::kBytes; }
+size_t gu_smem(const DevModel& m) { return 128 + vec_bytes(m.H) + 128 + PipeB::kBytes; }
 size_t down_smem(const DevModel& m) {
-    return static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 128 +
+    return 128 + static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 32 * 4 + 128 +
            static_cast<size_t>(m.K) * PipeD::kBytes;
 }
-size_t final_smem(const DevModel& m) { return 64 + m.H * 4 + 128 + PipeB::kBytes; }
+size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t attn_smem(const DevModel& m) {
+    size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * m.D * 4;
+    if (m.cap <= kAttnSmemPositions) b += static_cast<size_t>(m.cap) * 12;
+    return b;
+}
 
 cudaError_t set_smem(const void* fn, size_t bytes) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -861,7 +1187,7 @@ cudaError_t set_smem(const void* fn, size_t bytes) {
 
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m), est_smem(m), gu_smem(m), down_smem(m),
-                  final_smem(m)};
+                  final_smem(m), attn_smem(m)};
     size_t mx = 0;
     for (size_t x : v) mx = x > mx ? x : mx;
     return static_cast<int>(mx);
@@ -880,13 +1206,13 @@ cudaError_t launch_gen_bf16(uint64_t seed, float stddev, int R, int C, int tile_
     }
     k_gen_bf16<<<gen_blocks(total), 256, 0, s>>>(seed, static_cast<double>(stddev), R, C,
                                                   tile_cols, layout, which, row_off, total, out);
-    return cudaGetLastError();
+    return counted(1);
 }
 
 cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
                          cudaStream_t s) {
-    k_embed<<<(m.Hp + 255) / 256, 256, 0, s>>>(m, st, token_src);
-    return cudaGetLastError();
+    PDL(k_embed, (m.Hp + 255) / 256, 256, 0, s, m, st, token_src);
+    return counted(1);
 }
 
 // Loads every kernel up front.  With CUDA lazy loading, the first launch of
@@ -909,23 +1235,24 @@ cudaError_t preload_kernels() {
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_final};
     for (const void* f : big)
         if ((e = set_smem(f, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
 cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
-    k_qkv<<<m.QKVp / 32, 32, qkv_smem(m), s>>>(m, st, layer);
-    return cudaGetLastError();
+    PDL(k_qkv, m.QKVp / 32, 32, qkv_smem(m), s, m, st, layer);
+    return counted(1);
 }
 
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
-    k_attn<<<1, 256, kMaxD * 4 + 32 * 4 + 32 * 8, s>>>(m, st, scratch, layer);
-    return cudaGetLastError();
+    PDL(k_attn, 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
+    return counted(1);
 }
 
 cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
-    k_wo<<<m.Hp / 32, 32, wo_smem(m), s>>>(m, st, layer);
-    return cudaGetLastError();
+    PDL(k_wo, m.Hp / 32, 32, wo_smem(m), s, m, st, layer);
+    return counted(1);
 }
 
 cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& ctl,
@@ -937,60 +1264,70 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
     int grid = nT + nP + nQ;
     if (grid < 1) grid = 1;
     DevState sh = shadow ? *shadow : st;
-    k_router<<<grid, 32, router_smem(m), s>>>(m, st, ctl, rl, sh, shadow ? 1 : 0);
-    return cudaGetLastError();
+    PDL(k_router, grid, 32, router_smem(m), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
+    return counted(1);
 }
 
 cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                              int post_pred, int step_tag, cudaStream_t s) {
     const size_t sm = est_smem(m);
-    k_est_stage<<<round_up(m.est_dm, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 0, 0, step_tag);
-    k_est_stage<<<round_up(m.est_mlp, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 1, 0, step_tag);
-    k_est_stage<<<round_up(m.est_dm, 32) / 32, 32, sm, s>>>(m, st, ctl, layer, 2, 0, step_tag);
-    k_est_stage<<<m.Ep / 32, 32, sm, s>>>(m, st, ctl, layer, 3, post_pred, step_tag);
-    return cudaGetLastError();
+    PDL(k_est_stage, round_up(m.est_dm, 32) / 32, 32, sm, s, m, st, ctl, layer, 0, 0, step_tag);
+    PDL(k_est_stage, round_up(m.est_mlp, 32) / 32, 32, sm, s, m, st, ctl, layer, 1, 0, step_tag);
+    PDL(k_est_stage, round_up(m.est_dm, 32) / 32, 32, sm, s, m, st, ctl, layer, 2, 0, step_tag);
+    PDL(k_est_stage, m.Ep / 32, 32, sm, s, m, st, ctl, layer, 3, post_pred, step_tag);
+    return counted(4);
 }
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s) {
-    k_ffn_gu<<<dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s>>>(m, st, ctl, layer);
-    k_ffn_down<<<m.Hp / 32, 32 * m.K, down_smem(m), s>>>(m, st, ctl, layer);
-    return cudaGetLastError();
+    PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer);
+    PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer);
+    return counted(2);
+}
+
+cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                            int part, cudaStream_t s) {
+    if (part == 0)
+        PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer);
+    else
+        PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer);
+    return counted(1);
 }
 
 cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,
                          int record_token, cudaStream_t s) {
-    k_final<<<m.Vp / 32, 32, final_smem(m), s>>>(m, st, ctl, record_token);
-    return cudaGetLastError();
+    PDL(k_final, m.Vp / 32, 32, final_smem(m), s, m, st, ctl, record_token);
+    return counted(1);
 }
 
 cudaError_t launch_dv_accum(const DevModel& m, const DevState& st, double* sums,
                             long long* counts, int layer, cudaStream_t s) {
-    k_dv_accum<<<(m.K * m.H + 255) / 256, 256, 0, s>>>(m, st, sums, counts, layer);
-    return cudaGetLastError();
+    PDL(k_dv_accum, (m.K * m.H + 255) / 256, 256, 0, s, m, st, sums, counts, layer);
+    return counted(1);
 }
 
 cudaError_t launch_dv_freeze(const double* sums, const long long* counts, float* dv,
                              long long LE, int H, cudaStream_t s) {
     k_dv_freeze<<<gen_blocks(LE * H), 256, 0, s>>>(sums, counts, dv, LE, H);
-    return cudaGetLastError();
+    return counted(1);
 }
 
 cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
                          cudaStream_t s) {
     if (!tr.full) {
-        k_trace<<<1, 256, 0, s>>>(m, st, tr);
+        PDL(k_trace, 1, 256, 0, s, m, st, tr);
     } else {
-        k_trace<<<64, 256, 0, s>>>(m, st, tr);
-        k_trace_bump<<<1, 1, 0, s>>>(tr);
+        PDL(k_trace, 64, 256, 0, s, m, st, tr);
+        PDL(k_trace_bump, 1, 1, 0, s, tr);
+        g_launches += 1;
     }
-    return cudaGetLastError();
+    return counted(1);
 }
 
 cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
                            cudaStream_t s) {
-    k_trace_y<<<16, 256, 0, s>>>(m, st, tr, layer);
-    return cudaGetLastError();
+    PDL(k_trace_y, 16, 256, 0, s, m, st, tr, layer);
+    return counted(1);
 }
 
 }  // namespace smoe

@@ -41,6 +41,8 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
                              int layer, int post_pred, int step_tag, cudaStream_t s);
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s);
+cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                            int part, cudaStream_t s);
 cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,
                          int record_token, cudaStream_t s);
 
@@ -67,5 +69,7 @@ cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev
 
 int max_dynamic_smem_needed(const DevModel& m);
 cudaError_t preload_kernels();
+// Number of kernel launches enqueued by the launchers so far (host counter).
+long long launch_counter();
 
 }  // namespace smoe

@@ -30,7 +30,12 @@ constexpr int kMailboxRing = 1024;
 enum PredKind : int { kBaselineS = 0, kRouterPF = 1, kEstPF = 2, kHybrid = 3, kOracle = 4, kNone = -1 };
 enum Gating : int { kSoftmaxTopK = 0, kTopKSoftmax = 1 };
 
-inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+#ifdef __CUDACC__
+#define SMOE_HD __host__ __device__
+#else
+#define SMOE_HD
+#endif
+SMOE_HD inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // One mailbox entry (pinned, mapped host memory).  Device writes the body,
 // __threadfence_system(), then `seq` last; the host scheduler polls `seq`.

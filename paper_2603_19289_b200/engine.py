@@ -28,7 +28,8 @@ EXPORTS = [
     "smoe_set_cache_fraction", "smoe_reset", "smoe_prefill", "smoe_decode",
     "smoe_run_offloaded_decode", "smoe_step", "smoe_calibrate", "smoe_steps_done",
     "smoe_read_tokens", "smoe_read_trace", "smoe_token_ms", "smoe_counters", "smoe_copy_events",
-    "smoe_cache_slots",
+    "smoe_cache_slots", "smoe_debug_state", "smoe_clear_stats", "smoe_profile_kernels",
+    "smoe_measure_link", "smoe_kernels_per_step",
 ]
 
 
@@ -237,6 +238,25 @@ class Session:
                                       C.byref(req)))
         return {"hits": hits, "misses": misses, "h2d_bytes": b.value, "copy_ms": ms.value,
                 "requests": req.value}
+
+    def clear_stats(self):
+        _check(self.lib.smoe_clear_stats(self._h))
+
+    def profile_kernels(self, reps: int = 3) -> dict:
+        out = np.zeros(7, np.float64)
+        _check(self.lib.smoe_profile_kernels(self._h, reps, _p(out)))
+        names = ["qkv", "attn", "wo", "router", "ffn_gate_up", "ffn_down", "final"]
+        return dict(zip(names, out.tolist()))
+
+    def measure_link(self, n_copies: int = 64) -> float:
+        g = C.c_double()
+        _check(self.lib.smoe_measure_link(self._h, n_copies, C.byref(g)))
+        return g.value
+
+    def kernels_per_step(self, mode: str) -> int:
+        n = C.c_int32()
+        _check(self.lib.smoe_kernels_per_step(self._h, MODE[mode], C.byref(n)))
+        return n.value
 
     def copy_events(self, cap: int = 65536):
         arr = (CopyEvent * cap)()
