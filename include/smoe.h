@@ -127,6 +127,9 @@ int smoe_counters(smoe_session* s, int64_t* hits, int64_t* misses, int64_t* h2d_
 int smoe_copy_events(smoe_session* s, smoe_copy_event* out, int32_t cap, int32_t* n);
 /* Slots per layer actually allocated. */
 int smoe_cache_slots(smoe_session* s, int32_t* slots);
+/* Copies every expert into HBM (cache_fraction 1.0 only): the model is fully
+ * resident, decode posts no copy requests and never waits on the copy lane. */
+int smoe_preload_all(smoe_session* s);
 /* Clears cache hit/miss counters, copy records and step timings (state kept). */
 int smoe_clear_stats(smoe_session* s);
 /* Average device time (us) per launch of each per-layer kernel, CUDA events on

@@ -230,6 +230,10 @@ int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->debug_state(out, cap); });
 }
 
+int smoe_preload_all(smoe_session* s) {
+    return guard([&] { S(s)->preload_all(); });
+}
+
 int smoe_clear_stats(smoe_session* s) {
     return guard([&] { S(s)->clear_stats(); });
 }

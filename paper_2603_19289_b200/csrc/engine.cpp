@@ -508,6 +508,31 @@ void Session::alloc() {
     reset(0, 0);
 }
 
+void Session::preload_all() {
+    sync();
+    if (C_ != cfg_.E) throw std::invalid_argument("preload_all: needs cache_fraction 1.0");
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    const long long per = dm_.expert_elems;
+    std::vector<int> ids(cfg_.E);
+    for (int e = 0; e < cfg_.E; ++e) ids[e] = e;
+    for (int l = 0; l < cfg_.L; ++l) {
+        int h = 0, mi = 0;
+        auto copies = cache_->request(l, ids.data(), cfg_.E, &h, &mi);
+        for (auto& [slot, expert] : copies)
+            ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * per,
+                               store_->expert(static_cast<long long>(l) * cfg_.E + expert), per * 2,
+                               cudaMemcpyHostToDevice, s_copy_),
+               "preload");
+        ck(cudaMemcpyAsync(d_slot_of_ + static_cast<long long>(l) * cfg_.E, cache_->slot_row(l).data(),
+                           4ull * cfg_.E, cudaMemcpyHostToDevice, s_copy_),
+           "preload table");
+        ck(cudaStreamSynchronize(s_copy_), "preload");
+    }
+    cache_->clear_stats();
+    ctl_.resident = 1;
+    drop_graphs();
+}
+
 void Session::set_cache_fraction(float frac) {
     if (!(frac > 0.0f && frac <= 1.0f)) throw std::invalid_argument("cache_fraction must be in (0, 1]");
     sync();
@@ -523,6 +548,7 @@ void Session::set_cache_fraction(float frac) {
             break;
         }
     opts_.cache_fraction = frac;
+    ctl_.resident = 0;
     C_ = C;
     dm_.C = C;
     d_slots_ = static_cast<uint16_t*>(dalloc(2ull * cfg_.L * C_ * dm_.expert_elems));
@@ -587,6 +613,8 @@ void Session::init_weights_seeded() {
     ck(cudaStreamSynchronize(s), "init sync");
     cudaFree(stage);
     cache_->invalidate();
+    ctl_.resident = 0;
+    drop_graphs();
     ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
 }
 
@@ -670,6 +698,8 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
         }
         // invalidate a resident copy of this expert
         cache_->invalidate();
+        ctl_.resident = 0;
+        drop_graphs();
         ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
         return;
     }

@@ -130,6 +130,9 @@ public:
     void load_estimator(const EstCfg& c, const float* flat);
     void set_predictor(int kind, const int* hybrid_map);
     void set_cache_fraction(float frac);
+    // Copies every expert into HBM (needs cache_fraction 1.0): the whole model
+    // is resident, so no copy requests are posted and no waits happen.
+    void preload_all();
 
     // --- decode --------------------------------------------------------------
     void reset(int max_steps, int trace_full);

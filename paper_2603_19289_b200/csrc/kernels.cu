@@ -191,8 +191,13 @@ __device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w <<
 __device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 // One 16-byte group of a lane's consecutive columns, in column order.
-__device__ __forceinline__ float chain_group(float acc, uint4 w, uint32_t xa, uint16_t) {
-    const float4 x0 = lds128f(xa), x1 = lds128f(xa + 16);
+struct XG {  // the matching activations
+    float4 a, b;
+};
+__device__ __forceinline__ XG load_x(uint32_t xa, uint16_t) { return {lds128f(xa), lds128f(xa + 16)}; }
+__device__ __forceinline__ XG load_x(uint32_t xa, float) { return {lds128f(xa), make_float4(0, 0, 0, 0)}; }
+__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, uint16_t) {
+    const float4 x0 = x.a, x1 = x.b;
     acc = acc + lo_bf(w.x) * x0.x;
     acc = acc + hi_bf(w.x) * x0.y;
     acc = acc + lo_bf(w.y) * x0.z;
@@ -203,13 +208,31 @@ __device__ __forceinline__ float chain_group(float acc, uint4 w, uint32_t xa, ui
     acc = acc + hi_bf(w.w) * x1.w;
     return acc;
 }
-__device__ __forceinline__ float chain_group(float acc, uint4 w, uint32_t xa, float) {
-    const float4 x0 = lds128f(xa);
+__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, float) {
+    const float4 x0 = x.a;
     acc = acc + __uint_as_float(w.x) * x0.x;
     acc = acc + __uint_as_float(w.y) * x0.y;
     acc = acc + __uint_as_float(w.z) * x0.z;
     acc = acc + __uint_as_float(w.w) * x0.w;
     return acc;
+}
+// The rounded products w[c] * x[c] of one group (acc + p is then the
+// reference's `acc += w * x`: product rounded, then the add rounded).
+__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, uint16_t) {
+    p[0] = lo_bf(w.x) * x.a.x;
+    p[1] = hi_bf(w.x) * x.a.y;
+    p[2] = lo_bf(w.y) * x.a.z;
+    p[3] = hi_bf(w.y) * x.a.w;
+    p[4] = lo_bf(w.z) * x.b.x;
+    p[5] = hi_bf(w.z) * x.b.y;
+    p[6] = lo_bf(w.w) * x.b.z;
+    p[7] = hi_bf(w.w) * x.b.w;
+}
+__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, float) {
+    p[0] = __uint_as_float(w.x) * x.a.x;
+    p[1] = __uint_as_float(w.y) * x.a.y;
+    p[2] = __uint_as_float(w.z) * x.a.z;
+    p[3] = __uint_as_float(w.w) * x.a.w;
 }
 __device__ __forceinline__ float group_elem(uint4 w, int i, uint16_t) {
     const uint32_t v = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
@@ -286,12 +309,23 @@ struct WarpPipe {
             const int cn = min(CC, cols - n * CC);
             const int ng = cn / G;
             if (ng == CC / G) {
-#pragma unroll 4
-                for (int q = 0; q < CC / G; ++q)
-                    acc = chain_group(acc, lds128(wb + q * 512), xb + q * G * 4, WT{});
+                // software pipelined: the products of group q+1 (independent
+                // FMULs) are formed while group q's sequential FADD chain runs
+                float pc[G], pn[G];
+                products(lds128(wb), load_x(xb, WT{}), pc, WT{});
+#pragma unroll 2
+                for (int q = 0; q < CC / G; ++q) {
+                    if (q + 1 < CC / G)
+                        products(lds128(wb + (q + 1) * 512), load_x(xb + (q + 1) * G * 4, WT{}), pn,
+                                 WT{});
+#pragma unroll
+                    for (int i = 0; i < G; ++i) acc = acc + pc[i];
+#pragma unroll
+                    for (int i = 0; i < G; ++i) pc[i] = pn[i];
+                }
             } else {
                 for (int q = 0; q < ng; ++q)
-                    acc = chain_group(acc, lds128(wb + q * 512), xb + q * G * 4, WT{});
+                    acc = chain_group(acc, lds128(wb + q * 512), load_x(xb + q * G * 4, WT{}), WT{});
                 const int tail = cn - ng * G;
                 if (tail) {
                     const uint4 w = lds128(wb + ng * 512);
@@ -427,7 +461,6 @@ __device__ void post_request(const DevCtl& ctl, int layer, int step, const int* 
     for (int i = 0; i < k; ++i) e->ids[i] = ids[i];
     __threadfence_system();
     e->seq = seq;
-    __threadfence_system();
 }
 
 // ------------------------------------------------------------- weight init --
@@ -786,8 +819,9 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
                 st.g_exec[l * K + i] = st.g_pred[l * K + i];
             }
         }
-        if (rl.post_exec) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
-        if (rl.post_pred) post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+        if (rl.post_exec && !ctl.resident) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
+        if (rl.post_pred && !ctl.resident)
+            post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
     }
     if (rl.pred_kind == kOracle && has_shadow)
         for (int e = threadIdx.x; e < E; e += blockDim.x)
@@ -799,9 +833,46 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
 //  A: z = A.q + pos[l]   B: act = silu_f32(B.z)   C: h = z + C.act, LayerNorm
 //  head: logits = W_head.(gain*xhat + bias), decision, mailbox.
 
-// expf as glibc rounds it: f64 exp rounded to f32 (estimator.cpp:121 uses std::exp<float>).
-__device__ __forceinline__ float expf_ref(float x) {
-    return static_cast<float>(exp(static_cast<double>(x)));
+// expf as glibc computes it (sysdeps/ieee754/flt-32/e_expf.c, the table and
+// constants of __exp2f_data, verified against this image's libm.so.6): the
+// reference's estimator SiLU calls std::exp(float) (estimator.cpp:121), so the
+// GPU reproduces glibc's algorithm bit for bit instead of CUDA's expf.
+__constant__ unsigned long long kExp2fTab[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull};
+
+__device__ float expf_glibc(float x) {
+    const uint32_t ux = __float_as_uint(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    if (abstop >= 0x42b) {  // |x| >= 88 (top12(88.0f)) and specials
+        if (ux == 0xff800000u) return 0.0f;  // -inf
+        if (abstop >= 0x7f8) return x + x;   // inf / nan
+        if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);  // overflow
+        if (x < -0x1.9fe368p6f) return 0.0f;                        // underflow
+    }
+    const double InvLn2N = 0x1.71547652b82fep+5, Shift = 0x1.8p+52;
+    const double C0 = 0x1.c6af84b912394p-20, C1 = 0x1.ebfce50fac4f3p-13,
+                 C2 = 0x1.62e42ff0c52d6p-6;
+    const double xd = static_cast<double>(x);
+    const double z = __dmul_rn(InvLn2N, xd);
+    double kd = __dadd_rn(z, Shift);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd = __dsub_rn(kd, Shift);
+    const double r = __dsub_rn(z, kd);
+    const unsigned long long t = kExp2fTab[ki % 32] + (ki << 47);
+    const double s = __longlong_as_double(static_cast<long long>(t));
+    const double zz = __dadd_rn(__dmul_rn(C0, r), C1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __dadd_rn(__dmul_rn(C2, r), 1.0);
+    y = __dadd_rn(__dmul_rn(zz, r2), y);
+    y = __dmul_rn(y, s);
+    return static_cast<float>(y);
 }
 
 __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCtl ctl, int layer,
@@ -845,7 +916,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     if (stage == 0) {
         if (row < dm) st.est_z[row] = acc + m.est_pos[static_cast<long long>(layer) * dm + row];
     } else if (stage == 1) {
-        if (row < mlp) st.est_act[row] = acc / (1.0f + expf_ref(-acc));
+        if (row < mlp) st.est_act[row] = acc / (1.0f + expf_glibc(-acc));
     } else if (stage == 2) {
         if (row < dm) st.est_xn[row] = st.est_z[row] + acc;  // h (normalised below)
     } else {
@@ -878,7 +949,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);
     warp_decision(st.lg_pred + static_cast<long long>(layer + 1) * m.E, m.E, m.K, m.gating, sp,
                   se, st.id_pred + (layer + 1) * m.K, st.g_pred + (layer + 1) * m.K);
-    if (threadIdx.x == 0 && post_pred)
+    if (threadIdx.x == 0 && post_pred && !ctl.resident)
         post_request(ctl, layer + 1, step_tag, st.id_pred + (layer + 1) * m.K, m.K);
 }
 
@@ -889,6 +960,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
 // hold gate row r and up row r); h = silu(g) * u.
 
 __device__ void wait_ready(const DevCtl& ctl, int layer) {
+    if (ctl.resident) return;
     if (threadIdx.x == 0) {
         const int want = ctl.req_seq[layer];
         const long long t0 = clock64();

@@ -127,6 +127,7 @@ struct DevCtl {
     int* step;               // decode step counter
     int* tokens_out;         // [max_steps]
     long long spin_limit;    // clock64 cycles before declaring a deadlock
+    int resident;            // 1: every expert is resident (no requests, no waits)
 };
 
 }  // namespace smoe

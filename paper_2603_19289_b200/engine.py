@@ -29,7 +29,7 @@ EXPORTS = [
     "smoe_run_offloaded_decode", "smoe_step", "smoe_calibrate", "smoe_steps_done",
     "smoe_read_tokens", "smoe_read_trace", "smoe_token_ms", "smoe_counters", "smoe_copy_events",
     "smoe_cache_slots", "smoe_debug_state", "smoe_clear_stats", "smoe_profile_kernels",
-    "smoe_measure_link", "smoe_kernels_per_step",
+    "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all",
 ]
 
 
@@ -238,6 +238,9 @@ class Session:
                                       C.byref(req)))
         return {"hits": hits, "misses": misses, "h2d_bytes": b.value, "copy_ms": ms.value,
                 "requests": req.value}
+
+    def preload_all(self):
+        _check(self.lib.smoe_preload_all(self._h))
 
     def clear_stats(self):
         _check(self.lib.smoe_clear_stats(self._h))

@@ -54,4 +54,4 @@ def test_no_gpu_fails_loudly():
     from paper_2603_19289_b200 import ModelConfig, Session, SmoeError
     with pytest.raises(SmoeError):
         Session(ModelConfig(layers=2, experts=4, top_k=2, hidden=16, expert_hidden=8, vocab=8,
-                            head_dim=4))
+                            head_dim=8))
