@@ -160,18 +160,29 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     s.set_cache_fraction(args.cache_fraction)
     s.set_predictor(args.predictor)
     prompt = token_stream(P, c["vocab"], 3)
-    res = {}
-    for mode in ("on_demand", "prefetch"):
+    # teacher-forced decode inputs (random_token_stream seed 4): routing changes
+    # every token as with real text, so the 25 % cache really misses
+    forced = token_stream(args.warmup + args.steps, c["vocab"], 4)
+
+    def measure(mode: str, workload: str) -> dict:
         tpots, h2d, cms, hit, miss, recall = [], [], [], [], [], []
+        clk = None
         for run in range(args.runs):
             S = P + args.warmup + args.steps
             s.reset(S, False)
             s.prefill(prompt)
-            if args.warmup:
-                s.decode(mode, args.warmup)
-            s.clear_stats()
-            with ClockSampler(dev) as clk:
-                s.decode(mode, args.steps)
+            if workload == "stream":
+                if args.warmup:
+                    s.decode_stream(mode, forced[: args.warmup])
+                s.clear_stats()
+                with ClockSampler(dev) as clk:
+                    s.decode_stream(mode, forced[args.warmup:])
+            else:
+                if args.warmup:
+                    s.decode(mode, args.warmup)
+                s.clear_stats()
+                with ClockSampler(dev) as clk:
+                    s.decode(mode, args.steps)
             ms = s.token_ms()
             tpots.append(float(np.mean(ms)))
             cnt = s.counters()
@@ -185,26 +196,32 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                 rc = [len(set(ti[t, l]) & set(ei[t, l])) / K
                       for t in range(ti.shape[0]) for l in range(1, L)]
                 recall.append(float(np.mean(rc)))
-        res[mode] = dict(tpot_ms=float(np.mean(tpots)),
-                         tpot_sd=float(np.std(tpots)), runs=tpots,
-                         h2d_bytes_per_token=float(np.mean(h2d)),
-                         copy_busy_ms=float(np.mean(cms)),
-                         cache_hits=hit, cache_misses=miss, clocks=clk.summary(),
-                         kernels_per_step=s.kernels_per_step(mode),
-                         online_recall=float(np.mean(recall)) if recall else None)
+        return dict(tpot_ms=float(np.mean(tpots)), tpot_sd=float(np.std(tpots)), runs=tpots,
+                    h2d_bytes_per_token=float(np.mean(h2d)), copy_busy_ms=float(np.mean(cms)),
+                    cache_hits=hit, cache_misses=miss, clocks=clk.summary() if clk else None,
+                    kernels_per_step=s.kernels_per_step(mode),
+                    online_recall=float(np.mean(recall)) if recall else None)
+
+    res = {}
+    for wl in ("stream", "greedy"):
+        res[wl] = {mode: measure(mode, wl) for mode in ("on_demand", "prefetch")}
     # kernel-level measurement (CUDA events on the compute stream) and link peak
     prof = s.profile_kernels(reps=3)
     link = s.measure_link(128)
     # end-to-end through the C ABI with host buffers (token H2D, logits D2H per step)
-    s.reset(P + args.steps + 4, False)
+    # (stream workload: the host feeds the forced token each step; greedy: the argmax)
+    s.reset(P + args.warmup + args.steps + 4, False)
     s.prefill(prompt)
     logits = np.zeros(c["vocab"], np.float32)
     tok = int(s.tokens(P)[P - 1])
-    for _ in range(min(2, args.warmup)):
-        tok = s.step("prefetch", tok, logits)
+    for i in range(args.warmup):
+        nxt = s.step("prefetch", int(forced[i]) if args.workload == "stream" else tok, logits)
+        tok = nxt
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        tok = s.step("prefetch", tok, logits)
+    for i in range(args.steps):
+        nxt = s.step("prefetch", int(forced[args.warmup + i]) if args.workload == "stream" else tok,
+                     logits)
+        tok = nxt
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     s.close()
     return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init,
@@ -290,6 +307,9 @@ def main():
     ap.add_argument("--ref-prompt", type=int, default=4)
     ap.add_argument("--ref-new", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="stream", choices=["stream", "greedy"],
+                    help="stream: decode inputs teacher-forced from a random token stream "
+                         "(headline; exercises the offload path); greedy: argmax feedback")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -301,7 +321,9 @@ def main():
                 "predictor": args.predictor, "calib_tokens": args.calib_tokens,
                 "vocab": c["vocab"], "head_dim": c["head_dim"],
                 "l2": "inputs larger than L2 (expert bytes per token >> 126 MB)",
-                "parallelism": f"ep{world}" if world > 1 else "single-gpu"}
+                "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+                "decode_inputs": ("teacher-forced random_token_stream(seed 4)" if args.workload == "stream"
+                                  else "greedy argmax feedback")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -343,8 +365,10 @@ def main():
         dist.destroy_process_group()
     if rank != 0:
         return
-    res, prof = out["res"], out["prof"]
+    allres, prof = out["res"], out["prof"]
+    res = allres[args.workload]
     pf, od = res["prefetch"], res["on_demand"]
+    other = allres["greedy" if args.workload == "stream" else "stream"]
     L, K, H, Hm, E = c["layers"], c["top_k"], c["hidden"], c["expert_hidden"], c["experts"]
     from paper_2603_19289_b200 import ModelConfig
     peaks = {}
@@ -410,6 +434,13 @@ def main():
                   "misses_prefetch": pf["cache_misses"], "hits_on_demand": od["cache_hits"],
                   "misses_on_demand": od["cache_misses"]},
         "online_recall_at_k": pf["online_recall"],
+        "secondary_workload": {"name": "greedy" if args.workload == "stream" else "stream",
+                               "tpot_prefetch_ms": other["prefetch"]["tpot_ms"],
+                               "tpot_on_demand_ms": other["on_demand"]["tpot_ms"],
+                               "h2d_bytes_per_token_prefetch": other["prefetch"]["h2d_bytes_per_token"],
+                               "h2d_bytes_per_token_on_demand": other["on_demand"]["h2d_bytes_per_token"],
+                               "online_recall_at_k": other["prefetch"]["online_recall"],
+                               "cache_misses_prefetch": other["prefetch"]["cache_misses"]},
         "cpu_baseline": cpu,
         "e2e": {"value": out["e2e_ms"], "unit": "ms", "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": 4 * c["vocab"] + 4,

@@ -97,6 +97,11 @@ int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n);
 /* n_steps greedy decode steps on the device (speculative_forward semantics in
  * SMOE_PREFETCH mode, forward_decode in SMOE_ON_DEMAND mode). */
 int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph);
+/* Teacher-forced decode: step i consumes tokens[i] instead of the previous
+ * argmax (the reference's trace workload over random_token_stream,
+ * trace.cpp:187-211, run through speculative_forward in SMOE_PREFETCH mode).
+ * The argmax of every step is still recorded (smoe_read_tokens). */
+int smoe_decode_stream(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t n_steps);
 /* run_offloaded_decode (executor.cpp:326-359): prefill + n_new-1 decode steps;
  * out_tokens[n_new]; per_token_ms[n_new-1] (device-timed, nullable). */
 int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_prompt,

@@ -352,6 +352,8 @@ class Oracle(_Common):
         L.orc_pred_new.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_pred_free.argtypes = [C.c_void_p]
         L.orc_generate_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 13
+        L.orc_generate_trace_forced.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                                 C.c_void_p, C.c_void_p] + [C.c_void_p] * 12
         L.orc_calibrate.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_void_p]
         L.orc_silu.restype = C.c_float
         L.orc_silu.argtypes = [C.c_float]
@@ -530,11 +532,16 @@ class OracleModel:
         self.orc._check(self.orc.lib.orc_calibrate(self.h, ntok, seed, seq_len, tb.h))
         return tb
 
-    def generate_trace(self, prompt, n_new, pred=None, outputs=False) -> Trace:
+    def generate_trace(self, prompt, n_new, pred=None, outputs=False, forced=None) -> Trace:
+        """generate(); `forced` (n_new-1 tokens) teacher-forces the decode inputs."""
         prompt = np.ascontiguousarray(prompt, np.int32)
         t = _alloc_trace(self.cfg, len(prompt), n_new, outputs, pred is not None)
-        self.orc._check(self.orc.lib.orc_generate_trace(
-            self.h, _ptr(prompt), len(prompt), n_new, pred.h if pred else None, _ptr(t.tokens),
+        fz = None if forced is None else np.ascontiguousarray(forced, np.int32)
+        if fz is not None and len(fz) < n_new - 1:
+            raise ValueError("forced stream shorter than n_new - 1")
+        self.orc._check(self.orc.lib.orc_generate_trace_forced(
+            self.h, _ptr(prompt), len(prompt), n_new, pred.h if pred else None, _ptr(fz),
+            _ptr(t.tokens),
             _ptr(t.s), _ptr(t.r), _ptr(t.m), _ptr(t.logits), _ptr(t.ids), _ptr(t.gates),
             _ptr(t.outputs), _ptr(t.final_logits), _ptr(t.pred_logits), _ptr(t.pred_ids),
             _ptr(t.pred_gates)))

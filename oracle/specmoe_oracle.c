@@ -782,10 +782,13 @@ void orc_pred_free(orc_pred* p) {
 /* generate (speculation.cpp:401-421) with the same per-step trace layout as
  * oracle/ref_driver.cpp:ref_generate_trace (step s < P: prefill token s;
  * step P+i: decode step i; S = P + n_new - 1).  Any trace buffer may be NULL. */
-int orc_generate_trace(const orc_model* m, const int* prompt, int P, int n_new, orc_pred* pred,
-                       int* out_tokens, float* s, float* r, float* mo, float* logits, int* ids,
-                       float* gates, float* outputs, float* final_logits, float* pred_logits,
-                       int* pred_ids, float* pred_gates) {
+/* `forced` (nullable, n_new-1 entries): teacher forcing — decode step i is fed
+ * forced[i] instead of the previous argmax (the GPU's smoe_decode_stream). */
+int orc_generate_trace_forced(const orc_model* m, const int* prompt, int P, int n_new,
+                              orc_pred* pred, const int* forced, int* out_tokens, float* s,
+                              float* r, float* mo, float* logits, int* ids, float* gates,
+                              float* outputs, float* final_logits, float* pred_logits,
+                              int* pred_ids, float* pred_gates) {
     const orc_config* c = &m->c;
     if (P < 1) FAIL(1, "generate: empty prompt");
     const int cap = P + n_new + 1;
@@ -806,7 +809,7 @@ int orc_generate_trace(const orc_model* m, const int* prompt, int P, int n_new, 
     for (int i = 0; i < n_new && !rc; ++i) {
         out_tokens[i] = next;
         if (i + 1 == n_new) break;
-        rc = forward(m, st, next, pred, pred != NULL, &tr, step, lg);
+        rc = forward(m, st, forced ? forced[i] : next, pred, pred != NULL, &tr, step, lg);
         if (rc) break;
         if (final_logits) memcpy(final_logits + (size_t)step * c->V, lg, sizeof(float) * c->V);
         next = argmax_token(lg, c->V);
@@ -815,6 +818,15 @@ int orc_generate_trace(const orc_model* m, const int* prompt, int P, int n_new, 
     free(lg);
     orc_state_free(st);
     return rc;
+}
+
+int orc_generate_trace(const orc_model* m, const int* prompt, int P, int n_new, orc_pred* pred,
+                       int* out_tokens, float* s, float* r, float* mo, float* logits, int* ids,
+                       float* gates, float* outputs, float* final_logits, float* pred_logits,
+                       int* pred_ids, float* pred_gates) {
+    return orc_generate_trace_forced(m, prompt, P, n_new, pred, NULL, out_tokens, s, r, mo, logits,
+                                     ids, gates, outputs, final_logits, pred_logits, pred_ids,
+                                     pred_gates);
 }
 
 /* accumulate_default_vectors over random_token_stream(ntok, vocab, seed) with

@@ -124,6 +124,14 @@ int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_grap
     });
 }
 
+int smoe_decode_stream(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t n_steps) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        if (!tokens && n_steps > 0) throw std::invalid_argument("null tokens");
+        S(s)->decode_stream(mode, tokens, n_steps);
+    });
+}
+
 int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
                               int32_t n_new, int32_t mode, int32_t* out_tokens,
                               double* per_token_ms) {

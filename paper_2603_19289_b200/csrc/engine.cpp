@@ -342,6 +342,11 @@ void Session::free_all() {
     drop_graphs();
     if (s_comp_) cudaStreamSynchronize(s_comp_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
+    if (s_side_) cudaStreamSynchronize(s_side_);
+    for (auto e : ev_fork_) cudaEventDestroy(e);
+    for (auto e : ev_join_) cudaEventDestroy(e);
+    ev_fork_.clear();
+    ev_join_.clear();
     for (void* p : dev_allocs_) cudaFree(p);
     dev_allocs_.clear();
     for (auto e : ev_copy_) cudaEventDestroy(e);
@@ -361,7 +366,8 @@ void Session::free_all() {
     store_.reset();
     if (s_comp_) cudaStreamDestroy(s_comp_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
-    s_comp_ = s_copy_ = nullptr;
+    if (s_side_) cudaStreamDestroy(s_side_);
+    s_comp_ = s_copy_ = s_side_ = nullptr;
 }
 
 void Session::drop_graphs() {
@@ -392,6 +398,13 @@ void Session::alloc() {
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_side_, cudaStreamNonBlocking), "stream");
+    ev_fork_.resize(L);
+    ev_join_.resize(L);
+    for (int l = 0; l < L; ++l) {
+        ck(cudaEventCreateWithFlags(&ev_fork_[l], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&ev_join_[l], cudaEventDisableTiming), "event");
+    }
 
     d_emb_ = static_cast<uint16_t*>(dalloc(2ull * V * H));
     d_unemb_ = static_cast<uint16_t*>(dalloc(2ull * m.Vp * H));
@@ -910,10 +923,18 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
         return pred_kind_ == kHybrid ? hybrid_[l] : pred_kind_;
     };
     const DevState* shadow = pred_kind_ == kOracle ? &sh_ : nullptr;
+    // Prefetch mode keeps routing off the critical path (Alg. 1): the experts
+    // executed at layer l were predicted at l-1, so the true router (logging
+    // only) and the predictor for l+1 run on a side stream forked after the
+    // attention output, while the expert FFN proceeds on the compute stream.
+    // The side work of layer l joins before the FFN of layer l+1 (which runs
+    // the decision it produced) and before the end of the step.
+    int pending_join = -1;
     for (int l = 0; l < c.L; ++l) {
         ck(launch_qkv(dm_, st, l, s), "qkv");
         ck(launch_attn(dm_, st, d_attn_scratch_, l, s), "attn");
         ck(launch_wo(dm_, st, l, s), "wo");
+        int exec_src = 0, s_from_r = 0;
         if (!prefetch) {
             RouterLaunch rl{l, 1, kNone, 0, 1, 0, step_tag};
             ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
@@ -922,32 +943,46 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
             if (l == 0) {
                 RouterLaunch rl{0, 1, kNone, 0, 1, 0, step_tag};
                 ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
+            }
+            ck(cudaEventRecord(ev_fork_[l], s), "fork");
+            ck(cudaStreamWaitEvent(s_side_, ev_fork_[l], 0), "fork");
+            if (l == 0) {
                 if (k != kNone) {
                     RouterLaunch rp{0, 0, k, -1, 0, k != kEstPF, step_tag};
-                    ck(launch_router(dm_, st, ctl_, rp, shadow, s), "router");
+                    ck(launch_router(dm_, st, ctl_, rp, shadow, s_side_), "router");
                 }
             } else {
                 RouterLaunch rl{l, 1, k, 1, 0, k != kNone && k != kEstPF, step_tag};
-                ck(launch_router(dm_, st, ctl_, rl, shadow, s), "router");
+                ck(launch_router(dm_, st, ctl_, rl, shadow, s_side_), "router");
             }
-            if (k == kEstPF) ck(launch_estimator(dm_, st, ctl_, l, 1, step_tag, s), "estimator");
+            if (k == kEstPF) ck(launch_estimator(dm_, st, ctl_, l, 1, step_tag, s_side_), "estimator");
+            if (pending_join >= 0) ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
+            ck(cudaEventRecord(ev_join_[l], s_side_), "join");
+            pending_join = l;
+            if (l > 0) {
+                exec_src = 1;
+                s_from_r = 1;
+            }
         }
-        ck(launch_ffn(dm_, st, ctl_, l, s), "ffn");
+        ck(launch_ffn(dm_, st, ctl_, l, s, exec_src, s_from_r), "ffn");
         if (calibrating) ck(launch_dv_accum(dm_, st, d_dv_sums_, d_dv_counts_, l, s), "dv");
         if (is_main && record && trace_full_ && tr_.cap > 0) ck(launch_trace_y(dm_, st, tr_, l, s), "trace");
     }
+    if (pending_join >= 0) ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
     ck(launch_final(dm_, st, ctl_, record && is_main, s), "final");
     if (is_main && record && tr_.cap > 0) ck(launch_trace(dm_, st, tr_, s), "trace");
 }
 
-void Session::enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s) {
+void Session::enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s,
+                           int stream) {
     const int* tok_src = st_.token;
+    const int* sp = stream ? d_stream_ : nullptr;
     if (!is_prefill && mode == 1 && pred_kind_ == kOracle) {
         // Oracle::begin_token (speculation.cpp:271-280): true path on the shadow state
-        ck(launch_embed(dm_, sh_, tok_src, s), "embed");
+        ck(launch_embed(dm_, sh_, tok_src, s, sp, ctl_.step), "embed");
         enqueue_pass(sh_, 0, 0, 0, -2, 0, s);
     }
-    ck(launch_embed(dm_, st_, tok_src, s), "embed");
+    ck(launch_embed(dm_, st_, tok_src, s, sp, ctl_.step), "embed");
     enqueue_pass(st_, is_prefill ? 0 : mode, is_prefill ? 0 : 1, calibrating, is_prefill ? -1 : 0,
                  record, s);
 }
@@ -996,6 +1031,34 @@ void Session::decode(int mode, int n_steps, int use_graph) {
             ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
         else
             enqueue_step(mode, 0, 1, 0, s_comp_);
+        if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
+        ++steps_;
+    }
+    sync();
+}
+
+void Session::decode_stream(int mode, const int* tokens, int n_steps) {
+    if (n_steps < 0) throw std::invalid_argument("decode: n_steps must be >= 0");
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    for (int i = 0; i < n_steps; ++i)
+        if (tokens[i] < 0 || tokens[i] >= cfg_.V)
+            throw std::invalid_argument("forward_decode: token out of vocab");
+    sync();
+    int pos = 0;
+    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
+    if (!d_stream_) d_stream_ = static_cast<int*>(dalloc(4ull * (dm_.cap + 2)));
+    int step = 0;
+    ck(cudaMemcpy(&step, ctl_.step, 4, cudaMemcpyDeviceToHost), "step");
+    if (step + n_steps > dm_.cap + 1) throw std::invalid_argument("decode: stream exceeds capacity");
+    ck(cudaMemcpy(d_stream_ + step, tokens, 4ull * n_steps, cudaMemcpyHostToDevice), "stream");
+    cudaGraphExec_t exec = get_graph(mode, 1);
+    ck(cudaEventRecord(ev_origin_, s_comp_), "event");
+    for (int i = 0; i < n_steps; ++i) {
+        const int ev = n_step_events_ < static_cast<int>(ev_step_.size() / 2) ? n_step_events_++ : -1;
+        if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev], s_comp_), "event");
+        ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
         if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
         ++steps_;
     }
@@ -1072,8 +1135,8 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
 
 int Session::steps_done() { return steps_; }
 
-cudaGraphExec_t Session::get_graph(int mode) {
-    const long long key = mode * 10 + 1;
+cudaGraphExec_t Session::get_graph(int mode, int stream) {
+    const long long key = mode * 10 + 1 + (stream ? 100 : 0);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;
     sync();
@@ -1081,7 +1144,7 @@ cudaGraphExec_t Session::get_graph(int mode) {
     cudaGraphExec_t exec = nullptr;
     const long long before = launch_counter();
     ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
-    enqueue_step(mode, 0, 1, 0, s_comp_);
+    enqueue_step(mode, 0, 1, 0, s_comp_, stream);
     ck(cudaStreamEndCapture(s_comp_, &g), "capture");
     graph_kernels_[key] = static_cast<int>(launch_counter() - before);
     ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");

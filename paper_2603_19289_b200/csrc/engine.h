@@ -138,6 +138,10 @@ public:
     void reset(int max_steps, int trace_full);
     void prefill(const int* tokens, int n);               // true routing per token
     void decode(int mode, int n_steps, int use_graph);    // greedy, device-driven
+    // Teacher-forced decode: step i consumes tokens[i] instead of the previous
+    // argmax (the reference's trace workload, trace.cpp:187-211, fed through
+    // speculative_forward).  Greedy argmax is still recorded per step.
+    void decode_stream(int mode, const int* tokens, int n_steps);
     int step_host(int mode, int token, float* logits_out);  // host token in, logits out
     void calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out, long long* c_out);
 
@@ -173,7 +177,8 @@ private:
     void alloc();
     void free_all();
     void build_devmodel();
-    void enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s);
+    void enqueue_step(int mode, int is_prefill, int record, int calibrating, cudaStream_t s,
+                      int stream = 0);
     void enqueue_pass(DevState& st, int mode, int pred_kind_enabled, int calibrating,
                       int step_tag, int record, cudaStream_t s);
     void check_device_error();
@@ -212,6 +217,8 @@ private:
     int* h_token_ = nullptr;  // pinned token staging [2]
     float* h_logits_ = nullptr;
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
+    cudaStream_t s_side_ = nullptr;               // routers/predictors in prefetch mode
+    std::vector<cudaEvent_t> ev_fork_, ev_join_;  // per layer
     std::vector<cudaEvent_t> ev_copy_;  // pairs
     std::vector<cudaEvent_t> ev_step_;  // pairs per decode step
     cudaEvent_t ev_origin_ = nullptr;
@@ -226,7 +233,8 @@ private:
 
     std::map<long long, cudaGraphExec_t> graphs_;
     std::map<long long, int> graph_kernels_;
-    cudaGraphExec_t get_graph(int mode);
+    cudaGraphExec_t get_graph(int mode, int stream = 0);
+    int* d_stream_ = nullptr;
     void drop_graphs();
 };
 

@@ -309,19 +309,19 @@ struct WarpPipe {
             const int cn = min(CC, cols - n * CC);
             const int ng = cn / G;
             if (ng == CC / G) {
-                // software pipelined: the products of group q+1 (independent
-                // FMULs) are formed while group q's sequential FADD chain runs
-                float pc[G], pn[G];
-                products(lds128(wb), load_x(xb, WT{}), pc, WT{});
-#pragma unroll 2
+                // software pipelined: group q+1's shared loads are in flight while
+                // group q's sequential FMUL/FADD chain runs
+                uint4 wn = lds128(wb);
+                XG xn = load_x(xb, WT{});
+#pragma unroll 4
                 for (int q = 0; q < CC / G; ++q) {
-                    if (q + 1 < CC / G)
-                        products(lds128(wb + (q + 1) * 512), load_x(xb + (q + 1) * G * 4, WT{}), pn,
-                                 WT{});
-#pragma unroll
-                    for (int i = 0; i < G; ++i) acc = acc + pc[i];
-#pragma unroll
-                    for (int i = 0; i < G; ++i) pc[i] = pn[i];
+                    const uint4 w = wn;
+                    const XG x = xn;
+                    if (q + 1 < CC / G) {
+                        wn = lds128(wb + (q + 1) * 512);
+                        xn = load_x(xb + (q + 1) * G * 4, WT{});
+                    }
+                    acc = chain_group(acc, w, x, WT{});
                 }
             } else {
                 for (int q = 0; q < ng; ++q)
@@ -523,10 +523,11 @@ __global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_
 
 // ------------------------------------------------------------- attention --
 
-__global__ void k_embed(DevModel m, DevState st, const int* token_src) {
+__global__ void k_embed(DevModel m, DevState st, const int* token_src, const int* stream,
+                        const int* step) {
     pdl_trigger();
     pdl_wait();
-    const int tok = *token_src;
+    const int tok = stream ? stream[*step] : *token_src;
     if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m.Hp; j += gridDim.x * blockDim.x)
         st.x[j] = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
@@ -976,29 +977,46 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer) {
+// exec_src 0: the executed decision is id_exec/g_exec[layer] (fixed by the
+// router before this kernel); 1: it is the decision predicted at layer-1
+// (id_pred/g_pred[layer]) — prefetch mode, where the routers of this layer
+// run concurrently on a side stream (Alg. 1: the predicted experts are known
+// before the layer starts).  s_from_r: compute s_l = rms_norm(r_l, moe_gain_l)
+// here instead of reading the router's copy.
+__global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
+                                               int exec_src, int s_from_r) {
     pdl_trigger();
     pdl_wait();
     wait_ready(ctl, layer);
     if (*(volatile int*)ctl.error) return;
     const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + round_up(H, 32)));
-    PipeB pipe;
-    pipe.init(pipe_mem);
-    Stager sg;
-    sg.init(bar);
-    sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
-    const int e = st.id_exec[layer * m.K + i];
+    float* gs = xs + round_up(H, 32);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(H, 32)));
+    const int e = (exec_src ? st.id_pred : st.id_exec)[layer * m.K + i];
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     if (slot < 0) {
         if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
         return;
     }
-    sg.wait();
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
+    PipeB pipe;
+    pipe.init(pipe_mem);
+    pipe.prime(tile, H);
+    Stager sg;
+    sg.init(bar);
+    if (s_from_r) {
+        sg.add(xs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
+        sg.add(gs, m.moe_gain + static_cast<long long>(layer) * H, H * 4);
+        sg.wait();
+        block_rms_norm(xs, gs, H, m.eps, xs, red);
+    } else {
+        sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
+        sg.wait();
+    }
     const float acc = pipe.run(tile, H, xs);
     const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
     const int lane = threadIdx.x & 31;
@@ -1012,7 +1030,7 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
 // gate-weighted mixture in decision order (model.cpp:297-301) and the residual
 // x = r + m (model.cpp:386).
 __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st, DevCtl ctl,
-                                                         int layer) {
+                                                         int layer, int exec_src) {
     pdl_trigger();
     pdl_wait();
     if (*(volatile int*)ctl.error) return;
@@ -1029,7 +1047,9 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
     sg.add(hs, st.h, K * Hmp * 4);
     sg.add(rr, st.r + static_cast<long long>(layer) * m.Hp + blockIdx.x * 32, 32 * 4);
     sg.wait();
-    const int e = st.id_exec[layer * K + w];
+    const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
+    const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
+    const int e = ids[w];
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     const int rb = blockIdx.x;
     float acc = 0.0f;
@@ -1045,7 +1065,7 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
     __syncthreads();
     if (w == 0 && j < m.H) {
         float out = 0.0f;
-        for (int i = 0; i < K; ++i) out += st.g_exec[layer * K + i] * ys[i * 32 + lane];
+        for (int i = 0; i < K; ++i) out += gts[i] * ys[i * 32 + lane];
         st.m[static_cast<long long>(layer) * m.Hp + j] = out;
         st.x[j] = rr[lane] + out;
     }
@@ -1239,7 +1259,7 @@ size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
     return vec_bytes(cols) + 64 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
 }
-size_t gu_smem(const DevModel& m) { return 128 + vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t gu_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
 size_t down_smem(const DevModel& m) {
     return 128 + static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 32 * 4 + 128 +
            static_cast<size_t>(m.K) * PipeD::kBytes;
@@ -1282,8 +1302,8 @@ cudaError_t launch_gen_bf16(uint64_t seed, float stddev, int R, int C, int tile_
 }
 
 cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
-                         cudaStream_t s) {
-    PDL(k_embed, (m.Hp + 255) / 256, 256, 0, s, m, st, token_src);
+                         cudaStream_t s, const int* stream, const int* step) {
+    PDL(k_embed, (m.Hp + 255) / 256, 256, 0, s, m, st, token_src, stream, step);
     return counted(1);
 }
 
@@ -1351,18 +1371,18 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 }
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
-                       cudaStream_t s) {
-    PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer);
-    PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer);
+                       cudaStream_t s, int exec_src, int s_from_r) {
+    PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+    PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer, exec_src);
     return counted(2);
 }
 
 cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                             int part, cudaStream_t s) {
     if (part == 0)
-        PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer);
+        PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, 0, 0);
     else
-        PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer);
+        PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer, 0);
     return counted(1);
 }
 

@@ -29,8 +29,9 @@ struct RouterLaunch {
     int step_tag;       // mailbox step tag
 };
 
+// token = stream ? stream[*step] : *token_src (stream: teacher-forced decode input)
 cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
-                         cudaStream_t s);
+                         cudaStream_t s, const int* stream = nullptr, const int* step = nullptr);
 cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s);
@@ -39,8 +40,10 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
                           const RouterLaunch& rl, const DevState* shadow, cudaStream_t s);
 cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl& ctl,
                              int layer, int post_pred, int step_tag, cudaStream_t s);
+// exec_src 1: run the decision predicted for `layer` (id_pred / g_pred);
+// s_from_r 1: normalise r_l inside the kernel (routers run concurrently).
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
-                       cudaStream_t s);
+                       cudaStream_t s, int exec_src = 0, int s_from_r = 0);
 cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                             int part, cudaStream_t s);
 cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,

@@ -29,7 +29,7 @@ EXPORTS = [
     "smoe_run_offloaded_decode", "smoe_step", "smoe_calibrate", "smoe_steps_done",
     "smoe_read_tokens", "smoe_read_trace", "smoe_token_ms", "smoe_counters", "smoe_copy_events",
     "smoe_cache_slots", "smoe_debug_state", "smoe_clear_stats", "smoe_profile_kernels",
-    "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all",
+    "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
 ]
 
 
@@ -176,6 +176,10 @@ class Session:
 
     def decode(self, mode: str, n_steps: int, use_graph: bool = True):
         _check(self.lib.smoe_decode(self._h, MODE[mode], n_steps, int(use_graph)))
+
+    def decode_stream(self, mode: str, tokens):
+        t = np.ascontiguousarray(tokens, np.int32)
+        _check(self.lib.smoe_decode_stream(self._h, MODE[mode], _p(t), len(t)))
 
     def run_offloaded_decode(self, prompt, n_new: int, mode: str):
         """run_offloaded_decode (executor.cpp:326-359): tokens + device-timed per-token ms."""

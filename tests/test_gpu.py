@@ -319,3 +319,27 @@ def test_q30_layer_shapes_vs_oracle(lib):
     assert np.array_equal(got["m"], want.m)
     assert np.array_equal(got["logits"], want.final_logits)
     s.close()
+
+
+def test_stream_decode_vs_oracle_teacher_forced(lib, toy_oracle):
+    """smoe_decode_stream (teacher-forced inputs, the bench's headline workload)
+    equals the oracle's speculative_forward over the same token stream."""
+    orc, om, table, est = toy_oracle
+    forced = np.array([(37 * i + 11) % TOY["vocab"] for i in range(11)], np.int32)
+    prompt = [5, 6, 7]
+    want = om.generate_trace(prompt, 12, orc.make_predictor("router-pf", om, table),
+                             outputs=True, forced=forced)
+    s = session(TOY, cache_fraction=0.25)
+    s.load_default_vectors(np.array(table.d))
+    s.set_predictor("router-pf")
+    for mode in ("prefetch", "on_demand"):
+        S = 3 + 11
+        s.reset(S, True)
+        s.prefill(prompt)
+        s.decode_stream(mode, forced)
+        if mode == "prefetch":
+            assert np.array_equal(s.tokens(S)[2:], want.tokens)
+            assert np.array_equal(s.trace("m", S), want.m)
+            assert np.array_equal(s.trace("id_exec", S), want.ids)
+            assert np.array_equal(s.trace("logits", S), want.final_logits)
+    s.close()
