@@ -60,6 +60,39 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Optional phase timing (build with -DSMOE_PHASES; tools/phase_run.py): block
+// (0,0)'s timeline between PHASE() marks, printed once per launch.
+#ifdef SMOE_PHASES
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PHASE_DECL \
+    unsigned long long ph_[10];  \
+    int nph_ = 0;
+#define PHASE()                                  \
+    do {                                         \
+        if (nph_ < 10) ph_[nph_++] = gtimer();   \
+    } while (0)
+#define PHASE_DUMP(name)                                                                   \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                      \
+            printf("%s:", name);                                                           \
+            for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);      \
+            printf(" | %llu\n", ph_[nph_ - 1] - ph_[0]);                                   \
+        }                                                                                  \
+    } while (0)
+#else
+#define PHASE_DECL
+#define PHASE() \
+    do {        \
+    } while (0)
+#define PHASE_DUMP(name) \
+    do {                 \
+    } while (0)
+#endif
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -102,16 +135,32 @@ __device__ float block_max_f(float v, float* red) {
 }
 
 // rms_norm (numerics.cpp:72-84): out[i] = (v[i] * scale) * gain[i],
-// scale = f32(1 / sqrt(sum_f64(v^2) / n + eps)).  Whole block participates.
+// scale = f32(1 / sqrt(sum_f64(v^2) / n + eps)).  Whole block participates;
+// v, gain, out are 16-byte aligned shared arrays and n % 4 == 0 (H % 8 == 0 is
+// validated).  The f64 sum runs as 4 independent partial sums per thread
+// (fixed order: the reduction tree is deterministic).
 __device__ void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
                                double* red) {
-    double ss = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-        ss += static_cast<double>(v[i]) * static_cast<double>(v[i]);
-    ss = block_sum_d(ss, red);
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(gain);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const int n4 = n >> 2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 t = v4[i];
+        a0 += static_cast<double>(t.x) * static_cast<double>(t.x);
+        a1 += static_cast<double>(t.y) * static_cast<double>(t.y);
+        a2 += static_cast<double>(t.z) * static_cast<double>(t.z);
+        a3 += static_cast<double>(t.w) * static_cast<double>(t.w);
+    }
+    const double ss = block_sum_d((a0 + a1) + (a2 + a3), red);
     const float scale =
         static_cast<float>(1.0 / sqrt(ss / static_cast<double>(n) + static_cast<double>(eps)));
-    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v[i] * scale * gain[i];
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 t = v4[i], g = g4[i];
+        o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z,
+                            t.w * scale * g.w);
+    }
     __syncthreads();
 }
 
@@ -346,6 +395,7 @@ constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
 constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
 constexpr int kCCd = 64;    // down-projection columns per chunk (4 KB)
 using PipeB = WarpPipe<uint16_t, kS, kCCb>;
+using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
 using PipeF = WarpPipe<float, kS, kCCf>;
 using PipeD = WarpPipe<uint16_t, kS, kCCd>;
 
@@ -537,6 +587,8 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int
 // and k (model.cpp:309-321, cos/sin precomputed on the host with libm), k and v
 // appended to the layer's KV cache at `pos`.  One warp per 32-row tile.
 __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) {
+    PHASE_DECL
+    PHASE();
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
@@ -545,7 +597,7 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     pdl_trigger();
     const int rb = blockIdx.x;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * m.H * 32;
-    PipeB pipe;
+    PipeBL pipe;
     pipe.init(pipe_mem);
     pipe.prime(tile, m.H);
     Stager sg;
@@ -553,18 +605,26 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     pdl_wait();
     sg.add(xs, st.x, m.H * 4);
     sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);
-    sg.wait();
-    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
-    float acc = pipe.run(tile, m.H, xs);
+    // the epilogue's position and RoPE factors load while the chain runs
     const int lane = threadIdx.x & 31;
     const int R = rb * 32 + lane;
     const int D = m.D;
     const int pos = *st.pos;
+    float c = 1.0f, s = 0.0f;
+    if (R < 2 * D) {
+        const int i = (R % D) >> 1;
+        c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
+        s = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2 + 1];
+    }
+    PHASE();
+    sg.wait();
+    PHASE();
+    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
+    PHASE();
+    float acc = pipe.run(tile, m.H, xs);
+    PHASE();
     const float other = __shfl_xor_sync(0xffffffffu, acc, 1);
     if (R < 2 * D) {  // RoPE pair (2i, 2i+1) lives in lanes (2i', 2i'+1)
-        const int i = (R % D) >> 1;
-        const float c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
-        const float s = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2 + 1];
         const bool even = (R & 1) == 0;
         const float x0 = even ? acc : other, x1 = even ? other : acc;
         acc = even ? (x0 * c - x1 * s) : (x0 * s + x1 * c);
@@ -576,6 +636,8 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
         st.kc[kv + R - D] = acc;
     else if (R < 3 * D)
         st.vc[kv + R - 2 * D] = acc;
+    PHASE();
+    PHASE_DUMP("qkv [pre, stage, norm, chain, epi]");
 }
 
 // scores / softmax / context (model.cpp:335-351), one CTA of kAttnThreads.
@@ -756,7 +818,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
     const int b = blockIdx.x;
     pdl_trigger();
-    PipeB pipe;
+    PipeBL pipe;
     const uint16_t* tile = nullptr;
     if (b < nT + nP) {
         const bool is_true = b < nT;
@@ -1082,7 +1144,7 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
     float* gs = xs + round_up(m.H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
     pdl_trigger();
-    PipeB pipe;
+    PipeBL pipe;
     pipe.init(pipe_mem);
     pipe.prime(m.unemb + static_cast<long long>(blockIdx.x) * m.H * 32, m.H);
     Stager sg;
@@ -1249,11 +1311,11 @@ inline int gen_blocks(long long n) {
     return static_cast<int>(b < 1 ? 1 : b);
 }
 size_t vec_bytes(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
-size_t qkv_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t qkv_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t wo_smem(const DevModel&) { return 128 + kMaxD * 4 + 32 * 4 + 128 + PipeB::kBytes; }
 size_t router_smem(const DevModel& m) {
     const size_t head = 128 + (3 + static_cast<size_t>(m.K)) * vec_bytes(m.H) + 128;
-    return head + (PipeB::kBytes > kMaxE * 12 ? PipeB::kBytes : kMaxE * 12);
+    return head + (PipeBL::kBytes > kMaxE * 12 ? PipeBL::kBytes : kMaxE * 12);
 }
 size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
@@ -1264,7 +1326,7 @@ size_t down_smem(const DevModel& m) {
     return 128 + static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 32 * 4 + 128 +
            static_cast<size_t>(m.K) * PipeD::kBytes;
 }
-size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
     size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * m.D * 4;
     if (m.cap <= kAttnSmemPositions) b += static_cast<size_t>(m.cap) * 12;
