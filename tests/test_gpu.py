@@ -343,3 +343,36 @@ def test_stream_decode_vs_oracle_teacher_forced(lib, toy_oracle):
             assert np.array_equal(s.trace("id_exec", S), want.ids)
             assert np.array_equal(s.trace("logits", S), want.final_logits)
     s.close()
+
+
+@pytest.mark.parametrize("shape", ["g20", "mx"])
+def test_other_baseline_shapes_vs_oracle(lib, shape):
+    """BASELINE configs[2] (GPT-OSS-20B shape, topk-softmax gating) and configs[3]
+    (Mixtral-8x7B shape with the lightweight estimator, est-pf), depth-truncated
+    to 2 layers: prefetch decode bit-exact against the oracle."""
+    from oracle.bindings import Config, Oracle
+    if shape == "g20":
+        cfg = dict(layers=2, experts=32, top_k=4, hidden=2880, expert_hidden=2880, vocab=256,
+                   head_dim=64, seed=1, gating="topk-softmax")
+        kind = "router-pf"
+    else:
+        cfg = dict(layers=2, experts=8, top_k=2, hidden=4096, expert_hidden=14336, vocab=256,
+                   head_dim=128, seed=1, gating="topk-softmax")
+        kind = "est-pf"
+    orc = Oracle()
+    om = orc.build_model(Config(**cfg), round_bf16=True)
+    table = om.calibrate(4, 2, 256)
+    est = orc.estimator(cfg["hidden"], 8, 4, cfg["experts"], cfg["layers"], seed=5)
+    prompt = [3, 30, 200]
+    want = om.generate_trace(prompt, 4, orc.make_predictor(kind, om, table, est), outputs=False)
+    s = session(cfg, cache_fraction=0.5)
+    s.load_default_vectors(np.array(table.d))
+    s.load_estimator(cfg["hidden"], 8, 4, cfg["experts"], cfg["layers"], 1e-5, np.array(est.flat))
+    s.set_predictor(kind)
+    got = run_trace(s, prompt, 4, "prefetch")
+    assert np.array_equal(got["tokens"], want.tokens)
+    assert np.array_equal(got["id_exec"], want.ids)
+    assert np.array_equal(got["g_exec"], want.gates)
+    assert np.array_equal(got["m"], want.m)
+    assert np.array_equal(got["logits"], want.final_logits)
+    s.close()
