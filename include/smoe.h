@@ -40,6 +40,8 @@ typedef struct smoe_options {
     int32_t max_positions;
     int32_t copy_latency_us;
     double deadlock_s;
+    int32_t ep_rank;   /* expert parallelism: this rank owns experts e % ep_world == ep_rank */
+    int32_t ep_world;  /* 1 = single GPU (default when 0) */
 } smoe_options;
 
 /* EstimatorConfig (estimator.hpp:20-39). */
@@ -132,6 +134,18 @@ int smoe_counters(smoe_session* s, int64_t* hits, int64_t* misses, int64_t* h2d_
 int smoe_copy_events(smoe_session* s, smoe_copy_event* out, int32_t cap, int32_t* n);
 /* Slots per layer actually allocated. */
 int smoe_cache_slots(smoe_session* s, int32_t* slots);
+/* Expert parallelism.  Each rank creates its session with
+ * ep_rank/ep_world (its pinned store, slot pool and copy lane hold only its
+ * shard), then connects to the exchange buffers and arrival counters of all
+ * ranks: either raw device pointers (ranks sharing a process; smoe_ep_buffers
+ * gives each rank's own) or CUDA IPC handles (one process per GPU; 128 bytes
+ * per rank from smoe_ep_ipc_handles, exchanged by the caller, e.g. with
+ * torch.distributed).  After connecting, every decode step combines expert
+ * outputs across ranks through peer memory; results equal the single-GPU path. */
+int smoe_ep_buffers(smoe_session* s, void** xbuf, void** counters);
+int smoe_ep_ipc_handles(smoe_session* s, unsigned char* out128);
+int smoe_ep_connect(smoe_session* s, void* const* xbufs, void* const* counters);
+int smoe_ep_connect_ipc(smoe_session* s, const unsigned char* handles);
 /* Copies every expert into HBM (cache_fraction 1.0 only): the model is fully
  * resident, decode posts no copy requests and never waits on the copy lane. */
 int smoe_preload_all(smoe_session* s);

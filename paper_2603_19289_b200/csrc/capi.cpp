@@ -51,6 +51,8 @@ int smoe_session_create(const smoe_config* cfg, const smoe_options* opt, smoe_se
             o.max_positions = opt->max_positions;
             o.copy_latency_us = opt->copy_latency_us;
             o.deadlock_s = opt->deadlock_s > 0 ? opt->deadlock_s : 10.0;
+            o.ep_rank = opt->ep_rank;
+            o.ep_world = opt->ep_world > 0 ? opt->ep_world : 1;
         }
         *out = reinterpret_cast<smoe_session*>(new smoe::Session(c, o));
     });
@@ -236,6 +238,34 @@ int smoe_cache_slots(smoe_session* s, int32_t* slots) {
 
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->debug_state(out, cap); });
+}
+
+int smoe_ep_buffers(smoe_session* s, void** xbuf, void** counters) {
+    return guard([&] {
+        if (!xbuf || !counters) throw std::invalid_argument("null argument");
+        S(s)->ep_buffers(xbuf, counters);
+    });
+}
+
+int smoe_ep_ipc_handles(smoe_session* s, unsigned char* out128) {
+    return guard([&] {
+        if (!out128) throw std::invalid_argument("null argument");
+        S(s)->ep_ipc_handles(out128);
+    });
+}
+
+int smoe_ep_connect(smoe_session* s, void* const* xbufs, void* const* counters) {
+    return guard([&] {
+        if (!xbufs || !counters) throw std::invalid_argument("null argument");
+        S(s)->ep_connect(xbufs, counters);
+    });
+}
+
+int smoe_ep_connect_ipc(smoe_session* s, const unsigned char* handles) {
+    return guard([&] {
+        if (!handles) throw std::invalid_argument("null argument");
+        S(s)->ep_connect_ipc(handles);
+    });
 }
 
 int smoe_preload_all(smoe_session* s) {

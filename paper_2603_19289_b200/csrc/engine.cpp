@@ -260,7 +260,11 @@ void CopyScheduler::handle(const MailboxEntry& e) {
     if (s.opts_.copy_latency_us > 0)
         std::this_thread::sleep_for(std::chrono::microseconds(s.opts_.copy_latency_us));
     int hits = 0, misses = 0;
-    auto copies = s.cache_->request(e.layer, e.ids, e.nids, &hits, &misses);
+    int local[kMaxK];
+    int nloc = 0;
+    for (int i = 0; i < e.nids; ++i)
+        if (s.is_local(e.ids[i])) local[nloc++] = e.ids[i];  // EP: only this rank's shard
+    auto copies = s.cache_->request(e.layer, local, nloc, &hits, &misses);
     const int npairs = static_cast<int>(s.ev_copy_.size() / 2);
     int ev = -1;
     {
@@ -272,7 +276,7 @@ void CopyScheduler::handle(const MailboxEntry& e) {
     const int E = s.cfg_.E;
     for (auto& [slot, expert] : copies) {
         uint16_t* dst = s.d_slots_ + (static_cast<long long>(e.layer) * s.C_ + slot) * s.dm_.expert_elems;
-        const uint16_t* src = s.store_->expert(static_cast<long long>(e.layer) * E + expert);
+        const uint16_t* src = s.store_->expert(s.store_index(e.layer, expert));
         ck(cudaMemcpyAsync(dst, src, bytes_per, cudaMemcpyHostToDevice, s.s_copy_), "H2D expert copy");
     }
     if (!copies.empty()) {
@@ -320,6 +324,10 @@ Session::Session(const ModelCfg& cfg, const SessionOpts& opts) : cfg_(cfg), opts
     if (!(opts_.cache_fraction > 0.0f && opts_.cache_fraction <= 1.0f))
         throw std::invalid_argument("cache_fraction must be in (0, 1]");
     if (opts_.max_positions < 2) throw std::invalid_argument("max_positions must be >= 2");
+    if (opts_.ep_world < 1 || opts_.ep_world > kMaxEP)
+        throw std::invalid_argument("ep_world must be in [1, 8]");
+    if (opts_.ep_rank < 0 || opts_.ep_rank >= opts_.ep_world)
+        throw std::invalid_argument("ep_rank must be in [0, ep_world)");
     ck(cudaSetDevice(opts_.device), "cudaSetDevice");
     write_value_fn();
     ck(preload_kernels(), "kernel preload");
@@ -347,6 +355,8 @@ void Session::free_all() {
     for (auto e : ev_join_) cudaEventDestroy(e);
     ev_fork_.clear();
     ev_join_.clear();
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    ipc_opened_.clear();
     for (void* p : dev_allocs_) cudaFree(p);
     dev_allocs_.clear();
     for (auto e : ev_copy_) cudaEventDestroy(e);
@@ -378,6 +388,7 @@ void Session::drop_graphs() {
 void Session::alloc() {
     const ModelCfg& c = cfg_;
     const int L = c.L, E = c.E, K = c.K, H = c.H, D = c.D, V = c.V;
+    el_max_ = (E + opts_.ep_world - 1) / opts_.ep_world;
     DevModel& m = dm_;
     m.L = L; m.E = E; m.K = K; m.H = H; m.Hm = c.Hm; m.V = V; m.D = D;
     m.eps = c.eps;
@@ -391,9 +402,7 @@ void Session::alloc() {
     m.inv_sqrt_d = 1.0f / std::sqrt(static_cast<float>(D));  // model.cpp:336
     m.gu_elems = static_cast<long long>(m.Hmp) * H * 2;
     m.expert_elems = m.gu_elems + static_cast<long long>(m.Hp) * m.Hmp;
-    C_ = static_cast<int>(std::ceil(static_cast<double>(opts_.cache_fraction) * E));
-    if (C_ < K) C_ = K;
-    if (C_ > E) C_ = E;
+    C_ = slots_for(opts_.cache_fraction);
     m.C = C_;
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
@@ -441,6 +450,14 @@ void Session::alloc() {
     d_slot_of_ = static_cast<int*>(dalloc(4ull * L * E));
     ck(cudaMemset(d_slot_of_, 0xff, 4ull * L * E), "memset");
     d_dv_ = static_cast<float*>(dalloc(4ull * L * E * H));
+    d_xbuf_ = static_cast<float*>(dalloc(4ull * 2 * K * m.Hp));
+    d_cnt_ = static_cast<int*>(dalloc(4ull * L));
+    d_epoch_ = static_cast<int*>(dalloc(4ull * L));
+    ctl_.ep.rank = 0;
+    ctl_.ep.world = 1;  // EP activates at ep_connect(); until then this rank runs everything it owns
+    ctl_.ep.xbuf[0] = d_xbuf_;
+    ctl_.ep.cnt[0] = d_cnt_;
+    ctl_.ep.epoch = d_epoch_;
     d_hybrid_ = static_cast<int*>(dalloc(4ull * L));
     d_attn_scratch_ = static_cast<double*>(dalloc(16ull * m.cap));
     d_prompt_tok_ = static_cast<int*>(dalloc(4ull * m.cap));
@@ -516,24 +533,87 @@ void Session::alloc() {
     for (auto& e : ev_step_) ck(cudaEventCreate(&e), "event");
     ck(cudaEventCreate(&ev_origin_), "event");
 
-    store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * E, m.expert_elems);
+    store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * el_max_, m.expert_elems);
     cache_ = std::make_unique<SlotCache>(L, E, C_);
     reset(0, 0);
 }
 
+int Session::slots_for(float frac) const {
+    const int El = local_experts();
+    int C = static_cast<int>(std::ceil(static_cast<double>(frac) * El));
+    const int lo = cfg_.K < El ? cfg_.K : El;  // one request holds at most min(k, El) local ids
+    if (C < lo) C = lo;
+    if (C > El) C = El;
+    if (C < 1) C = 1;
+    return C;
+}
+
+void Session::ep_buffers(void** xbuf, void** cnt) {
+    *xbuf = d_xbuf_;
+    *cnt = d_cnt_;
+}
+
+void Session::ep_ipc_handles(unsigned char* out128) {
+    cudaIpcMemHandle_t a, b;
+    ck(cudaIpcGetMemHandle(&a, d_xbuf_), "ipc handle");
+    ck(cudaIpcGetMemHandle(&b, d_cnt_), "ipc handle");
+    std::memcpy(out128, &a, 64);
+    std::memcpy(out128 + 64, &b, 64);
+}
+
+// Every rank passes the exchange buffers / counters of all ranks (its own at
+// index ep_rank).  Replicated dense path + these peer stores = bit-exact EP.
+void Session::ep_connect(void* const* xbufs, void* const* cnts) {
+    sync();
+    const int W = opts_.ep_world;
+    for (int p = 0; p < W; ++p) {
+        if (!xbufs[p] || !cnts[p]) throw std::invalid_argument("ep_connect: null peer buffer");
+        ctl_.ep.xbuf[p] = static_cast<float*>(xbufs[p]);
+        ctl_.ep.cnt[p] = static_cast<int*>(cnts[p]);
+    }
+    ctl_.ep.xbuf[opts_.ep_rank] = d_xbuf_;
+    ctl_.ep.cnt[opts_.ep_rank] = d_cnt_;
+    ctl_.ep.rank = opts_.ep_rank;
+    ctl_.ep.world = W;
+    ck(cudaMemset(d_cnt_, 0, 4ull * cfg_.L), "ep reset");
+    ck(cudaMemset(d_epoch_, 0, 4ull * cfg_.L), "ep reset");
+    drop_graphs();
+}
+
+void Session::ep_connect_ipc(const unsigned char* handles) {
+    const int W = opts_.ep_world;
+    std::vector<void*> xb(W), cn(W);
+    for (int p = 0; p < W; ++p) {
+        if (p == opts_.ep_rank) {
+            xb[p] = d_xbuf_;
+            cn[p] = d_cnt_;
+            continue;
+        }
+        cudaIpcMemHandle_t a, b;
+        std::memcpy(&a, handles + p * 128, 64);
+        std::memcpy(&b, handles + p * 128 + 64, 64);
+        ck(cudaIpcOpenMemHandle(&xb[p], a, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        ck(cudaIpcOpenMemHandle(&cn[p], b, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        ipc_opened_.push_back(xb[p]);
+        ipc_opened_.push_back(cn[p]);
+    }
+    ep_connect(xb.data(), cn.data());
+}
+
 void Session::preload_all() {
     sync();
-    if (C_ != cfg_.E) throw std::invalid_argument("preload_all: needs cache_fraction 1.0");
+    if (C_ != local_experts()) throw std::invalid_argument("preload_all: needs cache_fraction 1.0");
     ck(cudaStreamSynchronize(s_copy_), "copy stream");
     const long long per = dm_.expert_elems;
-    std::vector<int> ids(cfg_.E);
-    for (int e = 0; e < cfg_.E; ++e) ids[e] = e;
+    std::vector<int> ids;
+    for (int e = 0; e < cfg_.E; ++e)
+        if (is_local(e)) ids.push_back(e);
     for (int l = 0; l < cfg_.L; ++l) {
         int h = 0, mi = 0;
-        auto copies = cache_->request(l, ids.data(), cfg_.E, &h, &mi);
+        auto copies = cache_->request(l, ids.data(), static_cast<int>(ids.size()), &h, &mi);
         for (auto& [slot, expert] : copies)
             ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * per,
-                               store_->expert(static_cast<long long>(l) * cfg_.E + expert), per * 2,
+                               store_->expert(store_index(l, expert)), per * 2,
                                cudaMemcpyHostToDevice, s_copy_),
                "preload");
         ck(cudaMemcpyAsync(d_slot_of_ + static_cast<long long>(l) * cfg_.E, cache_->slot_row(l).data(),
@@ -549,9 +629,7 @@ void Session::preload_all() {
 void Session::set_cache_fraction(float frac) {
     if (!(frac > 0.0f && frac <= 1.0f)) throw std::invalid_argument("cache_fraction must be in (0, 1]");
     sync();
-    int C = static_cast<int>(std::ceil(static_cast<double>(frac) * cfg_.E));
-    if (C < cfg_.K) C = cfg_.K;
-    if (C > cfg_.E) C = cfg_.E;
+    const int C = slots_for(frac);
     if (C == C_) return;
     // replace the slot pool
     for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
@@ -601,7 +679,7 @@ void Session::init_weights_seeded() {
     }
     // experts: batches through an HBM staging buffer
     const long long per = m.expert_elems;
-    const long long total = static_cast<long long>(c.L) * c.E;
+    const long long total = static_cast<long long>(c.L) * el_max_;
     long long batch = (1ll << 30) / (per * 2);  // ~1 GiB staging
     if (batch < 1) batch = 1;
     if (batch > total) batch = total;
@@ -612,7 +690,9 @@ void Session::init_weights_seeded() {
         ck(cudaMemsetAsync(stage, 0, static_cast<size_t>(nb) * per * 2, s), "memset");
         for (long long i = 0; i < nb; ++i) {
             const long long x = b0 + i;
-            const int l = static_cast<int>(x / c.E), e = static_cast<int>(x % c.E);
+            const int l = static_cast<int>(x / el_max_);
+            const int e = static_cast<int>(x % el_max_) * opts_.ep_world + opts_.ep_rank;
+            if (e >= c.E) continue;  // padding block of a short shard
             const std::string p = "layer" + std::to_string(l) + ".expert" + std::to_string(e) + ".";
             uint16_t* blk = stage + i * per;
             gen(p + "w_gate", c.Hm, c.H, c.H, kGateUp, 0, 0, blk);
@@ -698,7 +778,8 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
     int e;
     char which[32];
     if (std::sscanf(rest.c_str(), "expert%d.%31s", &e, which) == 2 && e >= 0 && e < c.E) {
-        uint16_t* blk = store_->expert(static_cast<long long>(l) * c.E + e);
+        if (!is_local(e)) return;  // EP: another rank owns this expert
+        uint16_t* blk = store_->expert(store_index(l, e));
         const std::string w = which;
         if (w == "w_gate" || w == "w_up") {
             need(static_cast<long long>(c.Hm) * c.H);
@@ -1240,7 +1321,7 @@ double Session::measure_link(int n_copies) {
     cudaEvent_t a, b;
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
-    const long long nexp = static_cast<long long>(cfg_.L) * cfg_.E;
+    const long long nexp = static_cast<long long>(cfg_.L) * el_max_;
     for (int i = 0; i < 4; ++i)
         ck(cudaMemcpyAsync(scratch, store_->expert(i % nexp), bytes, cudaMemcpyHostToDevice, s_copy_), "warm");
     ck(cudaEventRecord(a, s_copy_), "event");

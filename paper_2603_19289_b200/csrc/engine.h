@@ -43,6 +43,8 @@ struct SessionOpts {
     int max_positions = 4096;     // KV capacity
     int copy_latency_us = 0;      // injected per copy request (ExecutorOptions parity)
     double deadlock_s = 10.0;     // device spin limit before "deadlock suspected"
+    int ep_rank = 0;              // expert parallelism: this rank owns experts e % ep_world == ep_rank
+    int ep_world = 1;
 };
 
 struct EstCfg {
@@ -158,6 +160,19 @@ public:
 
     const ModelCfg& cfg() const { return cfg_; }
     int slots_per_layer() const { return C_; }
+    // --- expert parallelism ----------------------------------------------------
+    bool is_local(int e) const { return e % opts_.ep_world == opts_.ep_rank; }
+    int local_experts() const {
+        return (cfg_.E - opts_.ep_rank + opts_.ep_world - 1) / opts_.ep_world;
+    }
+    long long store_index(int l, int e) const {
+        return static_cast<long long>(l) * el_max_ + e / opts_.ep_world;
+    }
+    int slots_for(float frac) const;
+    void ep_buffers(void** xbuf, void** cnt);
+    void ep_ipc_handles(unsigned char* out128);
+    void ep_connect(void* const* xbufs, void* const* cnts);
+    void ep_connect_ipc(const unsigned char* handles);  // world x 128 bytes
     void debug_state(int* out, int cap);
     void clear_stats();
     // Average device time (us) per launch of each per-layer kernel, timed with
@@ -207,6 +222,11 @@ private:
     float* d_est_ = nullptr;
     int* d_hybrid_ = nullptr;
     int* d_prompt_tok_ = nullptr;
+    int el_max_ = 0;                       // store blocks per layer = ceil(E / ep_world)
+    float* d_xbuf_ = nullptr;              // EP exchange buffer [2][K][Hp]
+    int* d_cnt_ = nullptr;                 // EP arrival counters [L]
+    int* d_epoch_ = nullptr;               // EP combines done [L]
+    std::vector<void*> ipc_opened_;
 
     // host
     std::unique_ptr<ExpertStore> store_;

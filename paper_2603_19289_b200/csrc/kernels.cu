@@ -1049,15 +1049,16 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
                                                int exec_src, int s_from_r) {
     pdl_trigger();
     pdl_wait();
+    const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
+    const int e = (exec_src ? st.id_pred : st.id_exec)[layer * m.K + i];
+    if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it
     wait_ready(ctl, layer);
     if (*(volatile int*)ctl.error) return;
-    const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* gs = xs + round_up(H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(H, 32)));
-    const int e = (exec_src ? st.id_pred : st.id_exec)[layer * m.K + i];
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     if (slot < 0) {
         if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
@@ -1112,17 +1113,34 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
     const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
     const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
     const int e = ids[w];
-    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    const bool local = ctl.ep.world == 1 || e % ctl.ep.world == ctl.ep.rank;
+    const int slot = local ? __ldcg(m.slot_of + layer * m.E + e) : -1;
     const int rb = blockIdx.x;
     float acc = 0.0f;
-    if (slot >= 0) {
+    if (local && slot < 0) {
+        if (lane == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+    } else if (local) {
         const uint16_t* tile = m.slots +
                                (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                                m.gu_elems + static_cast<long long>(rb) * Hmp * 32;
         acc = pipe.run(tile, m.Hm, hs + w * Hmp);
     }
-    ys[w * 32 + lane] = acc;
     const int j = rb * 32 + lane;
+    if (ctl.ep.world > 1) {
+        // EP: publish this rank's expert rows to every rank, then bump their
+        // per-layer arrival counters; k_ep_mix does the mixture.
+        if (local && j < m.H) {
+            const long long o = (static_cast<long long>(layer & 1) * K + w) * m.Hp + j;
+            for (int p = 0; p < ctl.ep.world; ++p) __stcg(ctl.ep.xbuf[p] + o, acc);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int p = 0; p < ctl.ep.world; ++p) atomicAdd_system(ctl.ep.cnt[p] + layer, 1);
+        }
+        return;
+    }
+    ys[w * 32 + lane] = acc;
     if (j < m.H) st.y[static_cast<long long>(w) * m.Hp + j] = acc;
     __syncthreads();
     if (w == 0 && j < m.H) {
@@ -1131,6 +1149,52 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
         st.m[static_cast<long long>(layer) * m.Hp + j] = out;
         st.x[j] = rr[lane] + out;
     }
+}
+
+// EP combine: wait until every rank's down-projection CTAs of this layer have
+// published their rows (system-scope acquire on the arrival counter), then
+// mix all k raw outputs in decision order (model.cpp:297-301) and add the
+// residual — identical arithmetic to the single-GPU epilogue.
+__global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl ctl, int layer,
+                                               int exec_src) {
+    pdl_trigger();
+    pdl_wait();
+    const int K = m.K, lane = threadIdx.x & 31, rb = blockIdx.x, j = rb * 32 + lane;
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        const long long target =
+            (static_cast<long long>(ctl.ep.epoch[layer]) + 1) * ctl.ep.world * gridDim.x;
+        const int* cnt = ctl.ep.cnt[ctl.ep.rank] + layer;
+        const long long t0 = clock64();
+        int ok = 1;
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            if (v >= target) break;
+            if (*(volatile int*)ctl.error || clock64() - t0 > ctl.spin_limit) {
+                atomicCAS(ctl.error, 0, 3000 + layer);
+                ok = 0;
+                break;
+            }
+            __nanosleep(64);
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (s_ok && j < m.H) {
+        const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
+        const float* xb = ctl.ep.xbuf[ctl.ep.rank] + static_cast<long long>(layer & 1) * K * m.Hp;
+        float out = 0.0f;
+        for (int i = 0; i < K; ++i) {
+            const float y = __ldcv(xb + static_cast<long long>(i) * m.Hp + j);
+            st.y[static_cast<long long>(i) * m.Hp + j] = y;
+            out += gts[i] * y;
+        }
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        st.x[j] = st.r[static_cast<long long>(layer) * m.Hp + j] + out;
+    }
+    if (!last_cta(st.counters + 3, gridDim.x)) return;
+    if (threadIdx.x == 0) ctl.ep.epoch[layer] += 1;
 }
 
 // ------------------------------------------------------------ final / argmax --
@@ -1378,7 +1442,8 @@ cudaError_t preload_kernels() {
                          (const void*)k_attn, (const void*)k_wo, (const void*)k_router,
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
                          (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
-                         (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump};
+                         (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
+                         (const void*)k_ep_mix};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -1436,6 +1501,10 @@ cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl,
                        cudaStream_t s, int exec_src, int s_from_r) {
     PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
     PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer, exec_src);
+    if (ctl.ep.world > 1) {
+        PDL(k_ep_mix, m.Hp / 32, 32, 0, s, m, st, ctl, layer, exec_src);
+        g_launches += 1;
+    }
     return counted(2);
 }
 

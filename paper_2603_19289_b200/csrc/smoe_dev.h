@@ -117,6 +117,21 @@ struct DevState {
     int* counters;     // last-CTA counters [64]
 };
 
+// Expert parallelism: expert e of every layer lives on rank
+// e % world.  Combine without summation: each rank writes the raw outputs of
+// its local experts into every rank's exchange buffer (peer memory over
+// NVLink, or the same device when ranks share a GPU) and bumps each rank's
+// per-layer arrival counter with a system-scope atomic; every rank then mixes
+// all k rows in decision order, so EP results equal single-GPU results bit
+// for bit.
+constexpr int kMaxEP = 8;
+struct DevEP {
+    int rank, world;
+    float* xbuf[kMaxEP];  // rank p's exchange buffer [2][K][Hp] (layer parity), mapped here
+    int* cnt[kMaxEP];     // rank p's arrival counters [L] (monotonic)
+    int* epoch;           // this rank's combines completed per layer [L]
+};
+
 // Cross-stream control block (device memory unless noted).
 struct DevCtl {
     MailboxEntry* mailbox;   // mapped pinned host memory, kMailboxRing entries
@@ -128,6 +143,7 @@ struct DevCtl {
     int* tokens_out;         // [max_steps]
     long long spin_limit;    // clock64 cycles before declaring a deadlock
     int resident;            // 1: every expert is resident (no requests, no waits)
+    DevEP ep;
 };
 
 }  // namespace smoe

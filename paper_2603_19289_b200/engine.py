@@ -30,6 +30,7 @@ EXPORTS = [
     "smoe_read_tokens", "smoe_read_trace", "smoe_token_ms", "smoe_counters", "smoe_copy_events",
     "smoe_cache_slots", "smoe_debug_state", "smoe_clear_stats", "smoe_profile_kernels",
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
+    "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
 ]
 
 
@@ -43,7 +44,7 @@ class _Config(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("cache_fraction", C.c_float),
                 ("max_positions", C.c_int32), ("copy_latency_us", C.c_int32),
-                ("deadlock_s", C.c_double)]
+                ("deadlock_s", C.c_double), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
 
 
 class _EstConfig(C.Structure):
@@ -114,11 +115,13 @@ class Session:
     """One model on one GPU: pinned expert store + HBM slot cache + decode state."""
 
     def __init__(self, cfg: ModelConfig, device: int = 0, cache_fraction: float = 1.0,
-                 max_positions: int = 4096, copy_latency_us: int = 0, deadlock_s: float = 10.0):
+                 max_positions: int = 4096, copy_latency_us: int = 0, deadlock_s: float = 10.0,
+                 ep_rank: int = 0, ep_world: int = 1):
         lib = load_library()
         self.cfg = cfg
         self._h = C.c_void_p()
-        opt = _Options(device, cache_fraction, max_positions, copy_latency_us, deadlock_s)
+        opt = _Options(device, cache_fraction, max_positions, copy_latency_us, deadlock_s,
+                       ep_rank, ep_world)
         c = cfg._c()
         _check(lib.smoe_session_create(C.byref(c), C.byref(opt), C.byref(self._h)))
         self.lib = lib
@@ -242,6 +245,29 @@ class Session:
                                       C.byref(req)))
         return {"hits": hits, "misses": misses, "h2d_bytes": b.value, "copy_ms": ms.value,
                 "requests": req.value}
+
+    # -- expert parallelism -----------------------------------------------------
+    def ep_buffers(self):
+        x = C.c_void_p()
+        c = C.c_void_p()
+        _check(self.lib.smoe_ep_buffers(self._h, C.byref(x), C.byref(c)))
+        return x.value, c.value
+
+    def ep_ipc_handles(self) -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(self.lib.smoe_ep_ipc_handles(self._h, buf))
+        return bytes(buf)
+
+    def ep_connect(self, xbufs, cnts):
+        W = len(xbufs)
+        xa = (C.c_void_p * W)(*xbufs)
+        ca = (C.c_void_p * W)(*cnts)
+        _check(self.lib.smoe_ep_connect(self._h, xa, ca))
+
+    def ep_connect_ipc(self, handles):
+        blob = b"".join(handles)
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(self.lib.smoe_ep_connect_ipc(self._h, buf))
 
     def preload_all(self):
         _check(self.lib.smoe_preload_all(self._h))

@@ -376,3 +376,58 @@ def test_other_baseline_shapes_vs_oracle(lib, shape):
     assert np.array_equal(got["m"], want.m)
     assert np.array_equal(got["logits"], want.final_logits)
     s.close()
+
+
+@pytest.mark.parametrize("mode", ["prefetch", "on_demand"])
+def test_expert_parallel_two_ranks_bit_exact(lib, toy_oracle, mode):
+    """EP with two ranks sharing this GPU: each rank stores, caches
+    and copies only experts e % 2 == rank, the dense path is replicated, and
+    the combine exchanges raw expert rows through peer stores + system-scope
+    arrival counters.  Both ranks must equal the single-GPU / oracle result."""
+    import threading
+    orc, om, table, est = toy_oracle
+    forced = np.array([(29 * i + 3) % TOY["vocab"] for i in range(9)], np.int32)
+    prompt = [8, 9, 10, 11]
+    pred = orc.make_predictor("router-pf", om, table) if mode == "prefetch" else None
+    want = om.generate_trace(prompt, 10, pred, outputs=True, forced=forced)
+    ranks = [session(TOY, cache_fraction=0.5, ep_rank=r, ep_world=2) for r in (0, 1)]
+    for s in ranks:
+        s.load_default_vectors(np.array(table.d))
+        s.set_predictor("router-pf")
+    bufs = [s.ep_buffers() for s in ranks]
+    for s in ranks:
+        s.ep_connect([b[0] for b in bufs], [b[1] for b in bufs])
+    S = len(prompt) + 9
+    out = [None, None]
+    errs = []
+
+    def run(i):
+        try:
+            s = ranks[i]
+            s.reset(S, True)
+            s.prefill(prompt)
+            s.decode_stream(mode, forced)
+            out[i] = dict(tokens=s.tokens(S)[len(prompt) - 1:], m=s.trace("m", S),
+                          ids=s.trace("id_exec", S), logits=s.trace("logits", S),
+                          y=s.trace("y", S), c=s.counters())
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for o in out:
+        assert np.array_equal(o["tokens"], want.tokens)
+        assert np.array_equal(o["ids"], want.ids)
+        assert np.array_equal(o["m"], want.m)
+        assert np.array_equal(o["y"], want.outputs)
+        assert np.array_equal(o["logits"], want.final_logits)
+    # each rank copied only its own shard
+    for s in ranks:
+        ev = s.copy_events()
+        assert all(e.hits + e.misses <= TOY["top_k"] for e in ev)
+    for s in ranks:
+        s.close()
