@@ -214,6 +214,18 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     res = {}
     for wl in ("stream", "greedy"):
         res[wl] = {mode: measure(mode, wl) for mode in ("on_demand", "prefetch")}
+    # lane breakdown (reference e2e output: per_token_reports + breakdown) from a
+    # measured timeline run of the headline workload
+    from paper_2603_19289_b200 import breakdown
+    for mode in ("on_demand", "prefetch"):
+        s.reset(P + args.warmup + args.steps, False)
+        s.prefill(prompt)
+        ev = s.timeline(mode, args.steps,
+                        forced[: args.steps] if args.workload == "stream" else None)
+        fr, tp = breakdown(ev)
+        res[args.workload][mode]["breakdown"] = {
+            "compute_frac": fr[0], "copy_frac": fr[1], "idle_frac": fr[2],
+            "timeline_tpot_ms": tp, "how": "smoe_timeline (no graph, CUDA events per phase)"}
     # kernel-level measurement (CUDA events on the compute stream) and link peak
     prof = s.profile_kernels(reps=3)
     link = s.measure_link(128)
@@ -454,6 +466,7 @@ def main():
                   "misses_prefetch": pf["cache_misses"], "hits_on_demand": od["cache_hits"],
                   "misses_on_demand": od["cache_misses"]},
         "online_recall_at_k": pf["online_recall"],
+        "breakdown": {"prefetch": pf.get("breakdown"), "on_demand": od.get("breakdown")},
         "secondary_workload": {"name": "greedy" if args.workload == "stream" else "stream",
                                "tpot_prefetch_ms": other["prefetch"]["tpot_ms"],
                                "tpot_on_demand_ms": other["on_demand"]["tpot_ms"],

@@ -65,6 +65,13 @@ typedef struct smoe_copy_event {
     double start_ms, end_ms;
 } smoe_copy_event;
 
+/* One measured lane event (MeasuredEvent, executor.hpp:31-37): lane 0 compute /
+ * 1 copy; kind 0 attn / 1 gate / 2 expert / 3 copy; token = decode step index. */
+typedef struct smoe_event {
+    int32_t lane, kind, layer, token;
+    double start_ms, end_ms;
+} smoe_event;
+
 const char* smoe_last_error(void);
 
 /* Creates a session: allocates the pinned bf16 expert store, HBM slot pool,
@@ -160,6 +167,28 @@ int smoe_profile_kernels(smoe_session* s, int32_t reps, double* out_us);
 int smoe_measure_link(smoe_session* s, int32_t n_copies, double* gbps);
 /* Kernel launches in one captured decode step (-1 before the first capture). */
 int smoe_kernels_per_step(smoe_session* s, int32_t mode, int32_t* n);
+/* Decode with a per-layer lane timeline (no CUDA graph; CUDA events around
+ * attention, routing and expert phases, plus the copy lane): the measured
+ * event log of run_offloaded_decode (executor.cpp:239-322).  tokens: forced
+ * inputs (nullable = greedy).  Returns up to cap events through out, total in *n. */
+int smoe_timeline(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t n_steps,
+                  smoe_event* out, int32_t cap, int32_t* n);
+
+/* Reporting (host-only, no GPU needed). */
+/* simulate_on_demand / simulate_prefetch (schedule.cpp:92-148) + breakdown
+ * (schedule.cpp:205-217) + analytic_improvement (Eq. 1, schedule.cpp:150-155).
+ * cold_start_copy < 0 means "use t_copy[0]". */
+int smoe_simulate(int32_t layers, const double* t_attn, const double* t_gate,
+                  const double* t_expert, const double* t_copy, double cold_start_copy,
+                  int32_t mode, double* tpot, double* fractions3, double* analytic);
+/* per_token_reports (executor.cpp:361-382) then breakdown, averaged over tokens:
+ * fractions {compute, copy on the critical path, idle}. */
+int smoe_breakdown(const smoe_event* events, int32_t n, double* mean_fractions3,
+                   double* mean_tpot);
+/* recall_at_k (metrics.cpp:9-20) and rank_alignment (metrics.cpp:22-28). */
+int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, double* recall,
+                     int32_t* rank_match);
+
 /* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap);
 

@@ -554,4 +554,31 @@ int ref_simulate(int L, const double* attn, const double* gate, const double* ex
     });
 }
 
+// per_token_reports (executor.cpp:361-382) + breakdown over an event list.
+int ref_breakdown_events(const int* lane, const int* kind, const int* layer, const int* token,
+                         const double* start_us, const double* end_us, int n, double* mean_fr,
+                         double* mean_tpot) {
+    return guard([&] {
+        ExecutorResult r;
+        for (int i = 0; i < n; ++i)
+            r.events.push_back({lane[i] == 0 ? Lane::kCompute : Lane::kCopy,
+                                static_cast<EventKind>(kind[i]), layer[i], start_us[i], end_us[i],
+                                token[i]});
+        auto reps = per_token_reports(r);
+        double acc[3] = {0, 0, 0}, tp = 0;
+        int c = 0;
+        for (auto& rep : reps) {
+            if (rep.events.empty()) continue;
+            BreakdownFractions f = breakdown(rep);
+            acc[0] += f.compute_frac;
+            acc[1] += f.copy_frac;
+            acc[2] += f.idle_frac;
+            tp += rep.tpot;
+            ++c;
+        }
+        for (int k = 0; k < 3; ++k) mean_fr[k] = c ? acc[k] / c : 0;
+        *mean_tpot = c ? tp / c : 0;
+    });
+}
+
 } // extern "C"

@@ -3,8 +3,8 @@
 The product is libsmoe_b200.so (paper_2603_19289_b200/csrc, C ABI in
 include/smoe.h); this package only binds it.
 """
-from .engine import (EXPORTS, GATING, MODE, PRED, CopyEvent, ModelConfig, Session, SmoeError,
-                     load_library)
+from .engine import (EXPORTS, GATING, MODE, PRED, CopyEvent, Event, ModelConfig, Session,
+                     SmoeError, breakdown, load_library, recall_at_k, simulate)
 
-__all__ = ["EXPORTS", "GATING", "MODE", "PRED", "CopyEvent", "ModelConfig", "Session",
-           "SmoeError", "load_library"]
+__all__ = ["EXPORTS", "GATING", "MODE", "PRED", "CopyEvent", "Event", "ModelConfig", "Session",
+           "SmoeError", "breakdown", "load_library", "recall_at_k", "simulate"]

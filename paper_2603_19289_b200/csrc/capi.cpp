@@ -29,6 +29,11 @@ int guard(F&& f) {
     }
 }
 
+}  // namespace
+
+void smoe_set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
 smoe::Session* S(smoe_session* s) {
     if (!s) throw std::invalid_argument("null session");
     return reinterpret_cast<smoe::Session*>(s);
@@ -233,6 +238,20 @@ int smoe_cache_slots(smoe_session* s, int32_t* slots) {
         const auto& c = ss->cfg();
         (void)c;
         *slots = ss->slots_per_layer();
+    });
+}
+
+int smoe_timeline(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t n_steps,
+                  smoe_event* out, int32_t cap, int32_t* n) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        std::vector<smoe::TimelineEvent> ev;
+        S(s)->decode_timeline(mode, tokens, n_steps, ev);
+        const int m = static_cast<int>(ev.size()) < cap ? static_cast<int>(ev.size()) : cap;
+        for (int i = 0; i < m; ++i)
+            out[i] = smoe_event{ev[i].lane, ev[i].kind, ev[i].layer, ev[i].token, ev[i].start_ms,
+                                ev[i].end_ms};
+        *n = static_cast<int32_t>(ev.size());
     });
 }
 

@@ -1011,22 +1011,30 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
     // The side work of layer l joins before the FFN of layer l+1 (which runs
     // the decision it produced) and before the end of the step.
     int pending_join = -1;
+    const bool tl = tl_ && is_main;  // timeline: CUDA events around each phase
     for (int l = 0; l < c.L; ++l) {
+        const int t_attn = tl ? tl_begin(0, 0, l, s) : -1;
         ck(launch_qkv(dm_, st, l, s), "qkv");
         ck(launch_attn(dm_, st, d_attn_scratch_, l, s), "attn");
         ck(launch_wo(dm_, st, l, s), "wo");
+        if (tl) tl_end(t_attn, s);
         int exec_src = 0, s_from_r = 0;
         if (!prefetch) {
+            const int t_gate = tl ? tl_begin(0, 1, l, s) : -1;
             RouterLaunch rl{l, 1, kNone, 0, 1, 0, step_tag};
             ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
+            if (tl) tl_end(t_gate, s);
         } else {
             const int k = kind_at(l);
             if (l == 0) {
+                const int t_gate = tl ? tl_begin(0, 1, l, s) : -1;
                 RouterLaunch rl{0, 1, kNone, 0, 1, 0, step_tag};
                 ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
+                if (tl) tl_end(t_gate, s);
             }
             ck(cudaEventRecord(ev_fork_[l], s), "fork");
             ck(cudaStreamWaitEvent(s_side_, ev_fork_[l], 0), "fork");
+            const int t_side = tl ? tl_begin(0, 1, l, s_side_) : -1;
             if (l == 0) {
                 if (k != kNone) {
                     RouterLaunch rp{0, 0, k, -1, 0, k != kEstPF, step_tag};
@@ -1037,6 +1045,7 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
                 ck(launch_router(dm_, st, ctl_, rl, shadow, s_side_), "router");
             }
             if (k == kEstPF) ck(launch_estimator(dm_, st, ctl_, l, 1, step_tag, s_side_), "estimator");
+            if (tl) tl_end(t_side, s_side_);
             if (pending_join >= 0) ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
             ck(cudaEventRecord(ev_join_[l], s_side_), "join");
             pending_join = l;
@@ -1045,7 +1054,9 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
                 s_from_r = 1;
             }
         }
+        const int t_exp = tl ? tl_begin(0, 2, l, s) : -1;
         ck(launch_ffn(dm_, st, ctl_, l, s, exec_src, s_from_r), "ffn");
+        if (tl) tl_end(t_exp, s);
         if (calibrating) ck(launch_dv_accum(dm_, st, d_dv_sums_, d_dv_counts_, l, s), "dv");
         if (is_main && record && trace_full_ && tr_.cap > 0) ck(launch_trace_y(dm_, st, tr_, l, s), "trace");
     }
@@ -1118,22 +1129,106 @@ void Session::decode(int mode, int n_steps, int use_graph) {
     sync();
 }
 
-void Session::decode_stream(int mode, const int* tokens, int n_steps) {
-    if (n_steps < 0) throw std::invalid_argument("decode: n_steps must be >= 0");
-    if (mode == 1 && pred_kind_ == kNone)
-        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+int Session::tl_begin(int lane, int kind, int layer, cudaStream_t s) {
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    ck(cudaEventRecord(a, s), "event");
+    tl_->ev.push_back({a, b});
+    tl_->meta.push_back({lane, kind, layer, tl_->step, 0.0, 0.0});
+    return static_cast<int>(tl_->meta.size()) - 1;
+}
+
+void Session::tl_end(int idx, cudaStream_t s) { ck(cudaEventRecord(tl_->ev[idx].second, s), "event"); }
+
+void Session::upload_stream(const int* tokens, int n_steps) {
     for (int i = 0; i < n_steps; ++i)
         if (tokens[i] < 0 || tokens[i] >= cfg_.V)
             throw std::invalid_argument("forward_decode: token out of vocab");
-    sync();
-    int pos = 0;
-    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
-    if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
     if (!d_stream_) d_stream_ = static_cast<int*>(dalloc(4ull * (dm_.cap + 2)));
     int step = 0;
     ck(cudaMemcpy(&step, ctl_.step, 4, cudaMemcpyDeviceToHost), "step");
     if (step + n_steps > dm_.cap + 1) throw std::invalid_argument("decode: stream exceeds capacity");
     ck(cudaMemcpy(d_stream_ + step, tokens, 4ull * n_steps, cudaMemcpyHostToDevice), "stream");
+}
+
+// run_offloaded_decode's measured event log (executor.cpp:239-322): compute
+// lane phases from CUDA events around each layer's attention, routing (side
+// stream in prefetch mode) and expert kernels; copy lane from the scheduler's
+// per-request events, assigned to the decode step whose window they start in.
+void Session::decode_timeline(int mode, const int* tokens, int n_steps,
+                              std::vector<TimelineEvent>& out) {
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    sync();
+    int pos = 0;
+    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
+    if (tokens) upload_stream(tokens, n_steps);
+    clear_stats();
+    TlRec rec;
+    tl_ = &rec;
+    try {
+        ck(cudaEventRecord(ev_origin_, s_comp_), "event");
+        for (int i = 0; i < n_steps; ++i) {
+            rec.step = i;
+            enqueue_step(mode, 0, 1, 0, s_comp_, tokens ? 1 : 0);
+            ++steps_;
+        }
+        sync();
+        ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    } catch (...) {
+        tl_ = nullptr;
+        for (auto& ab : rec.ev) {
+            cudaEventDestroy(ab.first);
+            cudaEventDestroy(ab.second);
+        }
+        throw;
+    }
+    tl_ = nullptr;
+    std::vector<double> step_start(n_steps, 1e300);
+    for (size_t i = 0; i < rec.meta.size(); ++i) {
+        float a = 0.0f, b = 0.0f;
+        ck(cudaEventElapsedTime(&a, ev_origin_, rec.ev[i].first), "elapsed");
+        ck(cudaEventElapsedTime(&b, ev_origin_, rec.ev[i].second), "elapsed");
+        TimelineEvent e = rec.meta[i];
+        e.start_ms = a;
+        e.end_ms = b;
+        step_start[e.token] = std::min(step_start[e.token], e.start_ms);
+        out.push_back(e);
+        cudaEventDestroy(rec.ev[i].first);
+        cudaEventDestroy(rec.ev[i].second);
+    }
+    std::map<std::pair<int, int>, double> copy_end;  // (step, layer) -> end of its copy
+    for (const CopyRecord& r : sched_->records()) {
+        if (r.ev < 0 || r.bytes == 0) continue;
+        const double a = event_ms(r.ev, 0), b = event_ms(r.ev, 1);
+        int t = -1;
+        for (int i = 0; i < n_steps; ++i)
+            if (a >= step_start[i] - 1e-6) t = i;
+        out.push_back({1, 3, r.layer, t, a, b});
+        copy_end[{t, r.layer}] = b;
+    }
+    // The expert kernel spins on the copy-ready flag inside its launch; the
+    // reference's expert compute starts after wait_ready (executor.cpp:306-316),
+    // so the compute-lane expert interval starts at max(launch, copy end).
+    for (TimelineEvent& e : out) {
+        if (e.lane != 0 || e.kind != 2) continue;
+        auto it = copy_end.find({e.token, e.layer});
+        if (it != copy_end.end() && it->second > e.start_ms)
+            e.start_ms = std::min(it->second, e.end_ms);
+    }
+}
+
+void Session::decode_stream(int mode, const int* tokens, int n_steps) {
+    if (n_steps < 0) throw std::invalid_argument("decode: n_steps must be >= 0");
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    sync();
+    int pos = 0;
+    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
+    upload_stream(tokens, n_steps);
     cudaGraphExec_t exec = get_graph(mode, 1);
     ck(cudaEventRecord(ev_origin_, s_comp_), "event");
     for (int i = 0; i < n_steps; ++i) {

@@ -52,6 +52,11 @@ struct EstCfg {
     float eps;
 };
 
+struct TimelineEvent {  // MeasuredEvent (executor.hpp:31-37)
+    int lane, kind, layer, token;
+    double start_ms, end_ms;
+};
+
 struct CopyRecord {  // one mailbox request as the copy lane saw it
     int seq, layer, step, hits, misses;
     long long bytes;
@@ -144,6 +149,9 @@ public:
     // argmax (the reference's trace workload, trace.cpp:187-211, fed through
     // speculative_forward).  Greedy argmax is still recorded per step.
     void decode_stream(int mode, const int* tokens, int n_steps);
+    // Non-graph decode recording CUDA events around each layer's attention,
+    // routing and expert phases plus the copy lane (tokens nullable = greedy).
+    void decode_timeline(int mode, const int* tokens, int n_steps, std::vector<TimelineEvent>& out);
     int step_host(int mode, int token, float* logits_out);  // host token in, logits out
     void calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out, long long* c_out);
 
@@ -255,6 +263,16 @@ private:
     std::map<long long, int> graph_kernels_;
     cudaGraphExec_t get_graph(int mode, int stream = 0);
     int* d_stream_ = nullptr;
+    // timeline recording (decode_timeline): event pairs per (step, layer, phase)
+    struct TlRec {
+        std::vector<TimelineEvent> meta;                      // times filled after sync
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // per meta entry
+        int step = 0;
+    };
+    TlRec* tl_ = nullptr;
+    int tl_begin(int lane, int kind, int layer, cudaStream_t s);
+    void tl_end(int idx, cudaStream_t s);
+    void upload_stream(const int* tokens, int n_steps);
     void drop_graphs();
 };
 

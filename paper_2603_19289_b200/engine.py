@@ -31,6 +31,7 @@ EXPORTS = [
     "smoe_cache_slots", "smoe_debug_state", "smoe_clear_stats", "smoe_profile_kernels",
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
+    "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
 ]
 
 
@@ -50,6 +51,13 @@ class _Options(C.Structure):
 class _EstConfig(C.Structure):
     _fields_ = [("d", C.c_int32), ("m", C.c_int32), ("n", C.c_int32), ("experts", C.c_int32),
                 ("layers", C.c_int32), ("eps", C.c_float)]
+
+
+class Event(C.Structure):
+    """MeasuredEvent (executor.hpp:31-37): lane 0 compute / 1 copy; kind 0 attn /
+    1 gate / 2 expert / 3 copy."""
+    _fields_ = [("lane", C.c_int32), ("kind", C.c_int32), ("layer", C.c_int32),
+                ("token", C.c_int32), ("start_ms", C.c_double), ("end_ms", C.c_double)]
 
 
 class CopyEvent(C.Structure):
@@ -99,6 +107,42 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 class SmoeError(RuntimeError):
     pass
+
+
+def simulate(t_attn, t_gate, t_expert, t_copy, mode: str, cold_start_copy: float = -1.0):
+    """simulate_on_demand / simulate_prefetch + breakdown + analytic_improvement
+    (schedule.cpp:92-217), host C++ — no GPU needed."""
+    lib = load_library()
+    arr = [np.ascontiguousarray(a, np.float64) for a in (t_attn, t_gate, t_expert, t_copy)]
+    tpot = C.c_double()
+    an = C.c_double()
+    fr = np.zeros(3, np.float64)
+    _check(lib.smoe_simulate(len(arr[0]), *[_p(a) for a in arr], C.c_double(cold_start_copy),
+                             MODE[mode], C.byref(tpot), _p(fr), C.byref(an)))
+    return tpot.value, fr, an.value
+
+
+def breakdown(events) -> tuple:
+    """per_token_reports + breakdown (executor.cpp:361-382, schedule.cpp:205-217):
+    mean {compute, copy, idle} fractions and mean TPOT over decode steps."""
+    lib = load_library()
+    n = len(events)
+    arr = (Event * max(n, 1))(*events)
+    fr = np.zeros(3, np.float64)
+    tp = C.c_double()
+    _check(lib.smoe_breakdown(arr, n, _p(fr), C.byref(tp)))
+    return fr, tp.value
+
+
+def recall_at_k(pred, truth):
+    """recall_at_k (metrics.cpp:9-20) and rank_alignment (metrics.cpp:22-28)."""
+    lib = load_library()
+    p = np.ascontiguousarray(pred, np.int32)
+    t = np.ascontiguousarray(truth, np.int32)
+    r = C.c_double()
+    m = np.zeros(len(p), np.int32)
+    _check(lib.smoe_recall_at_k(_p(p), _p(t), len(p), C.byref(r), _p(m)))
+    return r.value, m.astype(bool)
 
 
 def _check(rc):
@@ -290,6 +334,14 @@ class Session:
         n = C.c_int32()
         _check(self.lib.smoe_kernels_per_step(self._h, MODE[mode], C.byref(n)))
         return n.value
+
+    def timeline(self, mode: str, n_steps: int, tokens=None, cap: int = 1 << 20):
+        """Decode n_steps with a measured lane timeline (list of Event)."""
+        t = None if tokens is None else np.ascontiguousarray(tokens, np.int32)
+        arr = (Event * cap)()
+        n = C.c_int32()
+        _check(self.lib.smoe_timeline(self._h, MODE[mode], _p(t), n_steps, arr, cap, C.byref(n)))
+        return [arr[i] for i in range(min(n.value, cap))]
 
     def copy_events(self, cap: int = 65536):
         arr = (CopyEvent * cap)()

@@ -431,3 +431,35 @@ def test_expert_parallel_two_ranks_bit_exact(lib, toy_oracle, mode):
         assert all(e.hits + e.misses <= TOY["top_k"] for e in ev)
     for s in ranks:
         s.close()
+
+
+def test_timeline_event_log(lib, toy_oracle):
+    """smoe_timeline: the measured lane log of run_offloaded_decode — 3 compute
+    events per layer per step, copy events serialised, breakdown sums to 1, and
+    the decode itself is unchanged (tokens equal the graph path's)."""
+    from paper_2603_19289_b200 import breakdown
+    orc, om, table, est = toy_oracle
+    forced = np.array([(17 * i + 5) % TOY["vocab"] for i in range(6)], np.int32)
+    s = session(TOY, cache_fraction=0.25)
+    s.load_default_vectors(np.array(table.d))
+    s.set_predictor("router-pf")
+    for mode in ("on_demand", "prefetch"):
+        S = 3 + 6
+        s.reset(S, False)
+        s.prefill([4, 5, 6])
+        ev = s.timeline(mode, 6, forced)
+        toks_tl = s.tokens(S)
+        s.reset(S, False)
+        s.prefill([4, 5, 6])
+        s.decode_stream(mode, forced)
+        assert np.array_equal(toks_tl, s.tokens(S))
+        comp = [e for e in ev if e.lane == 0]
+        per_step = TOY["layers"] * 3 + (1 if mode == "prefetch" else 0)  # + layer-0 predictor
+        assert len(comp) == 6 * per_step
+        assert all(e.end_ms >= e.start_ms for e in ev)
+        cp = sorted((e.start_ms, e.end_ms) for e in ev if e.lane == 1)
+        for (a0, a1), (b0, b1) in zip(cp, cp[1:]):
+            assert b0 >= a1 - 1e-3
+        fr, tp = breakdown(ev)
+        assert abs(fr.sum() - 1.0) < 1e-9 and tp > 0
+    s.close()
