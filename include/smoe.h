@@ -146,7 +146,9 @@ int smoe_cache_slots(smoe_session* s, int32_t* slots);
  * shard), then connects to the exchange buffers and arrival counters of all
  * ranks: either raw device pointers (ranks sharing a process; smoe_ep_buffers
  * gives each rank's own) or CUDA IPC handles (one process per GPU; 128 bytes
- * per rank from smoe_ep_ipc_handles, exchanged by the caller, e.g. with
+ * per rank from smoe_ep_ipc_handles — the handle of the allocation holding
+ * the rank's exchange region plus the region's offset in it, since a peer's
+ * opened pointer is the allocation base — exchanged by the caller, e.g. with
  * torch.distributed).  After connecting, every decode step combines expert
  * outputs across ranks through peer memory; results equal the single-GPU path. */
 int smoe_ep_buffers(smoe_session* s, void** xbuf, void** counters);

@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <random>
+#include <unistd.h>
 #include <string>
 
 namespace smoe {
@@ -79,6 +81,22 @@ WriteValueFn write_value_fn() {
             q != cudaDriverEntryPointSuccess || !p)
             throw std::runtime_error("cuStreamWriteValue32 entry point unavailable");
         return reinterpret_cast<WriteValueFn>(p);
+    }();
+    return fn;
+}
+
+// cuMemGetAddressRange: a cudaMalloc'd pointer may live inside a larger
+// driver allocation; CUDA IPC handles name the allocation, and the peer's
+// opened pointer is its base, so the offset must travel with the handle.
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+    static AddrRangeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            throw std::runtime_error("cuMemGetAddressRange entry point unavailable");
+        return reinterpret_cast<AddrRangeFn>(p);
     }();
     return fn;
 }
@@ -311,10 +329,27 @@ void CopyScheduler::handle(const MailboxEntry& e) {
 
 // ---------------------------------------------------------------- Session --
 
+// Host<->device transfers and memsets outside the decode graph are ordered on
+// the compute stream.  The streams are non-blocking, so a legacy-stream
+// cudaMemcpy/cudaMemset is NOT ordered before their kernels: a pageable H2D
+// cudaMemcpy may return before its DMA lands, and a kernel could read the old
+// bytes (seen as wrong prompt tokens when another process time-sliced the GPU).
+void Session::h2d(void* dst, const void* src, size_t n, const char* what) {
+    ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s_comp_), what);
+    ck(cudaStreamSynchronize(s_comp_), what);  // the host buffer may be reused on return
+}
+void Session::d2h(void* dst, const void* src, size_t n, const char* what) {
+    ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s_comp_), what);
+    ck(cudaStreamSynchronize(s_comp_), what);
+}
+void Session::dset(void* p, int v, size_t n, const char* what) {
+    ck(cudaMemsetAsync(p, v, n, s_comp_), what);
+}
+
 void* Session::dalloc(size_t bytes) {
     void* p = nullptr;
     ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), "cudaMalloc");
-    ck(cudaMemset(p, 0, bytes < 256 ? 256 : bytes), "cudaMemset");
+    dset(p, 0, bytes < 256 ? 256 : bytes, "cudaMemset");
     dev_allocs_.push_back(p);
     return p;
 }
@@ -428,9 +463,9 @@ void Session::alloc() {
     d_moe_gain_ = static_cast<float*>(dalloc(4ull * L * H));
     {
         std::vector<float> ones(static_cast<size_t>(L) * H, 1.0f);  // model.cpp:126-131
-        ck(cudaMemcpy(d_final_gain_, ones.data(), 4ull * H, cudaMemcpyHostToDevice), "gain");
-        ck(cudaMemcpy(d_attn_gain_, ones.data(), 4ull * L * H, cudaMemcpyHostToDevice), "gain");
-        ck(cudaMemcpy(d_moe_gain_, ones.data(), 4ull * L * H, cudaMemcpyHostToDevice), "gain");
+        h2d(d_final_gain_, ones.data(), 4ull * H, "gain");
+        h2d(d_attn_gain_, ones.data(), 4ull * L * H, "gain");
+        h2d(d_moe_gain_, ones.data(), 4ull * L * H, "gain");
     }
     // RoPE table with the host libm, exactly model.cpp:311-316.
     {
@@ -444,14 +479,29 @@ void Session::alloc() {
                 rope[(static_cast<size_t>(p) * (D / 2) + i) * 2 + 1] = static_cast<float>(std::sin(angle));
             }
         d_rope_ = static_cast<float*>(dalloc(rope.size() * 4));
-        ck(cudaMemcpy(d_rope_, rope.data(), rope.size() * 4, cudaMemcpyHostToDevice), "rope");
+        h2d(d_rope_, rope.data(), rope.size() * 4, "rope");
     }
     d_slots_ = static_cast<uint16_t*>(dalloc(2ull * L * C_ * m.expert_elems));
     d_slot_of_ = static_cast<int*>(dalloc(4ull * L * E));
-    ck(cudaMemset(d_slot_of_, 0xff, 4ull * L * E), "memset");
+    dset(d_slot_of_, 0xff, 4ull * L * E, "memset");
     d_dv_ = static_cast<float*>(dalloc(4ull * L * E * H));
-    d_xbuf_ = static_cast<float*>(dalloc(4ull * 2 * K * m.Hp));
-    d_cnt_ = static_cast<int*>(dalloc(4ull * L));
+    // EP exchange region (shared with peers through one CUDA IPC handle):
+    // [tag 256 B | arrival counters L ints, padded to 256 B | exchange buffer [2][K][Hp] f32]
+    // The tag (a random 128-bit value) lets a peer verify, and if need be
+    // find, the region inside the block its cudaIpcOpenMemHandle mapped:
+    // small cudaMallocs are sub-allocated from shared driver blocks.
+    {
+        const size_t cnt_bytes = (4ull * L + 255) / 256 * 256;
+        unsigned char* reg = static_cast<unsigned char*>(dalloc(256 + cnt_bytes + 4ull * 2 * K * m.Hp));
+        std::random_device rd;
+        ep_tag_[0] = 0x31585045454f4d53ull;  // "SMOEEPX1"
+        ep_tag_[1] = (static_cast<uint64_t>(rd()) << 32 ^ rd()) ^ reinterpret_cast<uintptr_t>(reg) ^
+                     static_cast<uint64_t>(getpid()) << 40;
+        h2d(reg, ep_tag_, 16, "ep tag");
+        d_ep_region_ = reg;
+        d_cnt_ = reinterpret_cast<int*>(reg + 256);
+        d_xbuf_ = reinterpret_cast<float*>(reg + 256 + cnt_bytes);
+    }
     d_epoch_ = static_cast<int*>(dalloc(4ull * L));
     ctl_.ep.rank = 0;
     ctl_.ep.world = 1;  // EP activates at ep_connect(); until then this rank runs everything it owns
@@ -535,6 +585,7 @@ void Session::alloc() {
 
     store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * el_max_, m.expert_elems);
     cache_ = std::make_unique<SlotCache>(L, E, C_);
+    ck(cudaDeviceSynchronize(), "alloc");
     reset(0, 0);
 }
 
@@ -553,12 +604,23 @@ void Session::ep_buffers(void** xbuf, void** cnt) {
     *cnt = d_cnt_;
 }
 
+// 128 bytes per rank: the IPC handle of the exchange region's allocation
+// (64 B), the region's offset in it as this process sees it (8 B), the
+// buffer's offset in the region (8 B) and the region's 16-byte tag.
 void Session::ep_ipc_handles(unsigned char* out128) {
-    cudaIpcMemHandle_t a, b;
-    ck(cudaIpcGetMemHandle(&a, d_xbuf_), "ipc handle");
-    ck(cudaIpcGetMemHandle(&b, d_cnt_), "ipc handle");
+    cudaIpcMemHandle_t a;
+    ck(cudaIpcGetMemHandle(&a, d_ep_region_), "ipc handle");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (addr_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(d_ep_region_)) != CUDA_SUCCESS)
+        throw std::runtime_error("cuMemGetAddressRange failed");
+    const unsigned long long off = reinterpret_cast<CUdeviceptr>(d_ep_region_) - base;
+    const unsigned long long xoff = reinterpret_cast<unsigned char*>(d_xbuf_) - d_ep_region_;
+    std::memset(out128, 0, 128);
     std::memcpy(out128, &a, 64);
-    std::memcpy(out128 + 64, &b, 64);
+    std::memcpy(out128 + 64, &off, 8);
+    std::memcpy(out128 + 72, &xoff, 8);
+    std::memcpy(out128 + 80, ep_tag_, 16);
 }
 
 // Every rank passes the exchange buffers / counters of all ranks (its own at
@@ -575,9 +637,35 @@ void Session::ep_connect(void* const* xbufs, void* const* cnts) {
     ctl_.ep.cnt[opts_.ep_rank] = d_cnt_;
     ctl_.ep.rank = opts_.ep_rank;
     ctl_.ep.world = W;
-    ck(cudaMemset(d_cnt_, 0, 4ull * cfg_.L), "ep reset");
-    ck(cudaMemset(d_epoch_, 0, 4ull * cfg_.L), "ep reset");
+    dset(d_cnt_, 0, 4ull * cfg_.L, "ep reset");
+    dset(d_epoch_, 0, 4ull * cfg_.L, "ep reset");
+    // the reset must land before any peer (released by the caller's barrier)
+    // starts adding to these counters
+    ck(cudaDeviceSynchronize(), "ep reset sync");
     drop_graphs();
+}
+
+// The peer's region: at `off` from the mapped base when the mapping starts
+// where the peer's allocation does; otherwise found by its tag, scanning the
+// mapped block at 256-byte steps (done once, at connect time).
+unsigned char* Session::locate_ep_region(unsigned char* base, unsigned long long off,
+                                         const unsigned long long tag[2]) {
+    unsigned long long got[2] = {0, 0};
+    CUdeviceptr b0 = 0;
+    size_t size = 0;
+    if (addr_range_fn()(&b0, &size, reinterpret_cast<CUdeviceptr>(base)) != CUDA_SUCCESS)
+        throw std::runtime_error("cuMemGetAddressRange failed on an IPC mapping");
+    unsigned char* lo = reinterpret_cast<unsigned char*>(b0);
+    if (base + off + 16 <= lo + size) {
+        d2h(got, base + off, 16, "ep tag read");
+        if (got[0] == tag[0] && got[1] == tag[1]) return base + off;
+    }
+    if (size > (1ull << 31)) return nullptr;
+    std::vector<unsigned long long> blk(size / 8);
+    d2h(blk.data(), lo, size / 8 * 8, "ep block read");
+    for (size_t i = 0; i + 1 < blk.size(); i += 32)
+        if (blk[i] == tag[0] && blk[i + 1] == tag[1]) return lo + i * 8;
+    return nullptr;
 }
 
 void Session::ep_connect_ipc(const unsigned char* handles) {
@@ -589,13 +677,21 @@ void Session::ep_connect_ipc(const unsigned char* handles) {
             cn[p] = d_cnt_;
             continue;
         }
-        cudaIpcMemHandle_t a, b;
+        cudaIpcMemHandle_t a;
+        unsigned long long off = 0, xoff = 0, tag[2];
         std::memcpy(&a, handles + p * 128, 64);
-        std::memcpy(&b, handles + p * 128 + 64, 64);
-        ck(cudaIpcOpenMemHandle(&xb[p], a, cudaIpcMemLazyEnablePeerAccess), "ipc open");
-        ck(cudaIpcOpenMemHandle(&cn[p], b, cudaIpcMemLazyEnablePeerAccess), "ipc open");
-        ipc_opened_.push_back(xb[p]);
-        ipc_opened_.push_back(cn[p]);
+        std::memcpy(&off, handles + p * 128 + 64, 8);
+        std::memcpy(&xoff, handles + p * 128 + 72, 8);
+        std::memcpy(tag, handles + p * 128 + 80, 16);
+        void* base = nullptr;
+        ck(cudaIpcOpenMemHandle(&base, a, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        ipc_opened_.push_back(base);
+        unsigned char* region = locate_ep_region(static_cast<unsigned char*>(base), off, tag);
+        if (!region)
+            throw std::runtime_error("ep_connect_ipc: rank " + std::to_string(p) +
+                                     "'s exchange region not found in the mapped IPC block");
+        cn[p] = region + 256;
+        xb[p] = region + xoff;
     }
     ep_connect(xb.data(), cn.data());
 }
@@ -644,7 +740,7 @@ void Session::set_cache_fraction(float frac) {
     dm_.C = C;
     d_slots_ = static_cast<uint16_t*>(dalloc(2ull * cfg_.L * C_ * dm_.expert_elems));
     dm_.slots = d_slots_;
-    ck(cudaMemset(d_slot_of_, 0xff, 4ull * cfg_.L * cfg_.E), "memset");
+    dset(d_slot_of_, 0xff, 4ull * cfg_.L * cfg_.E, "memset");
     cache_ = std::make_unique<SlotCache>(cfg_.L, cfg_.E, C_);
     drop_graphs();
 }
@@ -708,7 +804,7 @@ void Session::init_weights_seeded() {
     cache_->invalidate();
     ctl_.resident = 0;
     drop_graphs();
-    ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
+    dset(d_slot_of_, 0xff, 4ull * c.L * c.E, "memset");
 }
 
 void Session::load_tensor(const std::string& name, const float* data, long long n) {
@@ -719,7 +815,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
         if (n != want) throw std::invalid_argument("load_tensor: " + name + " has wrong size");
     };
     auto upload16 = [&](uint16_t* dst, const std::vector<uint16_t>& v) {
-        ck(cudaMemcpy(dst, v.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
+        h2d(dst, v.data(), v.size() * 2, "upload");
     };
     if (name == "embedding") {
         need(static_cast<long long>(c.V) * c.H);
@@ -737,7 +833,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
     }
     if (name == "final_norm_gain") {
         need(c.H);
-        ck(cudaMemcpy(d_final_gain_, data, 4ull * c.H, cudaMemcpyHostToDevice), "upload");
+        h2d(d_final_gain_, data, 4ull * c.H, "upload");
         return;
     }
     int l;
@@ -747,7 +843,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
     if (rest == "attn_norm_gain" || rest == "moe_norm_gain") {
         need(c.H);
         float* dst = (rest == "attn_norm_gain" ? d_attn_gain_ : d_moe_gain_) + static_cast<long long>(l) * c.H;
-        ck(cudaMemcpy(dst, data, 4ull * c.H, cudaMemcpyHostToDevice), "upload");
+        h2d(dst, data, 4ull * c.H, "upload");
         drop_graphs();
         return;
     }
@@ -755,7 +851,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
         need(static_cast<long long>(c.D) * c.H);
         std::vector<uint16_t> v(m.qkv_stride);
         uint16_t* dst = d_wqkv_ + l * m.qkv_stride;
-        ck(cudaMemcpy(v.data(), dst, v.size() * 2, cudaMemcpyDeviceToHost), "download");
+        d2h(v.data(), dst, v.size() * 2, "download");
         const int off = rest == "wq" ? 0 : rest == "wk" ? c.D : 2 * c.D;
         tile_write_bf16(v.data(), data, c.D, c.H, c.H, 1, 0, off);
         upload16(dst, v);
@@ -794,7 +890,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
         cache_->invalidate();
         ctl_.resident = 0;
         drop_graphs();
-        ck(cudaMemset(d_slot_of_, 0xff, 4ull * c.L * c.E), "memset");
+        dset(d_slot_of_, 0xff, 4ull * c.L * c.E, "memset");
         return;
     }
     throw std::invalid_argument("load_tensor: unknown tensor " + name);
@@ -802,7 +898,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
 
 void Session::load_default_vectors(const float* d) {
     sync();
-    ck(cudaMemcpy(d_dv_, d, 4ull * cfg_.L * cfg_.E * cfg_.H, cudaMemcpyHostToDevice), "dv upload");
+    h2d(d_dv_, d, 4ull * cfg_.L * cfg_.E * cfg_.H, "dv upload");
     have_dv_ = true;
 }
 
@@ -848,7 +944,7 @@ void Session::load_estimator(const EstCfg& e, const float* flat) {
         mk(st_);
         mk(sh_);
     }
-    ck(cudaMemcpy(d_est_, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice), "est upload");
+    h2d(d_est_, buf.data(), buf.size() * 4, "est upload");
     est_ = e;
     DevModel& m = dm_;
     m.est_d = e.d;
@@ -912,14 +1008,14 @@ void Session::sync() {
 
 void Session::check_device_error() {
     int err = 0;
-    ck(cudaMemcpy(&err, ctl_.error, 4, cudaMemcpyDeviceToHost), "error flag");
+    d2h(&err, ctl_.error, 4, "error flag");
     const std::string se = sched_ ? sched_->error() : std::string();
     if (!se.empty()) {
-        cudaMemset(ctl_.error, 0, 4);
+        cudaMemsetAsync(ctl_.error, 0, 4, s_comp_);
         throw std::runtime_error(se);
     }
     if (err != 0) {
-        cudaMemset(ctl_.error, 0, 4);
+        cudaMemsetAsync(ctl_.error, 0, 4, s_comp_);
         if (err >= 1000 && err < 2000)
             throw std::runtime_error("deadlock suspected: compute waited " +
                                      std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
@@ -933,10 +1029,10 @@ void Session::reset(int max_steps, int trace_full) {
     const ModelCfg& c = cfg_;
     int zero = 0;
     for (DevState* st : {&st_, &sh_}) {
-        ck(cudaMemcpy(st->pos, &zero, 4, cudaMemcpyHostToDevice), "reset");
-        ck(cudaMemset(st->counters, 0, 256), "reset");
+        h2d(st->pos, &zero, 4, "reset");
+        dset(st->counters, 0, 256, "reset");
     }
-    ck(cudaMemcpy(ctl_.step, &zero, 4, cudaMemcpyHostToDevice), "reset");
+    h2d(ctl_.step, &zero, 4, "reset");
     // trace buffers
     if (max_steps != max_steps_ || trace_full != trace_full_ || !tr_.step) {
         auto drop = [&](void* p) {
@@ -979,10 +1075,10 @@ void Session::reset(int max_steps, int trace_full) {
         trace_full_ = trace_full;
         drop_graphs();
     }
-    ck(cudaMemset(tr_.step, 0, 4), "reset");
+    dset(tr_.step, 0, 4, "reset");
     if (max_steps > 0) {
         const long long n = static_cast<long long>(max_steps) * c.L * c.K * 4;
-        ck(cudaMemset(tr_.id_pred, 0xff, n), "reset");
+        dset(tr_.id_pred, 0xff, n, "reset");
     }
     steps_ = 0;
     n_step_events_ = 0;
@@ -1091,9 +1187,9 @@ void Session::prefill(const int* tokens, int n) {
     for (int i = 0; i < n; ++i)
         if (tokens[i] < 0 || tokens[i] >= cfg_.V) throw std::invalid_argument("forward_decode: token out of vocab");
     int pos = 0;
-    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    d2h(&pos, st_.pos, 4, "pos");
     if (pos + n >= dm_.cap) throw std::invalid_argument("prefill: KV capacity exceeded");
-    ck(cudaMemcpy(d_prompt_tok_, tokens, 4ull * n, cudaMemcpyHostToDevice), "prompt");
+    h2d(d_prompt_tok_, tokens, 4ull * n, "prompt");
     for (int i = 0; i < n; ++i) {
         ck(launch_embed(dm_, st_, d_prompt_tok_ + i, s_comp_), "embed");
         enqueue_pass(st_, 0, 0, 0, -1, 1, s_comp_);
@@ -1112,7 +1208,7 @@ void Session::decode(int mode, int n_steps, int use_graph) {
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
     sync();
     int pos = 0;
-    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    d2h(&pos, st_.pos, 4, "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
     cudaGraphExec_t exec = use_graph ? get_graph(mode) : nullptr;
     ck(cudaEventRecord(ev_origin_, s_comp_), "event");
@@ -1147,9 +1243,9 @@ void Session::upload_stream(const int* tokens, int n_steps) {
             throw std::invalid_argument("forward_decode: token out of vocab");
     if (!d_stream_) d_stream_ = static_cast<int*>(dalloc(4ull * (dm_.cap + 2)));
     int step = 0;
-    ck(cudaMemcpy(&step, ctl_.step, 4, cudaMemcpyDeviceToHost), "step");
+    d2h(&step, ctl_.step, 4, "step");
     if (step + n_steps > dm_.cap + 1) throw std::invalid_argument("decode: stream exceeds capacity");
-    ck(cudaMemcpy(d_stream_ + step, tokens, 4ull * n_steps, cudaMemcpyHostToDevice), "stream");
+    h2d(d_stream_ + step, tokens, 4ull * n_steps, "stream");
 }
 
 // run_offloaded_decode's measured event log (executor.cpp:239-322): compute
@@ -1162,7 +1258,7 @@ void Session::decode_timeline(int mode, const int* tokens, int n_steps,
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
     sync();
     int pos = 0;
-    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    d2h(&pos, st_.pos, 4, "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
     if (tokens) upload_stream(tokens, n_steps);
     clear_stats();
@@ -1226,7 +1322,7 @@ void Session::decode_stream(int mode, const int* tokens, int n_steps) {
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
     sync();
     int pos = 0;
-    ck(cudaMemcpy(&pos, st_.pos, 4, cudaMemcpyDeviceToHost), "pos");
+    d2h(&pos, st_.pos, 4, "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
     upload_stream(tokens, n_steps);
     cudaGraphExec_t exec = get_graph(mode, 1);
@@ -1282,7 +1378,7 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
         }
     }
     int* d_toks = static_cast<int*>(dalloc(4ull * ntok));
-    ck(cudaMemcpy(d_toks, toks.data(), 4ull * ntok, cudaMemcpyHostToDevice), "tokens");
+    h2d(d_toks, toks.data(), 4ull * ntok, "tokens");
     int zero = 0;
     for (long long i = 0; i < ntok; ++i) {
         if (i % seq_len == 0) ck(cudaMemcpyAsync(st_.pos, &zero, 4, cudaMemcpyHostToDevice, s_comp_), "pos");
@@ -1292,8 +1388,8 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
     }
     ck(launch_dv_freeze(d_dv_sums_, d_dv_counts_, d_dv_, LE, c.H, s_comp_), "freeze");
     sync();
-    if (d_out) ck(cudaMemcpy(d_out, d_dv_, 4ull * LE * c.H, cudaMemcpyDeviceToHost), "dv");
-    if (c_out) ck(cudaMemcpy(c_out, d_dv_counts_, 8ull * LE, cudaMemcpyDeviceToHost), "counts");
+    if (d_out) d2h(d_out, d_dv_, 4ull * LE * c.H, "dv");
+    if (c_out) d2h(c_out, d_dv_counts_, 8ull * LE, "counts");
     for (void* p : {(void*)d_dv_sums_, (void*)d_dv_counts_, (void*)d_toks})
         for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
             if (*it == p) {
@@ -1303,7 +1399,7 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
             }
     d_dv_sums_ = nullptr;
     d_dv_counts_ = nullptr;
-    ck(cudaMemcpy(st_.pos, &zero, 4, cudaMemcpyHostToDevice), "pos");
+    h2d(st_.pos, &zero, 4, "pos");
     have_dv_ = true;
 }
 
@@ -1439,6 +1535,7 @@ double Session::measure_link(int n_copies) {
 void Session::debug_state(int* out, int cap) {
     std::vector<int> v;
     int x = 0;
+    cudaStreamSynchronize(s_comp_);
     cudaMemcpy(&x, ctl_.req_counter, 4, cudaMemcpyDeviceToHost);
     v.push_back(x);
     cudaMemcpy(&x, ctl_.error, 4, cudaMemcpyDeviceToHost);
@@ -1457,7 +1554,7 @@ void Session::debug_state(int* out, int cap) {
 
 void Session::read_tokens(int* out, int n) {
     sync();
-    ck(cudaMemcpy(out, ctl_.tokens_out, 4ull * n, cudaMemcpyDeviceToHost), "tokens");
+    d2h(out, ctl_.tokens_out, 4ull * n, "tokens");
 }
 
 void Session::read_trace(const char* field, void* out, long long n) {
@@ -1480,7 +1577,7 @@ void Session::read_trace(const char* field, void* out, long long n) {
     else if (f == "logits") src = tr_.logits;
     else throw std::invalid_argument("read_trace: unknown field " + f);
     if (!src) throw std::invalid_argument("read_trace: field not captured (trace_full=0?)");
-    ck(cudaMemcpy(out, src, n * esz, cudaMemcpyDeviceToHost), "trace");
+    d2h(out, src, n * esz, "trace");
 }
 
 std::vector<double> Session::token_ms() {

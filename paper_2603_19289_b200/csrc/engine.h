@@ -180,6 +180,8 @@ public:
     void ep_buffers(void** xbuf, void** cnt);
     void ep_ipc_handles(unsigned char* out128);
     void ep_connect(void* const* xbufs, void* const* cnts);
+    unsigned char* locate_ep_region(unsigned char* base, unsigned long long off,
+                                    const unsigned long long tag[2]);
     void ep_connect_ipc(const unsigned char* handles);  // world x 128 bytes
     void debug_state(int* out, int cap);
     void clear_stats();
@@ -219,6 +221,9 @@ private:
     // device allocations (owned)
     std::vector<void*> dev_allocs_;
     void* dalloc(size_t bytes);
+    void h2d(void* dst, const void* src, size_t n, const char* what);
+    void d2h(void* dst, const void* src, size_t n, const char* what);
+    void dset(void* p, int v, size_t n, const char* what);
     uint16_t *d_emb_ = nullptr, *d_unemb_ = nullptr, *d_wqkv_ = nullptr, *d_wo_ = nullptr,
              *d_gate_ = nullptr, *d_slots_ = nullptr;
     float *d_final_gain_ = nullptr, *d_attn_gain_ = nullptr, *d_moe_gain_ = nullptr,
@@ -231,6 +236,8 @@ private:
     int* d_hybrid_ = nullptr;
     int* d_prompt_tok_ = nullptr;
     int el_max_ = 0;                       // store blocks per layer = ceil(E / ep_world)
+    unsigned char* d_ep_region_ = nullptr;  // EP region: tag | counters | exchange buffer
+    unsigned long long ep_tag_[2] = {0, 0};
     float* d_xbuf_ = nullptr;              // EP exchange buffer [2][K][Hp]
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]
     int* d_epoch_ = nullptr;               // EP combines done [L]

@@ -43,12 +43,14 @@ def _rank(rank, world, port, q):
         s.reset(S, True)
         s.prefill([1, 2, 3])
         s.decode_stream("prefetch", forced)
-        ok = (np.array_equal(s.tokens(S)[2:], want.tokens)
-              and np.array_equal(s.trace("m", S), want.m)
-              and np.array_equal(s.trace("logits", S), want.final_logits))
+        bad = [name for name, got, w in (("tokens", s.tokens(S)[2:], want.tokens),
+                                         ("m", s.trace("m", S), want.m),
+                                         ("logits", s.trace("logits", S), want.final_logits))
+               if not np.array_equal(got, w)]
+        ok = True if not bad else f"mismatch {bad}: tokens {s.tokens(S).tolist()} want {want.tokens.tolist()}"
         dist.barrier()
         s.close()
-        q.put((rank, bool(ok)))
+        q.put((rank, ok))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
