@@ -550,6 +550,8 @@ void Session::alloc() {
         st.pos = static_cast<int*>(dalloc(4));
         st.token = static_cast<int*>(dalloc(4));
         st.counters = static_cast<int*>(dalloc(4 * 64));
+        st.ssq_x = static_cast<double*>(dalloc(8ull * (L + 1) * (m.Hp / 32)));
+        st.ssq_r = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.est_z = st.est_act = st.est_xn = nullptr;
     };
     mk_state(st_);

@@ -14,390 +14,12 @@
 // rounding of the result except at measure-zero midpoints (reported by the
 // parity tests as exact-match fractions).
 #include "kernels.h"
+#include "smoe_chain.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace smoe {
-
-// ---------------------------------------------------------------- helpers --
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-// Programmatic dependent launch: let the next kernel in the stream start its
-// prologue (barrier init, static weight prefetch) while this one runs; every
-// kernel calls pdl_wait() before touching activations written upstream.
-__device__ __forceinline__ void pdl_trigger() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-// Optional phase timing (build with -DSMOE_PHASES; tools/phase_run.py): block
-// (0,0)'s timeline between PHASE() marks, printed once per launch.
-#ifdef SMOE_PHASES
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#define PHASE_DECL \
-    unsigned long long ph_[10];  \
-    int nph_ = 0;
-#define PHASE()                                  \
-    do {                                         \
-        if (nph_ < 10) ph_[nph_++] = gtimer();   \
-    } while (0)
-#define PHASE_DUMP(name)                                                                   \
-    do {                                                                                   \
-        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                      \
-            printf("%s:", name);                                                           \
-            for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);      \
-            printf(" | %llu\n", ph_[nph_ - 1] - ph_[0]);                                   \
-        }                                                                                  \
-    } while (0)
-#else
-#define PHASE_DECL
-#define PHASE() \
-    do {        \
-    } while (0)
-#define PHASE_DUMP(name) \
-    do {                 \
-    } while (0)
-#endif
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ float bf2f(uint16_t b) {
-    return __uint_as_float(static_cast<uint32_t>(b) << 16);
-}
-__device__ __forceinline__ float to_f(uint16_t b) { return bf2f(b); }
-__device__ __forceinline__ float to_f(float f) { return f; }
-
-// numerics.cpp:86-89 — silu in f64, rounded to f32.
-__device__ __forceinline__ float silu_ref(float x) {
-    const double xd = static_cast<double>(x);
-    return static_cast<float>(xd / (1.0 + exp(-xd)));
-}
-
-// Deterministic block reduction of a per-thread double (tree order fixed by
-// blockDim).  Returns the same value in every thread.
-__device__ double block_sum_d(double v, double* red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    if ((threadIdx.x & 31) == 0) red[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (int i = 0; i < nw; ++i) t += red[i];
-    __syncthreads();
-    return t;
-}
-
-__device__ float block_max_f(float v, float* red) {
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_down_sync(0xffffffffu, v, o));
-    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    if ((threadIdx.x & 31) == 0) red[w] = v;
-    __syncthreads();
-    float t = red[0];
-    for (int i = 1; i < nw; ++i) t = fmaxf(t, red[i]);
-    __syncthreads();
-    return t;
-}
-
-// rms_norm (numerics.cpp:72-84): out[i] = (v[i] * scale) * gain[i],
-// scale = f32(1 / sqrt(sum_f64(v^2) / n + eps)).  Whole block participates;
-// v, gain, out are 16-byte aligned shared arrays and n % 4 == 0 (H % 8 == 0 is
-// validated).  The f64 sum runs as 4 independent partial sums per thread
-// (fixed order: the reduction tree is deterministic).
-__device__ void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
-                               double* red) {
-    const float4* v4 = reinterpret_cast<const float4*>(v);
-    const float4* g4 = reinterpret_cast<const float4*>(gain);
-    float4* o4 = reinterpret_cast<float4*>(out);
-    const int n4 = n >> 2;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-        const float4 t = v4[i];
-        a0 += static_cast<double>(t.x) * static_cast<double>(t.x);
-        a1 += static_cast<double>(t.y) * static_cast<double>(t.y);
-        a2 += static_cast<double>(t.z) * static_cast<double>(t.z);
-        a3 += static_cast<double>(t.w) * static_cast<double>(t.w);
-    }
-    const double ss = block_sum_d((a0 + a1) + (a2 + a3), red);
-    const float scale =
-        static_cast<float>(1.0 / sqrt(ss / static_cast<double>(n) + static_cast<double>(eps)));
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-        const float4 t = v4[i], g = g4[i];
-        o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z,
-                            t.w * scale * g.w);
-    }
-    __syncthreads();
-}
-
-// ------------------------------------------------------------ smem stager --
-//
-// Stages a kernel's input vectors (activations, gains, default-vector rows,
-// expert hidden states) global -> shared with cp.async.bulk: thread 0 issues
-// one bulk copy per vector on a single mbarrier, so every vector is in flight
-// at once instead of one global-latency round trip per scalar load.  A
-// vector whose address/size is not 16-byte aligned falls back to a
-// block-strided copy.
-
-__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-
-struct Stager {
-    uint64_t* bar;
-    uint32_t phase;
-    __device__ void init(uint64_t* b) {  // whole block
-        bar = b;
-        phase = 0;
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-    }
-    // whole block; `bytes` is rounded up to 16 (buffers are padded)
-    __device__ void add(void* dst, const void* src, int bytes) {
-        const uint32_t b = static_cast<uint32_t>((bytes + 15) & ~15);
-        if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
-            if (threadIdx.x == 0) {
-                mbar_expect(bar, b);
-                bulk_g2s(dst, src, b, bar);
-            }
-        } else {
-            const float* s = static_cast<const float*>(src);
-            float* d = static_cast<float*>(dst);
-            for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) d[i] = s[i];
-        }
-    }
-    __device__ void wait() {  // whole block
-        if (threadIdx.x == 0) mbar_arrive(bar);
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        __syncthreads();
-    }
-};
-
-// ------------------------------------------------------- warp tile stream --
-//
-// One warp computes 32 sequential dot products acc(lane) = sum_c W[c][lane]*x[c]
-// over a row tile [cols][32] in global memory.  Lane 0 keeps S chunks of CC
-// columns in flight with cp.async.bulk; every lane walks the columns in order.
-
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float4 lds128f(uint32_t a) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-
-// One 16-byte group of a lane's consecutive columns, in column order.
-struct XG {  // the matching activations
-    float4 a, b;
-};
-__device__ __forceinline__ XG load_x(uint32_t xa, uint16_t) { return {lds128f(xa), lds128f(xa + 16)}; }
-__device__ __forceinline__ XG load_x(uint32_t xa, float) { return {lds128f(xa), make_float4(0, 0, 0, 0)}; }
-__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, uint16_t) {
-    const float4 x0 = x.a, x1 = x.b;
-    acc = acc + lo_bf(w.x) * x0.x;
-    acc = acc + hi_bf(w.x) * x0.y;
-    acc = acc + lo_bf(w.y) * x0.z;
-    acc = acc + hi_bf(w.y) * x0.w;
-    acc = acc + lo_bf(w.z) * x1.x;
-    acc = acc + hi_bf(w.z) * x1.y;
-    acc = acc + lo_bf(w.w) * x1.z;
-    acc = acc + hi_bf(w.w) * x1.w;
-    return acc;
-}
-__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, float) {
-    const float4 x0 = x.a;
-    acc = acc + __uint_as_float(w.x) * x0.x;
-    acc = acc + __uint_as_float(w.y) * x0.y;
-    acc = acc + __uint_as_float(w.z) * x0.z;
-    acc = acc + __uint_as_float(w.w) * x0.w;
-    return acc;
-}
-// The rounded products w[c] * x[c] of one group (acc + p is then the
-// reference's `acc += w * x`: product rounded, then the add rounded).
-__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, uint16_t) {
-    p[0] = lo_bf(w.x) * x.a.x;
-    p[1] = hi_bf(w.x) * x.a.y;
-    p[2] = lo_bf(w.y) * x.a.z;
-    p[3] = hi_bf(w.y) * x.a.w;
-    p[4] = lo_bf(w.z) * x.b.x;
-    p[5] = hi_bf(w.z) * x.b.y;
-    p[6] = lo_bf(w.w) * x.b.z;
-    p[7] = hi_bf(w.w) * x.b.w;
-}
-__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, float) {
-    p[0] = __uint_as_float(w.x) * x.a.x;
-    p[1] = __uint_as_float(w.y) * x.a.y;
-    p[2] = __uint_as_float(w.z) * x.a.z;
-    p[3] = __uint_as_float(w.w) * x.a.w;
-}
-__device__ __forceinline__ float group_elem(uint4 w, int i, uint16_t) {
-    const uint32_t v = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
-    return (i & 1) ? hi_bf(v) : lo_bf(v);
-}
-__device__ __forceinline__ float group_elem(uint4 w, int i, float) {
-    return __uint_as_float(i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w);
-}
-
-// Row tile layout (smoe_dev.h): 32 rows, columns in groups of G = 16 B / sizeof(WT);
-// element (row lane, col c) at (c / G) * 32 * G + lane * G + c % G.  A chunk of
-// CC columns (CC % G == 0) is CC * 32 contiguous elements = one bulk copy; each
-// lane reads its G columns with one conflict-free ld.shared.v4.
-template <typename WT, int S, int CC>
-struct WarpPipe {
-    static constexpr int G = 16 / static_cast<int>(sizeof(WT));
-    static constexpr int kChunkElems = CC * 32;
-    static constexpr int kChunkBytes = kChunkElems * static_cast<int>(sizeof(WT));
-    static constexpr int kBytes = S * kChunkBytes + S * 8;
-    static_assert(CC % G == 0, "chunk must hold whole column groups");
-    uint64_t* full;  // [S]
-    WT* buf;         // [S][CC*32]
-    uint32_t sbuf;   // shared-window address of buf
-    int ctr;         // chunks consumed so far (phase tracking)
-    int primed;      // chunks already issued for the next run()
-
-    __device__ void init(unsigned char* smem) {  // call with the owning warp; then syncwarp
-        buf = reinterpret_cast<WT*>(smem);
-        sbuf = smem_u32(smem);
-        full = reinterpret_cast<uint64_t*>(smem + S * kChunkBytes);
-        ctr = 0;
-        primed = 0;
-        if ((threadIdx.x & 31) == 0) {
-            for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
-            fence_mbar_init();
-        }
-        __syncwarp();
-    }
-
-    __device__ void issue(const WT* tile, int cols, int n, int g) {
-        const int st = g % S;
-        const int c0 = n * CC;
-        const int cn = min(CC, round_up(cols, G) - c0);
-        const uint32_t bytes = static_cast<uint32_t>(cn) * 32u * sizeof(WT);
-        mbar_expect_tx(&full[st], bytes);
-        bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
-    }
-
-    // Issue the first chunks of `tile` before the input vector exists (weights
-    // are independent of the activations), so the first wait finds data.
-    __device__ void prime(const WT* tile, int cols) {
-        const int nch = (cols + CC - 1) / CC;
-        if ((threadIdx.x & 31) == 0)
-            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
-        primed = 1;
-    }
-
-    // Returns this lane's dot product over the first `cols` columns, in
-    // column order.  xs: shared-memory f32 vector (16-byte aligned).
-    __device__ float run(const WT* tile, int cols, const float* xs) {
-        const int lane = threadIdx.x & 31;
-        const int nch = (cols + CC - 1) / CC;
-        if (lane == 0 && !primed)
-            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
-        primed = 0;
-        const uint32_t xbase = smem_u32(xs);
-        float acc = 0.0f;
-        for (int n = 0; n < nch; ++n) {
-            const int g = ctr + n;
-            const int st = g % S;
-            mbar_wait(&full[st], static_cast<uint32_t>((g / S) & 1));
-            const uint32_t wb = sbuf + st * kChunkBytes + lane * 16;
-            const uint32_t xb = xbase + n * CC * 4;
-            const int cn = min(CC, cols - n * CC);
-            const int ng = cn / G;
-            if (ng == CC / G) {
-                // software pipelined: group q+1's shared loads are in flight while
-                // group q's sequential FMUL/FADD chain runs
-                uint4 wn = lds128(wb);
-                XG xn = load_x(xb, WT{});
-#pragma unroll 4
-                for (int q = 0; q < CC / G; ++q) {
-                    const uint4 w = wn;
-                    const XG x = xn;
-                    if (q + 1 < CC / G) {
-                        wn = lds128(wb + (q + 1) * 512);
-                        xn = load_x(xb + (q + 1) * G * 4, WT{});
-                    }
-                    acc = chain_group(acc, w, x, WT{});
-                }
-            } else {
-                for (int q = 0; q < ng; ++q)
-                    acc = chain_group(acc, lds128(wb + q * 512), load_x(xb + q * G * 4, WT{}), WT{});
-                const int tail = cn - ng * G;
-                if (tail) {
-                    const uint4 w = lds128(wb + ng * 512);
-                    const float* xt = xs + n * CC + ng * G;
-                    for (int i = 0; i < tail; ++i) acc = acc + group_elem(w, i, WT{}) * xt[i];
-                }
-            }
-            __syncwarp();
-            if (lane == 0 && n + S < nch) issue(tile, cols, n + S, g + S);
-        }
-        ctr += nch;
-        return acc;
-    }
-};
-
-constexpr int kS = 4;       // stages per warp
-constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
-constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
-constexpr int kCCd = 64;    // down-projection columns per chunk (4 KB)
-using PipeB = WarpPipe<uint16_t, kS, kCCb>;
-using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
-using PipeF = WarpPipe<float, kS, kCCf>;
-using PipeD = WarpPipe<uint16_t, kS, kCCd>;
 
 __device__ __forceinline__ unsigned char* align128(unsigned char* p) {
     return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
@@ -575,12 +197,14 @@ __global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_
 
 __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int* stream,
                         const int* step) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int tok = stream ? stream[*step] : *token_src;
     if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m.Hp; j += gridDim.x * blockDim.x)
-        st.x[j] = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
+    const int j = blockIdx.x * 32 + threadIdx.x;  // grid Hp/32 x 32
+    const float v = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
+    st.x[j] = v;
+    warp_ssq_partial(v, st.ssq_x + blockIdx.x);  // layer 0's input
 }
 
 // q, k, v = W{q,k,v} . rms_norm(x, attn_gain) (model.cpp:325-333), RoPE on q
@@ -594,7 +218,6 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* gs = xs + round_up(m.H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
-    pdl_trigger();
     const int rb = blockIdx.x;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * m.H * 32;
     PipeBL pipe;
@@ -603,6 +226,7 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
     sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);
     // the epilogue's position and RoPE factors load while the chain runs
@@ -617,9 +241,11 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
         s = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2 + 1];
     }
     PHASE();
+    const float scale = rms_scale_from_partials(st.ssq_x + static_cast<long long>(layer) * (m.Hp / 32),
+                                                m.Hp / 32, m.H, m.eps);
     sg.wait();
     PHASE();
-    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
+    block_apply_norm(xs, gs, m.H, scale, xs);
     PHASE();
     float acc = pipe.run(tile, m.H, xs);
     PHASE();
@@ -638,85 +264,132 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
         st.vc[kv + R - 2 * D] = acc;
     PHASE();
     PHASE_DUMP("qkv [pre, stage, norm, chain, epi]");
+#ifdef SMOE_PHASES
+    if (blockIdx.x == 0 && threadIdx.x == 0) printf("qkv chain waits (cycles): %lld\n", pipe.wait_cyc);
+#endif
 }
 
 // scores / softmax / context (model.cpp:335-351), one CTA of kAttnThreads.
-// Keys, then values, stream through a 2-deep ring of kAttnChunk-position
-// tiles (cp.async.bulk); thread j owns position j's dot product (sequential
-// over head dims), thread i owns context dim i (sequential over positions).
+// Keys, then values, stream through 2-chunk rings of kAttnChunk positions,
+// copied global -> smem with cp.async (16 B per thread, L2 only).  Key rows
+// are padded to D+4 floats so that thread j's LDS.128 of its own row is
+// bank-conflict-free (8 rows per phase cover all 32 banks); thread j owns
+// position j's dot product (sequential over head dims), thread i owns
+// context dim i (sequential over positions).  Rows of earlier positions are
+// final before this step, so the first chunks are fetched BEFORE the PDL
+// wait; only row `pos` (written by k_qkv of this step) and q wait for it.
 constexpr int kAttnChunk = 64;
 constexpr int kAttnThreads = 256;
 constexpr int kAttnSmemPositions = 4096;
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// rows [p0, p0+pn) of a [cap][D] f32 cache into smem rows of `stride` floats;
+// row `skip` (the current position, not yet written) is left out.
+__device__ __forceinline__ void attn_fetch(float* dst, const float* src, int p0, int pn, int D,
+                                           int stride, int skip) {
+    const int per = D / 4;  // 16-byte pieces per row
+    for (int t = threadIdx.x; t < pn * per; t += blockDim.x) {
+        const int r = t / per, c = (t % per) * 4;
+        if (p0 + r == skip) continue;
+        cp_async16(dst + r * stride + c, src + static_cast<long long>(p0 + r) * D + c);
+    }
+}
+
 __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, double* scratch,
                                                         int layer) {
-    const int D = m.D;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(g_smem);              // [3]
-    float* red = reinterpret_cast<float*>(g_smem + 32);                // [32]
+    const int D = m.D, KS = D + 4;  // padded key row stride (floats)
+    float* red = reinterpret_cast<float*>(g_smem);                     // [32]
     float* qs = reinterpret_cast<float*>(g_smem + 256);                // [kMaxD]
-    float* tiles = qs + kMaxD;                                         // [2][chunk][D]
-    double* e = reinterpret_cast<double*>(tiles + 2 * kAttnChunk * D);  // [n] (smem when it fits)
+    float* kt = qs + kMaxD;                                            // [2][chunk][D+4]
+    float* vt = kt + 2 * kAttnChunk * KS;                              // [2][chunk][D]
+    double* e = reinterpret_cast<double*>(vt + 2 * kAttnChunk * D);    // [n] (smem when it fits)
     float* sc = reinterpret_cast<float*>(e + m.cap);
     if (m.cap > kAttnSmemPositions) {  // long contexts: f64/f32 scratch in global
         e = scratch;
         sc = reinterpret_cast<float*>(scratch + m.cap);
     }
     const long long base = static_cast<long long>(layer) * m.cap * D;
-    pdl_trigger();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    pdl_wait();
-    Stager sg;
-    sg.bar = &bars[2];
-    sg.phase = 0;
-    sg.add(qs, st.q, D * 4);
-    sg.wait();
-    const int n = *st.pos + 1;
+    const float* K = st.kc + base;
+    const float* V = st.vc + base;
+    // st.pos is only advanced by k_final, which completed before this grid could launch
+    const int pos = __ldcg(st.pos);
+    const int n = pos + 1;
     const int nch = (n + kAttnChunk - 1) / kAttnChunk;
-    auto issue = [&](const float* src, int c) {  // thread 0
-        const int p0 = c * kAttnChunk;
-        const int pn = min(kAttnChunk, n - p0);
-        const uint32_t bytes = static_cast<uint32_t>(pn) * D * 4;
-        mbar_expect_tx(&bars[c & 1], bytes);
-        bulk_g2s(tiles + (c & 1) * kAttnChunk * D, src + base + static_cast<long long>(p0) * D, bytes,
-                 &bars[c & 1]);
+    auto fetch_k = [&](int c, int skip) {
+        attn_fetch(kt + (c & 1) * kAttnChunk * KS, K, c * kAttnChunk, min(kAttnChunk, n - c * kAttnChunk), D,
+                   KS, skip);
     };
-    uint32_t ph[2] = {0, 0};
-    // pass 1: scores
-    if (threadIdx.x == 0) {
-        issue(st.kc, 0);
-        if (nch > 1) issue(st.kc, 1);
+    auto fetch_v = [&](int c, int skip) {
+        attn_fetch(vt + (c & 1) * kAttnChunk * D, V, c * kAttnChunk, min(kAttnChunk, n - c * kAttnChunk), D, D,
+                   skip);
+    };
+    // prefetch (groups 0, 1): K chunks 0-1 and, for short contexts, V chunks 0-1
+    fetch_k(0, pos);
+    if (nch > 1) fetch_k(1, pos);
+    cp_async_commit();
+    const bool v_early = nch <= 2;
+    if (v_early) {
+        fetch_v(0, pos);
+        if (nch > 1) fetch_v(1, pos);
     }
+    cp_async_commit();
+    pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
+    // q and the current position's key/value row (written by k_qkv)
+    for (int t = threadIdx.x; t < D / 4; t += blockDim.x) {
+        cp_async16(qs + 4 * t, st.q + 4 * t);
+        const int c = pos / kAttnChunk, r = pos % kAttnChunk;
+        if (c < 2) {
+            cp_async16(kt + (c & 1) * kAttnChunk * KS + r * KS + 4 * t, K + static_cast<long long>(pos) * D + 4 * t);
+            if (v_early)
+                cp_async16(vt + (c & 1) * kAttnChunk * D + r * D + 4 * t, V + static_cast<long long>(pos) * D + 4 * t);
+        }
+    }
+    cp_async_commit();
+    // pass 1: scores
     float lmax = -INFINITY;
     for (int c = 0; c < nch; ++c) {
-        mbar_wait(&bars[c & 1], ph[c & 1]);
-        ph[c & 1] ^= 1;
-        const float* t = tiles + (c & 1) * kAttnChunk * D;
+        if (c >= 2) {  // chunks past the prefetched pair load after the wait (row pos included)
+            fetch_k(c, -1);
+            cp_async_commit();
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        const float* t = kt + (c & 1) * kAttnChunk * KS;
         const int p0 = c * kAttnChunk;
         const int pn = min(kAttnChunk, n - p0);
         for (int j = threadIdx.x; j < pn; j += blockDim.x) {
-            const float* kj = t + j * D;
+            const float* kj = t + j * KS;
             float acc = 0.0f;
-            for (int i = 0; i < D; ++i) acc = acc + qs[i] * kj[i];
+            for (int i = 0; i < D; i += 4) {
+                const float4 kv = *reinterpret_cast<const float4*>(kj + i);
+                const float4 qv = *reinterpret_cast<const float4*>(qs + i);
+                acc = acc + qv.x * kv.x;
+                acc = acc + qv.y * kv.y;
+                acc = acc + qv.z * kv.z;
+                acc = acc + qv.w * kv.w;
+            }
             const float v = acc * m.inv_sqrt_d;
             sc[p0 + j] = v;
             lmax = fmaxf(lmax, v);
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && c + 2 < nch) issue(st.kc, c + 2);
+        __syncthreads();  // the ring slot may be refilled next iteration
+    }
+    if (!v_early) {  // stream values: first two chunks now, the rest in pass 2
+        fetch_v(0, -1);
+        if (nch > 1) fetch_v(1, -1);
+        cp_async_commit();
     }
     const float mx = block_max_f(lmax, red);
     for (int j = threadIdx.x; j < n; j += blockDim.x)
         e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
     __syncthreads();
-    // pass 2 prefetch overlaps the partition sum
-    if (threadIdx.x == 0) {
-        issue(st.vc, 0);
-        if (nch > 1) issue(st.vc, 1);
-    }
     __shared__ double zs;
     if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
         double z = 0.0;
@@ -730,15 +403,18 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     float acc = 0.0f;
     const int i = threadIdx.x;
     for (int c = 0; c < nch; ++c) {
-        mbar_wait(&bars[c & 1], ph[c & 1]);
-        ph[c & 1] ^= 1;
-        const float* t = tiles + (c & 1) * kAttnChunk * D;
+        if (c >= 2) {
+            fetch_v(c, -1);
+            cp_async_commit();
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        const float* t = vt + (c & 1) * kAttnChunk * D;
         const int p0 = c * kAttnChunk;
         const int pn = min(kAttnChunk, n - p0);
         if (i < D)
             for (int j = 0; j < pn; ++j) acc = acc + sc[p0 + j] * t[j * D + i];
         __syncthreads();
-        if (threadIdx.x == 0 && c + 2 < nch) issue(st.vc, c + 2);
     }
     if (i < D) st.ctx[i] = acc;
 }
@@ -749,13 +425,13 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* xr = xs + kMaxD;  // residual rows of this tile
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xr + 32));
-    pdl_trigger();
     PipeB pipe;
     pipe.init(pipe_mem);
     pipe.prime(m.wo + layer * m.wo_stride + static_cast<long long>(blockIdx.x) * m.D * 32, m.D);
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.ctx, m.D * 4);
     sg.add(xr, st.x + blockIdx.x * 32, 32 * 4);
     sg.wait();
@@ -763,7 +439,9 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
     const float acc = pipe.run(tile, m.D, xs);
     const int j = rb * 32 + (threadIdx.x & 31);
-    if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = xr[threadIdx.x & 31] + acc;
+    const float r = j < m.H ? xr[threadIdx.x & 31] + acc : 0.0f;
+    if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = r;
+    warp_ssq_partial(r, st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32) + rb);
 }
 
 // ---------------------------------------------------------------- router --
@@ -817,7 +495,6 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     const int nP = gemv_pred ? m.Ep / 32 : 0;
     const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
     const int b = blockIdx.x;
-    pdl_trigger();
     PipeBL pipe;
     const uint16_t* tile = nullptr;
     if (b < nT + nP) {
@@ -830,11 +507,14 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     if (b < nT || (b < nT + nP && rl.pred_kind == kBaselineS)) {
         sg.add(rs, st.r + static_cast<long long>(l) * m.Hp, H * 4);
         sg.add(gs, m.moe_gain + static_cast<long long>(l) * H, H * 4);
+        const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(l) * (m.Hp / 32),
+                                                    m.Hp / 32, H, m.eps);
         sg.wait();
-        block_rms_norm(rs, gs, H, m.eps, xs, red);
+        block_apply_norm(rs, gs, H, scale, xs);
         if (b == 0 && rl.do_true)
             for (int j = threadIdx.x; j < H; j += blockDim.x) st.s[static_cast<long long>(l) * m.Hp + j] = xs[j];
     } else if (b < nT + nP + nQ) {
@@ -964,7 +644,6 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     }
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem + round_up(cols, 32) * 4);
     unsigned char* pipe_mem = align128(g_smem + round_up(cols, 32) * 4 + 64);
-    pdl_trigger();
     const int rb = blockIdx.x;
     PipeF pipe;
     pipe.init(pipe_mem);
@@ -972,6 +651,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, in, cols * 4);
     sg.wait();
     const float acc = pipe.run(tiles + static_cast<long long>(rb) * cols * 32, cols, xs);
@@ -1047,8 +727,11 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
 // here instead of reading the router's copy.
 __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src, int s_from_r) {
-    pdl_trigger();
+    PHASE_DECL
+    PHASE();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
+    PHASE();
     const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
     const int e = (exec_src ? st.id_pred : st.id_exec)[layer * m.K + i];
     if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it
@@ -1074,19 +757,29 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     if (s_from_r) {
         sg.add(xs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
         sg.add(gs, m.moe_gain + static_cast<long long>(layer) * H, H * 4);
+        const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32),
+                                                    m.Hp / 32, H, m.eps);
         sg.wait();
-        block_rms_norm(xs, gs, H, m.eps, xs, red);
+        block_apply_norm(xs, gs, H, scale, xs);
     } else {
         sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
         sg.wait();
     }
+    PHASE();
     const float acc = pipe.run(tile, H, xs);
+    PHASE();
     const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
     const int lane = threadIdx.x & 31;
     if ((lane & 1) == 0) {
         const int row = rb * 16 + (lane >> 1);
         st.h[static_cast<long long>(i) * m.Hmp + row] = silu_ref(acc) * up;
     }
+    PHASE();
+    PHASE_DUMP("ffn_gu [pdl, ready+stage+norm, chain, epi]");
+#ifdef SMOE_PHASES
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        printf("ffn_gu chain waits (cycles): %lld\n", pipe.wait_cyc);
+#endif
 }
 
 // down: grid Hp/32, K warps per CTA (warp i = i-th executed expert); then the
@@ -1094,8 +787,8 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
 // x = r + m (model.cpp:386).
 __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st, DevCtl ctl,
                                                          int layer, int exec_src) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     if (*(volatile int*)ctl.error) return;
     const int K = m.K, Hmp = m.Hmp, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
@@ -1143,11 +836,16 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
     ys[w * 32 + lane] = acc;
     if (j < m.H) st.y[static_cast<long long>(w) * m.Hp + j] = acc;
     __syncthreads();
-    if (w == 0 && j < m.H) {
-        float out = 0.0f;
-        for (int i = 0; i < K; ++i) out += gts[i] * ys[i * 32 + lane];
-        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
-        st.x[j] = rr[lane] + out;
+    if (w == 0) {
+        float xv = 0.0f;
+        if (j < m.H) {
+            float out = 0.0f;
+            for (int i = 0; i < K; ++i) out += gts[i] * ys[i * 32 + lane];
+            st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+            xv = rr[lane] + out;
+            st.x[j] = xv;
+        }
+        warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
     }
 }
 
@@ -1157,8 +855,8 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
 // residual — identical arithmetic to the single-GPU epilogue.
 __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int K = m.K, lane = threadIdx.x & 31, rb = blockIdx.x, j = rb * 32 + lane;
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
@@ -1181,6 +879,7 @@ __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl c
         s_ok = ok;
     }
     __syncthreads();
+    float xv = 0.0f;
     if (s_ok && j < m.H) {
         const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
         const float* xb = ctl.ep.xbuf[ctl.ep.rank] + static_cast<long long>(layer & 1) * K * m.Hp;
@@ -1191,8 +890,10 @@ __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl c
             out += gts[i] * y;
         }
         st.m[static_cast<long long>(layer) * m.Hp + j] = out;
-        st.x[j] = st.r[static_cast<long long>(layer) * m.Hp + j] + out;
+        xv = st.r[static_cast<long long>(layer) * m.Hp + j] + out;
+        st.x[j] = xv;
     }
+    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
     if (!last_cta(st.counters + 3, gridDim.x)) return;
     if (threadIdx.x == 0) ctl.ep.epoch[layer] += 1;
 }
@@ -1207,17 +908,19 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* gs = xs + round_up(m.H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
-    pdl_trigger();
     PipeBL pipe;
     pipe.init(pipe_mem);
     pipe.prime(m.unemb + static_cast<long long>(blockIdx.x) * m.H * 32, m.H);
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
     sg.add(gs, m.final_gain, m.H * 4);
+    const float scale = rms_scale_from_partials(st.ssq_x + static_cast<long long>(m.L) * (m.Hp / 32),
+                                                m.Hp / 32, m.H, m.eps);
     sg.wait();
-    block_rms_norm(xs, gs, m.H, m.eps, xs, red);
+    block_apply_norm(xs, gs, m.H, scale, xs);
     const int rb = blockIdx.x;
     const float acc = pipe.run(m.unemb + static_cast<long long>(rb) * m.H * 32, m.H, xs);
     const int v = rb * 32 + (threadIdx.x & 31);
@@ -1255,8 +958,8 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
 // ----------------------------------------------------------- calibration ----
 
 __global__ void k_dv_accum(DevModel m, DevState st, double* sums, long long* counts, int layer) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int K = m.K, H = m.H;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * H; t += gridDim.x * blockDim.x) {
         const int i = t / H, j = t % H;
@@ -1279,8 +982,8 @@ __global__ void k_dv_freeze(const double* sums, const long long* counts, float* 
 // ----------------------------------------------------------------- trace ----
 
 __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int step = *tr.step;
     if (step >= tr.cap) return;
     const int L = m.L, H = m.H, E = m.E, K = m.K, V = m.V, Hp = m.Hp;
@@ -1320,8 +1023,8 @@ __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
 // Per-layer raw outputs are overwritten by the next layer, so the full trace
 // grabs them right after each layer's down projection.
 __global__ void k_trace_y(DevModel m, DevState st, TraceDev tr, int layer) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int step = *tr.step;
     if (step >= tr.cap) return;
     const int K = m.K, H = m.H, L = m.L;
@@ -1353,8 +1056,9 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool no_pdl = std::getenv("SMOE_NO_PDL") != nullptr;  // diagnostics
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = no_pdl ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 #define PDL(k, grid, block, smem, s, ...)                                   \
@@ -1392,7 +1096,7 @@ size_t down_smem(const DevModel& m) {
 }
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
-    size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * m.D * 4;
+    size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * (2 * m.D + 4) * 4;
     if (m.cap <= kAttnSmemPositions) b += static_cast<size_t>(m.cap) * 12;
     return b;
 }
@@ -1429,7 +1133,7 @@ cudaError_t launch_gen_bf16(uint64_t seed, float stddev, int R, int C, int tile_
 
 cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token_src,
                          cudaStream_t s, const int* stream, const int* step) {
-    PDL(k_embed, (m.Hp + 255) / 256, 256, 0, s, m, st, token_src, stream, step);
+    PDL(k_embed, m.Hp / 32, 32, 0, s, m, st, token_src, stream, step);
     return counted(1);
 }
 

@@ -1,0 +1,481 @@
+// smoe_chain.cuh — device primitives shared by kernels.cu and the tools'
+// micro-benchmarks: mbarrier / cp.async.bulk helpers, programmatic dependent
+// launch, the smem Stager, the bit-exact f64 block reductions and rms_norm,
+// and WarpPipe, the per-warp TMA-fed sequential-chain GEMV.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+
+#include "smoe_dev.h"
+
+namespace smoe {
+
+// ---------------------------------------------------------------- helpers --
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue (barrier init, static weight prefetch) while this one runs; every
+// kernel calls pdl_wait() before touching activations written upstream.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Optional phase timing (build with -DSMOE_PHASES; tools/phase_run.py): block
+// (0,0)'s timeline between PHASE() marks, printed once per launch.
+#ifdef SMOE_PHASES
+__device__ __forceinline__ unsigned long long gtimer() {  // SM cycles
+    return clock64();
+}
+#define PHASE_DECL \
+    unsigned long long ph_[10];  \
+    int nph_ = 0;
+#define PHASE()                                  \
+    do {                                         \
+        if (nph_ < 10) ph_[nph_++] = gtimer();   \
+    } while (0)
+#define PHASE_DUMP(name)                                                                   \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                      \
+            printf("%s (cycles):", name);                                                  \
+            for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);      \
+            printf(" | %llu\n", ph_[nph_ - 1] - ph_[0]);                                   \
+        }                                                                                  \
+    } while (0)
+#else
+#define PHASE_DECL
+#define PHASE() \
+    do {        \
+    } while (0)
+#define PHASE_DUMP(name) \
+    do {                 \
+    } while (0)
+#endif
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float bf2f(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+__device__ __forceinline__ float to_f(uint16_t b) { return bf2f(b); }
+__device__ __forceinline__ float to_f(float f) { return f; }
+
+// numerics.cpp:86-89 — silu in f64, rounded to f32.
+__device__ __forceinline__ float silu_ref(float x) {
+    const double xd = static_cast<double>(x);
+    return static_cast<float>(xd / (1.0 + exp(-xd)));
+}
+
+// Deterministic block reduction of a per-thread double (tree order fixed by
+// blockDim).  Returns the same value in every thread.
+__device__ double block_sum_d(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    __syncthreads();
+    return t;
+}
+
+__device__ float block_max_f(float v, float* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    float t = red[0];
+    for (int i = 1; i < nw; ++i) t = fmaxf(t, red[i]);
+    __syncthreads();
+    return t;
+}
+
+// rms_norm (numerics.cpp:72-84): out[i] = (v[i] * scale) * gain[i],
+// scale = f32(1 / sqrt(sum_f64(v^2) / n + eps)).  Whole block participates;
+// v, gain, out are 16-byte aligned shared arrays and n % 4 == 0 (H % 8 == 0 is
+// validated).  The f64 sum runs as 4 independent partial sums per thread
+// (fixed order: the reduction tree is deterministic).
+__device__ void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
+                               double* red) {
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(gain);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const int n4 = n >> 2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 t = v4[i];
+        a0 += static_cast<double>(t.x) * static_cast<double>(t.x);
+        a1 += static_cast<double>(t.y) * static_cast<double>(t.y);
+        a2 += static_cast<double>(t.z) * static_cast<double>(t.z);
+        a3 += static_cast<double>(t.w) * static_cast<double>(t.w);
+    }
+    const double ss = block_sum_d((a0 + a1) + (a2 + a3), red);
+    const float scale =
+        static_cast<float>(1.0 / sqrt(ss / static_cast<double>(n) + static_cast<double>(eps)));
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 t = v4[i], g = g4[i];
+        o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z,
+                            t.w * scale * g.w);
+    }
+    __syncthreads();
+}
+
+// Producer side of rms_norm (numerics.cpp:72-84) fused into the kernel that
+// writes the vector: one warp's 32 rows -> one f64 partial sum of squares
+// (fixed shuffle tree).  Every lane passes its value (0 for padding rows);
+// lane 0 stores the partial.
+__device__ __forceinline__ void warp_ssq_partial(float v, double* dst) {
+    double d = static_cast<double>(v) * static_cast<double>(v);
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_down_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) *dst = d;
+}
+
+// Consumer side: sum the nb partials in a fixed order (lane-strided, then a
+// fixed shuffle tree) and form the reference's scale
+// f32(1 / sqrt(sum / n + eps)).  Executed by a whole warp; every warp of a
+// block computes the same value.  Like the in-block tree this replaces, the
+// f64 order differs from the reference's sequential loop; the difference
+// (~1e-16 relative) survives the f32 rounding of the scale only at
+// measure-zero midpoints.
+__device__ __forceinline__ float rms_scale_from_partials(const double* part, int nb, int n,
+                                                         float eps) {
+    double v = 0.0;
+    for (int i = threadIdx.x & 31; i < nb; i += 32) v += __ldcg(part + i);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    return static_cast<float>(1.0 / sqrt(v / static_cast<double>(n) + static_cast<double>(eps)));
+}
+
+// out[i] = (v[i] * scale) * gain[i] over a block (16-byte aligned smem, n % 4 == 0).
+__device__ __forceinline__ void block_apply_norm(const float* v, const float* gain, int n, float scale,
+                                                 float* out) {
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(gain);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x) {
+        const float4 t = v4[i], g = g4[i];
+        o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z, t.w * scale * g.w);
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ smem stager --
+//
+// Stages a kernel's input vectors (activations, gains, default-vector rows,
+// expert hidden states) global -> shared with cp.async.bulk: thread 0 issues
+// one bulk copy per vector on a single mbarrier, so every vector is in flight
+// at once instead of one global-latency round trip per scalar load.  A
+// vector whose address/size is not 16-byte aligned falls back to a
+// block-strided copy.
+
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+struct Stager {
+    uint64_t* bar;
+    uint32_t phase;
+    __device__ void init(uint64_t* b) {  // whole block
+        bar = b;
+        phase = 0;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    // whole block; `bytes` is rounded up to 16 (buffers are padded)
+    __device__ void add(void* dst, const void* src, int bytes) {
+        const uint32_t b = static_cast<uint32_t>((bytes + 15) & ~15);
+        if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+            if (threadIdx.x == 0) {
+                mbar_expect(bar, b);
+                bulk_g2s(dst, src, b, bar);
+            }
+        } else {
+            const float* s = static_cast<const float*>(src);
+            float* d = static_cast<float*>(dst);
+            for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) d[i] = s[i];
+        }
+    }
+    __device__ void wait() {  // whole block
+        if (threadIdx.x == 0) mbar_arrive(bar);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        __syncthreads();
+    }
+};
+
+// ------------------------------------------------------- warp tile stream --
+//
+// One warp computes 32 sequential dot products acc(lane) = sum_c W[c][lane]*x[c]
+// over a row tile [cols][32] in global memory.  Lane 0 keeps S chunks of CC
+// columns in flight with cp.async.bulk; every lane walks the columns in order.
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+// bf16 halves of a 32-bit word as f32, on the ALU pipe (PRMT / LOP3) so the
+// FMA pipe is left to the FMUL/FADD chain (ptxas would use IMAD.SHL for <<).
+__device__ __forceinline__ float lo_bf(uint32_t w) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(r) : "r"(w));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ float hi_bf(uint32_t w) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, 0xffff0000, 0, 0xc0;" : "=r"(r) : "r"(w));
+    return __uint_as_float(r);
+}
+
+// One 16-byte group of a lane's consecutive columns, in column order.
+struct XG {  // the matching activations
+    float4 a, b;
+};
+__device__ __forceinline__ XG load_x(uint32_t xa, uint16_t) { return {lds128f(xa), lds128f(xa + 16)}; }
+__device__ __forceinline__ XG load_x(uint32_t xa, float) { return {lds128f(xa), make_float4(0, 0, 0, 0)}; }
+__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, uint16_t) {
+    const float4 x0 = x.a, x1 = x.b;
+    acc = acc + lo_bf(w.x) * x0.x;
+    acc = acc + hi_bf(w.x) * x0.y;
+    acc = acc + lo_bf(w.y) * x0.z;
+    acc = acc + hi_bf(w.y) * x0.w;
+    acc = acc + lo_bf(w.z) * x1.x;
+    acc = acc + hi_bf(w.z) * x1.y;
+    acc = acc + lo_bf(w.w) * x1.z;
+    acc = acc + hi_bf(w.w) * x1.w;
+    return acc;
+}
+__device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, float) {
+    const float4 x0 = x.a;
+    acc = acc + __uint_as_float(w.x) * x0.x;
+    acc = acc + __uint_as_float(w.y) * x0.y;
+    acc = acc + __uint_as_float(w.z) * x0.z;
+    acc = acc + __uint_as_float(w.w) * x0.w;
+    return acc;
+}
+// The rounded products w[c] * x[c] of one group (acc + p is then the
+// reference's `acc += w * x`: product rounded, then the add rounded).
+__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, uint16_t) {
+    p[0] = lo_bf(w.x) * x.a.x;
+    p[1] = hi_bf(w.x) * x.a.y;
+    p[2] = lo_bf(w.y) * x.a.z;
+    p[3] = hi_bf(w.y) * x.a.w;
+    p[4] = lo_bf(w.z) * x.b.x;
+    p[5] = hi_bf(w.z) * x.b.y;
+    p[6] = lo_bf(w.w) * x.b.z;
+    p[7] = hi_bf(w.w) * x.b.w;
+}
+__device__ __forceinline__ void products(uint4 w, const XG& x, float* p, float) {
+    p[0] = __uint_as_float(w.x) * x.a.x;
+    p[1] = __uint_as_float(w.y) * x.a.y;
+    p[2] = __uint_as_float(w.z) * x.a.z;
+    p[3] = __uint_as_float(w.w) * x.a.w;
+}
+__device__ __forceinline__ float group_elem(uint4 w, int i, uint16_t) {
+    const uint32_t v = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
+    return (i & 1) ? hi_bf(v) : lo_bf(v);
+}
+__device__ __forceinline__ float group_elem(uint4 w, int i, float) {
+    return __uint_as_float(i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w);
+}
+
+// Row tile layout (smoe_dev.h): 32 rows, columns in groups of G = 16 B / sizeof(WT);
+// element (row lane, col c) at (c / G) * 32 * G + lane * G + c % G.  A chunk of
+// CC columns (CC % G == 0) is CC * 32 contiguous elements = one bulk copy; each
+// lane reads its G columns with one conflict-free ld.shared.v4.
+#ifdef SMOE_PHASES
+#define PIPE_WAIT(stmt)                 \
+    do {                                \
+        const long long t_ = clock64(); \
+        stmt;                           \
+        wait_cyc += clock64() - t_;     \
+    } while (0)
+#else
+#define PIPE_WAIT(stmt) stmt
+#endif
+
+template <typename WT, int S, int CC>
+struct WarpPipe {
+#ifdef SMOE_PHASES
+    long long wait_cyc = 0;  // cycles spent waiting for chunks (phase builds only)
+#endif
+    static constexpr int G = 16 / static_cast<int>(sizeof(WT));
+    static constexpr int kChunkElems = CC * 32;
+    static constexpr int kChunkBytes = kChunkElems * static_cast<int>(sizeof(WT));
+    static constexpr int kBytes = S * kChunkBytes + S * 8;
+    static_assert(CC % G == 0, "chunk must hold whole column groups");
+    uint64_t* full;  // [S]
+    WT* buf;         // [S][CC*32]
+    uint32_t sbuf;   // shared-window address of buf
+    int ctr;         // chunks consumed so far (phase tracking)
+    int primed;      // chunks already issued for the next run()
+
+    __device__ void init(unsigned char* smem) {  // call with the owning warp; then syncwarp
+        buf = reinterpret_cast<WT*>(smem);
+        sbuf = smem_u32(smem);
+        full = reinterpret_cast<uint64_t*>(smem + S * kChunkBytes);
+        ctr = 0;
+        primed = 0;
+        if ((threadIdx.x & 31) == 0) {
+            for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+    }
+
+    __device__ void issue(const WT* tile, int cols, int n, int g) {
+        const int st = g % S;
+        const int c0 = n * CC;
+        const int cn = min(CC, round_up(cols, G) - c0);
+        const uint32_t bytes = static_cast<uint32_t>(cn) * 32u * sizeof(WT);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
+    }
+
+    // Issue the first chunks of `tile` before the input vector exists (weights
+    // are independent of the activations), so the first wait finds data.
+    __device__ void prime(const WT* tile, int cols) {
+        const int nch = (cols + CC - 1) / CC;
+        if ((threadIdx.x & 31) == 0)
+            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        primed = 1;
+    }
+
+    // Returns this lane's dot product over the first `cols` columns, in
+    // column order.  xs: shared-memory f32 vector (16-byte aligned).
+    //
+    // Software pipeline: the shared loads of group j+2 are issued while group
+    // j's FMUL/FADD chain runs (LDS latency ~30 cycles vs the 32-cycle FADD
+    // chain of a group), also across chunk boundaries; the group loop of a
+    // full chunk is unrolled so the only branches are one mbarrier wait and
+    // one refill per chunk.  A partial last chunk takes the plain loop.
+    __device__ float run(const WT* tile, int cols, const float* xs) {
+        constexpr int GPC = CC / G;  // groups per chunk
+        static_assert(GPC >= 2, "chunk must hold at least two groups");
+        const int lane = threadIdx.x & 31;
+        const int nch = (cols + CC - 1) / CC;
+        if (lane == 0 && !primed)
+            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        primed = 0;
+        const uint32_t xbase = smem_u32(xs);
+        const uint32_t lbase = sbuf + lane * 16;
+        const int c0 = ctr;
+        const int nfull = cols / CC;
+        float acc = 0.0f;
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+        XG x0{}, x1{};
+        if (nfull > 0) {
+            PIPE_WAIT(mbar_wait(&full[c0 % S], static_cast<uint32_t>((c0 / S) & 1)));
+            w0 = lds128(lbase + (c0 % S) * kChunkBytes);
+            w1 = lds128(lbase + (c0 % S) * kChunkBytes + 512);
+            x0 = load_x(xbase, WT{});
+            x1 = load_x(xbase + G * 4, WT{});
+        }
+        for (int n = 0; n < nfull; ++n) {
+            const int g = c0 + n;
+            const uint32_t cb = lbase + (g % S) * kChunkBytes;
+            const uint32_t nb = lbase + ((g + 1) % S) * kChunkBytes;
+            const bool next_full = n + 1 < nfull;
+            const uint32_t xc = xbase + n * CC * 4;
+#pragma unroll
+            for (int j = 0; j < GPC; ++j) {
+                const uint4 w = w0;
+                const XG x = x0;
+                w0 = w1;
+                x0 = x1;
+                if (j + 2 < GPC) {
+                    w1 = lds128(cb + (j + 2) * 512);
+                    x1 = load_x(xc + (j + 2) * G * 4, WT{});
+                } else if (next_full) {
+                    if (j + 2 == GPC)
+                        PIPE_WAIT(mbar_wait(&full[(g + 1) % S], static_cast<uint32_t>(((g + 1) / S) & 1)));
+                    w1 = lds128(nb + (j + 2 - GPC) * 512);
+                    x1 = load_x(xc + (j + 2) * G * 4, WT{});
+                }
+                acc = chain_group(acc, w, x, WT{});
+            }
+            __syncwarp();  // every lane is done with this stage: refill it
+            if (lane == 0 && n + S < nch) issue(tile, cols, n + S, g + S);
+        }
+        if (nfull < nch) {  // partial last chunk
+            const int n = nfull, g = c0 + n;
+            mbar_wait(&full[g % S], static_cast<uint32_t>((g / S) & 1));
+            const uint32_t wb = lbase + (g % S) * kChunkBytes;
+            const uint32_t xb = xbase + n * CC * 4;
+            const int cn = cols - n * CC;
+            const int ng = cn / G;
+            for (int q = 0; q < ng; ++q)
+                acc = chain_group(acc, lds128(wb + q * 512), load_x(xb + q * G * 4, WT{}), WT{});
+            const int tail = cn - ng * G;
+            if (tail) {
+                const uint4 w = lds128(wb + ng * 512);
+                const float* xt = xs + n * CC + ng * G;
+                for (int i = 0; i < tail; ++i) acc = acc + group_elem(w, i, WT{}) * xt[i];
+            }
+            __syncwarp();
+        }
+        ctr += nch;
+        return acc;
+    }
+};
+
+constexpr int kS = 4;       // stages per warp
+constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
+constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
+constexpr int kCCd = 64;    // down-projection columns per chunk (4 KB)
+using PipeB = WarpPipe<uint16_t, kS, kCCb>;
+using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
+using PipeF = WarpPipe<float, kS, kCCf>;
+using PipeD = WarpPipe<uint16_t, kS, kCCd>;
+
+}  // namespace smoe

@@ -115,6 +115,11 @@ struct DevState {
     int* pos;          // position
     int* token;        // current token
     int* counters;     // last-CTA counters [64]
+    // rms_norm statistics, computed by the kernel that produces the vector:
+    // f64 partial sums of squares per 32-row block (Hp/32 per vector), summed
+    // by consumers in a fixed order (rms_scale_from_partials).
+    double* ssq_x;     // [L+1][Hp/32]  x entering layer l (index L: final norm)
+    double* ssq_r;     // [L][Hp/32]    r_l (pre-MoE residual)
 };
 
 // Expert parallelism: expert e of every layer lives on rank

@@ -159,6 +159,26 @@ def test_toy_all_predictors_vs_oracle(lib, toy_oracle, kind, frac):
     s.close()
 
 
+@pytest.mark.parametrize("plen", [130, 200])
+def test_long_context_attention_chunks(lib, toy_oracle, plen):
+    """Contexts past the two prefetched 64-position chunks: keys and values
+    stream through the cp.async rings (k_attn), the current row arrives in a
+    chunk loaded after the PDL wait, and ring slots are reused."""
+    orc, om, table, est = toy_oracle
+    rng = np.random.default_rng(plen)
+    prompt = rng.integers(0, TOY["vocab"], plen).astype(np.int32)
+    want = om.generate_trace(prompt, 6, orc.make_predictor("router-pf", om, table), outputs=True)
+    s = session(TOY, cache_fraction=0.5)
+    s.load_default_vectors(np.array(table.d))
+    s.set_predictor("router-pf")
+    got = run_trace(s, prompt, 6, "prefetch")
+    w = dict(tokens=want.tokens, s=want.s, r=want.r, m=want.m, logits=want.logits, ids=want.ids,
+             gates=want.gates, outputs=want.outputs, final_logits=want.final_logits,
+             pred_ids=want.pred_ids, pred_gates=want.pred_gates)
+    assert_trace_equal(got, w, True, len(prompt))
+    s.close()
+
+
 def test_topk_softmax_gating(lib):
     from oracle.bindings import Config, Oracle
     cfg = dict(TOY, gating="topk-softmax", seed=9)
