@@ -43,6 +43,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Non-blocking probe of a phase (mbarrier.test_wait): issued well before the
+// data is needed so its latency (~90 cycles even when complete) overlaps the
+// chain instead of stalling it.
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok;
+}
+// One lane of a converged warp (elect.sync): lets ptxas issue the bulk copy
+// without a per-lane uniformity loop.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(p));
+    return p != 0;
+}
 // Programmatic dependent launch: let the next kernel in the stream start its
 // prologue (barrier init, static weight prefetch) while this one runs; every
 // kernel calls pdl_wait() before touching activations written upstream.
@@ -283,16 +308,25 @@ struct XG {  // the matching activations
 };
 __device__ __forceinline__ XG load_x(uint32_t xa, uint16_t) { return {lds128f(xa), lds128f(xa + 16)}; }
 __device__ __forceinline__ XG load_x(uint32_t xa, float) { return {lds128f(xa), make_float4(0, 0, 0, 0)}; }
+// Products are formed two at a time with FMUL2 (__fmul2_rn: each lane of the
+// pair rounds exactly like __fmul_rn) and summed by scalar FADDs in column
+// order, so the FMA pipe carries 4 FMUL2 + 8 FADD per 8 columns (24 cycles at
+// 2 cycles each) under the 32-cycle FADD latency chain.  The products must
+// never feed a packed add: ptxas contracts FMUL2 -> FADD2 into FFMA2 even for
+// _rn intrinsics (tests/test_sass.py checks the library has no FFMA2).
 __device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, uint16_t) {
-    const float4 x0 = x.a, x1 = x.b;
-    acc = acc + lo_bf(w.x) * x0.x;
-    acc = acc + hi_bf(w.x) * x0.y;
-    acc = acc + lo_bf(w.y) * x0.z;
-    acc = acc + hi_bf(w.y) * x0.w;
-    acc = acc + lo_bf(w.z) * x1.x;
-    acc = acc + hi_bf(w.z) * x1.y;
-    acc = acc + lo_bf(w.w) * x1.z;
-    acc = acc + hi_bf(w.w) * x1.w;
+    const float2 p0 = __fmul2_rn(make_float2(lo_bf(w.x), hi_bf(w.x)), make_float2(x.a.x, x.a.y));
+    const float2 p1 = __fmul2_rn(make_float2(lo_bf(w.y), hi_bf(w.y)), make_float2(x.a.z, x.a.w));
+    const float2 p2 = __fmul2_rn(make_float2(lo_bf(w.z), hi_bf(w.z)), make_float2(x.b.x, x.b.y));
+    const float2 p3 = __fmul2_rn(make_float2(lo_bf(w.w), hi_bf(w.w)), make_float2(x.b.z, x.b.w));
+    acc = acc + p0.x;
+    acc = acc + p0.y;
+    acc = acc + p1.x;
+    acc = acc + p1.y;
+    acc = acc + p2.x;
+    acc = acc + p2.y;
+    acc = acc + p3.x;
+    acc = acc + p3.y;
     return acc;
 }
 __device__ __forceinline__ float chain_group(float acc, uint4 w, const XG& x, float) {
@@ -427,17 +461,20 @@ struct WarpPipe {
             const uint32_t nb = lbase + ((g + 1) % S) * kChunkBytes;
             const bool next_full = n + 1 < nfull;
             const uint32_t xc = xbase + n * CC * 4;
+            uint32_t next_ready = 0;
 #pragma unroll
             for (int j = 0; j < GPC; ++j) {
                 const uint4 w = w0;
                 const XG x = x0;
                 w0 = w1;
                 x0 = x1;
+                if (j == GPC / 2 && next_full)  // early, non-blocking probe of the next chunk
+                    next_ready = mbar_test(&full[(g + 1) % S], static_cast<uint32_t>(((g + 1) / S) & 1));
                 if (j + 2 < GPC) {
                     w1 = lds128(cb + (j + 2) * 512);
                     x1 = load_x(xc + (j + 2) * G * 4, WT{});
                 } else if (next_full) {
-                    if (j + 2 == GPC)
+                    if (j + 2 == GPC && !next_ready)
                         PIPE_WAIT(mbar_wait(&full[(g + 1) % S], static_cast<uint32_t>(((g + 1) / S) & 1)));
                     w1 = lds128(nb + (j + 2 - GPC) * 512);
                     x1 = load_x(xc + (j + 2) * G * 4, WT{});
@@ -445,7 +482,7 @@ struct WarpPipe {
                 acc = chain_group(acc, w, x, WT{});
             }
             __syncwarp();  // every lane is done with this stage: refill it
-            if (lane == 0 && n + S < nch) issue(tile, cols, n + S, g + S);
+            if (n + S < nch && elect_one()) issue(tile, cols, n + S, g + S);
         }
         if (nfull < nch) {  // partial last chunk
             const int n = nfull, g = c0 + n;

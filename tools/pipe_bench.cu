@@ -101,15 +101,14 @@ void bench(int ntiles, int cols, const char* label) {
 }
 
 int main() {
-    for (int rnd = 0; rnd < 2; ++rnd) {
     g_random = true;
-    int nd = rnd;
+    int nd = 1;
     cudaMemcpyToSymbol(g_norm_dev, &nd, 4);
-    printf("production prologue (stager + rms_norm): %d\n", rnd);
-    for (int t : {12, 384}) {
-        const char* l = t == 12 ? "qkv" : t == 4 ? "router" : "ffn_gu";
-        bench<4, 128>(t, 2048, l);
-        bench<4, 256>(t, 2048, l);
-    }
-    }
+    bench<4, 256>(12, 2048, "qkv");
+    bench<3, 512>(12, 2048, "qkv");
+    bench<2, 1024>(12, 2048, "qkv");
+    bench<4, 128>(384, 2048, "ffn_gu");
+    bench<3, 256>(384, 2048, "ffn_gu");
+    bench<2, 256>(384, 2048, "ffn_gu");
+    bench<2, 512>(384, 2048, "ffn_gu");
 }
