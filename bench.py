@@ -76,29 +76,59 @@ def token_stream(n: int, vocab: int, seed: int) -> np.ndarray:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region (NVML every
+    ~5 ms; nvidia-smi as the fallback).  One sampler can span several timed
+    regions: enter/exit pairs accumulate into the same sample list."""
+
+    _REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                0x4: "sw_power_cap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._th = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return (float(sm), float(mx), int(rs))
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        r = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                            "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                           timeout=5)
+        f = [x.strip() for x in r.stdout.strip().split(",")]
+        bits = 0
+        for i, bit in enumerate((0x8, 0x40, 0x20, 0x4)):
+            if len(f) > 2 + i and f[2 + i].lower() == "active":
+                bits |= bit
+        return (float(f[0]), float(f[1]), bits)
 
     def __enter__(self):
+        self._stop.clear()
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    r = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                        f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                       capture_output=True, text=True, timeout=5)
-                    if r.returncode == 0 and r.stdout.strip():
-                        self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+                    self.rows.append(self._sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.005 if self._nvml else 0.2)
         self._th = threading.Thread(target=run, daemon=True)
         self._th.start()
         return self
@@ -111,14 +141,22 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        reasons = sorted({name for r in self.rows for bit, name in self._REASONS.items()
+                          if r[2] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture summary
+    (tools/ncu_summary.py writes profiles/ncu_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        k = d["kernels"][kernel]
+        return k["dram_read_bytes"] + k["dram_write_bytes"]
+    except Exception:
+        return None
 
 
 def hbm_bytes_per_token(c: dict, P: int) -> dict:
@@ -175,7 +213,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
 
     def measure(mode: str, workload: str) -> dict:
         tpots, h2d, cms, hit, miss, recall = [], [], [], [], [], []
-        clk = None
+        clk = ClockSampler(dev)  # accumulates over every timed region of this mode
         for run in range(args.runs):
             S = P + args.warmup + args.steps
             s.reset(S, False)
@@ -184,13 +222,13 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                 if args.warmup:
                     s.decode_stream(mode, forced[: args.warmup])
                 s.clear_stats()
-                with ClockSampler(dev) as clk:
+                with clk:
                     s.decode_stream(mode, forced[args.warmup:])
             else:
                 if args.warmup:
                     s.decode(mode, args.warmup)
                 s.clear_stats()
-                with ClockSampler(dev) as clk:
+                with clk:
                     s.decode(mode, args.steps)
             ms = s.token_ms()
             tpots.append(float(np.mean(ms)))
@@ -207,7 +245,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                 recall.append(float(np.mean(rc)))
         return dict(tpot_ms=float(np.mean(tpots)), tpot_sd=float(np.std(tpots)), runs=tpots,
                     h2d_bytes_per_token=float(np.mean(h2d)), copy_busy_ms=float(np.mean(cms)),
-                    cache_hits=hit, cache_misses=miss, clocks=clk.summary() if clk else None,
+                    cache_hits=hit, cache_misses=miss, clocks=clk.summary(),
                     kernels_per_step=s.kernels_per_step(mode),
                     online_recall=float(np.mean(recall)) if recall else None)
 
@@ -244,8 +282,9 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                      logits)
         tok = nxt
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    slots = s.cache_slots()
     s.close()
-    return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init,
+    return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init, slots=slots,
                 t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P)
 
 
@@ -458,11 +497,13 @@ def main():
                           "formula": "max(copy_bytes/link_peak, hbm_bytes/hbm_peak)"},
         "roofline": {"bound": "hbm", "kernel": "k_ffn_gu (expert gate+up GEMV)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("k_ffn_gu"),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
+                                       "dram__bytes_read.sum + dram__bytes_write.sum per launch)",
                      "bytes_per_launch": gu_bytes, "avg_launch_us": gu_us,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
         "kernel_us": prof,
-        "cache": {"slots_per_layer": None, "hits_prefetch": pf["cache_hits"],
+        "cache": {"slots_per_layer": out.get("slots"), "hits_prefetch": pf["cache_hits"],
                   "misses_prefetch": pf["cache_misses"], "hits_on_demand": od["cache_hits"],
                   "misses_on_demand": od["cache_misses"]},
         "online_recall_at_k": pf["online_recall"],

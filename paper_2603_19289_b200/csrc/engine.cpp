@@ -386,8 +386,11 @@ void Session::free_all() {
     if (s_comp_) cudaStreamSynchronize(s_comp_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_side_) cudaStreamSynchronize(s_side_);
+    if (s_log_) cudaStreamSynchronize(s_log_);
     for (auto e : ev_fork_) cudaEventDestroy(e);
     for (auto e : ev_join_) cudaEventDestroy(e);
+    if (ev_side_end_) cudaEventDestroy(ev_side_end_);
+    if (ev_log_end_) cudaEventDestroy(ev_log_end_);
     ev_fork_.clear();
     ev_join_.clear();
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
@@ -412,7 +415,8 @@ void Session::free_all() {
     if (s_comp_) cudaStreamDestroy(s_comp_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
     if (s_side_) cudaStreamDestroy(s_side_);
-    s_comp_ = s_copy_ = s_side_ = nullptr;
+    if (s_log_) cudaStreamDestroy(s_log_);
+    s_comp_ = s_copy_ = s_side_ = s_log_ = nullptr;
 }
 
 void Session::drop_graphs() {
@@ -442,13 +446,22 @@ void Session::alloc() {
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&s_side_, cudaStreamNonBlocking), "stream");
+    {
+        // the side stream (routers / predictor) gets the highest priority, so
+        // its few CTAs are placed before pending expert-kernel CTAs
+        int lo = 0, hi = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+        ck(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
+        ck(cudaStreamCreateWithPriority(&s_log_, cudaStreamNonBlocking, lo), "stream");
+    }
     ev_fork_.resize(L);
     ev_join_.resize(L);
     for (int l = 0; l < L; ++l) {
         ck(cudaEventCreateWithFlags(&ev_fork_[l], cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&ev_join_[l], cudaEventDisableTiming), "event");
     }
+    ck(cudaEventCreateWithFlags(&ev_side_end_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_log_end_, cudaEventDisableTiming), "event");
 
     d_emb_ = static_cast<uint16_t*>(dalloc(2ull * V * H));
     d_unemb_ = static_cast<uint16_t*>(dalloc(2ull * m.Vp * H));
@@ -550,8 +563,11 @@ void Session::alloc() {
         st.pos = static_cast<int*>(dalloc(4));
         st.token = static_cast<int*>(dalloc(4));
         st.counters = static_cast<int*>(dalloc(4 * 64));
+        st.down_cnt = static_cast<int*>(dalloc(4ull * (m.Hp / 32)));
         st.ssq_x = static_cast<double*>(dalloc(8ull * (L + 1) * (m.Hp / 32)));
         st.ssq_r = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
+        st.rd = static_cast<float*>(dalloc(4ull * L * m.Hp));
+        st.ssq_rd = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.est_z = st.est_act = st.est_xn = nullptr;
     };
     mk_state(st_);
@@ -1033,6 +1049,7 @@ void Session::reset(int max_steps, int trace_full) {
     for (DevState* st : {&st_, &sh_}) {
         h2d(st->pos, &zero, 4, "reset");
         dset(st->counters, 0, 256, "reset");
+        dset(st->down_cnt, 0, 4ull * (dm_.Hp / 32), "reset");
     }
     h2d(ctl_.step, &zero, 4, "reset");
     // trace buffers
@@ -1109,24 +1126,34 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
     // The side work of layer l joins before the FFN of layer l+1 (which runs
     // the decision it produced) and before the end of the step.
     int pending_join = -1;
+    bool side_used = false, log_used = false;
     const bool tl = tl_ && is_main;  // timeline: CUDA events around each phase
     for (int l = 0; l < c.L; ++l) {
         const int t_attn = tl ? tl_begin(0, 0, l, s) : -1;
         ck(launch_qkv(dm_, st, l, s), "qkv");
         ck(launch_attn(dm_, st, d_attn_scratch_, l, s), "attn");
-        ck(launch_wo(dm_, st, l, s), "wo");
+        // prefetch, l >= 1: the decision executed here (predicted at l-1, on the
+        // side stream) is joined before k_wo, which then also forms
+        // rd_l = r_l + d_l for this layer's q_l (router-pf / est-pf)
+        const int kq = prefetch && l > 0 ? kind_at(l) : kNone;
+        const int quasi_ready = kq == kRouterPF || kq == kEstPF;
+        if (pending_join >= 0) {
+            ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
+            pending_join = -1;
+        }
+        ck(launch_wo(dm_, st, l, s, quasi_ready), "wo");
         if (tl) tl_end(t_attn, s);
         int exec_src = 0, s_from_r = 0;
         if (!prefetch) {
             const int t_gate = tl ? tl_begin(0, 1, l, s) : -1;
-            RouterLaunch rl{l, 1, kNone, 0, 1, 0, step_tag};
+            RouterLaunch rl{l, 1, kNone, 0, 1, 0, step_tag, 0};
             ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
             if (tl) tl_end(t_gate, s);
         } else {
             const int k = kind_at(l);
             if (l == 0) {
                 const int t_gate = tl ? tl_begin(0, 1, l, s) : -1;
-                RouterLaunch rl{0, 1, kNone, 0, 1, 0, step_tag};
+                RouterLaunch rl{0, 1, kNone, 0, 1, 0, step_tag, 0};
                 ck(launch_router(dm_, st, ctl_, rl, nullptr, s), "router");
                 if (tl) tl_end(t_gate, s);
             }
@@ -1135,17 +1162,34 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
             const int t_side = tl ? tl_begin(0, 1, l, s_side_) : -1;
             if (l == 0) {
                 if (k != kNone) {
-                    RouterLaunch rp{0, 0, k, -1, 0, k != kEstPF, step_tag};
+                    const int q0 = k == kRouterPF || k == kEstPF;
+                    if (q0) ck(launch_quasi_rd(dm_, st, 0, s_side_), "quasi");
+                    RouterLaunch rp{0, 0, k, -1, 0, k != kEstPF, step_tag, q0};
                     ck(launch_router(dm_, st, ctl_, rp, shadow, s_side_), "router");
                 }
             } else {
-                RouterLaunch rl{l, 1, k, 1, 0, k != kNone && k != kEstPF, step_tag};
-                ck(launch_router(dm_, st, ctl_, rl, shadow, s_side_), "router");
+                // the predictor first: its copy request and decision gate the
+                // next layer; the true router of this layer only feeds the
+                // hit-rate log, so it runs after the join point
+                RouterLaunch rp{l, 0, k, 1, 0, k != kNone && k != kEstPF, step_tag, quasi_ready};
+                ck(launch_router(dm_, st, ctl_, rp, shadow, s_side_), "router");
             }
             if (k == kEstPF) ck(launch_estimator(dm_, st, ctl_, l, 1, step_tag, s_side_), "estimator");
-            if (tl) tl_end(t_side, s_side_);
-            if (pending_join >= 0) ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
+            // joined before k_wo of the next layer (see above); kernels read the
+            // side stream's results only after their griddepcontrol.wait (a
+            // captured PDL launch makes even a cross-stream edge programmatic)
             ck(cudaEventRecord(ev_join_[l], s_side_), "join");
+            if (tl) tl_end(t_side, s_side_);
+            if (l > 0) {
+                // true router of layer l (speculation.cpp:370-371: logged every
+                // layer, never executed here) on the lowest-priority log stream,
+                // so it never delays the next predictor on the side stream
+                ck(cudaStreamWaitEvent(s_log_, ev_fork_[l], 0), "fork");
+                RouterLaunch rt{l, 1, kNone, -1, 0, 0, step_tag, 0};
+                ck(launch_router(dm_, st, ctl_, rt, nullptr, s_log_), "router");
+                log_used = true;
+            }
+            side_used = true;
             pending_join = l;
             if (l > 0) {
                 exec_src = 1;
@@ -1158,7 +1202,14 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
         if (calibrating) ck(launch_dv_accum(dm_, st, d_dv_sums_, d_dv_counts_, l, s), "dv");
         if (is_main && record && trace_full_ && tr_.cap > 0) ck(launch_trace_y(dm_, st, tr_, l, s), "trace");
     }
-    if (pending_join >= 0) ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
+    if (side_used) {  // everything on the side stream
+        ck(cudaEventRecord(ev_side_end_, s_side_), "join");
+        ck(cudaStreamWaitEvent(s, ev_side_end_, 0), "join");
+    }
+    if (log_used) {  // and the logging routers
+        ck(cudaEventRecord(ev_log_end_, s_log_), "join");
+        ck(cudaStreamWaitEvent(s, ev_log_end_, 0), "join");
+    }
     ck(launch_final(dm_, st, ctl_, record && is_main, s), "final");
     if (is_main && record && tr_.cap > 0) ck(launch_trace(dm_, st, tr_, s), "trace");
 }
@@ -1427,9 +1478,14 @@ cudaGraphExec_t Session::get_graph(int mode, int stream) {
     return exec;
 }
 
+// Kernels in one captured decode step: the teacher-forced (stream) graph if
+// it was built, else the greedy one; -1 before any graph exists.
 int Session::kernels_per_step(int mode) const {
-    auto it = graph_kernels_.find(mode * 10 + 1);
-    return it == graph_kernels_.end() ? -1 : it->second;
+    for (const long long key : {mode * 10 + 1 + 100LL, mode * 10 + 1LL}) {
+        auto it = graph_kernels_.find(key);
+        if (it != graph_kernels_.end()) return it->second;
+    }
+    return -1;
 }
 
 void Session::clear_stats() {
@@ -1459,7 +1515,7 @@ void Session::profile_kernels(int reps, double* out) {
                     case 1: ck(launch_attn(dm_, st_, d_attn_scratch_, l, s_comp_), "attn"); break;
                     case 2: ck(launch_wo(dm_, st_, l, s_comp_), "wo"); break;
                     case 3: {
-                        RouterLaunch rl{l, 1, kNone, -1, 0, 0, -9};
+                        RouterLaunch rl{l, 1, kNone, -1, 0, 0, -9, 0};
                         ck(launch_router(dm_, st_, ctl_, rl, nullptr, s_comp_), "router");
                         break;
                     }

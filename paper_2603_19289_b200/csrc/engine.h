@@ -253,7 +253,10 @@ private:
     float* h_logits_ = nullptr;
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
     cudaStream_t s_side_ = nullptr;               // routers/predictors in prefetch mode
+    cudaStream_t s_log_ = nullptr;                // logging-only true routers (lowest priority)
     std::vector<cudaEvent_t> ev_fork_, ev_join_;  // per layer
+    cudaEvent_t ev_side_end_ = nullptr;           // side stream fully done (before k_final)
+    cudaEvent_t ev_log_end_ = nullptr;            // log stream fully done (before k_final)
     std::vector<cudaEvent_t> ev_copy_;  // pairs
     std::vector<cudaEvent_t> ev_step_;  // pairs per decode step
     cudaEvent_t ev_origin_ = nullptr;

@@ -16,6 +16,46 @@
 #include "kernels.h"
 #include "smoe_chain.cuh"
 
+#ifdef SMOE_KTRACE
+// Device-side kernel timeline (instrumented builds only, tools/ktrace_run.py):
+// per (kernel kind, layer) the first CTA entry, the first CTA past its PDL
+// wait and the last CTA exit, in globaltimer ns, min/max over CTAs.
+namespace smoe {
+constexpr int kKtKinds = 16, kKtLayers = 128;
+__device__ unsigned long long g_kt[kKtKinds * kKtLayers][3];
+__device__ __forceinline__ unsigned long long kt_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct KTrace {
+    int slot;
+    __device__ KTrace(int kind, int layer) : slot(kind * kKtLayers + (layer & (kKtLayers - 1))) {
+        if (threadIdx.x == 0) atomicMin(&g_kt[slot][0], kt_now());
+    }
+    __device__ void waited() const {
+        if (threadIdx.x == 0) atomicMin(&g_kt[slot][1], kt_now());
+    }
+    __device__ ~KTrace() {
+        if (threadIdx.x == 0) atomicMax(&g_kt[slot][2], kt_now());
+    }
+};
+}  // namespace smoe
+extern "C" int smoe_ktrace_reset() {
+    static unsigned long long h[smoe::kKtKinds * smoe::kKtLayers][3];
+    for (auto& r : h) { r[0] = ~0ull; r[1] = ~0ull; r[2] = 0; }
+    return cudaMemcpyToSymbol(smoe::g_kt, h, sizeof(h)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int smoe_ktrace_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, smoe::g_kt, sizeof(smoe::g_kt)) == cudaSuccess ? 0 : 1;
+}
+#define KTRACE(kind, layer) const KTrace kt_(kind, layer)
+#define KT_WAITED() kt_.waited()
+#else
+#define KTRACE(kind, layer)
+#define KT_WAITED()
+#endif
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -42,84 +82,6 @@ __device__ bool last_cta(int* counter, int total) {
     return s_last != 0;
 }
 
-// -------------------------------------------------------------- decision --
-//
-// make_decision (model.cpp:258-274) for one logits row, executed by warp 0.
-// softmax (numerics.cpp:37-54): f32 max, f64 exp, f64 partition summed in
-// index order by lane 0 (exactly the reference's order), f32 probabilities;
-// top_k (numerics.cpp:56-70): value desc, lower index first; gates renormalised
-// by an f32 sum in rank order.  topk-softmax: top_k on logits, softmax of the k.
-__device__ void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
-                              double* se /*smem E*/, int* ids, float* gates) {
-    const int lane = threadIdx.x & 31;
-    const float* v = logits;
-    if (gating == kSoftmaxTopK) {
-        float mx = -INFINITY;
-        for (int i = lane; i < E; i += 32) mx = fmaxf(mx, v[i]);
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        for (int i = lane; i < E; i += 32)
-            se[i] = exp(static_cast<double>(v[i]) - static_cast<double>(mx));
-        __syncwarp();
-        double z = 0.0;
-        if (lane == 0)
-            for (int i = 0; i < E; ++i) z += se[i];
-        z = __shfl_sync(0xffffffffu, z, 0);
-        for (int i = lane; i < E; i += 32) sp[i] = static_cast<float>(se[i] / z);
-        __syncwarp();
-        v = sp;
-    }
-    // top-k by repeated warp argmax; selected entries marked in `taken` bits
-    unsigned taken_lo = 0;  // up to 32 elements per lane tracked by bit (E <= 1024)
-    int sel[kMaxK];
-    float val[kMaxK];
-    for (int t = 0; t < K; ++t) {
-        float bv = -INFINITY;
-        int bi = 0x7fffffff;
-        int j = 0;
-        for (int i = lane; i < E; i += 32, ++j) {
-            if (taken_lo & (1u << j)) continue;
-            const float x = v[i];
-            if (bi == 0x7fffffff || x > bv) {  // i increases: strict > keeps lower index
-                bv = x;
-                bi = i;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) {
-                bv = ov;
-                bi = oi;
-            }
-        }
-        sel[t] = bi;
-        val[t] = bv;
-        if ((bi & 31) == lane) taken_lo |= 1u << (bi >> 5);
-    }
-    if (lane == 0) {
-        if (gating == kSoftmaxTopK) {
-            float total = 0.0f;
-            for (int t = 0; t < K; ++t) total += val[t];
-            for (int t = 0; t < K; ++t) {
-                ids[t] = sel[t];
-                gates[t] = val[t] / total;
-            }
-        } else {
-            float mx = val[0];
-            for (int t = 0; t < K; ++t) mx = fmaxf(mx, val[t]);
-            double e[kMaxK], z = 0.0;
-            for (int t = 0; t < K; ++t) {
-                e[t] = exp(static_cast<double>(val[t]) - static_cast<double>(mx));
-                z += e[t];
-            }
-            for (int t = 0; t < K; ++t) {
-                ids[t] = sel[t];
-                gates[t] = static_cast<float>(e[t] / z);
-            }
-        }
-    }
-    __syncwarp();
-}
 
 // Mailbox post (single thread): request copies of `ids` for `layer`.
 __device__ void post_request(const DevCtl& ctl, int layer, int step, const int* ids, int k) {
@@ -197,7 +159,9 @@ __global__ void k_gen_bf16(uint64_t seed, double stddev, int R, int C, int tile_
 
 __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int* stream,
                         const int* step) {
+    KTRACE(0, 0);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int tok = stream ? stream[*step] : *token_src;
     if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
@@ -211,6 +175,7 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int
 // and k (model.cpp:309-321, cos/sin precomputed on the host with libm), k and v
 // appended to the layer's KV cache at `pos`.  One warp per 32-row tile.
 __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) {
+    KTRACE(1, layer);
     PHASE_DECL
     PHASE();
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
@@ -226,6 +191,7 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
     sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);
@@ -303,6 +269,7 @@ __device__ __forceinline__ void attn_fetch(float* dst, const float* src, int p0,
 
 __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, double* scratch,
                                                         int layer) {
+    KTRACE(2, layer);
     const int D = m.D, KS = D + 4;  // padded key row stride (floats)
     float* red = reinterpret_cast<float*>(g_smem);                     // [32]
     float* qs = reinterpret_cast<float*>(g_smem + 256);                // [kMaxD]
@@ -340,6 +307,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     }
     cp_async_commit();
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     // q and the current position's key/value row (written by k_qkv)
     for (int t = threadIdx.x; t < D / 4; t += blockDim.x) {
@@ -420,7 +388,29 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
-__global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
+// layer_default (speculation.cpp:104-117) for row j of a decision of K
+// experts: d_j = sum_i g_i * D[layer][e_i][j] in decision order (f32).  The K
+// loads (one coalesced 128-byte line per warp and expert) are all in flight.
+__device__ __forceinline__ float layer_default_row(const DevModel& m, const int* ids, const float* gts,
+                                                   int layer, int j) {
+    float dv[kMaxK], gv[kMaxK];
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i) {
+        if (i < m.K) {
+            const int e = __ldcg(ids + i);
+            gv[i] = __ldcg(gts + i);
+            dv[i] = __ldcg(m.dv + (static_cast<long long>(layer) * m.E + e) * m.H + j);
+        }
+    }
+    float d = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < m.K) d = d + gv[i] * dv[i];
+    return d;
+}
+
+__global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer, int rd_from_pred) {
+    KTRACE(3, layer);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* xr = xs + kMaxD;  // residual rows of this tile
@@ -431,17 +421,44 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer) {
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.ctx, m.D * 4);
     sg.add(xr, st.x + blockIdx.x * 32, 32 * 4);
-    sg.wait();
     const int rb = blockIdx.x;
+    const int j = rb * 32 + (threadIdx.x & 31);
+    // d_l of the decision predicted for this layer (for q_l), loaded while the
+    // context vector lands and the wo chain runs
+    const float d = rd_from_pred && j < m.H
+                        ? layer_default_row(m, st.id_pred + layer * m.K, st.g_pred + layer * m.K, layer, j)
+                        : 0.0f;
+    sg.wait();
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
     const float acc = pipe.run(tile, m.D, xs);
-    const int j = rb * 32 + (threadIdx.x & 31);
     const float r = j < m.H ? xr[threadIdx.x & 31] + acc : 0.0f;
     if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = r;
     warp_ssq_partial(r, st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32) + rb);
+    if (rd_from_pred) {  // rd_l = r_l + d_l (speculation.cpp:119-121) and its rms_norm partial
+        const float rd = j < m.H ? r + d : 0.0f;
+        if (j < m.H) st.rd[static_cast<long long>(layer) * m.Hp + j] = rd;
+        warp_ssq_partial(rd, st.ssq_rd + static_cast<long long>(layer) * (m.Hp / 32) + rb);
+    }
+}
+
+// rd_l = r_l + d_l of the executed decision (id_exec / g_exec) when it is only
+// known after k_wo (layer 0 in prefetch mode, where the true router decides):
+// grid Hp/32 x 32, launched on the side stream ahead of the predictor.
+__global__ void __launch_bounds__(32) k_quasi_rd(DevModel m, DevState st, int layer) {
+    pdl_wait();
+    pdl_trigger();
+    const int rb = blockIdx.x, j = rb * 32 + (threadIdx.x & 31);
+    float rd = 0.0f;
+    if (j < m.H) {
+        const float d = layer_default_row(m, st.id_exec + layer * m.K, st.g_exec + layer * m.K, layer, j);
+        rd = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j) + d;
+        st.rd[static_cast<long long>(layer) * m.Hp + j] = rd;
+    }
+    warp_ssq_partial(rd, st.ssq_rd + static_cast<long long>(layer) * (m.Hp / 32) + rb);
 }
 
 // ---------------------------------------------------------------- router --
@@ -482,31 +499,38 @@ __device__ void compute_quasi(const DevModel& m, const DevState& st, int layer, 
 
 __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl ctl,
                                                RouterLaunch rl, DevState sh, int has_shadow) {
+    KTRACE(rl.do_true ? 4 : 13, rl.layer);
+    PHASE_DECL
+    PHASE();
     const int H = m.H, E = m.E, K = m.K, l = rl.layer, Hr = round_up(H, 32);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* rs = xs + Hr;
     float* gs = rs + Hr;
-    float* dvs = gs + Hr;  // [K][Hr] (quasi CTAs only)
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(dvs + K * Hr));
+    // [K][Hr] default-vector rows, only for a q_l not prepared by k_wo (layer 0)
+    float* dvs = gs + Hr;
+    unsigned char* pipe_mem =
+        align128(reinterpret_cast<unsigned char*>(dvs + (rl.quasi_ready ? 0 : K * Hr)));
     const int nT = rl.do_true ? m.Ep / 32 : 0;
     const bool gemv_pred = rl.pred_kind == kBaselineS || rl.pred_kind == kRouterPF;
     const int nP = gemv_pred ? m.Ep / 32 : 0;
     const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
     const int b = blockIdx.x;
-    PipeBL pipe;
+    PipeR pipe;
     const uint16_t* tile = nullptr;
     if (b < nT + nP) {
         const bool is_true = b < nT;
         const int rb = is_true ? b : b - nT;
         tile = m.gate + (is_true ? l : l + 1) * m.gate_stride + static_cast<long long>(rb) * H * 32;
-        pipe.init(pipe_mem);
+        pipe.init(pipe_mem, kL2EvictLast);
         pipe.prime(tile, H);
     }
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    KT_WAITED();
+    PHASE();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     if (b < nT || (b < nT + nP && rl.pred_kind == kBaselineS)) {
         sg.add(rs, st.r + static_cast<long long>(l) * m.Hp, H * 4);
@@ -518,10 +542,20 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
         if (b == 0 && rl.do_true)
             for (int j = threadIdx.x; j < H; j += blockDim.x) st.s[static_cast<long long>(l) * m.Hp + j] = xs[j];
     } else if (b < nT + nP + nQ) {
-        compute_quasi(m, st, l, rl.exec_from, xs, rs, gs, dvs, red, sg);
+        if (rl.quasi_ready) {  // q_l = rms_norm(r_l + d_l, gain_{l+1}) from k_wo's rd_l
+            sg.add(rs, st.rd + static_cast<long long>(l) * m.Hp, H * 4);
+            sg.add(gs, m.moe_gain + static_cast<long long>(l + 1) * H, H * 4);
+            const float scale = rms_scale_from_partials(
+                st.ssq_rd + static_cast<long long>(l) * (m.Hp / 32), m.Hp / 32, H, m.eps);
+            sg.wait();
+            block_apply_norm(rs, gs, H, scale, xs);
+        } else {
+            compute_quasi(m, st, l, rl.exec_from, xs, rs, gs, dvs, red, sg);
+        }
         if (b == nT)
             for (int j = threadIdx.x; j < H; j += blockDim.x) st.quasi[j] = xs[j];
     }
+    PHASE();
     if (b < nT + nP) {
         const bool is_true = b < nT;
         const int rb = is_true ? b : b - nT;
@@ -534,41 +568,59 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
                 st.lg_pred[static_cast<long long>(l + 1) * E + e] = acc;
         }
     }
-    if (!last_cta(st.counters + 0, gridDim.x)) return;
-    // ---- finalize (one CTA, warp 0) ----
+    PHASE();
+    // ---- finalize: the true-router CTAs and the predictor CTAs each elect
+    // their own last CTA, so the two decisions run in parallel; the predictor's
+    // copy request is posted without waiting for the (logging-only) true one.
+    const bool in_true = b < nT;
+    const bool has_b = static_cast<int>(gridDim.x) > nT;  // predictor / quasi CTAs exist
+    if (!last_cta(st.counters + (in_true ? 0 : 4), in_true ? nT : gridDim.x - nT)) return;
+    PHASE();
     double* se = reinterpret_cast<double*>(pipe_mem);            // [E]
     float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);  // [E]
-    if (rl.do_true)
+    if (in_true) {
         warp_decision(st.lg_true + static_cast<long long>(l) * E, E, K, m.gating, sp, se,
                       st.id_true + l * K, st.g_true + l * K);
-    if (gemv_pred)
-        warp_decision(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, m.gating, sp, se,
-                      st.id_pred + (l + 1) * K, st.g_pred + (l + 1) * K);
-    if (threadIdx.x == 0) {
-        if (rl.pred_kind == kOracle && has_shadow) {  // Oracle: shadow true decisions (speculation.cpp:296-305)
-            for (int i = 0; i < K; ++i) {
-                st.id_pred[(l + 1) * K + i] = sh.id_true[(l + 1) * K + i];
-                st.g_pred[(l + 1) * K + i] = sh.g_true[(l + 1) * K + i];
-            }
-        }
-        if (rl.exec_from == 0) {
+        if (threadIdx.x == 0 && rl.exec_from == 0) {
             for (int i = 0; i < K; ++i) {
                 st.id_exec[l * K + i] = st.id_true[l * K + i];
                 st.g_exec[l * K + i] = st.g_true[l * K + i];
             }
-        } else if (rl.exec_from == 1) {
-            for (int i = 0; i < K; ++i) {
-                st.id_exec[l * K + i] = st.id_pred[l * K + i];
-                st.g_exec[l * K + i] = st.g_pred[l * K + i];
+            if (rl.post_exec && !ctl.resident) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
+        }
+    }
+    if (!in_true || !has_b) {
+        if (gemv_pred)
+            warp_decision(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, m.gating, sp, se,
+                          st.id_pred + (l + 1) * K, st.g_pred + (l + 1) * K);
+        if (threadIdx.x == 0) {
+            if (rl.pred_kind == kOracle && has_shadow) {  // Oracle: shadow true decisions (speculation.cpp:296-305)
+                for (int i = 0; i < K; ++i) {
+                    st.id_pred[(l + 1) * K + i] = sh.id_true[(l + 1) * K + i];
+                    st.g_pred[(l + 1) * K + i] = sh.g_true[(l + 1) * K + i];
+                }
+            }
+            if (rl.post_pred && !ctl.resident)
+                post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+            if (rl.exec_from == 1) {
+                for (int i = 0; i < K; ++i) {
+                    st.id_exec[l * K + i] = __ldcg(st.id_pred + l * K + i);
+                    st.g_exec[l * K + i] = __ldcg(st.g_pred + l * K + i);
+                }
             }
         }
-        if (rl.post_exec && !ctl.resident) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
-        if (rl.post_pred && !ctl.resident)
-            post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+        if (rl.pred_kind == kOracle && has_shadow)
+            for (int e = threadIdx.x; e < E; e += blockDim.x)
+                st.lg_pred[static_cast<long long>(l + 1) * E + e] = sh.lg_true[static_cast<long long>(l + 1) * E + e];
     }
-    if (rl.pred_kind == kOracle && has_shadow)
-        for (int e = threadIdx.x; e < E; e += blockDim.x)
-            st.lg_pred[static_cast<long long>(l + 1) * E + e] = sh.lg_true[static_cast<long long>(l + 1) * E + e];
+#ifdef SMOE_PHASES
+    PHASE();
+    if (threadIdx.x == 0) {
+        printf("router(last CTA %d, l=%d) [pdl, stage+norm, chain, lastcta, decide] (cycles):", blockIdx.x, l);
+        for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);
+        printf("\n");
+    }
+#endif
 }
 
 // --------------------------------------------------------------- estimator --
@@ -620,6 +672,7 @@ __device__ float expf_glibc(float x) {
 
 __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCtl ctl, int layer,
                                                   int stage, int post_pred, int step_tag) {
+    KTRACE(5 + stage, layer);
     const int dm = m.est_dm, mlp = m.est_mlp;
     float* xs = reinterpret_cast<float*>(g_smem);
     int cols;
@@ -651,6 +704,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, in, cols * 4);
     sg.wait();
@@ -705,7 +759,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
 __device__ void wait_ready(const DevCtl& ctl, int layer) {
     if (ctl.resident) return;
     if (threadIdx.x == 0) {
-        const int want = ctl.req_seq[layer];
+        const int want = __ldcg(ctl.req_seq + layer);
         const long long t0 = clock64();
         while (ld_acquire(ctl.ready + layer) < want) {
             if (*(volatile int*)ctl.error) break;
@@ -727,18 +781,17 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
 // here instead of reading the router's copy.
 __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src, int s_from_r) {
+    KTRACE(9, layer);
     PHASE_DECL
     PHASE();
-    pdl_wait();
-    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
-    PHASE();
+    pdl_wait();  // the decision may come from a side-stream kernel: read it only after this
+    KT_WAITED();
     const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
-    const int e = (exec_src ? st.id_pred : st.id_exec)[layer * m.K + i];
+    const int e = __ldcg((exec_src ? st.id_pred : st.id_exec) + layer * m.K + i);
     if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it
     wait_ready(ctl, layer);
     if (*(volatile int*)ctl.error) return;
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
-    double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* gs = xs + round_up(H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(H, 32)));
@@ -749,9 +802,13 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     }
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
+    // every CTA is past its copy wait: k_ffn_down may now read ids / slot_of and
+    // stream its weights before its own PDL wait
+    pdl_trigger();
     PipeB pipe;
-    pipe.init(pipe_mem);
+    pipe.init(pipe_mem, kL2EvictFirst);
     pipe.prime(tile, H);
+    PHASE();
     Stager sg;
     sg.init(bar);
     if (s_from_r) {
@@ -782,71 +839,124 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
 #endif
 }
 
-// down: grid Hp/32, K warps per CTA (warp i = i-th executed expert); then the
-// gate-weighted mixture in decision order (model.cpp:297-301) and the residual
-// x = r + m (model.cpp:386).
-__global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st, DevCtl ctl,
-                                                         int layer, int exec_src) {
-    pdl_wait();
-    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
-    if (*(volatile int*)ctl.error) return;
-    const int K = m.K, Hmp = m.Hmp, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
-    float* hs = reinterpret_cast<float*>(g_smem + 128);    // [K][Hmp]
-    float* ys = hs + K * Hmp;                                // [K][32]
-    float* rr = ys + K * 32;                                 // [32] residual rows
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(rr + 32));
-    PipeD pipe;
-    pipe.init(pipe_mem + w * PipeD::kBytes);
-    Stager sg;
-    sg.init(bar);
-    sg.add(hs, st.h, K * Hmp * 4);
-    sg.add(rr, st.r + static_cast<long long>(layer) * m.Hp + blockIdx.x * 32, 32 * 4);
-    sg.wait();
+// down: grid (Hp/32, K), one warp per (32-row block, executed expert), so the
+// 25 MB of Q30 down weights stream through every SM.  Each CTA writes its raw
+// expert rows y_i; the last of the K CTAs of a row block (device-scope arrival
+// counter, threadfence pattern) forms the gate-weighted mixture in decision
+// order (model.cpp:297-301), the residual x = r + m (model.cpp:386) and the
+// rms_norm partial of x for the next layer.
+__global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                 int exec_src) {
+    KTRACE(10, layer);
+    PHASE_DECL
+    PHASE();
+    // ids and slot_of are final once every k_ffn_gu CTA passed its copy wait
+    // (its PDL trigger point), so the weight stream starts before our PDL wait;
+    // h (written by k_ffn_gu) is read after it.
+    const int K = m.K, Hmp = m.Hmp, lane = threadIdx.x & 31, rb = blockIdx.x, i = blockIdx.y;
+    float* hs = reinterpret_cast<float*>(g_smem + 128);  // [Hmp] this expert's hidden state
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(hs + Hmp));
     const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
     const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
-    const int e = ids[w];
+    const int e = __ldcg(ids + i);
     const bool local = ctl.ep.world == 1 || e % ctl.ep.world == ctl.ep.rank;
-    const int slot = local ? __ldcg(m.slot_of + layer * m.E + e) : -1;
-    const int rb = blockIdx.x;
-    float acc = 0.0f;
-    if (local && slot < 0) {
-        if (lane == 0) atomicCAS(ctl.error, 0, 2000 + layer);
-    } else if (local) {
-        const uint16_t* tile = m.slots +
-                               (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
-                               m.gu_elems + static_cast<long long>(rb) * Hmp * 32;
-        acc = pipe.run(tile, m.Hm, hs + w * Hmp);
-    }
     const int j = rb * 32 + lane;
+    const int slot = local ? __ldcg(m.slot_of + layer * m.E + e) : 0;
+    PipeD pipe;
+    const uint16_t* tile = nullptr;
+    if (local && slot >= 0) {
+        tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems +
+               static_cast<long long>(rb) * Hmp * 32;
+        pipe.init(pipe_mem, kL2EvictFirst);
+        pipe.prime(tile, m.Hm);
+    }
+    pdl_wait();
+    KT_WAITED();
+    pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
+    PHASE();
+    if (*(volatile int*)ctl.error) return;
+    float acc = 0.0f;
+    if (local) {
+        if (slot < 0) {
+            if (lane == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+            return;
+        }
+        PHASE();
+        // h (written by k_ffn_gu, L2-resident): direct 16-byte loads, 8 in flight per lane
+        const float4* h4 = reinterpret_cast<const float4*>(st.h + static_cast<long long>(i) * Hmp);
+        for (int t0 = 0; t0 < Hmp / 4; t0 += 8 * 32) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * 32 + lane;
+                if (t < Hmp / 4) v[u] = __ldcg(h4 + t);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * 32 + lane;
+                if (t < Hmp / 4) reinterpret_cast<float4*>(hs)[t] = v[u];
+            }
+        }
+        __syncwarp();
+        PHASE();
+        acc = pipe.run(tile, m.Hm, hs);
+        PHASE();
+    }
     if (ctl.ep.world > 1) {
-        // EP: publish this rank's expert rows to every rank, then bump their
-        // per-layer arrival counters; k_ep_mix does the mixture.
+        // EP: the owning rank publishes these expert rows to every rank; every
+        // CTA of every rank (owner or not) then bumps every rank's per-layer
+        // arrival counter (world x K x Hp/32 arrivals per layer).  Counting
+        // non-owners too keeps the ranks within one layer of each other, which
+        // the layer-parity double buffer of the exchange relies on.
         if (local && j < m.H) {
-            const long long o = (static_cast<long long>(layer & 1) * K + w) * m.Hp + j;
+            const long long o = (static_cast<long long>(layer & 1) * K + i) * m.Hp + j;
             for (int p = 0; p < ctl.ep.world; ++p) __stcg(ctl.ep.xbuf[p] + o, acc);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        __syncwarp();
+        if (lane == 0) {
             __threadfence_system();
             for (int p = 0; p < ctl.ep.world; ++p) atomicAdd_system(ctl.ep.cnt[p] + layer, 1);
         }
         return;
     }
-    ys[w * 32 + lane] = acc;
-    if (j < m.H) st.y[static_cast<long long>(w) * m.Hp + j] = acc;
-    __syncthreads();
-    if (w == 0) {
-        float xv = 0.0f;
-        if (j < m.H) {
-            float out = 0.0f;
-            for (int i = 0; i < K; ++i) out += gts[i] * ys[i * 32 + lane];
-            st.m[static_cast<long long>(layer) * m.Hp + j] = out;
-            xv = rr[lane] + out;
-            st.x[j] = xv;
+    if (j < m.H) st.y[static_cast<long long>(i) * m.Hp + j] = acc;
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(st.down_cnt + rb, 1) == K - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    PHASE();
+    if (!last) return;
+    __threadfence();
+    if (lane == 0) st.down_cnt[rb] = 0;
+    float xv = 0.0f;
+    if (j < m.H) {
+        // all loads first (independent, one L2 round trip), then the mixture in
+        // decision order
+        float yv[kMaxK], gv[kMaxK];
+#pragma unroll
+        for (int q = 0; q < kMaxK; ++q) {
+            yv[q] = q < K ? __ldcg(st.y + static_cast<long long>(q) * m.Hp + j) : 0.0f;
+            gv[q] = q < K ? gts[q] : 0.0f;
         }
-        warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
+        const float rv = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j);
+        float out = 0.0f;
+#pragma unroll
+        for (int q = 0; q < kMaxK; ++q)
+            if (q < K) out += gv[q] * yv[q];
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        xv = rv + out;
+        st.x[j] = xv;
     }
+    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
+    PHASE();
+#ifdef SMOE_PHASES
+    if (rb == 0 && lane == 0) {
+        printf("ffn_down(last, expert %d) [pdl, ids+slot, stage, chain, y+fence+atomic, mix] (cycles):", i);
+        for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);
+        printf("\n");
+    }
+#endif
 }
 
 // EP combine: wait until every rank's down-projection CTAs of this layer have
@@ -855,13 +965,15 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down(DevModel m, DevState st
 // residual — identical arithmetic to the single-GPU epilogue.
 __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src) {
+    KTRACE(11, layer);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int K = m.K, lane = threadIdx.x & 31, rb = blockIdx.x, j = rb * 32 + lane;
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
         const long long target =
-            (static_cast<long long>(ctl.ep.epoch[layer]) + 1) * ctl.ep.world * gridDim.x;
+            (static_cast<long long>(ctl.ep.epoch[layer]) + 1) * ctl.ep.world * m.K * gridDim.x;
         const int* cnt = ctl.ep.cnt[ctl.ep.rank] + layer;
         const long long t0 = clock64();
         int ok = 1;
@@ -903,6 +1015,7 @@ __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl c
 // greedy argmax, first maximum (model.cpp:391-396).
 __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ctl,
                                               int record_token) {
+    KTRACE(12, 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
@@ -914,6 +1027,7 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
     Stager sg;
     sg.init(bar);
     pdl_wait();
+    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
     sg.add(gs, m.final_gain, m.H * 4);
@@ -1053,12 +1167,17 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // the stream's priority as a launch attribute, so it survives graph capture
+    int prio = 0;
+    cudaStreamGetPriority(s, &prio);
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = prio;
     static const bool no_pdl = std::getenv("SMOE_NO_PDL") != nullptr;  // diagnostics
-    cfg.attrs = attr;
-    cfg.numAttrs = no_pdl ? 0 : 1;
+    cfg.attrs = no_pdl ? attr + 1 : attr;
+    cfg.numAttrs = no_pdl ? 1 : 2;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 #define PDL(k, grid, block, smem, s, ...)                                   \
@@ -1081,19 +1200,18 @@ inline int gen_blocks(long long n) {
 size_t vec_bytes(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
 size_t qkv_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t wo_smem(const DevModel&) { return 128 + kMaxD * 4 + 32 * 4 + 128 + PipeB::kBytes; }
-size_t router_smem(const DevModel& m) {
-    const size_t head = 128 + (3 + static_cast<size_t>(m.K)) * vec_bytes(m.H) + 128;
-    return head + (PipeBL::kBytes > kMaxE * 12 ? PipeBL::kBytes : kMaxE * 12);
+// Router CTAs stay small enough (Q30: ~72 KB with q_l from k_wo) to co-reside
+// with three k_ffn_gu CTAs, so the side-stream router never waits for SM space.
+size_t router_smem(const DevModel& m, int quasi_ready) {
+    const size_t head = 128 + (3 + (quasi_ready ? 0 : static_cast<size_t>(m.K))) * vec_bytes(m.H) + 128;
+    return head + (PipeR::kBytes > kMaxE * 12 ? PipeR::kBytes : kMaxE * 12);
 }
 size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
     return vec_bytes(cols) + 64 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
 }
 size_t gu_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
-size_t down_smem(const DevModel& m) {
-    return 128 + static_cast<size_t>(m.K) * m.Hmp * 4 + m.K * 32 * 4 + 32 * 4 + 128 +
-           static_cast<size_t>(m.K) * PipeD::kBytes;
-}
+size_t down_smem(const DevModel& m) { return 128 + static_cast<size_t>(m.Hmp) * 4 + 128 + PipeD::kBytes; }
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
     size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * (2 * m.D + 4) * 4;
@@ -1108,7 +1226,7 @@ cudaError_t set_smem(const void* fn, size_t bytes) {
 }  // namespace
 
 int max_dynamic_smem_needed(const DevModel& m) {
-    size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m), est_smem(m), gu_smem(m), down_smem(m),
+    size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), gu_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
     size_t mx = 0;
     for (size_t x : v) mx = x > mx ? x : mx;
@@ -1147,7 +1265,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
                          (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
-                         (const void*)k_ep_mix};
+                         (const void*)k_ep_mix, (const void*)k_quasi_rd};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -1173,8 +1291,14 @@ cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, 
     return counted(1);
 }
 
-cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
-    PDL(k_wo, m.Hp / 32, 32, wo_smem(m), s, m, st, layer);
+cudaError_t launch_quasi_rd(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
+    PDL(k_quasi_rd, m.Hp / 32, 32, 0, s, m, st, layer);
+    return counted(1);
+}
+
+cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
+                      int rd_from_pred) {
+    PDL(k_wo, m.Hp / 32, 32, wo_smem(m), s, m, st, layer, rd_from_pred);
     return counted(1);
 }
 
@@ -1187,7 +1311,7 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
     int grid = nT + nP + nQ;
     if (grid < 1) grid = 1;
     DevState sh = shadow ? *shadow : st;
-    PDL(k_router, grid, 32, router_smem(m), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
+    PDL(k_router, grid, 32, router_smem(m, rl.quasi_ready), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
     return counted(1);
 }
 
@@ -1204,7 +1328,7 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
     PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
-    PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer, exec_src);
+    PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, exec_src);
     if (ctl.ep.world > 1) {
         PDL(k_ep_mix, m.Hp / 32, 32, 0, s, m, st, ctl, layer, exec_src);
         g_launches += 1;
@@ -1217,7 +1341,7 @@ cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl&
     if (part == 0)
         PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, 0, 0);
     else
-        PDL(k_ffn_down, m.Hp / 32, 32 * m.K, down_smem(m), s, m, st, ctl, layer, 0);
+        PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, 0);
     return counted(1);
 }
 

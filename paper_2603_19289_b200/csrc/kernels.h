@@ -27,6 +27,7 @@ struct RouterLaunch {
     int post_exec;      // post (layer, exec ids) to the mailbox
     int post_pred;      // post (layer+1, pred ids) to the mailbox
     int step_tag;       // mailbox step tag
+    int quasi_ready;    // st.rd / ssq_rd of `layer` hold r_l + d_l (k_wo computed them)
 };
 
 // token = stream ? stream[*step] : *token_src (stream: teacher-forced decode input)
@@ -35,7 +36,12 @@ cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token
 cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s);
-cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
+// rd_from_pred: also form rd_l = r_l + d_l from the decision predicted for
+// `layer` (id_pred / g_pred), for the predictor's q_l.
+cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
+                      int rd_from_pred = 0);
+// rd_l = r_l + d_l of the executed decision (id_exec) after the true router
+cudaError_t launch_quasi_rd(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
 cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& ctl,
                           const RouterLaunch& rl, const DevState* shadow, cudaStream_t s);
 cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl& ctl,

@@ -34,6 +34,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// L2 eviction-priority hints for weight streams (createpolicy): expert
+// weights are read once per token and marked evict-first, so the dense
+// per-layer weights (router gates, attention) keep their L2 residency.
+enum L2Hint : int { kL2Normal = 0, kL2EvictFirst = 1, kL2EvictLast = 2 };
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+    uint64_t p = 0;
+    if (hint == kL2EvictFirst)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else if (hint == kL2EvictLast)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -210,6 +230,7 @@ __device__ __forceinline__ void block_apply_norm(const float* v, const float* ga
     const float4* v4 = reinterpret_cast<const float4*>(v);
     const float4* g4 = reinterpret_cast<const float4*>(gain);
     float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll 4
     for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x) {
         const float4 t = v4[i], g = g4[i];
         o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z, t.w * scale * g.w);
@@ -394,7 +415,11 @@ struct WarpPipe {
     int ctr;         // chunks consumed so far (phase tracking)
     int primed;      // chunks already issued for the next run()
 
-    __device__ void init(unsigned char* smem) {  // call with the owning warp; then syncwarp
+    uint64_t policy;  // L2 hint for the weight stream (0 with hint kL2Normal)
+    int hinted;
+    __device__ void init(unsigned char* smem, int hint = kL2Normal) {  // owning warp; then syncwarp
+        hinted = hint != kL2Normal;
+        policy = hinted ? l2_policy(hint) : 0;
         buf = reinterpret_cast<WT*>(smem);
         sbuf = smem_u32(smem);
         full = reinterpret_cast<uint64_t*>(smem + S * kChunkBytes);
@@ -413,7 +438,11 @@ struct WarpPipe {
         const int cn = min(CC, round_up(cols, G) - c0);
         const uint32_t bytes = static_cast<uint32_t>(cn) * 32u * sizeof(WT);
         mbar_expect_tx(&full[st], bytes);
-        bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
+        if (hinted)
+            bulk_g2s_hint(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st],
+                          policy);
+        else
+            bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
     }
 
     // Issue the first chunks of `tile` before the input vector exists (weights
@@ -509,10 +538,125 @@ struct WarpPipe {
 constexpr int kS = 4;       // stages per warp
 constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
 constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
-constexpr int kCCd = 64;    // down-projection columns per chunk (4 KB)
+constexpr int kCCd = 192;   // down-projection columns per chunk (12 KB: a 768-column Q30 tile = 4 chunks, all in flight)
 using PipeB = WarpPipe<uint16_t, kS, kCCb>;
 using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
 using PipeF = WarpPipe<float, kS, kCCf>;
 using PipeD = WarpPipe<uint16_t, kS, kCCd>;
+using PipeR = WarpPipe<uint16_t, 3, 256>;  // router: 48 KB, fits beside three k_ffn_gu CTAs
+
+// -------------------------------------------------------------- decision --
+//
+// make_decision (model.cpp:258-274) for one logits row, executed by warp 0.
+// softmax (numerics.cpp:37-54): f32 max, f64 exp, f64 partition summed in
+// index order by lane 0 (exactly the reference's order), f32 probabilities;
+// top_k (numerics.cpp:56-70): value desc, lower index first; gates renormalised
+// by an f32 sum in rank order.  topk-softmax: top_k on logits, softmax of the k.
+__device__ void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
+                              double* se /*smem E*/, int* ids, float* gates) {
+    const int lane = threadIdx.x & 31;
+    // logits were written by other CTAs: L2 loads, all in flight, into smem
+    for (int i0 = 0; i0 < E; i0 += 8 * 32) {
+        float t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * 32 + lane;
+            t[u] = i < E ? __ldcg(logits + i) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * 32 + lane;
+            if (i < E) sp[i] = t[u];
+        }
+    }
+    __syncwarp();
+    if (gating == kSoftmaxTopK) {
+        float mx = -INFINITY;
+        for (int i = lane; i < E; i += 32) mx = fmaxf(mx, sp[i]);
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        // independent f64 exps per lane, 8 in flight (the routine is a long
+        // dependent DFMA chain)
+        for (int i0 = 0; i0 < E; i0 += 8 * 32) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < E) se[i] = exp(static_cast<double>(sp[i]) - static_cast<double>(mx));
+            }
+        }
+        __syncwarp();
+        double z = 0.0;
+        if (lane == 0)  // f64 partition in index order, as numerics.cpp:46-49
+            for (int i = 0; i < E; ++i) z += se[i];
+        z = __shfl_sync(0xffffffffu, z, 0);
+        for (int i0 = 0; i0 < E; i0 += 8 * 32) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < E) sp[i] = static_cast<float>(se[i] / z);
+            }
+        }
+        __syncwarp();
+    }
+    // top_k (numerics.cpp:56-70): value descending, lower index first on ties.
+    // Rank of element i = #{j : v_j > v_i or (v_j == v_i and j < i)}; the
+    // elements of rank < K are the selection, in rank order.  All lanes rank
+    // their elements in parallel against broadcast smem reads.
+    __shared__ int s_sel[kMaxK];
+    __shared__ float s_val[kMaxK];
+    for (int i0 = 0; i0 < E; i0 += 4 * 32) {
+        float x[4];
+        int rank[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * 32 + lane;
+            x[u] = i < E ? sp[i] : 0.0f;
+            rank[u] = 0;
+        }
+        for (int j = 0; j < E; ++j) {
+            const float y = sp[j];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * 32 + lane;
+                rank[u] += (y > x[u]) | ((y == x[u]) & (j < i));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * 32 + lane;
+            if (i < E && rank[u] < K) {
+                s_sel[rank[u]] = i;
+                s_val[rank[u]] = x[u];
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        if (gating == kSoftmaxTopK) {  // gates renormalised by an f32 sum in rank order
+            float total = 0.0f;
+            for (int t = 0; t < K; ++t) total += s_val[t];
+            for (int t = 0; t < K; ++t) {
+                ids[t] = s_sel[t];
+                gates[t] = s_val[t] / total;
+            }
+        } else {  // topk-softmax: softmax of the k selected logits (f64 exp, f32 out)
+            float mx = s_val[0];
+            for (int t = 0; t < K; ++t) mx = fmaxf(mx, s_val[t]);
+            double e[kMaxK], z = 0.0;
+#pragma unroll
+            for (int t = 0; t < kMaxK; ++t)
+                if (t < K) e[t] = exp(static_cast<double>(s_val[t]) - static_cast<double>(mx));
+#pragma unroll
+            for (int t = 0; t < kMaxK; ++t)
+                if (t < K) z += e[t];
+#pragma unroll
+            for (int t = 0; t < kMaxK; ++t)
+                if (t < K) {
+                    ids[t] = s_sel[t];
+                    gates[t] = static_cast<float>(e[t] / z);
+                }
+        }
+    }
+    __syncwarp();
+}
 
 }  // namespace smoe

@@ -115,11 +115,18 @@ struct DevState {
     int* pos;          // position
     int* token;        // current token
     int* counters;     // last-CTA counters [64]
+    int* down_cnt;     // [Hp/32] k_ffn_down per-row-block arrival counters (self-resetting)
     // rms_norm statistics, computed by the kernel that produces the vector:
     // f64 partial sums of squares per 32-row block (Hp/32 per vector), summed
     // by consumers in a fixed order (rms_scale_from_partials).
     double* ssq_x;     // [L+1][Hp/32]  x entering layer l (index L: final norm)
     double* ssq_r;     // [L][Hp/32]    r_l (pre-MoE residual)
+    // q_l prologue fused into k_wo when the executed decision of layer l is
+    // known before it (prefetch mode, l >= 1): rd_l = r_l + d_l with d_l the
+    // layer_default of that decision (speculation.cpp:104-121), and its
+    // rms_norm partials; the predictor then only scales it (gain_{l+1}).
+    float* rd;         // [L][Hp]
+    double* ssq_rd;    // [L][Hp/32]
 };
 
 // Expert parallelism: expert e of every layer lives on rank
