@@ -567,6 +567,8 @@ void Session::alloc() {
         st.ssq_x = static_cast<double*>(dalloc(8ull * (L + 1) * (m.Hp / 32)));
         st.ssq_r = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.rd = static_cast<float*>(dalloc(4ull * L * m.Hp));
+        st.pass_id = static_cast<int*>(dalloc(4));
+        st.dec_ready = static_cast<int*>(dalloc(4ull * L));
         st.ssq_rd = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.est_z = st.est_act = st.est_xn = nullptr;
     };
@@ -1179,6 +1181,8 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
             // side stream's results only after their griddepcontrol.wait (a
             // captured PDL launch makes even a cross-stream edge programmatic)
             ck(cudaEventRecord(ev_join_[l], s_side_), "join");
+            if (k != kNone && l + 1 < c.L && l2_prefetch_)  // warm L2 with layer l+1's experts
+                ck(launch_l2_prefetch(dm_, st, ctl_, l + 1, s_side_), "l2 prefetch");
             if (tl) tl_end(t_side, s_side_);
             if (l > 0) {
                 // true router of layer l (speculation.cpp:370-371: logged every

@@ -19,6 +19,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -254,6 +255,9 @@ private:
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
     cudaStream_t s_side_ = nullptr;               // routers/predictors in prefetch mode
     cudaStream_t s_log_ = nullptr;                // logging-only true routers (lowest priority)
+    // L2 warm-up of the next layer's experts (k_l2_prefetch): measured slower on Q30
+    // (competes with the attention kernels for HBM), so off unless requested
+    bool l2_prefetch_ = std::getenv("SMOE_L2_PREFETCH") != nullptr;
     std::vector<cudaEvent_t> ev_fork_, ev_join_;  // per layer
     cudaEvent_t ev_side_end_ = nullptr;           // side stream fully done (before k_final)
     cudaEvent_t ev_log_end_ = nullptr;            // log stream fully done (before k_final)

@@ -83,6 +83,14 @@ __device__ bool last_cta(int* counter, int total) {
 }
 
 
+// The decision for `layer` (and its copy request) is complete: release it to
+// the expert kernel of `layer`, which may start before its own PDL wait.
+__device__ __forceinline__ void publish_decision(const DevState& st, int layer) {
+    __threadfence();
+    const int p = __ldcg(st.pass_id);
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(st.dec_ready + layer), "r"(p) : "memory");
+}
+
 // Mailbox post (single thread): request copies of `ids` for `layer`.
 __device__ void post_request(const DevCtl& ctl, int layer, int step, const int* ids, int k) {
     const int seq = *ctl.req_counter + 1;
@@ -164,7 +172,10 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int
     KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     const int tok = stream ? stream[*step] : *token_src;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *st.token = tok;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *st.token = tok;
+        *st.pass_id = *st.pass_id + 1;  // read by later kernels of this pass only
+    }
     const int j = blockIdx.x * 32 + threadIdx.x;  // grid Hp/32 x 32
     const float v = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
     st.x[j] = v;
@@ -602,6 +613,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
             }
             if (rl.post_pred && !ctl.resident)
                 post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+            if ((gemv_pred || rl.pred_kind == kOracle) && l + 1 < m.L) publish_decision(st, l + 1);
             if (rl.exec_from == 1) {
                 for (int i = 0; i < K; ++i) {
                     st.id_exec[l * K + i] = __ldcg(st.id_pred + l * K + i);
@@ -748,6 +760,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
                   se, st.id_pred + (layer + 1) * m.K, st.g_pred + (layer + 1) * m.K);
     if (threadIdx.x == 0 && post_pred && !ctl.resident)
         post_request(ctl, layer + 1, step_tag, st.id_pred + (layer + 1) * m.K, m.K);
+    if (threadIdx.x == 0 && layer + 1 < m.L) publish_decision(st, layer + 1);
 }
 
 // ------------------------------------------------------------- expert FFN --
@@ -784,8 +797,33 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     KTRACE(9, layer);
     PHASE_DECL
     PHASE();
-    pdl_wait();  // the decision may come from a side-stream kernel: read it only after this
-    KT_WAITED();
+    // prefetch mode: the executed decision was published by the predictor of
+    // layer l-1 on the side stream (publish_decision); wait for that flag, not
+    // for the PDL edge, and start the copy wait and weight stream before the
+    // PDL wait, overlapping the attention tail.  On-demand: the router of this
+    // layer (our predecessor) decides, so wait for it first.
+    const bool early = exec_src != 0;
+    if (early) {
+        if (threadIdx.x == 0) {
+            const int want = __ldcg(st.pass_id);
+            const long long t0 = clock64();
+            for (;;) {
+                int v;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(st.dec_ready + layer) : "memory");
+                if (v == want) break;
+                if (*(volatile int*)ctl.error) break;
+                if (clock64() - t0 > ctl.spin_limit) {
+                    atomicCAS(ctl.error, 0, 1000 + layer);
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        __syncwarp();
+    } else {
+        pdl_wait();
+        KT_WAITED();
+    }
     const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
     const int e = __ldcg((exec_src ? st.id_pred : st.id_exec) + layer * m.K + i);
     if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it
@@ -802,12 +840,16 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     }
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
-    // every CTA is past its copy wait: k_ffn_down may now read ids / slot_of and
-    // stream its weights before its own PDL wait
-    pdl_trigger();
     PipeB pipe;
     pipe.init(pipe_mem, kL2EvictFirst);
     pipe.prime(tile, H);
+    if (early) {
+        pdl_wait();
+        KT_WAITED();
+    }
+    // every CTA is past its copy wait: k_ffn_down may now read ids / slot_of and
+    // stream its weights before its own PDL wait
+    pdl_trigger();
     PHASE();
     Stager sg;
     sg.init(bar);
@@ -957,6 +999,34 @@ __global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl
         printf("\n");
     }
 #endif
+}
+
+// L2 prefetch of the experts a decision will execute (prefetch mode): issued on
+// the side stream right after the predictor of layer l-1, it streams layer l's
+// resident expert blocks (cache hits; misses are still in flight over PCIe and
+// are skipped) into L2 while the attention of layer l runs, so the expert
+// kernels of layer l read L2 instead of HBM.  grid (parts, K), one thread
+// issues cp.async.bulk.prefetch.L2 (SASS UBLKPF) in 64 KB pieces.
+__global__ void __launch_bounds__(32) k_l2_prefetch(DevModel m, DevState st, DevCtl ctl, int layer) {
+    KTRACE(14, layer);
+    pdl_wait();
+    KT_WAITED();
+    pdl_trigger();
+    if (threadIdx.x != 0) return;
+    const int i = blockIdx.y;
+    const int e = __ldcg(st.id_pred + layer * m.K + i);
+    if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    if (slot < 0) return;  // not resident yet (copy in flight)
+    const char* base = reinterpret_cast<const char*>(
+        m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems);
+    const long long bytes = m.expert_elems * 2;
+    const long long part = ((bytes + gridDim.x - 1) / gridDim.x + 15) / 16 * 16;
+    const long long b0 = part * blockIdx.x, b1 = min(bytes, b0 + part);
+    for (long long o = b0; o < b1; o += 65536) {
+        const uint32_t n = static_cast<uint32_t>(min(65536LL, b1 - o)) & ~15u;
+        if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(n) : "memory");
+    }
 }
 
 // EP combine: wait until every rank's down-projection CTAs of this layer have
@@ -1265,7 +1335,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
                          (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
-                         (const void*)k_ep_mix, (const void*)k_quasi_rd};
+                         (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -1288,6 +1358,12 @@ cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStr
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
     PDL(k_attn, 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
+    return counted(1);
+}
+
+cudaError_t launch_l2_prefetch(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                               cudaStream_t s) {
+    PDL(k_l2_prefetch, dim3(16, m.K), 32, 0, s, m, st, ctl, layer);
     return counted(1);
 }
 

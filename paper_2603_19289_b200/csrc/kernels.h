@@ -40,6 +40,9 @@ cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, 
 // `layer` (id_pred / g_pred), for the predictor's q_l.
 cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
                       int rd_from_pred = 0);
+// L2 prefetch of the resident expert blocks of the decision predicted for `layer`
+cudaError_t launch_l2_prefetch(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                               cudaStream_t s);
 // rd_l = r_l + d_l of the executed decision (id_exec) after the true router
 cudaError_t launch_quasi_rd(const DevModel& m, const DevState& st, int layer, cudaStream_t s);
 cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& ctl,

@@ -126,6 +126,11 @@ struct DevState {
     // layer_default of that decision (speculation.cpp:104-121), and its
     // rms_norm partials; the predictor then only scales it (gain_{l+1}).
     float* rd;         // [L][Hp]
+    // decision handshake for the expert kernels' early start (prefetch mode):
+    // k_embed bumps pass_id at every pass; the predictor that decides layer l
+    // publishes dec_ready[l] = pass_id after the decision and its copy request
+    int* pass_id;      // [1]
+    int* dec_ready;    // [L]
     double* ssq_rd;    // [L][Hp/32]
 };
 
