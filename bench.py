@@ -250,6 +250,10 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                     online_recall=float(np.mean(recall)) if recall else None)
 
     res = {}
+    if args.ncu:  # profiling pass: the headline workload's decode steps only
+        res[args.workload] = {mode: measure(mode, args.workload) for mode in ("on_demand", "prefetch")}
+        s.close()
+        return dict(res=res, ncu=True)
     for wl in ("stream", "greedy"):
         res[wl] = {mode: measure(mode, wl) for mode in ("on_demand", "prefetch")}
     # lane breakdown (reference e2e output: per_token_reports + breakdown) from a
@@ -367,10 +371,16 @@ def main():
     ap.add_argument("--ref-prompt", type=int, default=4)
     ap.add_argument("--ref-new", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling pass for the ncu launch list: experts resident (ncu serialises "
+                         "the copy lane), headline workload only, no kernel/link/e2e extras; the "
+                         "printed line is not a bench value")
     ap.add_argument("--workload", default="stream", choices=["stream", "greedy"],
                     help="stream: decode inputs teacher-forced from a random token stream "
                          "(headline; exercises the offload path); greedy: argmax feedback")
     args = ap.parse_args()
+    if args.ncu:
+        args.cache_fraction, args.runs, args.no_cpu_baseline = 1.0, 1, True
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -418,6 +428,12 @@ def main():
         dist.init_process_group("gloo", init_method="env://")
         dist.barrier()
     out = run_ours(args, rank, world)
+    if out.get("ncu"):
+        if rank == 0:
+            r = out["res"][args.workload]
+            print(json.dumps({"ncu_profile_pass": True, "not_a_bench_value": True,
+                              "tpot_ms_under_ncu": {m: r[m]["tpot_ms"] for m in r}}))
+        return
     if world > 1:
         import torch.distributed as dist
         gathered = [None] * world

@@ -1,0 +1,46 @@
+"""Arithmetic-order guards on the compiled sm_100a code (CPU-only: cuobjdump).
+
+The kernels reproduce the reference's separately rounded `acc += w * x`
+(numerics.cpp:136-147).  Packed products (FMUL2) are used, but ptxas contracts
+an FMUL2 feeding a packed add into FFMA2 even for the _rn intrinsics, which
+would fuse the rounding; the library must therefore contain no FFMA2, and the
+chain kernels must contain the FMUL2 / FADD pair the design relies on."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+OBJ = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                   "paper_2603_19289_b200", "csrc", "build", "kernels.o")
+
+
+def _sass():
+    if not os.path.exists(OBJ) or not shutil.which("cuobjdump"):
+        pytest.skip("kernels.o or cuobjdump not available")
+    return subprocess.run(["cuobjdump", "-sass", OBJ], capture_output=True, text=True,
+                          check=True).stdout
+
+
+def _functions(sass):
+    out, cur = {}, None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            cur = line.split("Function :")[1].strip()
+            out[cur] = []
+        elif cur:
+            out[cur].append(line)
+    return out
+
+
+def test_no_packed_fma_anywhere():
+    sass = _sass()
+    assert "FFMA2" not in sass
+
+
+def test_chain_kernels_use_separate_products_and_adds():
+    fns = _functions(_sass())
+    for short in ("k_qkv", "k_ffn_gu", "k_ffn_down", "k_router", "k_final", "k_wo"):
+        body = "\n".join(next(v for k, v in fns.items() if short in k))
+        assert "FMUL2" in body, short
+        assert "FADD" in body, short
