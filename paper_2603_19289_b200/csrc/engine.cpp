@@ -569,6 +569,8 @@ void Session::alloc() {
         st.rd = static_cast<float*>(dalloc(4ull * L * m.Hp));
         st.pass_id = static_cast<int*>(dalloc(4));
         st.dec_ready = static_cast<int*>(dalloc(4ull * L));
+        st.gu_done = static_cast<int*>(dalloc(4ull * L * K));
+        st.ffn_epoch = static_cast<int*>(dalloc(4ull * L));
         st.ssq_rd = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.est_z = st.est_act = st.est_xn = nullptr;
     };

@@ -627,11 +627,10 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     }
 #ifdef SMOE_PHASES
     PHASE();
-    if (threadIdx.x == 0) {
-        printf("router(last CTA %d, l=%d) [pdl, stage+norm, chain, lastcta, decide] (cycles):", blockIdx.x, l);
-        for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);
-        printf("\n");
-    }
+    if (threadIdx.x == 0)
+        phase_print(rl.do_true ? "true router [pdl, stage+norm, chain, lastcta, decide]"
+                               : "predictor [pdl, stage+norm, chain, lastcta, decide]",
+                    ph_, nph_);
 #endif
 }
 
@@ -792,9 +791,46 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
 // run concurrently on a side stream (Alg. 1: the predicted experts are known
 // before the layer starts).  s_from_r: compute s_l = rms_norm(r_l, moe_gain_l)
 // here instead of reading the router's copy.
-__global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
-                                               int exec_src, int s_from_r) {
+// Wait (thread 0) until the predictor of layer-1 published this layer's
+// decision for the current pass (publish_decision).
+__device__ __forceinline__ void wait_decision(const DevState& st, const DevCtl& ctl, int layer) {
+    if (threadIdx.x == 0) {
+        const int want = __ldcg(st.pass_id);
+        const long long t0 = clock64();
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(st.dec_ready + layer) : "memory");
+            if (v == want) break;
+            if (*(volatile int*)ctl.error) break;
+            if (clock64() - t0 > ctl.spin_limit) {
+                atomicCAS(ctl.error, 0, 1000 + layer);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncwarp();
+}
+
+// gate/up role of one (16-row block rb, executed expert i).  `fused`: the down
+// role runs in the same grid and waits on gu_done[layer][i].
+__device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                                            int layer, int exec_src, int s_from_r, int rb, int i,
+                                            bool fused) {
     KTRACE(9, layer);
+    // counts this CTA towards gu_done[layer][i] on every exit path, so a down
+    // CTA never waits for a gate/up CTA that left early (EP peer expert, error)
+    struct Done {
+        const DevState& st;
+        int idx;
+        bool on;
+        __device__ ~Done() {
+            if (on && threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(st.gu_done + idx, 1);
+            }
+        }
+    } done{st, layer * m.K + i, fused};
     PHASE_DECL
     PHASE();
     // prefetch mode: the executed decision was published by the predictor of
@@ -804,27 +840,12 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     // layer (our predecessor) decides, so wait for it first.
     const bool early = exec_src != 0;
     if (early) {
-        if (threadIdx.x == 0) {
-            const int want = __ldcg(st.pass_id);
-            const long long t0 = clock64();
-            for (;;) {
-                int v;
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(st.dec_ready + layer) : "memory");
-                if (v == want) break;
-                if (*(volatile int*)ctl.error) break;
-                if (clock64() - t0 > ctl.spin_limit) {
-                    atomicCAS(ctl.error, 0, 1000 + layer);
-                    break;
-                }
-                __nanosleep(64);
-            }
-        }
-        __syncwarp();
+        wait_decision(st, ctl, layer);
     } else {
         pdl_wait();
         KT_WAITED();
     }
-    const int H = m.H, i = blockIdx.y, rb = blockIdx.x;
+    const int H = m.H;
     const int e = __ldcg((exec_src ? st.id_pred : st.id_exec) + layer * m.K + i);
     if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it
     wait_ready(ctl, layer);
@@ -879,6 +900,12 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
         printf("ffn_gu chain waits (cycles): %lld\n", pipe.wait_cyc);
 #endif
+    if (fused) __syncwarp();  // h rows written by every lane before the count (Done)
+}
+
+__global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
+                                               int exec_src, int s_from_r) {
+    ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false);
 }
 
 // down: grid (Hp/32, K), one warp per (32-row block, executed expert), so the
@@ -887,15 +914,26 @@ __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl c
 // counter, threadfence pattern) forms the gate-weighted mixture in decision
 // order (model.cpp:297-301), the residual x = r + m (model.cpp:386) and the
 // rms_norm partial of x for the next layer.
-__global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl ctl, int layer,
-                                                 int exec_src) {
+__device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState& st, const DevCtl& ctl,
+                                              int layer, int exec_src, int rb, int i, bool fused,
+                                              int gu_target) {
     KTRACE(10, layer);
     PHASE_DECL
     PHASE();
-    // ids and slot_of are final once every k_ffn_gu CTA passed its copy wait
-    // (its PDL trigger point), so the weight stream starts before our PDL wait;
-    // h (written by k_ffn_gu) is read after it.
-    const int K = m.K, Hmp = m.Hmp, lane = threadIdx.x & 31, rb = blockIdx.x, i = blockIdx.y;
+    // separate kernel: ids and slot_of are final once every k_ffn_gu CTA passed
+    // its copy wait (its PDL trigger point), so the weight stream starts before
+    // our PDL wait; fused grid: this CTA waits for the decision and the copy
+    // itself, and for the gate/up CTAs of its expert (gu_done) before reading h.
+    const int K = m.K, Hmp = m.Hmp, lane = threadIdx.x & 31;
+    if (fused) {
+        if (exec_src != 0) {
+            wait_decision(st, ctl, layer);
+        } else {
+            pdl_wait();
+            KT_WAITED();
+        }
+        wait_ready(ctl, layer);
+    }
     float* hs = reinterpret_cast<float*>(g_smem + 128);  // [Hmp] this expert's hidden state
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(hs + Hmp));
     const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
@@ -916,6 +954,22 @@ __global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl
     KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     PHASE();
+    if (fused && local && threadIdx.x == 0) {  // the gate/up CTAs of this expert are done
+        const int* cnt = st.gu_done + layer * K + i;
+        const long long t0 = clock64();
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            if (v >= gu_target) break;
+            if (*(volatile int*)ctl.error) break;
+            if (clock64() - t0 > ctl.spin_limit) {
+                atomicCAS(ctl.error, 0, 1000 + layer);
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    __syncwarp();
     if (*(volatile int*)ctl.error) return;
     float acc = 0.0f;
     if (local) {
@@ -993,12 +1047,33 @@ __global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl
     warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
     PHASE();
 #ifdef SMOE_PHASES
-    if (rb == 0 && lane == 0) {
-        printf("ffn_down(last, expert %d) [pdl, ids+slot, stage, chain, y+fence+atomic, mix] (cycles):", i);
-        for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);
-        printf("\n");
-    }
+    if (rb == 0 && lane == 0)
+        phase_print("ffn_down(last) [pdl, ids+slot, stage, chain, y+fence+atomic, mix]", ph_, nph_);
 #endif
+}
+
+__global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                 int exec_src) {
+    ffn_down_body(m, st, ctl, layer, exec_src, blockIdx.x, blockIdx.y, false, 0);
+}
+
+// Gate/up and down in ONE grid: blocks [0, nGU) run the gate/up role, blocks
+// [nGU, nGU + nDN) the down role.  Down CTAs prefetch their weights while the
+// gate/up CTAs compute and start as soon as their expert's 16-row blocks are
+// done (gu_done, monotonic; target from the per-layer launch epoch), with no
+// kernel boundary in between.  CTAs are dispatched in block order, so every
+// gate/up CTA is resident before a down CTA can wait on it.
+__global__ void __launch_bounds__(32) k_ffn(DevModel m, DevState st, DevCtl ctl, int layer,
+                                            int exec_src, int s_from_r) {
+    const int ngu_x = m.Hmp / 16, ngu = ngu_x * m.K, ndn_x = m.Hp / 32;
+    const int epoch = __ldcg(st.ffn_epoch + layer);  // before this launch's last CTA bumps it
+    const int b = blockIdx.x;
+    if (b < ngu)
+        ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, b % ngu_x, b / ngu_x, true);
+    else
+        ffn_down_body(m, st, ctl, layer, exec_src, (b - ngu) % ndn_x, (b - ngu) / ndn_x, true,
+                      (epoch + 1) * ngu_x);
+    if (last_cta(st.counters + 5, gridDim.x) && threadIdx.x == 0) st.ffn_epoch[layer] = epoch + 1;
 }
 
 // L2 prefetch of the experts a decision will execute (prefetch mode): issued on
@@ -1256,6 +1331,10 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
         if (e_ != cudaSuccess) return e_;                                   \
     } while (0)
 long long launch_counter() { return g_launches; }
+// SMOE_FUSED_FFN=1: gate/up and down in one grid (k_ffn).  Off by default:
+// measured slower on Q30 — the waiting down CTAs hold SM slots and starve the
+// side-stream predictor, which then delays the next layer.
+static const bool g_split_ffn = std::getenv("SMOE_FUSED_FFN") == nullptr;
 static inline cudaError_t counted(int n = 1) {
     g_launches += n;
     return cudaGetLastError();
@@ -1335,7 +1414,8 @@ cudaError_t preload_kernels() {
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
                          (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
-                         (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch};
+                         (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
+                         (const void*)k_ffn};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -1347,6 +1427,7 @@ cudaError_t preload_kernels() {
     for (const void* f : big)
         if ((e = set_smem(f, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn, 220 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
@@ -1403,6 +1484,11 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
+    if (ctl.ep.world == 1 && !g_split_ffn) {
+        const size_t sm = gu_smem(m) > down_smem(m) ? gu_smem(m) : down_smem(m);
+        PDL(k_ffn, (m.Hmp / 16 + m.Hp / 32) * m.K, 32, sm, s, m, st, ctl, layer, exec_src, s_from_r);
+        return counted(1);
+    }
     PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
     PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, exec_src);
     if (ctl.ep.world > 1) {

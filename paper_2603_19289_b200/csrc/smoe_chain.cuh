@@ -102,6 +102,13 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ unsigned long long gtimer() {  // SM cycles
     return clock64();
 }
+// one printf per dump, so concurrent kernels do not interleave their lines
+__device__ inline void phase_print(const char* name, const unsigned long long* ph, int n) {
+    unsigned long long d[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 1; i < n && i < 10; ++i) d[i - 1] = ph[i] - ph[i - 1];
+    printf("%s (cycles): %llu %llu %llu %llu %llu %llu %llu %llu | %llu\n", name, d[0], d[1], d[2], d[3], d[4],
+           d[5], d[6], d[7], ph[n - 1] - ph[0]);
+}
 #define PHASE_DECL \
     unsigned long long ph_[10];  \
     int nph_ = 0;
@@ -111,11 +118,7 @@ __device__ __forceinline__ unsigned long long gtimer() {  // SM cycles
     } while (0)
 #define PHASE_DUMP(name)                                                                   \
     do {                                                                                   \
-        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                      \
-            printf("%s (cycles):", name);                                                  \
-            for (int i_ = 1; i_ < nph_; ++i_) printf(" %llu", ph_[i_] - ph_[i_ - 1]);      \
-            printf(" | %llu\n", ph_[nph_ - 1] - ph_[0]);                                   \
-        }                                                                                  \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) phase_print(name, ph_, nph_); \
     } while (0)
 #else
 #define PHASE_DECL
@@ -546,6 +549,12 @@ using PipeD = WarpPipe<uint16_t, kS, kCCd>;
 using PipeR = WarpPipe<uint16_t, 3, 256>;  // router: 48 KB, fits beside three k_ffn_gu CTAs
 
 // -------------------------------------------------------------- decision --
+#ifdef DECISION_TIMING
+__device__ long long g_dec_t[8];
+#define DEC_T(i) do { __syncwarp(); if ((threadIdx.x & 31) == 0) g_dec_t[i] = clock64(); } while (0)
+#else
+#define DEC_T(i) do {} while (0)
+#endif
 //
 // make_decision (model.cpp:258-274) for one logits row, executed by warp 0.
 // softmax (numerics.cpp:37-54): f32 max, f64 exp, f64 partition summed in
@@ -555,6 +564,7 @@ using PipeR = WarpPipe<uint16_t, 3, 256>;  // router: 48 KB, fits beside three k
 __device__ void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
                               double* se /*smem E*/, int* ids, float* gates) {
     const int lane = threadIdx.x & 31;
+    DEC_T(0);
     // logits were written by other CTAs: L2 loads, all in flight, into smem
     for (int i0 = 0; i0 < E; i0 += 8 * 32) {
         float t[8];
@@ -570,6 +580,7 @@ __device__ void warp_decision(const float* logits, int E, int K, int gating, flo
         }
     }
     __syncwarp();
+    DEC_T(1);
     if (gating == kSoftmaxTopK) {
         float mx = -INFINITY;
         for (int i = lane; i < E; i += 32) mx = fmaxf(mx, sp[i]);
@@ -597,39 +608,82 @@ __device__ void warp_decision(const float* logits, int E, int K, int gating, flo
         }
         __syncwarp();
     }
+    DEC_T(2);
     // top_k (numerics.cpp:56-70): value descending, lower index first on ties.
-    // Rank of element i = #{j : v_j > v_i or (v_j == v_i and j < i)}; the
-    // elements of rank < K are the selection, in rank order.  All lanes rank
-    // their elements in parallel against broadcast smem reads.
+    // Each element becomes a 64-bit key (order-preserving bits of the value,
+    // then the inverted index), every lane keeps its elements' keys in
+    // registers, and each of the K rounds takes the warp maximum with two
+    // REDUX.MAX (high word, then low word among the lanes holding it).
     __shared__ int s_sel[kMaxK];
     __shared__ float s_val[kMaxK];
-    for (int i0 = 0; i0 < E; i0 += 4 * 32) {
-        float x[4];
-        int rank[4];
+    if (E <= 8 * 32) {
+        unsigned hi[8], lo[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * 32 + lane;
-            x[u] = i < E ? sp[i] : 0.0f;
-            rank[u] = 0;
+        for (int u = 0; u < 8; ++u) {
+            const int i = u * 32 + lane;
+            if (i < E) {
+                unsigned b = __float_as_uint(sp[i]);
+                hi[u] = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+                lo[u] = 0xFFFFFFFFu - static_cast<unsigned>(i);
+            } else {
+                hi[u] = 0;
+                lo[u] = 0;
+            }
         }
-        for (int j = 0; j < E; ++j) {
-            const float y = sp[j];
+        for (int t = 0; t < K; ++t) {
+            unsigned mh = 0, ml = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (hi[u] > mh || (hi[u] == mh && lo[u] > ml)) {
+                    mh = hi[u];
+                    ml = lo[u];
+                }
+            const unsigned wh = __reduce_max_sync(0xffffffffu, mh);
+            const unsigned wl = __reduce_max_sync(0xffffffffu, mh == wh ? ml : 0u);
+            const int i = static_cast<int>(0xFFFFFFFFu - wl);
+            if ((i & 31) == lane) {  // the owner drops the winner from its keys
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u == (i >> 5)) {
+                        hi[u] = 0;
+                        lo[u] = 0;
+                    }
+            }
+            if (lane == 0) {
+                s_sel[t] = i;
+                s_val[t] = sp[i];
+            }
+        }
+    } else {  // large E: rank of i = #{j : v_j > v_i or (v_j == v_i and j < i)}
+        for (int i0 = 0; i0 < E; i0 += 4 * 32) {
+            float x[4];
+            int rank[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = i0 + u * 32 + lane;
-                rank[u] += (y > x[u]) | ((y == x[u]) & (j < i));
+                x[u] = i < E ? sp[i] : 0.0f;
+                rank[u] = 0;
             }
-        }
+            for (int j = 0; j < E; ++j) {
+                const float y = sp[j];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * 32 + lane;
-            if (i < E && rank[u] < K) {
-                s_sel[rank[u]] = i;
-                s_val[rank[u]] = x[u];
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * 32 + lane;
+                    rank[u] += (y > x[u]) | ((y == x[u]) & (j < i));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < E && rank[u] < K) {
+                    s_sel[rank[u]] = i;
+                    s_val[rank[u]] = x[u];
+                }
             }
         }
     }
     __syncwarp();
+    DEC_T(3);
     if (lane == 0) {
         if (gating == kSoftmaxTopK) {  // gates renormalised by an f32 sum in rank order
             float total = 0.0f;
@@ -657,6 +711,7 @@ __device__ void warp_decision(const float* logits, int E, int K, int gating, flo
         }
     }
     __syncwarp();
+    DEC_T(4);
 }
 
 }  // namespace smoe

@@ -131,6 +131,8 @@ struct DevState {
     // publishes dec_ready[l] = pass_id after the decision and its copy request
     int* pass_id;      // [1]
     int* dec_ready;    // [L]
+    int* gu_done;      // [L][K] gate/up CTAs finished, monotonic (fused k_ffn)
+    int* ffn_epoch;    // [L] completed k_ffn launches per layer
     double* ssq_rd;    // [L][Hp/32]
 };
 

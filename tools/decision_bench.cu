@@ -1,5 +1,6 @@
 // Microbenchmark (tools only): warp_decision (smoe_chain.cuh) for E logits,
 // top-k, both gating orders; cycles per call from one warp.
+#define DECISION_TIMING
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -46,6 +47,9 @@ int main() {
         k_dec<<<1, 32>>>(lg, E, K, gating, ids, g, cyc);
         long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
         printf("warp_decision E=%d K=%d gating=%d: %lld cycles\n", E, K, gating, c);
+        long long tt[8];
+        cudaMemcpyFromSymbol(tt, g_dec_t, sizeof tt);
+        printf("   stage %lld, softmax %lld, topk %lld, gates %lld\n", tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3]);
     }
     k_parts<<<1, 32>>>(lg, E, cyc);
     k_parts<<<1, 32>>>(lg, E, cyc);
