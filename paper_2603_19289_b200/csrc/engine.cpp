@@ -451,6 +451,7 @@ void Session::alloc() {
         // its few CTAs are placed before pending expert-kernel CTAs
         int lo = 0, hi = 0;
         ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+        if (std::getenv("SMOE_NO_PRIO")) lo = hi = 0;  // diagnostics
         ck(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
         ck(cudaStreamCreateWithPriority(&s_log_, cudaStreamNonBlocking, lo), "stream");
     }
@@ -564,6 +565,7 @@ void Session::alloc() {
         st.token = static_cast<int*>(dalloc(4));
         st.counters = static_cast<int*>(dalloc(4 * 64));
         st.down_cnt = static_cast<int*>(dalloc(4ull * (m.Hp / 32)));
+        st.log_cnt = static_cast<int*>(dalloc(4ull * L));
         st.ssq_x = static_cast<double*>(dalloc(8ull * (L + 1) * (m.Hp / 32)));
         st.ssq_r = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
         st.rd = static_cast<float*>(dalloc(4ull * L * m.Hp));
@@ -1186,13 +1188,14 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
             if (k != kNone && l + 1 < c.L && l2_prefetch_)  // warm L2 with layer l+1's experts
                 ck(launch_l2_prefetch(dm_, st, ctl_, l + 1, s_side_), "l2 prefetch");
             if (tl) tl_end(t_side, s_side_);
-            if (l > 0) {
-                // true router of layer l (speculation.cpp:370-371: logged every
-                // layer, never executed here) on the lowest-priority log stream,
-                // so it never delays the next predictor on the side stream
+            if (l == c.L - 1 && c.L > 1) {
+                // true routers of layers 1..L-1 (speculation.cpp:370-371: logged
+                // every layer, never executed here) in ONE launch on the
+                // lowest-priority log stream once r_{L-1} exists, overlapping the
+                // last layer's experts.  (Launched per layer, the graph executor
+                // queued each one behind the compute stream's expert kernel.)
                 ck(cudaStreamWaitEvent(s_log_, ev_fork_[l], 0), "fork");
-                RouterLaunch rt{l, 1, kNone, -1, 0, 0, step_tag, 0};
-                ck(launch_router(dm_, st, ctl_, rt, nullptr, s_log_), "router");
+                ck(launch_log_routers(dm_, st, ctl_, 1, c.L - 1, step_tag, s_log_), "router");
                 log_used = true;
             }
             side_used = true;

@@ -22,7 +22,7 @@
 // wait and the last CTA exit, in globaltimer ns, min/max over CTAs.
 namespace smoe {
 constexpr int kKtKinds = 16, kKtLayers = 128;
-__device__ unsigned long long g_kt[kKtKinds * kKtLayers][3];
+__device__ unsigned long long g_kt[kKtKinds * kKtLayers][4];
 __device__ __forceinline__ unsigned long long kt_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -31,7 +31,11 @@ __device__ __forceinline__ unsigned long long kt_now() {
 struct KTrace {
     int slot;
     __device__ KTrace(int kind, int layer) : slot(kind * kKtLayers + (layer & (kKtLayers - 1))) {
-        if (threadIdx.x == 0) atomicMin(&g_kt[slot][0], kt_now());
+        if (threadIdx.x == 0) {
+            const unsigned long long t = kt_now();
+            atomicMin(&g_kt[slot][0], t);
+            atomicMax(&g_kt[slot][3], t);  // last CTA to start
+        }
     }
     __device__ void waited() const {
         if (threadIdx.x == 0) atomicMin(&g_kt[slot][1], kt_now());
@@ -42,8 +46,8 @@ struct KTrace {
 };
 }  // namespace smoe
 extern "C" int smoe_ktrace_reset() {
-    static unsigned long long h[smoe::kKtKinds * smoe::kKtLayers][3];
-    for (auto& r : h) { r[0] = ~0ull; r[1] = ~0ull; r[2] = 0; }
+    static unsigned long long h[smoe::kKtKinds * smoe::kKtLayers][4];
+    for (auto& r : h) { r[0] = ~0ull; r[1] = ~0ull; r[2] = 0; r[3] = 0; }
     return cudaMemcpyToSymbol(smoe::g_kt, h, sizeof(h)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int smoe_ktrace_read(unsigned long long* out) {
@@ -513,7 +517,9 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     KTRACE(rl.do_true ? 4 : 13, rl.layer);
     PHASE_DECL
     PHASE();
-    const int H = m.H, E = m.E, K = m.K, l = rl.layer, Hr = round_up(H, 32);
+    // gridDim.y > 1: the logging true routers of layers rl.layer .. +gridDim.y-1
+    // in one launch (one y-slice per layer, per-layer last-CTA counters)
+    const int H = m.H, E = m.E, K = m.K, l = rl.layer + static_cast<int>(blockIdx.y), Hr = round_up(H, 32);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     double* red = reinterpret_cast<double*>(g_smem + 64);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
@@ -585,7 +591,8 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     // copy request is posted without waiting for the (logging-only) true one.
     const bool in_true = b < nT;
     const bool has_b = static_cast<int>(gridDim.x) > nT;  // predictor / quasi CTAs exist
-    if (!last_cta(st.counters + (in_true ? 0 : 4), in_true ? nT : gridDim.x - nT)) return;
+    int* gate_cnt = gridDim.y > 1 ? st.log_cnt + l : st.counters + (in_true ? 0 : 4);
+    if (!last_cta(gate_cnt, in_true ? nT : gridDim.x - nT)) return;
     PHASE();
     double* se = reinterpret_cast<double*>(pipe_mem);            // [E]
     float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);  // [E]
@@ -1420,6 +1427,13 @@ cudaError_t preload_kernels() {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
         if (e != cudaSuccess) return e;
+        // Maximum shared-memory carveout for every kernel: the SM's L1/smem
+        // split is chosen per kernel, and a kernel sized by its own needs
+        // leaves no room for the CTAs of concurrent kernels (the side-stream
+        // predictor, a PDL-launched dependent prefetching its weights).
+        e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
     }
     cudaError_t e = cudaSuccess;
     const void* big[] = {(const void*)k_qkv, (const void*)k_wo, (const void*)k_router,
@@ -1469,6 +1483,13 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
     if (grid < 1) grid = 1;
     DevState sh = shadow ? *shadow : st;
     PDL(k_router, grid, 32, router_smem(m, rl.quasi_ready), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
+    return counted(1);
+}
+
+cudaError_t launch_log_routers(const DevModel& m, const DevState& st, const DevCtl& ctl, int l0,
+                               int nl, int step_tag, cudaStream_t s) {
+    RouterLaunch rl{l0, 1, kNone, -1, 0, 0, step_tag, 0};
+    PDL(k_router, dim3(m.Ep / 32, nl), 32, router_smem(m, 0), s, m, st, ctl, rl, st, 0);
     return counted(1);
 }
 

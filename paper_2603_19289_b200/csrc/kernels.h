@@ -40,6 +40,9 @@ cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, 
 // `layer` (id_pred / g_pred), for the predictor's q_l.
 cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
                       int rd_from_pred = 0);
+// logging-only true routers of layers l0 .. l0+nl-1 in one launch (prefetch mode)
+cudaError_t launch_log_routers(const DevModel& m, const DevState& st, const DevCtl& ctl, int l0,
+                               int nl, int step_tag, cudaStream_t s);
 // L2 prefetch of the resident expert blocks of the decision predicted for `layer`
 cudaError_t launch_l2_prefetch(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                                cudaStream_t s);

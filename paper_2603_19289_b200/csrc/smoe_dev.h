@@ -116,6 +116,7 @@ struct DevState {
     int* token;        // current token
     int* counters;     // last-CTA counters [64]
     int* down_cnt;     // [Hp/32] k_ffn_down per-row-block arrival counters (self-resetting)
+    int* log_cnt;      // [L] last-CTA counters of the batched logging routers
     // rms_norm statistics, computed by the kernel that produces the vector:
     // f64 partial sums of squares per 32-row block (Hp/32 per vector), summed
     // by consumers in a fixed order (rms_scale_from_partials).

@@ -24,6 +24,7 @@ KINDS = {14: "l2_pf", 0: "embed", 1: "qkv", 2: "attn", 3: "wo", 4: "router", 5: 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 wl = sys.argv[3] if len(sys.argv) > 3 else "greedy"
+use_graph = "--no-graph" not in sys.argv
 lib = C.CDLL(LIB)
 lib.smoe_ktrace_read.argtypes = [C.c_void_p]
 cfg = ModelConfig(layers=L, experts=128, top_k=8, hidden=2048, expert_hidden=768, vocab=256,
@@ -47,20 +48,20 @@ for mode in ("prefetch", "on_demand"):
     if wl == "stream":
         s.decode_stream(mode, forced[8:9])
     else:
-        s.decode(mode, 1)
-    buf = np.zeros((16 * 128, 3), np.uint64)
+        s.decode(mode, 1, use_graph=use_graph)
+    buf = np.zeros((16 * 128, 4), np.uint64)
     lib.smoe_ktrace_read(buf.ctypes.data)
     t0 = min(int(r[0]) for r in buf if r[0] != np.uint64(~np.uint64(0)) and r[2] > 0)
     print(f"== {mode} ({wl}, cache {frac}, L={L}) step {float(s.token_ms()[-1]):.3f} ms ==")
-    print(f"{'layer':>5} {'kernel':>9} {'entry':>8} {'waited':>8} {'exit':>8} {'run':>7}")
+    print(f"{'layer':>5} {'kernel':>9} {'entry':>8} {'waited':>8} {'exit':>8} {'run':>7} {'lastCTA':>8}")
     rows = []
     for kind, name in KINDS.items():
         for layer in range(L if kind not in (0, 12) else 1):
             r = buf[kind * 128 + layer]
             if r[2] == 0:
                 continue
-            e, w, x = ((int(v) - t0) / 1e3 if int(v) != 2**64 - 1 else float("nan") for v in r)
-            rows.append((x, layer, name, e, w))
-    for x, layer, name, e, w in sorted(rows, key=lambda t: (t[3], t[0])):
-        print(f"{layer:>5} {name:>9} {e:8.2f} {w:8.2f} {x:8.2f} {x - w:7.2f}")
+            e, w, x, lc = ((int(v) - t0) / 1e3 if int(v) != 2**64 - 1 else float("nan") for v in r)
+            rows.append((x, layer, name, e, w, lc))
+    for x, layer, name, e, w, lc in sorted(rows, key=lambda t: (t[3], t[0])):
+        print(f"{layer:>5} {name:>9} {e:8.2f} {w:8.2f} {x:8.2f} {x - w:7.2f} {lc:8.2f}")
 s.close()
