@@ -1131,23 +1131,22 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
     // attention output, while the expert FFN proceeds on the compute stream.
     // The side work of layer l joins before the FFN of layer l+1 (which runs
     // the decision it produced) and before the end of the step.
-    int pending_join = -1;
+    std::vector<char> side_at(c.L, 0);  // layers whose side work recorded ev_join_
     bool side_used = false, log_used = false;
     const bool tl = tl_ && is_main;  // timeline: CUDA events around each phase
     for (int l = 0; l < c.L; ++l) {
         const int t_attn = tl ? tl_begin(0, 0, l, s) : -1;
         ck(launch_qkv(dm_, st, l, s), "qkv");
         ck(launch_attn(dm_, st, d_attn_scratch_, l, s), "attn");
-        // prefetch, l >= 1: the decision executed here (predicted at l-1, on the
-        // side stream) is joined before k_wo, which then also forms
-        // rd_l = r_l + d_l for this layer's q_l (router-pf / est-pf)
+        // prefetch, l >= 1: k_wo also forms rd_l = r_l + d_l for this layer's
+        // q_l (router-pf / est-pf) from the decision predicted at l-1, which it
+        // and k_ffn_gu take from the predictor's device flag (dec_ready), not
+        // from a stream join: a graph-captured PDL launch makes even the
+        // cross-stream edge programmatic, and a join here would hold the whole
+        // layer behind the predictor's tail.
         const int kq = prefetch && l > 0 ? kind_at(l) : kNone;
         const int quasi_ready = kq == kRouterPF || kq == kEstPF;
-        if (pending_join >= 0) {
-            ck(cudaStreamWaitEvent(s, ev_join_[pending_join], 0), "join");
-            pending_join = -1;
-        }
-        ck(launch_wo(dm_, st, l, s, quasi_ready), "wo");
+        ck(launch_wo(dm_, st, ctl_, l, s, quasi_ready), "wo");
         if (tl) tl_end(t_attn, s);
         int exec_src = 0, s_from_r = 0;
         if (!prefetch) {
@@ -1199,12 +1198,16 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
                 log_used = true;
             }
             side_used = true;
-            pending_join = l;
+            side_at[l] = 1;
             if (l > 0) {
                 exec_src = 1;
                 s_from_r = 1;
             }
         }
+        // guard join, one layer behind: the side work of layer l-2 is complete
+        // before the FFN of layer l (its flags were consumed a layer earlier),
+        // so spinning expert CTAs can never starve an unfinished predictor
+        if (l >= 2 && side_at[l - 2]) ck(cudaStreamWaitEvent(s, ev_join_[l - 2], 0), "join");
         const int t_exp = tl ? tl_begin(0, 2, l, s) : -1;
         ck(launch_ffn(dm_, st, ctl_, l, s, exec_src, s_from_r), "ffn");
         if (tl) tl_end(t_exp, s);
@@ -1522,7 +1525,7 @@ void Session::profile_kernels(int reps, double* out) {
                     switch (k) {
                     case 0: ck(launch_qkv(dm_, st_, l, s_comp_), "qkv"); break;
                     case 1: ck(launch_attn(dm_, st_, d_attn_scratch_, l, s_comp_), "attn"); break;
-                    case 2: ck(launch_wo(dm_, st_, l, s_comp_), "wo"); break;
+                    case 2: ck(launch_wo(dm_, st_, ctl_, l, s_comp_), "wo"); break;
                     case 3: {
                         RouterLaunch rl{l, 1, kNone, -1, 0, 0, -9, 0};
                         ck(launch_router(dm_, st_, ctl_, rl, nullptr, s_comp_), "router");

@@ -403,6 +403,27 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
+// Wait (thread 0) until the predictor of layer-1 published this layer's
+// decision for the current pass (publish_decision).
+__device__ __forceinline__ void wait_decision(const DevState& st, const DevCtl& ctl, int layer) {
+    if (threadIdx.x == 0) {
+        const int want = __ldcg(st.pass_id);
+        const long long t0 = clock64();
+        for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(st.dec_ready + layer) : "memory");
+            if (v == want) break;
+            if (*(volatile int*)ctl.error) break;
+            if (clock64() - t0 > ctl.spin_limit) {
+                atomicCAS(ctl.error, 0, 1000 + layer);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncwarp();
+}
+
 // layer_default (speculation.cpp:104-117) for row j of a decision of K
 // experts: d_j = sum_i g_i * D[layer][e_i][j] in decision order (f32).  The K
 // loads (one coalesced 128-byte line per warp and expert) are all in flight.
@@ -424,7 +445,8 @@ __device__ __forceinline__ float layer_default_row(const DevModel& m, const int*
     return d;
 }
 
-__global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer, int rd_from_pred) {
+__global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, DevCtl ctl, int layer,
+                                           int rd_from_pred) {
     KTRACE(3, layer);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
@@ -435,18 +457,21 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, int layer, i
     pipe.prime(m.wo + layer * m.wo_stride + static_cast<long long>(blockIdx.x) * m.D * 32, m.D);
     Stager sg;
     sg.init(bar);
+    const int rb = blockIdx.x;
+    const int j = rb * 32 + (threadIdx.x & 31);
+    // d_l of the decision predicted for this layer (for q_l): once the
+    // predictor of layer-1 has published it (device flag, not the PDL edge),
+    // its default-vector rows load while the attention still runs
+    float d = 0.0f;
+    if (rd_from_pred) {
+        wait_decision(st, ctl, layer);
+        if (j < m.H) d = layer_default_row(m, st.id_pred + layer * m.K, st.g_pred + layer * m.K, layer, j);
+    }
     pdl_wait();
     KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.ctx, m.D * 4);
     sg.add(xr, st.x + blockIdx.x * 32, 32 * 4);
-    const int rb = blockIdx.x;
-    const int j = rb * 32 + (threadIdx.x & 31);
-    // d_l of the decision predicted for this layer (for q_l), loaded while the
-    // context vector lands and the wo chain runs
-    const float d = rd_from_pred && j < m.H
-                        ? layer_default_row(m, st.id_pred + layer * m.K, st.g_pred + layer * m.K, layer, j)
-                        : 0.0f;
     sg.wait();
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
     const float acc = pipe.run(tile, m.D, xs);
@@ -798,27 +823,6 @@ __device__ void wait_ready(const DevCtl& ctl, int layer) {
 // run concurrently on a side stream (Alg. 1: the predicted experts are known
 // before the layer starts).  s_from_r: compute s_l = rms_norm(r_l, moe_gain_l)
 // here instead of reading the router's copy.
-// Wait (thread 0) until the predictor of layer-1 published this layer's
-// decision for the current pass (publish_decision).
-__device__ __forceinline__ void wait_decision(const DevState& st, const DevCtl& ctl, int layer) {
-    if (threadIdx.x == 0) {
-        const int want = __ldcg(st.pass_id);
-        const long long t0 = clock64();
-        for (;;) {
-            int v;
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(st.dec_ready + layer) : "memory");
-            if (v == want) break;
-            if (*(volatile int*)ctl.error) break;
-            if (clock64() - t0 > ctl.spin_limit) {
-                atomicCAS(ctl.error, 0, 1000 + layer);
-                break;
-            }
-            __nanosleep(64);
-        }
-    }
-    __syncwarp();
-}
-
 // gate/up role of one (16-row block rb, executed expert i).  `fused`: the down
 // role runs in the same grid and waits on gu_done[layer][i].
 __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& st, const DevCtl& ctl,
@@ -1467,9 +1471,9 @@ cudaError_t launch_quasi_rd(const DevModel& m, const DevState& st, int layer, cu
     return counted(1);
 }
 
-cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
-                      int rd_from_pred) {
-    PDL(k_wo, m.Hp / 32, 32, wo_smem(m), s, m, st, layer, rd_from_pred);
+cudaError_t launch_wo(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                      cudaStream_t s, int rd_from_pred) {
+    PDL(k_wo, m.Hp / 32, 32, wo_smem(m), s, m, st, ctl, layer, rd_from_pred);
     return counted(1);
 }
 

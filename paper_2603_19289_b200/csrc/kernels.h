@@ -38,8 +38,8 @@ cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, 
                         cudaStream_t s);
 // rd_from_pred: also form rd_l = r_l + d_l from the decision predicted for
 // `layer` (id_pred / g_pred), for the predictor's q_l.
-cudaError_t launch_wo(const DevModel& m, const DevState& st, int layer, cudaStream_t s,
-                      int rd_from_pred = 0);
+cudaError_t launch_wo(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                      cudaStream_t s, int rd_from_pred = 0);
 // logging-only true routers of layers l0 .. l0+nl-1 in one launch (prefetch mode)
 cudaError_t launch_log_routers(const DevModel& m, const DevState& st, const DevCtl& ctl, int l0,
                                int nl, int step_tag, cudaStream_t s);
