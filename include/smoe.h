@@ -131,8 +131,16 @@ int smoe_read_tokens(smoe_session* s, int32_t* out, int32_t n);
 /* field: id_true, id_exec, id_pred ([steps][L][K] int32), g_true, g_exec,
  * g_pred ([steps][L][K]), s, r, m ([steps][L][H]), lg_true, lg_pred
  * ([steps][L][E]; lg_pred row l = prediction for layer l), y ([steps][L][K][H]),
- * logits ([steps][vocab]). */
+ * logits ([steps][vocab]), tok_in ([steps] input token of each step). */
 int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n_elems);
+/* Trace bundle of steps [first, first + n) in the reference's format
+ * (TraceWriter, trace.cpp:60-122; MOET files, moet.hpp:3-9): manifest.json
+ * plus token_ids, s, r, m, router_logits (true router), expert_ids /
+ * expert_gates (executed decision, ids as f32) and expert_outputs (raw) .moet
+ * files in `dir`, readable by the reference's TraceReader.  Needs
+ * smoe_reset(..., trace_full = 1). */
+int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
+                            int32_t seq_len, const char* source, uint64_t seed);
 int smoe_token_ms(smoe_session* s, double* out, int32_t cap, int32_t* n);
 /* Per-layer cache hits/misses [L], total H2D bytes, summed copy-lane busy ms,
  * number of copy requests. */

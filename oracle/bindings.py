@@ -286,6 +286,13 @@ class RefModel:
         c = self.cfg
         return RefHandle(self.ref, h, "ref_free_table", shape=(c.layers, c.experts, c.hidden))
 
+    def write_trace(self, tokens, seq_len: int, path: str, source: str = "", seed: int = 0):
+        """The reference's TraceWriter over stream_decode_trace (true path)."""
+        t = np.ascontiguousarray(tokens, np.int32)
+        self.ref._check(self.ref.lib.ref_write_trace(self.h, _ptr(t), C.c_int64(len(t)), seq_len,
+                                                     path.encode(), source.encode(),
+                                                     C.c_uint64(seed)))
+
     def generate_trace(self, prompt, n_new, pred=None, outputs=False) -> Trace:
         prompt = np.ascontiguousarray(prompt, np.int32)
         t = _alloc_trace(self.cfg, len(prompt), n_new, outputs, pred is not None)

@@ -469,6 +469,26 @@ int ref_offloaded_decode(void* h, const int* prompt, int P, int n_new, void* pre
 
 // --- leaf numerics (numerics.cpp, model.cpp:258-304) -------------------------
 
+// The reference's own trace capture (cmd_trace, main.cpp:90-147): the true path
+// over `tokens` with state resets every seq_len tokens (stream_decode_trace,
+// trace.cpp:187-203), written by TraceWriter (trace.cpp:60-122).
+int ref_write_trace(void* h, const int* tokens, std::int64_t n, int seq_len, const char* dir,
+                    const char* source, std::uint64_t seed) {
+    return guard([&] {
+        const Model& m = *static_cast<Model*>(h);
+        TraceManifest man;
+        man.config = m.config;
+        man.tokens = n;
+        man.seq_len = seq_len;
+        man.source = source;
+        man.seed = seed;
+        TraceWriter w(dir, man);
+        stream_decode_trace(m, std::span<const int>(tokens, static_cast<size_t>(n)), seq_len,
+                            [&](std::int64_t, const TraceToken& t) { w.add_token(t.token_id, t.layers); });
+        w.finish();
+    });
+}
+
 std::uint64_t ref_derive_seed(std::uint64_t seed, const char* label) { return derive_seed(seed, label); }
 
 void ref_gaussian_stream(std::uint64_t seed, float stddev, std::int64_t n, float* out) {

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <immintrin.h>
 
+#include <charconv>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -11,6 +12,8 @@
 #include <cstring>
 #include <random>
 #include <unistd.h>
+#include <sys/stat.h>
+#include <cerrno>
 #include <string>
 
 namespace smoe {
@@ -563,6 +566,7 @@ void Session::alloc() {
         st.logits = static_cast<float*>(dalloc(4ull * m.Vp));
         st.pos = static_cast<int*>(dalloc(4));
         st.token = static_cast<int*>(dalloc(4));
+        st.tok_in = static_cast<int*>(dalloc(4));
         st.counters = static_cast<int*>(dalloc(4 * 64));
         st.down_cnt = static_cast<int*>(dalloc(4ull * (m.Hp / 32)));
         st.log_cnt = static_cast<int*>(dalloc(4ull * L));
@@ -1072,7 +1076,7 @@ void Session::reset(int max_steps, int trace_full) {
         for (void* p : {(void*)tr_.s, (void*)tr_.r, (void*)tr_.m, (void*)tr_.lg_true, (void*)tr_.g_true,
                         (void*)tr_.g_exec, (void*)tr_.lg_pred, (void*)tr_.g_pred, (void*)tr_.y,
                         (void*)tr_.logits, (void*)tr_.id_true, (void*)tr_.id_exec, (void*)tr_.id_pred,
-                        (void*)tr_.step})
+                        (void*)tr_.tok_in, (void*)tr_.step})
             drop(p);
         tr_ = TraceDev{};
         tr_.step = static_cast<int*>(dalloc(4));
@@ -1080,6 +1084,7 @@ void Session::reset(int max_steps, int trace_full) {
         tr_.full = trace_full;
         const long long S = max_steps > 0 ? max_steps : 1;
         const long long LK = static_cast<long long>(c.L) * c.K;
+        tr_.tok_in = static_cast<int*>(dalloc(4 * S));
         tr_.id_true = static_cast<int*>(dalloc(4 * S * LK));
         tr_.id_exec = static_cast<int*>(dalloc(4 * S * LK));
         tr_.id_pred = static_cast<int*>(dalloc(4 * S * LK));
@@ -1632,7 +1637,8 @@ void Session::read_trace(const char* field, void* out, long long n) {
     const std::string f = field;
     const void* src = nullptr;
     long long esz = 4;
-    if (f == "id_true") src = tr_.id_true;
+    if (f == "tok_in") src = tr_.tok_in;
+    else if (f == "id_true") src = tr_.id_true;
     else if (f == "id_exec") src = tr_.id_exec;
     else if (f == "id_pred") src = tr_.id_pred;
     else if (f == "g_true") src = tr_.g_true;
@@ -1648,6 +1654,101 @@ void Session::read_trace(const char* field, void* out, long long n) {
     else throw std::invalid_argument("read_trace: unknown field " + f);
     if (!src) throw std::invalid_argument("read_trace: field not captured (trace_full=0?)");
     d2h(out, src, n * esz, "trace");
+}
+
+// ---- trace bundles in the reference's format (trace.cpp:60-122, moet.cpp) ----
+namespace {
+void moet_write(const std::string& path, const std::vector<unsigned long long>& dims,
+                const std::vector<float>& data) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("trace: cannot write " + path);
+    unsigned char hdr[10] = {'M', 'O', 'E', 'T', 1, 0, 0, 0, 1, static_cast<unsigned char>(dims.size())};
+    bool ok = std::fwrite(hdr, 1, 10, f) == 10;
+    for (unsigned long long d : dims) {
+        unsigned char b[8];
+        for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(d >> (8 * i));
+        ok = ok && std::fwrite(b, 1, 8, f) == 8;
+    }
+    // little-endian host: the f32 payload is written as is (moet.cpp:9-13)
+    ok = ok && std::fwrite(data.data(), 4, data.size(), f) == data.size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw std::runtime_error("trace: short write to " + path);
+}
+std::string json_str(const std::string& s) {
+    std::string o = "\"";
+    for (char ch : s) {
+        if (ch == '"' || ch == '\\') o += '\\';
+        o += ch;
+    }
+    return o + "\"";
+}
+}  // namespace
+
+void Session::write_trace_bundle(const std::string& dir, int first, int n, int seq_len,
+                                 const std::string& source, unsigned long long seed) {
+    sync();
+    if (!trace_full_ || !tr_.s) throw std::invalid_argument("write_trace_bundle: needs reset(trace_full=1)");
+    if (n < 1 || first < 0 || first + n > tr_.cap) throw std::invalid_argument("trace: empty workload");
+    const ModelCfg& c = cfg_;
+    const long long N = n, L = c.L, H = c.H, E = c.E, K = c.K;
+    auto rd = [&](const char* field, long long per, bool ints) {
+        std::vector<float> out(static_cast<size_t>(N * per));
+        if (ints) {
+            std::vector<int> v(static_cast<size_t>(N * per));
+            std::vector<int> all(static_cast<size_t>((first + N) * per));
+            read_trace(field, all.data(), static_cast<long long>(all.size()));
+            for (size_t i = 0; i < v.size(); ++i) out[i] = static_cast<float>(all[first * per + i]);
+        } else {
+            std::vector<float> all(static_cast<size_t>((first + N) * per));
+            read_trace(field, all.data(), static_cast<long long>(all.size()));
+            std::copy(all.begin() + first * per, all.end(), out.begin());
+        }
+        return out;
+    };
+    if (::mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST)
+        throw std::runtime_error("trace: cannot create " + dir);
+    const unsigned long long n_ = N, L_ = L, H_ = H, E_ = E, K_ = K;
+    moet_write(dir + "/token_ids.moet", {n_}, rd("tok_in", 1, true));
+    moet_write(dir + "/s.moet", {n_, L_, H_}, rd("s", L * H, false));
+    moet_write(dir + "/r.moet", {n_, L_, H_}, rd("r", L * H, false));
+    moet_write(dir + "/m.moet", {n_, L_, H_}, rd("m", L * H, false));
+    moet_write(dir + "/router_logits.moet", {n_, L_, E_}, rd("lg_true", L * E, false));
+    moet_write(dir + "/expert_ids.moet", {n_, L_, K_}, rd("id_exec", L * K, true));
+    moet_write(dir + "/expert_gates.moet", {n_, L_, K_}, rd("g_exec", L * K, false));
+    moet_write(dir + "/expert_outputs.moet", {n_, L_, K_, H_}, rd("y", L * K * H, false));
+    // manifest.json (trace.cpp:19-41; keys in nlohmann's sorted order)
+    char eps[64];  // shortest round-trip form of double(eps), as nlohmann prints it
+    {
+        const auto res = std::to_chars(eps, eps + sizeof eps - 1, static_cast<double>(c.eps));
+        *res.ptr = 0;
+    }
+    std::string j = "{\n  \"config\": {\n";
+    j += "    \"eps\": " + std::string(eps) + ",\n";
+    j += "    \"expert_hidden\": " + std::to_string(c.Hm) + ",\n";
+    j += "    \"experts\": " + std::to_string(c.E) + ",\n";
+    j += "    \"gating\": " + json_str(c.gating == kTopKSoftmax ? "topk-softmax" : "softmax-topk-renorm") + ",\n";
+    j += "    \"head_dim\": " + std::to_string(c.D) + ",\n";
+    j += "    \"hidden\": " + std::to_string(c.H) + ",\n";
+    j += "    \"layers\": " + std::to_string(c.L) + ",\n";
+    j += "    \"seed\": " + std::to_string(c.seed) + ",\n";
+    j += "    \"top_k\": " + std::to_string(c.K) + ",\n";
+    j += "    \"vocab\": " + std::to_string(c.V) + "\n  },\n  \"fields\": [\n";
+    const std::vector<std::pair<std::string, std::vector<unsigned long long>>> shapes = {
+        {"token_ids", {n_}}, {"s", {n_, L_, H_}}, {"r", {n_, L_, H_}}, {"m", {n_, L_, H_}},
+        {"router_logits", {n_, L_, E_}}, {"expert_ids", {n_, L_, K_}},
+        {"expert_gates", {n_, L_, K_}}, {"expert_outputs", {n_, L_, K_, H_}}};
+    for (size_t f = 0; f < shapes.size(); ++f) {
+        j += "    {\n      \"dims\": [";
+        for (size_t d = 0; d < shapes[f].second.size(); ++d)
+            j += (d ? "," : "") + std::to_string(shapes[f].second[d]);
+        j += "],\n      \"name\": " + json_str(shapes[f].first) + "\n    }" + (f + 1 < shapes.size() ? "," : "") + "\n";
+    }
+    j += "  ],\n  \"seed\": " + std::to_string(seed) + ",\n  \"seq_len\": " + std::to_string(seq_len) +
+         ",\n  \"source\": " + json_str(source) + ",\n  \"tokens\": " + std::to_string(N) + "\n}\n";
+    FILE* f = std::fopen((dir + "/manifest.json").c_str(), "w");
+    if (!f) throw std::runtime_error("trace: cannot write manifest");
+    std::fputs(j.c_str(), f);
+    std::fclose(f);
 }
 
 std::vector<double> Session::token_ms() {

@@ -160,6 +160,8 @@ public:
     int steps_done();
     void read_tokens(int* out, int n);
     void read_trace(const char* field, void* out, long long n_elems);
+    void write_trace_bundle(const std::string& dir, int first, int n, int seq_len,
+                            const std::string& source, unsigned long long seed);
     std::vector<double> token_ms();  // device-timed duration of each decode() step
     void counters(long long* hits, long long* misses, long long* bytes, double* copy_ms,
                   int* requests);

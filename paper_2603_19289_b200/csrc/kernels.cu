@@ -178,6 +178,7 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int
     const int tok = stream ? stream[*step] : *token_src;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *st.token = tok;
+        *st.tok_in = tok;
         *st.pass_id = *st.pass_id + 1;  // read by later kernels of this pass only
     }
     const int j = blockIdx.x * 32 + threadIdx.x;  // grid Hp/32 x 32
@@ -1258,6 +1259,7 @@ __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {
     if (step >= tr.cap) return;
     const int L = m.L, H = m.H, E = m.E, K = m.K, V = m.V, Hp = m.Hp;
     const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t0 == 0) tr.tok_in[step] = *st.tok_in;
     const long long gs = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long t = t0; t < static_cast<long long>(L) * K; t += gs) {
         const long long o = static_cast<long long>(step) * L * K + t;

@@ -75,6 +75,7 @@ struct TraceDev {
     int full;           // 0: ids only (hit-rate history), 1: all fields
     float *s, *r, *m, *lg_true, *g_true, *g_exec, *lg_pred, *g_pred, *y, *logits;
     int *id_true, *id_exec, *id_pred;
+    int* tok_in;        // [cap] input token per step
 };
 cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
                          cudaStream_t s);

@@ -114,6 +114,7 @@ struct DevState {
     float* logits;     // [V]
     int* pos;          // position
     int* token;        // current token
+    int* tok_in;       // input token of the current step (for the trace)
     int* counters;     // last-CTA counters [64]
     int* down_cnt;     // [Hp/32] k_ffn_down per-row-block arrival counters (self-resetting)
     int* log_cnt;      // [L] last-CTA counters of the batched logging routers

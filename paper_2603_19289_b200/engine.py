@@ -32,6 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
+    "smoe_write_trace_bundle",
 ]
 
 
@@ -266,11 +267,18 @@ class Session:
         L, K, H, E, V = c.layers, c.top_k, c.hidden, c.experts, c.vocab
         shapes = {"id_true": (L, K), "id_exec": (L, K), "id_pred": (L, K), "g_true": (L, K),
                   "g_exec": (L, K), "g_pred": (L, K), "s": (L, H), "r": (L, H), "m": (L, H),
-                  "lg_true": (L, E), "lg_pred": (L, E), "y": (L, K, H), "logits": (V,)}
-        dt = np.int32 if field.startswith("id_") else np.float32
+                  "lg_true": (L, E), "lg_pred": (L, E), "y": (L, K, H), "logits": (V,),
+                  "tok_in": ()}
+        dt = np.int32 if field.startswith("id_") or field == "tok_in" else np.float32
         out = np.zeros((steps,) + shapes[field], dt)
         _check(self.lib.smoe_read_trace(self._h, field.encode(), _p(out), C.c_int64(out.size)))
         return out
+
+    def write_trace_bundle(self, path: str, first: int, n: int, seq_len: int = 0,
+                           source: str = "", seed: int = 0):
+        """Trace bundle in the reference's format (TraceWriter, trace.cpp:60-122)."""
+        _check(self.lib.smoe_write_trace_bundle(self._h, path.encode(), first, n, seq_len,
+                                                source.encode(), C.c_uint64(seed)))
 
     def token_ms(self) -> np.ndarray:
         out = np.zeros(4096, np.float64)

@@ -483,3 +483,37 @@ def test_timeline_event_log(lib, toy_oracle):
         fr, tp = breakdown(ev)
         assert abs(fr.sum() - 1.0) < 1e-9 and tp > 0
     s.close()
+
+
+def test_trace_bundle_matches_reference_writer(lib, tmp_path):
+    """§8f: the GPU's trace bundle (smoe_write_trace_bundle) equals, file for
+    file and byte for byte, the bundle the reference writes itself
+    (TraceWriter over stream_decode_trace, the `specmoe trace` workload) on the
+    same bf16 model and token stream; manifests agree field by field."""
+    import json
+
+    from oracle.bindings import REF_SO, Config, Ref
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    cfg = dict(layers=3, experts=8, top_k=2, hidden=64, expert_hidden=96, vocab=64, head_dim=16,
+               seed=21)
+    N = 12
+    toks = np.array([(7 * i + 3) % cfg["vocab"] for i in range(N)], np.int32)
+    ref = Ref()
+    rm = ref.build_model(Config(**cfg), round_bf16=True)
+    rdir, gdir = str(tmp_path / "ref"), str(tmp_path / "gpu")
+    rm.write_trace(toks, N, rdir, "parity", 5)
+    s = session(cfg, cache_fraction=0.5)
+    s.reset(N, True)
+    s.prefill(toks)
+    s.write_trace_bundle(gdir, 0, N, N, "parity", 5)
+    s.close()
+    for f in ("token_ids", "s", "r", "m", "router_logits", "expert_ids", "expert_gates",
+              "expert_outputs"):
+        a = open(os.path.join(rdir, f + ".moet"), "rb").read()
+        b = open(os.path.join(gdir, f + ".moet"), "rb").read()
+        assert a == b, f
+    ja = json.load(open(os.path.join(rdir, "manifest.json")))
+    jb = json.load(open(os.path.join(gdir, "manifest.json")))
+    assert np.float32(ja["config"].pop("eps")) == np.float32(jb["config"].pop("eps"))
+    assert ja == jb
