@@ -404,6 +404,10 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
+// SMOE_DOWN_L2=1: k_ffn_gu warms L2 with the down-projection blocks (measured
+// neutral on Q30: down gets faster, gate/up slower by as much)
+__device__ int g_down_l2_dev = 0;
+
 // Wait (thread 0) until the predictor of layer-1 published this layer's
 // decision for the current pass (publish_decision).
 __device__ __forceinline__ void wait_decision(const DevState& st, const DevCtl& ctl, int layer) {
@@ -876,6 +880,20 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
     PipeB pipe;
     pipe.init(pipe_mem, kL2EvictFirst);
     pipe.prime(tile, H);
+    if (g_down_l2_dev && threadIdx.x == 0) {
+        // warm L2 with this CTA's share of the expert's down-projection block,
+        // so k_ffn_down streams it from L2 while our gate/up stream runs on HBM
+        const char* dn = reinterpret_cast<const char*>(
+            m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems);
+        const long long bytes = static_cast<long long>(m.Hp) * m.Hmp * 2;
+        const int parts = m.Hmp / 16;
+        const long long part = ((bytes + parts - 1) / parts + 15) / 16 * 16;
+        const long long b0 = part * rb, b1 = min(bytes, b0 + part);
+        for (long long o = b0; o < b1; o += 65536) {
+            const uint32_t nb = static_cast<uint32_t>(min(65536LL, b1 - o)) & ~15u;
+            if (nb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(dn + o), "r"(nb) : "memory");
+        }
+    }
     if (early) {
         pdl_wait();
         KT_WAITED();
@@ -1422,6 +1440,11 @@ cudaError_t launch_embed(const DevModel& m, const DevState& st, const int* token
 // expert kernel spins on a copy-ready flag the copy thread's API calls block
 // behind it (observed deadlock).  Session construction calls this once.
 cudaError_t preload_kernels() {
+    {
+        const int v = std::getenv("SMOE_DOWN_L2") ? 1 : 0;
+        cudaError_t e = cudaMemcpyToSymbol(g_down_l2_dev, &v, sizeof v);
+        if (e != cudaSuccess) return e;
+    }
     const void* fns[] = {(const void*)k_gen_bf16, (const void*)k_embed, (const void*)k_qkv,
                          (const void*)k_attn, (const void*)k_wo, (const void*)k_router,
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_ffn_down,
