@@ -153,7 +153,10 @@ ExpertStore::~ExpertStore() {
 SlotCache::SlotCache(int L, int E, int C)
     : L_(L), E_(E), C_(C), expert_slot_(L, std::vector<int>(E, -1)),
       slot_expert_(L, std::vector<int>(C, -1)), stamp_(L, std::vector<long long>(C, -1)),
-      hits_(L, 0), misses_(L, 0) {}
+      freq_(L, std::vector<long long>(E, 0)), hits_(L, 0), misses_(L, 0) {
+    const char* p = std::getenv("SMOE_CACHE_POLICY");
+    lfu_ = p && std::string(p) == "lfu";
+}
 
 void SlotCache::clear_stats() {
     std::fill(hits_.begin(), hits_.end(), 0);
@@ -178,6 +181,9 @@ std::vector<std::pair<int, int>> SlotCache::request(int layer, const int* ids, i
     auto& es = expert_slot_[layer];
     auto& se = slot_expert_[layer];
     auto& st = stamp_[layer];
+    auto& fq = freq_[layer];
+    for (int i = 0; i < n; ++i)
+        if (ids[i] >= 0 && ids[i] < E_) ++fq[ids[i]];
     for (int i = 0; i < n; ++i) {
         const int e = ids[i];
         if (e < 0 || e >= E_) throw std::runtime_error("copy request with bad expert id");
@@ -189,7 +195,16 @@ std::vector<std::pair<int, int>> SlotCache::request(int layer, const int* ids, i
         int victim = -1;
         for (int c = 0; c < C_; ++c) {
             if (st[c] == now) continue;  // holds an expert of this request
-            if (victim < 0 || st[c] < st[victim]) victim = c;
+            if (victim < 0) {
+                victim = c;
+                continue;
+            }
+            if (lfu_ && se[c] >= 0 && se[victim] >= 0) {  // least requested, then least recent
+                const long long fc = fq[se[c]], fv = fq[se[victim]];
+                if (fc < fv || (fc == fv && st[c] < st[victim])) victim = c;
+            } else if (st[c] < st[victim]) {
+                victim = c;
+            }
         }
         if (victim < 0) throw std::runtime_error("slot pool smaller than the request");
         if (se[victim] >= 0) es[se[victim]] = -1;

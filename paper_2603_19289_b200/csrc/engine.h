@@ -95,6 +95,8 @@ private:
     std::vector<std::vector<int>> expert_slot_;   // [L][E] -> slot or -1
     std::vector<std::vector<int>> slot_expert_;   // [L][C] -> expert or -1
     std::vector<std::vector<long long>> stamp_;   // [L][C]
+    std::vector<std::vector<long long>> freq_;    // [L][E] requests seen (LFU)
+    bool lfu_ = false;
     std::vector<long long> hits_, misses_;
 };
 
