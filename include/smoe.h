@@ -103,6 +103,12 @@ int smoe_set_cache_fraction(smoe_session* s, float cache_fraction);
 int smoe_reset(smoe_session* s, int32_t max_steps, int32_t trace_full);
 /* Prefill with true routing, one forward_decode per token (model.cpp:355-389). */
 int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n);
+/* Batched prefill: the same results as smoe_prefill (KV cache, next token,
+ * every later decode step), all n tokens per layer at once — dense weights
+ * and each executed expert are streamed once per layer, experts loaded into
+ * the slot pool in waves.  The prompt's per-token trace rows are not recorded.
+ * Single GPU; with the Oracle predictor it falls back to smoe_prefill. */
+int smoe_prefill_batched(smoe_session* s, const int32_t* tokens, int32_t n);
 /* n_steps greedy decode steps on the device (speculative_forward semantics in
  * SMOE_PREFETCH mode, forward_decode in SMOE_ON_DEMAND mode). */
 int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph);

@@ -117,6 +117,13 @@ int smoe_reset(smoe_session* s, int32_t max_steps, int32_t trace_full) {
     });
 }
 
+int smoe_prefill_batched(smoe_session* s, const int32_t* tokens, int32_t n) {
+    return guard([&] {
+        if (!tokens && n > 0) throw std::invalid_argument("null tokens");
+        S(s)->prefill_batched(tokens, n);
+    });
+}
+
 int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n) {
     return guard([&] {
         if (!tokens && n > 0) throw std::invalid_argument("null tokens");

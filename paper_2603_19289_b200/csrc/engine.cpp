@@ -384,6 +384,7 @@ Session::Session(const ModelCfg& cfg, const SessionOpts& opts) : cfg_(cfg), opts
     ck(cudaSetDevice(opts_.device), "cudaSetDevice");
     write_value_fn();
     ck(preload_kernels(), "kernel preload");
+    ck(pf_preload(), "prefill kernel preload");
     try {
         alloc();
     } catch (...) {
@@ -1284,6 +1285,118 @@ void Session::prefill(const int* tokens, int n) {
         }
         ++steps_;
     }
+    sync();
+}
+
+// Batched prefill: true routing, all tokens per layer at
+// once; the executed experts of a layer are loaded once (in waves of at most
+// C slots) instead of once per token.  Produces the same KV cache, next token
+// and later decode steps as prefill() (tests/test_gpu.py); per-token trace
+// rows of the prompt are not recorded.
+void Session::prefill_batched(const int* tokens, int n) {
+    if (n < 1) throw std::invalid_argument("generate: empty prompt");
+    if (opts_.ep_world > 1) throw std::invalid_argument("prefill_batched: single GPU only");
+    if (pred_kind_ == kOracle) {  // the Oracle replays a shadow state token by token
+        prefill(tokens, n);
+        return;
+    }
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    const ModelCfg& c = cfg_;
+    for (int i = 0; i < n; ++i)
+        if (tokens[i] < 0 || tokens[i] >= c.V) throw std::invalid_argument("forward_decode: token out of vocab");
+    int pos = 0;
+    d2h(&pos, st_.pos, 4, "pos");
+    if (pos + n >= dm_.cap) throw std::invalid_argument("prefill: KV capacity exceeded");
+    const DevModel& m = dm_;
+    const long long E = c.E, K = c.K, Hp = m.Hp, D = c.D, nb = m.Hp / 32;
+    if (n > pf_cap_) {  // (re)allocate for n tokens
+        auto fr = [&](void* p) {
+            for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
+                if (*it == p) {
+                    cudaFree(p);
+                    dev_allocs_.erase(it);
+                    return;
+                }
+        };
+        for (void* p : {(void*)pf_.tokens, (void*)pf_.X, (void*)pf_.ssqx, (void*)pf_.Q, (void*)pf_.ctx,
+                        (void*)pf_.R, (void*)pf_.ssqr, (void*)pf_.lg, (void*)pf_.ids, (void*)pf_.gates,
+                        (void*)pf_.cnt, (void*)pf_.off, (void*)pf_.fill, (void*)pf_.list, (void*)pf_.Hb,
+                        (void*)pf_.Y, (void*)pf_.attn_scratch})
+            if (p) fr(p);
+        const long long P = n;
+        pf_ = PrefillDev{};
+        pf_.tokens = static_cast<int*>(dalloc(4ull * P));
+        pf_.X = static_cast<float*>(dalloc(4ull * P * Hp));
+        pf_.ssqx = static_cast<double*>(dalloc(8ull * P * nb));
+        pf_.Q = static_cast<float*>(dalloc(4ull * P * D));
+        pf_.ctx = static_cast<float*>(dalloc(4ull * P * D));
+        pf_.R = static_cast<float*>(dalloc(4ull * P * Hp));
+        pf_.ssqr = static_cast<double*>(dalloc(8ull * P * nb));
+        pf_.lg = static_cast<float*>(dalloc(4ull * P * E));
+        pf_.ids = static_cast<int*>(dalloc(4ull * P * K));
+        pf_.gates = static_cast<float*>(dalloc(4ull * P * K));
+        pf_.cnt = static_cast<int*>(dalloc(4ull * E));
+        pf_.off = static_cast<int*>(dalloc(4ull * (E + 1)));
+        pf_.fill = static_cast<int*>(dalloc(4ull * E));
+        pf_.list = static_cast<int*>(dalloc(4ull * P * K));
+        pf_.Hb = static_cast<float*>(dalloc(4ull * P * K * m.Hmp));
+        pf_.Y = static_cast<float*>(dalloc(4ull * P * K * Hp));
+        if (m.cap > pf_attn_smem_positions())
+            pf_.attn_scratch = static_cast<double*>(dalloc(8ull * P * 2 * m.cap));
+        pf_cap_ = n;
+    }
+    pf_.P = n;
+    pf_.pos0 = pos;
+    pf_.attn_smem_positions = pf_attn_smem_positions();
+    pf_.dev_step = ctl_.step;
+    pf_.trace_step = tr_.cap > 0 ? tr_.step : nullptr;
+    h2d(const_cast<int*>(pf_.tokens), tokens, 4ull * n, "prompt");
+    ck(launch_pf_embed(m, pf_, s_comp_), "prefill embed");
+    std::vector<int> cnt(E);
+    for (int l = 0; l < c.L; ++l) {
+        dset(pf_.cnt, 0, 4ull * E, "prefill counts");
+        ck(launch_pf_layer_dense(m, st_, pf_, l, s_comp_), "prefill layer");
+        d2h(cnt.data(), pf_.cnt, 4ull * E, "prefill counts");  // (synchronises)
+        std::vector<int> uni;
+        for (int e = 0; e < c.E; ++e)
+            if (cnt[e] > 0) uni.push_back(e);
+        const int W = std::min<int>(C_, kMaxWave);
+        for (size_t w0 = 0; w0 < uni.size(); w0 += W) {
+            const int nw = static_cast<int>(std::min<size_t>(W, uni.size() - w0));
+            PfWave wv{};
+            wv.n = nw;
+            int chunks = 1;
+            for (int u = 0; u < nw; ++u) {
+                wv.e[u] = uni[w0 + u];
+                chunks = std::max(chunks, (cnt[uni[w0 + u]] + 7) / 8);
+            }
+            if (!ctl_.resident) {  // load the wave's experts into this layer's slots
+                int hits = 0, misses = 0;
+                auto copies = cache_->request(l, wv.e, nw, &hits, &misses);
+                const long long bytes = store_->bytes_per_expert();
+                for (auto& [slot, expert] : copies)
+                    ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems,
+                                       store_->expert(store_index(l, expert)), bytes, cudaMemcpyHostToDevice,
+                                       s_copy_),
+                       "prefill expert copy");
+                ck(cudaStreamSynchronize(s_copy_), "prefill copies");
+                h2d(d_slot_of_ + static_cast<long long>(l) * c.E, cache_->slot_row(l).data(), 4ull * c.E,
+                    "slot table");
+            }
+            const std::vector<int>& row = cache_->slot_row(l);
+            for (int u = 0; u < nw; ++u) {
+                wv.slot[u] = row[wv.e[u]];
+                if (wv.slot[u] < 0) throw std::runtime_error("expert read before readiness at layer " + std::to_string(l));
+            }
+            ck(launch_pf_experts(m, pf_, l, wv, chunks, s_comp_), "prefill experts");
+            if (w0 + W < uni.size()) ck(cudaStreamSynchronize(s_comp_), "prefill wave");  // slots reused
+        }
+        ck(launch_pf_mix(m, pf_, s_comp_), "prefill mix");
+    }
+    ck(launch_pf_handoff(m, st_, pf_, s_comp_), "prefill handoff");
+    ck(launch_final(dm_, st_, ctl_, 1, s_comp_), "final");
+    steps_ += n;
     sync();
 }
 

@@ -147,6 +147,8 @@ public:
     // --- decode --------------------------------------------------------------
     void reset(int max_steps, int trace_full);
     void prefill(const int* tokens, int n);               // true routing per token
+    // all n prompt tokens per layer at once (prefill.cu); same results
+    void prefill_batched(const int* tokens, int n);
     void decode(int mode, int n_steps, int use_graph);    // greedy, device-driven
     // Teacher-forced decode: step i consumes tokens[i] instead of the previous
     // argmax (the reference's trace workload, trace.cpp:187-211, fed through
@@ -244,6 +246,8 @@ private:
     unsigned char* d_ep_region_ = nullptr;  // EP region: tag | counters | exchange buffer
     unsigned long long ep_tag_[2] = {0, 0};
     float* d_xbuf_ = nullptr;              // EP exchange buffer [2][K][Hp]
+    PrefillDev pf_{};                      // batched-prefill buffers (sized for pf_cap_ tokens)
+    int pf_cap_ = 0;
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]
     int* d_epoch_ = nullptr;               // EP combines done [L]
     std::vector<void*> ipc_opened_;

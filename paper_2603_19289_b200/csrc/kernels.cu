@@ -65,26 +65,6 @@ extern "C" int smoe_ktrace_read(unsigned long long* out) {
 
 namespace smoe {
 
-__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
-    return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
-}
-
-extern __shared__ __align__(128) unsigned char g_smem[];
-
-// "Last CTA done" gate: returns true in every thread of the last CTA to arrive.
-__device__ bool last_cta(int* counter, int total) {
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const int prev = atomicAdd(counter, 1);
-        s_last = (prev == total - 1);
-        if (s_last) *counter = 0;
-    }
-    __syncthreads();
-    if (s_last) __threadfence();
-    return s_last != 0;
-}
 
 
 // The decision for `layer` (and its copy request) is complete: release it to
@@ -1333,34 +1313,6 @@ __global__ void k_trace_bump(TraceDev tr) {
 
 static long long g_launches = 0;
 
-// Every decode-path kernel is launched with programmatic stream
-// serialization (PDL); captured into the step graph as programmatic edges.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // the stream's priority as a launch attribute, so it survives graph capture
-    int prio = 0;
-    cudaStreamGetPriority(s, &prio);
-    attr[1].id = cudaLaunchAttributePriority;
-    attr[1].val.priority = prio;
-    static const bool no_pdl = std::getenv("SMOE_NO_PDL") != nullptr;  // diagnostics
-    cfg.attrs = no_pdl ? attr + 1 : attr;
-    cfg.numAttrs = no_pdl ? 1 : 2;
-    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-#define PDL(k, grid, block, smem, s, ...)                                   \
-    do {                                                                    \
-        cudaError_t e_ = launch_pdl(k, dim3(grid), dim3(block), smem, s, __VA_ARGS__); \
-        if (e_ != cudaSuccess) return e_;                                   \
-    } while (0)
 long long launch_counter() { return g_launches; }
 // SMOE_FUSED_FFN=1: gate/up and down in one grid (k_ffn).  Off by default:
 // measured slower on Q30 — the waiting down CTAs hold SM slots and starve the

@@ -83,6 +83,47 @@ cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& 
 cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
                            cudaStream_t s);
 
+// ---- batched prefill (prefill.cu) ----
+struct PrefillDev {
+    int P;              // tokens in this prefill
+    int pos0;           // KV position of token 0
+    int attn_smem_positions;
+    const int* tokens;  // [P]
+    float* X;           // [P][Hp] residual stream (layer input)
+    double* ssqx;       // [P][Hp/32] rms partials of X
+    float* Q;           // [P][D]
+    float* ctx;         // [P][D]
+    float* R;           // [P][Hp] r_l
+    double* ssqr;       // [P][Hp/32]
+    float* lg;          // [P][E] true router logits
+    int* ids;           // [P][K]
+    float* gates;       // [P][K]
+    int* cnt;           // [E] tokens per expert
+    int* off;           // [E+1]
+    int* fill;          // [E]
+    int* list;          // [P*K] entries t*K+i grouped by expert
+    float* Hb;          // [P*K][Hmp]
+    float* Y;           // [P*K][Hp] raw expert rows per (token, slot)
+    double* attn_scratch;  // [P][2*cap] when contexts exceed the smem budget
+    int* dev_step;      // ctl.step (token records)
+    int* trace_step;    // trace step counter (nullable)
+};
+constexpr int kMaxWave = 128;
+struct PfWave {
+    int n;
+    int e[kMaxWave];
+    int slot[kMaxWave];
+};
+int pf_attn_smem_positions();
+cudaError_t pf_preload();
+cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
+cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
+                                  cudaStream_t s);
+cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
+                              int chunks, cudaStream_t s);
+cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
+cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
+
 int max_dynamic_smem_needed(const DevModel& m);
 cudaError_t preload_kernels();
 // Number of kernel launches enqueued by the launchers so far (host counter).

@@ -1,0 +1,435 @@
+// prefill.cu — batched prefill: all P prompt tokens go
+// through a layer together, with true routing (forward_decode semantics,
+// model.cpp:355-389), so every dense weight is streamed once per layer instead
+// of once per token and every executed expert once per layer instead of once
+// per token that selected it.
+//
+// Arithmetic contract: identical to the per-token path (kernels.cu) — each
+// (row, token) dot product is the reference's sequential f32 chain in column
+// order (run_multi: one weight stream, T independent chains per lane), the
+// f64 softmax / rms steps are the same, the mixture is summed in decision
+// order.  The prefilled KV cache, the last token's logits and every later
+// decode step therefore equal the token-by-token prefill bit for bit
+// (tests/test_gpu.py::test_batched_prefill_*).
+//
+// Orchestration (Session::prefill_batched): per layer, qkv -> attention ->
+// wo -> router -> decisions + per-expert token lists on the device; the host
+// reads the union of executed experts, loads them into HBM slots in waves of
+// at most C experts (cache fraction permitting) and runs the gate/up and down
+// kernels per wave; then the per-token mixture.
+#include "kernels.h"
+#include "smoe_chain.cuh"
+
+namespace smoe {
+
+namespace {
+
+constexpr int kPT = 8;  // tokens per CTA (independent chains per lane)
+constexpr int kPW = 4;  // warps per CTA: four row tiles share one staging of the token inputs
+using PipePF = WarpPipe<uint16_t, kS, kCCb>;  // 8 KB chunks
+using PipePD = WarpPipe<uint16_t, kS, kCCb>;
+
+__device__ __forceinline__ void pf_prologue() {
+    pdl_wait();
+    pdl_trigger();
+}
+
+// xs[t][*] = (v_t * scale_t) * gain (rms_norm, numerics.cpp:72-84) for the
+// tokens of this CTA; scale from the producer's f64 partials (same fixed
+// order as the per-token path).  Whole block (one warp).
+__device__ void pf_stage_norm(const DevModel& m, const float* V, const double* ssq, const float* gain,
+                              const int* tok_of, int nt, float* xs, int xstride) {
+    const int H = m.H, nb = m.Hp / 32;
+    for (int t = 0; t < nt; ++t) {
+        const int tok = tok_of[t];
+        const float scale = rms_scale_from_partials(ssq + static_cast<long long>(tok) * nb, nb, H, m.eps);
+        const float4* v4 = reinterpret_cast<const float4*>(V + static_cast<long long>(tok) * m.Hp);
+        const float4* g4 = reinterpret_cast<const float4*>(gain);
+        float4* o4 = reinterpret_cast<float4*>(xs + t * xstride);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < (H >> 2); i += blockDim.x) {
+            const float4 a = __ldcg(v4 + i), g = __ldg(g4 + i);
+            o4[i] = make_float4(a.x * scale * g.x, a.y * scale * g.y, a.z * scale * g.z, a.w * scale * g.w);
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ embed --
+__global__ void __launch_bounds__(32) k_pf_embed(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    const int t = blockIdx.y, j = blockIdx.x * 32 + threadIdx.x;
+    const int tok = pf.tokens[t];
+    const float v = j < m.H ? bf2f(m.emb[static_cast<long long>(tok) * m.H + j]) : 0.0f;
+    pf.X[static_cast<long long>(t) * m.Hp + j] = v;
+    warp_ssq_partial(v, pf.ssqx + static_cast<long long>(t) * (m.Hp / 32) + blockIdx.x);
+}
+
+// -------------------------------------------------------------------- qkv --
+// q, k, v for kPT tokens per CTA (model.cpp:325-333), RoPE at position
+// pos0 + t, K/V appended to the layer's cache, q kept per token.
+__global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, PrefillDev pf, int layer) {
+    const int H = m.H, Hr = round_up(H, 32), D = m.D, w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
+    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    const bool has_tile = rb * 32 < m.QKVp;
+    const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * H * 32;
+    PipePF pipe;
+    pipe.init(pipe_mem);
+    if (has_tile) pipe.prime(tile, H);
+    pf_prologue();
+    int tok_of[kPT];
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
+    pf_stage_norm(m, pf.X, pf.ssqx, m.attn_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    const int lane = threadIdx.x & 31, R = rb * 32 + lane;
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) {
+        float a = acc[t];
+        const float other = __shfl_xor_sync(0xffffffffu, a, 1);
+        if (t >= nt) continue;
+        const int pos = pf.pos0 + t0 + t;
+        if (R < 2 * D) {  // RoPE pair (2i, 2i+1), model.cpp:309-321
+            const int i = (R % D) >> 1;
+            const float c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
+            const float s = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2 + 1];
+            const bool even = (R & 1) == 0;
+            const float x0 = even ? a : other, x1 = even ? other : a;
+            a = even ? (x0 * c - x1 * s) : (x0 * s + x1 * c);
+        }
+        const long long kv = (static_cast<long long>(layer) * m.cap + pos) * D;
+        if (R < D)
+            pf.Q[static_cast<long long>(t0 + t) * D + R] = a;
+        else if (R < 2 * D)
+            st.kc[kv + R - D] = a;
+        else if (R < 3 * D)
+            st.vc[kv + R - 2 * D] = a;
+    }
+}
+
+// -------------------------------------------------------------- attention --
+// scores / softmax / context for token t over positions 0 .. pos0 + t
+// (model.cpp:335-351), one CTA per token; the same operation order as k_attn.
+constexpr int kPfAttnThreads = 256;
+__global__ void __launch_bounds__(kPfAttnThreads) k_pf_attn(DevModel m, DevState st, PrefillDev pf,
+                                                             int layer) {
+    pf_prologue();
+    const int D = m.D, t = blockIdx.x, n = pf.pos0 + t + 1;
+    float* red = reinterpret_cast<float*>(g_smem);  // [32]
+    float* qs = red + 32;                           // [D]
+    double* e = reinterpret_cast<double*>(qs + kMaxD);
+    float* sc = reinterpret_cast<float*>(e + n);
+    if (pf.pos0 + pf.P > pf.attn_smem_positions) {  // long contexts: per-token scratch in global memory
+        e = pf.attn_scratch + static_cast<long long>(t) * 2 * m.cap;
+        sc = reinterpret_cast<float*>(e + m.cap);
+    }
+    const float* K = st.kc + static_cast<long long>(layer) * m.cap * D;
+    const float* V = st.vc + static_cast<long long>(layer) * m.cap * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = __ldcg(pf.Q + static_cast<long long>(t) * D + i);
+    __syncthreads();
+    float lmax = -INFINITY;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const float4* kj = reinterpret_cast<const float4*>(K + static_cast<long long>(j) * D);
+        float acc = 0.0f;
+        for (int i = 0; i < D / 4; ++i) {
+            const float4 kv = __ldcg(kj + i);
+            acc = acc + qs[4 * i] * kv.x;
+            acc = acc + qs[4 * i + 1] * kv.y;
+            acc = acc + qs[4 * i + 2] * kv.z;
+            acc = acc + qs[4 * i + 3] * kv.w;
+        }
+        const float v = acc * m.inv_sqrt_d;
+        sc[j] = v;
+        lmax = fmaxf(lmax, v);
+    }
+    const float mx = block_max_f(lmax, red);
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
+    __syncthreads();
+    __shared__ double zs;
+    if (threadIdx.x == 0) {  // f64 partition in index order, numerics.cpp:46-49
+        double z = 0.0;
+        for (int j = 0; j < n; ++j) z += e[j];
+        zs = z;
+    }
+    __syncthreads();
+    const double z = zs;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) sc[j] = static_cast<float>(e[j] / z);
+    __syncthreads();
+    const int i = threadIdx.x;
+    if (i < D) {
+        float acc = 0.0f;
+        for (int j = 0; j < n; ++j) acc = acc + sc[j] * __ldcg(V + static_cast<long long>(j) * D + i);
+        pf.ctx[static_cast<long long>(t) * D + i] = acc;
+    }
+}
+
+// --------------------------------------------------------------------- wo --
+// r = x + wo . ctx (model.cpp:352, 380) for kPT tokens, rms partials of r.
+__global__ void __launch_bounds__(32 * kPW) k_pf_wo(DevModel m, PrefillDev pf, int layer) {
+    const int D = m.D, w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][kMaxD]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * kMaxD)) + w * PipePD::kBytes;
+    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    const bool has_tile = rb * 32 < m.Hp;
+    const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * D * 32;
+    PipePD pipe;
+    pipe.init(pipe_mem);
+    if (has_tile) pipe.prime(tile, D);
+    pf_prologue();
+    for (int t = 0; t < nt; ++t)
+        for (int i = threadIdx.x; i < D; i += blockDim.x)
+            xs[t * kMaxD + i] = __ldcg(pf.ctx + static_cast<long long>(t0 + t) * D + i);
+    __syncthreads();
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, D, xs, kMaxD, nt, acc);
+    const int j = rb * 32 + (threadIdx.x & 31);
+    for (int t = 0; t < nt; ++t) {
+        const long long o = static_cast<long long>(t0 + t) * m.Hp + j;
+        const float r = j < m.H ? __ldcg(pf.X + o) + acc[t] : 0.0f;
+        pf.R[o] = r;
+        warp_ssq_partial(r, pf.ssqr + static_cast<long long>(t0 + t) * (m.Hp / 32) + rb);
+    }
+}
+
+// ----------------------------------------------------------------- router --
+// true router logits gate . rms_norm(r, moe_gain) (model.cpp:276-281).
+__global__ void __launch_bounds__(32 * kPW) k_pf_router(DevModel m, PrefillDev pf, int layer) {
+    const int H = m.H, Hr = round_up(H, 32), E = m.E, w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
+    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    const bool has_tile = rb * 32 < m.Ep;
+    const uint16_t* tile = m.gate + layer * m.gate_stride + static_cast<long long>(rb) * H * 32;
+    PipePF pipe;
+    pipe.init(pipe_mem);
+    if (has_tile) pipe.prime(tile, H);
+    pf_prologue();
+    int tok_of[kPT];
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
+    pf_stage_norm(m, pf.R, pf.ssqr, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    const int e = rb * 32 + (threadIdx.x & 31);
+    if (e < E)
+        for (int t = 0; t < nt; ++t) pf.lg[static_cast<long long>(t0 + t) * E + e] = acc[t];
+}
+
+// make_decision per token (model.cpp:258-274) and per-expert counts.
+__global__ void __launch_bounds__(32) k_pf_decide(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    __shared__ double se[kMaxE];
+    __shared__ float sp[kMaxE];
+    const int t = blockIdx.x, K = m.K;
+    warp_decision(pf.lg + static_cast<long long>(t) * m.E, m.E, K, m.gating, sp, se, pf.ids + t * K,
+                  pf.gates + t * K);
+    __syncwarp();
+    if (threadIdx.x < K) atomicAdd(pf.cnt + __ldcg(pf.ids + t * K + threadIdx.x), 1);
+}
+
+// offsets of the per-expert (token, slot) lists: exclusive scan over E (1 CTA)
+__global__ void k_pf_offsets(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int e = 0; e < m.E; ++e) {
+            pf.off[e] = s;
+            s += pf.cnt[e];
+            pf.fill[e] = 0;
+        }
+        pf.off[m.E] = s;
+    }
+}
+
+// list entries t * K + i grouped by expert (order inside a group is free: every
+// (token, expert) pair is computed independently and mixed per token later)
+__global__ void __launch_bounds__(32) k_pf_scatter(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    const int t = blockIdx.x, K = m.K;
+    if (threadIdx.x < K) {
+        const int e = pf.ids[t * K + threadIdx.x];
+        const int slot = pf.off[e] + atomicAdd(pf.fill + e, 1);
+        pf.list[slot] = t * K + threadIdx.x;
+    }
+}
+
+// ---------------------------------------------------------------- experts --
+// gate/up: grid (Hmp/16, wave experts, token chunks of kPT); h = silu(g) * u.
+__global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, int layer, PfWave wv) {
+    const int H = m.H, Hr = round_up(H, 32), K = m.K, w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
+    const int rb = blockIdx.x * kPW + w, u = blockIdx.y, e = wv.e[u];
+    pf_prologue();
+    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = blockIdx.z * kPT;
+    if (c0 >= cnt) return;
+    const int nt = min(kPT, cnt - c0);
+    const bool has_tile = rb * 16 < m.Hmp;
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
+                           static_cast<long long>(rb) * H * 32;
+    PipePF pipe;
+    pipe.init(pipe_mem, kL2EvictFirst);
+    if (has_tile) pipe.prime(tile, H);
+    int ent[kPT], tok_of[kPT];
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) {
+        ent[t] = t < nt ? __ldcg(pf.list + b0 + c0 + t) : 0;
+        tok_of[t] = ent[t] / K;
+    }
+    pf_stage_norm(m, pf.R, pf.ssqr, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) {
+        const float up = __shfl_xor_sync(0xffffffffu, acc[t], 1);
+        if (t < nt && (lane & 1) == 0)
+            pf.Hb[static_cast<long long>(ent[t]) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc[t]) * up;
+    }
+}
+
+// down: grid (Hp/32, wave experts, token chunks); raw expert rows into Y.
+__global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf, int layer, PfWave wv) {
+    const int Hmp = m.Hmp, w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hmp]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hmp)) + w * PipePD::kBytes;
+    const int rb = blockIdx.x * kPW + w, u = blockIdx.y, e = wv.e[u];
+    pf_prologue();
+    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = blockIdx.z * kPT;
+    if (c0 >= cnt) return;
+    const int nt = min(kPT, cnt - c0);
+    const bool has_tile = rb * 32 < m.Hp;
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
+                           m.gu_elems + static_cast<long long>(rb) * Hmp * 32;
+    PipePD pipe;
+    pipe.init(pipe_mem, kL2EvictFirst);
+    if (has_tile) pipe.prime(tile, m.Hm);
+    int ent[kPT];
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) ent[t] = t < nt ? __ldcg(pf.list + b0 + c0 + t) : 0;
+    for (int t = 0; t < nt; ++t) {
+        const float4* h4 = reinterpret_cast<const float4*>(pf.Hb + static_cast<long long>(ent[t]) * Hmp);
+        for (int i = threadIdx.x; i < Hmp / 4; i += blockDim.x)
+            reinterpret_cast<float4*>(xs + t * Hmp)[i] = __ldcg(h4 + i);
+    }
+    __syncthreads();
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, m.Hm, xs, Hmp, nt, acc);
+    const int j = rb * 32 + (threadIdx.x & 31);
+    if (j < m.H)
+        for (int t = 0; t < nt; ++t) pf.Y[static_cast<long long>(ent[t]) * m.Hp + j] = acc[t];
+}
+
+// mixture in decision order (model.cpp:297-301), x = r + m, rms partials of x.
+__global__ void __launch_bounds__(32) k_pf_mix(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    const int t = blockIdx.y, rb = blockIdx.x, j = rb * 32 + threadIdx.x, K = m.K;
+    float xv = 0.0f;
+    if (j < m.H) {
+        float out = 0.0f;
+        for (int i = 0; i < K; ++i)
+            out += __ldcg(pf.gates + t * K + i) * __ldcg(pf.Y + (static_cast<long long>(t) * K + i) * m.Hp + j);
+        xv = __ldcg(pf.R + static_cast<long long>(t) * m.Hp + j) + out;
+    }
+    pf.X[static_cast<long long>(t) * m.Hp + j] = xv;
+    warp_ssq_partial(xv, pf.ssqx + static_cast<long long>(t) * (m.Hp / 32) + rb);
+}
+
+// hands the last token to the per-token state: x, its final-norm partials,
+// position and input token, so k_final produces the prefill's next token.
+__global__ void __launch_bounds__(32) k_pf_handoff(DevModel m, DevState st, PrefillDev pf) {
+    pf_prologue();
+    const int t = pf.P - 1, rb = blockIdx.x, j = rb * 32 + threadIdx.x;
+    st.x[j] = __ldcg(pf.X + static_cast<long long>(t) * m.Hp + j);
+    if (threadIdx.x == 0) {
+        st.ssq_x[static_cast<long long>(m.L) * (m.Hp / 32) + rb] = __ldcg(pf.ssqx + static_cast<long long>(t) * (m.Hp / 32) + rb);
+        if (rb == 0) {
+            *st.pos = pf.pos0 + t;
+            *st.tok_in = pf.tokens[t];
+            // token / trace records of the P - 1 earlier steps are skipped, so
+            // the last prefill token and later decode steps keep their indices
+            *pf.dev_step = *pf.dev_step + t;  // k_final records the last token at t
+            if (pf.trace_step) *pf.trace_step = *pf.trace_step + pf.P;  // no trace rows
+        }
+    }
+}
+
+// ---------------------------------------------------------------- launchers --
+namespace {
+size_t vecf(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
+size_t pf_h_smem(const DevModel& m) { return kPT * vecf(m.H) + 128 + kPW * PipePF::kBytes; }
+size_t pf_wo_smem(const DevModel& m) { return kPT * kMaxD * 4 + 128 + kPW * PipePD::kBytes; }
+size_t pf_down_smem(const DevModel& m) { return kPT * static_cast<size_t>(m.Hmp) * 4 + 128 + kPW * PipePD::kBytes; }
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+size_t pf_attn_smem(const DevModel& m, int npos) {
+    return (32 + kMaxD) * 4 + static_cast<size_t>(npos) * 12;
+}
+}  // namespace
+
+int pf_attn_smem_positions() { return 12 * 1024; }
+
+cudaError_t pf_preload() {
+    const void* fns[] = {(const void*)k_pf_embed, (const void*)k_pf_qkv, (const void*)k_pf_attn,
+                         (const void*)k_pf_wo, (const void*)k_pf_router, (const void*)k_pf_decide,
+                         (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu,
+                         (const void*)k_pf_down, (const void*)k_pf_mix, (const void*)k_pf_handoff};
+    for (const void* f : fns) {
+        cudaFuncAttributes a;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+        // opt-in maximum per block (227 KB on sm_100) minus the static shared memory
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(227 * 1024 - a.sharedSizeBytes));
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
+                                  cudaStream_t s) {
+    const int tg = (pf.P + kPT - 1) / kPT;
+    PDL(k_pf_qkv, dim3(cdiv(m.QKVp / 32, kPW), tg), 32 * kPW, pf_h_smem(m), s, m, st, pf, layer);
+    const int npos = pf.pos0 + pf.P <= pf.attn_smem_positions ? pf.pos0 + pf.P : 0;
+    PDL(k_pf_attn, pf.P, kPfAttnThreads, pf_attn_smem(m, npos), s, m, st, pf, layer);
+    PDL(k_pf_wo, dim3(cdiv(m.Hp / 32, kPW), tg), 32 * kPW, pf_wo_smem(m), s, m, pf, layer);
+    PDL(k_pf_router, dim3(cdiv(m.Ep / 32, kPW), tg), 32 * kPW, pf_h_smem(m), s, m, pf, layer);
+    PDL(k_pf_decide, pf.P, 32, 0, s, m, pf);
+    PDL(k_pf_offsets, 1, 32, 0, s, m, pf);
+    PDL(k_pf_scatter, pf.P, 32, 0, s, m, pf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
+    PDL(k_pf_embed, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
+                              int chunks, cudaStream_t s) {
+    PDL(k_pf_gu, dim3(cdiv(m.Hmp / 16, kPW), wv.n, chunks), 32 * kPW, pf_h_smem(m), s, m, pf, layer, wv);
+    PDL(k_pf_down, dim3(cdiv(m.Hp / 32, kPW), wv.n, chunks), 32 * kPW, pf_down_smem(m), s, m, pf, layer, wv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
+    PDL(k_pf_mix, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s) {
+    PDL(k_pf_handoff, m.Hp / 32, 32, 0, s, m, st, pf);
+    return cudaGetLastError();
+}
+
+}  // namespace smoe

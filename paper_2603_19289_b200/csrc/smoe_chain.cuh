@@ -5,6 +5,7 @@
 #pragma once
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "smoe_dev.h"
 
@@ -149,7 +150,7 @@ __device__ __forceinline__ float silu_ref(float x) {
 
 // Deterministic block reduction of a per-thread double (tree order fixed by
 // blockDim).  Returns the same value in every thread.
-__device__ double block_sum_d(double v, double* red) {
+__device__ inline double block_sum_d(double v, double* red) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     if ((threadIdx.x & 31) == 0) red[w] = v;
@@ -160,7 +161,7 @@ __device__ double block_sum_d(double v, double* red) {
     return t;
 }
 
-__device__ float block_max_f(float v, float* red) {
+__device__ inline float block_max_f(float v, float* red) {
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_down_sync(0xffffffffu, v, o));
     const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     if ((threadIdx.x & 31) == 0) red[w] = v;
@@ -176,7 +177,7 @@ __device__ float block_max_f(float v, float* red) {
 // v, gain, out are 16-byte aligned shared arrays and n % 4 == 0 (H % 8 == 0 is
 // validated).  The f64 sum runs as 4 independent partial sums per thread
 // (fixed order: the reduction tree is deterministic).
-__device__ void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
+__device__ inline void block_rms_norm(const float* v, const float* gain, int n, float eps, float* out,
                                double* red) {
     const float4* v4 = reinterpret_cast<const float4*>(v);
     const float4* g4 = reinterpret_cast<const float4*>(gain);
@@ -239,6 +240,27 @@ __device__ __forceinline__ void block_apply_norm(const float* v, const float* ga
         o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z, t.w * scale * g.w);
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+    return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+extern __shared__ __align__(128) unsigned char g_smem[];
+
+// "Last CTA done" gate: returns true in every thread of the last CTA to arrive.
+__device__ inline bool last_cta(int* counter, int total) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(counter, 1);
+        s_last = (prev == total - 1);
+        if (s_last) *counter = 0;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
 }
 
 // ------------------------------------------------------------ smem stager --
@@ -408,6 +430,7 @@ struct WarpPipe {
     long long wait_cyc = 0;  // cycles spent waiting for chunks (phase builds only)
 #endif
     static constexpr int G = 16 / static_cast<int>(sizeof(WT));
+    static constexpr int kS = S, kCC = CC;
     static constexpr int kChunkElems = CC * 32;
     static constexpr int kChunkBytes = kChunkElems * static_cast<int>(sizeof(WT));
     static constexpr int kBytes = S * kChunkBytes + S * 8;
@@ -538,6 +561,74 @@ struct WarpPipe {
     }
 };
 
+// Multi-token variant (batched prefill): the same bf16 row tile applied to nt
+// <= T tokens at once — T independent sequential chains per lane, one weight
+// stream.  xs: nt vectors of `xstride` floats in shared memory (16-byte
+// aligned).  Every token's chain is the single-token chain bit for bit (same
+// products, same column order); the T chains hide each other's FADD latency.
+template <int T, typename Pipe>
+__device__ inline void run_multi(Pipe& p, const uint16_t* tile, int cols, const float* xs, int xstride, int nt,
+                          float (&acc)[T]) {
+    constexpr int G = Pipe::G, CC = Pipe::kCC, S = Pipe::kS, GPC = CC / G;
+    const int lane = threadIdx.x & 31;
+    const int nch = (cols + CC - 1) / CC;
+    if (lane == 0 && !p.primed)
+        for (int n = 0; n < S && n < nch; ++n) p.issue(tile, cols, n, p.ctr + n);
+    p.primed = 0;
+    const uint32_t xbase = smem_u32(xs);
+    const uint32_t lbase = p.sbuf + lane * 16;
+    const int c0 = p.ctr;
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = 0.0f;
+    for (int n = 0; n < nch; ++n) {
+        const int g = c0 + n;
+        mbar_wait(&p.full[g % S], static_cast<uint32_t>((g / S) & 1));
+        const uint32_t cb = lbase + (g % S) * Pipe::kChunkBytes;
+        const int cn = min(CC, cols - n * CC);
+        const int ng = cn / G;
+        for (int q = 0; q < ng; ++q) {
+            const uint4 w = lds128(cb + q * 512);
+            const float w0 = lo_bf(w.x), w1 = hi_bf(w.x), w2 = lo_bf(w.y), w3 = hi_bf(w.y);
+            const float w4 = lo_bf(w.z), w5 = hi_bf(w.z), w6 = lo_bf(w.w), w7 = hi_bf(w.w);
+            const uint32_t xo = xbase + (n * CC + q * G) * 4;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                if (t < nt) {
+                    const float4 a = lds128f(xo + t * xstride * 4), b = lds128f(xo + t * xstride * 4 + 16);
+                    const float2 p0 = __fmul2_rn(make_float2(w0, w1), make_float2(a.x, a.y));
+                    const float2 p1 = __fmul2_rn(make_float2(w2, w3), make_float2(a.z, a.w));
+                    const float2 p2 = __fmul2_rn(make_float2(w4, w5), make_float2(b.x, b.y));
+                    const float2 p3 = __fmul2_rn(make_float2(w6, w7), make_float2(b.z, b.w));
+                    float s = acc[t];
+                    s = s + p0.x;
+                    s = s + p0.y;
+                    s = s + p1.x;
+                    s = s + p1.y;
+                    s = s + p2.x;
+                    s = s + p2.y;
+                    s = s + p3.x;
+                    s = s + p3.y;
+                    acc[t] = s;
+                }
+            }
+        }
+        const int tail = cn - ng * G;
+        if (tail) {
+            const uint4 w = lds128(cb + ng * 512);
+#pragma unroll
+            for (int t = 0; t < T; ++t)
+                if (t < nt) {
+                    const float* xt = xs + t * xstride + n * CC + ng * G;
+                    for (int i = 0; i < tail; ++i) acc[t] = acc[t] + group_elem(w, i, uint16_t{}) * xt[i];
+                }
+        }
+        __syncwarp();
+        if (n + S < nch && elect_one()) p.issue(tile, cols, n + S, g + S);
+    }
+    __syncwarp();
+    p.ctr += nch;
+}
+
 constexpr int kS = 4;       // stages per warp
 constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
 constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
@@ -561,7 +652,7 @@ __device__ long long g_dec_t[8];
 // index order by lane 0 (exactly the reference's order), f32 probabilities;
 // top_k (numerics.cpp:56-70): value desc, lower index first; gates renormalised
 // by an f32 sum in rank order.  topk-softmax: top_k on logits, softmax of the k.
-__device__ void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
+__device__ inline void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
                               double* se /*smem E*/, int* ids, float* gates) {
     const int lane = threadIdx.x & 31;
     DEC_T(0);
@@ -713,5 +804,35 @@ __device__ void warp_decision(const float* logits, int E, int K, int gating, flo
     __syncwarp();
     DEC_T(4);
 }
+
+// ------------------------------------------------------------- launching --
+// Every decode-path kernel is launched with programmatic stream
+// serialization (PDL); captured into the step graph as programmatic edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // the stream's priority as a launch attribute, so it survives graph capture
+    int prio = 0;
+    cudaStreamGetPriority(s, &prio);
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = prio;
+    static const bool no_pdl = std::getenv("SMOE_NO_PDL") != nullptr;  // diagnostics
+    cfg.attrs = no_pdl ? attr + 1 : attr;
+    cfg.numAttrs = no_pdl ? 1 : 2;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+#define PDL(k, grid, block, smem, s, ...)                                   \
+    do {                                                                    \
+        cudaError_t e_ = launch_pdl(k, dim3(grid), dim3(block), smem, s, __VA_ARGS__); \
+        if (e_ != cudaSuccess) return e_;                                   \
+    } while (0)
 
 }  // namespace smoe

@@ -32,7 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle",
+    "smoe_write_trace_bundle", "smoe_prefill_batched",
 ]
 
 
@@ -221,6 +221,11 @@ class Session:
     def prefill(self, tokens):
         t = np.ascontiguousarray(tokens, np.int32)
         _check(self.lib.smoe_prefill(self._h, _p(t), len(t)))
+
+    def prefill_batched(self, tokens):
+        """All prompt tokens per layer at once (same results as prefill)."""
+        t = np.ascontiguousarray(tokens, np.int32)
+        _check(self.lib.smoe_prefill_batched(self._h, _p(t), len(t)))
 
     def decode(self, mode: str, n_steps: int, use_graph: bool = True):
         _check(self.lib.smoe_decode(self._h, MODE[mode], n_steps, int(use_graph)))

@@ -517,3 +517,53 @@ def test_trace_bundle_matches_reference_writer(lib, tmp_path):
     jb = json.load(open(os.path.join(gdir, "manifest.json")))
     assert np.float32(ja["config"].pop("eps")) == np.float32(jb["config"].pop("eps"))
     assert ja == jb
+
+
+def _decode_after(cfg, prompt, n_dec, batched, frac, pred="router-pf", table=None):
+    from paper_2603_19289_b200 import ModelConfig, Session
+    s = Session(ModelConfig(**cfg), cache_fraction=frac, max_positions=512)
+    s.init_weights_seeded()
+    if table is not None:
+        s.load_default_vectors(table)
+    if frac == 1.0:
+        s.preload_all()
+    s.set_predictor(pred)
+    P = len(prompt)
+    S = P + n_dec
+    s.reset(S, True)
+    (s.prefill_batched if batched else s.prefill)(prompt)
+    s.decode("prefetch", n_dec)
+    out = {f: s.trace(f, S)[P:] for f in ("s", "r", "m", "lg_true", "id_exec", "g_exec", "y",
+                                         "logits", "id_pred")}
+    out["tokens"] = s.tokens(S)[P - 1:]
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("plen,frac", [(20, 0.25), (150, 1.0)])
+def test_batched_prefill_matches_token_prefill(lib, toy_oracle, plen, frac):
+    """§8f row 2: the batched prefill (all prompt tokens per layer, experts
+    loaded in slot-pool waves) leaves exactly the state the token-by-token
+    prefill leaves: the next token and every later decode step (tokens,
+    hidden states, router logits, decisions, expert outputs, logits) are
+    bit-identical; the token path itself is pinned to the reference."""
+    orc, om, table, est = toy_oracle
+    rng = np.random.default_rng(plen)
+    prompt = rng.integers(0, TOY["vocab"], plen).astype(np.int32)
+    a = _decode_after(TOY, prompt, 6, False, frac, table=np.array(table.d))
+    b = _decode_after(TOY, prompt, 6, True, frac, table=np.array(table.d))
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_batched_prefill_q30_layer_shapes(lib):
+    """Q30 layer shapes (H 2048, 128 experts top-8, Hm 768), 2 layers: batched
+    and token-by-token prefill agree bit for bit on the following decode."""
+    cfg = dict(layers=2, experts=128, top_k=8, hidden=2048, expert_hidden=768, vocab=256,
+               head_dim=128, seed=1)
+    prompt = (np.arange(24) * 37 % 256).astype(np.int32)
+    dv = np.zeros((2, 128, 2048), np.float32)
+    a = _decode_after(cfg, prompt, 3, False, 0.25, table=dv)
+    b = _decode_after(cfg, prompt, 3, True, 0.25, table=dv)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
