@@ -1322,7 +1322,8 @@ void Session::prefill_batched(const int* tokens, int n) {
         for (void* p : {(void*)pf_.tokens, (void*)pf_.X, (void*)pf_.ssqx, (void*)pf_.Q, (void*)pf_.ctx,
                         (void*)pf_.R, (void*)pf_.ssqr, (void*)pf_.lg, (void*)pf_.ids, (void*)pf_.gates,
                         (void*)pf_.cnt, (void*)pf_.off, (void*)pf_.fill, (void*)pf_.list, (void*)pf_.Hb,
-                        (void*)pf_.Y, (void*)pf_.attn_scratch})
+                        (void*)pf_.Y, (void*)pf_.attn_scratch, (void*)pf_.scale, (void*)pf_.chunk_u,
+                        (void*)pf_.chunk_c})
             if (p) fr(p);
         const long long P = n;
         pf_ = PrefillDev{};
@@ -1344,6 +1345,9 @@ void Session::prefill_batched(const int* tokens, int n) {
         pf_.Y = static_cast<float*>(dalloc(4ull * P * K * Hp));
         if (m.cap > pf_attn_smem_positions())
             pf_.attn_scratch = static_cast<double*>(dalloc(8ull * P * 2 * m.cap));
+        pf_.scale = static_cast<float*>(dalloc(4ull * P));
+        pf_.chunk_u = static_cast<int*>(dalloc(4ull * (P * K + E)));  // >= sum of ceil(cnt/8)
+        pf_.chunk_c = static_cast<int*>(dalloc(4ull * (P * K + E)));
         pf_cap_ = n;
     }
     pf_.P = n;
@@ -1366,11 +1370,17 @@ void Session::prefill_batched(const int* tokens, int n) {
             const int nw = static_cast<int>(std::min<size_t>(W, uni.size() - w0));
             PfWave wv{};
             wv.n = nw;
-            int chunks = 1;
+            std::vector<int> cu, cc;  // (expert, 8-token chunk) work items of the wave
             for (int u = 0; u < nw; ++u) {
                 wv.e[u] = uni[w0 + u];
-                chunks = std::max(chunks, (cnt[uni[w0 + u]] + 7) / 8);
+                for (int q = 0; q < (cnt[uni[w0 + u]] + 7) / 8; ++q) {
+                    cu.push_back(u);
+                    cc.push_back(q);
+                }
             }
+            const int chunks = static_cast<int>(cu.size());
+            h2d(pf_.chunk_u, cu.data(), 4ull * chunks, "prefill chunks");
+            h2d(pf_.chunk_c, cc.data(), 4ull * chunks, "prefill chunks");
             if (!ctl_.resident) {  // load the wave's experts into this layer's slots
                 int hits = 0, misses = 0;
                 auto copies = cache_->request(l, wv.e, nw, &hits, &misses);

@@ -105,6 +105,9 @@ struct PrefillDev {
     float* Hb;          // [P*K][Hmp]
     float* Y;           // [P*K][Hp] raw expert rows per (token, slot)
     double* attn_scratch;  // [P][2*cap] when contexts exceed the smem budget
+    float* scale;       // [P] rms scale of the vector being normalised (per stage)
+    int* chunk_u;       // [max chunks] wave expert index of each (expert, 8-token chunk)
+    int* chunk_c;       // [max chunks] chunk index within the expert's token list
     int* dev_step;      // ctl.step (token records)
     int* trace_step;    // trace step counter (nullable)
 };

@@ -25,9 +25,10 @@ namespace smoe {
 namespace {
 
 constexpr int kPT = 8;  // tokens per CTA (independent chains per lane)
-constexpr int kPW = 4;  // warps per CTA: four row tiles share one staging of the token inputs
-using PipePF = WarpPipe<uint16_t, kS, kCCb>;  // 8 KB chunks
-using PipePD = WarpPipe<uint16_t, kS, kCCb>;
+constexpr int kPW = 12;  // max warps per CTA: row tiles sharing one staging of the token inputs
+using PipePF = WarpPipe<uint16_t, 3, kCCf>;  // 4 KB chunks, 12 KB per warp
+using PipePD = PipePF;
+constexpr int kPipeStride = (PipePF::kBytes + 127) & ~127;  // per-warp pipe footprint, 128-aligned
 
 __device__ __forceinline__ void pf_prologue() {
     pdl_wait();
@@ -35,14 +36,14 @@ __device__ __forceinline__ void pf_prologue() {
 }
 
 // xs[t][*] = (v_t * scale_t) * gain (rms_norm, numerics.cpp:72-84) for the
-// tokens of this CTA; scale from the producer's f64 partials (same fixed
-// order as the per-token path).  Whole block (one warp).
-__device__ void pf_stage_norm(const DevModel& m, const float* V, const double* ssq, const float* gain,
+// tokens of this CTA; scale_t precomputed per token by k_pf_scales from the
+// producer's f64 partials (same fixed order as the per-token path).
+__device__ void pf_stage_norm(const DevModel& m, const float* V, const float* scales, const float* gain,
                               const int* tok_of, int nt, float* xs, int xstride) {
-    const int H = m.H, nb = m.Hp / 32;
+    const int H = m.H;
     for (int t = 0; t < nt; ++t) {
         const int tok = tok_of[t];
-        const float scale = rms_scale_from_partials(ssq + static_cast<long long>(tok) * nb, nb, H, m.eps);
+        const float scale = __ldcg(scales + tok);
         const float4* v4 = reinterpret_cast<const float4*>(V + static_cast<long long>(tok) * m.Hp);
         const float4* g4 = reinterpret_cast<const float4*>(gain);
         float4* o4 = reinterpret_cast<float4*>(xs + t * xstride);
@@ -56,6 +57,14 @@ __device__ void pf_stage_norm(const DevModel& m, const float* V, const double* s
 }
 
 }  // namespace
+
+// per-token rms scale from the f64 partials of V (one warp per token)
+__global__ void __launch_bounds__(32) k_pf_scales(DevModel m, PrefillDev pf, const double* ssq) {
+    pf_prologue();
+    const int t = blockIdx.x, nb = m.Hp / 32;
+    const float s = rms_scale_from_partials(ssq + static_cast<long long>(t) * nb, nb, m.H, m.eps);
+    if (threadIdx.x == 0) pf.scale[t] = s;
+}
 
 // ------------------------------------------------------------------ embed --
 __global__ void __launch_bounds__(32) k_pf_embed(DevModel m, PrefillDev pf) {
@@ -73,8 +82,8 @@ __global__ void __launch_bounds__(32) k_pf_embed(DevModel m, PrefillDev pf) {
 __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, PrefillDev pf, int layer) {
     const int H = m.H, Hr = round_up(H, 32), D = m.D, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
-    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < m.QKVp;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * H * 32;
     PipePF pipe;
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, Pr
     int tok_of[kPT];
 #pragma unroll
     for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
-    pf_stage_norm(m, pf.X, pf.ssqx, m.attn_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    pf_stage_norm(m, pf.X, pf.scale, m.attn_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
     run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
@@ -175,8 +184,8 @@ __global__ void __launch_bounds__(kPfAttnThreads) k_pf_attn(DevModel m, DevState
 __global__ void __launch_bounds__(32 * kPW) k_pf_wo(DevModel m, PrefillDev pf, int layer) {
     const int D = m.D, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][kMaxD]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * kMaxD)) + w * PipePD::kBytes;
-    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * kMaxD)) + w * kPipeStride;
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < m.Hp;
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * D * 32;
     PipePD pipe;
@@ -204,8 +213,8 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_wo(DevModel m, PrefillDev pf, i
 __global__ void __launch_bounds__(32 * kPW) k_pf_router(DevModel m, PrefillDev pf, int layer) {
     const int H = m.H, Hr = round_up(H, 32), E = m.E, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
-    const int rb = blockIdx.x * kPW + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < m.Ep;
     const uint16_t* tile = m.gate + layer * m.gate_stride + static_cast<long long>(rb) * H * 32;
     PipePF pipe;
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_router(DevModel m, PrefillDev p
     int tok_of[kPT];
 #pragma unroll
     for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
-    pf_stage_norm(m, pf.R, pf.ssqr, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    pf_stage_norm(m, pf.R, pf.scale, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
     run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
@@ -267,11 +276,11 @@ __global__ void __launch_bounds__(32) k_pf_scatter(DevModel m, PrefillDev pf) {
 __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, int layer, PfWave wv) {
     const int H = m.H, Hr = round_up(H, 32), K = m.K, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * PipePF::kBytes;
-    const int rb = blockIdx.x * kPW + w, u = blockIdx.y, e = wv.e[u];
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
     pf_prologue();
-    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = blockIdx.z * kPT;
-    if (c0 >= cnt) return;
+    const int u = __ldcg(pf.chunk_u + blockIdx.y), e = wv.e[u];
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w;
+    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + blockIdx.y) * kPT;
     const int nt = min(kPT, cnt - c0);
     const bool has_tile = rb * 16 < m.Hmp;
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
         ent[t] = t < nt ? __ldcg(pf.list + b0 + c0 + t) : 0;
         tok_of[t] = ent[t] / K;
     }
-    pf_stage_norm(m, pf.R, pf.ssqr, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
+    pf_stage_norm(m, pf.R, pf.scale, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
     run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
@@ -302,11 +311,11 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
 __global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf, int layer, PfWave wv) {
     const int Hmp = m.Hmp, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hmp]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hmp)) + w * PipePD::kBytes;
-    const int rb = blockIdx.x * kPW + w, u = blockIdx.y, e = wv.e[u];
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hmp)) + w * kPipeStride;
     pf_prologue();
-    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = blockIdx.z * kPT;
-    if (c0 >= cnt) return;
+    const int u = __ldcg(pf.chunk_u + blockIdx.y), e = wv.e[u];
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w;
+    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + blockIdx.y) * kPT;
     const int nt = min(kPT, cnt - c0);
     const bool has_tile = rb * 32 < m.Hp;
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
@@ -368,9 +377,32 @@ __global__ void __launch_bounds__(32) k_pf_handoff(DevModel m, DevState st, Pref
 // ---------------------------------------------------------------- launchers --
 namespace {
 size_t vecf(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
-size_t pf_h_smem(const DevModel& m) { return kPT * vecf(m.H) + 128 + kPW * PipePF::kBytes; }
-size_t pf_wo_smem(const DevModel& m) { return kPT * kMaxD * 4 + 128 + kPW * PipePD::kBytes; }
-size_t pf_down_smem(const DevModel& m) { return kPT * static_cast<size_t>(m.Hmp) * 4 + 128 + kPW * PipePD::kBytes; }
+// Warps per CTA for a kernel whose token staging takes `stage` bytes: as many
+// row tiles (each with its own 16 KB pipe) as fit next to it, up to kPW.
+constexpr size_t kPfSmemBudget = 220 * 1024;
+// Warps per CTA: maximise resident row-tile warps per SM (CTAs per SM x W,
+// each warp with its own pipe next to the CTA's token staging), discounted by
+// the idle warps of the last CTA over the kernel's `tiles` row tiles.
+int pf_warps(size_t stage, int tiles) {
+    int best = 1;
+    double best_score = -1.0;
+    for (int w = kPW; w >= 1; --w) {
+        const size_t smem = stage + 128 + static_cast<size_t>(w) * kPipeStride;
+        if (smem > kPfSmemBudget) continue;
+        const int per_sm = static_cast<int>((228 * 1024) / (smem + 1024));
+        const double used = static_cast<double>(tiles) / (((tiles + w - 1) / w) * w);
+        const double score = std::min(per_sm * w, 16) * used;
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = w;
+        }
+    }
+    return best;
+}
+size_t pf_smem(size_t stage, int w) { return stage + 128 + static_cast<size_t>(w) * kPipeStride; }
+size_t pf_h_stage(const DevModel& m) { return kPT * vecf(m.H); }
+size_t pf_wo_stage(const DevModel&) { return kPT * kMaxD * 4; }
+size_t pf_down_stage(const DevModel& m) { return kPT * static_cast<size_t>(m.Hmp) * 4; }
 int cdiv(int a, int b) { return (a + b - 1) / b; }
 size_t pf_attn_smem(const DevModel& m, int npos) {
     return (32 + kMaxD) * 4 + static_cast<size_t>(npos) * 12;
@@ -383,7 +415,8 @@ cudaError_t pf_preload() {
     const void* fns[] = {(const void*)k_pf_embed, (const void*)k_pf_qkv, (const void*)k_pf_attn,
                          (const void*)k_pf_wo, (const void*)k_pf_router, (const void*)k_pf_decide,
                          (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu,
-                         (const void*)k_pf_down, (const void*)k_pf_mix, (const void*)k_pf_handoff};
+                         (const void*)k_pf_down, (const void*)k_pf_mix, (const void*)k_pf_handoff,
+                         (const void*)k_pf_scales};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -399,11 +432,15 @@ cudaError_t pf_preload() {
 cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
                                   cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
-    PDL(k_pf_qkv, dim3(cdiv(m.QKVp / 32, kPW), tg), 32 * kPW, pf_h_smem(m), s, m, st, pf, layer);
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
+    const int wh = pf_warps(pf_h_stage(m), m.QKVp / 32), ww = pf_warps(pf_wo_stage(m), m.Hp / 32);
+    PDL(k_pf_qkv, dim3(cdiv(m.QKVp / 32, wh), tg), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, st, pf, layer);
     const int npos = pf.pos0 + pf.P <= pf.attn_smem_positions ? pf.pos0 + pf.P : 0;
     PDL(k_pf_attn, pf.P, kPfAttnThreads, pf_attn_smem(m, npos), s, m, st, pf, layer);
-    PDL(k_pf_wo, dim3(cdiv(m.Hp / 32, kPW), tg), 32 * kPW, pf_wo_smem(m), s, m, pf, layer);
-    PDL(k_pf_router, dim3(cdiv(m.Ep / 32, kPW), tg), 32 * kPW, pf_h_smem(m), s, m, pf, layer);
+    PDL(k_pf_wo, dim3(cdiv(m.Hp / 32, ww), tg), 32 * ww, pf_smem(pf_wo_stage(m), ww), s, m, pf, layer);
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
+    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
+    PDL(k_pf_router, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf, layer);
     PDL(k_pf_decide, pf.P, 32, 0, s, m, pf);
     PDL(k_pf_offsets, 1, 32, 0, s, m, pf);
     PDL(k_pf_scatter, pf.P, 32, 0, s, m, pf);
@@ -417,8 +454,11 @@ cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_
 
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
                               int chunks, cudaStream_t s) {
-    PDL(k_pf_gu, dim3(cdiv(m.Hmp / 16, kPW), wv.n, chunks), 32 * kPW, pf_h_smem(m), s, m, pf, layer, wv);
-    PDL(k_pf_down, dim3(cdiv(m.Hp / 32, kPW), wv.n, chunks), 32 * kPW, pf_down_smem(m), s, m, pf, layer, wv);
+    // `chunks` = number of (expert, 8-token chunk) work items in pf.chunk_u / chunk_c;
+    // the router's scales (of r_l) are still in pf.scale
+    const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16), wd = pf_warps(pf_down_stage(m), m.Hp / 32);
+    PDL(k_pf_gu, dim3(cdiv(m.Hmp / 16, wh), chunks), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, pf, layer, wv);
+    PDL(k_pf_down, dim3(cdiv(m.Hp / 32, wd), chunks), 32 * wd, pf_smem(pf_down_stage(m), wd), s, m, pf, layer, wv);
     return cudaGetLastError();
 }
 

@@ -591,9 +591,11 @@ __device__ inline void run_multi(Pipe& p, const uint16_t* tile, int cols, const 
             const float w0 = lo_bf(w.x), w1 = hi_bf(w.x), w2 = lo_bf(w.y), w3 = hi_bf(w.y);
             const float w4 = lo_bf(w.z), w5 = hi_bf(w.z), w6 = lo_bf(w.w), w7 = hi_bf(w.w);
             const uint32_t xo = xbase + (n * CC + q * G) * 4;
+            // all T chains run unconditionally (rows t >= nt compute on stale
+            // staging and are discarded) so the compiler interleaves them
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                if (t < nt) {
+                {
                     const float4 a = lds128f(xo + t * xstride * 4), b = lds128f(xo + t * xstride * 4 + 16);
                     const float2 p0 = __fmul2_rn(make_float2(w0, w1), make_float2(a.x, a.y));
                     const float2 p1 = __fmul2_rn(make_float2(w2, w3), make_float2(a.z, a.w));
