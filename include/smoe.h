@@ -50,6 +50,23 @@ typedef struct smoe_estimator_config {
     float eps;
 } smoe_estimator_config;
 
+/* TrainHyper (estimator.hpp:151-160) and CurvePoint (estimator.hpp:162-166). */
+typedef struct smoe_train_hyper {
+    double lr;
+    int32_t batch_tokens;
+    int64_t max_steps;
+    int64_t eval_every;
+    double val_fraction;
+    uint64_t seed;
+    int32_t k;
+    double early_stop_hit_rate;
+} smoe_train_hyper;
+typedef struct smoe_curve_point {
+    int64_t tokens_seen;
+    double val_kl;
+    double val_hit_rate;
+} smoe_curve_point;
+
 /* Predictor kinds (PredictorKind, speculation.hpp:64): -1 none,
  * 0 baseline-s, 1 router-pf, 2 est-pf, 3 hybrid, 4 oracle. */
 enum { SMOE_PRED_NONE = -1, SMOE_PRED_BASELINE_S = 0, SMOE_PRED_ROUTER_PF = 1,
@@ -89,6 +106,22 @@ int smoe_init_weights_seeded(smoe_session* s);
 int smoe_load_tensor(smoe_session* s, const char* name, const float* data, int64_t count);
 /* DefaultVectorTable [L][E][H] (speculation.hpp:18-33). */
 int smoe_load_default_vectors(smoe_session* s, const float* d, int64_t count);
+/* init_estimator_params<float> (estimator.cpp:54-75): the flat parameter
+ * block (param_count() floats, estimator.cpp:29-33) for config c and seed. */
+int smoe_estimator_param_count(const smoe_estimator_config* c, int64_t* n);
+int smoe_estimator_init(const smoe_estimator_config* c, uint64_t seed, float* flat, int64_t cap);
+/* train_estimator (estimator.cpp:374-450) on the GPU: KL distillation with
+ * hand-derived gradients and Adam, bit-exact with the reference.  The
+ * DistillDataset (estimator.hpp:117-131) is given flat: inputs
+ * [tokens][layers_predicting][d], targets [tokens][layers_predicting][E].
+ * Writes the trained flat params and the validation curve (n_curve points;
+ * at most curve_cap stored).  train_ms (nullable): device time of the
+ * training steps, evaluation excluded.  Needs no session. */
+int smoe_train_estimator(const smoe_estimator_config* c, uint64_t seed, const float* inputs,
+                         const float* targets, int64_t tokens, int32_t layers_predicting,
+                         const smoe_train_hyper* h, float* params_out, int64_t params_cap,
+                         smoe_curve_point* curve_out, int32_t curve_cap, int32_t* n_curve,
+                         double* train_ms);
 /* EstimatorParams flat layout (estimator.hpp:41-72). */
 int smoe_load_estimator(smoe_session* s, const smoe_estimator_config* c, const float* flat,
                         int64_t count);

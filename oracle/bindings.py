@@ -226,6 +226,27 @@ class Ref(_Common):
         self._check(self.lib.ref_estimator_logits(est.h, _ptr(q), layer, _ptr(out)))
         return out
 
+    def train_estimator(self, inputs, targets, d, m, n, E, L, eps=1e-5, seed=0, lr=1e-3, batch=32,
+                        max_steps=0, eval_every=50, val_fraction=0.1, hseed=0, k=1, early_stop=0.0):
+        """train_estimator (estimator.cpp:374-450) -> (flat params, curve [n][3])."""
+        inputs = np.ascontiguousarray(inputs, np.float32)
+        targets = np.ascontiguousarray(targets, np.float32)
+        tokens = inputs.size // ((L - 1) * d)
+        est = self.estimator_init(d, m, n, E, L, eps, seed)
+        params = np.zeros(est.count, np.float32)
+        cap = int(max_steps // max(eval_every, 1)) + 3
+        curve = np.zeros((cap, 3), np.float64)
+        nc = C.c_int()
+        L_ = self.lib
+        L_.ref_train_estimator.argtypes = [C.c_int] * 5 + [C.c_float, C.c_uint64, C.c_void_p, C.c_void_p,
+                                           C.c_int64, C.c_double, C.c_int, C.c_int64, C.c_int64,
+                                           C.c_double, C.c_uint64, C.c_int, C.c_double, C.c_void_p,
+                                           C.c_void_p, C.c_int, C.c_void_p]
+        self._check(L_.ref_train_estimator(d, m, n, E, L, eps, seed, _ptr(inputs), _ptr(targets), tokens, lr,
+                                           batch, max_steps, eval_every, val_fraction, hseed, k, early_stop,
+                                           _ptr(params), _ptr(curve), cap, C.byref(nc)))
+        return params, curve[:nc.value].copy()
+
     def make_predictor(self, kind: str, L: int, table=None, est=None, hybrid=None):
         h = C.c_void_p()
         hm = None if hybrid is None else np.ascontiguousarray(

@@ -341,6 +341,49 @@ int ref_estimator_logits(void* h, const float* q, int layer, float* out) {
     });
 }
 
+// train_estimator (estimator.cpp:374-450) on a DistillDataset given as flat
+// arrays.  curve: n_curve x {tokens_seen, val_kl, val_hit_rate} as doubles.
+int ref_train_estimator(int d, int mred, int nexp, int E, int L, float eps, std::uint64_t seed,
+                        const float* inputs, const float* targets, std::int64_t tokens, double lr,
+                        int batch, std::int64_t max_steps, std::int64_t eval_every,
+                        double val_fraction, std::uint64_t hseed, int k, double early_stop,
+                        float* params_out, double* curve_out, int curve_cap, int* n_curve) {
+    return guard([&] {
+        EstimatorConfig c;
+        c.d = d;
+        c.m = mred;
+        c.n = nexp;
+        c.experts = E;
+        c.layers = L;
+        c.eps = eps;
+        c.seed = seed;
+        DistillDataset data;
+        data.d = d;
+        data.experts = E;
+        data.layers_predicting = L - 1;
+        data.tokens = tokens;
+        data.inputs.assign(inputs, inputs + tokens * (L - 1) * d);
+        data.targets.assign(targets, targets + tokens * (L - 1) * E);
+        TrainHyper h;
+        h.lr = lr;
+        h.batch_tokens = batch;
+        h.max_steps = max_steps;
+        h.eval_every = eval_every;
+        h.val_fraction = val_fraction;
+        h.seed = hseed;
+        h.k = k;
+        h.early_stop_hit_rate = early_stop;
+        TrainResult r = train_estimator(data, c, h);
+        std::memcpy(params_out, r.params.flat.data(), r.params.flat.size() * 4);
+        *n_curve = static_cast<int>(r.curve.size());
+        for (int i = 0; i < *n_curve && i < curve_cap; ++i) {
+            curve_out[3 * i] = static_cast<double>(r.curve[i].tokens_seen);
+            curve_out[3 * i + 1] = r.curve[i].val_kl;
+            curve_out[3 * i + 2] = r.curve[i].val_hit_rate;
+        }
+    });
+}
+
 // --- predictors (speculation.cpp:167-346) ------------------------------------
 
 void ref_free_predictor(void* p) { delete static_cast<RecordingPredictor*>(p); }

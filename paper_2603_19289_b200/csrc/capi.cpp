@@ -5,6 +5,7 @@
 #include "../../include/smoe.h"
 
 #include "engine.h"
+#include "train.h"
 
 #include <cstring>
 #include <string>
@@ -326,3 +327,42 @@ int smoe_kernels_per_step(smoe_session* s, int32_t mode, int32_t* n) {
 }
 
 }  // extern "C"
+
+namespace {
+smoe::EstTrainCfg est_cfg(const smoe_estimator_config* c, uint64_t seed) {
+    if (!c) throw std::invalid_argument("null estimator config");
+    return smoe::EstTrainCfg{c->d, c->m, c->n, c->experts, c->layers, c->eps, seed};
+}
+}  // namespace
+
+int smoe_estimator_param_count(const smoe_estimator_config* c, int64_t* n) {
+    return guard([&] { *n = static_cast<int64_t>(smoe::estimator_init_params(est_cfg(c, 0)).size()); });
+}
+
+int smoe_estimator_init(const smoe_estimator_config* c, uint64_t seed, float* flat, int64_t cap) {
+    return guard([&] {
+        const std::vector<float> p = smoe::estimator_init_params(est_cfg(c, seed));
+        if (cap < static_cast<int64_t>(p.size())) throw std::invalid_argument("estimator init: buffer too small");
+        std::memcpy(flat, p.data(), p.size() * 4);
+    });
+}
+
+int smoe_train_estimator(const smoe_estimator_config* c, uint64_t seed, const float* inputs,
+                         const float* targets, int64_t tokens, int32_t layers_predicting,
+                         const smoe_train_hyper* h, float* params_out, int64_t params_cap,
+                         smoe_curve_point* curve_out, int32_t curve_cap, int32_t* n_curve,
+                         double* train_ms) {
+    return guard([&] {
+        if (!h || !inputs || !targets || !params_out) throw std::invalid_argument("train: null argument");
+        const smoe::EstTrainCfg cfg = est_cfg(c, seed);
+        const int64_t need = static_cast<int64_t>(smoe::estimator_init_params(cfg).size());
+        if (params_cap < need) throw std::invalid_argument("train: params buffer too small");
+        const smoe::EstTrainHyper hy{h->lr, h->batch_tokens, h->max_steps, h->eval_every,
+                                     h->val_fraction, h->seed, h->k, h->early_stop_hit_rate};
+        const std::vector<smoe::EstCurvePoint> curve = smoe::train_estimator_gpu(
+            cfg, inputs, targets, tokens, layers_predicting, hy, params_out, train_ms);
+        if (n_curve) *n_curve = static_cast<int32_t>(curve.size());
+        for (size_t i = 0; i < curve.size() && static_cast<int64_t>(i) < curve_cap && curve_out; ++i)
+            curve_out[i] = smoe_curve_point{curve[i].tokens_seen, curve[i].val_kl, curve[i].val_hit_rate};
+    });
+}

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
     PipePF pipe;
-    pipe.init(pipe_mem, kL2EvictFirst);
+    pipe.init(pipe_mem, kL2Normal);  // expert tiles are re-read by the other token chunks
     if (has_tile) pipe.prime(tile, H);
     int ent[kPT], tok_of[kPT];
 #pragma unroll
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf,
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems +
                            m.gu_elems + static_cast<long long>(rb) * Hmp * 32;
     PipePD pipe;
-    pipe.init(pipe_mem, kL2EvictFirst);
+    pipe.init(pipe_mem, kL2Normal);  // expert tiles are re-read by the other token chunks
     if (has_tile) pipe.prime(tile, m.Hm);
     int ent[kPT];
 #pragma unroll

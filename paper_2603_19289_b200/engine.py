@@ -32,7 +32,8 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle", "smoe_prefill_batched",
+    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count",
+    "smoe_estimator_init", "smoe_train_estimator",
 ]
 
 
@@ -52,6 +53,16 @@ class _Options(C.Structure):
 class _EstConfig(C.Structure):
     _fields_ = [("d", C.c_int32), ("m", C.c_int32), ("n", C.c_int32), ("experts", C.c_int32),
                 ("layers", C.c_int32), ("eps", C.c_float)]
+
+
+class _TrainHyper(C.Structure):
+    _fields_ = [("lr", C.c_double), ("batch_tokens", C.c_int32), ("max_steps", C.c_int64),
+                ("eval_every", C.c_int64), ("val_fraction", C.c_double), ("seed", C.c_uint64),
+                ("k", C.c_int32), ("early_stop_hit_rate", C.c_double)]
+
+
+class _CurvePoint(C.Structure):
+    _fields_ = [("tokens_seen", C.c_int64), ("val_kl", C.c_double), ("val_hit_rate", C.c_double)]
 
 
 class Event(C.Structure):
@@ -144,6 +155,41 @@ def recall_at_k(pred, truth):
     m = np.zeros(len(p), np.int32)
     _check(lib.smoe_recall_at_k(_p(p), _p(t), len(p), C.byref(r), _p(m)))
     return r.value, m.astype(bool)
+
+
+def estimator_init(d, m, n, E, L, eps=1e-5, seed=0) -> np.ndarray:
+    """init_estimator_params<float> (estimator.cpp:54-75): the flat parameter block."""
+    lib = load_library()
+    c = _EstConfig(d, m, n, E, L, eps)
+    cnt = C.c_int64()
+    _check(lib.smoe_estimator_param_count(C.byref(c), C.byref(cnt)))
+    out = np.zeros(cnt.value, np.float32)
+    _check(lib.smoe_estimator_init(C.byref(c), C.c_uint64(seed), _p(out), cnt))
+    return out
+
+
+def train_estimator(inputs, targets, d, m, n, E, L, eps=1e-5, seed=0, lr=1e-3, batch=32, max_steps=0,
+                    eval_every=50, val_fraction=0.1, hseed=0, k=1, early_stop=0.0):
+    """train_estimator (estimator.cpp:374-450) on the GPU.  inputs [tokens][L-1][d],
+    targets [tokens][L-1][E].  Returns (flat params, curve [n][3] = tokens_seen, val_kl,
+    val_hit_rate, device ms of the training steps)."""
+    lib = load_library()
+    inputs = np.ascontiguousarray(inputs, np.float32)
+    targets = np.ascontiguousarray(targets, np.float32)
+    tokens = inputs.size // ((L - 1) * d)
+    c = _EstConfig(d, m, n, E, L, eps)
+    cnt = C.c_int64()
+    _check(lib.smoe_estimator_param_count(C.byref(c), C.byref(cnt)))
+    params = np.zeros(cnt.value, np.float32)
+    cap = int(max_steps // max(eval_every, 1)) + 3
+    curve = (_CurvePoint * cap)()
+    nc = C.c_int32()
+    ms = C.c_double()
+    h = _TrainHyper(lr, batch, max_steps, eval_every, val_fraction, hseed, k, early_stop)
+    _check(lib.smoe_train_estimator(C.byref(c), C.c_uint64(seed), _p(inputs), _p(targets), C.c_int64(tokens),
+                                    L - 1, C.byref(h), _p(params), cnt, curve, cap, C.byref(nc), C.byref(ms)))
+    cv = np.array([(p.tokens_seen, p.val_kl, p.val_hit_rate) for p in curve[:nc.value]], np.float64)
+    return params, cv.reshape(-1, 3), ms.value
 
 
 def _check(rc):
