@@ -178,6 +178,14 @@ int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n_ele
  * expert_gates (executed decision, ids as f32) and expert_outputs (raw) .moet
  * files in `dir`, readable by the reference's TraceReader.  Needs
  * smoe_reset(..., trace_full = 1). */
+/* build_distill_dataset (speculation.cpp:437-484) from captured trace steps
+ * [first, first+n) (needs smoe_reset with trace_full=1), on the GPU:
+ * mode 0 (DistillInput::kQuasiHidden, needs default vectors): inputs are
+ * q_l = rms_norm(r_l + layer_default(executed_l), gain_{l+1}); mode 1
+ * (kSNext): s_{l+1}.  targets: the true router logits of layer l+1.
+ * inputs [n][L-1][H], targets [n][L-1][E] (host). */
+int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_t mode, float* inputs,
+                               float* targets);
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
                             int32_t seq_len, const char* source, uint64_t seed);
 int smoe_token_ms(smoe_session* s, double* out, int32_t cap, int32_t* n);

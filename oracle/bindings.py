@@ -307,6 +307,16 @@ class RefModel:
         c = self.cfg
         return RefHandle(self.ref, h, "ref_free_table", shape=(c.layers, c.experts, c.hidden))
 
+    def distill_dataset(self, prompt, table=None, mode="quasi"):
+        """DistillDatasetBuilder (speculation.cpp:437-471) over forward_decode(prompt)."""
+        c = self.cfg
+        t = np.ascontiguousarray(prompt, np.int32)
+        inp = np.zeros((len(t), c.layers - 1, c.hidden), np.float32)
+        tgt = np.zeros((len(t), c.layers - 1, c.experts), np.float32)
+        self.ref._check(self.ref.lib.ref_distill_dataset(self.h, _ptr(t), len(t), table.h if table else None,
+                                                         0 if mode == "quasi" else 1, _ptr(inp), _ptr(tgt)))
+        return inp, tgt
+
     def write_trace(self, tokens, seq_len: int, path: str, source: str = "", seed: int = 0):
         """The reference's TraceWriter over stream_decode_trace (true path)."""
         t = np.ascontiguousarray(tokens, np.int32)

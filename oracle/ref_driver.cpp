@@ -384,6 +384,32 @@ int ref_train_estimator(int d, int mred, int nexp, int E, int L, float eps, std:
     });
 }
 
+// DistillDatasetBuilder (speculation.cpp:437-471) fed with the records of
+// forward_decode over `prompt` (one sequence from a fresh DecodeState).
+// mode 0 quasi-hidden (table required), 1 s_{l+1}.
+int ref_distill_dataset(void* h, const int* prompt, int P, void* table, int mode, float* inputs,
+                        float* targets) {
+    return guard([&] {
+        const Model& model = *static_cast<Model*>(h);
+        const int L = model.config.layers;
+        const DefaultVectorTable* tb =
+            table ? static_cast<std::shared_ptr<const DefaultVectorTable>*>(table)->get() : nullptr;
+        DistillDatasetBuilder b(model, tb, mode == 0 ? DistillInput::kQuasiHidden : DistillInput::kSNext, P);
+        DecodeState state(L);
+        for (int i = 0; i < P; ++i) {
+            TraceToken tok;
+            tok.token_id = prompt[i];
+            tok.layers.resize(static_cast<std::size_t>(L));
+            TraceSink sink = [&](int l, const LayerTraceRecord& rec) { tok.layers[static_cast<std::size_t>(l)] = rec; };
+            forward_decode(model, state, prompt[i], &sink);
+            b.add_token(tok);
+        }
+        DistillDataset d = b.take();
+        std::memcpy(inputs, d.inputs.data(), d.inputs.size() * 4);
+        std::memcpy(targets, d.targets.data(), d.targets.size() * 4);
+    });
+}
+
 // --- predictors (speculation.cpp:167-346) ------------------------------------
 
 void ref_free_predictor(void* p) { delete static_cast<RecordingPredictor*>(p); }

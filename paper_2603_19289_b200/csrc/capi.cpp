@@ -195,6 +195,11 @@ int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n) {
     return guard([&] { S(s)->read_trace(field, out, n); });
 }
 
+int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_t mode, float* inputs,
+                               float* targets) {
+    return guard([&] { S(s)->build_distill_dataset(first, n, mode, inputs, targets); });
+}
+
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
                             int32_t seq_len, const char* source, uint64_t seed) {
     return guard([&] { S(s)->write_trace_bundle(dir, first, n, seq_len, source ? source : "", seed); });

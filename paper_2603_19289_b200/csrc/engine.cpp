@@ -1794,6 +1794,26 @@ void Session::read_trace(const char* field, void* out, long long n) {
     d2h(out, src, n * esz, "trace");
 }
 
+void Session::build_distill_dataset(int first, int n, int mode, float* inputs, float* targets) {
+    sync();
+    if (!trace_full_ || !tr_.s) throw std::invalid_argument("distill dataset: needs reset(trace_full=1)");
+    if (cfg_.L < 2) throw std::invalid_argument("distill dataset: need at least 2 layers");
+    if (mode != 0 && mode != 1) throw std::invalid_argument("distill dataset: mode must be 0 (quasi) or 1 (s-next)");
+    if (mode == 0 && !have_dv_) throw std::invalid_argument("distill dataset: quasi-hidden inputs need a table");
+    if (n < 1 || first < 0 || first + n > tr_.cap) throw std::invalid_argument("distill dataset: steps out of range");
+    const size_t ns = static_cast<size_t>(n) * (cfg_.L - 1);
+    float *di = nullptr, *dt = nullptr;
+    ck(cudaMalloc(&di, ns * cfg_.H * 4), "distill alloc");
+    ck(cudaMalloc(&dt, ns * cfg_.E * 4), "distill alloc");
+    cudaError_t err = launch_distill(dm_, tr_, first, n, mode, di, dt, s_comp_);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(inputs, di, ns * cfg_.H * 4, cudaMemcpyDeviceToHost, s_comp_);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(targets, dt, ns * cfg_.E * 4, cudaMemcpyDeviceToHost, s_comp_);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s_comp_);
+    cudaFree(di);
+    cudaFree(dt);
+    ck(err, "distill dataset");
+}
+
 // ---- trace bundles in the reference's format (trace.cpp:60-122, moet.cpp) ----
 namespace {
 void moet_write(const std::string& path, const std::vector<unsigned long long>& dims,

@@ -164,6 +164,9 @@ public:
     int steps_done();
     void read_tokens(int* out, int n);
     void read_trace(const char* field, void* out, long long n_elems);
+    // build_distill_dataset (speculation.cpp:476-484) from captured steps:
+    // mode 0 quasi-hidden inputs (needs default vectors), 1 s_{l+1}.
+    void build_distill_dataset(int first, int n, int mode, float* inputs, float* targets);
     void write_trace_bundle(const std::string& dir, int first, int n, int seq_len,
                             const std::string& source, unsigned long long seed);
     std::vector<double> token_ms();  // device-timed duration of each decode() step

@@ -1207,6 +1207,58 @@ __global__ void k_dv_freeze(const double* sums, const long long* counts, float* 
     }
 }
 
+// ---------------------------------------------------------- distill data --
+// DistillDatasetBuilder::add_token (speculation.cpp:455-471) over captured
+// trace steps: one CTA per (token, predicting layer l).  Input: quasi-hidden
+// q_l = rms_norm(r_l + layer_default(exec_l), gain_{l+1}) (mode 0), or s_{l+1}
+// (mode 1); target: the true router logits of layer l+1.  The rms scale uses
+// the decode path's partial order (warp_ssq_partial / rms_scale_from_partials).
+__global__ void __launch_bounds__(256) k_distill(DevModel m, TraceDev tr, int first, int mode, float* inputs,
+                                                 float* targets) {
+    double* part = reinterpret_cast<double*>(g_smem);  // [ceil(H/32)]
+    __shared__ float scale_s;
+    const int L = m.L, H = m.H, E = m.E, K = m.K, lp = L - 1;
+    const long long smp = blockIdx.x;
+    const long long t = first + smp / lp;
+    const int l = static_cast<int>(smp % lp);
+    float* out = inputs + smp * H;
+    if (mode == 1) {
+        const float* s = tr.s + (t * L + l + 1) * H;
+        for (int j = threadIdx.x; j < H; j += blockDim.x) out[j] = s[j];
+    } else {
+        const float* r = tr.r + (t * L + l) * H;
+        const int* ids = tr.id_exec + (t * L + l) * K;
+        const float* gts = tr.g_exec + (t * L + l) * K;
+        const int nb = (H + 31) / 32;
+        for (int rb = threadIdx.x >> 5; rb < nb; rb += blockDim.x >> 5) {
+            const int j = rb * 32 + (threadIdx.x & 31);
+            const float rd = j < H ? r[j] + layer_default_row(m, ids, gts, l, j) : 0.0f;
+            if (j < H) out[j] = rd;
+            warp_ssq_partial(rd, part + rb);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // rms_scale_from_partials' order over smem
+            double v = 0.0;
+            for (int i = threadIdx.x; i < nb; i += 32) v += part[i];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (threadIdx.x == 0)
+                scale_s = static_cast<float>(1.0 / sqrt(v / static_cast<double>(H) + static_cast<double>(m.eps)));
+        }
+        __syncthreads();
+        const float sc = scale_s;
+        const float* gain = m.moe_gain + static_cast<long long>(l + 1) * H;
+        for (int j = threadIdx.x; j < H; j += blockDim.x) out[j] = (out[j] * sc) * gain[j];
+    }
+    const float* lg = tr.lg_true + (t * L + l + 1) * E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) targets[smp * E + e] = lg[e];
+}
+
+cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,
+                           float* targets, cudaStream_t s) {
+    k_distill<<<n * (m.L - 1), 256, (m.H + 31) / 32 * 8, s>>>(m, tr, first, mode, inputs, targets);
+    return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------- trace ----
 
 __global__ void k_trace(DevModel m, DevState st, TraceDev tr) {

@@ -80,6 +80,10 @@ struct TraceDev {
 cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
                          cudaStream_t s);
 
+// DistillDatasetBuilder (speculation.cpp:437-471) over trace steps [first, first+n).
+cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,
+                           float* targets, cudaStream_t s);
+
 cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
                            cudaStream_t s);
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count",
+    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator",
 ]
 
@@ -324,6 +324,15 @@ class Session:
         out = np.zeros((steps,) + shapes[field], dt)
         _check(self.lib.smoe_read_trace(self._h, field.encode(), _p(out), C.c_int64(out.size)))
         return out
+
+    def build_distill_dataset(self, first: int, n: int, mode: str = "quasi"):
+        """build_distill_dataset (speculation.cpp:476-484) on captured steps -> (inputs, targets)."""
+        L, H, E = self.cfg.layers, self.cfg.hidden, self.cfg.experts
+        inp = np.zeros((n, L - 1, H), np.float32)
+        tgt = np.zeros((n, L - 1, E), np.float32)
+        _check(self.lib.smoe_build_distill_dataset(self._h, first, n, {"quasi": 0, "s-next": 1}[mode],
+                                                   _p(inp), _p(tgt)))
+        return inp, tgt
 
     def write_trace_bundle(self, path: str, first: int, n: int, seq_len: int = 0,
                            source: str = "", seed: int = 0):

@@ -64,3 +64,36 @@ def test_train_estimator_on_model_trace():
     gp, gc, _ = engine.train_estimator(inp, tgt, 64, 2, 4, 16, 8, **kw)
     np.testing.assert_array_equal(gc, rc)
     assert np.array_equal(gp.view(np.uint32), rp.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["quasi", "s-next"])
+def test_distill_dataset_and_training_match_reference(mode):
+    """build_distill_dataset (speculation.cpp:476-484) on the GPU from a captured
+    decode, against the reference's builder over the reference's own trace of
+    the same model and prompt; then both train on it (bit-exact end to end)."""
+    from paper_2603_19289_b200 import ModelConfig, Session
+    from oracle.bindings import Config
+    cfg = dict(layers=8, experts=16, top_k=4, hidden=64, expert_hidden=128, vocab=256, head_dim=32, seed=5)
+    ref = Ref()
+    rm = ref.build_model(Config(**cfg))
+    prompt = [int(x) for x in np.random.default_rng(1).integers(0, 256, 40)]
+    table = None
+    s = Session(ModelConfig(**cfg), max_positions=128)
+    s.init_weights_seeded()
+    if mode == "quasi":
+        table = rm.calibrate(64, 7, 32)
+        d, _ = ref.table_get(table)
+        s.load_default_vectors(d)
+    T = len(prompt)
+    s.reset(T, True)
+    s.prefill(prompt)
+    gi, gt = s.build_distill_dataset(0, T, mode)
+    ri, rt = rm.distill_dataset(prompt, table, mode)
+    assert np.array_equal(gt, rt)
+    assert np.array_equal(gi.view(np.uint32), ri.view(np.uint32))
+    kw = dict(seed=2, lr=1e-2, batch=8, max_steps=8, eval_every=4, hseed=1, k=4)
+    rp, rc = ref.train_estimator(ri, rt, 64, 2, 4, 16, 8, **kw)
+    gp, gc, _ = engine.train_estimator(gi, gt, 64, 2, 4, 16, 8, **kw)
+    np.testing.assert_array_equal(gc, rc)
+    assert np.array_equal(gp.view(np.uint32), rp.view(np.uint32))
