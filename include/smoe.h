@@ -186,6 +186,12 @@ int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n_ele
  * inputs [n][L-1][H], targets [n][L-1][E] (host). */
 int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_t mode, float* inputs,
                                float* targets);
+/* Router-pf predictions `depth` layers ahead (multi-layer-
+ * ahead prefetch study) from captured steps (trace_full=1, default vectors
+ * loaded): ids[t][l][:] = top-k of gate_l . rms_norm(r_{l-depth} +
+ * layer_default(executed_{l-depth}), gain_l); -1 for l < depth.  depth 1 is
+ * the paper's router-pf predictor (speculation.cpp:206-228). */
+int smoe_predict_ahead(smoe_session* s, int32_t first, int32_t n, int32_t depth, int32_t* ids);
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
                             int32_t seq_len, const char* source, uint64_t seed);
 int smoe_token_ms(smoe_session* s, double* out, int32_t cap, int32_t* n);
@@ -238,6 +244,20 @@ int smoe_timeline(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t 
 int smoe_simulate(int32_t layers, const double* t_attn, const double* t_gate,
                   const double* t_expert, const double* t_copy, double cold_start_copy,
                   int32_t mode, double* tpot, double* fractions3, double* analytic);
+/* Trace-driven two-lane schedule with a per-layer slot cache (SURVEY §8f
+ * row 4; extends simulate_prefetch / simulate_on_demand, schedule.cpp:92-148).
+ * exec_ids [tokens][layers][k]: executed experts; pred_ids [tokens][layers][k]:
+ * the prediction for layer l made at layer l-1 (lookahead >= 1); pred2_ids:
+ * the prediction for layer l made at layer l-2 (lookahead 2).  policy 0 LRU,
+ * 1 LFU; one copy of t_copy_expert per expert, single FIFO copy lane.
+ * out4 = {mean TPOT, on-demand (stall) copies, speculative copies, useful
+ * speculative copies} per measured token (tokens after warm_tokens). */
+typedef struct smoe_cache_sim {
+    int32_t tokens, layers, k, capacity, policy, lookahead, warm_tokens;
+} smoe_cache_sim;
+int smoe_simulate_cache(const smoe_cache_sim* c, const int32_t* exec_ids, const int32_t* pred_ids,
+                        const int32_t* pred2_ids, const double* t_attn, const double* t_gate,
+                        const double* t_expert, double t_copy_expert, double* out4);
 /* per_token_reports (executor.cpp:361-382) then breakdown, averaged over tokens:
  * fractions {compute, copy on the critical path, idle}. */
 int smoe_breakdown(const smoe_event* events, int32_t n, double* mean_fractions3,

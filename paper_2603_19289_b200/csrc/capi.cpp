@@ -200,6 +200,10 @@ int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_
     return guard([&] { S(s)->build_distill_dataset(first, n, mode, inputs, targets); });
 }
 
+int smoe_predict_ahead(smoe_session* s, int32_t first, int32_t n, int32_t depth, int32_t* ids) {
+    return guard([&] { S(s)->predict_ahead(first, n, depth, ids); });
+}
+
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
                             int32_t seq_len, const char* source, uint64_t seed) {
     return guard([&] { S(s)->write_trace_bundle(dir, first, n, seq_len, source ? source : "", seed); });

@@ -1814,6 +1814,23 @@ void Session::build_distill_dataset(int first, int n, int mode, float* inputs, f
     ck(err, "distill dataset");
 }
 
+void Session::predict_ahead(int first, int n, int depth, int* ids) {
+    sync();
+    if (!trace_full_ || !tr_.s) throw std::invalid_argument("predict_ahead: needs reset(trace_full=1)");
+    if (!have_dv_) throw std::invalid_argument("predict_ahead: quasi-hidden inputs need a table");
+    if (depth < 1 || depth >= cfg_.L) throw std::invalid_argument("predict_ahead: depth must be in [1, L)");
+    if (n < 1 || first < 0 || first + n > tr_.cap) throw std::invalid_argument("predict_ahead: steps out of range");
+    const size_t cnt = static_cast<size_t>(n) * cfg_.L * cfg_.K;
+    int* d = nullptr;
+    ck(cudaMalloc(&d, cnt * 4), "predict_ahead alloc");
+    cudaError_t err = cudaMemsetAsync(d, 0xff, cnt * 4, s_comp_);
+    if (err == cudaSuccess) err = launch_pred_ahead(dm_, tr_, first, n, depth, d, s_comp_);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(ids, d, cnt * 4, cudaMemcpyDeviceToHost, s_comp_);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s_comp_);
+    cudaFree(d);
+    ck(err, "predict_ahead");
+}
+
 // ---- trace bundles in the reference's format (trace.cpp:60-122, moet.cpp) ----
 namespace {
 void moet_write(const std::string& path, const std::vector<unsigned long long>& dims,

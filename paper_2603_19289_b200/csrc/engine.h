@@ -167,6 +167,8 @@ public:
     // build_distill_dataset (speculation.cpp:476-484) from captured steps:
     // mode 0 quasi-hidden inputs (needs default vectors), 1 s_{l+1}.
     void build_distill_dataset(int first, int n, int mode, float* inputs, float* targets);
+    // router-pf predictions `depth` layers ahead from captured steps (ids [n][L][K], -1 where l < depth)
+    void predict_ahead(int first, int n, int depth, int* ids);
     void write_trace_bundle(const std::string& dir, int first, int n, int seq_len,
                             const std::string& source, unsigned long long seed);
     std::vector<double> token_ms();  // device-timed duration of each decode() step

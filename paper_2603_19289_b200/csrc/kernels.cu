@@ -1253,6 +1253,75 @@ __global__ void __launch_bounds__(256) k_distill(DevModel m, TraceDev tr, int fi
     for (int e = threadIdx.x; e < E; e += blockDim.x) targets[smp * E + e] = lg[e];
 }
 
+// Router-pf prediction `depth` layers ahead over captured steps (SURVEY §8f
+// row 4): q = rms_norm(r_l + layer_default(exec_l), gain_{l+depth}), logits =
+// gate_{l+depth} . q (sequential chains), top-k ids (value desc, index asc).
+// depth 1 is the paper's router-pf (speculation.cpp:206-228).  One CTA per
+// (token, l); writes ids of layer l+depth.
+__global__ void __launch_bounds__(256) k_pred_ahead(DevModel m, TraceDev tr, int first, int depth, int* out) {
+    const int L = m.L, H = m.H, E = m.E, K = m.K, nl = L - depth;
+    const long long smp = blockIdx.x;
+    const long long t = first + smp / nl;
+    const int l = static_cast<int>(smp % nl), tl = l + depth;
+    const int nb = (H + 31) / 32;
+    double* part = reinterpret_cast<double*>(g_smem);
+    float* q = reinterpret_cast<float*>(g_smem + round_up(nb, 2) * 8);
+    float* lg = q + round_up(H, 4);
+    __shared__ float scale_s;
+    const float* r = tr.r + (t * L + l) * H;
+    const int* ids = tr.id_exec + (t * L + l) * K;
+    const float* gts = tr.g_exec + (t * L + l) * K;
+    for (int rb = threadIdx.x >> 5; rb < nb; rb += blockDim.x >> 5) {
+        const int j = rb * 32 + (threadIdx.x & 31);
+        const float rd = j < H ? r[j] + layer_default_row(m, ids, gts, l, j) : 0.0f;
+        if (j < H) q[j] = rd;
+        warp_ssq_partial(rd, part + rb);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = 0.0;
+        for (int i = threadIdx.x; i < nb; i += 32) v += part[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0)
+            scale_s = static_cast<float>(1.0 / sqrt(v / static_cast<double>(H) + static_cast<double>(m.eps)));
+    }
+    __syncthreads();
+    const float* gain = m.moe_gain + static_cast<long long>(tl) * H;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) q[j] = (q[j] * scale_s) * gain[j];
+    __syncthreads();
+    const uint16_t* g = m.gate + tl * m.gate_stride;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        // row tile layout (k_gen_bf16): [E/32][H/8][32 rows][8 cols]
+        const uint16_t* row = g + static_cast<long long>(e / 32) * H * 32 + (e % 32) * 8;
+        float acc = 0.0f;
+        for (int j = 0; j < H; ++j)
+            acc = acc + __uint_as_float(static_cast<uint32_t>(row[(j >> 3) * 256 + (j & 7)]) << 16) * q[j];
+        lg[e] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* o = out + (t - first) * static_cast<long long>(L) * K + static_cast<long long>(tl) * K;
+        for (int i = 0; i < K; ++i) {
+            int best = -1;
+            for (int e = 0; e < E; ++e) {
+                bool taken = false;
+                for (int p = 0; p < i; ++p) taken |= o[p] == e;
+                if (taken) continue;
+                if (best < 0 || lg[e] > lg[best]) best = e;
+            }
+            o[i] = best;
+        }
+    }
+}
+
+cudaError_t launch_pred_ahead(const DevModel& m, const TraceDev& tr, int first, int n, int depth, int* out,
+                              cudaStream_t s) {
+    const int nb = (m.H + 31) / 32;
+    const size_t smem = round_up(nb, 2) * 8 + (round_up(m.H, 4) + m.E) * 4;
+    k_pred_ahead<<<n * (m.L - depth), 256, smem, s>>>(m, tr, first, depth, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,
                            float* targets, cudaStream_t s) {
     k_distill<<<n * (m.L - 1), 256, (m.H + 31) / 32 * 8, s>>>(m, tr, first, mode, inputs, targets);

@@ -84,6 +84,10 @@ cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& 
 cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,
                            float* targets, cudaStream_t s);
 
+// Router-pf ids `depth` layers ahead over trace steps; out [n][L][K] (rows < depth untouched).
+cudaError_t launch_pred_ahead(const DevModel& m, const TraceDev& tr, int first, int n, int depth, int* out,
+                              cudaStream_t s);
+
 cudaError_t launch_trace_y(const DevModel& m, const DevState& st, const TraceDev& tr, int layer,
                            cudaStream_t s);
 

@@ -161,6 +161,135 @@ void breakdown(const Report& r, double* f) {
     f[2] = 1.0 - f[0] - f[1];
 }
 
+// ---- trace-driven two-lane schedule with a per-layer slot cache ----------
+// (SURVEY §8f row 4.)  simulate_prefetch / simulate_on_demand
+// (schedule.cpp:92-148) assume every layer copies its experts; here each
+// layer holds `capacity` expert slots (LRU or LFU), a copy moves one expert,
+// and requests come from a decode trace: the executed experts of layer l are
+// copied on demand after layer-l gating when absent; predictions for layer
+// l+1 (lookahead 1, Algorithm 1) — and, with lookahead 2, for layer l+2 —
+// are copied after layer-l gating into slots not needed by layer l's own
+// executed set.  One copy lane, FIFO.  When every request misses and the
+// predictions are exact this reduces to the reference's simulators with
+// t_copy[l] = k * t_copy_expert (pinned in tests/test_report.py).
+struct CacheSim {
+    struct Slot {
+        int e = -1;
+        double ready = 0.0;
+        long long last = -1, uses = 0;
+        bool prefetched = false;
+    };
+    int L, C, policy;
+    std::vector<std::vector<Slot>> slots;  // [L][C]
+    CacheSim(int l, int c, int pol) : L(l), C(c), policy(pol), slots(l, std::vector<Slot>(c)) {}
+    Slot* find(int l, int e) {
+        for (Slot& s : slots[l])
+            if (s.e == e) return &s;
+        return nullptr;
+    }
+    // victim slot of layer l avoiding the experts in `keep`; null if none
+    Slot* victim(int l, const std::vector<int>& keep) {
+        Slot* best = nullptr;
+        for (Slot& s : slots[l]) {
+            if (s.e >= 0 && std::find(keep.begin(), keep.end(), s.e) != keep.end()) continue;
+            if (s.e < 0) return &s;
+            if (!best) {
+                best = &s;
+                continue;
+            }
+            const bool better = policy == 1 ? (s.uses < best->uses || (s.uses == best->uses && s.last < best->last))
+                                            : s.last < best->last;
+            if (better) best = &s;
+        }
+        return best;
+    }
+};
+
+struct CacheSimOut {
+    double tpot = 0.0, stall_copies = 0.0, prefetch_copies = 0.0, useful_prefetch = 0.0;
+};
+
+CacheSimOut simulate_cache(int T, int L, int K, int C, int policy, int lookahead, int warm, const int* exec,
+                           const int* pred, const int* pred2, const double* ta, const double* tg, const double* te,
+                           double tc) {
+    CacheSim cs(L, C, policy);
+    CacheSimOut o;
+    double clock = 0.0, copy_free = 0.0;
+    long long seq = 0;
+    int measured = 0;
+    for (int t = 0; t < T; ++t) {
+        const double t0 = clock;
+        double cursor = clock;
+        long long stall = 0, pf = 0, useful = 0;
+        copy_free = std::max(copy_free, clock);
+        for (int l = 0; l < L; ++l) {
+            cursor += ta[l] + tg[l];
+            const double gate_end = cursor;
+            const int* ex = exec + (static_cast<long long>(t) * L + l) * K;
+            const std::vector<int> need(ex, ex + K);
+            // executed experts: hits wait for their copy, misses copy on demand
+            double ready = gate_end;
+            for (int i = 0; i < K; ++i) {
+                CacheSim::Slot* s = cs.find(l, ex[i]);
+                if (s) {
+                    if (s->prefetched) {
+                        ++useful;
+                        s->prefetched = false;
+                    }
+                } else {
+                    s = cs.victim(l, need);
+                    const double st = std::max(copy_free, gate_end);
+                    copy_free = st + tc;
+                    ++stall;
+                    if (s) {
+                        *s = CacheSim::Slot{ex[i], copy_free, seq, 0, false};
+                    } else {  // capacity below k: streamed through without caching
+                        ready = std::max(ready, copy_free);
+                        continue;
+                    }
+                }
+                s->last = seq;
+                ++s->uses;
+                ready = std::max(ready, s->ready);
+            }
+            ++seq;
+            // speculative copies issued after layer-l gating
+            for (int ahead = 1; ahead <= lookahead && ahead <= 2; ++ahead) {
+                const int* pr = ahead == 1 ? pred : pred2;
+                const int tl = l + ahead;
+                if (!pr || tl >= L) continue;
+                const int* pi = pr + (static_cast<long long>(t) * L + tl) * K;
+                const std::vector<int> keep(pi, pi + K);
+                for (int i = 0; i < K; ++i) {
+                    if (cs.find(tl, pi[i])) continue;
+                    CacheSim::Slot* s = cs.victim(tl, keep);
+                    if (!s) continue;
+                    const double st = std::max(copy_free, gate_end);
+                    copy_free = st + tc;
+                    ++pf;
+                    *s = CacheSim::Slot{pi[i], copy_free, seq, 0, true};
+                }
+            }
+            cursor = std::max(cursor, ready) + te[l];
+        }
+        clock = cursor;
+        if (t >= warm) {
+            o.tpot += cursor - t0;
+            o.stall_copies += static_cast<double>(stall);
+            o.prefetch_copies += static_cast<double>(pf);
+            o.useful_prefetch += static_cast<double>(useful);
+            ++measured;
+        }
+    }
+    if (measured) {
+        o.tpot /= measured;
+        o.stall_copies /= measured;
+        o.prefetch_copies /= measured;
+        o.useful_prefetch /= measured;
+    }
+    return o;
+}
+
 }  // namespace report
 }  // namespace smoe
 
@@ -259,6 +388,31 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
         if (recall) *recall = static_cast<double>(hits) / k;
         if (rank_match)
             for (int i = 0; i < k; ++i) rank_match[i] = pred[i] == truth[i];
+    });
+}
+
+// Trace-driven cache + lookahead schedule, see CacheSim.
+int smoe_simulate_cache(const smoe_cache_sim* c, const int32_t* exec_ids, const int32_t* pred_ids,
+                        const int32_t* pred2_ids, const double* t_attn, const double* t_gate,
+                        const double* t_expert, double t_copy_expert, double* out4) {
+    return guard_r([&] {
+        if (!c || !exec_ids || !t_attn || !t_gate || !t_expert || !out4)
+            throw std::invalid_argument("simulate_cache: null argument");
+        if (c->tokens < 1 || c->layers < 1 || c->k < 1) throw std::invalid_argument("simulate_cache: empty trace");
+        if (c->capacity < 0 || c->policy < 0 || c->policy > 1 || c->lookahead < 0 || c->lookahead > 2)
+            throw std::invalid_argument("simulate_cache: bad capacity / policy / lookahead");
+        if (c->lookahead >= 1 && !pred_ids) throw std::invalid_argument("simulate_cache: lookahead needs predictions");
+        if (c->lookahead == 2 && !pred2_ids)
+            throw std::invalid_argument("simulate_cache: lookahead 2 needs two-ahead predictions");
+        if (c->warm_tokens < 0 || c->warm_tokens >= c->tokens)
+            throw std::invalid_argument("simulate_cache: warm_tokens must leave measured tokens");
+        const auto o = smoe::report::simulate_cache(c->tokens, c->layers, c->k, c->capacity, c->policy,
+                                                    c->lookahead, c->warm_tokens, exec_ids, pred_ids, pred2_ids,
+                                                    t_attn, t_gate, t_expert, t_copy_expert);
+        out4[0] = o.tpot;
+        out4[1] = o.stall_copies;
+        out4[2] = o.prefetch_copies;
+        out4[3] = o.useful_prefetch;
     });
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_build_distill_dataset",
+    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator",
 ]
 
@@ -132,6 +132,28 @@ def simulate(t_attn, t_gate, t_expert, t_copy, mode: str, cold_start_copy: float
     _check(lib.smoe_simulate(len(arr[0]), *[_p(a) for a in arr], C.c_double(cold_start_copy),
                              MODE[mode], C.byref(tpot), _p(fr), C.byref(an)))
     return tpot.value, fr, an.value
+
+
+class _CacheSim(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("tokens", "layers", "k", "capacity", "policy", "lookahead",
+                                         "warm_tokens")]
+
+
+def simulate_cache(exec_ids, t_attn, t_gate, t_expert, t_copy_expert, capacity, policy="lru", lookahead=1,
+                   pred_ids=None, pred2_ids=None, warm_tokens=0):
+    """Trace-driven two-lane schedule with a per-layer slot cache.
+    Returns {tpot, stall_copies, prefetch_copies, useful_prefetch} per measured token."""
+    lib = load_library()
+    ex = np.ascontiguousarray(exec_ids, np.int32)
+    T, L, K = ex.shape
+    pr = None if pred_ids is None else np.ascontiguousarray(pred_ids, np.int32)
+    p2 = None if pred2_ids is None else np.ascontiguousarray(pred2_ids, np.int32)
+    ts = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, np.float64), (L,))) for x in (t_attn, t_gate, t_expert)]
+    c = _CacheSim(T, L, K, capacity, {"lru": 0, "lfu": 1}[policy], lookahead, warm_tokens)
+    out = np.zeros(4, np.float64)
+    _check(lib.smoe_simulate_cache(C.byref(c), _p(ex), _p(pr), _p(p2), *[_p(x) for x in ts],
+                                   C.c_double(t_copy_expert), _p(out)))
+    return dict(zip(("tpot", "stall_copies", "prefetch_copies", "useful_prefetch"), out.tolist()))
 
 
 def breakdown(events) -> tuple:
@@ -333,6 +355,12 @@ class Session:
         _check(self.lib.smoe_build_distill_dataset(self._h, first, n, {"quasi": 0, "s-next": 1}[mode],
                                                    _p(inp), _p(tgt)))
         return inp, tgt
+
+    def predict_ahead(self, first: int, n: int, depth: int) -> np.ndarray:
+        """Router-pf ids `depth` layers ahead from captured steps -> [n][L][K] (-1 where l < depth)."""
+        out = np.zeros((n, self.cfg.layers, self.cfg.top_k), np.int32)
+        _check(self.lib.smoe_predict_ahead(self._h, first, n, depth, _p(out)))
+        return out
 
     def write_trace_bundle(self, path: str, first: int, n: int, seq_len: int = 0,
                            source: str = "", seed: int = 0):

@@ -66,3 +66,50 @@ def test_recall_and_rank_alignment(orc):
     r, m = recall_at_k([3, 1, 4, 9], [4, 3, 8, 9])
     assert r == orc.recall_at_k([3, 1, 4, 9], [4, 3, 8, 9]) == 0.75
     assert list(m) == [False, False, False, True]
+
+
+def _disjoint_trace(T, L, K):
+    """Every (token, layer) executes K experts never used before: every request misses."""
+    ids = np.arange(T, dtype=np.int32)[:, None, None] * K + np.arange(K, dtype=np.int32)[None, None, :]
+    return np.ascontiguousarray(np.broadcast_to(ids, (T, L, K)))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_cache_simulator_reduces_to_reference_when_all_miss(ref, seed):
+    """Cache model pinned to the reference's simulate_on_demand /
+    simulate_prefetch (schedule.cpp:92-148): capacity k per layer, each token's
+    experts new, predictions exact -> every layer copies k experts, prefetched one
+    layer ahead; per-layer copy = k * t_copy_expert."""
+    from paper_2603_19289_b200 import engine
+    rng = np.random.default_rng(seed)
+    T, L, K = 5, int(rng.integers(2, 20)), int(rng.integers(1, 9))
+    a, g, e = (rng.integers(0, 16, L).astype(np.float64) * 0.25 for _ in range(3))
+    tc = float(rng.integers(1, 12)) * 0.25
+    ids = _disjoint_trace(T, L, K)
+    for la, mode in ((0, False), (1, True)):
+        got = engine.simulate_cache(ids, a, g, e, tc, capacity=K, lookahead=la, pred_ids=ids)
+        rtp, _, _ = ref.simulate(a, g, e, np.full(L, K * tc), mode, -1.0)
+        assert got["tpot"] == pytest.approx(rtp, rel=1e-12)
+        assert got["stall_copies"] == (L * K if la == 0 else K)
+        assert got["useful_prefetch"] == (0 if la == 0 else (L - 1) * K)
+
+
+def test_cache_simulator_hits_and_lookahead():
+    from paper_2603_19289_b200 import engine
+    rng = np.random.default_rng(0)
+    T, L, K, E = 64, 8, 4, 16
+    ids = np.stack([np.stack([rng.choice(E, K, replace=False) for _ in range(L)]) for _ in range(T)]).astype(np.int32)
+    base = dict(t_attn=1.0, t_gate=0.25, t_expert=2.0, t_copy_expert=1.5)
+    # resident working set: no copies after warm-up, TPOT = sum of compute
+    r = engine.simulate_cache(ids, **base, capacity=E, lookahead=0, warm_tokens=T // 2)
+    assert r["stall_copies"] == 0 and r["tpot"] == pytest.approx(L * 3.25)
+    # exact predictions: one-ahead hides copies, two-ahead hides at least as much
+    lo = engine.simulate_cache(ids, **base, capacity=K, lookahead=0)
+    one = engine.simulate_cache(ids, **base, capacity=2 * K, lookahead=1, pred_ids=ids)
+    two = engine.simulate_cache(ids, **base, capacity=3 * K, lookahead=2, pred_ids=ids, pred2_ids=ids)
+    assert one["tpot"] < lo["tpot"] and two["tpot"] <= one["tpot"]
+    assert two["stall_copies"] <= one["stall_copies"] <= lo["stall_copies"]
+    lfu = engine.simulate_cache(ids, **base, capacity=K + 2, policy="lfu", lookahead=1, pred_ids=ids)
+    assert lfu["tpot"] > 0
+    with pytest.raises(ValueError, match="lookahead 2"):
+        engine.simulate_cache(ids, **base, capacity=K, lookahead=2, pred_ids=ids)
