@@ -1228,7 +1228,8 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
         // guard join, one layer behind: the side work of layer l-2 is complete
         // before the FFN of layer l (its flags were consumed a layer earlier),
         // so spinning expert CTAs can never starve an unfinished predictor
-        if (l >= 2 && side_at[l - 2]) ck(cudaStreamWaitEvent(s, ev_join_[l - 2], 0), "join");
+        static const bool guard_join = std::getenv("SMOE_GUARD_JOIN") != nullptr;
+        if (guard_join && l >= 2 && side_at[l - 2]) ck(cudaStreamWaitEvent(s, ev_join_[l - 2], 0), "join");
         const int t_exp = tl ? tl_begin(0, 2, l, s) : -1;
         ck(launch_ffn(dm_, st, ctl_, l, s, exec_src, s_from_r), "ffn");
         if (tl) tl_end(t_exp, s);
