@@ -816,7 +816,7 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
     }
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32;
-    PipeB pipe;
+    PipeGU pipe;
     pipe.init(pipe_mem, kL2EvictFirst);
     pipe.prime(tile, H);
     if (g_down_l2_dev && threadIdx.x == 0) {
@@ -1422,7 +1422,7 @@ size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
     return vec_bytes(cols) + 64 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
 }
-size_t gu_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeB::kBytes; }
+size_t gu_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeGU::kBytes; }
 size_t down_smem(const DevModel& m) { return 128 + static_cast<size_t>(m.Hmp) * 4 + 128 + PipeD::kBytes; }
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {

@@ -636,6 +636,10 @@ constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
 constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)
 constexpr int kCCd = 192;   // down-projection columns per chunk (12 KB: a 768-column Q30 tile = 4 chunks, all in flight)
 using PipeB = WarpPipe<uint16_t, kS, kCCb>;
+#ifndef SMOE_GU_STAGES
+#define SMOE_GU_STAGES 6
+#endif
+using PipeGU = WarpPipe<uint16_t, SMOE_GU_STAGES, kCCb>;  // expert gate/up: deeper HBM stream per warp
 using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
 using PipeF = WarpPipe<float, kS, kCCf>;
 using PipeD = WarpPipe<uint16_t, kS, kCCd>;

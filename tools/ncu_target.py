@@ -19,6 +19,13 @@ s.set_predictor("router-pf")
 prompt = (np.arange(8) * 37 % 256).astype(np.int32)
 s.reset(64)
 s.prefill(prompt)
+ranged = "--profile-range" in sys.argv  # with `ncu --profile-from-start off`: decode only
+if ranged:
+    import torch
+    torch.cuda.init()
+    torch.cuda.profiler.start()
 s.decode("prefetch", steps)
 s.decode("on_demand", steps)
+if ranged:
+    torch.cuda.profiler.stop()
 print("ok", s.token_ms())
