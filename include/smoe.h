@@ -186,6 +186,17 @@ int smoe_read_trace(smoe_session* s, const char* field, void* out, int64_t n_ele
  * inputs [n][L-1][H], targets [n][L-1][E] (host). */
 int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_t mode, float* inputs,
                                float* targets);
+/* B independent sequences decoded together (batch 1-16 configs): for every
+ * sequence b, generate(model, prompts[b], n_new, predictor)
+ * (speculation.cpp:401-421) — prompt via the true path, then on-demand
+ * (mode 0, forward_decode) or speculative (mode 1, Algorithm 1 with the
+ * router-pf predictor) steps — with the B tokens of a step sharing every
+ * weight stream and expert load.  Each sequence's tokens and logits equal
+ * its single-sequence run.  prompts [B][prompt_len]; out_tokens [B][n_new];
+ * out_logits (nullable) [B][n_new][V].  Does not touch the session's own
+ * decode state. */
+int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, int32_t prompt_len,
+                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits);
 /* Router-pf predictions `depth` layers ahead (multi-layer-
  * ahead prefetch study) from captured steps (trace_full=1, default vectors
  * loaded): ids[t][l][:] = top-k of gate_l . rms_norm(r_{l-depth} +

@@ -204,6 +204,11 @@ int smoe_predict_ahead(smoe_session* s, int32_t first, int32_t n, int32_t depth,
     return guard([&] { S(s)->predict_ahead(first, n, depth, ids); });
 }
 
+int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, int32_t prompt_len,
+                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits) {
+    return guard([&] { S(s)->batch_generate(batch, prompts, prompt_len, n_new, mode, out_tokens, out_logits); });
+}
+
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,
                             int32_t seq_len, const char* source, uint64_t seed) {
     return guard([&] { S(s)->write_trace_bundle(dir, first, n, seq_len, source ? source : "", seed); });

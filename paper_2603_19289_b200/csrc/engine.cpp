@@ -1363,51 +1363,165 @@ void Session::prefill_batched(const int* tokens, int n) {
         dset(pf_.cnt, 0, 4ull * E, "prefill counts");
         ck(launch_pf_layer_dense(m, st_, pf_, l, s_comp_), "prefill layer");
         d2h(cnt.data(), pf_.cnt, 4ull * E, "prefill counts");  // (synchronises)
-        std::vector<int> uni;
-        for (int e = 0; e < c.E; ++e)
-            if (cnt[e] > 0) uni.push_back(e);
-        const int W = std::min<int>(C_, kMaxWave);
-        for (size_t w0 = 0; w0 < uni.size(); w0 += W) {
-            const int nw = static_cast<int>(std::min<size_t>(W, uni.size() - w0));
-            PfWave wv{};
-            wv.n = nw;
-            std::vector<int> cu, cc;  // (expert, 8-token chunk) work items of the wave
-            for (int u = 0; u < nw; ++u) {
-                wv.e[u] = uni[w0 + u];
-                for (int q = 0; q < (cnt[uni[w0 + u]] + 7) / 8; ++q) {
-                    cu.push_back(u);
-                    cc.push_back(q);
-                }
-            }
-            const int chunks = static_cast<int>(cu.size());
-            h2d(pf_.chunk_u, cu.data(), 4ull * chunks, "prefill chunks");
-            h2d(pf_.chunk_c, cc.data(), 4ull * chunks, "prefill chunks");
-            if (!ctl_.resident) {  // load the wave's experts into this layer's slots
-                int hits = 0, misses = 0;
-                auto copies = cache_->request(l, wv.e, nw, &hits, &misses);
-                const long long bytes = store_->bytes_per_expert();
-                for (auto& [slot, expert] : copies)
-                    ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems,
-                                       store_->expert(store_index(l, expert)), bytes, cudaMemcpyHostToDevice,
-                                       s_copy_),
-                       "prefill expert copy");
-                ck(cudaStreamSynchronize(s_copy_), "prefill copies");
-                h2d(d_slot_of_ + static_cast<long long>(l) * c.E, cache_->slot_row(l).data(), 4ull * c.E,
-                    "slot table");
-            }
-            const std::vector<int>& row = cache_->slot_row(l);
-            for (int u = 0; u < nw; ++u) {
-                wv.slot[u] = row[wv.e[u]];
-                if (wv.slot[u] < 0) throw std::runtime_error("expert read before readiness at layer " + std::to_string(l));
-            }
-            ck(launch_pf_experts(m, pf_, l, wv, chunks, s_comp_), "prefill experts");
-            if (w0 + W < uni.size()) ck(cudaStreamSynchronize(s_comp_), "prefill wave");  // slots reused
-        }
+        pf_waves(pf_, l, cnt);
         ck(launch_pf_mix(m, pf_, s_comp_), "prefill mix");
     }
     ck(launch_pf_handoff(m, st_, pf_, s_comp_), "prefill handoff");
     ck(launch_final(dm_, st_, ctl_, 1, s_comp_), "final");
     steps_ += n;
+    sync();
+}
+
+// The experts of one layer for a batch of tokens, in waves of at most C
+// slot-resident experts: copies (cache misses) on the copy stream, then the
+// gate/up and down kernels over the wave's (expert, 8-token chunk) items.
+void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt) {
+    const ModelCfg& c = cfg_;
+    const DevModel& m = dm_;
+    std::vector<int> uni;
+    for (int e = 0; e < c.E; ++e)
+        if (cnt[e] > 0) uni.push_back(e);
+    const int W = std::min<int>(C_, kMaxWave);
+    for (size_t w0 = 0; w0 < uni.size(); w0 += W) {
+        const int nw = static_cast<int>(std::min<size_t>(W, uni.size() - w0));
+        PfWave wv{};
+        wv.n = nw;
+        std::vector<int> cu, cc;  // (expert, 8-token chunk) work items of the wave
+        for (int u = 0; u < nw; ++u) {
+            wv.e[u] = uni[w0 + u];
+            for (int q = 0; q < (cnt[uni[w0 + u]] + 7) / 8; ++q) {
+                cu.push_back(u);
+                cc.push_back(q);
+            }
+        }
+        const int chunks = static_cast<int>(cu.size());
+        h2d(pf.chunk_u, cu.data(), 4ull * chunks, "prefill chunks");
+        h2d(pf.chunk_c, cc.data(), 4ull * chunks, "prefill chunks");
+        if (!ctl_.resident) {  // load the wave's experts into this layer's slots
+            int hits = 0, misses = 0;
+            auto copies = cache_->request(l, wv.e, nw, &hits, &misses);
+            const long long bytes = store_->bytes_per_expert();
+            for (auto& [slot, expert] : copies)
+                ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems,
+                                   store_->expert(store_index(l, expert)), bytes, cudaMemcpyHostToDevice, s_copy_),
+                   "prefill expert copy");
+            ck(cudaStreamSynchronize(s_copy_), "prefill copies");
+            h2d(d_slot_of_ + static_cast<long long>(l) * c.E, cache_->slot_row(l).data(), 4ull * c.E, "slot table");
+        }
+        const std::vector<int>& row = cache_->slot_row(l);
+        for (int u = 0; u < nw; ++u) {
+            wv.slot[u] = row[wv.e[u]];
+            if (wv.slot[u] < 0) throw std::runtime_error("expert read before readiness at layer " + std::to_string(l));
+        }
+        ck(launch_pf_experts(m, pf, l, wv, chunks, s_comp_), "prefill experts");
+        if (w0 + W < uni.size()) ck(cudaStreamSynchronize(s_comp_), "prefill wave");  // slots reused
+    }
+}
+
+void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mode, int* out_tokens,
+                             float* out_logits) {
+    if (B < 1) throw std::invalid_argument("batch_generate: batch must be >= 1");
+    if (P < 1) throw std::invalid_argument("generate: empty prompt");
+    if (n_new < 1) throw std::invalid_argument("generate: n_new must be >= 1");
+    if (opts_.ep_world > 1) throw std::invalid_argument("batch_generate: single GPU only");
+    if (mode == 1 && pred_kind_ == kNone)
+        throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    if (mode == 1 && pred_kind_ != kRouterPF)
+        throw std::invalid_argument("batch_generate: prefetch supports the router-pf predictor");
+    if (mode == 1 && !have_dv_) throw std::invalid_argument("batch_generate: router-pf needs default vectors");
+    const ModelCfg& c = cfg_;
+    const DevModel& m = dm_;
+    for (long long i = 0; i < static_cast<long long>(B) * P; ++i)
+        if (prompts[i] < 0 || prompts[i] >= c.V) throw std::invalid_argument("forward_decode: token out of vocab");
+    if (P + n_new - 1 > m.cap) throw std::invalid_argument("batch_generate: KV capacity exceeded");
+    sync();
+    ck(cudaStreamSynchronize(s_copy_), "copy stream");
+    const long long E = c.E, K = c.K, Hp = m.Hp, D = c.D, nb = m.Hp / 32, Bl = B;
+    std::vector<void*> mine;
+    auto al = [&](size_t bytes) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "batch alloc");
+        mine.push_back(p);
+        return p;
+    };
+    struct Free {
+        std::vector<void*>& v;
+        ~Free() {
+            for (void* p : v) cudaFree(p);
+        }
+    } fr{mine};
+    PrefillDev bd{};
+    bd.P = B;
+    bd.attn_smem_positions = pf_attn_smem_positions();
+    bd.tokens = static_cast<int*>(al(4ull * Bl));
+    bd.X = static_cast<float*>(al(4ull * Bl * Hp));
+    bd.ssqx = static_cast<double*>(al(8ull * Bl * nb));
+    bd.Q = static_cast<float*>(al(4ull * Bl * D));
+    bd.ctx = static_cast<float*>(al(4ull * Bl * D));
+    bd.R = static_cast<float*>(al(4ull * Bl * Hp));
+    bd.ssqr = static_cast<double*>(al(8ull * Bl * nb));
+    bd.lg = static_cast<float*>(al(4ull * Bl * E));
+    bd.ids = static_cast<int*>(al(4ull * Bl * K));
+    bd.gates = static_cast<float*>(al(4ull * Bl * K));
+    bd.cnt = static_cast<int*>(al(4ull * E));
+    bd.off = static_cast<int*>(al(4ull * (E + 1)));
+    bd.fill = static_cast<int*>(al(4ull * E));
+    bd.list = static_cast<int*>(al(4ull * Bl * K));
+    bd.Hb = static_cast<float*>(al(4ull * Bl * K * m.Hmp));
+    bd.Y = static_cast<float*>(al(4ull * Bl * K * Hp));
+    if (m.cap > pf_attn_smem_positions()) bd.attn_scratch = static_cast<double*>(al(8ull * Bl * 2 * m.cap));
+    bd.scale = static_cast<float*>(al(4ull * Bl));
+    bd.chunk_u = static_cast<int*>(al(4ull * (Bl * K + E)));
+    bd.chunk_c = static_cast<int*>(al(4ull * (Bl * K + E)));
+    bd.bkv_stride = static_cast<long long>(c.L) * m.cap * D;
+    bd.bkc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
+    bd.bvc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
+    bd.RD = static_cast<float*>(al(4ull * Bl * Hp));
+    bd.ssqrd = static_cast<double*>(al(8ull * Bl * nb));
+    bd.lgp = static_cast<float*>(al(4ull * Bl * E));
+    bd.pids = static_cast<int*>(al(4ull * 2 * Bl * K));
+    bd.pgates = static_cast<float*>(al(4ull * 2 * Bl * K));
+    bd.logits = static_cast<float*>(al(4ull * Bl * c.V));
+    bd.next = static_cast<int*>(al(4ull * Bl));
+    std::vector<int> cnt(E), tok(B), next(B);
+    std::vector<float> lg(static_cast<size_t>(Bl) * c.V);
+    // one token of every sequence at position pos (forward_decode /
+    // speculative_forward, model.cpp:355-398, speculation.cpp:350-399)
+    auto step = [&](const int* toks, int pos, int md) {
+        bd.pos0 = pos;
+        h2d(const_cast<int*>(bd.tokens), toks, 4ull * B, "batch tokens");
+        ck(launch_pf_embed(m, bd, s_comp_), "batch embed");
+        for (int l = 0; l < c.L; ++l) {
+            dset(bd.cnt, 0, 4ull * E, "batch counts");
+            ck(launch_pf_attn_block(m, st_, bd, l, s_comp_), "batch attention");
+            if (md == 0 || l == 0)
+                ck(launch_pf_route(m, bd, l, s_comp_), "batch router");
+            else
+                ck(launch_pf_exec_pred(m, bd, l & 1, s_comp_), "batch executed = predicted");
+            d2h(cnt.data(), bd.cnt, 4ull * E, "batch counts");  // (synchronises)
+            pf_waves(bd, l, cnt);
+            ck(launch_pf_mix(m, bd, s_comp_), "batch mix");
+            if (md == 1 && l + 1 < c.L) ck(launch_pf_predict(m, bd, l, (l + 1) & 1, s_comp_), "batch predictor");
+        }
+        ck(launch_pf_final(m, bd, s_comp_), "batch final");
+        d2h(next.data(), bd.next, 4ull * B, "batch next");
+        if (out_logits) d2h(lg.data(), bd.logits, 4ull * Bl * c.V, "batch logits");
+    };
+    for (int i = 0; i < P; ++i) {  // prompt: true path (generate, speculation.cpp:404-409)
+        for (int b = 0; b < B; ++b) tok[b] = prompts[static_cast<long long>(b) * P + i];
+        step(tok.data(), i, 0);
+    }
+    for (int i = 0; i < n_new; ++i) {
+        for (int b = 0; b < B; ++b) {
+            out_tokens[static_cast<long long>(b) * n_new + i] = next[b];
+            if (out_logits)
+                std::memcpy(out_logits + (static_cast<long long>(b) * n_new + i) * c.V,
+                            lg.data() + static_cast<long long>(b) * c.V, 4ull * c.V);
+        }
+        if (i + 1 == n_new) break;
+        tok = next;
+        step(tok.data(), P + i, mode);
+    }
     sync();
 }
 

@@ -149,6 +149,12 @@ public:
     void prefill(const int* tokens, int n);               // true routing per token
     // all n prompt tokens per layer at once (prefill.cu); same results
     void prefill_batched(const int* tokens, int n);
+    // B independent sequences decoded together (generate, speculation.cpp:401-421,
+    // per sequence): prompts [B][P], out_tokens [B][n_new], out_logits
+    // (nullable) [B][n_new][V] = the logits each output token was taken from.
+    // mode 0 on-demand (true routing), 1 prefetch (Algorithm 1, router-pf).
+    void batch_generate(int B, const int* prompts, int P, int n_new, int mode, int* out_tokens,
+                        float* out_logits);
     void decode(int mode, int n_steps, int use_graph);    // greedy, device-driven
     // Teacher-forced decode: step i consumes tokens[i] instead of the previous
     // argmax (the reference's trace workload, trace.cpp:187-211, fed through
@@ -233,6 +239,7 @@ private:
     // device allocations (owned)
     std::vector<void*> dev_allocs_;
     void* dalloc(size_t bytes);
+    void pf_waves(const PrefillDev& pf, int layer, const std::vector<int>& cnt);
     void h2d(void* dst, const void* src, size_t n, const char* what);
     void d2h(void* dst, const void* src, size_t n, const char* what);
     void dset(void* p, int v, size_t n, const char* what);

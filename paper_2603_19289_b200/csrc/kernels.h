@@ -118,6 +118,18 @@ struct PrefillDev {
     int* chunk_c;       // [max chunks] chunk index within the expert's token list
     int* dev_step;      // ctl.step (token records)
     int* trace_step;    // trace step counter (nullable)
+    // batched decode (Session::batch_generate): token t is sequence t, all at
+    // position pos0, each with its own KV cache at bkc/bvc + t * bkv_stride
+    float* bkc;         // nullable (prefill of one sequence)
+    float* bvc;
+    long long bkv_stride;
+    float* RD;          // [P][Hp] r_l + d_l (router-pf predictor input)
+    double* ssqrd;      // [P][Hp/32]
+    float* lgp;         // [P][E] predicted logits
+    int* pids;          // [2][P][K] predicted decisions (double-buffered by layer parity)
+    float* pgates;      // [2][P][K]
+    float* logits;      // [P][V] final logits
+    int* next;          // [P] argmax tokens
 };
 constexpr int kMaxWave = 128;
 struct PfWave {
@@ -133,6 +145,16 @@ cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const P
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
                               int chunks, cudaStream_t s);
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
+// batched decode pieces (prefill.cu)
+cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
+                                 cudaStream_t s);
+cudaError_t launch_pf_route(const DevModel& m, const PrefillDev& pf, int layer, cudaStream_t s);
+// executed decision := pids/pgates[buf] (Algorithm 1, l >= 1), then counts / lists
+cudaError_t launch_pf_exec_pred(const DevModel& m, const PrefillDev& pf, int buf, cudaStream_t s);
+// router-pf prediction for layer+1 from r_l and the executed decision -> pids/pgates[buf]
+cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer, int buf, cudaStream_t s);
+// final rms_norm + unembed + argmax for every token -> pf.logits, pf.next
+cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
 cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
 
 int max_dynamic_smem_needed(const DevModel& m);

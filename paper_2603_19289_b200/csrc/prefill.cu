@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, Pr
         float a = acc[t];
         const float other = __shfl_xor_sync(0xffffffffu, a, 1);
         if (t >= nt) continue;
-        const int pos = pf.pos0 + t0 + t;
+        const int pos = pf.bkc ? pf.pos0 : pf.pos0 + t0 + t;
         if (R < 2 * D) {  // RoPE pair (2i, 2i+1), model.cpp:309-321
             const int i = (R % D) >> 1;
             const float c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
@@ -112,13 +112,14 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, Pr
             const float x0 = even ? a : other, x1 = even ? other : a;
             a = even ? (x0 * c - x1 * s) : (x0 * s + x1 * c);
         }
-        const long long kv = (static_cast<long long>(layer) * m.cap + pos) * D;
+        const long long kv = (static_cast<long long>(layer) * m.cap + pos) * D +
+                             (pf.bkc ? static_cast<long long>(t0 + t) * pf.bkv_stride : 0);
         if (R < D)
             pf.Q[static_cast<long long>(t0 + t) * D + R] = a;
         else if (R < 2 * D)
-            st.kc[kv + R - D] = a;
+            (pf.bkc ? pf.bkc : st.kc)[kv + R - D] = a;
         else if (R < 3 * D)
-            st.vc[kv + R - 2 * D] = a;
+            (pf.bkc ? pf.bvc : st.vc)[kv + R - 2 * D] = a;
     }
 }
 
@@ -129,17 +130,18 @@ constexpr int kPfAttnThreads = 256;
 __global__ void __launch_bounds__(kPfAttnThreads) k_pf_attn(DevModel m, DevState st, PrefillDev pf,
                                                              int layer) {
     pf_prologue();
-    const int D = m.D, t = blockIdx.x, n = pf.pos0 + t + 1;
+    const int D = m.D, t = blockIdx.x, n = (pf.bkc ? pf.pos0 : pf.pos0 + t) + 1;
     float* red = reinterpret_cast<float*>(g_smem);  // [32]
     float* qs = red + 32;                           // [D]
     double* e = reinterpret_cast<double*>(qs + kMaxD);
     float* sc = reinterpret_cast<float*>(e + n);
-    if (pf.pos0 + pf.P > pf.attn_smem_positions) {  // long contexts: per-token scratch in global memory
+    if ((pf.bkc ? pf.pos0 + 1 : pf.pos0 + pf.P) > pf.attn_smem_positions) {  // long contexts: global scratch
         e = pf.attn_scratch + static_cast<long long>(t) * 2 * m.cap;
         sc = reinterpret_cast<float*>(e + m.cap);
     }
-    const float* K = st.kc + static_cast<long long>(layer) * m.cap * D;
-    const float* V = st.vc + static_cast<long long>(layer) * m.cap * D;
+    const long long seq = pf.bkc ? static_cast<long long>(t) * pf.bkv_stride : 0;
+    const float* K = (pf.bkc ? pf.bkc : st.kc) + seq + static_cast<long long>(layer) * m.cap * D;
+    const float* V = (pf.bkc ? pf.bvc : st.vc) + seq + static_cast<long long>(layer) * m.cap * D;
     for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = __ldcg(pf.Q + static_cast<long long>(t) * D + i);
     __syncthreads();
     float lmax = -INFINITY;
@@ -374,6 +376,99 @@ __global__ void __launch_bounds__(32) k_pf_handoff(DevModel m, DevState st, Pref
     }
 }
 
+// ------------------------------------------------------ batched decode --
+// Normalised GEMV for kPT tokens per CTA: out[t][row] = W . ((V_t * scale_t) * gain)
+// (predictor: gate_{l+1} over q_l; final: unembed over h).
+__global__ void __launch_bounds__(32 * kPW) k_pf_gemvn(DevModel m, PrefillDev pf, const float* V, const float* gain,
+                                                       const uint16_t* W, int rows, float* out, int out_stride) {
+    const int H = m.H, Hr = round_up(H, 32), w = threadIdx.x >> 5;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
+    const bool has_tile = rb * 32 < round_up(rows, 32);
+    const uint16_t* tile = W + static_cast<long long>(rb) * H * 32;
+    PipePF pipe;
+    pipe.init(pipe_mem);
+    if (has_tile) pipe.prime(tile, H);
+    pf_prologue();
+    int tok_of[kPT];
+#pragma unroll
+    for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
+    pf_stage_norm(m, V, pf.scale, gain, tok_of, nt, xs, Hr);
+    if (!has_tile) return;
+    float acc[kPT];
+    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    const int r = rb * 32 + (threadIdx.x & 31);
+    if (r < rows)
+        for (int t = 0; t < nt; ++t) out[static_cast<long long>(t0 + t) * out_stride + r] = acc[t];
+}
+
+// make_decision per token on predicted logits -> pids/pgates[buf]
+__global__ void __launch_bounds__(32) k_pf_decide_pred(DevModel m, PrefillDev pf, int buf) {
+    pf_prologue();
+    __shared__ double se[kMaxE];
+    __shared__ float sp[kMaxE];
+    const int t = blockIdx.x, K = m.K;
+    const long long o = (static_cast<long long>(buf) * pf.P + t) * K;
+    warp_decision(pf.lgp + static_cast<long long>(t) * m.E, m.E, K, m.gating, sp, se, pf.pids + o, pf.pgates + o);
+}
+
+// executed decision of every token := its prediction (Algorithm 1, l >= 1); counts
+__global__ void __launch_bounds__(32) k_pf_take_pred(DevModel m, PrefillDev pf, int buf) {
+    pf_prologue();
+    const int t = blockIdx.x, K = m.K;
+    if (threadIdx.x < K) {
+        const long long o = (static_cast<long long>(buf) * pf.P + t) * K + threadIdx.x;
+        const int e = __ldcg(pf.pids + o);
+        pf.ids[t * K + threadIdx.x] = e;
+        pf.gates[t * K + threadIdx.x] = __ldcg(pf.pgates + o);
+        atomicAdd(pf.cnt + e, 1);
+    }
+}
+
+// rd = r_l + layer_default(executed_l) (speculation.cpp:104-121) and its rms
+// partials; grid (Hp/32, P).
+__global__ void __launch_bounds__(32) k_pf_quasi(DevModel m, PrefillDev pf, int layer) {
+    pf_prologue();
+    const int t = blockIdx.y, rb = blockIdx.x, j = rb * 32 + threadIdx.x, K = m.K;
+    float rd = 0.0f;
+    if (j < m.H) {
+        float d = 0.0f;
+        for (int i = 0; i < K; ++i) {
+            const int e = __ldcg(pf.ids + t * K + i);
+            d = d + __ldcg(pf.gates + t * K + i) * __ldcg(m.dv + (static_cast<long long>(layer) * m.E + e) * m.H + j);
+        }
+        rd = __ldcg(pf.R + static_cast<long long>(t) * m.Hp + j) + d;
+    }
+    pf.RD[static_cast<long long>(t) * m.Hp + j] = rd;
+    warp_ssq_partial(rd, pf.ssqrd + static_cast<long long>(t) * (m.Hp / 32) + rb);
+}
+
+// argmax_token (model.cpp:391-396): first maximum of each token's logits
+__global__ void __launch_bounds__(32) k_pf_argmax(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    const int t = blockIdx.x;
+    const float* lg = pf.logits + static_cast<long long>(t) * m.V;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < m.V; i += 32) {
+        const float v = lg[i];
+        if (v > best) {  // first maximum within the lane's strided subsequence
+            best = v;
+            bi = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+        }
+    }
+    if (threadIdx.x == 0) pf.next[t] = bi == 0x7fffffff ? 0 : bi;
+}
+
 // ---------------------------------------------------------------- launchers --
 namespace {
 size_t vecf(int n) { return static_cast<size_t>(round_up(n, 32)) * 4; }
@@ -416,7 +511,8 @@ cudaError_t pf_preload() {
                          (const void*)k_pf_wo, (const void*)k_pf_router, (const void*)k_pf_decide,
                          (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu,
                          (const void*)k_pf_down, (const void*)k_pf_mix, (const void*)k_pf_handoff,
-                         (const void*)k_pf_scales};
+                         (const void*)k_pf_scales, (const void*)k_pf_gemvn, (const void*)k_pf_decide_pred,
+                         (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -429,15 +525,26 @@ cudaError_t pf_preload() {
     return cudaSuccess;
 }
 
-cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
-                                  cudaStream_t s) {
+cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
+    PDL(k_pf_embed, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
+                                 cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
     const int wh = pf_warps(pf_h_stage(m), m.QKVp / 32), ww = pf_warps(pf_wo_stage(m), m.Hp / 32);
     PDL(k_pf_qkv, dim3(cdiv(m.QKVp / 32, wh), tg), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, st, pf, layer);
-    const int npos = pf.pos0 + pf.P <= pf.attn_smem_positions ? pf.pos0 + pf.P : 0;
+    const int nmax = pf.bkc ? pf.pos0 + 1 : pf.pos0 + pf.P;
+    const int npos = nmax <= pf.attn_smem_positions ? nmax : 0;
     PDL(k_pf_attn, pf.P, kPfAttnThreads, pf_attn_smem(m, npos), s, m, st, pf, layer);
     PDL(k_pf_wo, dim3(cdiv(m.Hp / 32, ww), tg), 32 * ww, pf_smem(pf_wo_stage(m), ww), s, m, pf, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_route(const DevModel& m, const PrefillDev& pf, int layer, cudaStream_t s) {
+    const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
     const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
     PDL(k_pf_router, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf, layer);
@@ -447,8 +554,40 @@ cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const P
     return cudaGetLastError();
 }
 
-cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
-    PDL(k_pf_embed, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf);
+cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
+                                  cudaStream_t s) {
+    cudaError_t e = launch_pf_attn_block(m, st, pf, layer, s);
+    return e != cudaSuccess ? e : launch_pf_route(m, pf, layer, s);
+}
+
+cudaError_t launch_pf_exec_pred(const DevModel& m, const PrefillDev& pf, int buf, cudaStream_t s) {
+    // the router's scales of r_l feed the expert kernels (pf_stage_norm of R)
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
+    PDL(k_pf_take_pred, pf.P, 32, 0, s, m, pf, buf);
+    PDL(k_pf_offsets, 1, 32, 0, s, m, pf);
+    PDL(k_pf_scatter, pf.P, 32, 0, s, m, pf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer, int buf, cudaStream_t s) {
+    const int tg = (pf.P + kPT - 1) / kPT;
+    PDL(k_pf_quasi, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf, layer);
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqrd));
+    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
+    PDL(k_pf_gemvn, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf,
+        static_cast<const float*>(pf.RD), m.moe_gain + static_cast<long long>(layer + 1) * m.H,
+        m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E);
+    PDL(k_pf_decide_pred, pf.P, 32, 0, s, m, pf, buf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
+    const int tg = (pf.P + kPT - 1) / kPT;
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
+    const int wv = pf_warps(pf_h_stage(m), m.Vp / 32);
+    PDL(k_pf_gemvn, dim3(cdiv(m.Vp / 32, wv), tg), 32 * wv, pf_smem(pf_h_stage(m), wv), s, m, pf,
+        static_cast<const float*>(pf.X), m.final_gain, m.unemb, m.V, pf.logits, m.V);
+    PDL(k_pf_argmax, pf.P, 32, 0, s, m, pf);
     return cudaGetLastError();
 }
 

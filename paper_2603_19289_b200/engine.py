@@ -32,7 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_build_distill_dataset",
+    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator",
 ]
 
@@ -355,6 +355,15 @@ class Session:
         _check(self.lib.smoe_build_distill_dataset(self._h, first, n, {"quasi": 0, "s-next": 1}[mode],
                                                    _p(inp), _p(tgt)))
         return inp, tgt
+
+    def batch_generate(self, prompts, n_new: int, mode: str = "prefetch", logits: bool = False):
+        """B sequences decoded together; prompts [B][P] -> tokens [B][n_new] (and logits [B][n_new][V])."""
+        pr = np.ascontiguousarray(prompts, np.int32)
+        B, P = pr.shape
+        out = np.zeros((B, n_new), np.int32)
+        lg = np.zeros((B, n_new, self.cfg.vocab), np.float32) if logits else None
+        _check(self.lib.smoe_batch_generate(self._h, B, _p(pr), P, n_new, MODE[mode], _p(out), _p(lg)))
+        return (out, lg) if logits else out
 
     def predict_ahead(self, first: int, n: int, depth: int) -> np.ndarray:
         """Router-pf ids `depth` layers ahead from captured steps -> [n][L][K] (-1 where l < depth)."""

@@ -1,0 +1,70 @@
+"""Batched decode (B independent sequences sharing weight streams and expert
+loads; BASELINE configs 2-3 ask for batch 1-16).  Parity at batch B means B
+independent streams (SURVEY "Batch"): every sequence's tokens and logits must
+equal its own single-sequence run, which tests/test_gpu.py pins to the
+reference."""
+import numpy as np
+import pytest
+
+TOY = dict(layers=8, experts=16, top_k=4, hidden=64, expert_hidden=128, vocab=256, head_dim=32, seed=11)
+
+
+def _single(s, prompt, n_new, mode):
+    P = len(prompt)
+    S = P + n_new - 1
+    s.reset(S, True)
+    s.prefill(prompt)
+    if n_new > 1:
+        s.decode(mode, n_new - 1)
+    toks = s.tokens(S)[P - 1:]
+    lg = s.trace("logits", S)[P - 1:]
+    return toks, lg
+
+
+def _session(cfg, frac):
+    from paper_2603_19289_b200 import ModelConfig, Session
+    s = Session(ModelConfig(**cfg), cache_fraction=frac, max_positions=128)
+    s.init_weights_seeded()
+    d, _ = s.calibrate(64, 2, 32)
+    s.load_default_vectors(d)
+    s.set_predictor("router-pf")
+    return s
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["on_demand", "prefetch"])
+@pytest.mark.parametrize("B,frac", [(1, 1.0), (5, 0.5), (16, 0.25)])
+def test_batch_generate_equals_independent_sequences(mode, B, frac):
+    s = _session(TOY, frac)
+    P, n_new = 4, 9
+    prompts = np.random.default_rng(B).integers(0, 256, (B, P)).astype(np.int32)
+    toks, lg = s.batch_generate(prompts, n_new, mode, logits=True)
+    for b in range(B):
+        want_t, want_lg = _single(s, prompts[b], n_new, mode)
+        assert np.array_equal(toks[b], want_t), (b, toks[b], want_t)
+        assert np.array_equal(lg[b].view(np.uint32), want_lg.view(np.uint32)), b
+    s.close()
+
+
+@pytest.mark.gpu
+def test_batch_generate_gptoss_shape_batch8():
+    """GPT-OSS-20B layer shapes (H 2880, 32 experts top-4), depth-truncated, batch 8."""
+    cfg = dict(layers=2, experts=32, top_k=4, hidden=2880, expert_hidden=2880, vocab=256, head_dim=64, seed=3,
+               gating="topk-softmax")
+    s = _session(cfg, 0.25)
+    prompts = np.random.default_rng(8).integers(0, 256, (8, 3)).astype(np.int32)
+    for mode in ("prefetch", "on_demand"):
+        toks = s.batch_generate(prompts, 5, mode)
+        for b in range(8):
+            want_t, _ = _single(s, prompts[b], 5, mode)
+            assert np.array_equal(toks[b], want_t), (mode, b)
+    s.close()
+
+
+@pytest.mark.gpu
+def test_batch_generate_rejects_unsupported_predictor():
+    s = _session(TOY, 1.0)
+    s.set_predictor("baseline-s")
+    with pytest.raises(ValueError, match="router-pf"):
+        s.batch_generate(np.zeros((2, 3), np.int32), 3, "prefetch")
+    s.close()
