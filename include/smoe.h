@@ -193,10 +193,12 @@ int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_
  * router-pf predictor) steps — with the B tokens of a step sharing every
  * weight stream and expert load.  Each sequence's tokens and logits equal
  * its single-sequence run.  prompts [B][prompt_len]; out_tokens [B][n_new];
- * out_logits (nullable) [B][n_new][V].  Does not touch the session's own
- * decode state. */
+ * out_logits (nullable) [B][n_new][V]; step_ms (nullable): mean wall ms per
+ * decode step (prompt excluded).  Does not touch the session's own decode
+ * state. */
 int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, int32_t prompt_len,
-                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits);
+                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits,
+                        double* step_ms);
 /* Router-pf predictions `depth` layers ahead (multi-layer-
  * ahead prefetch study) from captured steps (trace_full=1, default vectors
  * loaded): ids[t][l][:] = top-k of gate_l . rms_norm(r_{l-depth} +

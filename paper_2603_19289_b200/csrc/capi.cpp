@@ -205,8 +205,11 @@ int smoe_predict_ahead(smoe_session* s, int32_t first, int32_t n, int32_t depth,
 }
 
 int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, int32_t prompt_len,
-                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits) {
-    return guard([&] { S(s)->batch_generate(batch, prompts, prompt_len, n_new, mode, out_tokens, out_logits); });
+                        int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits,
+                        double* step_ms) {
+    return guard([&] {
+        S(s)->batch_generate(batch, prompts, prompt_len, n_new, mode, out_tokens, out_logits, step_ms);
+    });
 }
 
 int smoe_write_trace_bundle(smoe_session* s, const char* dir, int32_t first, int32_t n,

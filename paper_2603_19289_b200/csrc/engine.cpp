@@ -403,6 +403,9 @@ Session::~Session() {
 void Session::free_all() {
     drop_graphs();
     if (s_comp_) cudaStreamSynchronize(s_comp_);
+    for (void* p : bd_allocs_) cudaFree(p);
+    bd_allocs_.clear();
+    bd_cap_ = 0;
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_side_) cudaStreamSynchronize(s_side_);
     if (s_log_) cudaStreamSynchronize(s_log_);
@@ -1413,13 +1416,14 @@ void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt)
             wv.slot[u] = row[wv.e[u]];
             if (wv.slot[u] < 0) throw std::runtime_error("expert read before readiness at layer " + std::to_string(l));
         }
-        ck(launch_pf_experts(m, pf, l, wv, chunks, s_comp_), "prefill experts");
+        // prefills fill whole 8-token chunks; decode batches (bkc set) get per-chunk dispatch
+        ck(launch_pf_experts(m, pf, l, wv, chunks, s_comp_, pf.bkc ? 0 : 8), "prefill experts");
         if (w0 + W < uni.size()) ck(cudaStreamSynchronize(s_comp_), "prefill wave");  // slots reused
     }
 }
 
 void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mode, int* out_tokens,
-                             float* out_logits) {
+                             float* out_logits, double* step_ms) {
     if (B < 1) throw std::invalid_argument("batch_generate: batch must be >= 1");
     if (P < 1) throw std::invalid_argument("generate: empty prompt");
     if (n_new < 1) throw std::invalid_argument("generate: n_new must be >= 1");
@@ -1437,52 +1441,60 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
     sync();
     ck(cudaStreamSynchronize(s_copy_), "copy stream");
     const long long E = c.E, K = c.K, Hp = m.Hp, D = c.D, nb = m.Hp / 32, Bl = B;
-    std::vector<void*> mine;
+    if (B > bd_cap_) {  // buffers sized for bd_cap_ sequences, kept across calls
+        for (void* p : bd_allocs_) cudaFree(p);
+        bd_allocs_.clear();
+        bd_cap_ = 0;
+    }
     auto al = [&](size_t bytes) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "batch alloc");
-        mine.push_back(p);
+        bd_allocs_.push_back(p);
         return p;
     };
-    struct Free {
-        std::vector<void*>& v;
-        ~Free() {
-            for (void* p : v) cudaFree(p);
-        }
-    } fr{mine};
-    PrefillDev bd{};
+    PrefillDev& bd = bd_;
+    if (bd_cap_ == 0) {
+        bd = PrefillDev{};
+        bd.tokens = static_cast<int*>(al(4ull * Bl));
+        bd.X = static_cast<float*>(al(4ull * Bl * Hp));
+        bd.ssqx = static_cast<double*>(al(8ull * Bl * nb));
+        bd.Q = static_cast<float*>(al(4ull * Bl * D));
+        bd.ctx = static_cast<float*>(al(4ull * Bl * D));
+        bd.R = static_cast<float*>(al(4ull * Bl * Hp));
+        bd.ssqr = static_cast<double*>(al(8ull * Bl * nb));
+        bd.lg = static_cast<float*>(al(4ull * Bl * E));
+        bd.ids = static_cast<int*>(al(4ull * Bl * K));
+        bd.gates = static_cast<float*>(al(4ull * Bl * K));
+        bd.cnt = static_cast<int*>(al(4ull * E));
+        bd.off = static_cast<int*>(al(4ull * (E + 1)));
+        bd.fill = static_cast<int*>(al(4ull * E));
+        bd.list = static_cast<int*>(al(4ull * Bl * K));
+        bd.Hb = static_cast<float*>(al(4ull * Bl * K * m.Hmp));
+        bd.Y = static_cast<float*>(al(4ull * Bl * K * Hp));
+        if (m.cap > pf_attn_smem_positions()) bd.attn_scratch = static_cast<double*>(al(8ull * Bl * 2 * m.cap));
+        bd.scale = static_cast<float*>(al(4ull * Bl));
+        bd.chunk_u = static_cast<int*>(al(4ull * (Bl * K + E)));
+        bd.chunk_c = static_cast<int*>(al(4ull * (Bl * K + E)));
+        bd.bkv_stride = static_cast<long long>(c.L) * m.cap * D;
+        bd.bkc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
+        bd.bvc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
+        bd.RD = static_cast<float*>(al(4ull * Bl * Hp));
+        bd.ssqrd = static_cast<double*>(al(8ull * Bl * nb));
+        bd.lgp = static_cast<float*>(al(4ull * Bl * E));
+        bd.pids = static_cast<int*>(al(4ull * 2 * Bl * K));
+        bd.pgates = static_cast<float*>(al(4ull * 2 * Bl * K));
+        bd.logits = static_cast<float*>(al(4ull * Bl * c.V));
+        bd.next = static_cast<int*>(al(4ull * Bl));
+        bd_nchunks_ = static_cast<int*>(al(4));
+        bd_cap_ = B;
+    }
     bd.P = B;
     bd.attn_smem_positions = pf_attn_smem_positions();
-    bd.tokens = static_cast<int*>(al(4ull * Bl));
-    bd.X = static_cast<float*>(al(4ull * Bl * Hp));
-    bd.ssqx = static_cast<double*>(al(8ull * Bl * nb));
-    bd.Q = static_cast<float*>(al(4ull * Bl * D));
-    bd.ctx = static_cast<float*>(al(4ull * Bl * D));
-    bd.R = static_cast<float*>(al(4ull * Bl * Hp));
-    bd.ssqr = static_cast<double*>(al(8ull * Bl * nb));
-    bd.lg = static_cast<float*>(al(4ull * Bl * E));
-    bd.ids = static_cast<int*>(al(4ull * Bl * K));
-    bd.gates = static_cast<float*>(al(4ull * Bl * K));
-    bd.cnt = static_cast<int*>(al(4ull * E));
-    bd.off = static_cast<int*>(al(4ull * (E + 1)));
-    bd.fill = static_cast<int*>(al(4ull * E));
-    bd.list = static_cast<int*>(al(4ull * Bl * K));
-    bd.Hb = static_cast<float*>(al(4ull * Bl * K * m.Hmp));
-    bd.Y = static_cast<float*>(al(4ull * Bl * K * Hp));
-    if (m.cap > pf_attn_smem_positions()) bd.attn_scratch = static_cast<double*>(al(8ull * Bl * 2 * m.cap));
-    bd.scale = static_cast<float*>(al(4ull * Bl));
-    bd.chunk_u = static_cast<int*>(al(4ull * (Bl * K + E)));
-    bd.chunk_c = static_cast<int*>(al(4ull * (Bl * K + E)));
-    bd.bkv_stride = static_cast<long long>(c.L) * m.cap * D;
-    bd.bkc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
-    bd.bvc = static_cast<float*>(al(4ull * Bl * bd.bkv_stride));
-    bd.RD = static_cast<float*>(al(4ull * Bl * Hp));
-    bd.ssqrd = static_cast<double*>(al(8ull * Bl * nb));
-    bd.lgp = static_cast<float*>(al(4ull * Bl * E));
-    bd.pids = static_cast<int*>(al(4ull * 2 * Bl * K));
-    bd.pgates = static_cast<float*>(al(4ull * 2 * Bl * K));
-    bd.logits = static_cast<float*>(al(4ull * Bl * c.V));
-    bd.next = static_cast<int*>(al(4ull * Bl));
+    // resident experts: every expert's slot is fixed, the work list is built on
+    // the device and a layer needs no host round trip
+    const bool dev_lists = ctl_.resident && c.E <= kMaxWave;
+    const int max_chunks = static_cast<int>(std::min<long long>(Bl * K, E * ((Bl + 7) / 8)));
+    bd.nchunks = dev_lists ? bd_nchunks_ : nullptr;  // null: host-built lists, no bound check
     std::vector<int> cnt(E), tok(B), next(B);
     std::vector<float> lg(static_cast<size_t>(Bl) * c.V);
     // one token of every sequence at position pos (forward_decode /
@@ -1498,8 +1510,19 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                 ck(launch_pf_route(m, bd, l, s_comp_), "batch router");
             else
                 ck(launch_pf_exec_pred(m, bd, l & 1, s_comp_), "batch executed = predicted");
-            d2h(cnt.data(), bd.cnt, 4ull * E, "batch counts");  // (synchronises)
-            pf_waves(bd, l, cnt);
+            if (dev_lists) {
+                PfWave wv{};
+                wv.n = c.E;
+                const std::vector<int>& row = cache_->slot_row(l);
+                for (int e = 0; e < c.E; ++e) {
+                    wv.e[e] = e;
+                    wv.slot[e] = row[e];
+                }
+                ck(launch_pf_experts_dev(m, bd, l, wv, max_chunks, s_comp_), "batch experts");
+            } else {
+                d2h(cnt.data(), bd.cnt, 4ull * E, "batch counts");  // (synchronises)
+                pf_waves(bd, l, cnt);
+            }
             ck(launch_pf_mix(m, bd, s_comp_), "batch mix");
             if (md == 1 && l + 1 < c.L) ck(launch_pf_predict(m, bd, l, (l + 1) & 1, s_comp_), "batch predictor");
         }
@@ -1511,6 +1534,7 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
         for (int b = 0; b < B; ++b) tok[b] = prompts[static_cast<long long>(b) * P + i];
         step(tok.data(), i, 0);
     }
+    double ms = 0.0;
     for (int i = 0; i < n_new; ++i) {
         for (int b = 0; b < B; ++b) {
             out_tokens[static_cast<long long>(b) * n_new + i] = next[b];
@@ -1520,8 +1544,11 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
         }
         if (i + 1 == n_new) break;
         tok = next;
-        step(tok.data(), P + i, mode);
+        const auto t0 = std::chrono::steady_clock::now();
+        step(tok.data(), P + i, mode);  // ends with the next-token read back
+        ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
+    if (step_ms) *step_ms = n_new > 1 ? ms / (n_new - 1) : 0.0;
     sync();
 }
 

@@ -154,7 +154,7 @@ public:
     // (nullable) [B][n_new][V] = the logits each output token was taken from.
     // mode 0 on-demand (true routing), 1 prefetch (Algorithm 1, router-pf).
     void batch_generate(int B, const int* prompts, int P, int n_new, int mode, int* out_tokens,
-                        float* out_logits);
+                        float* out_logits, double* step_ms);
     void decode(int mode, int n_steps, int use_graph);    // greedy, device-driven
     // Teacher-forced decode: step i consumes tokens[i] instead of the previous
     // argmax (the reference's trace workload, trace.cpp:187-211, fed through
@@ -259,6 +259,10 @@ private:
     unsigned long long ep_tag_[2] = {0, 0};
     float* d_xbuf_ = nullptr;              // EP exchange buffer [2][K][Hp]
     PrefillDev pf_{};                      // batched-prefill buffers (sized for pf_cap_ tokens)
+    PrefillDev bd_{};                      // batched-decode buffers (sized for bd_cap_ sequences)
+    int bd_cap_ = 0;
+    int* bd_nchunks_ = nullptr;
+    std::vector<void*> bd_allocs_;
     int pf_cap_ = 0;
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]
     int* d_epoch_ = nullptr;               // EP combines done [L]

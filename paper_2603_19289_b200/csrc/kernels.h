@@ -130,6 +130,7 @@ struct PrefillDev {
     float* pgates;      // [2][P][K]
     float* logits;      // [P][V] final logits
     int* next;          // [P] argmax tokens
+    int* nchunks;       // device-built (expert, chunk) list length (resident batches), nullable
 };
 constexpr int kMaxWave = 128;
 struct PfWave {
@@ -142,8 +143,9 @@ cudaError_t pf_preload();
 cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
 cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
                                   cudaStream_t s);
+// chains: tokens per chunk worth computing (at most 8; fewer for small batches)
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
-                              int chunks, cudaStream_t s);
+                              int chunks, cudaStream_t s, int chains = 8);
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
 // batched decode pieces (prefill.cu)
 cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
@@ -154,6 +156,10 @@ cudaError_t launch_pf_exec_pred(const DevModel& m, const PrefillDev& pf, int buf
 // router-pf prediction for layer+1 from r_l and the executed decision -> pids/pgates[buf]
 cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer, int buf, cudaStream_t s);
 // final rms_norm + unembed + argmax for every token -> pf.logits, pf.next
+// resident experts: the (expert, chunk) list is built on the device from the
+// counts (no host round trip); wv must map every expert u < E to its slot.
+cudaError_t launch_pf_experts_dev(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
+                                  int max_chunks, cudaStream_t s);
 cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
 cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
 

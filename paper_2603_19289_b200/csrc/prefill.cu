@@ -30,6 +30,29 @@ using PipePF = WarpPipe<uint16_t, 3, kCCf>;  // 4 KB chunks, 12 KB per warp
 using PipePD = PipePF;
 constexpr int kPipeStride = (PipePF::kBytes + 127) & ~127;  // per-warp pipe footprint, 128-aligned
 
+// run_multi with as many chains as the CTA has tokens (1, 2, 4 or 8): a
+// batch of one sequence must not pay for eight chains.
+template <class Pipe>
+__device__ __forceinline__ void run_multi_n(Pipe& pipe, const uint16_t* tile, int cols, const float* xs, int stride,
+                                            int nt, float (&acc)[kPT]) {
+    if (nt <= 1) {
+        float a[1];
+        run_multi<1>(pipe, tile, cols, xs, stride, nt, a);
+        acc[0] = a[0];
+    } else if (nt <= 2) {
+        float a[2];
+        run_multi<2>(pipe, tile, cols, xs, stride, nt, a);
+        acc[0] = a[0], acc[1] = a[1];
+    } else if (nt <= 4) {
+        float a[4];
+        run_multi<4>(pipe, tile, cols, xs, stride, nt, a);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[t] = a[t];
+    } else {
+        run_multi<kPT>(pipe, tile, cols, xs, stride, nt, acc);
+    }
+}
+
 __device__ __forceinline__ void pf_prologue() {
     pdl_wait();
     pdl_trigger();
@@ -96,7 +119,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, Pr
     pf_stage_norm(m, pf.X, pf.scale, m.attn_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    run_multi_n(pipe, tile, H, xs, Hr, nt, acc);
     const int lane = threadIdx.x & 31, R = rb * 32 + lane;
 #pragma unroll
     for (int t = 0; t < kPT; ++t) {
@@ -200,7 +223,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_wo(DevModel m, PrefillDev pf, i
     __syncthreads();
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, D, xs, kMaxD, nt, acc);
+    run_multi_n(pipe, tile, D, xs, kMaxD, nt, acc);
     const int j = rb * 32 + (threadIdx.x & 31);
     for (int t = 0; t < nt; ++t) {
         const long long o = static_cast<long long>(t0 + t) * m.Hp + j;
@@ -229,7 +252,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_router(DevModel m, PrefillDev p
     pf_stage_norm(m, pf.R, pf.scale, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    run_multi_n(pipe, tile, H, xs, Hr, nt, acc);
     const int e = rb * 32 + (threadIdx.x & 31);
     if (e < E)
         for (int t = 0; t < nt; ++t) pf.lg[static_cast<long long>(t0 + t) * E + e] = acc[t];
@@ -275,11 +298,30 @@ __global__ void __launch_bounds__(32) k_pf_scatter(DevModel m, PrefillDev pf) {
 
 // ---------------------------------------------------------------- experts --
 // gate/up: grid (Hmp/16, wave experts, token chunks of kPT); h = silu(g) * u.
+// T = chains per lane (tokens per CTA actually used): 8 for prefill, the
+// next power of two of the batch for batched decode.
+template <int T>
+__device__ __forceinline__ void run_multi_t(PipePF& pipe, const uint16_t* tile, int cols, const float* xs, int stride,
+                                            int nt, float (&acc)[kPT]) {
+    if constexpr (T == kPT) {
+        run_multi<kPT>(pipe, tile, cols, xs, stride, nt, acc);
+    } else if constexpr (T == 0) {  // per-chunk dispatch (batched decode: chunks of 1-8 tokens)
+        run_multi_n(pipe, tile, cols, xs, stride, nt, acc);
+    } else {
+        float a[T];
+        run_multi<T>(pipe, tile, cols, xs, stride, nt, a);
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[t] = a[t];
+    }
+}
+
+template <int T>
 __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, int layer, PfWave wv) {
     const int H = m.H, Hr = round_up(H, 32), K = m.K, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
     pf_prologue();
+    if (pf.nchunks && static_cast<int>(blockIdx.y) >= __ldcg(pf.nchunks)) return;
     const int u = __ldcg(pf.chunk_u + blockIdx.y), e = wv.e[u];
     const int rb = blockIdx.x * (blockDim.x >> 5) + w;
     const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + blockIdx.y) * kPT;
@@ -299,10 +341,10 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
     pf_stage_norm(m, pf.R, pf.scale, m.moe_gain + static_cast<long long>(layer) * H, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    run_multi_t<T>(pipe, tile, H, xs, Hr, nt, acc);
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int t = 0; t < kPT; ++t) {
+    for (int t = 0; t < (T == 0 ? kPT : T); ++t) {
         const float up = __shfl_xor_sync(0xffffffffu, acc[t], 1);
         if (t < nt && (lane & 1) == 0)
             pf.Hb[static_cast<long long>(ent[t]) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc[t]) * up;
@@ -310,11 +352,13 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
 }
 
 // down: grid (Hp/32, wave experts, token chunks); raw expert rows into Y.
+template <int T>
 __global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf, int layer, PfWave wv) {
     const int Hmp = m.Hmp, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hmp]
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hmp)) + w * kPipeStride;
     pf_prologue();
+    if (pf.nchunks && static_cast<int>(blockIdx.y) >= __ldcg(pf.nchunks)) return;
     const int u = __ldcg(pf.chunk_u + blockIdx.y), e = wv.e[u];
     const int rb = blockIdx.x * (blockDim.x >> 5) + w;
     const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + blockIdx.y) * kPT;
@@ -336,7 +380,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf,
     __syncthreads();
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, m.Hm, xs, Hmp, nt, acc);
+    run_multi_t<T>(pipe, tile, m.Hm, xs, Hmp, nt, acc);
     const int j = rb * 32 + (threadIdx.x & 31);
     if (j < m.H)
         for (int t = 0; t < nt; ++t) pf.Y[static_cast<long long>(ent[t]) * m.Hp + j] = acc[t];
@@ -397,7 +441,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gemvn(DevModel m, PrefillDev pf
     pf_stage_norm(m, V, pf.scale, gain, tok_of, nt, xs, Hr);
     if (!has_tile) return;
     float acc[kPT];
-    run_multi<kPT>(pipe, tile, H, xs, Hr, nt, acc);
+    run_multi_n(pipe, tile, H, xs, Hr, nt, acc);
     const int r = rb * 32 + (threadIdx.x & 31);
     if (r < rows)
         for (int t = 0; t < nt; ++t) out[static_cast<long long>(t0 + t) * out_stride + r] = acc[t];
@@ -442,6 +486,21 @@ __global__ void __launch_bounds__(32) k_pf_quasi(DevModel m, PrefillDev pf, int 
     }
     pf.RD[static_cast<long long>(t) * m.Hp + j] = rd;
     warp_ssq_partial(rd, pf.ssqrd + static_cast<long long>(t) * (m.Hp / 32) + rb);
+}
+
+// (expert, 8-token chunk) work list from the per-expert counts, expert order
+__global__ void k_pf_chunks(DevModel m, PrefillDev pf) {
+    pf_prologue();
+    if (threadIdx.x == 0) {
+        int k = 0;
+        for (int e = 0; e < m.E; ++e)
+            for (int q = 0; q < (pf.cnt[e] + kPT - 1) / kPT; ++q) {
+                pf.chunk_u[k] = e;
+                pf.chunk_c[k] = q;
+                ++k;
+            }
+        *pf.nchunks = k;
+    }
 }
 
 // argmax_token (model.cpp:391-396): first maximum of each token's logits
@@ -509,10 +568,11 @@ int pf_attn_smem_positions() { return 12 * 1024; }
 cudaError_t pf_preload() {
     const void* fns[] = {(const void*)k_pf_embed, (const void*)k_pf_qkv, (const void*)k_pf_attn,
                          (const void*)k_pf_wo, (const void*)k_pf_router, (const void*)k_pf_decide,
-                         (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu,
-                         (const void*)k_pf_down, (const void*)k_pf_mix, (const void*)k_pf_handoff,
+                         (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu<0>,
+                         (const void*)k_pf_gu<8>, (const void*)k_pf_down<0>, (const void*)k_pf_down<8>, (const void*)k_pf_mix, (const void*)k_pf_handoff,
                          (const void*)k_pf_scales, (const void*)k_pf_gemvn, (const void*)k_pf_decide_pred,
-                         (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax};
+                         (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax,
+                         (const void*)k_pf_chunks};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -581,6 +641,12 @@ cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer
     return cudaGetLastError();
 }
 
+cudaError_t launch_pf_experts_dev(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
+                                  int max_chunks, cudaStream_t s) {
+    PDL(k_pf_chunks, 1, 32, 0, s, m, pf);
+    return launch_pf_experts(m, pf, layer, wv, max_chunks, s, 0);
+}
+
 cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
@@ -591,14 +657,23 @@ cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_
     return cudaGetLastError();
 }
 
+template <int T>
+cudaError_t launch_pf_experts_t(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv, int chunks,
+                                cudaStream_t s) {
+    const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16), wd = pf_warps(pf_down_stage(m), m.Hp / 32);
+    PDL(k_pf_gu<T>, dim3(cdiv(m.Hmp / 16, wh), chunks), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, pf, layer, wv);
+    PDL(k_pf_down<T>, dim3(cdiv(m.Hp / 32, wd), chunks), 32 * wd, pf_smem(pf_down_stage(m), wd), s, m, pf, layer,
+        wv);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
-                              int chunks, cudaStream_t s) {
+                              int chunks, cudaStream_t s, int chains) {
     // `chunks` = number of (expert, 8-token chunk) work items in pf.chunk_u / chunk_c;
     // the router's scales (of r_l) are still in pf.scale
-    const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16), wd = pf_warps(pf_down_stage(m), m.Hp / 32);
-    PDL(k_pf_gu, dim3(cdiv(m.Hmp / 16, wh), chunks), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, pf, layer, wv);
-    PDL(k_pf_down, dim3(cdiv(m.Hp / 32, wd), chunks), 32 * wd, pf_smem(pf_down_stage(m), wd), s, m, pf, layer, wv);
-    return cudaGetLastError();
+    // chains < 8: small batches whose chunks hold 1-8 tokens -> per-chunk dispatch
+    if (chains < kPT) return launch_pf_experts_t<0>(m, pf, layer, wv, chunks, s);
+    return launch_pf_experts_t<kPT>(m, pf, layer, wv, chunks, s);
 }
 
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {

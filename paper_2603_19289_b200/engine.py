@@ -356,14 +356,19 @@ class Session:
                                                    _p(inp), _p(tgt)))
         return inp, tgt
 
-    def batch_generate(self, prompts, n_new: int, mode: str = "prefetch", logits: bool = False):
-        """B sequences decoded together; prompts [B][P] -> tokens [B][n_new] (and logits [B][n_new][V])."""
+    def batch_generate(self, prompts, n_new: int, mode: str = "prefetch", logits: bool = False,
+                       timing: bool = False):
+        """B sequences decoded together; prompts [B][P] -> tokens [B][n_new] (and logits
+        [B][n_new][V] with logits=True; mean ms per decode step with timing=True)."""
         pr = np.ascontiguousarray(prompts, np.int32)
         B, P = pr.shape
         out = np.zeros((B, n_new), np.int32)
         lg = np.zeros((B, n_new, self.cfg.vocab), np.float32) if logits else None
-        _check(self.lib.smoe_batch_generate(self._h, B, _p(pr), P, n_new, MODE[mode], _p(out), _p(lg)))
-        return (out, lg) if logits else out
+        ms = C.c_double()
+        _check(self.lib.smoe_batch_generate(self._h, B, _p(pr), P, n_new, MODE[mode], _p(out), _p(lg),
+                                            C.byref(ms)))
+        res = (out,) + ((lg,) if logits else ()) + ((ms.value,) if timing else ())
+        return res if len(res) > 1 else out
 
     def predict_ahead(self, first: int, n: int, depth: int) -> np.ndarray:
         """Router-pf ids `depth` layers ahead from captured steps -> [n][L][K] (-1 where l < depth)."""
