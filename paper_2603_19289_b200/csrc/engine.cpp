@@ -1,5 +1,6 @@
 // engine.cpp — host runtime (see engine.h).
 #include "engine.h"
+#include "train.h"
 
 #include <cuda.h>
 #include <immintrin.h>
@@ -992,6 +993,13 @@ void Session::load_estimator(const EstCfg& e, const float* flat) {
         mk(sh_);
     }
     h2d(d_est_, buf.data(), buf.size() * 4, "est upload");
+    // the flat block as well: batched decode runs estimator_forward as chain GEMMs (train.cu)
+    const size_t flat_n = static_cast<size_t>(g_off + 2 * dm) + static_cast<size_t>(e.E) * dm;
+    if (!d_est_flat_ || est_flat_n_ != flat_n) {
+        d_est_flat_ = static_cast<float*>(dalloc(flat_n * 4));
+        est_flat_n_ = flat_n;
+    }
+    h2d(d_est_flat_, flat, flat_n * 4, "est upload");
     est_ = e;
     DevModel& m = dm_;
     m.est_d = e.d;
@@ -1430,9 +1438,16 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
     if (opts_.ep_world > 1) throw std::invalid_argument("batch_generate: single GPU only");
     if (mode == 1 && pred_kind_ == kNone)
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
-    if (mode == 1 && pred_kind_ != kRouterPF)
-        throw std::invalid_argument("batch_generate: prefetch supports the router-pf predictor");
-    if (mode == 1 && !have_dv_) throw std::invalid_argument("batch_generate: router-pf needs default vectors");
+    if (mode == 1 && pred_kind_ == kOracle)
+        throw std::invalid_argument("batch_generate: the oracle predictor replays one shadow state; not batched");
+    auto kind_at = [&](int l) -> int { return pred_kind_ == kHybrid ? hybrid_[l] : pred_kind_; };
+    if (mode == 1)
+        for (int l = 0; l + 1 < cfg_.L; ++l) {
+            const int k = kind_at(l);
+            if ((k == kRouterPF || k == kEstPF) && !have_dv_)
+                throw std::invalid_argument("batch_generate: quasi-hidden inputs need default vectors");
+            if (k == kEstPF && !have_est_) throw std::invalid_argument("batch_generate: est-pf needs an estimator");
+        }
     const ModelCfg& c = cfg_;
     const DevModel& m = dm_;
     for (long long i = 0; i < static_cast<long long>(B) * P; ++i)
@@ -1486,10 +1501,33 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
         bd.logits = static_cast<float*>(al(4ull * Bl * c.V));
         bd.next = static_cast<int*>(al(4ull * Bl));
         bd_nchunks_ = static_cast<int*>(al(4));
+        bd_qn_ = static_cast<float*>(al(4ull * Bl * c.H));
         bd_cap_ = B;
     }
     bd.P = B;
     bd.attn_smem_positions = pf_attn_smem_positions();
+    float *ez = nullptr, *eu = nullptr, *ea = nullptr, *eh = nullptr, *ex = nullptr, *ey = nullptr, *ei = nullptr;
+    int edm = 0, emlp = 0;
+    std::vector<void*> scratch;
+    struct FreeAll {
+        std::vector<void*>& v;
+        ~FreeAll() {
+            for (void* p : v) cudaFree(p);
+        }
+    } free_scratch{scratch};
+    auto tmp = [&](size_t bytes) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "batch alloc");
+        scratch.push_back(p);
+        return static_cast<float*>(p);
+    };
+    if (have_est_ && mode == 1) {  // estimator_forward scratch for B tokens (freed with this call)
+        edm = est_.d / est_.m;
+        emlp = edm * est_.n;
+        for (float** p : {&ez, &eh, &ex, &ey}) *p = tmp(4ull * Bl * edm);
+        for (float** p : {&eu, &ea}) *p = tmp(4ull * Bl * emlp);
+        ei = tmp(4ull * Bl);
+    }
     // resident experts: every expert's slot is fixed, the work list is built on
     // the device and a layer needs no host round trip
     const bool dev_lists = ctl_.resident && c.E <= kMaxWave;
@@ -1524,7 +1562,32 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                 pf_waves(bd, l, cnt);
             }
             ck(launch_pf_mix(m, bd, s_comp_), "batch mix");
-            if (md == 1 && l + 1 < c.L) ck(launch_pf_predict(m, bd, l, (l + 1) & 1, s_comp_), "batch predictor");
+            if (md == 1 && l + 1 < c.L) {  // prediction for l+1 (speculation.cpp:174-252)
+                const int k = kind_at(l), buf = (l + 1) & 1;
+                if (k == kBaselineS) {
+                    ck(launch_pf_predict_baseline_s(m, bd, l, buf, s_comp_), "batch predictor");
+                } else if (k == kRouterPF) {
+                    ck(launch_pf_predict(m, bd, l, buf, s_comp_), "batch predictor");
+                } else {  // est-pf: estimator_forward (estimator.cpp:94-161) over the B q_l
+                    const long long d = est_.d, L = est_.L, dm = edm, mlp = emlp;
+                    const float* A = d_est_flat_;
+                    const float* pos = A + dm * d + static_cast<long long>(l) * dm;
+                    const float* Bw = A + dm * d + L * dm;
+                    const float* Cw = Bw + mlp * dm;
+                    const float* gain = Cw + dm * mlp;
+                    const float* bias = gain + dm;
+                    const float* head = bias + dm;
+                    ck(launch_pf_quasi_q(m, bd, l, bd_qn_, s_comp_), "batch q");
+                    auto gm = [&](ChainGemm g) { ck(launch_chain_gemm(g, s_comp_), "batch estimator"); };
+                    gm({bd_qn_, 1, d, A, 1, d, ez, dm, 1, nullptr, B, edm, static_cast<int>(d), kEpiAddPos, pos,
+                        nullptr, 1});
+                    gm({ez, 1, dm, Bw, 1, dm, eu, mlp, 1, nullptr, B, emlp, edm, kEpiSilu, nullptr, ea, 1});
+                    gm({ea, 1, mlp, Cw, 1, mlp, eh, dm, 1, nullptr, B, edm, emlp, kEpiAddAfter, ez, nullptr, 1});
+                    ck(launch_est_layernorm(eh, gain, bias, B, edm, est_.eps, ex, ey, ei, s_comp_), "batch estimator");
+                    gm({ey, 1, dm, head, 1, dm, bd.lgp, c.E, 1, nullptr, B, c.E, edm, kEpiNone, nullptr, nullptr, 1});
+                    ck(launch_pf_decide_pred(m, bd, buf, s_comp_), "batch predictor");
+                }
+            }
         }
         ck(launch_pf_final(m, bd, s_comp_), "batch final");
         d2h(next.data(), bd.next, 4ull * B, "batch next");

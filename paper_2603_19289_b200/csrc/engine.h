@@ -262,6 +262,9 @@ private:
     PrefillDev bd_{};                      // batched-decode buffers (sized for bd_cap_ sequences)
     int bd_cap_ = 0;
     int* bd_nchunks_ = nullptr;
+    float* bd_qn_ = nullptr;          // [B][H] q_l for the batched estimator
+    float* d_est_flat_ = nullptr;     // estimator params, flat layout (estimator.hpp:41-72)
+    size_t est_flat_n_ = 0;
     std::vector<void*> bd_allocs_;
     int pf_cap_ = 0;
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]

@@ -155,6 +155,13 @@ cudaError_t launch_pf_route(const DevModel& m, const PrefillDev& pf, int layer, 
 cudaError_t launch_pf_exec_pred(const DevModel& m, const PrefillDev& pf, int buf, cudaStream_t s);
 // router-pf prediction for layer+1 from r_l and the executed decision -> pids/pgates[buf]
 cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer, int buf, cudaStream_t s);
+// baseline-s prediction for layer+1 (gate_{l+1} over s_l) -> pids/pgates[buf]
+cudaError_t launch_pf_predict_baseline_s(const DevModel& m, const PrefillDev& pf, int layer, int buf,
+                                         cudaStream_t s);
+// q_l = rms_norm(r_l + d_l, gain_{l+1}) materialised as [P][H] (estimator input)
+cudaError_t launch_pf_quasi_q(const DevModel& m, const PrefillDev& pf, int layer, float* qn, cudaStream_t s);
+// make_decision on pf.lgp -> pids/pgates[buf]
+cudaError_t launch_pf_decide_pred(const DevModel& m, const PrefillDev& pf, int buf, cudaStream_t s);
 // final rms_norm + unembed + argmax for every token -> pf.logits, pf.next
 // resident experts: the (expert, chunk) list is built on the device from the
 // counts (no host round trip); wv must map every expert u < E to its slot.

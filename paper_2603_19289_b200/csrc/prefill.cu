@@ -353,10 +353,12 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_gu(DevModel m, PrefillDev pf, i
 
 // down: grid (Hp/32, wave experts, token chunks); raw expert rows into Y.
 template <int T>
-__global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf, int layer, PfWave wv) {
+__global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf, int layer, PfWave wv, int tpb) {
+    // tpb: tokens staged at a time (8, or fewer when Hmp * 4 B per token would
+    // not fit, e.g. Mixtral's 14336); the tile is streamed once per staging.
     const int Hmp = m.Hmp, w = threadIdx.x >> 5;
-    float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hmp]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hmp)) + w * kPipeStride;
+    float* xs = reinterpret_cast<float*>(g_smem);  // [tpb][Hmp]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + tpb * Hmp)) + w * kPipeStride;
     pf_prologue();
     if (pf.nchunks && static_cast<int>(blockIdx.y) >= __ldcg(pf.nchunks)) return;
     const int u = __ldcg(pf.chunk_u + blockIdx.y), e = wv.e[u];
@@ -372,18 +374,26 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_down(DevModel m, PrefillDev pf,
     int ent[kPT];
 #pragma unroll
     for (int t = 0; t < kPT; ++t) ent[t] = t < nt ? __ldcg(pf.list + b0 + c0 + t) : 0;
-    for (int t = 0; t < nt; ++t) {
-        const float4* h4 = reinterpret_cast<const float4*>(pf.Hb + static_cast<long long>(ent[t]) * Hmp);
-        for (int i = threadIdx.x; i < Hmp / 4; i += blockDim.x)
-            reinterpret_cast<float4*>(xs + t * Hmp)[i] = __ldcg(h4 + i);
-    }
-    __syncthreads();
-    if (!has_tile) return;
-    float acc[kPT];
-    run_multi_t<T>(pipe, tile, m.Hm, xs, Hmp, nt, acc);
     const int j = rb * 32 + (threadIdx.x & 31);
-    if (j < m.H)
-        for (int t = 0; t < nt; ++t) pf.Y[static_cast<long long>(ent[t]) * m.Hp + j] = acc[t];
+    for (int s0 = 0; s0 < nt; s0 += tpb) {
+        const int ns = min(tpb, nt - s0);
+        if (s0) __syncthreads();  // every warp is done with the previous staging
+        for (int t = 0; t < ns; ++t) {
+            const float4* h4 = reinterpret_cast<const float4*>(pf.Hb + static_cast<long long>(ent[s0 + t]) * Hmp);
+            for (int i = threadIdx.x; i < Hmp / 4; i += blockDim.x)
+                reinterpret_cast<float4*>(xs + t * Hmp)[i] = __ldcg(h4 + i);
+        }
+        __syncthreads();
+        if (has_tile) {
+            float acc[kPT];
+            if (tpb == kPT)
+                run_multi_t<T>(pipe, tile, m.Hm, xs, Hmp, ns, acc);
+            else
+                run_multi_n(pipe, tile, m.Hm, xs, Hmp, ns, acc);
+            if (j < m.H)
+                for (int t = 0; t < ns; ++t) pf.Y[static_cast<long long>(ent[s0 + t]) * m.Hp + j] = acc[t];
+        }
+    }
 }
 
 // mixture in decision order (model.cpp:297-301), x = r + m, rms partials of x.
@@ -488,6 +498,16 @@ __global__ void __launch_bounds__(32) k_pf_quasi(DevModel m, PrefillDev pf, int 
     warp_ssq_partial(rd, pf.ssqrd + static_cast<long long>(t) * (m.Hp / 32) + rb);
 }
 
+// q_l materialised for the estimator (est-pf): Qn[t] = (RD_t * scale_t) * gain
+// (rms_norm, numerics.cpp:72-84); grid (ceil(H/32), P).
+__global__ void __launch_bounds__(32) k_pf_normq(DevModel m, PrefillDev pf, const float* gain, float* qn) {
+    pf_prologue();
+    const int t = blockIdx.y, j = blockIdx.x * 32 + threadIdx.x;
+    if (j < m.H)
+        qn[static_cast<long long>(t) * m.H + j] =
+            (__ldcg(pf.RD + static_cast<long long>(t) * m.Hp + j) * __ldcg(pf.scale + t)) * gain[j];
+}
+
 // (expert, 8-token chunk) work list from the per-expert counts, expert order
 __global__ void k_pf_chunks(DevModel m, PrefillDev pf) {
     pf_prologue();
@@ -556,7 +576,15 @@ int pf_warps(size_t stage, int tiles) {
 size_t pf_smem(size_t stage, int w) { return stage + 128 + static_cast<size_t>(w) * kPipeStride; }
 size_t pf_h_stage(const DevModel& m) { return kPT * vecf(m.H); }
 size_t pf_wo_stage(const DevModel&) { return kPT * kMaxD * 4; }
-size_t pf_down_stage(const DevModel& m) { return kPT * static_cast<size_t>(m.Hmp) * 4; }
+// tokens staged at a time by k_pf_down: 8 unless a token's h row is too large
+// (a power of two: run_multi reads every one of its T <= tpb staged rows)
+int pf_down_tpb(const DevModel& m) {
+    const size_t row = static_cast<size_t>(m.Hmp) * 4;
+    int t = kPT;
+    while (t > 1 && static_cast<size_t>(t) * row > 200 * 1024) t >>= 1;
+    return t;
+}
+size_t pf_down_stage(const DevModel& m) { return pf_down_tpb(m) * static_cast<size_t>(m.Hmp) * 4; }
 int cdiv(int a, int b) { return (a + b - 1) / b; }
 size_t pf_attn_smem(const DevModel& m, int npos) {
     return (32 + kMaxD) * 4 + static_cast<size_t>(npos) * 12;
@@ -572,7 +600,7 @@ cudaError_t pf_preload() {
                          (const void*)k_pf_gu<8>, (const void*)k_pf_down<0>, (const void*)k_pf_down<8>, (const void*)k_pf_mix, (const void*)k_pf_handoff,
                          (const void*)k_pf_scales, (const void*)k_pf_gemvn, (const void*)k_pf_decide_pred,
                          (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax,
-                         (const void*)k_pf_chunks};
+                         (const void*)k_pf_chunks, (const void*)k_pf_normq};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -647,6 +675,32 @@ cudaError_t launch_pf_experts_dev(const DevModel& m, const PrefillDev& pf, int l
     return launch_pf_experts(m, pf, layer, wv, max_chunks, s, 0);
 }
 
+cudaError_t launch_pf_predict_baseline_s(const DevModel& m, const PrefillDev& pf, int layer, int buf,
+                                         cudaStream_t s) {
+    // BaselineS (speculation.cpp:180-190): gate_{l+1} over s_l = rms_norm(r_l, gain_l)
+    const int tg = (pf.P + kPT - 1) / kPT;
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
+    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
+    PDL(k_pf_gemvn, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf,
+        static_cast<const float*>(pf.R), m.moe_gain + static_cast<long long>(layer) * m.H,
+        m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E);
+    PDL(k_pf_decide_pred, pf.P, 32, 0, s, m, pf, buf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_quasi_q(const DevModel& m, const PrefillDev& pf, int layer, float* qn, cudaStream_t s) {
+    PDL(k_pf_quasi, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf, layer);
+    PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqrd));
+    PDL(k_pf_normq, dim3(cdiv(m.H, 32), pf.P), 32, 0, s, m, pf, m.moe_gain + static_cast<long long>(layer + 1) * m.H,
+        qn);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pf_decide_pred(const DevModel& m, const PrefillDev& pf, int buf, cudaStream_t s) {
+    PDL(k_pf_decide_pred, pf.P, 32, 0, s, m, pf, buf);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
@@ -663,7 +717,7 @@ cudaError_t launch_pf_experts_t(const DevModel& m, const PrefillDev& pf, int lay
     const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16), wd = pf_warps(pf_down_stage(m), m.Hp / 32);
     PDL(k_pf_gu<T>, dim3(cdiv(m.Hmp / 16, wh), chunks), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, pf, layer, wv);
     PDL(k_pf_down<T>, dim3(cdiv(m.Hp / 32, wd), chunks), 32 * wd, pf_smem(pf_down_stage(m), wd), s, m, pf, layer,
-        wv);
+        wv, pf_down_tpb(m));
     return cudaGetLastError();
 }
 

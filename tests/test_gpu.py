@@ -567,3 +567,17 @@ def test_batched_prefill_q30_layer_shapes(lib):
     b = _decode_after(cfg, prompt, 3, True, 0.25, table=dv)
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_batched_prefill_mixtral_layer_shapes(lib):
+    """Mixtral layer shapes (H 4096, Hm 14336: the down kernel stages two
+    tokens' h rows at a time), 2 layers, cache 0.5: batched and token-by-token
+    prefill agree bit for bit on the following decode."""
+    cfg = dict(layers=2, experts=8, top_k=2, hidden=4096, expert_hidden=14336, vocab=256,
+               head_dim=128, seed=1, gating="topk-softmax")
+    prompt = (np.arange(20) * 53 % 256).astype(np.int32)
+    dv = np.zeros((2, 8, 4096), np.float32)
+    a = _decode_after(cfg, prompt, 3, False, 0.5, table=dv)
+    b = _decode_after(cfg, prompt, 3, True, 0.5, table=dv)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k

@@ -62,9 +62,47 @@ def test_batch_generate_gptoss_shape_batch8():
 
 
 @pytest.mark.gpu
-def test_batch_generate_rejects_unsupported_predictor():
+@pytest.mark.parametrize("kind", ["baseline-s", "est-pf", "hybrid"])
+def test_batch_generate_other_predictors(kind):
+    """baseline-s, est-pf (the Mixtral config's lightweight estimator, run as chain
+    GEMMs) and a hybrid per-layer map, batched, against single-sequence runs."""
+    from paper_2603_19289_b200 import engine
+    s = _session(TOY, 0.5)
+    flat = engine.estimator_init(64, 4, 2, 16, 8, 1e-5, 9)
+    s.load_estimator(64, 4, 2, 16, 8, 1e-5, flat)
+    hybrid = ["est-pf", "router-pf", "baseline-s", "est-pf", "router-pf", "baseline-s", "est-pf"]
+    s.set_predictor(kind, hybrid if kind == "hybrid" else None)
+    prompts = np.random.default_rng(3).integers(0, 256, (6, 4)).astype(np.int32)
+    toks, lg = s.batch_generate(prompts, 8, "prefetch", logits=True)
+    for b in range(6):
+        want_t, want_lg = _single(s, prompts[b], 8, "prefetch")
+        assert np.array_equal(toks[b], want_t), (kind, b)
+        assert np.array_equal(lg[b].view(np.uint32), want_lg.view(np.uint32)), (kind, b)
+    s.close()
+
+
+@pytest.mark.gpu
+def test_batch_generate_rejects_oracle():
     s = _session(TOY, 1.0)
-    s.set_predictor("baseline-s")
-    with pytest.raises(ValueError, match="router-pf"):
+    s.set_predictor("oracle")
+    with pytest.raises(ValueError, match="oracle"):
         s.batch_generate(np.zeros((2, 3), np.int32), 3, "prefetch")
+    s.close()
+
+
+@pytest.mark.gpu
+def test_batch_generate_mixtral_shape_batch16_est_pf():
+    """Mixtral-8x7B layer shapes (H 4096, Hm 14336, 8 experts top-2) with the
+    lightweight estimator (est-pf), depth-truncated, batch 16, half the experts cached."""
+    from paper_2603_19289_b200 import engine
+    cfg = dict(layers=2, experts=8, top_k=2, hidden=4096, expert_hidden=14336, vocab=256, head_dim=128, seed=1,
+               gating="topk-softmax")
+    s = _session(cfg, 0.5)
+    s.load_estimator(4096, 8, 4, 8, 2, 1e-5, engine.estimator_init(4096, 8, 4, 8, 2, 1e-5, 5))
+    s.set_predictor("est-pf")
+    prompts = np.random.default_rng(16).integers(0, 256, (16, 3)).astype(np.int32)
+    toks = s.batch_generate(prompts, 4, "prefetch")
+    for b in range(16):
+        want_t, _ = _single(s, prompts[b], 4, "prefetch")
+        assert np.array_equal(toks[b], want_t), b
     s.close()
