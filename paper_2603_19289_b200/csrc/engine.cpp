@@ -1502,6 +1502,7 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
         bd.next = static_cast<int*>(al(4ull * Bl));
         bd_nchunks_ = static_cast<int*>(al(4));
         bd_qn_ = static_cast<float*>(al(4ull * Bl * c.H));
+        bd_pos_ = static_cast<int*>(al(4));
         bd_cap_ = B;
     }
     bd.P = B;
@@ -1537,9 +1538,11 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
     std::vector<float> lg(static_cast<size_t>(Bl) * c.V);
     // one token of every sequence at position pos (forward_decode /
     // speculative_forward, model.cpp:355-398, speculation.cpp:350-399)
-    auto step = [&](const int* toks, int pos, int md) {
-        bd.pos0 = pos;
-        h2d(const_cast<int*>(bd.tokens), toks, 4ull * B, "batch tokens");
+    // resident experts: each step mode is captured once as a CUDA graph (the
+    // position and the tokens live on the device; nothing in a step needs the host)
+    const bool use_graph = dev_lists && std::getenv("SMOE_BATCH_NO_GRAPH") == nullptr;
+    bd.pos_dev = use_graph ? bd_pos_ : nullptr;
+    auto body = [&](int md) {
         ck(launch_pf_embed(m, bd, s_comp_), "batch embed");
         for (int l = 0; l < c.L; ++l) {
             dset(bd.cnt, 0, 4ull * E, "batch counts");
@@ -1590,6 +1593,33 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
             }
         }
         ck(launch_pf_final(m, bd, s_comp_), "batch final");
+    };
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    struct GraphFree {
+        cudaGraphExec_t* g;
+        ~GraphFree() {
+            for (int i = 0; i < 2; ++i)
+                if (g[i]) cudaGraphExecDestroy(g[i]);
+        }
+    } graph_free{gexec};
+    auto step = [&](const int* toks, int pos, int md) {
+        bd.pos0 = pos;
+        h2d(const_cast<int*>(bd.tokens), toks, 4ull * B, "batch tokens");
+        if (use_graph) {
+            h2d(bd_pos_, &pos, 4, "batch position");
+            if (!gexec[md]) {
+                cudaGraph_t g;
+                ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
+                body(md);
+                ck(cudaStreamEndCapture(s_comp_, &g), "capture");
+                const cudaError_t e = cudaGraphInstantiate(&gexec[md], g, 0);
+                cudaGraphDestroy(g);
+                ck(e, "instantiate");
+            }
+            ck(cudaGraphLaunch(gexec[md], s_comp_), "batch graph");
+        } else {
+            body(md);
+        }
         d2h(next.data(), bd.next, 4ull * B, "batch next");
         if (out_logits) d2h(lg.data(), bd.logits, 4ull * Bl * c.V, "batch logits");
     };

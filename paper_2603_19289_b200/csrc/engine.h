@@ -263,6 +263,7 @@ private:
     int bd_cap_ = 0;
     int* bd_nchunks_ = nullptr;
     float* bd_qn_ = nullptr;          // [B][H] q_l for the batched estimator
+    int* bd_pos_ = nullptr;           // device position of a graph-captured batched step
     float* d_est_flat_ = nullptr;     // estimator params, flat layout (estimator.hpp:41-72)
     size_t est_flat_n_ = 0;
     std::vector<void*> bd_allocs_;

@@ -131,6 +131,7 @@ struct PrefillDev {
     float* logits;      // [P][V] final logits
     int* next;          // [P] argmax tokens
     int* nchunks;       // device-built (expert, chunk) list length (resident batches), nullable
+    const int* pos_dev; // batched decode under a CUDA graph: the position lives on the device
 };
 constexpr int kMaxWave = 128;
 struct PfWave {

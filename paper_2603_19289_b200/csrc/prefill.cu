@@ -29,6 +29,11 @@ constexpr int kPW = 12;  // max warps per CTA: row tiles sharing one staging of 
 using PipePF = WarpPipe<uint16_t, 3, kCCf>;  // 4 KB chunks, 12 KB per warp
 using PipePD = PipePF;
 constexpr int kPipeStride = (PipePF::kBytes + 127) & ~127;  // per-warp pipe footprint, 128-aligned
+// one-warp CTAs (small batches: few row tiles per token group) have the SM's
+// shared memory to themselves: a 64 KB in-flight window instead of 12 KB
+using PipeDeep = WarpPipe<uint16_t, 4, 256>;
+template <class Pipe>
+__host__ __device__ constexpr int pipe_stride() { return (Pipe::kBytes + 127) & ~127; }
 
 // run_multi with as many chains as the CTA has tokens (1, 2, 4 or 8): a
 // batch of one sequence must not pay for eight chains.
@@ -102,17 +107,19 @@ __global__ void __launch_bounds__(32) k_pf_embed(DevModel m, PrefillDev pf) {
 // -------------------------------------------------------------------- qkv --
 // q, k, v for kPT tokens per CTA (model.cpp:325-333), RoPE at position
 // pos0 + t, K/V appended to the layer's cache, q kept per token.
+template <class Pipe>
 __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, PrefillDev pf, int layer) {
     const int H = m.H, Hr = round_up(H, 32), D = m.D, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * pipe_stride<Pipe>();
     const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < m.QKVp;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * H * 32;
-    PipePF pipe;
+    Pipe pipe;
     pipe.init(pipe_mem);
     if (has_tile) pipe.prime(tile, H);
     pf_prologue();
+    const int p0 = pf.pos_dev ? __ldcg(pf.pos_dev) : pf.pos0;
     int tok_of[kPT];
 #pragma unroll
     for (int t = 0; t < kPT; ++t) tok_of[t] = t0 + t;
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_qkv(DevModel m, DevState st, Pr
         float a = acc[t];
         const float other = __shfl_xor_sync(0xffffffffu, a, 1);
         if (t >= nt) continue;
-        const int pos = pf.bkc ? pf.pos0 : pf.pos0 + t0 + t;
+        const int pos = pf.bkc ? p0 : pf.pos0 + t0 + t;
         if (R < 2 * D) {  // RoPE pair (2i, 2i+1), model.cpp:309-321
             const int i = (R % D) >> 1;
             const float c = m.rope[(static_cast<long long>(pos) * (D / 2) + i) * 2];
@@ -153,12 +160,13 @@ constexpr int kPfAttnThreads = 256;
 __global__ void __launch_bounds__(kPfAttnThreads) k_pf_attn(DevModel m, DevState st, PrefillDev pf,
                                                              int layer) {
     pf_prologue();
-    const int D = m.D, t = blockIdx.x, n = (pf.bkc ? pf.pos0 : pf.pos0 + t) + 1;
+    const int p0 = pf.pos_dev ? __ldcg(pf.pos_dev) : pf.pos0;
+    const int D = m.D, t = blockIdx.x, n = (pf.bkc ? p0 : pf.pos0 + t) + 1;
     float* red = reinterpret_cast<float*>(g_smem);  // [32]
     float* qs = red + 32;                           // [D]
     double* e = reinterpret_cast<double*>(qs + kMaxD);
     float* sc = reinterpret_cast<float*>(e + n);
-    if ((pf.bkc ? pf.pos0 + 1 : pf.pos0 + pf.P) > pf.attn_smem_positions) {  // long contexts: global scratch
+    if ((pf.bkc ? (pf.pos_dev ? m.cap : p0 + 1) : pf.pos0 + pf.P) > pf.attn_smem_positions) {  // global scratch
         e = pf.attn_scratch + static_cast<long long>(t) * 2 * m.cap;
         sc = reinterpret_cast<float*>(e + m.cap);
     }
@@ -235,14 +243,15 @@ __global__ void __launch_bounds__(32 * kPW) k_pf_wo(DevModel m, PrefillDev pf, i
 
 // ----------------------------------------------------------------- router --
 // true router logits gate . rms_norm(r, moe_gain) (model.cpp:276-281).
+template <class Pipe>
 __global__ void __launch_bounds__(32 * kPW) k_pf_router(DevModel m, PrefillDev pf, int layer) {
     const int H = m.H, Hr = round_up(H, 32), E = m.E, w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * pipe_stride<Pipe>();
     const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < m.Ep;
     const uint16_t* tile = m.gate + layer * m.gate_stride + static_cast<long long>(rb) * H * 32;
-    PipePF pipe;
+    Pipe pipe;
     pipe.init(pipe_mem);
     if (has_tile) pipe.prime(tile, H);
     pf_prologue();
@@ -433,15 +442,16 @@ __global__ void __launch_bounds__(32) k_pf_handoff(DevModel m, DevState st, Pref
 // ------------------------------------------------------ batched decode --
 // Normalised GEMV for kPT tokens per CTA: out[t][row] = W . ((V_t * scale_t) * gain)
 // (predictor: gate_{l+1} over q_l; final: unembed over h).
+template <class Pipe>
 __global__ void __launch_bounds__(32 * kPW) k_pf_gemvn(DevModel m, PrefillDev pf, const float* V, const float* gain,
                                                        const uint16_t* W, int rows, float* out, int out_stride) {
     const int H = m.H, Hr = round_up(H, 32), w = threadIdx.x >> 5;
     float* xs = reinterpret_cast<float*>(g_smem);  // [kPT][Hr]
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * kPipeStride;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + kPT * Hr)) + w * pipe_stride<Pipe>();
     const int rb = blockIdx.x * (blockDim.x >> 5) + w, t0 = blockIdx.y * kPT, nt = min(kPT, pf.P - t0);
     const bool has_tile = rb * 32 < round_up(rows, 32);
     const uint16_t* tile = W + static_cast<long long>(rb) * H * 32;
-    PipePF pipe;
+    Pipe pipe;
     pipe.init(pipe_mem);
     if (has_tile) pipe.prime(tile, H);
     pf_prologue();
@@ -557,7 +567,10 @@ constexpr size_t kPfSmemBudget = 220 * 1024;
 // Warps per CTA: maximise resident row-tile warps per SM (CTAs per SM x W,
 // each warp with its own pipe next to the CTA's token staging), discounted by
 // the idle warps of the last CTA over the kernel's `tiles` row tiles.
-int pf_warps(size_t stage, int tiles) {
+int pf_warps(size_t stage, int tiles, long long groups) {
+    // few row tiles x token groups (small batches): one warp per CTA, so the
+    // tiles stream through as many SMs as possible
+    if (groups <= 2 && static_cast<long long>(tiles) * groups <= 2 * 148) return 1;
     int best = 1;
     double best_score = -1.0;
     for (int w = kPW; w >= 1; --w) {
@@ -573,7 +586,9 @@ int pf_warps(size_t stage, int tiles) {
     }
     return best;
 }
-size_t pf_smem(size_t stage, int w) { return stage + 128 + static_cast<size_t>(w) * kPipeStride; }
+size_t pf_smem(size_t stage, int w) {
+    return stage + 128 + static_cast<size_t>(w) * (w == 1 ? pipe_stride<PipeDeep>() : kPipeStride);
+}
 size_t pf_h_stage(const DevModel& m) { return kPT * vecf(m.H); }
 size_t pf_wo_stage(const DevModel&) { return kPT * kMaxD * 4; }
 // tokens staged at a time by k_pf_down: 8 unless a token's h row is too large
@@ -594,11 +609,14 @@ size_t pf_attn_smem(const DevModel& m, int npos) {
 int pf_attn_smem_positions() { return 12 * 1024; }
 
 cudaError_t pf_preload() {
-    const void* fns[] = {(const void*)k_pf_embed, (const void*)k_pf_qkv, (const void*)k_pf_attn,
-                         (const void*)k_pf_wo, (const void*)k_pf_router, (const void*)k_pf_decide,
+    const void* fns[] = {(const void*)k_pf_embed, (const void*)k_pf_qkv<PipePF>, (const void*)k_pf_qkv<PipeDeep>,
+                         (const void*)k_pf_attn,
+                         (const void*)k_pf_wo, (const void*)k_pf_router<PipePF>,
+                         (const void*)k_pf_router<PipeDeep>, (const void*)k_pf_decide,
                          (const void*)k_pf_offsets, (const void*)k_pf_scatter, (const void*)k_pf_gu<0>,
                          (const void*)k_pf_gu<8>, (const void*)k_pf_down<0>, (const void*)k_pf_down<8>, (const void*)k_pf_mix, (const void*)k_pf_handoff,
-                         (const void*)k_pf_scales, (const void*)k_pf_gemvn, (const void*)k_pf_decide_pred,
+                         (const void*)k_pf_scales, (const void*)k_pf_gemvn<PipePF>,
+                         (const void*)k_pf_gemvn<PipeDeep>, (const void*)k_pf_decide_pred,
                          (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax,
                          (const void*)k_pf_chunks, (const void*)k_pf_normq};
     for (const void* f : fns) {
@@ -618,13 +636,28 @@ cudaError_t launch_pf_embed(const DevModel& m, const PrefillDev& pf, cudaStream_
     return cudaGetLastError();
 }
 
+cudaError_t launch_gemvn(const DevModel& m, const PrefillDev& pf, int tiles, int tg, const float* V,
+                         const float* gain, const uint16_t* W, int rows, float* out, int out_stride, cudaStream_t s) {
+    const int w = pf_warps(pf_h_stage(m), tiles, tg);
+    if (w == 1)
+        PDL(k_pf_gemvn<PipeDeep>, dim3(tiles, tg), 32, pf_smem(pf_h_stage(m), 1), s, m, pf, V, gain, W, rows, out,
+            out_stride);
+    else
+        PDL(k_pf_gemvn<PipePF>, dim3(cdiv(tiles, w), tg), 32 * w, pf_smem(pf_h_stage(m), w), s, m, pf, V, gain, W,
+            rows, out, out_stride);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
                                  cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
-    const int wh = pf_warps(pf_h_stage(m), m.QKVp / 32), ww = pf_warps(pf_wo_stage(m), m.Hp / 32);
-    PDL(k_pf_qkv, dim3(cdiv(m.QKVp / 32, wh), tg), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, st, pf, layer);
-    const int nmax = pf.bkc ? pf.pos0 + 1 : pf.pos0 + pf.P;
+    const int wh = pf_warps(pf_h_stage(m), m.QKVp / 32, tg), ww = pf_warps(pf_wo_stage(m), m.Hp / 32, tg);
+    if (wh == 1)
+        PDL(k_pf_qkv<PipeDeep>, dim3(m.QKVp / 32, tg), 32, pf_smem(pf_h_stage(m), 1), s, m, st, pf, layer);
+    else
+        PDL(k_pf_qkv<PipePF>, dim3(cdiv(m.QKVp / 32, wh), tg), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, st, pf, layer);
+    const int nmax = pf.bkc ? (pf.pos_dev ? m.cap : pf.pos0 + 1) : pf.pos0 + pf.P;
     const int npos = nmax <= pf.attn_smem_positions ? nmax : 0;
     PDL(k_pf_attn, pf.P, kPfAttnThreads, pf_attn_smem(m, npos), s, m, st, pf, layer);
     PDL(k_pf_wo, dim3(cdiv(m.Hp / 32, ww), tg), 32 * ww, pf_smem(pf_wo_stage(m), ww), s, m, pf, layer);
@@ -634,8 +667,11 @@ cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const Pr
 cudaError_t launch_pf_route(const DevModel& m, const PrefillDev& pf, int layer, cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
-    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
-    PDL(k_pf_router, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf, layer);
+    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32, tg);
+    if (wr == 1)
+        PDL(k_pf_router<PipeDeep>, dim3(m.Ep / 32, tg), 32, pf_smem(pf_h_stage(m), 1), s, m, pf, layer);
+    else
+        PDL(k_pf_router<PipePF>, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf, layer);
     PDL(k_pf_decide, pf.P, 32, 0, s, m, pf);
     PDL(k_pf_offsets, 1, 32, 0, s, m, pf);
     PDL(k_pf_scatter, pf.P, 32, 0, s, m, pf);
@@ -661,10 +697,9 @@ cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_quasi, dim3(m.Hp / 32, pf.P), 32, 0, s, m, pf, layer);
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqrd));
-    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
-    PDL(k_pf_gemvn, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf,
-        static_cast<const float*>(pf.RD), m.moe_gain + static_cast<long long>(layer + 1) * m.H,
-        m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E);
+    cudaError_t e = launch_gemvn(m, pf, m.Ep / 32, tg, pf.RD, m.moe_gain + static_cast<long long>(layer + 1) * m.H,
+                                 m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E, s);
+    if (e != cudaSuccess) return e;
     PDL(k_pf_decide_pred, pf.P, 32, 0, s, m, pf, buf);
     return cudaGetLastError();
 }
@@ -680,10 +715,9 @@ cudaError_t launch_pf_predict_baseline_s(const DevModel& m, const PrefillDev& pf
     // BaselineS (speculation.cpp:180-190): gate_{l+1} over s_l = rms_norm(r_l, gain_l)
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqr));
-    const int wr = pf_warps(pf_h_stage(m), m.Ep / 32);
-    PDL(k_pf_gemvn, dim3(cdiv(m.Ep / 32, wr), tg), 32 * wr, pf_smem(pf_h_stage(m), wr), s, m, pf,
-        static_cast<const float*>(pf.R), m.moe_gain + static_cast<long long>(layer) * m.H,
-        m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E);
+    cudaError_t e = launch_gemvn(m, pf, m.Ep / 32, tg, pf.R, m.moe_gain + static_cast<long long>(layer) * m.H,
+                                 m.gate + (layer + 1) * m.gate_stride, m.E, pf.lgp, m.E, s);
+    if (e != cudaSuccess) return e;
     PDL(k_pf_decide_pred, pf.P, 32, 0, s, m, pf, buf);
     return cudaGetLastError();
 }
@@ -704,9 +738,8 @@ cudaError_t launch_pf_decide_pred(const DevModel& m, const PrefillDev& pf, int b
 cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {
     const int tg = (pf.P + kPT - 1) / kPT;
     PDL(k_pf_scales, pf.P, 32, 0, s, m, pf, static_cast<const double*>(pf.ssqx));
-    const int wv = pf_warps(pf_h_stage(m), m.Vp / 32);
-    PDL(k_pf_gemvn, dim3(cdiv(m.Vp / 32, wv), tg), 32 * wv, pf_smem(pf_h_stage(m), wv), s, m, pf,
-        static_cast<const float*>(pf.X), m.final_gain, m.unemb, m.V, pf.logits, m.V);
+    cudaError_t e = launch_gemvn(m, pf, m.Vp / 32, tg, pf.X, m.final_gain, m.unemb, m.V, pf.logits, m.V, s);
+    if (e != cudaSuccess) return e;
     PDL(k_pf_argmax, pf.P, 32, 0, s, m, pf);
     return cudaGetLastError();
 }
@@ -714,7 +747,7 @@ cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_
 template <int T>
 cudaError_t launch_pf_experts_t(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv, int chunks,
                                 cudaStream_t s) {
-    const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16), wd = pf_warps(pf_down_stage(m), m.Hp / 32);
+    const int wh = pf_warps(pf_h_stage(m), m.Hmp / 16, chunks), wd = pf_warps(pf_down_stage(m), m.Hp / 32, chunks);
     PDL(k_pf_gu<T>, dim3(cdiv(m.Hmp / 16, wh), chunks), 32 * wh, pf_smem(pf_h_stage(m), wh), s, m, pf, layer, wv);
     PDL(k_pf_down<T>, dim3(cdiv(m.Hp / 32, wd), chunks), 32 * wd, pf_smem(pf_down_stage(m), wd), s, m, pf, layer,
         wv, pf_down_tpb(m));
