@@ -187,7 +187,9 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     cap = P + (args.warmup + args.steps) * 2 + 16
     t0 = time.time()
     # expert parallel over `world` GPUs: this rank owns experts e % world == rank
-    s = Session(cfg, device=dev, cache_fraction=1.0, max_positions=max(cap, 300),
+    lc = args.long_prompt if world == 1 and not args.ncu else 0
+    s = Session(cfg, device=dev, cache_fraction=1.0,
+                max_positions=max(cap, 300, lc + args.warmup + args.steps + 16),
                 ep_rank=rank, ep_world=world)
     if world > 1:
         import torch.distributed as dist
@@ -287,9 +289,24 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         tok = nxt
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     slots = s.cache_slots()
+    # long context (PAPER.md:423 prompts of 1k-64k tokens): the prompt through the
+    # batched prefill, then the headline stream workload
+    long_ctx = None
+    if lc:
+        lp = token_stream(lc, c["vocab"], 5)
+        s.reset(lc + args.warmup + args.steps, False)
+        t0 = time.perf_counter()
+        s.prefill_batched(lp)
+        pf_ms = (time.perf_counter() - t0) * 1e3
+        s.decode_stream("prefetch", forced[: args.warmup])
+        s.clear_stats()
+        s.decode_stream("prefetch", forced[args.warmup:])
+        long_ctx = {"prompt_len": lc, "prefill_ms": pf_ms, "prefill_how": "smoe_prefill_batched, wall clock",
+                    "tpot_prefetch_ms": float(np.mean(s.token_ms())), "workload": args.workload,
+                    "cache_fraction": args.cache_fraction}
     s.close()
     return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init, slots=slots,
-                t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P)
+                t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P, long_ctx=long_ctx)
 
 
 # ------------------------------------------------------------- reference ----
@@ -363,6 +380,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="q30", choices=list(CONFIGS))
     ap.add_argument("--prompt-len", type=int, default=32)
+    ap.add_argument("--long-prompt", type=int, default=2048,
+                    help="extra long-context measurement (0 = off): prompt via batched prefill")
     ap.add_argument("--cache-fraction", type=float, default=0.25)
     ap.add_argument("--predictor", default="router-pf")
     ap.add_argument("--calib-tokens", type=int, default=2000)
@@ -537,6 +556,7 @@ def main():
                 "how": "smoe_step(): host token -> device, graph step, logits -> host, wall clock"},
         "gpu_launches": ks * args.steps if ks and ks > 0 else None,
         "kernels_per_step": ks,
+        "long_context": out.get("long_ctx"),
         "clocks": pf["clocks"],
         "setup_s": {"alloc": out["t_alloc"], "init_weights": out["t_init"],
                     "calibrate": out["t_cal"]},

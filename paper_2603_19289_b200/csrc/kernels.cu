@@ -319,12 +319,13 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     cp_async_commit();
     // pass 1: scores
     float lmax = -INFINITY;
+    // chunk c + 2 is fetched into chunk c's slot as soon as c is consumed, so
+    // one chunk load is always in flight behind the one being scored
     for (int c = 0; c < nch; ++c) {
-        if (c >= 2) {  // chunks past the prefetched pair load after the wait (row pos included)
-            fetch_k(c, -1);
-            cp_async_commit();
-        }
-        cp_async_wait<0>();
+        if (c >= 1 && c + 1 < nch)
+            cp_async_wait<1>();  // chunk c landed; chunk c + 1's group may still be pending
+        else
+            cp_async_wait<0>();
         __syncthreads();
         const float* t = kt + (c & 1) * kAttnChunk * KS;
         const int p0 = c * kAttnChunk;
@@ -344,7 +345,11 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
             sc[p0 + j] = v;
             lmax = fmaxf(lmax, v);
         }
-        __syncthreads();  // the ring slot may be refilled next iteration
+        __syncthreads();  // the ring slot is refilled now
+        if (c + 2 < nch) {  // (row pos included: the chunk loads after the PDL wait)
+            fetch_k(c + 2, -1);
+            cp_async_commit();
+        }
     }
     if (!v_early) {  // stream values: first two chunks now, the rest in pass 2
         fetch_v(0, -1);
@@ -368,11 +373,10 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     float acc = 0.0f;
     const int i = threadIdx.x;
     for (int c = 0; c < nch; ++c) {
-        if (c >= 2) {
-            fetch_v(c, -1);
-            cp_async_commit();
-        }
-        cp_async_wait<0>();
+        if (c >= 1 && c + 1 < nch)
+            cp_async_wait<1>();
+        else
+            cp_async_wait<0>();
         __syncthreads();
         const float* t = vt + (c & 1) * kAttnChunk * D;
         const int p0 = c * kAttnChunk;
@@ -380,6 +384,10 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         if (i < D)
             for (int j = 0; j < pn; ++j) acc = acc + sc[p0 + j] * t[j * D + i];
         __syncthreads();
+        if (c + 2 < nch) {
+            fetch_v(c + 2, -1);
+            cp_async_commit();
+        }
     }
     if (i < D) st.ctx[i] = acc;
 }
