@@ -264,9 +264,7 @@ __device__ __forceinline__ void attn_fetch(float* dst, const float* src, int p0,
     }
 }
 
-__global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, double* scratch,
-                                                        int layer) {
-    KTRACE(2, layer);
+__device__ __forceinline__ void attn_single(const DevModel& m, const DevState& st, double* scratch, int layer) {
     const int D = m.D, KS = D + 4;  // padded key row stride (floats)
     float* red = reinterpret_cast<float*>(g_smem);                     // [32]
     float* qs = reinterpret_cast<float*>(g_smem + 256);                // [kMaxD]
@@ -304,7 +302,6 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     }
     cp_async_commit();
     pdl_wait();
-    KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     // q and the current position's key/value row (written by k_qkv)
     for (int t = threadIdx.x; t < D / 4; t += blockDim.x) {
@@ -390,6 +387,128 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         }
     }
     if (i < D) st.ctx[i] = acc;
+}
+
+// Long contexts (more than kAttnSplitMin positions): kAttnSplit CTAs share the
+// work with the same arithmetic as attn_single.  Each CTA scores its slice of
+// positions (one sequential chain per position), the last CTA to arrive forms
+// the softmax (max is order-free; the f64 partition is one sequential chain in
+// index order, numerics.cpp:46-49) and publishes the probabilities; then each
+// CTA produces its slice of the D context outputs (one sequential chain over
+// the positions per output).  All kAttnSplit CTAs are co-resident, so waiting
+// on the last one is safe.  Scratch: e [cap] f64 | p [cap] f32 | ctl | maxes.
+// the dynamic shared memory k_attn is launched with (attn_smem on the host)
+__device__ __forceinline__ size_t attn_smem_bytes(const DevModel& m) {
+    size_t bts = 256 + kMaxD * 4 + 2ull * kAttnChunk * (2 * m.D + 4) * 4;
+    if (m.cap <= kAttnSmemPositions) bts += static_cast<size_t>(m.cap) * 12;
+    return bts;
+}
+
+constexpr int kAttnSplit = 16;
+constexpr int kAttnSplitMin = 512;
+
+__global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, double* scratch, int layer) {
+    KTRACE(2, layer);
+    // st.pos is only advanced by k_final, which completed before this grid could launch
+    const int n = __ldcg(st.pos) + 1;
+    if (n <= kAttnSplitMin || gridDim.x == 1) {
+        if (blockIdx.x == 0) attn_single(m, st, scratch, layer);
+        return;
+    }
+    const int D = m.D, G = gridDim.x, b = blockIdx.x;
+    float* red = reinterpret_cast<float*>(g_smem);       // [32]
+    float* qs = reinterpret_cast<float*>(g_smem + 256);  // [kMaxD]
+    double* eg = scratch;
+    float* pg = reinterpret_cast<float*>(scratch + m.cap);
+    int* ctl = reinterpret_cast<int*>(pg + m.cap);       // [0] arrivals, [1] published generation
+    float* mxs = reinterpret_cast<float*>(ctl + 32);     // [G] per-CTA maxima
+    const long long base = static_cast<long long>(layer) * m.cap * D;
+    const float* K = st.kc + base;
+    const float* V = st.vc + base;
+    pdl_wait();
+    KT_WAITED();
+    pdl_trigger();
+    for (int t = threadIdx.x; t < D; t += blockDim.x) qs[t] = __ldcg(st.q + t);
+    __syncthreads();
+    const int per = (n + G - 1) / G, j0 = b * per, j1 = min(n, j0 + per);
+    float lmax = -INFINITY;
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const float4* kj = reinterpret_cast<const float4*>(K + static_cast<long long>(j) * D);
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int i = 0; i < D / 4; ++i) {
+            const float4 kv = __ldcg(kj + i);
+            acc = acc + qs[4 * i] * kv.x;
+            acc = acc + qs[4 * i + 1] * kv.y;
+            acc = acc + qs[4 * i + 2] * kv.z;
+            acc = acc + qs[4 * i + 3] * kv.w;
+        }
+        const float v = acc * m.inv_sqrt_d;
+        pg[j] = v;  // scores; replaced by probabilities below
+        lmax = fmaxf(lmax, v);
+    }
+    const float mb = block_max_f(lmax, red);
+    __shared__ int s_gen, s_last;
+    __shared__ double zs;
+    if (threadIdx.x == 0) {
+        mxs[b] = mb;
+        __threadfence();
+        const int old = atomicAdd(ctl, 1);
+        s_gen = old / G;
+        s_last = (old % G) == G - 1;
+    }
+    __syncthreads();
+    const int gen = s_gen;
+    // staging area behind q: the exponentials (last CTA), then p and V slices
+    unsigned char* stage = g_smem + 256 + kMaxD * 4;
+    const int cap_s = static_cast<int>((attn_smem_bytes(m) - 256 - kMaxD * 4) / 8);  // f64 slots
+    if (s_last) {
+        __threadfence();
+        float mx = -INFINITY;
+        for (int k = 0; k < G; ++k) mx = fmaxf(mx, __ldcg(mxs + k));
+        double* es = n <= cap_s ? reinterpret_cast<double*>(stage) : eg;
+        for (int j = threadIdx.x; j < n; j += blockDim.x)
+            es[j] = exp(static_cast<double>(__ldcg(pg + j)) - static_cast<double>(mx));
+        __syncthreads();
+        if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
+            double z = 0.0;
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) z += es[j];
+            zs = z;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < n; j += blockDim.x) pg[j] = static_cast<float>(es[j] / zs);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctl + 1), "r"(gen + 1) : "memory");
+        }
+    }
+    if (threadIdx.x == 0)
+        while (ld_acquire(ctl + 1) < gen + 1) __nanosleep(32);
+    __syncthreads();
+    // context slice: outputs [i0, i0 + ipc), p and V[:, slice] staged in chunks
+    // of positions, one sequential chain per output over all positions
+    const int ipc = (D + G - 1) / G, i0 = b * ipc, ni = max(0, min(ipc, D - i0));
+    float* ps = reinterpret_cast<float*>(stage);
+    const int chunk = max(32, min(n, static_cast<int>(cap_s * 8 / (4 * (1 + ipc)))) / 32 * 32);
+    float* vs = ps + chunk;
+    float acc = 0.0f;
+    for (int c0 = 0; c0 < n; c0 += chunk) {
+        const int cn = min(chunk, n - c0);
+        if (c0) __syncthreads();
+        for (int j = threadIdx.x; j < cn; j += blockDim.x) ps[j] = __ldcg(pg + c0 + j);
+        for (int x = threadIdx.x; x < cn * ni; x += blockDim.x) {
+            const int j = x / ni, k = x % ni;
+            vs[j * ipc + k] = __ldcg(V + static_cast<long long>(c0 + j) * D + i0 + k);
+        }
+        __syncthreads();
+        if (threadIdx.x < ni) {
+#pragma unroll 8
+            for (int j = 0; j < cn; ++j) acc = acc + ps[j] * vs[j * ipc + threadIdx.x];
+        }
+    }
+    if (threadIdx.x < ni) st.ctx[i0 + threadIdx.x] = acc;
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
@@ -1521,7 +1640,8 @@ cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStr
 
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
-    PDL(k_attn, 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
+    static const int split = std::getenv("SMOE_ATTN_SPLIT") ? std::atoi(std::getenv("SMOE_ATTN_SPLIT")) : 1;
+    PDL(k_attn, split ? kAttnSplit : 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
     return counted(1);
 }
 

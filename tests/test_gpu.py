@@ -581,3 +581,25 @@ def test_batched_prefill_mixtral_layer_shapes(lib):
     b = _decode_after(cfg, prompt, 3, True, 0.5, table=dv)
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_long_context_split_attention_vs_oracle(lib):
+    """Contexts beyond 512 positions take the split attention (16 CTAs share the
+    scores and the context outputs; the last one forms the softmax): decode after
+    a 700-token prompt stays bit-identical to the oracle."""
+    from oracle.bindings import Config, Oracle
+    cfg = dict(TOY, seed=13)
+    orc = Oracle()
+    om = orc.build_model(Config(**cfg), round_bf16=True)
+    table = om.calibrate(64, 2, 32)
+    prompt = list(np.random.default_rng(7).integers(0, TOY["vocab"], 700))
+    want = om.generate_trace(prompt, 4, orc.make_predictor("router-pf", om, table), outputs=True)
+    s = session(cfg, cache_fraction=0.5, max_positions=800)
+    s.load_default_vectors(np.array(table.d))
+    s.set_predictor("router-pf")
+    got = run_trace(s, prompt, 4, "prefetch")
+    w = dict(tokens=want.tokens, s=want.s, r=want.r, m=want.m, logits=want.logits, ids=want.ids,
+             gates=want.gates, outputs=want.outputs, final_logits=want.final_logits,
+             pred_ids=want.pred_ids, pred_gates=want.pred_gates)
+    assert_trace_equal(got, w, True, len(prompt))
+    s.close()
