@@ -776,6 +776,11 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
         phase_print(rl.do_true ? "true router [pdl, stage+norm, chain, lastcta, decide]"
                                : "predictor [pdl, stage+norm, chain, lastcta, decide]",
                     ph_, nph_);
+#ifdef DECISION_TIMING
+    if (threadIdx.x == 0 && !rl.do_true)
+        printf("predictor decision [stage, softmax, topk, gates] (cycles): %lld %lld %lld %lld\n",
+               g_dec_t[1] - g_dec_t[0], g_dec_t[2] - g_dec_t[1], g_dec_t[3] - g_dec_t[2], g_dec_t[4] - g_dec_t[3]);
+#endif
 #endif
 }
 
