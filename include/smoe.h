@@ -199,6 +199,10 @@ int smoe_build_distill_dataset(smoe_session* s, int32_t first, int32_t n, int32_
 int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, int32_t prompt_len,
                         int32_t n_new, int32_t mode, int32_t* out_tokens, float* out_logits,
                         double* step_ms);
+/* Diagnostics: y = exp(x) computed on the GPU by the device restatement of
+ * glibc's exp(double) that every f64 softmax / silu on the path uses
+ * (exp_glibc.cuh); equal to the host libm's exp bit for bit. */
+int smoe_exp(const double* x, double* y, int64_t n);
 /* Router-pf predictions `depth` layers ahead (multi-layer-
  * ahead prefetch study) from captured steps (trace_full=1, default vectors
  * loaded): ids[t][l][:] = top-k of gate_l . rms_norm(r_{l-depth} +

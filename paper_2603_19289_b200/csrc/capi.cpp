@@ -383,3 +383,21 @@ int smoe_train_estimator(const smoe_estimator_config* c, uint64_t seed, const fl
             curve_out[i] = smoe_curve_point{curve[i].tokens_seen, curve[i].val_kl, curve[i].val_hit_rate};
     });
 }
+
+int smoe_exp(const double* x, double* y, int64_t n) {
+    return guard([&] {
+        if (n < 0 || (n && (!x || !y))) throw std::invalid_argument("smoe_exp: bad arguments");
+        double *dx = nullptr, *dy = nullptr;
+        auto ck = [](cudaError_t e) {
+            if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in smoe_exp: ") + cudaGetErrorString(e));
+        };
+        ck(cudaMalloc(&dx, 8 * std::max<int64_t>(n, 1)));
+        ck(cudaMalloc(&dy, 8 * std::max<int64_t>(n, 1)));
+        cudaError_t e = cudaMemcpy(dx, x, 8 * n, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = smoe::launch_exp_glibc(dx, dy, n, nullptr);
+        if (e == cudaSuccess) e = cudaMemcpy(y, dy, 8 * n, cudaMemcpyDeviceToHost);
+        cudaFree(dx);
+        cudaFree(dy);
+        ck(e);
+    });
+}

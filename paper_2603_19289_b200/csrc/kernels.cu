@@ -355,7 +355,7 @@ __device__ __forceinline__ void attn_single(const DevModel& m, const DevState& s
     }
     const float mx = block_max_f(lmax, red);
     for (int j = threadIdx.x; j < n; j += blockDim.x)
-        e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
+        e[j] = exp_glibc(static_cast<double>(sc[j]) - static_cast<double>(mx));
     __syncthreads();
     __shared__ double zs;
     if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         for (int k = 0; k < G; ++k) mx = fmaxf(mx, __ldcg(mxs + k));
         double* es = n <= cap_s ? reinterpret_cast<double*>(stage) : eg;
         for (int j = threadIdx.x; j < n; j += blockDim.x)
-            es[j] = exp(static_cast<double>(__ldcg(pg + j)) - static_cast<double>(mx));
+            es[j] = exp_glibc(static_cast<double>(__ldcg(pg + j)) - static_cast<double>(mx));
         __syncthreads();
         if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
             double z = 0.0;
@@ -1337,6 +1337,19 @@ __global__ void k_dv_freeze(const double* sums, const long long* counts, float* 
         const long long c = counts[t / H];
         dv[t] = c == 0 ? 0.0f : static_cast<float>(sums[t] / static_cast<double>(c));
     }
+}
+
+// ------------------------------------------------------------ exp check --
+// y = exp_glibc(x) for the parity test of the device exp (tests/test_gpu.py)
+__global__ void k_exp_glibc(const double* x, double* y, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        y[i] = exp_glibc(x[i]);
+}
+
+cudaError_t launch_exp_glibc(const double* x, double* y, long long n, cudaStream_t s) {
+    k_exp_glibc<<<148, 256, 0, s>>>(x, y, n);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------- distill data --

@@ -80,6 +80,9 @@ struct TraceDev {
 cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& tr,
                          cudaStream_t s);
 
+// exp_glibc over n doubles (device buffers) — the parity check of the device exp.
+cudaError_t launch_exp_glibc(const double* x, double* y, long long n, cudaStream_t s);
+
 // DistillDatasetBuilder (speculation.cpp:437-471) over trace steps [first, first+n).
 cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,
                            float* targets, cudaStream_t s);

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kPfAttnThreads) k_pf_attn(DevModel m, DevState
     }
     const float mx = block_max_f(lmax, red);
     for (int j = threadIdx.x; j < n; j += blockDim.x)
-        e[j] = exp(static_cast<double>(sc[j]) - static_cast<double>(mx));
+        e[j] = exp_glibc(static_cast<double>(sc[j]) - static_cast<double>(mx));
     __syncthreads();
     __shared__ double zs;
     if (threadIdx.x == 0) {  // f64 partition in index order, numerics.cpp:46-49

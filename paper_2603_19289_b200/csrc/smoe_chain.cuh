@@ -3,6 +3,7 @@
 // launch, the smem Stager, the bit-exact f64 block reductions and rms_norm,
 // and WarpPipe, the per-warp TMA-fed sequential-chain GEMV.
 #pragma once
+#include "exp_glibc.cuh"
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -145,7 +146,7 @@ __device__ __forceinline__ float to_f(float f) { return f; }
 // numerics.cpp:86-89 — silu in f64, rounded to f32.
 __device__ __forceinline__ float silu_ref(float x) {
     const double xd = static_cast<double>(x);
-    return static_cast<float>(xd / (1.0 + exp(-xd)));
+    return static_cast<float>(xd / (1.0 + exp_glibc(-xd)));
 }
 
 // Deterministic block reduction of a per-thread double (tree order fixed by
@@ -688,7 +689,7 @@ __device__ inline void warp_decision(const float* logits, int E, int K, int gati
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i = i0 + u * 32 + lane;
-                if (i < E) se[i] = exp(static_cast<double>(sp[i]) - static_cast<double>(mx));
+                if (i < E) se[i] = exp_glibc(static_cast<double>(sp[i]) - static_cast<double>(mx));
             }
         }
         __syncwarp();
@@ -795,7 +796,7 @@ __device__ inline void warp_decision(const float* logits, int E, int K, int gati
             double e[kMaxK], z = 0.0;
 #pragma unroll
             for (int t = 0; t < kMaxK; ++t)
-                if (t < K) e[t] = exp(static_cast<double>(s_val[t]) - static_cast<double>(mx));
+                if (t < K) e[t] = exp_glibc(static_cast<double>(s_val[t]) - static_cast<double>(mx));
 #pragma unroll
             for (int t = 0; t < kMaxK; ++t)
                 if (t < K) z += e[t];

@@ -32,7 +32,7 @@ EXPORTS = [
     "smoe_measure_link", "smoe_kernels_per_step", "smoe_preload_all", "smoe_decode_stream",
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
-    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_build_distill_dataset",
+    "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator",
 ]
 
@@ -177,6 +177,15 @@ def recall_at_k(pred, truth):
     m = np.zeros(len(p), np.int32)
     _check(lib.smoe_recall_at_k(_p(p), _p(t), len(p), C.byref(r), _p(m)))
     return r.value, m.astype(bool)
+
+
+def device_exp(x) -> np.ndarray:
+    """exp on the GPU through the device restatement of glibc's exp(double)."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros_like(x)
+    _check(lib.smoe_exp(_p(x), _p(y), C.c_int64(x.size)))
+    return y
 
 
 def estimator_init(d, m, n, E, L, eps=1e-5, seed=0) -> np.ndarray:
