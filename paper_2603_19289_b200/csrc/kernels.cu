@@ -76,6 +76,26 @@ __device__ __forceinline__ void publish_decision(const DevState& st, int layer) 
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(st.dec_ready + layer), "r"(p) : "memory");
 }
 
+// dst := src for one decision (single thread): every load issued before the
+// first store, so the K round trips overlap instead of serialising behind
+// the stores.
+__device__ __forceinline__ void copy_decision(const int* sid, const float* sg, int* did, float* dg, int k) {
+    int iv[kMaxK];
+    float gv[kMaxK];
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < k) {
+            iv[i] = __ldcg(sid + i);
+            gv[i] = __ldcg(sg + i);
+        }
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < k) {
+            did[i] = iv[i];
+            dg[i] = gv[i];
+        }
+}
+
 // Mailbox post (single thread): request copies of `ids` for `layer`.
 __device__ void post_request(const DevCtl& ctl, int layer, int step, const int* ids, int k) {
     const int seq = *ctl.req_counter + 1;
@@ -85,7 +105,15 @@ __device__ void post_request(const DevCtl& ctl, int layer, int step, const int* 
     e->layer = layer;
     e->step = step;
     e->nids = k;
-    for (int i = 0; i < k; ++i) e->ids[i] = ids[i];
+    // all loads first: a load after a store to (possibly aliasing) memory
+    // would otherwise wait for it, one L2 round trip per id
+    int v[kMaxK];
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < k) v[i] = __ldcg(ids + i);
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < k) e->ids[i] = v[i];
     __threadfence_system();
     e->seq = seq;
 }
@@ -738,10 +766,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
         warp_decision(st.lg_true + static_cast<long long>(l) * E, E, K, m.gating, sp, se,
                       st.id_true + l * K, st.g_true + l * K);
         if (threadIdx.x == 0 && rl.exec_from == 0) {
-            for (int i = 0; i < K; ++i) {
-                st.id_exec[l * K + i] = st.id_true[l * K + i];
-                st.g_exec[l * K + i] = st.g_true[l * K + i];
-            }
+            copy_decision(st.id_true + l * K, st.g_true + l * K, st.id_exec + l * K, st.g_exec + l * K, K);
             if (rl.post_exec && !ctl.resident) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
         }
     }
@@ -759,12 +784,8 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
             if (rl.post_pred && !ctl.resident)
                 post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
             if ((gemv_pred || rl.pred_kind == kOracle) && l + 1 < m.L) publish_decision(st, l + 1);
-            if (rl.exec_from == 1) {
-                for (int i = 0; i < K; ++i) {
-                    st.id_exec[l * K + i] = __ldcg(st.id_pred + l * K + i);
-                    st.g_exec[l * K + i] = __ldcg(st.g_pred + l * K + i);
-                }
-            }
+            if (rl.exec_from == 1)
+                copy_decision(st.id_pred + l * K, st.g_pred + l * K, st.id_exec + l * K, st.g_exec + l * K, K);
         }
         if (rl.pred_kind == kOracle && has_shadow)
             for (int e = threadIdx.x; e < E; e += blockDim.x)
