@@ -444,6 +444,8 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         return;
     }
     const int D = m.D, G = gridDim.x, b = blockIdx.x;
+    PHASE_DECL
+    PHASE();
     float* red = reinterpret_cast<float*>(g_smem);       // [32]
     float* qs = reinterpret_cast<float*>(g_smem + 256);  // [kMaxD]
     double* eg = scratch;
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         lmax = fmaxf(lmax, v);
     }
     const float mb = block_max_f(lmax, red);
+    PHASE();
     __shared__ int s_gen, s_last;
     __shared__ double zs;
     if (threadIdx.x == 0) {
@@ -500,13 +503,21 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         __syncthreads();
         if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
             double z = 0.0;
-#pragma unroll 8
-            for (int j = 0; j < n; ++j) z += es[j];
+            int j = 0;
+            for (; j + 8 <= n; j += 8) {  // loads of a block in flight together, adds in order
+                double ev[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) ev[u] = es[j + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) z += ev[u];
+            }
+            for (; j < n; ++j) z += es[j];
             zs = z;
         }
         __syncthreads();
         for (int j = threadIdx.x; j < n; j += blockDim.x) pg[j] = static_cast<float>(es[j] / zs);
         __syncthreads();
+        PHASE();
         if (threadIdx.x == 0) {
             __threadfence();
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctl + 1), "r"(gen + 1) : "memory");
@@ -515,6 +526,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     if (threadIdx.x == 0)
         while (ld_acquire(ctl + 1) < gen + 1) __nanosleep(32);
     __syncthreads();
+    PHASE();
     // context slice: outputs [i0, i0 + ipc), p and V[:, slice] staged in chunks
     // of positions, one sequential chain per output over all positions
     const int ipc = (D + G - 1) / G, i0 = b * ipc, ni = max(0, min(ipc, D - i0));
@@ -526,17 +538,43 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         const int cn = min(chunk, n - c0);
         if (c0) __syncthreads();
         for (int j = threadIdx.x; j < cn; j += blockDim.x) ps[j] = __ldcg(pg + c0 + j);
-        for (int x = threadIdx.x; x < cn * ni; x += blockDim.x) {
-            const int j = x / ni, k = x % ni;
-            vs[j * ipc + k] = __ldcg(V + static_cast<long long>(c0 + j) * D + i0 + k);
+        if ((ipc & 3) == 0 && ni == ipc) {  // float4 rows, every load of a thread in flight together
+            const int q4 = ipc >> 2;        // float4 per row slice
+#pragma unroll 8
+            for (int x = threadIdx.x; x < cn * q4; x += blockDim.x) {
+                const int j = x / q4, k = x % q4;
+                reinterpret_cast<float4*>(vs + j * ipc)[k] =
+                    __ldcg(reinterpret_cast<const float4*>(V + static_cast<long long>(c0 + j) * D + i0) + k);
+            }
+        } else {
+            for (int x = threadIdx.x; x < cn * ni; x += blockDim.x) {
+                const int j = x / ni, k = x % ni;
+                vs[j * ipc + k] = __ldcg(V + static_cast<long long>(c0 + j) * D + i0 + k);
+            }
         }
         __syncthreads();
         if (threadIdx.x < ni) {
-#pragma unroll 8
-            for (int j = 0; j < cn; ++j) acc = acc + ps[j] * vs[j * ipc + threadIdx.x];
+            int j = 0;
+            for (; j + 8 <= cn; j += 8) {  // operands of a block loaded together, chain in order
+                float pv[8], vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    pv[u] = ps[j + u];
+                    vv[u] = vs[(j + u) * ipc + threadIdx.x];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = acc + pv[u] * vv[u];
+            }
+            for (; j < cn; ++j) acc = acc + ps[j] * vs[j * ipc + threadIdx.x];
         }
     }
     if (threadIdx.x < ni) st.ctx[i0 + threadIdx.x] = acc;
+    PHASE();
+#ifdef SMOE_PHASES
+    if (threadIdx.x == 0 && (b == 0 || s_last))
+        phase_print(s_last ? "attn split LAST [start, scores, softmax, flag wait, context]"
+                           : "attn split cta0 [start, scores, flag wait, context]", ph_, nph_);
+#endif
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).

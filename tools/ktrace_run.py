@@ -3,7 +3,7 @@ instrumented build (make -C paper_2603_19289_b200/csrc ktrace): per layer and
 kernel the first CTA entry, first CTA past its PDL wait and last CTA exit,
 in µs from the step start.  Tools only.
 
-    python tools/ktrace_run.py [layers] [cache_fraction] [greedy|stream]
+    python tools/ktrace_run.py [layers] [cache_fraction] [greedy|stream] [--prompt=N]
 """
 import ctypes as C
 import os
@@ -25,11 +25,12 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 wl = sys.argv[3] if len(sys.argv) > 3 else "greedy"
 use_graph = "--no-graph" not in sys.argv
+plen = next((int(a.split("=")[1]) for a in sys.argv if a.startswith("--prompt=")), 32)
 lib = C.CDLL(LIB)
 lib.smoe_ktrace_read.argtypes = [C.c_void_p]
 cfg = ModelConfig(layers=L, experts=128, top_k=8, hidden=2048, expert_hidden=768, vocab=256,
                   head_dim=128, seed=1)
-s = Session(cfg, cache_fraction=frac, max_positions=512)
+s = Session(cfg, cache_fraction=frac, max_positions=max(512, plen + 96))
 s.init_weights_seeded()
 if frac == 1.0:
     s.preload_all()
@@ -38,8 +39,8 @@ s.set_predictor("router-pf")
 rng = np.random.default_rng(4)
 forced = rng.integers(0, 256, 64).astype(np.int32)
 for mode in ("prefetch", "on_demand"):
-    s.reset(128)
-    s.prefill(list(range(32)))
+    s.reset(plen + 96)
+    s.prefill_batched(list(rng.integers(0, 256, plen)) if plen > 32 else list(range(32)))
     if wl == "stream":
         s.decode_stream(mode, forced[:8])
     else:
