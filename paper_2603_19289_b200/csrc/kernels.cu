@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         for (int j = threadIdx.x; j < n; j += blockDim.x)
             es[j] = exp_glibc(static_cast<double>(__ldcg(pg + j)) - static_cast<double>(mx));
         __syncthreads();
+        PHASE();
         if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
             double z = 0.0;
             int j = 0;
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
             zs = z;
         }
         __syncthreads();
+        PHASE();
         for (int j = threadIdx.x; j < n; j += blockDim.x) pg[j] = static_cast<float>(es[j] / zs);
         __syncthreads();
         PHASE();
@@ -537,16 +539,21 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     for (int c0 = 0; c0 < n; c0 += chunk) {
         const int cn = min(chunk, n - c0);
         if (c0) __syncthreads();
-        for (int j = threadIdx.x; j < cn; j += blockDim.x) ps[j] = __ldcg(pg + c0 + j);
-        if ((ipc & 3) == 0 && ni == ipc) {  // float4 rows, every load of a thread in flight together
-            const int q4 = ipc >> 2;        // float4 per row slice
-#pragma unroll 8
+        if ((ipc & 3) == 0 && ni == ipc && (reinterpret_cast<uintptr_t>(pg + c0) & 15) == 0) {  // cp.async
+            const int q4 = ipc >> 2;                           // float4 per row slice
+            for (int x = threadIdx.x; x < (cn + 3) / 4; x += blockDim.x)
+                if (4 * x + 3 < cn)
+                    cp_async16(ps + 4 * x, pg + c0 + 4 * x);
+                else
+                    for (int j = 4 * x; j < cn; ++j) ps[j] = __ldcg(pg + c0 + j);
             for (int x = threadIdx.x; x < cn * q4; x += blockDim.x) {
                 const int j = x / q4, k = x % q4;
-                reinterpret_cast<float4*>(vs + j * ipc)[k] =
-                    __ldcg(reinterpret_cast<const float4*>(V + static_cast<long long>(c0 + j) * D + i0) + k);
+                cp_async16(vs + j * ipc + 4 * k, V + static_cast<long long>(c0 + j) * D + i0 + 4 * k);
             }
+            cp_async_commit();
+            cp_async_wait<0>();
         } else {
+            for (int j = threadIdx.x; j < cn; j += blockDim.x) ps[j] = __ldcg(pg + c0 + j);
             for (int x = threadIdx.x; x < cn * ni; x += blockDim.x) {
                 const int j = x / ni, k = x % ni;
                 vs[j * ipc + k] = __ldcg(V + static_cast<long long>(c0 + j) * D + i0 + k);
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
     PHASE();
 #ifdef SMOE_PHASES
     if (threadIdx.x == 0 && (b == 0 || s_last))
-        phase_print(s_last ? "attn split LAST [start, scores, softmax, flag wait, context]"
+        phase_print(s_last ? "attn split LAST [start, scores, exps, z, p, flag, context]"
                            : "attn split cta0 [start, scores, flag wait, context]", ph_, nph_);
 #endif
 }
