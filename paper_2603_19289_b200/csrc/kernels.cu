@@ -505,12 +505,12 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
         if (threadIdx.x == 0) {  // f64 partition in index order, as numerics.cpp:46-49
             double z = 0.0;
             int j = 0;
-            for (; j + 8 <= n; j += 8) {  // loads of a block in flight together, adds in order
-                double ev[8];
+            for (; j + 32 <= n; j += 32) {  // loads of a block in flight together, adds in order
+                double ev[32];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) ev[u] = es[j + u];
+                for (int u = 0; u < 32; ++u) ev[u] = es[j + u];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) z += ev[u];
+                for (int u = 0; u < 32; ++u) z += ev[u];
             }
             for (; j < n; ++j) z += es[j];
             zs = z;
