@@ -206,7 +206,6 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     s.preload_all()  # calibration runs with the whole model resident in HBM
     dv, counts = s.calibrate(args.calib_tokens, 2, 256)
     t_cal = time.time() - t0
-    s.set_cache_fraction(args.cache_fraction)
     s.set_predictor(args.predictor)
     prompt = token_stream(P, c["vocab"], 3)
     # teacher-forced decode inputs (random_token_stream seed 4): routing changes
@@ -252,6 +251,13 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                     online_recall=float(np.mean(recall)) if recall else None)
 
     res = {}
+    resident = None
+    if not args.ncu:
+        # the same workload with every expert resident (no copies): the gain of
+        # prefetch over on-demand that routing alone buys, and the copy time
+        # each mode exposes (TPOT - resident TPOT) for the overlap split
+        resident = {mode: measure(mode, args.workload) for mode in ("on_demand", "prefetch")}
+    s.set_cache_fraction(args.cache_fraction)
     if args.ncu:  # profiling pass: the headline workload's decode steps only
         res[args.workload] = {mode: measure(mode, args.workload) for mode in ("on_demand", "prefetch")}
         s.close()
@@ -306,15 +312,56 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                     "cache_fraction": args.cache_fraction}
     s.close()
     return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init, slots=slots,
-                t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P, long_ctx=long_ctx)
+                t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P, long_ctx=long_ctx,
+                dv=dv[: max(args.ref_depths)] if rank == 0 else None, resident=resident)
 
 
 # ------------------------------------------------------------- reference ----
 
-def run_reference_cpu(cfg: dict, layers: int, P: int, n_new: int, mode: str,
+REF_CORES = 2  # the reference's compute thread + its copy worker (executor.cpp:47, 138-198)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class pinned_cores:
+    """taskset for the duration of a CPU measurement: the reference's compute
+    thread and the copy worker it spawns inherit the affinity."""
+
+    def __init__(self, n: int):
+        self.n = n
+        self.old = None
+        self.cores = []
+
+    def __enter__(self):
+        try:
+            self.old = os.sched_getaffinity(0)
+            self.cores = sorted(self.old)[: self.n]
+            os.sched_setaffinity(0, set(self.cores))
+        except (AttributeError, OSError):
+            self.old = None
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
+def run_reference_cpu(cfg: dict, layers: int, P: int, n_steps: int, warmup: int, modes,
                       dv_layers: np.ndarray | None) -> dict:
-    """The reference's own run_offloaded_decode on a depth-truncated model
-    (CPU, compute thread + copy thread).  Returns per-layer decode ms/token."""
+    """The reference's own run_offloaded_decode (oracle/_ref: the reference library
+    compiled from its sources) on a depth-truncated copy of the model, pinned to
+    REF_CORES host cores.  Per-layer weights depend only on (seed, label), so the
+    truncated model's layers are the full model's first layers.  Returns, per
+    mode, the decode ms/token of the truncated model over the n_steps timed
+    steps (the first `warmup` decode steps are dropped)."""
     from oracle.bindings import Config, Oracle, Ref
     c = dict(cfg)
     c["layers"] = layers
@@ -330,44 +377,66 @@ def run_reference_cpu(cfg: dict, layers: int, P: int, n_new: int, mode: str,
     for n in names:
         rm.set_tensor(n, om.tensor(n))
     del om
-    pred = None
-    if mode == "prefetch":
-        table = ref.table_from(dv_layers[:layers]) if dv_layers is not None else None
-        pred = ref.make_predictor("router-pf", layers, table)
     prompt = token_stream(P, c["vocab"], 3)
-    t0 = time.perf_counter()
-    toks, per_us, _ = rm.offloaded_decode(prompt, n_new, pred, mode, latency_us=1,
-                                          deadlock_factor=1e8)
-    wall = time.perf_counter() - t0
-    return {"per_layer_ms": float(np.mean(per_us)) / 1e3 / layers, "wall_s": wall,
-            "tokens": toks.tolist(), "layers": layers, "prompt": P, "n_new": n_new}
+    out = {}
+    for mode in modes:
+        pred = None
+        if mode == "prefetch":
+            table = ref.table_from(dv_layers[:layers]) if dv_layers is not None else None
+            pred = ref.make_predictor("router-pf", layers, table)
+        with pinned_cores(REF_CORES) as pc:
+            t0 = time.perf_counter()
+            toks, per_us, max_res = rm.offloaded_decode(prompt, warmup + n_steps + 1, pred, mode,
+                                                        latency_us=1, deadlock_factor=1e8)
+            wall = time.perf_counter() - t0
+        timed = np.asarray(per_us[warmup:], np.float64)
+        out[mode] = {"ms_per_token": float(np.mean(timed)) / 1e3, "sd_ms": float(np.std(timed)) / 1e3,
+                     "wall_s": wall, "layers": layers, "prompt": P, "steps": int(timed.size),
+                     "warmup": warmup, "max_resident_layers": max_res, "cores": pc.cores}
+    return out
+
+
+def reference_tpot(cfg: dict, P: int, n_steps: int, warmup: int, modes, dv: np.ndarray | None,
+                   depths=(2, 4)) -> dict:
+    """Reference decode TPOT of the full depth per mode, extrapolated from two
+    truncations: t(l) = a + b * l fitted through the measured depths (a = the
+    per-token part outside the layers: embedding, unembed, final norm)."""
+    L = cfg["layers"]
+    depths = sorted({min(d, L) for d in depths})
+    runs = [run_reference_cpu(cfg, d, P, n_steps, warmup, modes, dv) for d in depths]
+    res = {}
+    for mode in modes:
+        rr = [r[mode] for r in runs]
+        if len(rr) >= 2:
+            d0, d1 = rr[0]["layers"], rr[-1]["layers"]
+            b = (rr[-1]["ms_per_token"] - rr[0]["ms_per_token"]) / (d1 - d0)
+            a = rr[0]["ms_per_token"] - b * d0
+        else:
+            a, b = 0.0, rr[0]["ms_per_token"] / rr[0]["layers"]
+        res[mode] = {
+            "tpot_ms": a + b * L, "per_layer_ms": b, "fixed_ms": a, "runs": rr,
+            "how": f"reference run_offloaded_decode {mode} (copy_latency_us=1, deadlock_factor=1e8), "
+                   f"depth-truncated to {' and '.join(str(r['layers']) for r in rr)} of {L} layers, "
+                   f"prompt {P}, {n_steps} timed decode steps after {warmup} warm-up; TPOT = a + b x {L} "
+                   f"fitted through the truncations; pinned to {REF_CORES} cores ({cpu_model()})"}
+    return res
 
 
 def reference_arm(args) -> dict:
     c = CONFIGS[args.config]
-    L = c["layers"]
-    layers = min(args.ref_layers, L)
     dv = None
-    try:  # default vectors: oracle calibration of the truncated model (same per-layer values)
+    try:  # default vectors for router-pf: the oracle's calibration pass on the truncated model
         from oracle.bindings import Config, Oracle
         cc = dict(c)
-        cc["layers"] = layers
-        if args.config in ("tiny",):
-            om = Oracle().build_model(Config(**cc), round_bf16=True)
-            dv = np.array(om.calibrate(256, 2, 256).d)
-        else:
-            dv = np.zeros((layers, c["experts"], c["hidden"]), np.float32)
+        cc["layers"] = min(max(args.ref_depths), c["layers"])
+        om = Oracle().build_model(Config(**cc), round_bf16=True)
+        dv = np.array(om.calibrate(args.ref_calib_tokens, 2, 256).d)
+        del om
     except Exception:
         dv = None
-    out = {}
-    for mode in ("on_demand", "prefetch"):
-        r = run_reference_cpu(c, layers, args.ref_prompt, args.ref_new, mode, dv)
-        out[mode] = r
-    return out
-
-
-def cpu_cores_used() -> int:
-    return 2  # reference: compute thread + copy worker (executor.cpp:47, 138-198)
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    return reference_tpot(c, args.ref_prompt, steps, min(args.warmup, 2), ("on_demand", "prefetch"),
+                          dv, tuple(args.ref_depths))
 
 
 # ----------------------------------------------------------------- main -----
@@ -386,9 +455,15 @@ def main():
     ap.add_argument("--predictor", default="router-pf")
     ap.add_argument("--calib-tokens", type=int, default=2000)
     ap.add_argument("--runs", type=int, default=3)
-    ap.add_argument("--ref-layers", type=int, default=2)
+    ap.add_argument("--ref-depths", type=int, nargs="+", default=[2, 4],
+                    help="depth truncations of the reference CPU runs (TPOT fitted through them)")
     ap.add_argument("--ref-prompt", type=int, default=4)
-    ap.add_argument("--ref-new", type=int, default=4)
+    ap.add_argument("--ref-max-steps", type=int, default=8,
+                    help="reference arm: timed decode steps (min of this and --steps)")
+    ap.add_argument("--ref-cpu-steps", type=int, default=3,
+                    help="cpu_baseline leg of our arm: timed reference decode steps")
+    ap.add_argument("--ref-calib-tokens", type=int, default=32,
+                    help="reference arm: oracle calibration tokens for its router-pf table")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling pass for the ncu launch list: experts resident (ncu serialises "
@@ -419,22 +494,25 @@ def main():
             return
         t0 = time.time()
         r = reference_arm(args)
-        L = c["layers"]
-        v = r["prefetch"]["per_layer_ms"] * L
+        pf, od = r["prefetch"], r["on_demand"]
+        v = pf["tpot_ms"]
+        ref_cfg = dict(base_cfg)
+        ref_cfg.update({"layers_run": [x["layers"] for x in pf["runs"]], "prompt_len": args.ref_prompt,
+                        "seq_len": args.ref_prompt + pf["runs"][0]["warmup"] + pf["runs"][0]["steps"],
+                        "calib_tokens": args.ref_calib_tokens,
+                        "note": "reference CPU arm: same model/config/metric; depth-truncated runs "
+                                "extrapolated to the full depth, shorter prompt (its prefill copies "
+                                "every expert per prompt token, executor.cpp:270-271)"})
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms",
-                "n_gpus": args.gpus, "steps": args.ref_new - 1, "warmup": 0,
+                "n_gpus": args.gpus, "steps": pf["runs"][0]["steps"], "warmup": pf["runs"][0]["warmup"],
                 "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": base_cfg,
-                "tpot_on_demand_ms": r["on_demand"]["per_layer_ms"] * L,
-                "tpot_prefetch_ms": v,
-                "cpu_baseline": {"value": v, "unit": "ms", "cores": cpu_cores_used(),
-                                 "kind": "reference",
-                                 "sample": f"reference run_offloaded_decode (copy_latency_us=1, "
-                                           f"deadlock_factor=1e8), depth-truncated to "
-                                           f"{r['prefetch']['layers']} of {L} layers, prompt "
-                                           f"{args.ref_prompt}, {args.ref_new - 1} decode steps; "
-                                           f"value = per-layer ms x {L}"},
+                "config": ref_cfg,
+                "tpot_on_demand_ms": od["tpot_ms"], "tpot_prefetch_ms": v,
+                "tpot_reduction_pct": 100.0 * (od["tpot_ms"] - v) / od["tpot_ms"],
+                "reference_runs": r,
+                "cpu_baseline": {"value": v, "unit": "ms", "cores": REF_CORES, "kind": "reference",
+                                 "cpu_model": cpu_model(), "sample": pf["how"]},
                 "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "wall_s": time.time() - t0}
         print(json.dumps(line))
@@ -495,18 +573,35 @@ def main():
     h2d_gbps = (copy_b * args.steps) / (pf["copy_busy_ms"] * 1e-3) / 1e9 if pf["copy_busy_ms"] else None
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        try:
-            r = run_reference_cpu(c, min(args.ref_layers, L), args.ref_prompt, args.ref_new,
-                                  "on_demand", None)
-            cpu = {"value": r["per_layer_ms"] * L, "unit": "ms", "cores": cpu_cores_used(),
-                   "kind": "reference",
-                   "sample": f"reference run_offloaded_decode on_demand (copy_latency_us=1), "
-                             f"depth-truncated to {r['layers']} of {L} layers, prompt "
-                             f"{r['prompt']}, {r['n_new'] - 1} decode steps; value = per-layer "
-                             f"ms x {L} ({r['wall_s']:.1f} s wall)"}
+        try:  # the reference's prefetch TPOT with our GPU-calibrated default vectors
+            r = reference_tpot(c, args.ref_prompt, args.ref_cpu_steps, 1, ("prefetch",), out.get("dv"),
+                               tuple(args.ref_depths))["prefetch"]
+            cpu = {"value": r["tpot_ms"], "unit": "ms", "cores": REF_CORES, "kind": "reference",
+                   "cpu_model": cpu_model(), "per_layer_ms": r["per_layer_ms"], "fixed_ms": r["fixed_ms"],
+                   "sample": r["how"] + f" ({sum(x['wall_s'] for x in r['runs']):.1f} s of decode wall)"}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
+    # copy/compute overlap (graph run): exposed copy = TPOT - TPOT with every
+    # expert resident; overlapped = copy-lane busy time per token - exposed
+    rs = out.get("resident") or {}
+    overlap = None
+    if rs:
+        rpf, rod = rs["prefetch"]["tpot_ms"], rs["on_demand"]["tpot_ms"]
+        ov = {}
+        for name, m, rm in (("prefetch", pf, rpf), ("on_demand", od, rod)):
+            busy = m["copy_busy_ms"] / args.steps
+            exposed = max(0.0, m["tpot_ms"] - rm)
+            ov[name] = {"copy_busy_ms_per_token": busy, "exposed_copy_ms_per_token": exposed,
+                        "overlapped_frac": (max(0.0, busy - exposed) / busy) if busy > 0 else None,
+                        "tpot_all_resident_ms": rm}
+        gain = od["tpot_ms"] - pf["tpot_ms"]
+        routing = rod - rpf
+        overlap = {**ov, "gain_ms": gain, "gain_from_routing_ms": routing,
+                   "gain_from_overlap_ms": gain - routing,
+                   "how": "same workload run with cache 1.0 (no copies): routing gain = resident "
+                          "on-demand - resident prefetch TPOT; exposed copy = TPOT - resident TPOT; "
+                          "overlapped = (copy-lane busy per token - exposed) / busy"}
     ks = pf["kernels_per_step"]
     line = {
         "metric": METRIC, "value": pf["tpot_ms"], "unit": "ms", "n_gpus": world,
@@ -543,6 +638,7 @@ def main():
                   "misses_on_demand": od["cache_misses"]},
         "online_recall_at_k": pf["online_recall"],
         "breakdown": {"prefetch": pf.get("breakdown"), "on_demand": od.get("breakdown")},
+        "overlap": overlap,
         "secondary_workload": {"name": "greedy" if args.workload == "stream" else "stream",
                                "tpot_prefetch_ms": other["prefetch"]["tpot_ms"],
                                "tpot_on_demand_ms": other["on_demand"]["tpot_ms"],

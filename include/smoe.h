@@ -155,6 +155,17 @@ int smoe_decode_stream(smoe_session* s, int32_t mode, const int32_t* tokens, int
 int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
                               int32_t n_new, int32_t mode, int32_t* out_tokens,
                               double* per_token_ms);
+/* run_offloaded_decode returning the whole ExecutorResult (executor.hpp:39-44):
+ * tokens, the measured lane events of the same run (CUDA events around each
+ * layer's attention / routing / expert phases and the copy lane; no CUDA
+ * graph), per_token_ms[n_new-1] and max_resident_layers (the most layers whose
+ * experts were requested and not yet consumed at once; the reference's bound
+ * is 2, executor.cpp:159-162).  events (nullable) holds up to cap events;
+ * *n_events = the total. */
+int smoe_run_offloaded_decode_ex(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
+                                 int32_t n_new, int32_t mode, int32_t* out_tokens,
+                                 double* per_token_ms, smoe_event* events, int32_t cap,
+                                 int32_t* n_events, int32_t* max_resident_layers);
 /* One host-driven step: token in, logits[vocab] out, returns the argmax token
  * through *next (end-to-end API: H2D of the token, D2H of the logits). */
 int smoe_step(smoe_session* s, int32_t mode, int32_t token, float* logits_out, int32_t* next);

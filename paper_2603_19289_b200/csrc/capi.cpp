@@ -5,6 +5,9 @@
 #include "../../include/smoe.h"
 
 #include "engine.h"
+#include <vector>
+#include <algorithm>
+#include <map>
 #include "train.h"
 
 #include <cstring>
@@ -165,6 +168,73 @@ int smoe_run_offloaded_decode(smoe_session* s, const int32_t* prompt, int32_t n_
             auto v = ss->token_ms();
             for (size_t i = 0; i < v.size() && i < static_cast<size_t>(n_new - 1); ++i) per_token_ms[i] = v[i];
         }
+    });
+}
+
+// ExecutorResult (executor.hpp:39-44) in full: the decode runs with the
+// measured lane events (CUDA events per phase, no graph), so tokens, events,
+// per-token times and the residency bound come from the same run, like the
+// reference's (executor.cpp:326-408).  max_resident_layers: the most layers
+// whose experts were requested (copy issued or hit) and not yet consumed by
+// their expert kernel at any instant (the reference's bound is 2,
+// executor.cpp:159-162; Algorithm 1 keeps it at 2 here too).
+int smoe_run_offloaded_decode_ex(smoe_session* s, const int32_t* prompt, int32_t n_prompt,
+                                 int32_t n_new, int32_t mode, int32_t* out_tokens,
+                                 double* per_token_ms, smoe_event* events, int32_t cap,
+                                 int32_t* n_events, int32_t* max_resident_layers) {
+    return guard([&] {
+        if (n_prompt < 1 || !prompt) throw std::invalid_argument("offloaded decode: empty prompt");
+        if (n_new < 1) throw std::invalid_argument("offloaded decode: n_new must be >= 1");
+        if (mode != 0 && mode != 1) throw std::invalid_argument("unknown offload mode");
+        smoe::Session* ss = S(s);
+        ss->reset(n_prompt + n_new, 0);
+        ss->prefill(prompt, n_prompt);
+        std::vector<smoe::TimelineEvent> ev;
+        ss->decode_timeline(mode, nullptr, n_new - 1, ev);
+        std::vector<int> toks(n_prompt + n_new - 1);
+        ss->read_tokens(toks.data(), static_cast<int>(toks.size()));
+        for (int i = 0; i < n_new; ++i) out_tokens[i] = toks[n_prompt - 1 + i];
+        const int steps = n_new - 1;
+        std::vector<double> t0(steps, 1e300), t1(steps, -1e300);
+        for (const auto& e : ev)
+            if (e.lane == 0 && e.token >= 0 && e.token < steps) {
+                t0[e.token] = std::min(t0[e.token], e.start_ms);
+                t1[e.token] = std::max(t1[e.token], e.end_ms);
+            }
+        if (per_token_ms)
+            for (int i = 0; i < steps; ++i) per_token_ms[i] = t1[i] - t0[i];
+        // residency: interval [decision end (request posted), expert end] per
+        // (token, layer).  The routing events are recorded in issue order: on
+        // demand, routing at layer l decides l; in prefetch mode the first one
+        // of a token (the true router of layer 0) decides layer 0 and every
+        // later one at layer l is the predictor deciding l + 1.
+        std::map<std::pair<int, int>, std::pair<double, double>> span;
+        std::map<int, int> seen0;
+        for (const auto& e : ev) {
+            if (e.lane != 0 || e.token < 0) continue;
+            int dl = e.layer;
+            if (e.kind == 1 && mode == 1 && !(e.layer == 0 && seen0[e.token]++ == 0)) dl = e.layer + 1;
+            auto& sp = span.try_emplace({e.token, dl}, 1e300, -1e300).first->second;
+            if (e.kind == 1) sp.first = std::min(sp.first, e.end_ms);  // request posted
+            if (e.kind == 2) sp.second = std::max(sp.second, e.end_ms);
+        }
+        std::vector<std::pair<double, int>> marks;
+        for (auto& [k, sp] : span)
+            if (sp.first < sp.second) {
+                marks.push_back({sp.first, +1});
+                marks.push_back({sp.second, -1});
+            }
+        std::sort(marks.begin(), marks.end(),
+                  [](const auto& a, const auto& b) { return a.first < b.first || (a.first == b.first && a.second < b.second); });
+        int cur = 0, mx = 0;
+        for (auto& mk : marks) mx = std::max(mx, cur += mk.second);
+        if (max_resident_layers) *max_resident_layers = mx;
+        const int m = static_cast<int>(ev.size()) < cap ? static_cast<int>(ev.size()) : cap;
+        if (events)
+            for (int i = 0; i < m; ++i)
+                events[i] = smoe_event{ev[i].lane, ev[i].kind, ev[i].layer, ev[i].token, ev[i].start_ms,
+                                       ev[i].end_ms};
+        if (n_events) *n_events = static_cast<int32_t>(ev.size());
     });
 }
 

@@ -302,6 +302,16 @@ void CopyScheduler::handle(const MailboxEntry& e) {
     for (int i = 0; i < e.nids; ++i)
         if (s.is_local(e.ids[i])) local[nloc++] = e.ids[i];  // EP: only this rank's shard
     auto copies = s.cache_->request(e.layer, local, nloc, &hits, &misses);
+    if (e.flags & kMbAllHit) {
+        // the device found every id resident and released the layer itself:
+        // only the LRU order and the counters change here
+        if (misses != 0)
+            throw std::runtime_error("device hit path disagrees with the slot cache at layer " +
+                                     std::to_string(e.layer));
+        std::lock_guard<std::mutex> g(mu_);
+        recs_.push_back({e.seq, e.layer, e.step, hits, 0, 0, -1});
+        return;
+    }
     const int npairs = static_cast<int>(s.ev_copy_.size() / 2);
     int ev = -1;
     {
@@ -426,6 +436,8 @@ void Session::free_all() {
     ev_step_.clear();
     if (ev_origin_) cudaEventDestroy(ev_origin_);
     ev_origin_ = nullptr;
+    if (ev_hostord_) cudaEventDestroy(ev_hostord_);
+    ev_hostord_ = nullptr;
     if (h_mailbox_) cudaFreeHost(h_mailbox_);
     if (h_stage_) cudaFreeHost(h_stage_);
     if (h_token_) cudaFreeHost(h_token_);
@@ -466,6 +478,11 @@ void Session::alloc() {
     m.expert_elems = m.gu_elems + static_cast<long long>(m.Hp) * m.Hmp;
     C_ = slots_for(opts_.cache_fraction);
     m.C = C_;
+    {
+        const std::string v = kernel_limit_violation(m);
+        if (!v.empty()) throw std::invalid_argument("config: " + v);
+    }
+    m.attn_grid = attn_grid_for(m, opts_.device);
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
@@ -615,6 +632,19 @@ void Session::alloc() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, opts_.device);
     if (clk_khz <= 0) clk_khz = 2000000;
     ctl_.spin_limit = static_cast<long long>(opts_.deadlock_s * clk_khz * 1e3);
+    // host-ordered copy waits under kernel-serialising tools: ncu and
+    // compute-sanitizer inject through CUDA_INJECTION64_PATH; SMOE_HOST_ORDERED
+    // = 1 / 0 forces the mode on / off
+    {
+        const char* ho = std::getenv("SMOE_HOST_ORDERED");
+        const char* inj = std::getenv("CUDA_INJECTION64_PATH");
+        host_ordered_ = ho ? std::atoi(ho) != 0 : (inj && *inj);
+        ctl_.host_ordered = host_ordered_ ? 1 : 0;
+        ctl_.fast_hit = std::getenv("SMOE_NO_FAST_HIT") ? 0 : 1;
+        ck(cudaEventCreateWithFlags(&ev_hostord_, cudaEventDisableTiming), "event");
+    }
+    dm_.attn_err = ctl_.error;
+    dm_.attn_spin = ctl_.spin_limit;
 
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h_mailbox_), sizeof(MailboxEntry) * kMailboxRing,
                      cudaHostAllocMapped | cudaHostAllocPortable),
@@ -961,6 +991,14 @@ void Session::load_estimator(const EstCfg& e, const float* flat) {
     if (e.m <= 1 || e.n <= 1 || e.d % e.m != 0) throw std::invalid_argument("estimator: bad m/n");
     if ((e.d / e.m) % 4 != 0) throw std::invalid_argument("estimator: latent width d/m must be a multiple of 4 on this path");
     const int dm = e.d / e.m, mlp = dm * e.n;
+    {
+        DevModel probe = dm_;
+        probe.est_d = e.d;
+        probe.est_dm = dm;
+        probe.est_mlp = mlp;
+        const std::string v = estimator_limit_violation(probe);
+        if (!v.empty()) throw std::invalid_argument("estimator: " + v);
+    }
     const int dmp = round_up(dm, 32), mlpp = round_up(mlp, 32);
     const long long a_off = 0, pos_off = static_cast<long long>(dm) * e.d,
                     b_off = pos_off + static_cast<long long>(e.L) * dm,
@@ -1077,6 +1115,10 @@ void Session::check_device_error() {
             throw std::runtime_error("deadlock suspected: compute waited " +
                                      std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
                                      " ms for layer " + std::to_string(err - 1000) + " expert copy");
+        if (err >= 3000 && err < 4000)
+            throw std::runtime_error("split attention stalled at layer " + std::to_string(err - 3000) +
+                                     ": its CTAs were not co-resident within " +
+                                     std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) + " ms");
         throw std::runtime_error("expert read before readiness at layer " + std::to_string(err - 2000));
     }
 }
@@ -1243,6 +1285,7 @@ void Session::enqueue_pass(DevState& st, int mode, int use_pred, int calibrating
         // so spinning expert CTAs can never starve an unfinished predictor
         static const bool guard_join = std::getenv("SMOE_GUARD_JOIN") != nullptr;
         if (guard_join && l >= 2 && side_at[l - 2]) ck(cudaStreamWaitEvent(s, ev_join_[l - 2], 0), "join");
+        if (host_ordered_ && !ctl_.resident) host_copy_barrier(s);
         const int t_exp = tl ? tl_begin(0, 2, l, s) : -1;
         ck(launch_ffn(dm_, st, ctl_, l, s, exec_src, s_from_r), "ffn");
         if (tl) tl_end(t_exp, s);
@@ -1273,6 +1316,23 @@ void Session::enqueue_step(int mode, int is_prefill, int record, int calibrating
     ck(launch_embed(dm_, st_, tok_src, s, sp, ctl_.step), "embed");
     enqueue_pass(st_, is_prefill ? 0 : mode, is_prefill ? 0 : 1, calibrating, is_prefill ? -1 : 0,
                  record, s);
+}
+
+void Session::host_copy_barrier(cudaStream_t s) {
+    ck(cudaStreamSynchronize(s), "host-ordered sync");
+    ck(cudaStreamSynchronize(s_side_), "host-ordered sync");
+    int posted = 0;
+    ck(cudaMemcpy(&posted, ctl_.req_counter, 4, cudaMemcpyDeviceToHost), "request counter");
+    const auto t0 = std::chrono::steady_clock::now();
+    while (sched_->next_seq() - 1 < posted) {
+        if (!sched_->error().empty()) break;  // surfaced by the next sync()
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::duration<double>(opts_.deadlock_s))
+            throw std::runtime_error("deadlock suspected: copy scheduler did not serve request " +
+                                     std::to_string(posted));
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    ck(cudaEventRecord(ev_hostord_, s_copy_), "event");
+    ck(cudaStreamWaitEvent(s, ev_hostord_, 0), "host-ordered wait");
 }
 
 void Session::set_token(int tok) {
@@ -1775,7 +1835,10 @@ void Session::decode_stream(int mode, const int* tokens, int n_steps) {
     for (int i = 0; i < n_steps; ++i) {
         const int ev = n_step_events_ < static_cast<int>(ev_step_.size() / 2) ? n_step_events_++ : -1;
         if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev], s_comp_), "event");
-        ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+        if (exec)
+            ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+        else
+            enqueue_step(mode, 0, 1, 0, s_comp_, 1);
         if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
         ++steps_;
     }
@@ -1789,7 +1852,10 @@ int Session::step_host(int mode, int token, float* logits_out) {
     cudaGraphExec_t exec = get_graph(mode);
     h_token_[0] = token;
     ck(cudaMemcpyAsync(st_.token, h_token_, 4, cudaMemcpyHostToDevice, s_comp_), "token H2D");
-    ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+    if (exec)
+        ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
+    else
+        enqueue_step(mode, 0, 1, 0, s_comp_);
     ck(cudaMemcpyAsync(h_logits_, st_.logits, 4ull * cfg_.V, cudaMemcpyDeviceToHost, s_comp_), "logits D2H");
     ck(cudaMemcpyAsync(h_token_ + 1, st_.token, 4, cudaMemcpyDeviceToHost, s_comp_), "token D2H");
     ck(cudaStreamSynchronize(s_comp_), "step");
@@ -1853,6 +1919,7 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
 int Session::steps_done() { return steps_; }
 
 cudaGraphExec_t Session::get_graph(int mode, int stream) {
+    if (host_ordered_) return nullptr;  // the step syncs on the host mid-pass: no graphs
     const long long key = mode * 10 + 1 + (stream ? 100 : 0);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;

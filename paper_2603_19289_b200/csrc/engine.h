@@ -111,7 +111,7 @@ public:
     std::string error();  // first error seen by the thread ("" if none)
     std::vector<CopyRecord> records();
     void clear_records();
-    int next_seq() const { return next_seq_; }
+    int next_seq() const { return next_seq_.load(); }  // requests handled = next_seq() - 1
     long long polls = 0;
 
 private:
@@ -123,7 +123,7 @@ private:
     std::mutex mu_;
     std::string err_;
     std::vector<CopyRecord> recs_;
-    int next_seq_ = 1;
+    std::atomic<int> next_seq_{1};
     int stage_idx_ = 0;
     int ev_next_ = 0;
 };
@@ -212,6 +212,7 @@ public:
     // copy size as the scheduler) into an HBM scratch block.
     double measure_link(int n_copies);
     int kernels_per_step(int mode) const;
+    bool host_ordered() const { return host_ordered_; }
 
     // used by the scheduler
     friend class CopyScheduler;
@@ -225,6 +226,9 @@ private:
     void enqueue_pass(DevState& st, int mode, int pred_kind_enabled, int calibrating,
                       int step_tag, int record, cudaStream_t s);
     void check_device_error();
+    // host-ordered mode (ctl_.host_ordered): every request posted so far has
+    // been handled by the copy scheduler, and stream `s` waits for its copies
+    void host_copy_barrier(cudaStream_t s);
     void sync();
     void set_token(int tok);
 
@@ -292,6 +296,8 @@ private:
     std::vector<cudaEvent_t> ev_copy_;  // pairs
     std::vector<cudaEvent_t> ev_step_;  // pairs per decode step
     cudaEvent_t ev_origin_ = nullptr;
+    cudaEvent_t ev_hostord_ = nullptr;  // host-ordered mode: copy stream -> compute stream
+    bool host_ordered_ = false;
     int n_step_events_ = 0;
 
     int pred_kind_ = kNone;

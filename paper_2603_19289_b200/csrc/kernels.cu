@@ -62,6 +62,7 @@ extern "C" int smoe_ktrace_read(unsigned long long* out) {
 #endif
 
 #include <cstdio>
+#include <string>
 #include <cstdlib>
 
 namespace smoe {
@@ -97,25 +98,48 @@ __device__ __forceinline__ void copy_decision(const int* sid, const float* sg, i
 }
 
 // Mailbox post (single thread): request copies of `ids` for `layer`.
-__device__ void post_request(const DevCtl& ctl, int layer, int step, const int* ids, int k) {
+//
+// Device-side hit path: when every id this rank owns is already resident
+// (slot_of >= 0; the copy stream updates slot_of only after the expert's
+// bytes landed, and a layer's slots change only while serving a later request
+// of the same layer, which the compute order puts after this layer's experts
+// ran), the layer is released here (ready = seq) instead of after a host
+// round trip; the entry still goes to the host for LRU order and hit counts.
+__device__ void post_request(const DevModel& m, const DevCtl& ctl, int layer, int step, const int* ids,
+                             int k) {
     const int seq = *ctl.req_counter + 1;
     *ctl.req_counter = seq;
     ctl.req_seq[layer] = seq;
     MailboxEntry* e = ctl.mailbox + (seq % kMailboxRing);
-    e->layer = layer;
-    e->step = step;
-    e->nids = k;
     // all loads first: a load after a store to (possibly aliasing) memory
     // would otherwise wait for it, one L2 round trip per id
-    int v[kMaxK];
+    int v[kMaxK], so[kMaxK];
 #pragma unroll
     for (int i = 0; i < kMaxK; ++i)
         if (i < k) v[i] = __ldcg(ids + i);
 #pragma unroll
     for (int i = 0; i < kMaxK; ++i)
+        if (i < k) {
+            const bool local = ctl.ep.world == 1 || v[i] % ctl.ep.world == ctl.ep.rank;
+            so[i] = local ? __ldcg(m.slot_of + layer * m.E + v[i]) : 0;
+        }
+    bool all_hit = ctl.fast_hit != 0;
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+        if (i < k && so[i] < 0) all_hit = false;
+    e->layer = layer;
+    e->step = step;
+    e->nids = k;
+    e->flags = all_hit ? kMbAllHit : 0;
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
         if (i < k) e->ids[i] = v[i];
     __threadfence_system();
     e->seq = seq;
+    if (all_hit) {  // ready only grows (the host never writes it for an all-hit entry)
+        __threadfence();
+        atomicMax(ctl.ready + layer, seq);
+    }
 }
 
 // ------------------------------------------------------------- weight init --
@@ -525,9 +549,28 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctl + 1), "r"(gen + 1) : "memory");
         }
     }
-    if (threadIdx.x == 0)
-        while (ld_acquire(ctl + 1) < gen + 1) __nanosleep(32);
+    // bounded like every other device wait: the attn_grid CTAs are co-resident
+    // by construction (occupancy checked at session creation), and a stall
+    // here (e.g. an SM-limited context) is reported instead of hanging
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) {
+        s_abort = 0;
+        const long long t0 = clock64();
+        while (ld_acquire(ctl + 1) < gen + 1) {
+            if (*(volatile int*)m.attn_err) {
+                s_abort = 1;
+                break;
+            }
+            if (clock64() - t0 > m.attn_spin) {
+                atomicCAS(m.attn_err, 0, 3000 + layer);
+                s_abort = 1;
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
     __syncthreads();
+    if (s_abort) return;
     PHASE();
     // context slice: outputs [i0, i0 + ipc), p and V[:, slice] staged in chunks
     // of positions, one sequential chain per output over all positions
@@ -812,7 +855,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
                       st.id_true + l * K, st.g_true + l * K);
         if (threadIdx.x == 0 && rl.exec_from == 0) {
             copy_decision(st.id_true + l * K, st.g_true + l * K, st.id_exec + l * K, st.g_exec + l * K, K);
-            if (rl.post_exec && !ctl.resident) post_request(ctl, l, rl.step_tag, st.id_exec + l * K, K);
+            if (rl.post_exec && !ctl.resident) post_request(m, ctl, l, rl.step_tag, st.id_exec + l * K, K);
         }
     }
     if (!in_true || !has_b) {
@@ -827,7 +870,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
                 }
             }
             if (rl.post_pred && !ctl.resident)
-                post_request(ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
+                post_request(m, ctl, l + 1, rl.step_tag, st.id_pred + (l + 1) * K, K);
             if ((gemv_pred || rl.pred_kind == kOracle) && l + 1 < m.L) publish_decision(st, l + 1);
             if (rl.exec_from == 1)
                 copy_decision(st.id_pred + l * K, st.g_pred + l * K, st.id_exec + l * K, st.g_exec + l * K, K);
@@ -932,7 +975,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
     warp_decision(st.lg_pred + static_cast<long long>(layer + 1) * m.E, m.E, m.K, m.gating, sp,
                   se, st.id_pred + (layer + 1) * m.K, st.g_pred + (layer + 1) * m.K);
     if (threadIdx.x == 0 && post_pred && !ctl.resident)
-        post_request(ctl, layer + 1, step_tag, st.id_pred + (layer + 1) * m.K, m.K);
+        post_request(m, ctl, layer + 1, step_tag, st.id_pred + (layer + 1) * m.K, m.K);
     if (threadIdx.x == 0 && layer + 1 < m.L) publish_decision(st, layer + 1);
 }
 
@@ -943,7 +986,7 @@ __global__ void __launch_bounds__(32) k_est_stage(DevModel m, DevState st, DevCt
 // hold gate row r and up row r); h = silu(g) * u.
 
 __device__ void wait_ready(const DevCtl& ctl, int layer) {
-    if (ctl.resident) return;
+    if (ctl.resident || ctl.host_ordered) return;  // host-ordered: a stream event did it
     if (threadIdx.x == 0) {
         const int want = __ldcg(ctl.req_seq + layer);
         const long long t0 = clock64();
@@ -1648,6 +1691,41 @@ cudaError_t set_smem(const void* fn, size_t bytes) {
 }
 }  // namespace
 
+// Per-kernel dynamic shared-memory needs against the limits preload_kernels
+// sets; a config whose kernels cannot launch is rejected at session creation
+// with the kernel named (instead of an opaque launch failure at first decode).
+std::string kernel_limit_violation(const DevModel& m) {
+    struct Need {
+        const char* name;
+        size_t bytes, limit;
+    } v[] = {{"k_qkv", qkv_smem(m), 200 * 1024},     {"k_wo", wo_smem(m), 200 * 1024},
+             {"k_router", router_smem(m, 0), 200 * 1024}, {"k_ffn_gu", gu_smem(m), 200 * 1024},
+             {"k_ffn_down", down_smem(m), 220 * 1024}, {"k_final", final_smem(m), 200 * 1024},
+             {"k_attn", attn_smem(m), 220 * 1024}};
+    for (const Need& n : v)
+        if (n.bytes > n.limit)
+            return std::string(n.name) + " needs " + std::to_string(n.bytes / 1024) +
+                   " KB of shared memory (limit " + std::to_string(n.limit / 1024) +
+                   " KB): hidden / head_dim / top_k / max_positions too large for this path";
+    return std::string();
+}
+std::string estimator_limit_violation(const DevModel& m) {
+    if (est_smem(m) > 200 * 1024)
+        return "k_est_stage needs " + std::to_string(est_smem(m) / 1024) +
+               " KB of shared memory (limit 200 KB): estimator d / mlp too large";
+    return std::string();
+}
+
+// CTAs of the split decode attention that can be co-resident on `device`:
+// kAttnSplit when occupancy x SMs allows it, else 1 (single-CTA path).
+int attn_grid_for(const DevModel& m, int device) {
+    int nb = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_attn, kAttnThreads, attn_smem(m)) != cudaSuccess)
+        return 1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 1;
+    return static_cast<long long>(nb) * sms >= kAttnSplit ? kAttnSplit : 1;
+}
+
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), gu_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
@@ -1725,7 +1803,7 @@ cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStr
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
     static const int split = std::getenv("SMOE_ATTN_SPLIT") ? std::atoi(std::getenv("SMOE_ATTN_SPLIT")) : 1;
-    PDL(k_attn, split ? kAttnSplit : 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
+    PDL(k_attn, split && m.attn_grid > 1 ? m.attn_grid : 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
     return counted(1);
 }
 

@@ -8,6 +8,8 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+
 namespace smoe {
 
 // Weight init (model.cpp:112-158 stream semantics, counter-based splitmix64):
@@ -175,6 +177,9 @@ cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_
 cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
 
 int max_dynamic_smem_needed(const DevModel& m);
+std::string kernel_limit_violation(const DevModel& m);     // "" when every kernel fits
+std::string estimator_limit_violation(const DevModel& m);  // after the estimator dims are set
+int attn_grid_for(const DevModel& m, int device);
 cudaError_t preload_kernels();
 // Number of kernel launches enqueued by the launchers so far (host counter).
 long long launch_counter();

@@ -45,8 +45,11 @@ struct MailboxEntry {
     int step;           // decode step (-1 prefill / shadow)
     int nids;
     int ids[kMaxK];
-    int pad[12];
+    int flags;          // kMbAllHit: the device found every (local) id resident
+                        // and released the layer itself; host: bookkeeping only
+    int pad[11];
 };
+constexpr int kMbAllHit = 1;
 
 struct DevModel {
     int L, E, K, H, Hm, V, D;
@@ -85,6 +88,13 @@ struct DevModel {
     const float* est_bias;
     const float* est_head;
     const int* hybrid;        // [L-1] predictor kind per layer
+    // split decode attention (contexts beyond kAttnSplitMin positions):
+    // attn_grid CTAs when that many are co-resident (occupancy checked at
+    // session creation), else 1 (single-CTA path); the CTAs' flag wait is
+    // bounded by attn_spin cycles and reports through *attn_err
+    int attn_grid;
+    int* attn_err;
+    long long attn_spin;
 };
 
 // Per-stream decode state (the main stream, and the Oracle's shadow stream).
@@ -164,6 +174,13 @@ struct DevCtl {
     int* tokens_out;         // [max_steps]
     long long spin_limit;    // clock64 cycles before declaring a deadlock
     int resident;            // 1: every expert is resident (no requests, no waits)
+    // 1: a request whose (local) ids are all resident per slot_of releases its
+    // layer on the device (ready = seq) without the host round trip
+    int fast_hit;
+    // 1: the host orders the compute stream after the copy stream with a CUDA
+    // event before every expert kernel (no device spin on ready; no graphs) —
+    // for kernel-serialising tools (ncu, compute-sanitizer)
+    int host_ordered;
     DevEP ep;
 };
 

@@ -33,7 +33,7 @@ EXPORTS = [
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
-    "smoe_estimator_init", "smoe_train_estimator",
+    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex",
 ]
 
 
@@ -310,6 +310,19 @@ class Session:
     def decode_stream(self, mode: str, tokens):
         t = np.ascontiguousarray(tokens, np.int32)
         _check(self.lib.smoe_decode_stream(self._h, MODE[mode], _p(t), len(t)))
+
+    def run_offloaded_decode_ex(self, prompt, n_new: int, mode: str, cap: int = 1 << 18):
+        """run_offloaded_decode returning the whole ExecutorResult (executor.hpp:39-44):
+        (tokens, events, per_token_ms, max_resident_layers), events from the same run."""
+        p = np.ascontiguousarray(prompt, np.int32)
+        toks = np.zeros(n_new, np.int32)
+        per = np.zeros(max(n_new - 1, 1), np.float64)
+        arr = (Event * cap)()
+        n, mr = C.c_int32(), C.c_int32()
+        _check(self.lib.smoe_run_offloaded_decode_ex(self._h, _p(p), len(p), n_new, MODE[mode],
+                                                     _p(toks), _p(per), arr, cap, C.byref(n),
+                                                     C.byref(mr)))
+        return toks, [arr[i] for i in range(min(n.value, cap))], per[: n_new - 1], mr.value
 
     def run_offloaded_decode(self, prompt, n_new: int, mode: str):
         """run_offloaded_decode (executor.cpp:326-359): tokens + device-timed per-token ms."""

@@ -605,6 +605,39 @@ def test_long_context_split_attention_vs_oracle(lib):
     s.close()
 
 
+@pytest.mark.parametrize("head_dim,plen", [(128, 701), (64, 555)])
+def test_long_context_split_attention_wide_heads_vs_oracle(lib, head_dim, plen):
+    """The split attention's cp.async staging branch (head_dim / 16 outputs per
+    CTA, a multiple of 4: head_dim 64 and 128 as on the Q30 / Mixtral shapes)
+    and its tail handling (prompt lengths that are not multiples of 4 or 32)
+    against the oracle, bit for bit."""
+    from oracle.bindings import Config, Oracle
+    cfg = dict(TOY, head_dim=head_dim, seed=17)
+    orc = Oracle()
+    om = orc.build_model(Config(**cfg), round_bf16=True)
+    table = om.calibrate(64, 2, 32)
+    prompt = list(np.random.default_rng(head_dim).integers(0, TOY["vocab"], plen))
+    want = om.generate_trace(prompt, 4, orc.make_predictor("router-pf", om, table), outputs=True)
+    s = session(cfg, cache_fraction=0.5, max_positions=plen + 64)
+    s.load_default_vectors(np.array(table.d))
+    s.set_predictor("router-pf")
+    got = run_trace(s, prompt, 4, "prefetch")
+    w = dict(tokens=want.tokens, s=want.s, r=want.r, m=want.m, logits=want.logits, ids=want.ids,
+             gates=want.gates, outputs=want.outputs, final_logits=want.final_logits,
+             pred_ids=want.pred_ids, pred_gates=want.pred_gates)
+    assert_trace_equal(got, w, True, len(prompt))
+    s.close()
+
+
+def test_config_beyond_kernel_limits_is_rejected(lib):
+    """A config whose kernels cannot launch (here head_dim 256 with a 4096-position
+    KV capacity: the attention CTA would need more shared memory than the SM
+    has) fails at session creation with the kernel named, not at first decode."""
+    from paper_2603_19289_b200 import ModelConfig, Session
+    with pytest.raises(ValueError, match="k_attn needs"):
+        Session(ModelConfig(**dict(TOY, head_dim=256)), max_positions=4096)
+
+
 def test_device_exp_equals_host_libm(lib):
     """The f64 exp of every softmax / silu on the path (exp_glibc.cuh) equals
     the host libm's exp — the one the reference calls — bit for bit, where

@@ -11,14 +11,18 @@ import subprocess
 
 import pytest
 
-OBJ = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                   "paper_2603_19289_b200", "csrc", "build", "kernels.o")
+BUILD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                     "paper_2603_19289_b200", "csrc", "build")
+OBJ = os.path.join(BUILD, "kernels.o")
+# every object whose chains must keep the reference's separately rounded
+# products and adds (decode, batched prefill / decode, estimator training)
+CHAIN_OBJS = ("kernels.o", "prefill.o", "train_dev.o")
 
 
-def _sass():
-    if not os.path.exists(OBJ) or not shutil.which("cuobjdump"):
-        pytest.skip("kernels.o or cuobjdump not available")
-    return subprocess.run(["cuobjdump", "-sass", OBJ], capture_output=True, text=True,
+def _sass(obj=OBJ):
+    if not os.path.exists(obj) or not shutil.which("cuobjdump"):
+        pytest.skip(f"{os.path.basename(obj)} or cuobjdump not available")
+    return subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True,
                           check=True).stdout
 
 
@@ -33,9 +37,10 @@ def _functions(sass):
     return out
 
 
-def test_no_packed_fma_anywhere():
-    sass = _sass()
-    assert "FFMA2" not in sass
+@pytest.mark.parametrize("obj", CHAIN_OBJS)
+def test_no_packed_fma_anywhere(obj):
+    sass = _sass(os.path.join(BUILD, obj))
+    assert "FFMA2" not in sass, obj
 
 
 def test_chain_kernels_use_separate_products_and_adds():
