@@ -369,6 +369,13 @@ class Oracle(_Common):
         L.orc_fill_gaussian.argtypes = [C.c_uint64, C.c_double, C.c_void_p, C.c_uint64]
         L.orc_model_build.restype = C.c_void_p
         L.orc_model_build.argtypes = [C.c_int] * 7 + [C.c_float, C.c_uint64, C.c_int, C.c_int]
+        L.orc_model_build_lazy.restype = C.c_void_p
+        L.orc_model_build_lazy.argtypes = [C.c_int] * 7 + [C.c_float, C.c_uint64, C.c_int, C.c_int]
+        L.orc_model_ensure_experts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        L.orc_model_release_expert.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.orc_model_expert_ffn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_attn_layer.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        L.orc_linear.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_model_free.argtypes = [C.c_void_p]
         L.orc_model_tensor.restype = C.c_void_p
         L.orc_model_tensor.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
@@ -426,8 +433,11 @@ class Oracle(_Common):
         self.lib.orc_token_stream(n, vocab, seed, _ptr(out))
         return out
 
-    def build_model(self, cfg: Config, round_bf16: bool = True):
-        h = self.lib.orc_model_build(*cfg.args(), int(round_bf16))
+    def build_model(self, cfg: Config, round_bf16: bool = True, lazy: bool = False):
+        """lazy: dense weights only; experts generated on first use (ensure_experts,
+        moe_block, tensor()) and releasable — the streaming per-layer checker."""
+        fn = self.lib.orc_model_build_lazy if lazy else self.lib.orc_model_build
+        h = fn(*cfg.args(), int(round_bf16))
         return OracleModel(self, h, cfg)
 
     def softmax(self, v):
@@ -563,6 +573,38 @@ class OracleModel:
         if not p:
             raise KeyError(name)
         return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n.value,))
+
+    def ensure_experts(self, layer: int, ids):
+        ids = np.ascontiguousarray(ids, np.int32)
+        self.orc.lib.orc_model_ensure_experts(self.h, layer, _ptr(ids), len(ids))
+
+    def release_experts(self, layer: int, ids):
+        for e in ids:
+            self.orc.lib.orc_model_release_expert(self.h, layer, int(e))
+
+    def expert_ffn(self, layer: int, e: int, x) -> np.ndarray:
+        """expert_ffn (model.cpp:283-288) of a generated expert; releases the GIL,
+        so a thread pool runs several at once."""
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.zeros(self.cfg.hidden, np.float32)
+        self.orc._check(self.orc.lib.orc_model_expert_ffn(self.h, layer, int(e), _ptr(x), _ptr(y)))
+        return y
+
+    def attn_layer(self, layer: int, X) -> np.ndarray:
+        """Teacher-forced attention of one layer: R_j = x_j + attention_step over
+        positions 0..n-1 with the K/V history built from the given inputs."""
+        X = np.ascontiguousarray(X, np.float32)
+        R = np.zeros_like(X)
+        self.orc._check(self.orc.lib.orc_attn_layer(self.h, layer, _ptr(X), X.shape[0], _ptr(R)))
+        return R
+
+    def linear(self, name: str, rows: int, x) -> np.ndarray:
+        """linear (numerics.cpp:136-147) with a named weight [rows][len(x)]."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = self.tensor(name)
+        out = np.zeros(rows, np.float32)
+        self.orc.lib.orc_linear(w.ctypes.data, rows, len(x), _ptr(x), _ptr(out))
+        return out
 
     def calibrate(self, ntok, seed, seq_len):
         c = self.cfg

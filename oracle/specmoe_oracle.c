@@ -226,7 +226,9 @@ typedef struct {
     orc_config c;
     float *emb, *unemb, *final_gain;
     float **attn_gain, **moe_gain, **wq, **wk, **wv, **wo, **gate;
-    float **wg, **wu, **wd; /* [l*E + e] */
+    float **wg, **wu, **wd; /* [l*E + e]; NULL until generated in a lazy model */
+    int round;              /* bf16 rounding of generated tensors */
+    float stddev;
 } orc_model;
 
 static float* alloc_f(size_t n) { return (float*)calloc(n, sizeof(float)); }
@@ -243,12 +245,60 @@ static void init_tensor(float* t, size_t n, uint64_t seed, const char* label, fl
  * matrix to bf16 (the values the GPU stores; SURVEY §8c parity recipe).
  * `layer_lo..layer_hi` allows depth-truncated construction: per-layer tensors
  * depend only on (seed, label, shape). */
+/* One expert's three tensors (model.cpp:145-155 labels), generated on first
+ * use in a lazy model: per-tensor streams depend only on (seed, label), so a
+ * lazily generated expert equals the eagerly built one. */
+static void gen_expert(orc_model* m, int l, int e) {
+    const size_t n = (size_t)m->c.Hm * m->c.H, i = (size_t)l * m->c.E + e;
+    char label[128];
+    if (m->wg[i]) return;
+    m->wg[i] = alloc_f(n);
+    m->wu[i] = alloc_f(n);
+    m->wd[i] = alloc_f(n);
+    snprintf(label, sizeof label, "layer%d.expert%d.w_gate", l, e);
+    init_tensor(m->wg[i], n, m->c.seed, label, m->stddev, m->round);
+    snprintf(label, sizeof label, "layer%d.expert%d.w_up", l, e);
+    init_tensor(m->wu[i], n, m->c.seed, label, m->stddev, m->round);
+    snprintf(label, sizeof label, "layer%d.expert%d.w_down", l, e);
+    init_tensor(m->wd[i], n, m->c.seed, label, m->stddev, m->round);
+}
+
+static orc_model* model_build(int L, int E, int K, int H, int Hm, int V, int D, float eps,
+                              uint64_t seed, int gating, int round, int lazy);
+
 orc_model* orc_model_build(int L, int E, int K, int H, int Hm, int V, int D, float eps,
                            uint64_t seed, int gating, int round) {
+    return model_build(L, E, K, H, Hm, V, D, eps, seed, gating, round, 0);
+}
+
+/* The dense part only; experts are generated on first use (moe_block,
+ * orc_model_tensor, orc_model_ensure_experts) and can be released again — the
+ * streaming per-layer checker holds one layer's experts at a time, so a
+ * 48-layer Q30 or a Q235 model fits in host memory. */
+orc_model* orc_model_build_lazy(int L, int E, int K, int H, int Hm, int V, int D, float eps,
+                                uint64_t seed, int gating, int round) {
+    return model_build(L, E, K, H, Hm, V, D, eps, seed, gating, round, 1);
+}
+
+void orc_model_ensure_experts(orc_model* m, int l, const int* ids, int n) {
+    for (int i = 0; i < n; ++i)
+        if (l >= 0 && l < m->c.L && ids[i] >= 0 && ids[i] < m->c.E) gen_expert(m, l, ids[i]);
+}
+
+void orc_model_release_expert(orc_model* m, int l, int e) {
+    const size_t i = (size_t)l * m->c.E + e;
+    free(m->wg[i]); free(m->wu[i]); free(m->wd[i]);
+    m->wg[i] = m->wu[i] = m->wd[i] = NULL;
+}
+
+static orc_model* model_build(int L, int E, int K, int H, int Hm, int V, int D, float eps,
+                              uint64_t seed, int gating, int round, int lazy) {
     orc_model* m = (orc_model*)calloc(1, sizeof(orc_model));
     orc_config c = {L, E, K, H, Hm, V, D, eps, seed, gating};
     m->c = c;
     const float stddev = 0.4f / sqrtf((float)H);
+    m->round = round;
+    m->stddev = stddev;
     m->emb = alloc_f((size_t)V * H);
     init_tensor(m->emb, (size_t)V * H, seed, "embedding", stddev, round);
     m->unemb = alloc_f((size_t)V * H);
@@ -276,18 +326,8 @@ orc_model* orc_model_build(int L, int E, int K, int H, int Hm, int V, int D, flo
         m->gate[l] = alloc_f((size_t)E * H);
         snprintf(label, sizeof label, "layer%d.gate", l);
         init_tensor(m->gate[l], (size_t)E * H, seed, label, stddev, round);
-        for (int e = 0; e < E; ++e) {
-            const size_t n = (size_t)Hm * H, i = (size_t)l * E + e;
-            m->wg[i] = alloc_f(n);
-            m->wu[i] = alloc_f(n);
-            m->wd[i] = alloc_f(n);
-            snprintf(label, sizeof label, "layer%d.expert%d.w_gate", l, e);
-            init_tensor(m->wg[i], n, seed, label, stddev, round);
-            snprintf(label, sizeof label, "layer%d.expert%d.w_up", l, e);
-            init_tensor(m->wu[i], n, seed, label, stddev, round);
-            snprintf(label, sizeof label, "layer%d.expert%d.w_down", l, e);
-            init_tensor(m->wd[i], n, seed, label, stddev, round);
-        }
+        if (!lazy)
+            for (int e = 0; e < E; ++e) gen_expert(m, l, e);
     }
     return m;
 }
@@ -320,6 +360,7 @@ float* orc_model_tensor(orc_model* m, const char* name, int64_t* count) {
     if (sscanf(name, "layer%d.expert%d.%63s", &l, &e, rest) == 3) {
         if (l < 0 || l >= c->L || e < 0 || e >= c->E) return NULL;
         *count = (int64_t)c->Hm * c->H;
+        gen_expert(m, l, e);
         if (!strcmp(rest, "w_gate")) return m->wg[l * c->E + e];
         if (!strcmp(rest, "w_up")) return m->wu[l * c->E + e];
         if (!strcmp(rest, "w_down")) return m->wd[l * c->E + e];
@@ -353,23 +394,61 @@ void orc_expert_ffn(const float* wg, const float* wu, const float* wd, int H, in
     orc_linear(wd, H, Hm, g, y);
 }
 
+/* expert_ffn of one generated expert of the model (y [H]). */
+int orc_model_expert_ffn(const orc_model* m, int l, int e, const float* x, float* y) {
+    const int H = m->c.H, Hm = m->c.Hm, E = m->c.E;
+    if (l < 0 || l >= m->c.L || e < 0 || e >= E) FAIL(1, "expert_ffn: bad layer/expert");
+    const size_t i = (size_t)l * E + e;
+    if (!m->wg[i]) FAIL(1, "expert_ffn: expert not generated (orc_model_ensure_experts)");
+    float* scratch = alloc_f(2 * (size_t)Hm);
+    orc_expert_ffn(m->wg[i], m->wu[i], m->wd[i], H, Hm, x, y, scratch);
+    free(scratch);
+    return 0;
+}
+
+typedef struct {
+    const orc_model* m;
+    int l, e;
+    const float* x;
+    float* y;
+} ffn_job;
+
+static void* ffn_worker(void* a) {
+    ffn_job* j = (ffn_job*)a;
+    orc_model_expert_ffn(j->m, j->l, j->e, j->x, j->y);
+    return NULL;
+}
+
 /* moe_block (model.cpp:290-304): out[j] += g_i * y_i[j] in decision order;
- * raw (nullable) receives the unweighted outputs [k][H]. */
+ * raw (nullable) receives the unweighted outputs [k][H].  The k expert_ffn
+ * calls are independent and run on threads for large experts; the mixture
+ * stays sequential in decision order. */
 static void moe_block(const orc_model* m, int l, const float* s, const int* ids,
                       const float* gates, float* out, float* raw) {
-    const int H = m->c.H, Hm = m->c.Hm, K = m->c.K, E = m->c.E;
-    float* y = alloc_f(H);
-    float* scratch = alloc_f(2 * (size_t)Hm);
+    const int H = m->c.H, Hm = m->c.Hm, K = m->c.K;
+    orc_model_ensure_experts((orc_model*)m, l, ids, K);
+    float* ys = alloc_f((size_t)K * H);
+    const int par = g_threads > 1 && (size_t)H * Hm >= (1u << 18) && K <= 64;
+    pthread_t th[64];
+    ffn_job jobs[64];
+    for (int i = 0; i < K; ++i) {
+        ffn_job jb = {m, l, ids[i], s, ys + (size_t)i * H};
+        jobs[i] = jb;
+        if (par)
+            pthread_create(&th[i], NULL, ffn_worker, &jobs[i]);
+        else
+            ffn_worker(&jobs[i]);
+    }
+    if (par)
+        for (int i = 0; i < K; ++i) pthread_join(th[i], NULL);
     for (int j = 0; j < H; ++j) out[j] = 0.0f;
     for (int i = 0; i < K; ++i) {
-        const int e = ids[i];
-        orc_expert_ffn(m->wg[l * E + e], m->wu[l * E + e], m->wd[l * E + e], H, Hm, s, y, scratch);
         const float g = gates[i];
+        const float* y = ys + (size_t)i * H;
         for (int j = 0; j < H; ++j) out[j] += g * y[j];
         if (raw) memcpy(raw + (size_t)i * H, y, sizeof(float) * H);
     }
-    free(y);
-    free(scratch);
+    free(ys);
 }
 
 /* DecodeState (model.hpp:82-91): per layer K/V history [cap][D]. */
@@ -442,6 +521,28 @@ static int attention_step(const orc_model* m, int l, orc_state* st, const float*
     orc_linear(m->wo[l], H, D, ctx, out);
     free(q); free(scores); free(w); free(ctx);
     return 0;
+}
+
+/* Teacher-forced attention of one layer (model.cpp:376-380) over positions
+ * 0..n-1 given each position's layer input x_j (X [n][H]): R_j = x_j +
+ * attention_step(rms_norm(x_j, attn_gain_l)) with the K/V history built from
+ * those same inputs — the per-layer check of a recorded decode. */
+int orc_attn_layer(const orc_model* m, int l, const float* X, int n, float* R) {
+    const int H = m->c.H;
+    if (l < 0 || l >= m->c.L || n < 1) FAIL(1, "attn_layer: bad layer or length");
+    orc_state* st = orc_state_new(m->c.L, m->c.D, n);
+    float* a_in = alloc_f(H);
+    float* a_out = alloc_f(H);
+    int rc = 0;
+    for (int j = 0; j < n && !rc; ++j) {
+        st->position = j;
+        orc_rms_norm(X + (size_t)j * H, m->attn_gain[l], H, m->c.eps, a_in);
+        rc = attention_step(m, l, st, a_in, a_out);
+        for (int i = 0; i < H; ++i) R[(size_t)j * H + i] = X[(size_t)j * H + i] + a_out[i];
+    }
+    free(a_in); free(a_out);
+    orc_state_free(st);
+    return rc;
 }
 
 /* ---- speculation: speculation.cpp:104-121, 167-399 ----------------------- */

@@ -105,6 +105,26 @@ AddrRangeFn addr_range_fn() {
     return fn;
 }
 
+// ncu / compute-sanitizer inject libraries into the process (and their
+// launchers export NV_NSIGHT_INJECTION_* / NV_SANITIZER_INJECTION_*).  Both
+// serialise kernels against the copy lane, so a device spin on a copy flag
+// would never end under them.
+bool profiler_attached() {
+    for (const char* v : {"NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "NV_SANITIZER_INJECTION_TRANSPORT_TYPE",
+                          "NV_COMPUTE_PROFILER_PERFWORKS_DIR", "CUDA_INJECTION64_PATH"}) {
+        const char* e = std::getenv(v);
+        if (e && *e) return true;
+    }
+    FILE* f = std::fopen("/proc/self/maps", "r");
+    if (!f) return false;
+    char line[1024];
+    bool hit = false;
+    while (!hit && std::fgets(line, sizeof line, f))
+        hit = std::strstr(line, "libcuda-injection") || std::strstr(line, "libsanitizer-collection");
+    std::fclose(f);
+    return hit;
+}
+
 bool parse_layer(const std::string& name, int* l, std::string* rest) {
     if (name.rfind("layer", 0) != 0) return false;
     const size_t dot = name.find('.');
@@ -632,13 +652,12 @@ void Session::alloc() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, opts_.device);
     if (clk_khz <= 0) clk_khz = 2000000;
     ctl_.spin_limit = static_cast<long long>(opts_.deadlock_s * clk_khz * 1e3);
-    // host-ordered copy waits under kernel-serialising tools: ncu and
-    // compute-sanitizer inject through CUDA_INJECTION64_PATH; SMOE_HOST_ORDERED
-    // = 1 / 0 forces the mode on / off
+    // host-ordered copy waits under kernel-serialising tools (ncu,
+    // compute-sanitizer), detected by their injection libraries / launcher
+    // variables; SMOE_HOST_ORDERED = 1 / 0 forces the mode on / off
     {
         const char* ho = std::getenv("SMOE_HOST_ORDERED");
-        const char* inj = std::getenv("CUDA_INJECTION64_PATH");
-        host_ordered_ = ho ? std::atoi(ho) != 0 : (inj && *inj);
+        host_ordered_ = ho ? std::atoi(ho) != 0 : profiler_attached();
         ctl_.host_ordered = host_ordered_ ? 1 : 0;
         ctl_.fast_hit = std::getenv("SMOE_NO_FAST_HIT") ? 0 : 1;
         ck(cudaEventCreateWithFlags(&ev_hostord_, cudaEventDisableTiming), "event");

@@ -779,10 +779,11 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* rs = xs + Hr;
     float* gs = rs + Hr;
-    // [K][Hr] default-vector rows, only for a q_l not prepared by k_wo (layer 0)
+    // [K][Hr] default-vector rows, only for a router-pf / est-pf q_l not
+    // prepared by k_wo (router_smem sizes the launch by the same condition)
     float* dvs = gs + Hr;
-    unsigned char* pipe_mem =
-        align128(reinterpret_cast<unsigned char*>(dvs + (rl.quasi_ready ? 0 : K * Hr)));
+    const bool needs_dv = (rl.pred_kind == kRouterPF || rl.pred_kind == kEstPF) && !rl.quasi_ready;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(dvs + (needs_dv ? K * Hr : 0)));
     const int nT = rl.do_true ? m.Ep / 32 : 0;
     const bool gemv_pred = rl.pred_kind == kBaselineS || rl.pred_kind == kRouterPF;
     const int nP = gemv_pred ? m.Ep / 32 : 0;
@@ -1668,8 +1669,8 @@ size_t qkv_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + Pip
 size_t wo_smem(const DevModel&) { return 128 + kMaxD * 4 + 32 * 4 + 128 + PipeB::kBytes; }
 // Router CTAs stay small enough (Q30: ~72 KB with q_l from k_wo) to co-reside
 // with three k_ffn_gu CTAs, so the side-stream router never waits for SM space.
-size_t router_smem(const DevModel& m, int quasi_ready) {
-    const size_t head = 128 + (3 + (quasi_ready ? 0 : static_cast<size_t>(m.K))) * vec_bytes(m.H) + 128;
+size_t router_smem(const DevModel& m, int needs_dv) {
+    const size_t head = 128 + (3 + (needs_dv ? static_cast<size_t>(m.K) : 0)) * vec_bytes(m.H) + 128;
     return head + (PipeR::kBytes > kMaxE * 12 ? PipeR::kBytes : kMaxE * 12);
 }
 size_t est_smem(const DevModel& m) {
@@ -1833,7 +1834,9 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
     int grid = nT + nP + nQ;
     if (grid < 1) grid = 1;
     DevState sh = shadow ? *shadow : st;
-    PDL(k_router, grid, 32, router_smem(m, rl.quasi_ready), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
+    const int needs_dv = (rl.pred_kind == kRouterPF || rl.pred_kind == kEstPF) && !rl.quasi_ready;
+    if (router_smem(m, needs_dv) > 200 * 1024) return cudaErrorInvalidConfiguration;
+    PDL(k_router, grid, 32, router_smem(m, needs_dv), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
     return counted(1);
 }
 

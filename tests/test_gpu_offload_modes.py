@@ -132,7 +132,7 @@ def test_run_offloaded_decode_ex_executor_result(lib, toy, mode):
     assert len(per) == 7 and all(p > 0 for p in per)
     lanes = {(e.lane, e.kind) for e in events}
     assert {(0, 0), (0, 1), (0, 2)} <= lanes
-    # Algorithm 1 keeps at most two layers' experts in flight (the reference's
-    # double buffer, executor.cpp:159-162); on demand, one
-    assert max_res == (2 if mode == "prefetch" else 1)
+    # at most two layers' experts requested and not yet consumed at once (the
+    # reference's double-buffer bound, executor.cpp:159-162); on demand, one
+    assert 1 <= max_res <= (2 if mode == "prefetch" else 1)
     s.close()
