@@ -295,6 +295,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         tok = nxt
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     slots = s.cache_slots()
+    path = s.path_info()
     # long context (PAPER.md:423 prompts of 1k-64k tokens): the prompt through the
     # batched prefill, then the headline stream workload
     long_ctx = None
@@ -313,7 +314,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     s.close()
     return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init, slots=slots,
                 t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P, long_ctx=long_ctx,
-                dv=dv[: max(args.ref_depths)] if rank == 0 else None, resident=resident)
+                dv=dv[: max(args.ref_depths)] if rank == 0 else None, resident=resident, path=path)
 
 
 # ------------------------------------------------------------- reference ----
@@ -560,10 +561,16 @@ def main():
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    # dominant kernel: expert gate/up GEMV; algorithmic bytes per launch = K experts x
-    # gate+up bf16 weights + K x H f32 input reads are negligible
-    gu_bytes = K * 2 * Hm * H * 2
-    gu_us = prof["ffn_gate_up"]
+    # dominant kernel: the expert FFN.  Fused (one launch per layer, k_ffn): K
+    # experts x gate+up+down bf16 weights per launch; split: the gate/up GEMV,
+    # K experts x gate+up weights.  Activation reads (K x H f32) are negligible.
+    fused = bool(out.get("path", {}).get("ffn_fused"))
+    if fused:
+        gu_name, gu_bytes, gu_us = "k_ffn", K * 3 * Hm * H * 2, prof["ffn"]
+        gu_desc = "k_ffn (fused expert FFN: gate/up + down GEMV, one launch per layer)"
+    else:
+        gu_name, gu_bytes, gu_us = "k_ffn_gu", K * 2 * Hm * H * 2, prof["ffn_gate_up"]
+        gu_desc = "k_ffn_gu (expert gate+up GEMV)"
     achieved = gu_bytes / (gu_us * 1e-6) / 1e9
     hb = hbm_bytes_per_token(c, out["P"])
     link = out["link"]
@@ -625,14 +632,15 @@ def main():
                           "on_demand_frac": t_roof_od / od["tpot_ms"],
                           "hbm_bytes_per_token": hb["total"], "hbm_peak_GBps": hbm_peak,
                           "formula": "max(copy_bytes/link_peak, hbm_bytes/hbm_peak)"},
-        "roofline": {"bound": "hbm", "kernel": "k_ffn_gu (expert gate+up GEMV)",
+        "roofline": {"bound": "hbm", "kernel": gu_desc,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("k_ffn_gu"),
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(gu_name),
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
                                        "dram__bytes_read.sum + dram__bytes_write.sum per launch)",
                      "bytes_per_launch": gu_bytes, "avg_launch_us": gu_us,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
         "kernel_us": prof,
+        "path": out.get("path"),
         "cache": {"slots_per_layer": out.get("slots"), "hits_prefetch": pf["cache_hits"],
                   "misses_prefetch": pf["cache_misses"], "hits_on_demand": od["cache_hits"],
                   "misses_on_demand": od["cache_misses"]},

@@ -251,8 +251,10 @@ int smoe_preload_all(smoe_session* s);
 int smoe_clear_stats(smoe_session* s);
 /* Average device time (us) per launch of each per-layer kernel, CUDA events on
  * the compute stream over L back-to-back launches (one per layer, weights
- * larger than L2), `reps` repetitions.  out_us[7]: qkv, attn, wo, router,
- * ffn_gate_up, ffn_down, final.  Needs a completed decode step (resident experts). */
+ * larger than L2), `reps` repetitions.  out_us[8]: qkv, attn, wo, router,
+ * ffn_gate_up, ffn_down, final, ffn (the whole expert FFN as decode launches
+ * it: the one-launch fused kernel when active, else gate/up + down).  Needs a
+ * completed decode step (resident experts). */
 int smoe_profile_kernels(smoe_session* s, int32_t reps, double* out_us);
 /* H2D GB/s of expert-sized copies from the pinned store into HBM. */
 int smoe_measure_link(smoe_session* s, int32_t n_copies, double* gbps);
@@ -293,6 +295,12 @@ int smoe_breakdown(const smoe_event* events, int32_t n, double* mean_fractions3,
 /* recall_at_k (metrics.cpp:9-20) and rank_alignment (metrics.cpp:22-28). */
 int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, double* recall,
                      int32_t* rank_match);
+
+/* Which variants this session runs: out[0] expert FFN fused into one launch
+ * (1) or gate/up + down kernels (0); out[1] split-attention CTAs; out[2]
+ * host-ordered copy waits (profiler / sanitizer attached or
+ * SMOE_HOST_ORDERED=1); out[3] device-side all-hit release. */
+int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap);
 
 /* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap);

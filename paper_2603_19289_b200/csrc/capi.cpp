@@ -355,6 +355,10 @@ int smoe_timeline(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t 
     });
 }
 
+int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap) {
+    return guard([&] { S(s)->path_info(out, cap); });
+}
+
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->debug_state(out, cap); });
 }

@@ -503,6 +503,7 @@ void Session::alloc() {
         if (!v.empty()) throw std::invalid_argument("config: " + v);
     }
     m.attn_grid = attn_grid_for(m, opts_.device);
+    m.ffn_fused = std::getenv("SMOE_FUSED_FFN") ? ffn_fused_ok(m, opts_.device) : 0;
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
@@ -1958,6 +1959,11 @@ cudaGraphExec_t Session::get_graph(int mode, int stream) {
 
 // Kernels in one captured decode step: the teacher-forced (stream) graph if
 // it was built, else the greedy one; -1 before any graph exists.
+void Session::path_info(int* out, int cap) const {
+    const int v[] = {dm_.ffn_fused, dm_.attn_grid, host_ordered_ ? 1 : 0, ctl_.fast_hit};
+    for (int i = 0; i < cap && i < 4; ++i) out[i] = v[i];
+}
+
 int Session::kernels_per_step(int mode) const {
     for (const long long key : {mode * 10 + 1 + 100LL, mode * 10 + 1LL}) {
         auto it = graph_kernels_.find(key);
@@ -2016,6 +2022,7 @@ void Session::profile_kernels(int reps, double* out) {
         const double n = k == 6 ? reps : static_cast<double>(reps) * L;
         out[k] = 1000.0 * ms / n;
     }
+    out[7] = out[4];  // the expert FFN as decode launches it (one fused launch when active)
     // split the FFN pair with a gate/up-only and down-only timing
     {
         ck(cudaEventRecord(a, s_comp_), "event");

@@ -206,13 +206,16 @@ public:
     // Average device time (us) per launch of each per-layer kernel, timed with
     // CUDA events on the compute stream over L back-to-back launches (one per
     // layer, so the streamed weights exceed L2), repeated `reps` times.
-    // out[7]: qkv, attn, wo, router, ffn_gate_up, ffn_down, final.
+    // out[8]: qkv, attn, wo, router, ffn_gate_up, ffn_down, final, ffn (the expert FFN
+    // as decode launches it: one fused launch when active, else gate/up + down).
     void profile_kernels(int reps, double* out);
     // H2D GB/s of expert-sized copies from the pinned store (same allocation and
     // copy size as the scheduler) into an HBM scratch block.
     double measure_link(int n_copies);
     int kernels_per_step(int mode) const;
     bool host_ordered() const { return host_ordered_; }
+    // {expert FFN fused into one launch, split-attention CTAs, host-ordered copy waits, device hit path}
+    void path_info(int* out, int cap) const;
 
     // used by the scheduler
     friend class CopyScheduler;

@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
 // SMOE_DOWN_L2=1: k_ffn_gu warms L2 with the down-projection blocks (measured
 // neutral on Q30: down gets faster, gate/up slower by as much)
 __device__ int g_down_l2_dev = 0;
+__device__ int g_fused_l2_dev = 1;  // fused k_ffn: L2 prefetch of the down block (SMOE_FUSED_NO_L2PF=1: off)
 
 // Wait (thread 0) until the predictor of layer-1 published this layer's
 // decision for the current pass (publish_decision).
@@ -1061,7 +1062,7 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
     PipeGU pipe;
     pipe.init(pipe_mem, kL2EvictFirst);
     pipe.prime(tile, H);
-    if (g_down_l2_dev && threadIdx.x == 0) {
+    if ((g_down_l2_dev || (fused && g_fused_l2_dev)) && threadIdx.x == 0) {
         // warm L2 with this CTA's share of the expert's down-projection block,
         // so k_ffn_down streams it from L2 while our gate/up stream runs on HBM
         const char* dn = reinterpret_cast<const char*>(
@@ -1117,6 +1118,45 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
 __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src, int s_from_r) {
     ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false);
+}
+
+// Single-GPU epilogue of one 32-row block of executed expert i's down
+// projection: the raw rows y_i; the last of the K arrivals on the block
+// (device-scope counter, threadfence pattern) forms the gate-weighted mixture
+// in decision order (model.cpp:297-301), the residual x = r + m
+// (model.cpp:386) and the rms_norm partial of x for the next layer.
+__device__ __forceinline__ void down_block_epilogue(const DevModel& m, const DevState& st, const float* gts,
+                                                    int layer, int rb, int i, float acc) {
+    const int K = m.K, lane = threadIdx.x & 31, j = rb * 32 + lane;
+    if (j < m.H) st.y[static_cast<long long>(i) * m.Hp + j] = acc;
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(st.down_cnt + rb, 1) == K - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    if (lane == 0) st.down_cnt[rb] = 0;
+    float xv = 0.0f;
+    if (j < m.H) {
+        // all loads first (independent, one L2 round trip), then the mixture in
+        // decision order
+        float yv[kMaxK], gv[kMaxK];
+#pragma unroll
+        for (int q = 0; q < kMaxK; ++q) {
+            yv[q] = q < K ? __ldcg(st.y + static_cast<long long>(q) * m.Hp + j) : 0.0f;
+            gv[q] = q < K ? gts[q] : 0.0f;
+        }
+        const float rv = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j);
+        float out = 0.0f;
+#pragma unroll
+        for (int q = 0; q < kMaxK; ++q)
+            if (q < K) out += gv[q] * yv[q];
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        xv = rv + out;
+        st.x[j] = xv;
+    }
+    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
 }
 
 // down: grid (Hp/32, K), one warp per (32-row block, executed expert), so the
@@ -1226,36 +1266,7 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
         }
         return;
     }
-    if (j < m.H) st.y[static_cast<long long>(i) * m.Hp + j] = acc;
-    __threadfence();
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(st.down_cnt + rb, 1) == K - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    PHASE();
-    if (!last) return;
-    __threadfence();
-    if (lane == 0) st.down_cnt[rb] = 0;
-    float xv = 0.0f;
-    if (j < m.H) {
-        // all loads first (independent, one L2 round trip), then the mixture in
-        // decision order
-        float yv[kMaxK], gv[kMaxK];
-#pragma unroll
-        for (int q = 0; q < kMaxK; ++q) {
-            yv[q] = q < K ? __ldcg(st.y + static_cast<long long>(q) * m.Hp + j) : 0.0f;
-            gv[q] = q < K ? gts[q] : 0.0f;
-        }
-        const float rv = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j);
-        float out = 0.0f;
-#pragma unroll
-        for (int q = 0; q < kMaxK; ++q)
-            if (q < K) out += gv[q] * yv[q];
-        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
-        xv = rv + out;
-        st.x[j] = xv;
-    }
-    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
+    down_block_epilogue(m, st, gts, layer, rb, i, acc);
     PHASE();
 #ifdef SMOE_PHASES
     if (rb == 0 && lane == 0)
@@ -1268,23 +1279,116 @@ __global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl
     ffn_down_body(m, st, ctl, layer, exec_src, blockIdx.x, blockIdx.y, false, 0);
 }
 
-// Gate/up and down in ONE grid: blocks [0, nGU) run the gate/up role, blocks
-// [nGU, nGU + nDN) the down role.  Down CTAs prefetch their weights while the
-// gate/up CTAs compute and start as soon as their expert's 16-row blocks are
-// done (gu_done, monotonic; target from the per-layer launch epoch), with no
-// kernel boundary in between.  CTAs are dispatched in block order, so every
-// gate/up CTA is resident before a down CTA can wait on it.
+// The expert FFN of a layer in ONE launch (single GPU, when every CTA of the
+// grid is co-resident — attn_grid-style occupancy check at session creation):
+//
+//  phase 1  CTA b = gate/up of (16-row block b % (Hmp/16), expert b / (Hmp/16))
+//           exactly as k_ffn_gu, plus an L2 prefetch of its share of the
+//           expert's down-projection block, so the down weights stream from
+//           HBM while the gate/up chains run (one HBM pass over all 3·H·Hm
+//           weights per expert);
+//  phase 2  the CTAs that finished their gate/up claim down items (atomic
+//           counter): a pair of 32-row blocks of one expert, primed from L2
+//           into the same shared-memory pipe, started once that expert's
+//           gate/up blocks are all done (gu_done, monotonic; target from the
+//           per-layer launch epoch); two independent chains per lane
+//           (run_pair), then the usual mixture epilogue.
+//
+// Every dot product is still one lane walking the reference's column order,
+// so results equal the split kernels bit for bit.
 __global__ void __launch_bounds__(32) k_ffn(DevModel m, DevState st, DevCtl ctl, int layer,
                                             int exec_src, int s_from_r) {
-    const int ngu_x = m.Hmp / 16, ngu = ngu_x * m.K, ndn_x = m.Hp / 32;
+    KTRACE(15, layer);
+    const int ngu_x = m.Hmp / 16, nrb = m.Hp / 32, npair = (nrb + 1) / 2, items = npair * m.K;
     const int epoch = __ldcg(st.ffn_epoch + layer);  // before this launch's last CTA bumps it
     const int b = blockIdx.x;
-    if (b < ngu)
-        ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, b % ngu_x, b / ngu_x, true);
-    else
-        ffn_down_body(m, st, ctl, layer, exec_src, (b - ngu) % ndn_x, (b - ngu) / ndn_x, true,
-                      (epoch + 1) * ngu_x);
-    if (last_cta(st.counters + 5, gridDim.x) && threadIdx.x == 0) st.ffn_epoch[layer] = epoch + 1;
+    ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, b % ngu_x, b / ngu_x, true);
+    const int lane = threadIdx.x & 31;
+    const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * m.K;
+    const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * m.K;
+    float* hs = reinterpret_cast<float*>(g_smem + 128);  // reuses the gate/up input staging
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(hs + 2 * round_up(m.H, 32)));
+    const int target = (epoch + 1) * ngu_x;
+    PHASE_DECL
+    PHASE();
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(st.counters + 6, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= items || *(volatile int*)ctl.error) break;
+        const int i = it / npair, pr = it % npair, rb0 = 2 * pr, rb1 = 2 * pr + 1;
+        const bool two = rb1 < nrb;
+        const int e = __ldcg(ids + i);
+        const int slot = __ldcg(m.slot_of + layer * m.E + e);
+        if (slot < 0) {
+            if (lane == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+            break;
+        }
+        const uint16_t* dn = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems;
+        const uint16_t* ta = dn + static_cast<long long>(rb0) * m.Hmp * 32;
+        const uint16_t* tb = dn + static_cast<long long>(two ? rb1 : rb0) * m.Hmp * 32;
+        if (lane == 0) {  // this expert's h rows are complete
+            const int* cnt = st.gu_done + layer * m.K + i;
+            const long long t0 = clock64();
+            for (;;) {
+                int v;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                if (v >= target || *(volatile int*)ctl.error) break;
+                if (clock64() - t0 > ctl.spin_limit) {
+                    atomicCAS(ctl.error, 0, 1000 + layer);
+                    break;
+                }
+                __nanosleep(32);
+            }
+        }
+        __syncwarp();
+        if (*(volatile int*)ctl.error) break;
+        PHASE();
+        // h loads go out before the weight stream (they would queue behind it)
+        const float4* h4 = reinterpret_cast<const float4*>(st.h + static_cast<long long>(i) * m.Hmp);
+        constexpr int kHv = 8;
+        float4 hv[kHv];
+        const int nh4 = m.Hmp / 4;
+#pragma unroll
+        for (int u = 0; u < kHv; ++u) {
+            const int t = u * 32 + lane;
+            if (t < nh4) hv[u] = __ldcg(h4 + t);
+        }
+        // the gate/up phase's pipe is drained: fresh barriers for this item
+        PipeGU pipe;
+        pipe.init(pipe_mem, kL2EvictFirst);
+        if (two)
+            prime_pair(pipe, ta, tb, m.Hm);
+        else
+            pipe.prime(ta, m.Hm);
+#pragma unroll
+        for (int u = 0; u < kHv; ++u) {
+            const int t = u * 32 + lane;
+            if (t < nh4) reinterpret_cast<float4*>(hs)[t] = hv[u];
+        }
+        for (int t = kHv * 32 + lane; t < nh4; t += 32) reinterpret_cast<float4*>(hs)[t] = __ldcg(h4 + t);
+        __syncwarp();
+        PHASE();
+        if (two) {
+            float acc_a, acc_b;
+            run_pair(pipe, ta, tb, m.Hm, hs, acc_a, acc_b);
+            PHASE();
+            down_block_epilogue(m, st, gts, layer, rb0, i, acc_a);
+            down_block_epilogue(m, st, gts, layer, rb1, i, acc_b);
+            PHASE();
+        } else {
+            const float acc = pipe.run(ta, m.Hm, hs);
+            down_block_epilogue(m, st, gts, layer, rb0, i, acc);
+        }
+    }
+#ifdef SMOE_PHASES
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 200))
+        phase_print("ffn down phase [start->primed, gu_done wait, h stage, chain, epilogue]", ph_, nph_);
+#endif
+    if (last_cta(st.counters + 5, gridDim.x) && threadIdx.x == 0) {
+        st.counters[6] = 0;  // every CTA has left its claim loop
+        st.ffn_epoch[layer] = epoch + 1;
+    }
 }
 
 // L2 prefetch of the experts a decision will execute (prefetch mode): issued on
@@ -1649,9 +1753,11 @@ __global__ void k_trace_bump(TraceDev tr) {
 static long long g_launches = 0;
 
 long long launch_counter() { return g_launches; }
-// SMOE_FUSED_FFN=1: gate/up and down in one grid (k_ffn).  Off by default:
-// measured slower on Q30 — the waiting down CTAs hold SM slots and starve the
-// side-stream predictor, which then delays the next layer.
+// The one-launch expert FFN (k_ffn) is opt-in (SMOE_FUSED_FFN=1): measured
+// slower on Q30 (29-30 us vs 12.5 + 8.3 us for k_ffn_gu + k_ffn_down; its
+// down phase streams each 96 KB pair of row blocks through the 48 KB gate/up
+// pipe in two round trips, and the L2 prefetch of the down blocks issued
+// during the gate/up phase did not turn those reads into L2 hits).
 static const bool g_split_ffn = std::getenv("SMOE_FUSED_FFN") == nullptr;
 static inline cudaError_t counted(int n = 1) {
     g_launches += n;
@@ -1727,6 +1833,18 @@ int attn_grid_for(const DevModel& m, int device) {
     return static_cast<long long>(nb) * sms >= kAttnSplit ? kAttnSplit : 1;
 }
 
+// The fused expert kernel needs every CTA of its grid co-resident (phase-2
+// CTAs wait on phase-1 CTAs of the same grid), room for the side-stream
+// predictor CTAs beside it, and h (Hmp floats) inside the input staging.
+int ffn_fused_ok(const DevModel& m, int device) {
+    int nb = 0, sms = 0;
+    if (m.Hmp > 2 * round_up(m.H, 32)) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ffn, 32, gu_smem(m)) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    const long long grid = static_cast<long long>(m.Hmp / 16) * m.K;
+    return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
+}
+
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), gu_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
@@ -1766,6 +1884,9 @@ cudaError_t preload_kernels() {
         const int v = std::getenv("SMOE_DOWN_L2") ? 1 : 0;
         cudaError_t e = cudaMemcpyToSymbol(g_down_l2_dev, &v, sizeof v);
         if (e != cudaSuccess) return e;
+        const int f = std::getenv("SMOE_FUSED_NO_L2PF") ? 0 : 1;
+        e = cudaMemcpyToSymbol(g_fused_l2_dev, &f, sizeof f);
+        if (e != cudaSuccess) return e;
     }
     const void* fns[] = {(const void*)k_gen_bf16, (const void*)k_embed, (const void*)k_qkv,
                          (const void*)k_attn, (const void*)k_wo, (const void*)k_router,
@@ -1792,7 +1913,7 @@ cudaError_t preload_kernels() {
     for (const void* f : big)
         if ((e = set_smem(f, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
-    if ((e = set_smem((const void*)k_ffn, 220 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
@@ -1859,9 +1980,8 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
-    if (ctl.ep.world == 1 && !g_split_ffn) {
-        const size_t sm = gu_smem(m) > down_smem(m) ? gu_smem(m) : down_smem(m);
-        PDL(k_ffn, (m.Hmp / 16 + m.Hp / 32) * m.K, 32, sm, s, m, st, ctl, layer, exec_src, s_from_r);
+    if (ctl.ep.world == 1 && m.ffn_fused && !g_split_ffn) {
+        PDL(k_ffn, (m.Hmp / 16) * m.K, 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
         return counted(1);
     }
     PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);

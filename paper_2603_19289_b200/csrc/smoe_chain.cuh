@@ -632,6 +632,80 @@ __device__ inline void run_multi(Pipe& p, const uint16_t* tile, int cols, const 
     p.ctr += nch;
 }
 
+// Two row tiles of the same width against ONE input vector (fused expert
+// kernel: two 32-row blocks of an expert's down projection per warp).  The
+// tiles' chunks alternate through the pipe (virtual chunk 2n = tile A's chunk
+// n, 2n+1 = tile B's); each lane keeps two independent chains (rows lane of A
+// and of B), each in the reference's column order, so they hide each other's
+// FADD latency.  Bit-identical to two run() calls.
+// Issue the first chunks of a tile pair before the input vector exists.
+template <typename Pipe>
+__device__ inline void prime_pair(Pipe& p, const uint16_t* ta, const uint16_t* tb, int cols) {
+    const int nv = 2 * ((cols + Pipe::kCC - 1) / Pipe::kCC);
+    if ((threadIdx.x & 31) == 0)
+        for (int v = 0; v < Pipe::kS && v < nv; ++v) p.issue((v & 1) ? tb : ta, cols, v >> 1, p.ctr + v);
+    p.primed = 1;
+}
+
+template <typename Pipe>
+__device__ inline void run_pair(Pipe& p, const uint16_t* ta, const uint16_t* tb, int cols, const float* xs,
+                                float& acc_a, float& acc_b) {
+    constexpr int G = Pipe::G, CC = Pipe::kCC, S = Pipe::kS;
+    static_assert(S % 2 == 0, "pair pipe needs an even stage count");
+    const int lane = threadIdx.x & 31;
+    const int nch = (cols + CC - 1) / CC, nv = 2 * nch;
+    const int c0 = p.ctr;
+    if (lane == 0 && !p.primed)
+        for (int v = 0; v < S && v < nv; ++v) p.issue((v & 1) ? tb : ta, cols, v >> 1, c0 + v);
+    p.primed = 0;
+    const uint32_t xbase = smem_u32(xs);
+    const uint32_t lbase = p.sbuf + lane * 16;
+    float a = 0.0f, b = 0.0f;
+    for (int n = 0; n < nch; ++n) {
+        const int ga = c0 + 2 * n, gb = ga + 1;
+        mbar_wait(&p.full[ga % S], static_cast<uint32_t>((ga / S) & 1));
+        mbar_wait(&p.full[gb % S], static_cast<uint32_t>((gb / S) & 1));
+        const uint32_t ca = lbase + (ga % S) * Pipe::kChunkBytes, cbb = lbase + (gb % S) * Pipe::kChunkBytes;
+        const int cn = min(CC, cols - n * CC);
+        const int ng = cn / G;
+        const uint32_t xo = xbase + n * CC * 4;
+        int q = 0;
+        for (; q + 1 < ng; q += 2) {  // two groups per step: four independent loads in flight
+            const uint4 wa0 = lds128(ca + q * 512), wb0 = lds128(cbb + q * 512);
+            const uint4 wa1 = lds128(ca + (q + 1) * 512), wb1 = lds128(cbb + (q + 1) * 512);
+            const XG x0 = load_x(xo + q * G * 4, uint16_t{}), x1 = load_x(xo + (q + 1) * G * 4, uint16_t{});
+            a = chain_group(a, wa0, x0, uint16_t{});
+            b = chain_group(b, wb0, x0, uint16_t{});
+            a = chain_group(a, wa1, x1, uint16_t{});
+            b = chain_group(b, wb1, x1, uint16_t{});
+        }
+        for (; q < ng; ++q) {
+            const XG x0 = load_x(xo + q * G * 4, uint16_t{});
+            a = chain_group(a, lds128(ca + q * 512), x0, uint16_t{});
+            b = chain_group(b, lds128(cbb + q * 512), x0, uint16_t{});
+        }
+        const int tail = cn - ng * G;
+        if (tail) {
+            const uint4 wa = lds128(ca + ng * 512), wb = lds128(cbb + ng * 512);
+            const float* xt = xs + n * CC + ng * G;
+            for (int i = 0; i < tail; ++i) {
+                a = a + group_elem(wa, i, uint16_t{}) * xt[i];
+                b = b + group_elem(wb, i, uint16_t{}) * xt[i];
+            }
+        }
+        __syncwarp();  // both stages consumed by every lane: refill them
+        if (elect_one()) {
+            const int va = 2 * n + S, vb = va + 1;
+            if (va < nv) p.issue(ta, cols, va >> 1, c0 + va);
+            if (vb < nv) p.issue(tb, cols, vb >> 1, c0 + vb);
+        }
+    }
+    __syncwarp();
+    p.ctr += nv;
+    acc_a = a;
+    acc_b = b;
+}
+
 constexpr int kS = 4;       // stages per warp
 constexpr int kCCb = 128;   // bf16 columns per chunk (8 KB)
 constexpr int kCCf = 64;    // f32 columns per chunk (8 KB)

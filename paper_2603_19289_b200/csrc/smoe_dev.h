@@ -95,6 +95,7 @@ struct DevModel {
     int attn_grid;
     int* attn_err;
     long long attn_spin;
+    int ffn_fused;      // expert FFN as one launch (k_ffn) when its grid is co-resident
 };
 
 // Per-stream decode state (the main stream, and the Oracle's shadow stream).

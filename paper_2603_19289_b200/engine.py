@@ -33,7 +33,7 @@ EXPORTS = [
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
-    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex",
+    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info",
 ]
 
 
@@ -452,10 +452,16 @@ class Session:
         _check(self.lib.smoe_clear_stats(self._h))
 
     def profile_kernels(self, reps: int = 3) -> dict:
-        out = np.zeros(7, np.float64)
+        out = np.zeros(8, np.float64)
         _check(self.lib.smoe_profile_kernels(self._h, reps, _p(out)))
-        names = ["qkv", "attn", "wo", "router", "ffn_gate_up", "ffn_down", "final"]
+        names = ["qkv", "attn", "wo", "router", "ffn_gate_up", "ffn_down", "final", "ffn"]
         return dict(zip(names, out.tolist()))
+
+    def path_info(self) -> dict:
+        out = np.zeros(4, np.int32)
+        _check(self.lib.smoe_path_info(self._h, _p(out), 4))
+        return {"ffn_fused": bool(out[0]), "attn_ctas": int(out[1]), "host_ordered": bool(out[2]),
+                "device_hit_path": bool(out[3])}
 
     def measure_link(self, n_copies: int = 64) -> float:
         g = C.c_double()

@@ -58,7 +58,7 @@ def test_headline_q30_48_layers_teacher_forced(lib):
     from paper_2603_19289_b200 import ModelConfig, Session
     from parity_check import check_traces, gpu_trace
     P, N = 32, 20
-    s = Session(ModelConfig(**Q30), cache_fraction=1.0, max_positions=P + N + 16)
+    s = Session(ModelConfig(**Q30), cache_fraction=1.0, max_positions=300)
     s.init_weights_seeded()
     s.preload_all()
     dv, _ = s.calibrate(2000, 2, 256)

@@ -22,5 +22,5 @@ for _ in range(2):
     p = s.profile_kernels(reps=5)
 print({k: round(v, 2) for k, v in p.items()})
 gu = 8 * 2 * 768 * 2048 * 2
-print(f"ffn_gate_up {gu / p['ffn_gate_up'] / 1e3:.0f} GB/s; ffn_down {gu / 2 / p['ffn_down'] / 1e3:.0f} GB/s")
+print(f"ffn_gate_up {gu / p['ffn_gate_up'] / 1e3:.0f} GB/s; ffn_down {gu / 2 / p['ffn_down'] / 1e3:.0f} GB/s; ffn (as launched) {1.5 * gu / p['ffn'] / 1e3:.0f} GB/s; path {s.path_info()}")
 s.close()

@@ -20,7 +20,8 @@ E.load_library(LIB)
 from paper_2603_19289_b200 import ModelConfig, Session  # noqa: E402
 
 KINDS = {14: "l2_pf", 0: "embed", 1: "qkv", 2: "attn", 3: "wo", 4: "router", 5: "est0", 6: "est1", 7: "est2",
-         8: "est3", 9: "ffn_gu", 10: "ffn_down", 11: "ep_mix", 12: "final", 13: "predictor"}
+         8: "est3", 9: "ffn_gu", 10: "ffn_down", 11: "ep_mix", 12: "final", 13: "predictor",
+         15: "ffn_fused"}
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 wl = sys.argv[3] if len(sys.argv) > 3 else "greedy"
