@@ -503,6 +503,11 @@ void Session::alloc() {
         if (!v.empty()) throw std::invalid_argument("config: " + v);
     }
     m.attn_grid = attn_grid_for(m, opts_.device);
+    // the one-launch expert FFN (k_ffn) is opt-in, SMOE_FUSED_FFN=1: measured
+    // slower on Q30 (29-30 us vs 12.5 + 8.3 us for k_ffn_gu + k_ffn_down: its
+    // down phase streams each 96 KB pair of row blocks through the 48 KB
+    // gate/up pipe in two round trips, and the L2 prefetch of the down blocks
+    // during the gate/up phase did not turn those reads into L2 hits)
     m.ffn_fused = std::getenv("SMOE_FUSED_FFN") ? ffn_fused_ok(m, opts_.device) : 0;
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");

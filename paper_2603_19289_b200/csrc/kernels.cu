@@ -1753,12 +1753,7 @@ __global__ void k_trace_bump(TraceDev tr) {
 static long long g_launches = 0;
 
 long long launch_counter() { return g_launches; }
-// The one-launch expert FFN (k_ffn) is opt-in (SMOE_FUSED_FFN=1): measured
-// slower on Q30 (29-30 us vs 12.5 + 8.3 us for k_ffn_gu + k_ffn_down; its
-// down phase streams each 96 KB pair of row blocks through the 48 KB gate/up
-// pipe in two round trips, and the L2 prefetch of the down blocks issued
-// during the gate/up phase did not turn those reads into L2 hits).
-static const bool g_split_ffn = std::getenv("SMOE_FUSED_FFN") == nullptr;
+
 static inline cudaError_t counted(int n = 1) {
     g_launches += n;
     return cudaGetLastError();
@@ -1980,7 +1975,7 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
-    if (ctl.ep.world == 1 && m.ffn_fused && !g_split_ffn) {
+    if (ctl.ep.world == 1 && m.ffn_fused) {
         PDL(k_ffn, (m.Hmp / 16) * m.K, 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
         return counted(1);
     }

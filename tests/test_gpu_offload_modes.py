@@ -136,3 +136,22 @@ def test_run_offloaded_decode_ex_executor_result(lib, toy, mode):
     # reference's double-buffer bound, executor.cpp:159-162); on demand, one
     assert 1 <= max_res <= (2 if mode == "prefetch" else 1)
     s.close()
+
+
+@pytest.mark.parametrize("mode", ["on_demand", "prefetch"])
+def test_fused_expert_ffn_matches_oracle(lib, toy, mode):
+    """The opt-in one-launch expert FFN (SMOE_FUSED_FFN=1: gate/up, then down
+    row-block pairs claimed by the finished CTAs, two chains per lane) is
+    bit-identical to the oracle."""
+    orc, om, table = toy
+    prompt = [5, 77, 200, 13, 9]
+    stream = list(np.random.default_rng(8).integers(0, 256, 12))
+    s = _session({"SMOE_FUSED_FFN": "1"})
+    assert s.path_info()["ffn_fused"]
+    got, _ = _decode(s, table, prompt, 12, mode, stream)
+    pred = orc.make_predictor("router-pf", om, table) if mode == "prefetch" else None
+    want = om.generate_trace(prompt, 13, pred, outputs=True, forced=np.array(stream, np.int32))
+    assert np.array_equal(got["id_exec"], want.ids)
+    assert np.array_equal(got["m"], want.m)
+    assert np.array_equal(got["logits"], want.final_logits)
+    s.close()
