@@ -214,6 +214,11 @@ int smoe_batch_generate(smoe_session* s, int32_t batch, const int32_t* prompts, 
  * glibc's exp(double) that every f64 softmax / silu on the path uses
  * (exp_glibc.cuh); equal to the host libm's exp bit for bit. */
 int smoe_exp(const double* x, double* y, int64_t n);
+/* Diagnostics: make_decision (model.cpp:258-274) of `rows` logits rows
+ * [rows][E] on the GPU through the decision routine every router, predictor
+ * and estimator on the path uses; ids / gates [rows][K]. */
+int smoe_decide(const float* logits, int32_t rows, int32_t E, int32_t K, int32_t gating, int32_t* ids,
+                float* gates);
 /* Router-pf predictions `depth` layers ahead (multi-layer-
  * ahead prefetch study) from captured steps (trace_full=1, default vectors
  * loaded): ids[t][l][:] = top-k of gate_l . rms_norm(r_{l-depth} +

@@ -458,6 +458,31 @@ int smoe_train_estimator(const smoe_estimator_config* c, uint64_t seed, const fl
     });
 }
 
+int smoe_decide(const float* logits, int32_t rows, int32_t E, int32_t K, int32_t gating, int32_t* ids,
+                float* gates) {
+    return guard([&] {
+        if (rows < 0 || E < 1 || E > smoe::kMaxE || K < 1 || K > E || K > smoe::kMaxK || (gating != 0 && gating != 1))
+            throw std::invalid_argument("smoe_decide: bad arguments");
+        if (rows == 0) return;
+        float *dl = nullptr, *dg = nullptr;
+        int* di = nullptr;
+        auto ck = [](cudaError_t e) {
+            if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in smoe_decide: ") + cudaGetErrorString(e));
+        };
+        ck(cudaMalloc(&dl, 4ull * rows * E));
+        ck(cudaMalloc(&di, 4ull * rows * K));
+        ck(cudaMalloc(&dg, 4ull * rows * K));
+        cudaError_t e = cudaMemcpy(dl, logits, 4ull * rows * E, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = smoe::launch_decide(dl, rows, E, K, gating, di, dg, nullptr);
+        if (e == cudaSuccess) e = cudaMemcpy(ids, di, 4ull * rows * K, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(gates, dg, 4ull * rows * K, cudaMemcpyDeviceToHost);
+        cudaFree(dl);
+        cudaFree(di);
+        cudaFree(dg);
+        ck(e);
+    });
+}
+
 int smoe_exp(const double* x, double* y, int64_t n) {
     return guard([&] {
         if (n < 0 || (n && (!x || !y))) throw std::invalid_argument("smoe_exp: bad arguments");

@@ -1561,6 +1561,25 @@ __global__ void k_exp_glibc(const double* x, double* y, long long n) {
         y[i] = exp_glibc(x[i]);
 }
 
+// make_decision of `rows` logits rows (diagnostics / tests): one warp per row
+// through warp_decision, the routine every router, predictor and estimator
+// decision on the path uses.
+__global__ void __launch_bounds__(32) k_decide(const float* logits, int E, int K, int gating, int* ids,
+                                               float* gates) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    float* sp = reinterpret_cast<float*>(dsm);
+    double* se = reinterpret_cast<double*>(dsm + 16 * ((E * 4 + 15) / 16));
+    const long long r = blockIdx.x;
+    warp_decision(logits + r * E, E, K, gating, sp, se, ids + r * K, gates + r * K);
+}
+
+cudaError_t launch_decide(const float* logits, int rows, int E, int K, int gating, int* ids, float* gates,
+                          cudaStream_t s) {
+    const size_t sm = 16 * ((E * 4 + 15) / 16) + 8ull * E;
+    k_decide<<<rows, 32, sm, s>>>(logits, E, K, gating, ids, gates);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_exp_glibc(const double* x, double* y, long long n, cudaStream_t s) {
     k_exp_glibc<<<148, 256, 0, s>>>(x, y, n);
     return cudaGetLastError();

@@ -84,6 +84,8 @@ cudaError_t launch_trace(const DevModel& m, const DevState& st, const TraceDev& 
 
 // exp_glibc over n doubles (device buffers) — the parity check of the device exp.
 cudaError_t launch_exp_glibc(const double* x, double* y, long long n, cudaStream_t s);
+cudaError_t launch_decide(const float* logits, int rows, int E, int K, int gating, int* ids, float* gates,
+                          cudaStream_t s);
 
 // DistillDatasetBuilder (speculation.cpp:437-471) over trace steps [first, first+n).
 cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int n, int mode, float* inputs,

@@ -733,7 +733,7 @@ __device__ long long g_dec_t[8];
 // index order by lane 0 (exactly the reference's order), f32 probabilities;
 // top_k (numerics.cpp:56-70): value desc, lower index first; gates renormalised
 // by an f32 sum in rank order.  topk-softmax: top_k on logits, softmax of the k.
-__device__ inline void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
+__device__ inline void warp_decision_rank(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
                               double* se /*smem E*/, int* ids, float* gates) {
     const int lane = threadIdx.x & 31;
     DEC_T(0);
@@ -880,6 +880,166 @@ __device__ inline void warp_decision(const float* logits, int E, int K, int gati
                     ids[t] = s_sel[t];
                     gates[t] = static_cast<float>(e[t] / z);
                 }
+        }
+    }
+    __syncwarp();
+    DEC_T(4);
+}
+
+// f32(e / z) for e >= 0, z >= 1 without a division per element: q = e * (1/z)
+// is within 3 double ulps of fl64(e / z) (two roundings), so the two round to
+// the same f32 unless an f32 rounding midpoint (low 29 mantissa bits = 2^28)
+// lies within a few ulps of q, or the result is f32-subnormal; those take the
+// exact division.  Bit-identical to static_cast<float>(e / z) by construction.
+__device__ __forceinline__ float div_to_f32(double e, double z, double rz) {
+    const double q = e * rz;
+    const long long b = __double_as_longlong(q);
+    const int low = static_cast<int>(b & ((1ll << 29) - 1)) - (1 << 28);
+    if (q < 2.3509887016445750e-38 || (low < 64 && low > -64)) return static_cast<float>(e / z);
+    return static_cast<float>(q);
+}
+
+// Order-preserving u32 key of an f32 (larger value -> larger key).
+__device__ __forceinline__ unsigned f32_key(float x) {
+    const unsigned b = __float_as_uint(x);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_f32(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// make_decision (model.cpp:258-274) for one logits row, executed by one warp,
+// E <= 256 (larger E: warp_decision_rank).
+// softmax (numerics.cpp:37-54): f32 max, f64 exp per element (glibc's
+// algorithm), the f64 partition summed in index order by lane 0 (exactly the
+// reference's order), f32 probabilities (div_to_f32).
+// top_k (numerics.cpp:56-70): value descending, lower index first on ties.
+// Each lane holds elements lane, lane+32, ... (ascending index), sorts its
+// (key, index) list with a sorting network, and K rounds take the warp
+// maximum of the list heads (REDUX on the key, then on the inverted index
+// among equal keys); the winner's lane pops its head.  Lane t keeps round t.
+// Gates: softmax-topk-renorm — p_t / (f32 sum of the K in rank order);
+// topk-softmax — f64 softmax of the K selected logits (rank order), f32 out.
+__device__ inline void warp_decision(const float* logits, int E, int K, int gating, float* sp /*smem E*/,
+                                     double* se /*smem E*/, int* ids, float* gates) {
+    if (E > 256) {
+        warp_decision_rank(logits, E, K, gating, sp, se, ids, gates);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    constexpr int U = 8;
+    DEC_T(0);
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = u * 32 + lane;
+        v[u] = i < E ? __ldcg(logits + i) : 0.0f;
+    }
+    DEC_T(1);
+    if (gating == kSoftmaxTopK) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u * 32 + lane < E) mx = fmaxf(mx, v[u]);
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double e[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = u * 32 + lane;
+            e[u] = i < E ? exp_glibc(static_cast<double>(v[u]) - static_cast<double>(mx)) : 0.0;
+            if (i < E) se[i] = e[u];
+        }
+        __syncwarp();
+        double z = 0.0;
+        if (lane == 0) {  // f64 partition in index order, as numerics.cpp:46-49
+            int i = 0;
+            for (; i + 8 <= E; i += 8) {  // loads of a block in flight together, adds in order
+                double t[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) t[q] = se[i + q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) z += t[q];
+            }
+            for (; i < E; ++i) z += se[i];
+        }
+        z = __shfl_sync(0xffffffffu, z, 0);
+        const double rz = 1.0 / z;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = div_to_f32(e[u], z, rz);
+        __syncwarp();
+    }
+    DEC_T(2);
+    // per-lane (key, index) lists, sorted by key desc then index asc
+    unsigned kk[U];
+    int ix[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = u * 32 + lane;
+        kk[u] = i < E ? f32_key(v[u]) : 0u;
+        ix[u] = i;
+    }
+    // Batcher odd-even merge sort of 8 (19 compare-exchanges); pairs (a, b)
+    // with a < b hold lower indices at a, so "b first" only on a strictly
+    // larger key keeps index order among equal keys
+#define SMOE_CX(a, b)                                             \
+    do {                                                          \
+        if (kk[b] > kk[a]) {                                      \
+            const unsigned tk = kk[a];                            \
+            kk[a] = kk[b];                                        \
+            kk[b] = tk;                                           \
+            const int ti = ix[a];                                 \
+            ix[a] = ix[b];                                        \
+            ix[b] = ti;                                           \
+        } else if (kk[b] == kk[a] && ix[b] < ix[a]) {             \
+            const int ti = ix[a];                                 \
+            ix[a] = ix[b];                                        \
+            ix[b] = ti;                                           \
+        }                                                         \
+    } while (0)
+    SMOE_CX(0, 1); SMOE_CX(2, 3); SMOE_CX(4, 5); SMOE_CX(6, 7);
+    SMOE_CX(0, 2); SMOE_CX(1, 3); SMOE_CX(4, 6); SMOE_CX(5, 7);
+    SMOE_CX(1, 2); SMOE_CX(5, 6);
+    SMOE_CX(0, 4); SMOE_CX(1, 5); SMOE_CX(2, 6); SMOE_CX(3, 7);
+    SMOE_CX(2, 4); SMOE_CX(3, 5);
+    SMOE_CX(1, 2); SMOE_CX(3, 4); SMOE_CX(5, 6);
+#undef SMOE_CX
+    int my_idx = 0;
+    float my_val = 0.0f;
+    for (int t = 0; t < K; ++t) {
+        const unsigned wk = __reduce_max_sync(0xffffffffu, kk[0]);
+        const unsigned wi = __reduce_max_sync(0xffffffffu, kk[0] == wk ? 0xFFFFFFFFu - static_cast<unsigned>(ix[0]) : 0u);
+        const int idx = static_cast<int>(0xFFFFFFFFu - wi);
+        if ((idx & 31) == lane) {  // pop the head
+#pragma unroll
+            for (int u = 0; u + 1 < U; ++u) {
+                kk[u] = kk[u + 1];
+                ix[u] = ix[u + 1];
+            }
+            kk[U - 1] = 0u;
+            ix[U - 1] = 0x7fffffff;
+        }
+        if (lane == t) {
+            my_idx = idx;
+            my_val = key_f32(wk);
+        }
+    }
+    DEC_T(3);
+    if (gating == kSoftmaxTopK) {  // gates renormalised by an f32 sum in rank order
+        float total = 0.0f;
+        for (int t = 0; t < K; ++t) total += __shfl_sync(0xffffffffu, my_val, t);
+        if (lane < K) {
+            ids[lane] = my_idx;
+            gates[lane] = my_val / total;
+        }
+    } else {  // topk-softmax: softmax of the k selected logits (f64 exp, f32 out)
+        float mx = lane < K ? my_val : -INFINITY;
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const double e = lane < K ? exp_glibc(static_cast<double>(my_val) - static_cast<double>(mx)) : 0.0;
+        double z = 0.0;
+        for (int t = 0; t < K; ++t) z += __shfl_sync(0xffffffffu, e, t);
+        if (lane < K) {
+            ids[lane] = my_idx;
+            gates[lane] = static_cast<float>(e / z);
         }
     }
     __syncwarp();

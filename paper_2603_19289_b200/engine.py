@@ -33,7 +33,7 @@ EXPORTS = [
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
-    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info",
+    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info", "smoe_decide",
 ]
 
 
@@ -186,6 +186,17 @@ def device_exp(x) -> np.ndarray:
     y = np.zeros_like(x)
     _check(lib.smoe_exp(_p(x), _p(y), C.c_int64(x.size)))
     return y
+
+
+def device_decide(logits, k: int, gating: str = "softmax-topk-renorm"):
+    """make_decision of every row of `logits` [rows][E] on the GPU -> (ids, gates)."""
+    lib = load_library()
+    lg = np.ascontiguousarray(logits, np.float32)
+    rows, E = lg.shape
+    ids = np.zeros((rows, k), np.int32)
+    gates = np.zeros((rows, k), np.float32)
+    _check(lib.smoe_decide(_p(lg), rows, E, k, GATING[gating], _p(ids), _p(gates)))
+    return ids, gates
 
 
 def estimator_init(d, m, n, E, L, eps=1e-5, seed=0) -> np.ndarray:

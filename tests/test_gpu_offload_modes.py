@@ -155,3 +155,33 @@ def test_fused_expert_ffn_matches_oracle(lib, toy, mode):
     assert np.array_equal(got["m"], want.m)
     assert np.array_equal(got["logits"], want.final_logits)
     s.close()
+
+
+@pytest.mark.parametrize("E,K", [(8, 2), (32, 4), (128, 8), (256, 16), (300, 8)])
+@pytest.mark.parametrize("gating", ["softmax-topk-renorm", "topk-softmax"])
+def test_decision_routine_vs_oracle(lib, E, K, gating):
+    """warp_decision (every router / predictor / estimator decision on the path)
+    against the oracle's make_decision on random rows, rows with exact ties
+    (duplicated logits, the lower index must win), near ties one ulp apart,
+    and large / tiny magnitudes (probabilities that underflow f32)."""
+    from oracle.bindings import Oracle
+    from paper_2603_19289_b200.engine import device_decide
+    orc = Oracle()
+    rng = np.random.default_rng(E * 31 + K)
+    rows = [rng.normal(0, 1, E), rng.normal(0, 30, E), rng.normal(0, 1e-3, E)]
+    for _ in range(40):
+        r = rng.normal(0, 2, E).astype(np.float32)
+        dup = rng.integers(0, E, max(2, E // 4))
+        r[dup] = r[dup[0]]                     # exact ties
+        j = int(rng.integers(0, E - 1))
+        r[j + 1] = np.nextafter(r[j], np.float32(np.inf))  # one-ulp neighbours
+        rows.append(r)
+    rows.append(np.zeros(E))                   # everything tied
+    rows.append(np.concatenate([[200.0], np.full(E - 1, -200.0)]))  # probabilities underflow
+    lg = np.stack(rows).astype(np.float32)
+    gid = 0 if gating == "softmax-topk-renorm" else 1
+    ids, gates = device_decide(lg, K, gating)
+    for r in range(lg.shape[0]):
+        wi, wg = orc.make_decision(lg[r], K, gid)
+        assert np.array_equal(ids[r], wi), (r, ids[r], wi)
+        assert np.array_equal(gates[r].view(np.uint32), wg.view(np.uint32)), (r, gates[r], wg)
