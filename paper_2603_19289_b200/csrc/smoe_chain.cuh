@@ -892,6 +892,7 @@ __device__ inline void warp_decision_rank(const float* logits, int E, int K, int
 // lies within a few ulps of q, or the result is f32-subnormal; those take the
 // exact division.  Bit-identical to static_cast<float>(e / z) by construction.
 __device__ __forceinline__ float div_to_f32(double e, double z, double rz) {
+    if (e == 0.0) return 0.0f;  // 0 / z (underflowed exponentials, padding)
     const double q = e * rz;
     const long long b = __double_as_longlong(q);
     const int low = static_cast<int>(b & ((1ll << 29) - 1)) - (1 << 28);
