@@ -297,6 +297,19 @@ int smoe_simulate_cache(const smoe_cache_sim* c, const int32_t* exec_ids, const 
  * fractions {compute, copy on the critical path, idle}. */
 int smoe_breakdown(const smoe_event* events, int32_t n, double* mean_fractions3,
                    double* mean_tpot);
+/* Per-layer online hit rates of a recorded decode: exec_ids / true_ids
+ * [steps][layers][k] (smoe_read_trace id_exec / id_true of the decode steps);
+ * rates[layers-1], entry l-1 = mean recall_at_k at layer l (the predictor
+ * dispatched at l-1).  Host-only. */
+int smoe_layer_hit_rates(const int32_t* exec_ids, const int32_t* true_ids, int32_t steps, int32_t layers,
+                         int32_t k, double* rates);
+/* Hybrid map selection from per-layer hit rates:
+ * rates [n_kinds][layers-1] of the candidate predictors kinds[] (SMOE_PRED_*
+ * baseline-s / router-pf / est-pf).  threshold > 0: kinds[0] unless its rate
+ * is below the threshold, then the best other; threshold <= 0: best per layer.
+ * map_out[layers-1] feeds smoe_set_predictor(SMOE_PRED_HYBRID, map).  Host-only. */
+int smoe_select_hybrid_map(const double* rates, const int32_t* kinds, int32_t n_kinds, int32_t layers,
+                           double threshold, int32_t* map_out);
 /* recall_at_k (metrics.cpp:9-20) and rank_alignment (metrics.cpp:22-28). */
 int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, double* recall,
                      int32_t* rank_match);

@@ -391,6 +391,66 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
     });
 }
 
+// Per-layer online hit rates of a decode: for every
+// recorded step t and layer l >= 1, recall_at_k (metrics.cpp:9-20) of the
+// executed decision (the one predicted at l-1) against the true router's
+// decision at l on the actual stream.  rates[l-1] = mean over steps (the
+// predictor for layer l is the one dispatched at l-1, speculation.cpp:243-252).
+int smoe_layer_hit_rates(const int32_t* exec_ids, const int32_t* true_ids, int32_t steps, int32_t layers,
+                         int32_t k, double* rates) {
+    return guard_r([&] {
+        if (!exec_ids || !true_ids || !rates || steps < 1 || layers < 2 || k < 1)
+            throw std::invalid_argument("layer_hit_rates: bad arguments");
+        for (int l = 1; l < layers; ++l) {
+            double sum = 0.0;
+            for (int t = 0; t < steps; ++t) {
+                const int32_t* p = exec_ids + (static_cast<long long>(t) * layers + l) * k;
+                const int32_t* q = true_ids + (static_cast<long long>(t) * layers + l) * k;
+                int hits = 0;
+                for (int i = 0; i < k; ++i)
+                    for (int j = 0; j < k; ++j)
+                        if (p[i] == q[j]) {
+                            ++hits;
+                            break;
+                        }
+                sum += static_cast<double>(hits) / k;
+            }
+            rates[l - 1] = sum / steps;
+        }
+    });
+}
+
+// Hybrid map selection ("applying the estimator only where
+// prefetch hit rates were low"; the map format is load_hybrid_map's,
+// speculation.cpp:145-165): rates [n_kinds][layers-1] per candidate kind
+// (SMOE_PRED_* codes in `kinds`, no hybrid/oracle).  threshold > 0: the first
+// candidate (the default, router-pf) unless its rate is below threshold, then
+// the best of the others; threshold <= 0: the best rate per layer (ties: the
+// earlier candidate).
+int smoe_select_hybrid_map(const double* rates, const int32_t* kinds, int32_t n_kinds, int32_t layers,
+                           double threshold, int32_t* map_out) {
+    return guard_r([&] {
+        if (!rates || !kinds || !map_out || n_kinds < 1 || layers < 2)
+            throw std::invalid_argument("select_hybrid_map: bad arguments");
+        for (int i = 0; i < n_kinds; ++i)
+            if (kinds[i] < SMOE_PRED_BASELINE_S || kinds[i] > SMOE_PRED_EST_PF)
+                throw std::invalid_argument("hybrid map: entries must be concrete predictors");
+        const int n = layers - 1;
+        for (int l = 0; l < n; ++l) {
+            int best = 0;
+            const int from = threshold > 0.0 ? 1 : 0;
+            if (threshold > 0.0 && (n_kinds == 1 || rates[l] >= threshold)) {
+                map_out[l] = kinds[0];
+                continue;
+            }
+            best = from;
+            for (int i = from + 1; i < n_kinds; ++i)
+                if (rates[static_cast<long long>(i) * n + l] > rates[static_cast<long long>(best) * n + l]) best = i;
+            map_out[l] = kinds[best];
+        }
+    });
+}
+
 // Trace-driven cache + lookahead schedule, see CacheSim.
 int smoe_simulate_cache(const smoe_cache_sim* c, const int32_t* exec_ids, const int32_t* pred_ids,
                         const int32_t* pred2_ids, const double* t_attn, const double* t_gate,

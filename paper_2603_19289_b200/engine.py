@@ -33,7 +33,8 @@ EXPORTS = [
     "smoe_ep_buffers", "smoe_ep_ipc_handles", "smoe_ep_connect", "smoe_ep_connect_ipc",
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
-    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info", "smoe_decide",
+    "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info", "smoe_decide", "smoe_layer_hit_rates",
+    "smoe_select_hybrid_map",
 ]
 
 
@@ -166,6 +167,38 @@ def breakdown(events) -> tuple:
     tp = C.c_double()
     _check(lib.smoe_breakdown(arr, n, _p(fr), C.byref(tp)))
     return fr, tp.value
+
+
+def layer_hit_rates(exec_ids, true_ids) -> np.ndarray:
+    """Per-layer online hit rates [L-1] of a recorded decode (id_exec vs id_true,
+    [steps][L][k]); entry l-1 belongs to the predictor dispatched at l-1."""
+    lib = load_library()
+    e = np.ascontiguousarray(exec_ids, np.int32)
+    t = np.ascontiguousarray(true_ids, np.int32)
+    steps, L, k = e.shape
+    out = np.zeros(L - 1, np.float64)
+    _check(lib.smoe_layer_hit_rates(_p(e), _p(t), steps, L, k, _p(out)))
+    return out
+
+
+def select_hybrid_map(rates: dict, threshold: float = 0.0) -> list:
+    """Hybrid map (layers-1 predictor names) from per-layer hit rates {kind: [L-1]};
+    the first kind is the default (threshold > 0: kept unless below it)."""
+    lib = load_library()
+    kinds = list(rates)
+    r = np.ascontiguousarray(np.stack([np.asarray(rates[k], np.float64) for k in kinds]))
+    codes = np.array([PRED[k] for k in kinds], np.int32)
+    out = np.zeros(r.shape[1], np.int32)
+    _check(lib.smoe_select_hybrid_map(_p(r), _p(codes), len(kinds), r.shape[1] + 1, C.c_double(threshold),
+                                      _p(out)))
+    inv = {v: k for k, v in PRED.items()}
+    return [inv[int(c)] for c in out]
+
+
+def hybrid_map_json(names) -> str:
+    """The map in load_hybrid_map's format (speculation.cpp:145-165): {"layer": "kind"}."""
+    import json
+    return json.dumps({str(l): n for l, n in enumerate(names)})
 
 
 def recall_at_k(pred, truth):
