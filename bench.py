@@ -43,13 +43,27 @@ CONFIGS = {
                 head_dim=64, seed=1, gating="topk-softmax"),
     "mx": dict(layers=32, experts=8, top_k=2, hidden=4096, expert_hidden=14336, vocab=256,
                head_dim=128, seed=1, gating="topk-softmax"),
+    "q235": dict(layers=94, experts=128, top_k=8, hidden=4096, expert_hidden=1536, vocab=256,
+                 head_dim=128, seed=1, gating="softmax-topk-renorm"),
 }
 WORKLOAD = {
     "q30": "Qwen3-30B-A3B shape (L48 E128 k8 H2048 Hm768), B=1, HBM cache 25% of experts",
     "tiny": "tiny synthetic MoE (L4 H512 E32 k4 Hm1024), B=1",
     "g20": "GPT-OSS-20B shape (L24 E32 k4 H2880 Hm2880), B=1",
     "mx": "Mixtral-8x7B shape (L32 E8 k2 H4096 Hm14336), B=1",
+    "q235": "Qwen3-235B-A22B shape (L94 E128 k8 H4096 Hm1536), B=1, expert parallel",
 }
+
+
+def host_ram_budget_layers(c: dict, world: int, frac: float = 0.6) -> int:
+    """Layers whose pinned expert shards (bf16, E/world experts per layer per rank,
+    all ranks on this host) fit in `frac` of the host's available memory."""
+    try:
+        avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable"))
+    except (OSError, StopIteration):
+        return c["layers"]
+    per_layer = c["experts"] * 3 * c["hidden"] * c["expert_hidden"] * 2  # all ranks together
+    return max(1, min(c["layers"], int(frac * avail // per_layer)))
 METRIC = "decode TPOT ms (spec-prefetch vs on-demand) + H2D GB/s vs link peak"
 
 
@@ -181,6 +195,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     dev = int(os.environ.get("LOCAL_RANK", 0)) % ndev
     torch.cuda.set_device(dev)
     c = dict(CONFIGS[args.config])
+    c["layers"] = args.layers_run
     cfg = ModelConfig(**c)
     L, K = c["layers"], c["top_k"]
     P = args.prompt_len
@@ -424,7 +439,8 @@ def reference_tpot(cfg: dict, P: int, n_steps: int, warmup: int, modes, dv: np.n
 
 
 def reference_arm(args) -> dict:
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    c["layers"] = args.layers_run  # the same depth as our arm (the host-RAM budget may cut it)
     dv = None
     try:  # default vectors for router-pf: the oracle's calibration pass on the truncated model
         from oracle.bindings import Config, Oracle
@@ -473,13 +489,19 @@ def main():
     ap.add_argument("--workload", default="stream", choices=["stream", "greedy"],
                     help="stream: decode inputs teacher-forced from a random token stream "
                          "(headline; exercises the offload path); greedy: argmax feedback")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="depth truncation (0 = the config's depth, cut to the host-RAM budget of the "
+                         "pinned expert store when it does not fit)")
     args = ap.parse_args()
     if args.ncu:
         args.cache_fraction, args.runs, args.no_cpu_baseline = 1.0, 1, True
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    full_layers = c["layers"]
+    args.layers_run = args.layers if args.layers > 0 else host_ram_budget_layers(c, world)
+    c["layers"] = args.layers_run
     base_cfg = {"workload": WORKLOAD[args.config], "model": f"{args.config}-shape random-init",
                 "global_batch": 1, "seq_len": args.prompt_len + args.steps,
                 "prompt_len": args.prompt_len, "cache_fraction": args.cache_fraction,
@@ -488,7 +510,9 @@ def main():
                 "l2": "inputs larger than L2 (expert bytes per token >> 126 MB)",
                 "parallelism": f"ep{world}" if world > 1 else "single-gpu",
                 "decode_inputs": ("teacher-forced random_token_stream(seed 4)" if args.workload == "stream"
-                                  else "greedy argmax feedback")}
+                                  else "greedy argmax feedback"),
+                "layers_run": args.layers_run,
+                "depth_truncated": args.layers_run < full_layers}
 
     if args.impl == "reference":
         if rank != 0:

@@ -317,7 +317,8 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
 /* Which variants this session runs: out[0] expert FFN fused into one launch
  * (1) or gate/up + down kernels (0); out[1] split-attention CTAs; out[2]
  * host-ordered copy waits (profiler / sanitizer attached or
- * SMOE_HOST_ORDERED=1); out[3] device-side all-hit release. */
+ * SMOE_HOST_ORDERED=1); out[3] device-side all-hit release; out[4] NUMA node
+ * the pinned expert store is bound to (-1: not bound — single-node host). */
 int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap);
 
 /* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */

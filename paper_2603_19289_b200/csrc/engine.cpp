@@ -14,6 +14,9 @@
 #include <random>
 #include <unistd.h>
 #include <sys/stat.h>
+#include <cctype>
+#include <sys/syscall.h>
+#include <sys/mman.h>
 #include <cerrno>
 #include <string>
 
@@ -159,14 +162,69 @@ void ModelCfg::validate() const {
 
 // ------------------------------------------------------------ ExpertStore --
 
-ExpertStore::ExpertStore(long long n, long long elems) : n_(n), elems_(elems) {
+namespace {
+// NUMA node of a GPU's PCIe root (sysfs), -1 if unknown.
+int gpu_numa_node(int device) {
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+    std::string id(bus);
+    for (char& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/numa_node").c_str(), "r");
+    if (!f) return -1;
+    int node = -1;
+    if (std::fscanf(f, "%d", &node) != 1) node = -1;
+    std::fclose(f);
+    return node;
+}
+int numa_nodes() {
+    int n = 0;
+    for (int i = 0; i < 1024; ++i) {
+        struct stat st;
+        if (stat(("/sys/devices/system/node/node" + std::to_string(i)).c_str(), &st) != 0) break;
+        ++n;
+    }
+    return n;
+}
+}  // namespace
+
+// Pinned host memory for the expert shard.  On a multi-socket host the pages
+// are bound to the NUMA node of the GPU's PCIe root (mmap + mbind, then
+// cudaHostRegister pins them there), so each rank's H2D copies read local
+// DRAM; otherwise cudaHostAlloc.
+ExpertStore::ExpertStore(long long n, long long elems, int device) : n_(n), elems_(elems) {
     const size_t bytes = static_cast<size_t>(n) * elems * 2;
+    const int node = gpu_numa_node(device);
+    if (node >= 0 && node < 64 && numa_nodes() > 1 && !std::getenv("SMOE_NO_NUMA_BIND")) {
+        void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) throw std::runtime_error("mmap(expert store) failed");
+        unsigned long mask = 1ul << node;
+        constexpr int kMpolBind = 2;
+        if (syscall(SYS_mbind, p, bytes, kMpolBind, &mask, 64, 0) != 0) {
+            munmap(p, bytes);
+            throw std::runtime_error("mbind(expert store) to NUMA node " + std::to_string(node) + " failed");
+        }
+        const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+        if (e != cudaSuccess) {
+            munmap(p, bytes);
+            ck(e, "cudaHostRegister(expert store)");
+        }
+        base_ = static_cast<uint16_t*>(p);
+        mapped_ = bytes;
+        node_ = node;
+        return;
+    }
     ck(cudaHostAlloc(reinterpret_cast<void**>(&base_), bytes, cudaHostAllocPortable),
        "cudaHostAlloc(expert store)");
 }
 
 ExpertStore::~ExpertStore() {
-    if (base_) cudaFreeHost(base_);
+    if (!base_) return;
+    if (mapped_) {
+        cudaHostUnregister(base_);
+        munmap(base_, mapped_);
+    } else {
+        cudaFreeHost(base_);
+    }
 }
 
 // -------------------------------------------------------------- SlotCache --
@@ -643,6 +701,7 @@ void Session::alloc() {
         st.gu_done = static_cast<int*>(dalloc(4ull * L * K));
         st.ffn_epoch = static_cast<int*>(dalloc(4ull * L));
         st.ssq_rd = static_cast<double*>(dalloc(8ull * L * (m.Hp / 32)));
+        st.ep_arrive = static_cast<int*>(dalloc(4ull * L));
         st.est_z = st.est_act = st.est_xn = nullptr;
     };
     mk_state(st_);
@@ -688,7 +747,7 @@ void Session::alloc() {
     for (auto& e : ev_step_) ck(cudaEventCreate(&e), "event");
     ck(cudaEventCreate(&ev_origin_), "event");
 
-    store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * el_max_, m.expert_elems);
+    store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * el_max_, m.expert_elems, opts_.device);
     cache_ = std::make_unique<SlotCache>(L, E, C_);
     ck(cudaDeviceSynchronize(), "alloc");
     reset(0, 0);
@@ -735,6 +794,21 @@ void Session::ep_connect(void* const* xbufs, void* const* cnts) {
     const int W = opts_.ep_world;
     for (int p = 0; p < W; ++p) {
         if (!xbufs[p] || !cnts[p]) throw std::invalid_argument("ep_connect: null peer buffer");
+        // ranks of one process on different GPUs: map the peer's memory over NVLink
+        cudaPointerAttributes a{};
+        if (p != opts_.ep_rank && cudaPointerGetAttributes(&a, xbufs[p]) == cudaSuccess &&
+            a.type == cudaMemoryTypeDevice && a.device != opts_.device) {
+            int can = 0;
+            ck(cudaDeviceCanAccessPeer(&can, opts_.device, a.device), "peer query");
+            if (!can)
+                throw std::runtime_error("ep_connect: device " + std::to_string(opts_.device) +
+                                         " cannot access peer device " + std::to_string(a.device));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled)
+                cudaGetLastError();
+            else
+                ck(e, "enable peer access");
+        }
         ctl_.ep.xbuf[p] = static_cast<float*>(xbufs[p]);
         ctl_.ep.cnt[p] = static_cast<int*>(cnts[p]);
     }
@@ -1141,7 +1215,12 @@ void Session::check_device_error() {
                                      std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
                                      " ms for layer " + std::to_string(err - 1000) + " expert copy");
         if (err >= 3000 && err < 4000)
-            throw std::runtime_error("split attention stalled at layer " + std::to_string(err - 3000) +
+            throw std::runtime_error("deadlock suspected: expert-parallel combine of layer " +
+                                     std::to_string(err - 3000) + " waited " +
+                                     std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
+                                     " ms for peer ranks");
+        if (err >= 4000 && err < 5000)
+            throw std::runtime_error("split attention stalled at layer " + std::to_string(err - 4000) +
                                      ": its CTAs were not co-resident within " +
                                      std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) + " ms");
         throw std::runtime_error("expert read before readiness at layer " + std::to_string(err - 2000));
@@ -1965,8 +2044,9 @@ cudaGraphExec_t Session::get_graph(int mode, int stream) {
 // Kernels in one captured decode step: the teacher-forced (stream) graph if
 // it was built, else the greedy one; -1 before any graph exists.
 void Session::path_info(int* out, int cap) const {
-    const int v[] = {dm_.ffn_fused, dm_.attn_grid, host_ordered_ ? 1 : 0, ctl_.fast_hit};
-    for (int i = 0; i < cap && i < 4; ++i) out[i] = v[i];
+    const int v[] = {dm_.ffn_fused, dm_.attn_grid, host_ordered_ ? 1 : 0, ctl_.fast_hit,
+                     store_ ? store_->numa_node() : -1};
+    for (int i = 0; i < cap && i < 5; ++i) out[i] = v[i];
 }
 
 int Session::kernels_per_step(int mode) const {

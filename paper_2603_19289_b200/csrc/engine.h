@@ -66,14 +66,17 @@ struct CopyRecord {  // one mailbox request as the copy lane saw it
 
 class ExpertStore {
 public:
-    ExpertStore(long long n_experts, long long elems_per_expert);
+    ExpertStore(long long n_experts, long long elems_per_expert, int device);
     ~ExpertStore();
     uint16_t* expert(long long i) { return base_ + i * elems_; }
     long long bytes_per_expert() const { return elems_ * 2; }
+    int numa_node() const { return node_; }  // -1: not NUMA-bound (single node / unknown)
 
 private:
     uint16_t* base_ = nullptr;
     long long n_, elems_;
+    size_t mapped_ = 0;  // mmap'd + cudaHostRegister'ed (NUMA-bound) when > 0
+    int node_ = -1;
 };
 
 class SlotCache {
@@ -214,7 +217,8 @@ public:
     double measure_link(int n_copies);
     int kernels_per_step(int mode) const;
     bool host_ordered() const { return host_ordered_; }
-    // {expert FFN fused into one launch, split-attention CTAs, host-ordered copy waits, device hit path}
+    // {expert FFN fused into one launch, split-attention CTAs, host-ordered copy waits, device hit
+    //  path, NUMA node the pinned expert store is bound to (-1: not bound)}
     void path_info(int* out, int cap) const;
 
     // used by the scheduler

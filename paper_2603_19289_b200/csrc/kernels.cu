@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
                 break;
             }
             if (clock64() - t0 > m.attn_spin) {
-                atomicCAS(m.attn_err, 0, 3000 + layer);
+                atomicCAS(m.attn_err, 0, 4000 + layer);
                 s_abort = 1;
                 break;
             }
@@ -1250,11 +1250,13 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
         PHASE();
     }
     if (ctl.ep.world > 1) {
-        // EP: the owning rank publishes these expert rows to every rank; every
-        // CTA of every rank (owner or not) then bumps every rank's per-layer
-        // arrival counter (world x K x Hp/32 arrivals per layer).  Counting
-        // non-owners too keeps the ranks within one layer of each other, which
-        // the layer-parity double buffer of the exchange relies on.
+        // EP: the owning rank publishes these expert rows to every rank (peer
+        // stores over NVLink), fences them system-wide and counts the CTA on a
+        // local per-layer counter; the last of the K x Hp/32 local CTAs (owner
+        // or not) then makes ONE system-scope arrival on every rank's counter.
+        // A rank therefore arrives for layer l only after all its CTAs of l
+        // ran, which keeps the ranks within one layer of each other (the
+        // layer-parity double buffer of the exchange relies on it).
         if (local && j < m.H) {
             const long long o = (static_cast<long long>(layer & 1) * K + i) * m.Hp + j;
             for (int p = 0; p < ctl.ep.world; ++p) __stcg(ctl.ep.xbuf[p] + o, acc);
@@ -1262,7 +1264,11 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
         __syncwarp();
         if (lane == 0) {
             __threadfence_system();
-            for (int p = 0; p < ctl.ep.world; ++p) atomicAdd_system(ctl.ep.cnt[p] + layer, 1);
+            if (atomicAdd(st.ep_arrive + layer, 1) == K * static_cast<int>(gridDim.x) - 1) {
+                st.ep_arrive[layer] = 0;
+                __threadfence_system();
+                for (int p = 0; p < ctl.ep.world; ++p) atomicAdd_system(ctl.ep.cnt[p] + layer, 1);
+            }
         }
         return;
     }
@@ -1432,8 +1438,7 @@ __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl c
     const int K = m.K, lane = threadIdx.x & 31, rb = blockIdx.x, j = rb * 32 + lane;
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
-        const long long target =
-            (static_cast<long long>(ctl.ep.epoch[layer]) + 1) * ctl.ep.world * m.K * gridDim.x;
+        const long long target = (static_cast<long long>(ctl.ep.epoch[layer]) + 1) * ctl.ep.world;
         const int* cnt = ctl.ep.cnt[ctl.ep.rank] + layer;
         const long long t0 = clock64();
         int ok = 1;

@@ -147,6 +147,7 @@ struct DevState {
     int* gu_done;      // [L][K] gate/up CTAs finished, monotonic (fused k_ffn)
     int* ffn_epoch;    // [L] completed k_ffn launches per layer
     double* ssq_rd;    // [L][Hp/32]
+    int* ep_arrive;    // [L] EP: this rank's k_ffn_down CTAs done (self-resetting)
 };
 
 // Expert parallelism: expert e of every layer lives on rank

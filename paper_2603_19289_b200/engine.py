@@ -502,10 +502,10 @@ class Session:
         return dict(zip(names, out.tolist()))
 
     def path_info(self) -> dict:
-        out = np.zeros(4, np.int32)
-        _check(self.lib.smoe_path_info(self._h, _p(out), 4))
+        out = np.zeros(5, np.int32)
+        _check(self.lib.smoe_path_info(self._h, _p(out), 5))
         return {"ffn_fused": bool(out[0]), "attn_ctas": int(out[1]), "host_ordered": bool(out[2]),
-                "device_hit_path": bool(out[3])}
+                "device_hit_path": bool(out[3]), "store_numa_node": int(out[4])}
 
     def measure_link(self, n_copies: int = 64) -> float:
         g = C.c_double()
