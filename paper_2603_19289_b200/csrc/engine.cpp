@@ -1756,6 +1756,30 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                     gm({ey, 1, dm, head, 1, dm, bd.lgp, c.E, 1, nullptr, B, c.E, edm, kEpiNone, nullptr, nullptr, 1});
                     ck(launch_pf_decide_pred(m, bd, buf, s_comp_), "batch predictor");
                 }
+                if (!dev_lists) {
+                    // Algorithm 1 for the batch: the predicted experts of l+1 (the
+                    // union over the B sequences, in the order pf_waves loads them)
+                    // start copying now, one layer ahead, on the copy stream; the
+                    // first wave of l+1 then finds them resident or in flight
+                    std::vector<int> pids(static_cast<size_t>(Bl) * K);
+                    d2h(pids.data(), bd.pids + static_cast<long long>(buf) * Bl * K, 4ull * Bl * K, "batch pids");
+                    std::vector<char> want(c.E, 0);
+                    for (int e : pids)
+                        if (e >= 0 && e < c.E) want[e] = 1;
+                    std::vector<int> first;
+                    const int W = std::min<int>(C_, kMaxWave);
+                    for (int e = 0; e < c.E && static_cast<int>(first.size()) < W; ++e)
+                        if (want[e]) first.push_back(e);
+                    int hits = 0, misses = 0;
+                    const auto copies = cache_->request(l + 1, first.data(), static_cast<int>(first.size()), &hits, &misses);
+                    const long long bytes = store_->bytes_per_expert();
+                    for (const auto& [slot, expert] : copies)
+                        ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l + 1) * C_ + slot) * m.expert_elems,
+                                           store_->expert(store_index(l + 1, expert)), bytes,
+                                           cudaMemcpyHostToDevice, s_copy_),
+                           "batch prefetch copy");
+                    batch_prefetched_bytes_ += static_cast<long long>(copies.size()) * bytes;
+                }
             }
         }
         ck(launch_pf_final(m, bd, s_comp_), "batch final");

@@ -272,6 +272,7 @@ private:
     PrefillDev pf_{};                      // batched-prefill buffers (sized for pf_cap_ tokens)
     PrefillDev bd_{};                      // batched-decode buffers (sized for bd_cap_ sequences)
     int bd_cap_ = 0;
+    long long batch_prefetched_bytes_ = 0;  // batched decode: expert bytes copied one layer ahead
     int* bd_nchunks_ = nullptr;
     float* bd_qn_ = nullptr;          // [B][H] q_l for the batched estimator
     int* bd_pos_ = nullptr;           // device position of a graph-captured batched step
