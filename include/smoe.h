@@ -142,6 +142,13 @@ int smoe_prefill(smoe_session* s, const int32_t* tokens, int32_t n);
  * the slot pool in waves.  The prompt's per-token trace rows are not recorded.
  * Single GPU; with the Oracle predictor it falls back to smoe_prefill. */
 int smoe_prefill_batched(smoe_session* s, const int32_t* tokens, int32_t n);
+/* Expert GEMMs of smoe_prefill_batched: mode 0 (default) exact — the
+ * reference's sequential f32 chains, bit-identical to smoe_prefill; mode 1
+ * tensor cores (tcgen05, M = 128 tokens of an expert, activations as bf16
+ * hi + lo, f32 accumulation in TMEM) — the hidden states then agree with the
+ * reference to a stated tolerance, not bit for bit (tests/test_gpu_prefill_tc.py).
+ * Needs hidden and expert_hidden to be multiples of 64. */
+int smoe_set_prefill_mode(smoe_session* s, int32_t mode);
 /* n_steps greedy decode steps on the device (speculative_forward semantics in
  * SMOE_PREFETCH mode, forward_decode in SMOE_ON_DEMAND mode). */
 int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph);

@@ -474,6 +474,7 @@ Session::Session(const ModelCfg& cfg, const SessionOpts& opts) : cfg_(cfg), opts
     write_value_fn();
     ck(preload_kernels(), "kernel preload");
     ck(pf_preload(), "prefill kernel preload");
+    ck(tc_preload(), "tensor-core prefill kernel preload");
     try {
         alloc();
     } catch (...) {
@@ -1552,6 +1553,13 @@ void Session::prefill_batched(const int* tokens, int n) {
 // The experts of one layer for a batch of tokens, in waves of at most C
 // slot-resident experts: copies (cache misses) on the copy stream, then the
 // gate/up and down kernels over the wave's (expert, 8-token chunk) items.
+void Session::set_prefill_mode(int mode) {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("prefill mode must be 0 (exact) or 1 (tensor cores)");
+    if (mode == 1 && !tc_prefill_supported(dm_))
+        throw std::invalid_argument("tensor-core prefill needs hidden and expert_hidden multiples of 64");
+    pf_tc_ = mode;
+}
+
 void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt) {
     const ModelCfg& c = cfg_;
     const DevModel& m = dm_;
@@ -1590,8 +1598,32 @@ void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt)
             wv.slot[u] = row[wv.e[u]];
             if (wv.slot[u] < 0) throw std::runtime_error("expert read before readiness at layer " + std::to_string(l));
         }
-        // prefills fill whole 8-token chunks; decode batches (bkc set) get per-chunk dispatch
-        ck(launch_pf_experts(m, pf, l, wv, chunks, s_comp_, pf.bkc ? 0 : 8), "prefill experts");
+        if (pf_tc_ && !pf.bkc) {  // tensor-core expert GEMMs over 128-token blocks
+            std::vector<int> tu, tcb;
+            for (int u = 0; u < nw; ++u)
+                for (int b = 0; b < (cnt[wv.e[u]] + 127) / 128; ++b) {
+                    tu.push_back(u);
+                    tcb.push_back(b);
+                }
+            const int items = static_cast<int>(tu.size());
+            h2d(pf.chunk_u, tu.data(), 4ull * items, "prefill items");
+            h2d(pf.chunk_c, tcb.data(), 4ull * items, "prefill items");
+            const size_t need = tc_pack_bytes(m, items);
+            if (need > tc_apk_cap_) {
+                for (auto it = dev_allocs_.begin(); it != dev_allocs_.end(); ++it)
+                    if (*it == d_tc_apk_) {
+                        cudaFree(d_tc_apk_);
+                        dev_allocs_.erase(it);
+                        break;
+                    }
+                d_tc_apk_ = static_cast<uint16_t*>(dalloc(need));
+                tc_apk_cap_ = need;
+            }
+            ck(launch_pf_experts_tc(m, pf, l, wv, items, d_tc_apk_, s_comp_), "prefill experts (tcgen05)");
+        } else {
+            // prefills fill whole 8-token chunks; decode batches (bkc set) get per-chunk dispatch
+            ck(launch_pf_experts(m, pf, l, wv, chunks, s_comp_, pf.bkc ? 0 : 8), "prefill experts");
+        }
         if (w0 + W < uni.size()) ck(cudaStreamSynchronize(s_comp_), "prefill wave");  // slots reused
     }
 }

@@ -152,6 +152,10 @@ public:
     void prefill(const int* tokens, int n);               // true routing per token
     // all n prompt tokens per layer at once (prefill.cu); same results
     void prefill_batched(const int* tokens, int n);
+    // 0: exact (sequential f32 chains, bit-identical to token-by-token prefill);
+    // 1: tensor-core expert GEMMs (tcgen05, bf16x2 activations, f32 accumulate;
+    // a stated tolerance instead of bit parity)
+    void set_prefill_mode(int mode);
     // B independent sequences decoded together (generate, speculation.cpp:401-421,
     // per sequence): prompts [B][P], out_tokens [B][n_new], out_logits
     // (nullable) [B][n_new][V] = the logits each output token was taken from.
@@ -273,6 +277,9 @@ private:
     PrefillDev bd_{};                      // batched-decode buffers (sized for bd_cap_ sequences)
     int bd_cap_ = 0;
     long long batch_prefetched_bytes_ = 0;  // batched decode: expert bytes copied one layer ahead
+    int pf_tc_ = 0;                         // batched prefill expert GEMMs on tcgen05 (tolerance mode)
+    uint16_t* d_tc_apk_ = nullptr;          // packed activations of the tensor-core prefill
+    size_t tc_apk_cap_ = 0;
     int* bd_nchunks_ = nullptr;
     float* bd_qn_ = nullptr;          // [B][H] q_l for the batched estimator
     int* bd_pos_ = nullptr;           // device position of a graph-captured batched step

@@ -155,6 +155,14 @@ cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const P
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
                               int chunks, cudaStream_t s, int chains = 8);
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
+// tensor-core expert GEMMs of the batched prefill (prefill_tc.cu, tolerance
+// mode): items = (wave expert, 128-token block) pairs in pf.chunk_u / chunk_c;
+// apk: packed-activation scratch of tc_pack_bytes(m, items)
+bool tc_prefill_supported(const DevModel& m);
+size_t tc_pack_bytes(const DevModel& m, int items);
+cudaError_t tc_preload();
+cudaError_t launch_pf_experts_tc(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv, int items,
+                                 uint16_t* apk, cudaStream_t s);
 // batched decode pieces (prefill.cu)
 cudaError_t launch_pf_attn_block(const DevModel& m, const DevState& st, const PrefillDev& pf, int layer,
                                  cudaStream_t s);
