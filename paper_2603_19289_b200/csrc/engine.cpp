@@ -18,6 +18,7 @@
 #include <sys/syscall.h>
 #include <sys/mman.h>
 #include <cerrno>
+#include <set>
 #include <string>
 
 namespace smoe {
@@ -300,10 +301,35 @@ std::vector<std::pair<int, int>> SlotCache::request(int layer, const int* ids, i
 
 // ---------------------------------------------------------- CopyScheduler --
 
+// Copy threads still running at process exit (a session the host program
+// never destroyed) must stop before the CUDA runtime tears itself down: the
+// exit hook is registered after the runtime initialised (first scheduler
+// start), so atexit's LIFO order runs it first.
+namespace {
+std::mutex g_live_mu;
+std::set<CopyScheduler*>* g_live = nullptr;
+void stop_live_schedulers() {
+    std::set<CopyScheduler*> live;
+    {
+        std::lock_guard<std::mutex> g(g_live_mu);
+        if (g_live) live = *g_live;
+    }
+    for (CopyScheduler* c : live) c->stop();
+}
+}  // namespace
+
 CopyScheduler::CopyScheduler(Session* s) : s_(s) {}
 CopyScheduler::~CopyScheduler() { stop(); }
 
 void CopyScheduler::start() {
+    {
+        std::lock_guard<std::mutex> g(g_live_mu);
+        if (!g_live) {
+            g_live = new std::set<CopyScheduler*>();
+            std::atexit(stop_live_schedulers);
+        }
+        g_live->insert(this);
+    }
     stop_ = false;
     th_ = std::thread([this] { loop(); });
 }
@@ -311,6 +337,8 @@ void CopyScheduler::start() {
 void CopyScheduler::stop() {
     stop_ = true;
     if (th_.joinable()) th_.join();
+    std::lock_guard<std::mutex> g(g_live_mu);
+    if (g_live) g_live->erase(this);
 }
 
 std::string CopyScheduler::error() {

@@ -8,8 +8,10 @@ missing or no GPU is present, constructing a ``Session`` raises.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -277,6 +279,20 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+_LIVE: "weakref.WeakSet[Session]" = weakref.WeakSet()
+
+
+@atexit.register
+def _close_live_sessions():
+    """Destroy sessions still open at interpreter exit while the CUDA runtime
+    is alive (module teardown order would otherwise decide)."""
+    for s in list(_LIVE):
+        try:
+            s.close()
+        except Exception:
+            pass
+
+
 class Session:
     """One model on one GPU: pinned expert store + HBM slot cache + decode state."""
 
@@ -291,6 +307,7 @@ class Session:
         c = cfg._c()
         _check(lib.smoe_session_create(C.byref(c), C.byref(opt), C.byref(self._h)))
         self.lib = lib
+        _LIVE.add(self)
 
     def close(self):
         if self._h:
