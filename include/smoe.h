@@ -149,6 +149,15 @@ int smoe_prefill_batched(smoe_session* s, const int32_t* tokens, int32_t n);
  * reference to a stated tolerance, not bit for bit (tests/test_gpu_prefill_tc.py).
  * Needs hidden and expert_hidden to be multiples of 64. */
 int smoe_set_prefill_mode(smoe_session* s, int32_t mode);
+/* Decode GEMV arithmetic for every single-sequence decode kernel (qkv, wo,
+ * routers / predictor, expert gate/up and down, unembed): mode 0 (default)
+ * exact — each output row one sequential f32 chain in the reference's column
+ * order, bit-identical to the reference (linear, numerics.cpp:136-147);
+ * mode 1 tolerance — four packed fused multiply-add partial sums per row, so
+ * the kernels are HBM-bound; hidden states and logits then agree with the
+ * reference within the stated tolerance and router ids are exact except
+ * reported near-ties (tests/test_gpu_fast.py).  Rebuilds the step graphs. */
+int smoe_set_decode_mode(smoe_session* s, int32_t mode);
 /* n_steps greedy decode steps on the device (speculative_forward semantics in
  * SMOE_PREFETCH mode, forward_decode in SMOE_ON_DEMAND mode). */
 int smoe_decode(smoe_session* s, int32_t mode, int32_t n_steps, int32_t use_graph);
@@ -263,10 +272,13 @@ int smoe_preload_all(smoe_session* s);
 int smoe_clear_stats(smoe_session* s);
 /* Average device time (us) per launch of each per-layer kernel, CUDA events on
  * the compute stream over L back-to-back launches (one per layer, weights
- * larger than L2), `reps` repetitions.  out_us[8]: qkv, attn, wo, router,
- * ffn_gate_up, ffn_down, final, ffn (the whole expert FFN as decode launches
- * it: the one-launch fused kernel when active, else gate/up + down).  Needs a
- * completed decode step (resident experts). */
+ * larger than L2), `reps` repetitions.  out_us[9]: qkv, attn, wo, router,
+ * ffn_gate_up (on-demand form: decision from this layer's router), ffn_down,
+ * final, ffn (the whole expert FFN as decode launches it: the one-launch fused
+ * kernel when active, else gate/up + down), ffn_gate_up_prefetch (the form the
+ * prefetch path launches for layers >= 1: decision published a layer ahead,
+ * weight stream started before the PDL wait).  Needs a completed prefetch
+ * decode step (resident experts). */
 int smoe_profile_kernels(smoe_session* s, int32_t reps, double* out_us);
 /* H2D GB/s of expert-sized copies from the pinned store into HBM. */
 int smoe_measure_link(smoe_session* s, int32_t n_copies, double* gbps);

@@ -355,6 +355,10 @@ int smoe_timeline(smoe_session* s, int32_t mode, const int32_t* tokens, int32_t 
     });
 }
 
+int smoe_set_decode_mode(smoe_session* s, int32_t mode) {
+    return guard([&] { S(s)->set_decode_mode(mode); });
+}
+
 int smoe_set_prefill_mode(smoe_session* s, int32_t mode) {
     return guard([&] { S(s)->set_prefill_mode(mode); });
 }

@@ -581,6 +581,7 @@ void Session::alloc() {
     m.QKVp = round_up(3 * D, 32);
     m.cap = opts_.max_positions;
     m.inv_sqrt_d = 1.0f / std::sqrt(static_cast<float>(D));  // model.cpp:336
+    m.fast = 0;
     m.gu_elems = static_cast<long long>(m.Hmp) * H * 2;
     m.expert_elems = m.gu_elems + static_cast<long long>(m.Hp) * m.Hmp;
     C_ = slots_for(opts_.cache_fraction);
@@ -1581,6 +1582,19 @@ void Session::prefill_batched(const int* tokens, int n) {
 // The experts of one layer for a batch of tokens, in waves of at most C
 // slot-resident experts: copies (cache misses) on the copy stream, then the
 // gate/up and down kernels over the wave's (expert, 8-token chunk) items.
+// Decode GEMV arithmetic (DESIGN "Decode arithmetic modes"): 0 exact — every
+// row a sequential f32 chain in the reference's column order (bit parity);
+// 1 tolerance — the same kernels with four packed FFMA partial sums per row
+// (WarpPipe::run_fast), HBM-bound instead of FADD-latency bound.  The captured
+// step graphs embed DevModel by value, so they are rebuilt.
+void Session::set_decode_mode(int mode) {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("decode mode must be 0 (exact) or 1 (tolerance)");
+    if (dm_.fast == mode) return;
+    sync();
+    drop_graphs();
+    dm_.fast = mode;
+}
+
 void Session::set_prefill_mode(int mode) {
     if (mode != 0 && mode != 1) throw std::invalid_argument("prefill mode must be 0 (exact) or 1 (tensor cores)");
     if (mode == 1 && !tc_prefill_supported(dm_))
@@ -2209,6 +2223,20 @@ void Session::profile_kernels(int reps, double* out) {
         ck(cudaEventSynchronize(b), "event");
         ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
         out[5] = 1000.0 * ms / (static_cast<double>(reps) * L);
+        // k_ffn_gu in the prefetch form (layers >= 1 of a prefetch pass); the
+        // predicted decisions of the last prefetch pass are resident
+        out[8] = out[4];
+        if (L > 1) {
+            ck(launch_mark_decided(st_, L, s_comp_), "mark");
+            for (int l = 1; l < L; ++l) ck(launch_ffn_part(dm_, st_, ctl_, l, 2, s_comp_), "ffn");
+            ck(cudaEventRecord(a, s_comp_), "event");
+            for (int r = 0; r < reps; ++r)
+                for (int l = 1; l < L; ++l) ck(launch_ffn_part(dm_, st_, ctl_, l, 2, s_comp_), "ffn");
+            ck(cudaEventRecord(b, s_comp_), "event");
+            ck(cudaEventSynchronize(b), "event");
+            ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+            out[8] = 1000.0 * ms / (static_cast<double>(reps) * (L - 1));
+        }
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);

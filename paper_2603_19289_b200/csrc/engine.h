@@ -156,6 +156,8 @@ public:
     // 1: tensor-core expert GEMMs (tcgen05, bf16x2 activations, f32 accumulate;
     // a stated tolerance instead of bit parity)
     void set_prefill_mode(int mode);
+    void set_decode_mode(int mode);
+    int decode_mode() const { return dm_.fast; }
     // B independent sequences decoded together (generate, speculation.cpp:401-421,
     // per sequence): prompts [B][P], out_tokens [B][n_new], out_logits
     // (nullable) [B][n_new][V] = the logits each output token was taken from.

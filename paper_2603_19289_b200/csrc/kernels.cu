@@ -22,6 +22,7 @@
 // per (kernel kind, layer) the first CTA entry, the first CTA past its PDL
 // wait and the last CTA exit, in globaltimer ns, min/max over CTAs.
 namespace smoe {
+
 constexpr int kKtKinds = 16, kKtLayers = 128;
 __device__ unsigned long long g_kt[kKtKinds * kKtLayers][4];
 __device__ __forceinline__ unsigned long long kt_now() {
@@ -66,6 +67,23 @@ extern "C" int smoe_ktrace_read(unsigned long long* out) {
 #include <cstdlib>
 
 namespace smoe {
+
+// Tolerance-mode code paths are compiled out of the exact-only object the SASS
+// guard inspects (Makefile build/kernels_exact.o, tests/test_sass.py): that
+// build proves the exact chains carry no fused multiply-add.
+#ifdef SMOE_EXACT_ONLY
+#define SMOE_FAST(m) false
+#else
+#define SMOE_FAST(m) ((m).fast != 0)
+#endif
+
+// A decode GEMV row chain in the session's arithmetic mode (DevModel::fast).
+template <typename Pipe>
+__device__ __forceinline__ float chain_run(Pipe& p, const DevModel& m, const uint16_t* tile, int cols,
+                                          const float* xs) {
+    return SMOE_FAST(m) ? p.run_fast(tile, cols, xs) : p.run(tile, cols, xs);
+}
+
 
 
 
@@ -223,7 +241,7 @@ __global__ void k_embed(DevModel m, DevState st, const int* token_src, const int
 // q, k, v = W{q,k,v} . rms_norm(x, attn_gain) (model.cpp:325-333), RoPE on q
 // and k (model.cpp:309-321, cos/sin precomputed on the host with libm), k and v
 // appended to the layer's KV cache at `pos`.  One warp per 32-row tile.
-__global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) {
+__global__ void __launch_bounds__(32 * kSplitWarps) k_qkv(DevModel m, DevState st, int layer) {
     KTRACE(1, layer);
     PHASE_DECL
     PHASE();
@@ -234,9 +252,16 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
     const int rb = blockIdx.x;
     const uint16_t* tile = m.wqkv + layer * m.qkv_stride + static_cast<long long>(rb) * m.H * 32;
+    // exact: one warp, the tile's sequential chains; fast: kSplitWarps warps
+    // split the columns (SplitLdg), weights loaded into registers right here
     PipeBL pipe;
-    pipe.init(pipe_mem);
-    pipe.prime(tile, m.H);
+    SplitG sp;
+    if (SMOE_FAST(m)) {
+        sp.prime(tile, m.H);
+    } else {
+        pipe.init(pipe_mem);
+        pipe.prime(tile, m.H);
+    }
     Stager sg;
     sg.init(bar);
     pdl_wait();
@@ -262,7 +287,8 @@ __global__ void __launch_bounds__(32) k_qkv(DevModel m, DevState st, int layer) 
     PHASE();
     block_apply_norm(xs, gs, m.H, scale, xs);
     PHASE();
-    float acc = pipe.run(tile, m.H, xs);
+    float acc = SMOE_FAST(m) ? sp.run(tile, m.H, xs, reinterpret_cast<float*>(pipe_mem)) : pipe.run(tile, m.H, xs);
+    if (threadIdx.x >= 32) return;  // fast mode: warp 0 holds the rows
     PHASE();
     const float other = __shfl_xor_sync(0xffffffffu, acc, 1);
     if (R < 2 * D) {  // RoPE pair (2i, 2i+1) lives in lanes (2i', 2i'+1)
@@ -704,7 +730,7 @@ __global__ void __launch_bounds__(32) k_wo(DevModel m, DevState st, DevCtl ctl, 
     sg.add(xr, st.x + blockIdx.x * 32, 32 * 4);
     sg.wait();
     const uint16_t* tile = m.wo + layer * m.wo_stride + static_cast<long long>(rb) * m.D * 32;
-    const float acc = pipe.run(tile, m.D, xs);
+    const float acc = chain_run(pipe, m, tile, m.D, xs);
     const float r = j < m.H ? xr[threadIdx.x & 31] + acc : 0.0f;
     if (j < m.H) st.r[static_cast<long long>(layer) * m.Hp + j] = r;
     warp_ssq_partial(r, st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32) + rb);
@@ -767,7 +793,7 @@ __device__ void compute_quasi(const DevModel& m, const DevState& st, int layer, 
     block_rms_norm(rs, gs, H, m.eps, qs, red);
 }
 
-__global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl ctl,
+__global__ void __launch_bounds__(32 * kRouterSplitWarps) k_router(DevModel m, DevState st, DevCtl ctl,
                                                RouterLaunch rl, DevState sh, int has_shadow) {
     KTRACE(rl.do_true ? 4 : 13, rl.layer);
     PHASE_DECL
@@ -776,8 +802,8 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     // in one launch (one y-slice per layer, per-layer last-CTA counters)
     const int H = m.H, E = m.E, K = m.K, l = rl.layer + static_cast<int>(blockIdx.y), Hr = round_up(H, 32);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
-    double* red = reinterpret_cast<double*>(g_smem + 64);
-    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    double* red = reinterpret_cast<double*>(g_smem + 64);  // [kRouterSplitWarps] (block reductions)
+    float* xs = reinterpret_cast<float*>(g_smem + 256);
     float* rs = xs + Hr;
     float* gs = rs + Hr;
     // [K][Hr] default-vector rows, only for a router-pf / est-pf q_l not
@@ -791,13 +817,18 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     const int nQ = (rl.pred_kind == kEstPF) ? 1 : 0;  // est-pf: one CTA writes q_l
     const int b = blockIdx.x;
     PipeR pipe;
+    SplitG spl;  // fast mode: kSplitWarps warps split the columns of the tile
     const uint16_t* tile = nullptr;
     if (b < nT + nP) {
         const bool is_true = b < nT;
         const int rb = is_true ? b : b - nT;
         tile = m.gate + (is_true ? l : l + 1) * m.gate_stride + static_cast<long long>(rb) * H * 32;
-        pipe.init(pipe_mem, kL2EvictLast);
-        pipe.prime(tile, H);
+        if (SMOE_FAST(m)) {
+            spl.prime(tile, H);
+        } else {
+            pipe.init(pipe_mem, kL2EvictLast);
+            pipe.prime(tile, H);
+        }
     }
     Stager sg;
     sg.init(bar);
@@ -832,9 +863,9 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     if (b < nT + nP) {
         const bool is_true = b < nT;
         const int rb = is_true ? b : b - nT;
-        const float acc = pipe.run(tile, H, xs);
+        const float acc = SMOE_FAST(m) ? spl.run(tile, H, xs, reinterpret_cast<float*>(pipe_mem)) : pipe.run(tile, H, xs);
         const int e = rb * 32 + (threadIdx.x & 31);
-        if (e < E) {
+        if (threadIdx.x < 32 && e < E) {
             if (is_true)
                 st.lg_true[static_cast<long long>(l) * E + e] = acc;
             else
@@ -849,6 +880,7 @@ __global__ void __launch_bounds__(32) k_router(DevModel m, DevState st, DevCtl c
     const bool has_b = static_cast<int>(gridDim.x) > nT;  // predictor / quasi CTAs exist
     int* gate_cnt = gridDim.y > 1 ? st.log_cnt + l : st.counters + (in_true ? 0 : 4);
     if (!last_cta(gate_cnt, in_true ? nT : gridDim.x - nT)) return;
+    if (threadIdx.x >= 32) return;  // the decision is one warp's
     PHASE();
     double* se = reinterpret_cast<double*>(pipe_mem);            // [E]
     float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);  // [E]
@@ -1050,8 +1082,12 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
     if (*(volatile int*)ctl.error) return;
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     float* xs = reinterpret_cast<float*>(g_smem + 128);
-    float* gs = xs + round_up(H, 32);
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(H, 32)));
+    // only the input vector is staged (the gain is read once from L2 by the
+    // norm), which keeps k_ffn_gu at ~41 KB so five CTAs fit per SM and the
+    // next launch's CTAs are resident (weights primed) while this one drains;
+    // the fused grid keeps 2 vectors of room for h (gu_stage_floats)
+    unsigned char* pipe_mem =
+        align128(reinterpret_cast<unsigned char*>(xs + (fused ? 2 : 1) * round_up(H, 32)));
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     if (slot < 0) {
         if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
@@ -1088,17 +1124,16 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
     sg.init(bar);
     if (s_from_r) {
         sg.add(xs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
-        sg.add(gs, m.moe_gain + static_cast<long long>(layer) * H, H * 4);
         const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32),
                                                     m.Hp / 32, H, m.eps);
         sg.wait();
-        block_apply_norm(xs, gs, H, scale, xs);
+        block_apply_norm(xs, m.moe_gain + static_cast<long long>(layer) * H, H, scale, xs);
     } else {
         sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
         sg.wait();
     }
     PHASE();
-    const float acc = pipe.run(tile, H, xs);
+    const float acc = chain_run(pipe, m, tile, H, xs);
     PHASE();
     const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
     const int lane = threadIdx.x & 31;
@@ -1118,6 +1153,70 @@ __device__ __forceinline__ void ffn_gu_body(const DevModel& m, const DevState& s
 __global__ void __launch_bounds__(32) k_ffn_gu(DevModel m, DevState st, DevCtl ctl, int layer,
                                                int exec_src, int s_from_r) {
     ffn_gu_body(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false);
+}
+
+// Gate/up with W row-tile warps per CTA (grid (ceil(Hmp/16 / W), K)).  Same
+// arithmetic as k_ffn_gu — every lane still walks one SwiGLU row's columns in
+// order — but the warps of a CTA sit on distinct SM sub-partitions (warp w on
+// SMSP w % 4), so no two chains share an issue slot, and the input staging
+// and norm are shared by the W warps.  Selected by gu_warps (launch_ffn).
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_ffn_gu_w(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                     int exec_src, int s_from_r) {
+    KTRACE(9, layer);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, i = blockIdx.y;
+    const int rb = blockIdx.x * W + warp;
+    const bool active = rb < m.Hmp / 16;
+    const bool early = exec_src != 0;  // prefetch mode: decision published a layer ahead
+    if (early) {
+        wait_decision(st, ctl, layer);
+    } else {
+        pdl_wait();
+        KT_WAITED();
+    }
+    __syncthreads();
+    const int H = m.H;
+    const int e = __ldcg((exec_src ? st.id_pred : st.id_exec) + layer * m.K + i);
+    if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it (CTA-uniform)
+    wait_ready(ctl, layer);
+    if (__syncthreads_or(*(volatile int*)ctl.error)) return;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    float* xs = reinterpret_cast<float*>(g_smem + 128);
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + round_up(H, 32))) +
+                              warp * round_up(PipeGU::kBytes, 128);
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    if (slot < 0) {
+        if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+        return;
+    }
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
+                           static_cast<long long>(rb) * H * 32;
+    PipeGU pipe;
+    if (active) {
+        pipe.init(pipe_mem, kL2EvictFirst);
+        pipe.prime(tile, H);
+    }
+    if (early) {
+        pdl_wait();
+        KT_WAITED();
+    }
+    pdl_trigger();  // every CTA is past its copy wait (k_ffn_down reads ids / slot_of early)
+    Stager sg;
+    sg.init(bar);
+    if (s_from_r) {
+        sg.add(xs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
+        const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32),
+                                                    m.Hp / 32, H, m.eps);
+        sg.wait();
+        block_apply_norm(xs, m.moe_gain + static_cast<long long>(layer) * H, H, scale, xs);
+    } else {
+        sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
+        sg.wait();
+    }
+    if (!active) return;
+    const float acc = chain_run(pipe, m, tile, H, xs);
+    const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
+    if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
 }
 
 // Single-GPU epilogue of one 32-row block of executed expert i's down
@@ -1246,7 +1345,7 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
         }
         __syncwarp();
         PHASE();
-        acc = pipe.run(tile, m.Hm, hs);
+        acc = chain_run(pipe, m, tile, m.Hm, hs);
         PHASE();
     }
     if (ctl.ep.world > 1) {
@@ -1383,7 +1482,7 @@ __global__ void __launch_bounds__(32) k_ffn(DevModel m, DevState st, DevCtl ctl,
             down_block_epilogue(m, st, gts, layer, rb1, i, acc_b);
             PHASE();
         } else {
-            const float acc = pipe.run(ta, m.Hm, hs);
+            const float acc = chain_run(pipe, m, ta, m.Hm, hs);
             down_block_epilogue(m, st, gts, layer, rb0, i, acc);
         }
     }
@@ -1478,7 +1577,7 @@ __global__ void __launch_bounds__(32) k_ep_mix(DevModel m, DevState st, DevCtl c
 // ------------------------------------------------------------ final / argmax --
 // h = rms_norm(x, final_gain); logits = unembed . h (model.cpp:388-389);
 // greedy argmax, first maximum (model.cpp:391-396).
-__global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ctl,
+__global__ void __launch_bounds__(32 * kSplitWarps) k_final(DevModel m, DevState st, DevCtl ctl,
                                               int record_token) {
     KTRACE(12, 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
@@ -1486,9 +1585,15 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
     float* xs = reinterpret_cast<float*>(g_smem + 128);
     float* gs = xs + round_up(m.H, 32);
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(gs + round_up(m.H, 32)));
+    const uint16_t* tile = m.unemb + static_cast<long long>(blockIdx.x) * m.H * 32;
     PipeBL pipe;
-    pipe.init(pipe_mem);
-    pipe.prime(m.unemb + static_cast<long long>(blockIdx.x) * m.H * 32, m.H);
+    SplitG sp;
+    if (SMOE_FAST(m)) {
+        sp.prime(tile, m.H);
+    } else {
+        pipe.init(pipe_mem);
+        pipe.prime(tile, m.H);
+    }
     Stager sg;
     sg.init(bar);
     pdl_wait();
@@ -1501,10 +1606,11 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
     sg.wait();
     block_apply_norm(xs, gs, m.H, scale, xs);
     const int rb = blockIdx.x;
-    const float acc = pipe.run(m.unemb + static_cast<long long>(rb) * m.H * 32, m.H, xs);
+    const float acc = SMOE_FAST(m) ? sp.run(tile, m.H, xs, reinterpret_cast<float*>(pipe_mem)) : pipe.run(tile, m.H, xs);
     const int v = rb * 32 + (threadIdx.x & 31);
-    if (v < m.V) st.logits[v] = acc;
+    if (threadIdx.x < 32 && v < m.V) st.logits[v] = acc;
     if (!last_cta(st.counters + 2, gridDim.x)) return;
+    if (threadIdx.x >= 32) return;
     // argmax_token (model.cpp:391-396): first maximum, warp-parallel
     int best = -1;
     float bv = -INFINITY;
@@ -1535,6 +1641,13 @@ __global__ void __launch_bounds__(32) k_final(DevModel m, DevState st, DevCtl ct
 }
 
 // ----------------------------------------------------------- calibration ----
+
+// Marks every layer's predicted decision as published for the current pass
+// (profiling the prefetch form of the expert kernels outside a decode pass).
+__global__ void k_mark_decided(DevState st, int L) {
+    const int p = __ldcg(st.pass_id);
+    for (int l = threadIdx.x; l < L; l += blockDim.x) st.dec_ready[l] = p;
+}
 
 __global__ void k_dv_accum(DevModel m, DevState st, double* sums, long long* counts, int layer) {
     pdl_wait();
@@ -1795,14 +1908,37 @@ size_t wo_smem(const DevModel&) { return 128 + kMaxD * 4 + 32 * 4 + 128 + PipeB:
 // Router CTAs stay small enough (Q30: ~72 KB with q_l from k_wo) to co-reside
 // with three k_ffn_gu CTAs, so the side-stream router never waits for SM space.
 size_t router_smem(const DevModel& m, int needs_dv) {
-    const size_t head = 128 + (3 + (needs_dv ? static_cast<size_t>(m.K) : 0)) * vec_bytes(m.H) + 128;
-    return head + (PipeR::kBytes > kMaxE * 12 ? PipeR::kBytes : kMaxE * 12);
+    const size_t head = 256 + (3 + (needs_dv ? static_cast<size_t>(m.K) : 0)) * vec_bytes(m.H) + 128;
+    // fast mode: no weight pipe (SplitLdg), only the warps' partial sums
+    const size_t body = m.fast ? kRouterSplitWarps * 32 * 4 : PipeR::kBytes;
+    return head + (body > kMaxE * 12 ? body : kMaxE * 12);
 }
 size_t est_smem(const DevModel& m) {
     int cols = m.est_d > m.est_mlp ? m.est_d : m.est_mlp;
     return vec_bytes(cols) + 64 + 128 + (PipeF::kBytes > kMaxE * 12 ? PipeF::kBytes : kMaxE * 12);
 }
-size_t gu_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeGU::kBytes; }
+size_t gu_smem(const DevModel& m) { return 128 + vec_bytes(m.H) + 128 + PipeGU::kBytes; }
+constexpr int kGuWarps = 1;
+size_t gu_w_smem(const DevModel& m, int w) {
+    return 128 + vec_bytes(m.H) + 128 + static_cast<size_t>(w) * round_up(PipeGU::kBytes, 128);
+}
+// warps per gate/up CTA (SMOE_GU_WARPS: 1 = k_ffn_gu, 2/3/4 = k_ffn_gu_w<W>)
+int gu_warps() {
+    static const int w = std::getenv("SMOE_GU_WARPS") ? std::atoi(std::getenv("SMOE_GU_WARPS")) : kGuWarps;
+    return w >= 1 && w <= 4 ? w : 1;
+}
+cudaError_t launch_gu(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer, int exec_src,
+                      int s_from_r, cudaStream_t s) {
+    const int w = gu_warps(), nt = m.Hmp / 16;
+    switch (w) {
+    case 2: PDL(k_ffn_gu_w<2>, dim3((nt + 1) / 2, m.K), 64, gu_w_smem(m, 2), s, m, st, ctl, layer, exec_src, s_from_r); break;
+    case 3: PDL(k_ffn_gu_w<3>, dim3((nt + 2) / 3, m.K), 96, gu_w_smem(m, 3), s, m, st, ctl, layer, exec_src, s_from_r); break;
+    case 4: PDL(k_ffn_gu_w<4>, dim3((nt + 3) / 4, m.K), 128, gu_w_smem(m, 4), s, m, st, ctl, layer, exec_src, s_from_r); break;
+    default: PDL(k_ffn_gu, dim3(nt, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+    }
+    return cudaSuccess;
+}
+size_t ffn_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeGU::kBytes; }
 size_t down_smem(const DevModel& m) { return 128 + static_cast<size_t>(m.Hmp) * 4 + 128 + PipeD::kBytes; }
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
@@ -1825,7 +1961,7 @@ std::string kernel_limit_violation(const DevModel& m) {
         const char* name;
         size_t bytes, limit;
     } v[] = {{"k_qkv", qkv_smem(m), 200 * 1024},     {"k_wo", wo_smem(m), 200 * 1024},
-             {"k_router", router_smem(m, 0), 200 * 1024}, {"k_ffn_gu", gu_smem(m), 200 * 1024},
+             {"k_router", router_smem(m, 0), 200 * 1024}, {"k_ffn_gu", gu_w_smem(m, gu_warps()), (gu_warps() > 1 ? 227u : 200u) * 1024},
              {"k_ffn_down", down_smem(m), 220 * 1024}, {"k_final", final_smem(m), 200 * 1024},
              {"k_attn", attn_smem(m), 220 * 1024}};
     for (const Need& n : v)
@@ -1858,14 +1994,14 @@ int attn_grid_for(const DevModel& m, int device) {
 int ffn_fused_ok(const DevModel& m, int device) {
     int nb = 0, sms = 0;
     if (m.Hmp > 2 * round_up(m.H, 32)) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ffn, 32, gu_smem(m)) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ffn, 32, ffn_smem(m)) != cudaSuccess) return 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
     const long long grid = static_cast<long long>(m.Hmp / 16) * m.K;
     return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
 }
 
 int max_dynamic_smem_needed(const DevModel& m) {
-    size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), gu_smem(m), down_smem(m),
+    size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), ffn_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
     size_t mx = 0;
     for (size_t x : v) mx = x > mx ? x : mx;
@@ -1913,7 +2049,8 @@ cudaError_t preload_kernels() {
                          (const void*)k_final, (const void*)k_dv_accum, (const void*)k_dv_freeze,
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
-                         (const void*)k_ffn};
+                         (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
+                         (const void*)k_ffn_gu_w<4>};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -1931,13 +2068,16 @@ cudaError_t preload_kernels() {
                          (const void*)k_est_stage, (const void*)k_ffn_gu, (const void*)k_final};
     for (const void* f : big)
         if ((e = set_smem(f, 200 * 1024)) != cudaSuccess) return e;
+    const void* gu_w[] = {(const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>, (const void*)k_ffn_gu_w<4>};
+    for (const void* f : gu_w)
+        if ((e = set_smem(f, 227 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
 cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStream_t s) {
-    PDL(k_qkv, m.QKVp / 32, 32, qkv_smem(m), s, m, st, layer);
+    PDL(k_qkv, m.QKVp / 32, m.fast ? 32 * kSplitWarps : 32, qkv_smem(m), s, m, st, layer);
     return counted(1);
 }
 
@@ -1976,14 +2116,16 @@ cudaError_t launch_router(const DevModel& m, const DevState& st, const DevCtl& c
     DevState sh = shadow ? *shadow : st;
     const int needs_dv = (rl.pred_kind == kRouterPF || rl.pred_kind == kEstPF) && !rl.quasi_ready;
     if (router_smem(m, needs_dv) > 200 * 1024) return cudaErrorInvalidConfiguration;
-    PDL(k_router, grid, 32, router_smem(m, needs_dv), s, m, st, ctl, rl, sh, shadow ? 1 : 0);
+    PDL(k_router, grid, m.fast ? 32 * kRouterSplitWarps : 32, router_smem(m, needs_dv), s, m, st, ctl, rl, sh,
+        shadow ? 1 : 0);
     return counted(1);
 }
 
 cudaError_t launch_log_routers(const DevModel& m, const DevState& st, const DevCtl& ctl, int l0,
                                int nl, int step_tag, cudaStream_t s) {
     RouterLaunch rl{l0, 1, kNone, -1, 0, 0, step_tag, 0};
-    PDL(k_router, dim3(m.Ep / 32, nl), 32, router_smem(m, 0), s, m, st, ctl, rl, st, 0);
+    PDL(k_router, dim3(m.Ep / 32, nl), m.fast ? 32 * kRouterSplitWarps : 32, router_smem(m, 0), s, m, st, ctl, rl,
+        st, 0);
     return counted(1);
 }
 
@@ -2000,10 +2142,13 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
     if (ctl.ep.world == 1 && m.ffn_fused) {
-        PDL(k_ffn, (m.Hmp / 16) * m.K, 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+        PDL(k_ffn, (m.Hmp / 16) * m.K, 32, ffn_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
         return counted(1);
     }
-    PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+    {
+        const cudaError_t e = launch_gu(m, st, ctl, layer, exec_src, s_from_r, s);
+        if (e != cudaSuccess) return e;
+    }
     PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, exec_src);
     if (ctl.ep.world > 1) {
         PDL(k_ep_mix, m.Hp / 32, 32, 0, s, m, st, ctl, layer, exec_src);
@@ -2012,18 +2157,29 @@ cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl,
     return counted(2);
 }
 
+// Per-kernel timing (Session::profile_kernels): part 0 = k_ffn_gu as on-demand
+// launches it (decision from this layer's router: PDL wait first), 2 = as the
+// prefetch path launches it for layers >= 1 (decision published a layer ahead:
+// slot lookup and weight stream start before the PDL wait; the flags are set
+// by k_mark_decided), 1 = k_ffn_down.
 cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                             int part, cudaStream_t s) {
-    if (part == 0)
-        PDL(k_ffn_gu, dim3(m.Hmp / 16, m.K), 32, gu_smem(m), s, m, st, ctl, layer, 0, 0);
-    else
+    if (part == 0 || part == 2) {
+        const cudaError_t e = launch_gu(m, st, ctl, layer, part == 2, part == 2, s);
+        if (e != cudaSuccess) return e;
+    } else
         PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, 0);
+    return counted(1);
+}
+
+cudaError_t launch_mark_decided(const DevState& st, int L, cudaStream_t s) {
+    k_mark_decided<<<1, 64, 0, s>>>(st, L);
     return counted(1);
 }
 
 cudaError_t launch_final(const DevModel& m, const DevState& st, const DevCtl& ctl,
                          int record_token, cudaStream_t s) {
-    PDL(k_final, m.Vp / 32, 32, final_smem(m), s, m, st, ctl, record_token);
+    PDL(k_final, m.Vp / 32, m.fast ? 32 * kSplitWarps : 32, final_smem(m), s, m, st, ctl, record_token);
     return counted(1);
 }
 

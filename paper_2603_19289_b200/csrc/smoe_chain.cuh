@@ -560,7 +560,139 @@ struct WarpPipe {
         ctr += nch;
         return acc;
     }
+
+    // Tolerance ("fast") decode arithmetic: the same weight stream and the
+    // same lane-per-row result, but the row's dot product is carried in four
+    // independent packed f32 partial sums (column pairs 0-1, 2-3, 4-5, 6-7 of
+    // every group) with fused multiply-adds (FFMA2), summed at the end.  No
+    // dependent chain: the loop is issue-bound (~15 instructions per 8
+    // columns) instead of FADD-latency bound, so the kernel is HBM-bound.
+    // Differs from the reference's sequential sum by rounding only (DESIGN
+    // "Decode arithmetic modes").  bf16 weights only.
+    __device__ __forceinline__ float run_fast(const WT* tile, int cols, const float* xs) {
+        static_assert(sizeof(WT) == 2, "fast chains take bf16 weights");
+        constexpr int GPC = CC / G;
+        const int lane = threadIdx.x & 31;
+        const int nch = (cols + CC - 1) / CC;
+        if (lane == 0 && !primed)
+            for (int n = 0; n < S && n < nch; ++n) issue(tile, cols, n, ctr + n);
+        primed = 0;
+        const uint32_t xbase = smem_u32(xs);
+        const uint32_t lbase = sbuf + lane * 16;
+        const int c0 = ctr;
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        for (int n = 0; n < nch; ++n) {
+            const int g = c0 + n;
+            mbar_wait(&full[g % S], static_cast<uint32_t>((g / S) & 1));
+            const uint32_t cb = lbase + (g % S) * kChunkBytes;
+            const uint32_t xc = xbase + n * CC * 4;
+            const int cn = min(CC, cols - n * CC);
+            if (cn == CC) {
+#pragma unroll
+                for (int j = 0; j < GPC; ++j) {
+                    const uint4 w = lds128(cb + j * 512);
+                    const float4 xa = lds128f(xc + j * 32), xb = lds128f(xc + j * 32 + 16);
+                    a0 = __ffma2_rn(make_float2(lo_bf(w.x), hi_bf(w.x)), make_float2(xa.x, xa.y), a0);
+                    a1 = __ffma2_rn(make_float2(lo_bf(w.y), hi_bf(w.y)), make_float2(xa.z, xa.w), a1);
+                    a2 = __ffma2_rn(make_float2(lo_bf(w.z), hi_bf(w.z)), make_float2(xb.x, xb.y), a2);
+                    a3 = __ffma2_rn(make_float2(lo_bf(w.w), hi_bf(w.w)), make_float2(xb.z, xb.w), a3);
+                }
+            } else {
+                const int ng = cn / G;
+                for (int j = 0; j < ng; ++j) {
+                    const uint4 w = lds128(cb + j * 512);
+                    const float4 xa = lds128f(xc + j * 32), xb = lds128f(xc + j * 32 + 16);
+                    a0 = __ffma2_rn(make_float2(lo_bf(w.x), hi_bf(w.x)), make_float2(xa.x, xa.y), a0);
+                    a1 = __ffma2_rn(make_float2(lo_bf(w.y), hi_bf(w.y)), make_float2(xa.z, xa.w), a1);
+                    a2 = __ffma2_rn(make_float2(lo_bf(w.z), hi_bf(w.z)), make_float2(xb.x, xb.y), a2);
+                    a3 = __ffma2_rn(make_float2(lo_bf(w.w), hi_bf(w.w)), make_float2(xb.z, xb.w), a3);
+                }
+                const int tail = cn - ng * G;
+                if (tail) {
+                    const uint4 w = lds128(cb + ng * 512);
+                    const float* xt = xs + n * CC + ng * G;
+                    for (int i = 0; i < tail; ++i) a0.x = fmaf(group_elem(w, i, WT{}), xt[i], a0.x);
+                }
+            }
+            __syncwarp();  // every lane is done with this stage: refill it
+            if (n + S < nch && elect_one()) issue(tile, cols, n + S, g + S);
+        }
+        ctr += nch;
+        return ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+    }
 };
+
+// Tolerance-mode GEMV of one 32-row bf16 tile split over the columns across
+// the CTA's warps (the exact chain cannot be split: it is one sequential
+// sum).  Warp w takes a contiguous slice of 8-column groups; each lane loads
+// its row's groups with 16-byte LDGs straight into registers (a warp-wide
+// load is 512 contiguous bytes of the tile), NB groups in flight, the first
+// batch issued before the kernel's PDL wait (weights never depend on the
+// activations).  Packed FFMA partial sums per lane; the warps' sums meet in
+// shared memory and warp 0 adds them in warp order (deterministic).  Used by
+// the few-tile decode kernels (qkv, routers, unembed), whose single-warp
+// chains are latency bound: 16 warps x 8 KB per tile go out in one round trip.
+template <int NB>
+struct SplitLdg {
+    uint4 wv[NB];
+    int g0, g1;  // this warp's groups [g0, g1)
+    __device__ __forceinline__ void load(const uint16_t* tile, int gb) {
+        const uint4* tp = reinterpret_cast<const uint4*>(tile) + (threadIdx.x & 31);
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+            if (gb + u < g1) wv[u] = __ldg(tp + static_cast<long long>(gb + u) * 32);
+    }
+    __device__ __forceinline__ void prime(const uint16_t* tile, int cols) {
+        const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+        const int ng = (cols + 7) / 8;
+        const int per = (ng + nw - 1) / nw;
+        g0 = min(ng, w * per);
+        g1 = min(ng, g0 + per);
+        load(tile, g0);
+    }
+    // red: [nwarps][32] floats of shared memory.  Returns the row sum in warp 0.
+    __device__ __forceinline__ float run(const uint16_t* tile, int cols, const float* xs, float* red) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        for (int gb = g0; gb < g1; gb += NB) {
+            if (gb != g0) load(tile, gb);
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int g = gb + u;
+                if (g < g1) {
+                    const uint4 wq = wv[u];
+                    float4 xa = *reinterpret_cast<const float4*>(xs + g * 8);
+                    float4 xb = *reinterpret_cast<const float4*>(xs + g * 8 + 4);
+                    if (g * 8 + 8 > cols) {  // ragged last group: columns >= cols contribute 0
+                        const int t = cols - g * 8;
+                        if (t <= 0) xa.x = 0.f;
+                        if (t <= 1) xa.y = 0.f;
+                        if (t <= 2) xa.z = 0.f;
+                        if (t <= 3) xa.w = 0.f;
+                        if (t <= 4) xb.x = 0.f;
+                        if (t <= 5) xb.y = 0.f;
+                        if (t <= 6) xb.z = 0.f;
+                        xb.w = 0.f;
+                    }
+                    a0 = __ffma2_rn(make_float2(lo_bf(wq.x), hi_bf(wq.x)), make_float2(xa.x, xa.y), a0);
+                    a1 = __ffma2_rn(make_float2(lo_bf(wq.y), hi_bf(wq.y)), make_float2(xa.z, xa.w), a1);
+                    a2 = __ffma2_rn(make_float2(lo_bf(wq.z), hi_bf(wq.z)), make_float2(xb.x, xb.y), a2);
+                    a3 = __ffma2_rn(make_float2(lo_bf(wq.w), hi_bf(wq.w)), make_float2(xb.z, xb.w), a3);
+                }
+            }
+        }
+        red[w * 32 + lane] = ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+        __syncthreads();
+        float s = 0.0f;
+        if (w == 0)
+            for (int q = 0; q < nw; ++q) s += red[q * 32 + lane];
+        return s;
+    }
+};
+constexpr int kSplitWarps = 16;       // warps per tile in the tolerance-mode split GEMVs (qkv, unembed)
+constexpr int kRouterSplitWarps = 8;  // routers: 256 threads x <= 128 registers, so a side-stream
+                                      // predictor CTA still fits beside three expert CTAs
+using SplitG = SplitLdg<16>;
 
 // Multi-token variant (batched prefill): the same bf16 row tile applied to nt
 // <= T tokens at once — T independent sequential chains per lane, one weight
@@ -714,7 +846,10 @@ using PipeB = WarpPipe<uint16_t, kS, kCCb>;
 #ifndef SMOE_GU_STAGES
 #define SMOE_GU_STAGES 6
 #endif
-using PipeGU = WarpPipe<uint16_t, SMOE_GU_STAGES, kCCb>;  // expert gate/up: deeper HBM stream per warp
+#ifndef SMOE_GU_CC
+#define SMOE_GU_CC 128
+#endif
+using PipeGU = WarpPipe<uint16_t, SMOE_GU_STAGES, SMOE_GU_CC>;  // expert gate/up: deeper HBM stream per warp
 using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
 using PipeF = WarpPipe<float, kS, kCCf>;
 using PipeD = WarpPipe<uint16_t, kS, kCCd>;

@@ -60,6 +60,7 @@ struct DevModel {
     int Ep, Vp, QKVp;   // router / unembed / qkv rows padded to 32
     int cap;            // KV capacity (positions)
     float inv_sqrt_d;   // 1.0f / sqrtf(D), computed on the host like model.cpp:336
+    int fast;           // decode GEMV arithmetic: 0 exact (reference order), 1 tolerance (run_fast)
     const uint16_t* emb;      // [V][H] row-major bf16
     const uint16_t* unemb;    // row tiles of unembed [V][H]
     const float* final_gain;  // [H]

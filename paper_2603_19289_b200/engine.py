@@ -36,7 +36,7 @@ EXPORTS = [
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info", "smoe_decide", "smoe_layer_hit_rates",
-    "smoe_select_hybrid_map", "smoe_set_prefill_mode",
+    "smoe_select_hybrid_map", "smoe_set_prefill_mode", "smoe_set_decode_mode",
 ]
 
 
@@ -513,10 +513,15 @@ class Session:
         _check(self.lib.smoe_clear_stats(self._h))
 
     def profile_kernels(self, reps: int = 3) -> dict:
-        out = np.zeros(8, np.float64)
+        out = np.zeros(9, np.float64)
         _check(self.lib.smoe_profile_kernels(self._h, reps, _p(out)))
-        names = ["qkv", "attn", "wo", "router", "ffn_gate_up", "ffn_down", "final", "ffn"]
+        names = ["qkv", "attn", "wo", "router", "ffn_gate_up", "ffn_down", "final", "ffn",
+                 "ffn_gate_up_prefetch"]
         return dict(zip(names, out.tolist()))
+
+    def set_decode_mode(self, mode: str):
+        """'exact' (sequential chains, bit parity) or 'fast' (packed FFMA partial sums, tolerance)."""
+        _check(self.lib.smoe_set_decode_mode(self._h, {"exact": 0, "fast": 1}[mode]))
 
     def set_prefill_mode(self, mode: str):
         """'exact' (sequential chains, bit parity) or 'tensor' (tcgen05 expert GEMMs, tolerance)."""

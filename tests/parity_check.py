@@ -25,6 +25,12 @@ Only one layer's experts are generated at a time (lazy oracle model), so a
 compared for bit equality; a routing decision that differs is classified by the
 oracle's logit gap at the deciding boundary (a near-tie when the gap is below
 ``eps``) and reported, never hidden.
+
+With ``rtol > 0`` (the tolerance decode mode, smoe_set_decode_mode(1)) every
+float vector is compared by its norm-relative error ||gpu - ref|| / ||ref||
+against rtol instead (the largest error per field is reported), the ids and
+the greedy token must still be equal unless the oracle's gap at the deciding
+boundary is below ``eps`` (reported as a near-tie).
 """
 from __future__ import annotations
 
@@ -45,19 +51,42 @@ class Report:
     near_ties: list = field(default_factory=list)   # (field, t, l, gap)
     mismatches: list = field(default_factory=list)  # (field, t, l, detail)
     min_boundary_gap: float = float("inf")
+    max_rel_err: dict = field(default_factory=dict)  # tolerance mode: field -> largest error
+    rtol: float = 0.0
 
     def add(self, f, ok):
         self.checked[f] += 1
         self.exact[f] += int(ok)
 
+    def vec(self, f, want, got, t, l):
+        """Bit equality, or (rtol > 0) norm-relative error within rtol."""
+        want = np.asarray(want, np.float32)
+        got = np.asarray(got, np.float32)
+        if np.array_equal(want, got):
+            self.add(f, True)
+            return
+        if self.rtol > 0:
+            err = float(np.linalg.norm(got.astype(np.float64) - want) /
+                        max(np.linalg.norm(want.astype(np.float64)), 1e-30))
+            self.max_rel_err[f] = max(self.max_rel_err.get(f, 0.0), err)
+            self.add(f, False)
+            if err > self.rtol:
+                self.mismatches.append((f, t, l, err))
+            return
+        self.add(f, False)
+        self.mismatches.append((f, t, l, float(np.abs(want - got).max())))
+
     def ok(self) -> bool:
         return not self.mismatches
 
     def summary(self) -> dict:
-        return {"checked": self.checked, "exact": self.exact,
-                "near_ties": len(self.near_ties), "near_tie_list": self.near_ties[:20],
-                "mismatches": len(self.mismatches), "mismatch_list": self.mismatches[:20],
-                "min_boundary_gap": self.min_boundary_gap}
+        out = {"checked": self.checked, "exact": self.exact,
+               "near_ties": len(self.near_ties), "near_tie_list": self.near_ties[:20],
+               "mismatches": len(self.mismatches), "mismatch_list": self.mismatches[:20],
+               "min_boundary_gap": self.min_boundary_gap}
+        if self.rtol > 0:
+            out.update({"rtol": self.rtol, "max_rel_err": self.max_rel_err})
+        return out
 
 
 def boundary_gap(orc, logits, k, gating):
@@ -72,7 +101,7 @@ def boundary_gap(orc, logits, k, gating):
 
 
 def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
-                 threads: int | None = None) -> dict:
+                 threads: int | None = None, rtol: float = 0.0) -> dict:
     """runs: [(name, trace, mode)], each trace over S recorded positions (prompt
     rows first): tok_in [S], s/r/m [S][L][H], lg_true/lg_pred [S][L][E],
     id_*/g_* [S][L][K], y [S][L][K][H], logits [S][V], tokens [S] (argmax of
@@ -87,7 +116,7 @@ def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
     ones = np.ones(H, np.float32)
     pool = cf.ThreadPoolExecutor(max_workers=threads or os.cpu_count() or 1)
     tb = orc.table(np.asarray(table, np.float32)) if table is not None else None
-    reps = {name: Report() for name, _, _ in runs}
+    reps = {name: Report(rtol=rtol) for name, _, _ in runs}
     xs = {name: np.stack([emb[int(t)] for t in tr["tok_in"]]).astype(np.float32)
           for name, tr, _ in runs}  # x_0 of every row
     for l in range(L):
@@ -98,29 +127,15 @@ def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
             r_gpu, s_gpu = tr["r"][:, l], tr["s"][:, l]
             R = om.attn_layer(l, xs[name])  # the K/V history needs every position
             for t in range(S):
-                ok = np.array_equal(R[t], r_gpu[t])
-                rep.add("attn_r", ok)
-                if not ok:
-                    rep.mismatches.append(("attn_r", t, l, float(np.abs(R[t] - r_gpu[t]).max())))
+                rep.vec("attn_r", R[t], r_gpu[t], t, l)
                 s_ref = orc.rms_norm(r_gpu[t], ones, eps)
-                ok = np.array_equal(s_ref, s_gpu[t])
-                rep.add("s", ok)
-                if not ok:
-                    rep.mismatches.append(("s", t, l, float(np.abs(s_ref - s_gpu[t]).max())))
+                rep.vec("s", s_ref, s_gpu[t], t, l)
                 lg = om.linear(f"layer{l}.gate", E, s_gpu[t])
-                ok = np.array_equal(lg, tr["lg_true"][t, l])
-                rep.add("lg_true", ok)
-                if not ok:
-                    rep.mismatches.append(("lg_true", t, l, float(np.abs(lg - tr["lg_true"][t, l]).max())))
+                rep.vec("lg_true", lg, tr["lg_true"][t, l], t, l)
                 ids, gates = orc.make_decision(lg, K, gating)
                 gap = boundary_gap(orc, lg, K, gating)
                 rep.min_boundary_gap = min(rep.min_boundary_gap, gap)
-                for f, want, got in (("id_true", ids, tr["id_true"][t, l]),
-                                     ("g_true", gates, tr["g_true"][t, l])):
-                    ok = np.array_equal(want, got)
-                    rep.add(f, ok)
-                    if not ok:
-                        (rep.near_ties if gap < eps_tie else rep.mismatches).append((f, t, l, gap))
+                _decision(rep, ids, gates, tr["id_true"][t, l], tr["g_true"][t, l], "true", t, l, gap, eps_tie)
                 decode_row = spec and t >= P and l >= 1
                 want_exec = tr["id_pred"][t, l] if decode_row else tr["id_true"][t, l]
                 ok = np.array_equal(tr["id_exec"][t, l], want_exec)
@@ -137,20 +152,12 @@ def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
                     orc.lib.orc_quasi_hidden(np.ascontiguousarray(r_gpu[t]).ctypes.data, d.ctypes.data,
                                              ones.ctypes.data, H, eps, q.ctypes.data)
                     lgp = om.linear(f"layer{l + 1}.gate", E, q)
-                    ok = np.array_equal(lgp, tr["lg_pred"][t, l + 1])
-                    rep.add("lg_pred", ok)
-                    if not ok:
-                        rep.mismatches.append(("lg_pred", t, l + 1,
-                                               float(np.abs(lgp - tr["lg_pred"][t, l + 1]).max())))
+                    rep.vec("lg_pred", lgp, tr["lg_pred"][t, l + 1], t, l + 1)
                     pids, pg = orc.make_decision(lgp, K, gating)
                     gap = boundary_gap(orc, lgp, K, gating)
                     rep.min_boundary_gap = min(rep.min_boundary_gap, gap)
-                    for f, want, got in (("id_pred", pids, tr["id_pred"][t, l + 1]),
-                                         ("g_pred", pg, tr["g_pred"][t, l + 1])):
-                        ok = np.array_equal(want, got)
-                        rep.add(f, ok)
-                        if not ok:
-                            (rep.near_ties if gap < eps_tie else rep.mismatches).append((f, t, l + 1, gap))
+                    _decision(rep, pids, pg, tr["id_pred"][t, l + 1], tr["g_pred"][t, l + 1], "pred", t, l + 1,
+                              gap, eps_tie)
             ex[name] = tr["id_exec"][:, l]
         # this layer's experts: the union over every run, generated once
         need = sorted({int(e) for name in ex for row in ex[name] for e in row})
@@ -166,18 +173,12 @@ def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
                 for i in range(K):
                     y = jobs[(t, i)].result()
                     ys.append(y)
-                    ok = np.array_equal(y, tr["y"][t, l, i])
-                    rep.add("y", ok)
-                    if not ok:
-                        rep.mismatches.append(("y", t, l, float(np.abs(y - tr["y"][t, l, i]).max())))
+                    rep.vec("y", y, tr["y"][t, l, i], t, l)
                 mm = np.zeros(H, np.float32)
                 g_ex = tr["g_exec"][t, l]
                 for i in range(K):  # moe_block mixture, f32 in decision order
                     mm = mm + np.float32(g_ex[i]) * ys[i]
-                ok = np.array_equal(mm, m_gpu[t])
-                rep.add("m", ok)
-                if not ok:
-                    rep.mismatches.append(("m", t, l, float(np.abs(mm - m_gpu[t]).max())))
+                rep.vec("m", mm, m_gpu[t], t, l)
             xs[name] = (tr["r"][:, l] + tr["m"][:, l]).astype(np.float32)  # next layer's input
         om.release_experts(l, need)
     for name, tr, mode in runs:  # final norm + unembed + greedy argmax
@@ -185,16 +186,30 @@ def check_traces(orc, om, cfg: dict, runs, table=None, eps_tie: float = 1e-6,
         for t in range(tr["s"].shape[0]):
             xn = orc.rms_norm(xs[name][t], ones, eps)
             lo = om.linear("unembed", cfg["vocab"], xn)
-            ok = np.array_equal(lo, tr["logits"][t])
-            rep.add("logits", ok)
-            if not ok:
-                rep.mismatches.append(("logits", t, L, float(np.abs(lo - tr["logits"][t]).max())))
+            rep.vec("logits", lo, tr["logits"][t], t, L)
             ok = int(np.argmax(lo)) == int(tr["tokens"][t])
             rep.add("token", ok)
             if not ok:
-                rep.mismatches.append(("token", t, L, int(np.argmax(lo))))
+                top2 = np.sort(lo.astype(np.float64))[-2:]
+                gap = float(top2[1] - top2[0])
+                if rtol > 0 and gap < eps_tie:
+                    rep.near_ties.append(("token", t, L, gap))
+                else:
+                    rep.mismatches.append(("token", t, L, int(np.argmax(lo))))
     pool.shutdown()
     return reps
+
+
+def _decision(rep, ids, gates, got_ids, got_g, kind, t, l, gap, eps_tie):
+    """Routing ids exact (a differing id at a boundary gap below eps_tie is a
+    reported near-tie); gates exact, or within rtol in tolerance mode."""
+    ok = np.array_equal(ids, got_ids)
+    rep.add(f"id_{kind}", ok)
+    if not ok:
+        (rep.near_ties if gap < eps_tie else rep.mismatches).append((f"id_{kind}", t, l, gap))
+        rep.add(f"g_{kind}", False)  # gates of another expert set: not comparable
+        return
+    rep.vec(f"g_{kind}", gates, got_g, t, l)
 
 
 def gpu_trace(s, S: int, P: int) -> dict:

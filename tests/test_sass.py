@@ -15,8 +15,11 @@ BUILD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                      "paper_2603_19289_b200", "csrc", "build")
 OBJ = os.path.join(BUILD, "kernels.o")
 # every object whose chains must keep the reference's separately rounded
-# products and adds (decode, batched prefill / decode, estimator training)
-CHAIN_OBJS = ("kernels.o", "prefill.o", "train_dev.o")
+# products and adds (decode, batched prefill / decode, estimator training).
+# The decode library also holds the tolerance mode (smoe_set_decode_mode(1):
+# packed FFMA partial sums by design), so the decode kernels are checked in
+# the exact-only build of the same source (kernels_exact.o, -DSMOE_EXACT_ONLY).
+CHAIN_OBJS = ("kernels_exact.o", "prefill.o", "train_dev.o")
 
 
 def _sass(obj=OBJ):
@@ -44,8 +47,16 @@ def test_no_packed_fma_anywhere(obj):
 
 
 def test_chain_kernels_use_separate_products_and_adds():
-    fns = _functions(_sass())
+    fns = _functions(_sass(os.path.join(BUILD, "kernels_exact.o")))
     for short in ("k_qkv", "k_ffn_gu", "k_ffn_down", "k_router", "k_final", "k_wo"):
         body = "\n".join(next(v for k, v in fns.items() if short in k))
         assert "FMUL2" in body, short
         assert "FADD" in body, short
+
+
+def test_tolerance_mode_uses_packed_fma():
+    """The shipped decode object does carry the tolerance mode's FFMA2 chains."""
+    fns = _functions(_sass())
+    for short in ("k_qkv", "k_ffn_gu", "k_ffn_down", "k_router", "k_final"):
+        body = "\n".join(next(v for k, v in fns.items() if short in k))
+        assert "FFMA2" in body, short
