@@ -202,7 +202,8 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     cap = P + (args.warmup + args.steps) * 2 + 16
     t0 = time.time()
     # expert parallel over `world` GPUs: this rank owns experts e % world == rank
-    lc = args.long_prompt if world == 1 and not args.ncu else 0
+    lcs = [x for x in args.long_prompts if x > 0] if world == 1 and not args.ncu else []
+    lc = max(lcs) if lcs else 0
     s = Session(cfg, device=dev, cache_fraction=1.0,
                 max_positions=max(cap, 300, lc + args.warmup + args.steps + 16),
                 ep_rank=rank, ep_world=world)
@@ -222,6 +223,10 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     dv, counts = s.calibrate(args.calib_tokens, 2, 256)
     t_cal = time.time() - t0
     s.set_predictor(args.predictor)
+    # decode GEMV arithmetic of the headline: "fast" (tolerance mode, packed FFMA
+    # partial sums; parity: tests/test_gpu_fast.py, 48-layer teacher-forced check)
+    # or "exact" (the reference's sequential chains, bit-identical)
+    s.set_decode_mode(args.decode_mode)
     prompt = token_stream(P, c["vocab"], 3)
     # teacher-forced decode inputs (random_token_stream seed 4): routing changes
     # every token as with real text, so the 25 % cache really misses
@@ -294,6 +299,14 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     # kernel-level measurement (CUDA events on the compute stream) and link peak
     prof = s.profile_kernels(reps=3)
     link = s.measure_link(128)
+    # the other decode arithmetic on the same session and workload (headline
+    # workload, both offload modes, kernel timings), then back
+    other_mode = "exact" if args.decode_mode == "fast" else "fast"
+    s.set_decode_mode(other_mode)
+    alt = {"decode_mode": other_mode,
+           **{mode: measure(mode, args.workload) for mode in ("on_demand", "prefetch")}}
+    alt["kernel_us"] = s.profile_kernels(reps=3)
+    s.set_decode_mode(args.decode_mode)
     # end-to-end through the C ABI with host buffers (token H2D, logits D2H per step)
     # (stream workload: the host feeds the forced token each step; greedy: the argmax)
     s.reset(P + args.warmup + args.steps + 4, False)
@@ -312,22 +325,38 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     slots = s.cache_slots()
     path = s.path_info()
     # long context (PAPER.md:423 prompts of 1k-64k tokens): the prompt through the
-    # batched prefill, then the headline stream workload
+    # batched prefill, then the headline stream workload in both
+    # offload modes and both decode arithmetic modes
     long_ctx = None
-    if lc:
-        lp = token_stream(lc, c["vocab"], 5)
-        s.reset(lc + args.warmup + args.steps, False)
-        t0 = time.perf_counter()
-        s.prefill_batched(lp)
-        pf_ms = (time.perf_counter() - t0) * 1e3
-        s.decode_stream("prefetch", forced[: args.warmup])
-        s.clear_stats()
-        s.decode_stream("prefetch", forced[args.warmup:])
-        long_ctx = {"prompt_len": lc, "prefill_ms": pf_ms, "prefill_how": "smoe_prefill_batched, wall clock",
-                    "tpot_prefetch_ms": float(np.mean(s.token_ms())), "workload": args.workload,
-                    "cache_fraction": args.cache_fraction}
+    if lcs:
+        n_lc = max(2, min(args.steps, 16))
+        rows = []
+        for plen in lcs:
+            lp = token_stream(plen, c["vocab"], 5)
+            row = {"prompt_len": plen}
+            for dm in (args.decode_mode, other_mode):
+                s.set_decode_mode(dm)
+                for mode in ("prefetch", "on_demand"):
+                    s.reset(plen + n_lc + 4, False)
+                    t0 = time.perf_counter()
+                    s.prefill_batched(lp)
+                    row["prefill_ms"] = (time.perf_counter() - t0) * 1e3
+                    s.decode_stream(mode, forced[:2])
+                    s.clear_stats()
+                    s.decode_stream(mode, forced[2:2 + n_lc])
+                    ms = s.token_ms()
+                    cnt = s.counters()
+                    key = f"{dm}_{mode}" if dm != args.decode_mode else mode
+                    row[f"tpot_{key}_ms"] = float(np.mean(ms))
+                    row[f"tpot_{key}_sd"] = float(np.std(ms))
+                    row[f"misses_per_token_{key}"] = float(cnt["misses"].sum()) / n_lc
+            rows.append(row)
+        s.set_decode_mode(args.decode_mode)
+        long_ctx = {"rows": rows, "steps": n_lc, "workload": args.workload, "cache_fraction": args.cache_fraction,
+                    "decode_mode": args.decode_mode,
+                    "prefill_how": "smoe_prefill_batched (exact chains), wall clock"}
     s.close()
-    return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, t_alloc=t_alloc, t_init=t_init, slots=slots,
+    return dict(res=res, prof=prof, link=link, e2e_ms=e2e_ms, alt=alt, t_alloc=t_alloc, t_init=t_init, slots=slots,
                 t_cal=t_cal, dv_nonzero=int((counts > 0).sum()), cfg=c, P=P, long_ctx=long_ctx,
                 dv=dv[: max(args.ref_depths)] if rank == 0 else None, resident=resident, path=path)
 
@@ -456,6 +485,24 @@ def reference_arm(args) -> dict:
                           dv, tuple(args.ref_depths))
 
 
+def _modes_block(args, pf, od, prof, alt, gu_bytes, hbm_peak) -> dict:
+    """Headline workload TPOT and the gate/up roofline in both decode arithmetic modes."""
+    def one(p, o, kp):
+        us = kp.get("ffn_gate_up_prefetch") or kp["ffn_gate_up"]
+        return {"tpot_prefetch_ms": p["tpot_ms"], "tpot_on_demand_ms": o["tpot_ms"],
+                "tpot_reduction_pct": 100.0 * (o["tpot_ms"] - p["tpot_ms"]) / o["tpot_ms"],
+                "gate_up_us": us, "gate_up_frac": gu_bytes / (us * 1e-6) / 1e9 / hbm_peak,
+                "kernel_us": kp}
+    out = {args.decode_mode: one(pf, od, prof)}
+    if alt:
+        out[alt["decode_mode"]] = one(alt["prefetch"], alt["on_demand"], alt["kernel_us"])
+    out["parity"] = {"exact": "bit-identical to the reference (tests/test_gpu*.py)",
+                     "fast": "hidden states / logits within rtol 2e-5 (norm-relative), ids exact "
+                             "except near-ties below 1e-5 (reported); 48-layer headline check: "
+                             "tests/test_gpu_fast.py, profiles/r02_parity"}
+    return out
+
+
 # ----------------------------------------------------------------- main -----
 
 def main():
@@ -466,8 +513,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="q30", choices=list(CONFIGS))
     ap.add_argument("--prompt-len", type=int, default=32)
-    ap.add_argument("--long-prompt", type=int, default=2048,
-                    help="extra long-context measurement (0 = off): prompt via batched prefill")
+    ap.add_argument("--long-prompts", type=int, nargs="*", default=[1024, 4096, 16384],
+                    help="long-context measurement (PAPER.md:423; none = off): prompt via batched "
+                         "prefill, then the headline workload in both offload and decode modes")
     ap.add_argument("--cache-fraction", type=float, default=0.25)
     ap.add_argument("--predictor", default="router-pf")
     ap.add_argument("--calib-tokens", type=int, default=2000)
@@ -489,6 +537,11 @@ def main():
     ap.add_argument("--workload", default="stream", choices=["stream", "greedy"],
                     help="stream: decode inputs teacher-forced from a random token stream "
                          "(headline; exercises the offload path); greedy: argmax feedback")
+    ap.add_argument("--decode-mode", default="fast", choices=["fast", "exact"],
+                    help="decode GEMV arithmetic of the headline: fast = tolerance mode (packed FFMA "
+                         "partial sums, ids exact except reported near-ties, tests/test_gpu_fast.py); "
+                         "exact = the reference's sequential chains, bit-identical; the other mode is "
+                         "measured on the headline workload too (decode_modes)")
     ap.add_argument("--layers", type=int, default=0,
                     help="depth truncation (0 = the config's depth, cut to the host-RAM budget of the "
                          "pinned expert store when it does not fit)")
@@ -512,7 +565,8 @@ def main():
                 "decode_inputs": ("teacher-forced random_token_stream(seed 4)" if args.workload == "stream"
                                   else "greedy argmax feedback"),
                 "layers_run": args.layers_run,
-                "depth_truncated": args.layers_run < full_layers}
+                "depth_truncated": args.layers_run < full_layers,
+                "decode_mode": args.decode_mode}
 
     if args.impl == "reference":
         if rank != 0:
@@ -593,8 +647,12 @@ def main():
         gu_name, gu_bytes, gu_us = "k_ffn", K * 3 * Hm * H * 2, prof["ffn"]
         gu_desc = "k_ffn (fused expert FFN: gate/up + down GEMV, one launch per layer)"
     else:
-        gu_name, gu_bytes, gu_us = "k_ffn_gu", K * 2 * Hm * H * 2, prof["ffn_gate_up"]
-        gu_desc = "k_ffn_gu (expert gate+up GEMV)"
+        # as the headline (prefetch) decode launches it for layers >= 1: decision
+        # published a layer ahead, weight stream started before the PDL wait
+        gu_name, gu_bytes = "k_ffn_gu", K * 2 * Hm * H * 2
+        gu_us = prof.get("ffn_gate_up_prefetch") or prof["ffn_gate_up"]
+        gu_desc = (f"k_ffn_gu (expert gate+up GEMV, {args.decode_mode} decode arithmetic, "
+                   "prefetch-path launch form)")
     achieved = gu_bytes / (gu_us * 1e-6) / 1e9
     hb = hbm_bytes_per_token(c, out["P"])
     link = out["link"]
@@ -662,8 +720,12 @@ def main():
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
                                        "dram__bytes_read.sum + dram__bytes_write.sum per launch)",
                      "bytes_per_launch": gu_bytes, "avg_launch_us": gu_us,
+                     "avg_launch_us_on_demand_form": prof["ffn_gate_up"],
+                     "timing": "CUDA events on the compute stream around L back-to-back launches "
+                               "(one per layer, distinct weights, 3 repetitions), Session::profile_kernels",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
         "kernel_us": prof,
+        "decode_modes": _modes_block(args, pf, od, prof, out.get("alt"), gu_bytes, hbm_peak),
         "path": out.get("path"),
         "cache": {"slots_per_layer": out.get("slots"), "hits_prefetch": pf["cache_hits"],
                   "misses_prefetch": pf["cache_misses"], "hits_on_demand": od["cache_hits"],

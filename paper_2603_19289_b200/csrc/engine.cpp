@@ -678,8 +678,8 @@ void Session::alloc() {
     ctl_.ep.epoch = d_epoch_;
     d_hybrid_ = static_cast<int*>(dalloc(4ull * L));
     // e [cap] f64 | p [cap] f32 (+pad) | split-attention control words and maxima
-    d_attn_scratch_ = static_cast<double*>(dalloc(16ull * m.cap + 1024));
-    dset(d_attn_scratch_, 0, 16ull * m.cap + 1024, "attn scratch");
+    d_attn_scratch_ = static_cast<double*>(dalloc(attn_scratch_bytes(m.cap)));
+    dset(d_attn_scratch_, 0, attn_scratch_bytes(m.cap), "attn scratch");
     d_prompt_tok_ = static_cast<int*>(dalloc(4ull * m.cap));
 
     m.emb = d_emb_;

@@ -653,6 +653,194 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn(DevModel m, DevState st, 
 #endif
 }
 
+// Tolerance-mode decode attention (DevModel::fast): split-K "flash decoding".
+// The positions are sliced over the CTAs that have any (grid sized for the KV
+// capacity, up to kAttnFastCtas; at least kAttnFastChunk positions each).  A
+// CTA streams its K and V rows through a 2-chunk cp.async ring in shared
+// memory (rows before `pos` are final, so the first chunks are requested
+// before the PDL wait), thread j scores position j of a chunk (q . k_j, four
+// f32 partial sums), and the CTA keeps an online softmax: running max m, sum
+// l and context acc (thread i owns dim i), rescaled by exp(m_old - m) per
+// chunk.  CTAs publish (m, l, acc[D]); the last to arrive merges them in CTA
+// order, normalises and writes ctx.  Same math as softmax + context
+// (model.cpp:337-351) up to f32 rounding (f32 exp, no sequential f64
+// partition): a 16 k-token context streams its 16 MB of K/V per layer at HBM
+// rate instead of one f64 chain over all positions.
+constexpr int kAttnFastThreads = 128;  // >= head_dim (thread i owns context dim i)
+constexpr int kAttnFastChunk = 32;     // positions per ring slot (66 KB of ring at head_dim 128: 3 CTAs per SM)
+constexpr int kAttnFastCtas = 296;     // 2 per SM
+__device__ __forceinline__ float* attn_fast_scratch(const DevModel& m, double* scratch) {
+    return reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(scratch) + 16ull * m.cap + 1024);
+}
+bool attn_fast_ok(const DevModel& m) { return SMOE_FAST(m) && m.D % 4 == 0 && m.D <= kAttnFastThreads; }
+size_t attn_fast_smem(const DevModel& m) { return 2ull * kAttnFastChunk * (2 * m.D + 4) * 4; }
+size_t attn_scratch_bytes(int cap) {
+    return 16ull * cap + 1024 + static_cast<size_t>(kAttnFastCtas) * (kMaxD + 2) * 4 + 64;
+}
+
+__global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevState st, double* scratch,
+                                                                int layer) {
+    KTRACE(2, layer);
+    const int D = m.D, KS = D + 4;  // padded key rows: thread j's LDS.128 of row j is conflict-free
+    __shared__ __align__(16) float qs[kAttnFastThreads];
+    __shared__ float red[kAttnFastThreads / 32];
+    __shared__ float s_l;
+    __shared__ int s_last;
+    float* kt = reinterpret_cast<float*>(g_smem);  // [2][chunk][D+4]
+    float* vt = kt + 2 * kAttnFastChunk * KS;      // [2][chunk][D]
+    __shared__ float ps[kAttnFastChunk];
+    const long long base = static_cast<long long>(layer) * m.cap * D;
+    const float* K = st.kc + base;
+    const float* V = st.vc + base;
+    float* part = attn_fast_scratch(m, scratch);  // [G][kMaxD + 2]: m, l, acc
+    int* cnt = reinterpret_cast<int*>(part + kAttnFastCtas * (kMaxD + 2));
+    // st.pos is only advanced by k_final, which completed before this grid could launch
+    const int pos = __ldcg(st.pos), n = pos + 1, b = blockIdx.x;
+    const int ppc = max(4 * kAttnFastChunk, (n + gridDim.x - 1) / gridDim.x);
+    const int G = (n + ppc - 1) / ppc;  // CTAs with positions
+    if (b >= G) {
+        pdl_wait();
+        pdl_trigger();
+        return;
+    }
+    const int j0 = b * ppc, j1 = min(n, j0 + ppc), nch = (j1 - j0 + kAttnFastChunk - 1) / kAttnFastChunk;
+    auto fetch = [&](int c, int skip) {
+        const int p0 = j0 + c * kAttnFastChunk, pn = min(kAttnFastChunk, j1 - p0);
+        float* kd = kt + (c & 1) * kAttnFastChunk * KS;
+        float* vd = vt + (c & 1) * kAttnFastChunk * D;
+        const int per = D / 4;
+        for (int t = threadIdx.x; t < pn * per; t += blockDim.x) {
+            const int r = t / per, q4 = (t % per) * 4;
+            if (p0 + r == skip) continue;
+            cp_async16(kd + r * KS + q4, K + static_cast<long long>(p0 + r) * D + q4);
+            cp_async16(vd + r * D + q4, V + static_cast<long long>(p0 + r) * D + q4);
+        }
+    };
+    fetch(0, pos);  // rows before pos are final: requested before the PDL wait
+    cp_async_commit();
+    if (nch > 1) fetch(1, pos);
+    cp_async_commit();
+    pdl_wait();  // q and row pos come from k_qkv
+    KT_WAITED();
+    pdl_trigger();
+    for (int t = threadIdx.x; t < D / 4; t += blockDim.x) {
+        cp_async16(qs + 4 * t, st.q + 4 * t);
+        const int c = (pos - j0) / kAttnFastChunk, r = (pos - j0) % kAttnFastChunk;
+        if (pos >= j0 && pos < j1 && c < 2) {
+            cp_async16(kt + (c & 1) * kAttnFastChunk * KS + r * KS + 4 * t, K + static_cast<long long>(pos) * D + 4 * t);
+            cp_async16(vt + (c & 1) * kAttnFastChunk * D + r * D + 4 * t, V + static_cast<long long>(pos) * D + 4 * t);
+        }
+    }
+    cp_async_commit();
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    float mrun = -INFINITY, lrun = 0.0f, acc = 0.0f;
+    for (int c = 0; c < nch; ++c) {
+        if (c >= 1 && c + 1 < nch)
+            cp_async_wait<1>();  // chunk c landed; chunk c + 1 may still be in flight
+        else
+            cp_async_wait<0>();  // (c = 0: q and row pos too)
+        __syncthreads();
+        const int p0 = j0 + c * kAttnFastChunk, pn = min(kAttnFastChunk, j1 - p0);
+        const float* kc = kt + (c & 1) * kAttnFastChunk * KS;
+        const float* vc = vt + (c & 1) * kAttnFastChunk * D;
+        float sj = -INFINITY;
+        if (tid < pn) {
+            const float* kj = kc + tid * KS;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < D; i += 4) {
+                const float4 kv = *reinterpret_cast<const float4*>(kj + i);
+                const float4 qv = *reinterpret_cast<const float4*>(qs + i);
+                a0 = fmaf(qv.x, kv.x, a0);
+                a1 = fmaf(qv.y, kv.y, a1);
+                a2 = fmaf(qv.z, kv.z, a2);
+                a3 = fmaf(qv.w, kv.w, a3);
+            }
+            sj = ((a0 + a1) + (a2 + a3)) * m.inv_sqrt_d;
+        }
+        float cm = sj;
+        for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+        if (lane == 0) red[w] = cm;
+        __syncthreads();
+        cm = red[0];
+        for (int q = 1; q < nw; ++q) cm = fmaxf(cm, red[q]);
+        const float mn = fmaxf(mrun, cm);
+        const float sc = __expf(mrun - mn);  // 0 on the first chunk
+        const float p = tid < pn ? __expf(sj - mn) : 0.0f;
+        if (tid < kAttnFastChunk) ps[tid] = p;
+        float cs = p;
+        for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        __syncthreads();  // red (max) read by all; ps complete
+        if (lane == 0) red[w] = cs;
+        __syncthreads();
+        float csum = 0.0f;
+        for (int q = 0; q < nw; ++q) csum += red[q];
+        lrun = lrun * sc + csum;
+        mrun = mn;
+        if (tid < D) {
+            float a = acc * sc;
+            for (int j = 0; j < pn; ++j) a = fmaf(ps[j], vc[j * D + tid], a);
+            acc = a;
+        }
+        __syncthreads();  // ring slot and ps free
+        if (c + 2 < nch) {
+            fetch(c + 2, -1);
+            cp_async_commit();
+        }
+    }
+    if (G == 1) {  // one CTA holds every position: no merge
+        if (tid < D) st.ctx[tid] = acc / lrun;
+        return;
+    }
+    float* pb = part + static_cast<long long>(b) * (kMaxD + 2);
+    if (tid == 0) {
+        pb[0] = mrun;
+        pb[1] = lrun;
+    }
+    if (tid < D) pb[2 + tid] = acc;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(cnt, 1) == G - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) *cnt = 0;
+    // merge: the CTAs' maxima and weights in parallel (f[q] = exp(m_q - M)),
+    // then thread i sums dim i over the CTAs in CTA order, loads in flight
+    __shared__ float fq[kAttnFastCtas];
+    float M = -INFINITY;
+    for (int q = tid; q < G; q += blockDim.x) M = fmaxf(M, __ldcg(part + static_cast<long long>(q) * (kMaxD + 2)));
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) red[w] = M;
+    __syncthreads();
+    M = red[0];
+    for (int q = 1; q < nw; ++q) M = fmaxf(M, red[q]);
+    for (int q = tid; q < G; q += blockDim.x) {
+        const float* pq = part + static_cast<long long>(q) * (kMaxD + 2);
+        fq[q] = __expf(__ldcg(pq) - M);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float Lt = 0.0f;
+        for (int q = 0; q < G; ++q) Lt = fmaf(fq[q], __ldcg(part + static_cast<long long>(q) * (kMaxD + 2) + 1), Lt);
+        s_l = Lt;
+    }
+    float a = 0.0f;
+    if (tid < D) {
+        int q = 0;
+        for (; q + 8 <= G; q += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + static_cast<long long>(q + u) * (kMaxD + 2) + 2 + tid);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a = fmaf(fq[q + u], v[u], a);
+        }
+        for (; q < G; ++q) a = fmaf(fq[q], __ldcg(part + static_cast<long long>(q) * (kMaxD + 2) + 2 + tid), a);
+    }
+    __syncthreads();
+    if (tid < D) st.ctx[tid] = a / s_l;
+}
+
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
 // SMOE_DOWN_L2=1: k_ffn_gu warms L2 with the down-projection blocks (measured
 // neutral on Q30: down gets faster, gate/up slower by as much)
@@ -2050,7 +2238,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
                          (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
-                         (const void*)k_ffn_gu_w<4>};
+                         (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -2072,6 +2260,7 @@ cudaError_t preload_kernels() {
     for (const void* f : gu_w)
         if ((e = set_smem(f, 227 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_attn_fast, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
@@ -2083,6 +2272,11 @@ cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStr
 
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
+    if (attn_fast_ok(m)) {  // tolerance mode: flash-decoding split over positions
+        const int g = static_cast<int>(std::min<long long>(kAttnFastCtas, std::max(1, m.cap / kAttnFastChunk)));
+        PDL(k_attn_fast, g, kAttnFastThreads, attn_fast_smem(m), s, m, st, scratch, layer);
+        return counted(1);
+    }
     static const int split = std::getenv("SMOE_ATTN_SPLIT") ? std::atoi(std::getenv("SMOE_ATTN_SPLIT")) : 1;
     PDL(k_attn, split && m.attn_grid > 1 ? m.attn_grid : 1, kAttnThreads, attn_smem(m), s, m, st, scratch, layer);
     return counted(1);

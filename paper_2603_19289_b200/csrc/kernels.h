@@ -58,6 +58,7 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 // s_from_r 1: normalise r_l inside the kernel (routers run concurrently).
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src = 0, int s_from_r = 0);
+size_t attn_scratch_bytes(int cap);  // split / fast attention scratch for a KV capacity
 cudaError_t launch_mark_decided(const DevState& st, int L, cudaStream_t s);
 cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                             int part, cudaStream_t s);

@@ -86,6 +86,16 @@ def test_fast_mode_q30_layers_teacher_forced(lib):
     _run(dict(Q30, layers=3), 16, 8, 0.25, 256, "q30_L3")
 
 
+def test_fast_mode_long_context_toy(lib):
+    """Flash-decoding attention over 700+ positions (several CTAs, ragged slices)."""
+    _run(dict(TOY, layers=3), 700, 6, 0.5, 64, "toy_long")
+
+
+def test_fast_mode_long_context_q30_layers(lib):
+    """head_dim 128 (float4 lanes) over 1100+ positions."""
+    _run(dict(Q30, layers=2), 1100, 4, 0.25, 256, "q30_L2_long")
+
+
 def test_fast_mode_headline_q30_48_layers(lib):
     """The bench's headline workload in the tolerance mode."""
     reps = _run(Q30, 32, 12, 0.25, 2000, "q30_L48")
