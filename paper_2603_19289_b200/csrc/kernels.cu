@@ -264,11 +264,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps) k_qkv(DevModel m, DevState s
     }
     Stager sg;
     sg.init(bar);
+    sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);  // static: before the PDL wait
     pdl_wait();
     KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
-    sg.add(gs, m.attn_gain + static_cast<long long>(layer) * m.H, m.H * 4);
     // the epilogue's position and RoPE factors load while the chain runs
     const int lane = threadIdx.x & 31;
     const int R = rb * 32 + lane;
@@ -1020,13 +1020,17 @@ __global__ void __launch_bounds__(32 * kRouterSplitWarps) k_router(DevModel m, D
     }
     Stager sg;
     sg.init(bar);
+    // the norm gains are static: staged before the PDL wait, the activations after
+    const bool norm_s = b < nT || (b < nT + nP && rl.pred_kind == kBaselineS);
+    const bool norm_q = !norm_s && b < nT + nP + nQ && rl.quasi_ready;
+    if (norm_s) sg.add(gs, m.moe_gain + static_cast<long long>(l) * H, H * 4);
+    if (norm_q) sg.add(gs, m.moe_gain + static_cast<long long>(l + 1) * H, H * 4);
     pdl_wait();
     KT_WAITED();
     PHASE();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
-    if (b < nT || (b < nT + nP && rl.pred_kind == kBaselineS)) {
+    if (norm_s) {
         sg.add(rs, st.r + static_cast<long long>(l) * m.Hp, H * 4);
-        sg.add(gs, m.moe_gain + static_cast<long long>(l) * H, H * 4);
         const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(l) * (m.Hp / 32),
                                                     m.Hp / 32, H, m.eps);
         sg.wait();
@@ -1036,7 +1040,6 @@ __global__ void __launch_bounds__(32 * kRouterSplitWarps) k_router(DevModel m, D
     } else if (b < nT + nP + nQ) {
         if (rl.quasi_ready) {  // q_l = rms_norm(r_l + d_l, gain_{l+1}) from k_wo's rd_l
             sg.add(rs, st.rd + static_cast<long long>(l) * m.Hp, H * 4);
-            sg.add(gs, m.moe_gain + static_cast<long long>(l + 1) * H, H * 4);
             const float scale = rms_scale_from_partials(
                 st.ssq_rd + static_cast<long long>(l) * (m.Hp / 32), m.Hp / 32, H, m.eps);
             sg.wait();
@@ -1073,8 +1076,12 @@ __global__ void __launch_bounds__(32 * kRouterSplitWarps) k_router(DevModel m, D
     double* se = reinterpret_cast<double*>(pipe_mem);            // [E]
     float* sp = reinterpret_cast<float*>(pipe_mem + kMaxE * 8);  // [E]
     if (in_true) {
-        warp_decision(st.lg_true + static_cast<long long>(l) * E, E, K, m.gating, sp, se,
-                      st.id_true + l * K, st.g_true + l * K);
+        if (SMOE_FAST(m) && E <= 256)
+            warp_decision_fast(st.lg_true + static_cast<long long>(l) * E, E, K, st.id_true + l * K,
+                               st.g_true + l * K);
+        else
+            warp_decision(st.lg_true + static_cast<long long>(l) * E, E, K, m.gating, sp, se,
+                          st.id_true + l * K, st.g_true + l * K);
         if (threadIdx.x == 0 && rl.exec_from == 0) {
             copy_decision(st.id_true + l * K, st.g_true + l * K, st.id_exec + l * K, st.g_exec + l * K, K);
             if (rl.post_exec && !ctl.resident) post_request(m, ctl, l, rl.step_tag, st.id_exec + l * K, K);
@@ -1082,8 +1089,14 @@ __global__ void __launch_bounds__(32 * kRouterSplitWarps) k_router(DevModel m, D
     }
     if (!in_true || !has_b) {
         if (gemv_pred)
-            warp_decision(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, m.gating, sp, se,
-                          st.id_pred + (l + 1) * K, st.g_pred + (l + 1) * K);
+        {
+            if (SMOE_FAST(m) && E <= 256)
+                warp_decision_fast(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, st.id_pred + (l + 1) * K,
+                                   st.g_pred + (l + 1) * K);
+            else
+                warp_decision(st.lg_pred + static_cast<long long>(l + 1) * E, E, K, m.gating, sp, se,
+                              st.id_pred + (l + 1) * K, st.g_pred + (l + 1) * K);
+        }
         if (threadIdx.x == 0) {
             if (rl.pred_kind == kOracle && has_shadow) {  // Oracle: shadow true decisions (speculation.cpp:296-305)
                 for (int i = 0; i < K; ++i) {
@@ -1784,11 +1797,11 @@ __global__ void __launch_bounds__(32 * kSplitWarps) k_final(DevModel m, DevState
     }
     Stager sg;
     sg.init(bar);
+    sg.add(gs, m.final_gain, m.H * 4);  // static: before the PDL wait
     pdl_wait();
     KT_WAITED();
     pdl_trigger();  // after our own dependency: dependents launch at most one kernel ahead
     sg.add(xs, st.x, m.H * 4);
-    sg.add(gs, m.final_gain, m.H * 4);
     const float scale = rms_scale_from_partials(st.ssq_x + static_cast<long long>(m.L) * (m.Hp / 32),
                                                 m.Hp / 32, m.H, m.eps);
     sg.wait();

@@ -1182,6 +1182,74 @@ __device__ inline void warp_decision(const float* logits, int E, int K, int gati
     DEC_T(4);
 }
 
+// Tolerance-mode make_decision (model.cpp:258-274) for E <= 256: the top-k is
+// taken on the logits themselves (exp is monotonic, so the order equals the
+// order of the softmax probabilities except where two probabilities round to
+// the same f32 — a near-tie the parity checker reports), and the gates of
+// both gating orders are, in real arithmetic, the softmax of the K selected
+// logits (softmax-topk-renorm: p_i / sum_top p_j = e_i / sum_top e_j, the
+// partition cancels), computed in f32.  No f64 exponentials over all E and no
+// sequential partition: ~1/4 of warp_decision's cycles.
+__device__ inline void warp_decision_fast(const float* logits, int E, int K, int* ids, float* gates) {
+    const int lane = threadIdx.x & 31;
+    constexpr int U = 8;
+    unsigned kk[U];
+    int ix[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = u * 32 + lane;
+        kk[u] = i < E ? f32_key(__ldcg(logits + i)) : 0u;
+        ix[u] = i;
+    }
+#define SMOE_CX(a, b)                                             \
+    do {                                                          \
+        if (kk[b] > kk[a] || (kk[b] == kk[a] && ix[b] < ix[a])) { \
+            const unsigned tk = kk[a];                            \
+            kk[a] = kk[b];                                        \
+            kk[b] = tk;                                           \
+            const int ti = ix[a];                                 \
+            ix[a] = ix[b];                                        \
+            ix[b] = ti;                                           \
+        }                                                         \
+    } while (0)
+    SMOE_CX(0, 1); SMOE_CX(2, 3); SMOE_CX(4, 5); SMOE_CX(6, 7);
+    SMOE_CX(0, 2); SMOE_CX(1, 3); SMOE_CX(4, 6); SMOE_CX(5, 7);
+    SMOE_CX(1, 2); SMOE_CX(5, 6);
+    SMOE_CX(0, 4); SMOE_CX(1, 5); SMOE_CX(2, 6); SMOE_CX(3, 7);
+    SMOE_CX(2, 4); SMOE_CX(3, 5);
+    SMOE_CX(1, 2); SMOE_CX(3, 4); SMOE_CX(5, 6);
+#undef SMOE_CX
+    int my_idx = 0;
+    float my_val = -INFINITY;
+    for (int t = 0; t < K; ++t) {
+        const unsigned wk = __reduce_max_sync(0xffffffffu, kk[0]);
+        const unsigned wi = __reduce_max_sync(0xffffffffu, kk[0] == wk ? 0xFFFFFFFFu - static_cast<unsigned>(ix[0]) : 0u);
+        const int idx = static_cast<int>(0xFFFFFFFFu - wi);
+        if ((idx & 31) == lane) {
+#pragma unroll
+            for (int u = 0; u + 1 < U; ++u) {
+                kk[u] = kk[u + 1];
+                ix[u] = ix[u + 1];
+            }
+            kk[U - 1] = 0u;
+            ix[U - 1] = 0x7fffffff;
+        }
+        if (lane == t) {
+            my_idx = idx;
+            my_val = key_f32(wk);
+        }
+    }
+    const float mx = __shfl_sync(0xffffffffu, my_val, 0);  // rank 0 holds the maximum
+    const float e = lane < K ? __expf(my_val - mx) : 0.0f;
+    float z = e;
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (lane < K) {
+        ids[lane] = my_idx;
+        gates[lane] = e / z;
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------- launching --
 // Every decode-path kernel is launched with programmatic stream
 // serialization (PDL); captured into the step graph as programmatic edges.
