@@ -16,6 +16,8 @@ if resident:
     s.preload_all()  # no copy-lane waits: ncu serialises streams
 s.calibrate(32, 2, 256)
 s.set_predictor("router-pf")
+import os
+s.set_decode_mode(os.environ.get("SMOE_DECODE_MODE", "fast"))
 prompt = (np.arange(8) * 37 % 256).astype(np.int32)
 s.reset(64)
 s.prefill(prompt)
