@@ -517,6 +517,8 @@ def main():
                     help="long-context measurement (PAPER.md:423; none = off): prompt via batched "
                          "prefill, then the headline workload in both offload and decode modes")
     ap.add_argument("--cache-fraction", type=float, default=0.25)
+    ap.add_argument("--cache-policy", default="lru", choices=["lru", "lfu"],
+                    help="slot replacement: lru, or lfu (least requested so far, then least recent)")
     ap.add_argument("--predictor", default="router-pf")
     ap.add_argument("--calib-tokens", type=int, default=2000)
     ap.add_argument("--runs", type=int, default=3)
@@ -546,6 +548,7 @@ def main():
                     help="depth truncation (0 = the config's depth, cut to the host-RAM budget of the "
                          "pinned expert store when it does not fit)")
     args = ap.parse_args()
+    os.environ["SMOE_CACHE_POLICY"] = args.cache_policy  # read by every SlotCache (engine.cpp)
     if args.ncu:
         args.cache_fraction, args.runs, args.no_cpu_baseline = 1.0, 1, True
 
@@ -566,7 +569,7 @@ def main():
                                   else "greedy argmax feedback"),
                 "layers_run": args.layers_run,
                 "depth_truncated": args.layers_run < full_layers,
-                "decode_mode": args.decode_mode}
+                "decode_mode": args.decode_mode, "cache_policy": args.cache_policy}
 
     if args.impl == "reference":
         if rank != 0:
@@ -649,9 +652,11 @@ def main():
     else:
         # as the headline (prefetch) decode launches it for layers >= 1: decision
         # published a layer ahead, weight stream started before the PDL wait
-        gu_name, gu_bytes = "k_ffn_gu", K * 2 * Hm * H * 2
+        # tolerance mode: the column-split kernel (k_ffn_gu_cs); exact: k_ffn_gu
+        gu_name = "k_ffn_gu_cs" if args.decode_mode == "fast" else "k_ffn_gu"
+        gu_bytes = K * 2 * Hm * H * 2
         gu_us = prof.get("ffn_gate_up_prefetch") or prof["ffn_gate_up"]
-        gu_desc = (f"k_ffn_gu (expert gate+up GEMV, {args.decode_mode} decode arithmetic, "
+        gu_desc = (f"{gu_name} (expert gate+up GEMV, {args.decode_mode} decode arithmetic, "
                    "prefetch-path launch form)")
     achieved = gu_bytes / (gu_us * 1e-6) / 1e9
     hb = hbm_bytes_per_token(c, out["P"])

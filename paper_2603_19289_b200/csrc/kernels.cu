@@ -14,6 +14,8 @@
 // rounding of the result except at measure-zero midpoints (reported by the
 // parity tests as exact-match fractions).
 #include "kernels.h"
+
+#include <atomic>
 #include "smoe_chain.cuh"
 #include "expf_glibc.cuh"
 
@@ -1420,6 +1422,118 @@ __global__ void __launch_bounds__(32 * W) k_ffn_gu_w(DevModel m, DevState st, De
     if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
 }
 
+// ---------------------------------------------- tolerance-mode expert FFN --
+//
+// Column-split expert GEMVs (DevModel::fast only).  The exact kernels give
+// each 32-row tile to ONE warp, because the reference's dot product is one
+// sequential sum; with one warp per SM sub-partition that stream is issue-
+// latency bound (ncu, profiles/r02_ncu_fast_summary.csv: ~4 cycles per
+// instruction, DRAM at 38 % of peak).  In tolerance mode the tile's columns
+// are split over kCsWarps warps of the CTA (warp w: a contiguous range of
+// 8-column groups, its own cp.async.bulk pipe of 8 KB chunks), each lane
+// keeps packed-FFMA partial sums of its row, and warp 0 adds the warps'
+// partials in warp order (deterministic) before the usual epilogue.  4x the
+// warps in flight for the same bytes; the CTA still fits three per SM.
+// Measured on Q30 (16 layers, tools/kbench.py): 10.3 us per launch in the
+// prefetch form against 12.1 us for the one-warp tile.  Also measured and
+// dropped: 8 warps (one CTA per SM: 17 us), 3-stage pipes (two CTAs per SM:
+// 14 us), register-streamed LDG tiles (18 us), and the same split for the
+// down projection (8.5 us against 7.5 us for the one-warp k_ffn_down, whose
+// whole 48 KB tile is in flight per warp).
+#ifndef SMOE_CS_WARPS
+#define SMOE_CS_WARPS 4
+#endif
+#ifndef SMOE_CS_S
+#define SMOE_CS_S 2
+#endif
+#ifndef SMOE_CS_CC
+#define SMOE_CS_CC 128
+#endif
+constexpr int kCsWarps = SMOE_CS_WARPS;
+using PipeCs = WarpPipe<uint16_t, SMOE_CS_S, SMOE_CS_CC>;  // gate/up: 2 x 8 KB per warp
+
+
+// this warp's column range [c0, c0 + n) of a `cols`-column tile
+__device__ __forceinline__ void cs_range(int cols, int& c0, int& n) {
+    const int ng = (cols + 7) / 8, per = (ng + kCsWarps - 1) / kCsWarps, w = threadIdx.x >> 5;
+    c0 = min(ng, w * per) * 8;
+    n = max(0, min(cols - c0, per * 8));
+}
+
+// red: [kCsWarps][32] floats; returns the row sum in warp 0 (others: 0)
+__device__ __forceinline__ float cs_reduce(float part, float* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    red[w * 32 + lane] = part;
+    __syncthreads();
+    float s = 0.0f;
+    if (w == 0) {
+#pragma unroll
+        for (int q = 0; q < kCsWarps; ++q) s += red[q * 32 + lane];
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                            int exec_src, int s_from_r) {
+    KTRACE(9, layer);
+    const int lane = threadIdx.x & 31, rb = blockIdx.x, i = blockIdx.y;
+    const bool early = exec_src != 0;  // prefetch mode: decision published a layer ahead
+    if (early) {
+        wait_decision(st, ctl, layer);
+    } else {
+        pdl_wait();
+        KT_WAITED();
+    }
+    __syncthreads();
+    const int H = m.H;
+    const int e = __ldcg((exec_src ? st.id_pred : st.id_exec) + layer * m.K + i);
+    if (ctl.ep.world > 1 && e % ctl.ep.world != ctl.ep.rank) return;  // a peer runs it (CTA-uniform)
+    wait_ready(ctl, layer);
+    if (__syncthreads_or(*(volatile int*)ctl.error)) return;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
+    float* red = reinterpret_cast<float*>(g_smem + 128);
+    float* xs = red + kCsWarps * 32;
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + round_up(H, 32))) +
+                              (threadIdx.x >> 5) * round_up(PipeCs::kBytes, 128);
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    if (slot < 0) {
+        if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+        return;
+    }
+    int c0, nc;
+    cs_range(H, c0, nc);
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
+                           static_cast<long long>(rb) * H * 32 + static_cast<long long>(c0) * 32;
+    PipeCs pipe;
+    if (nc > 0) {
+        pipe.init(pipe_mem, kL2EvictFirst);
+        pipe.prime(tile, nc);
+    }
+    if (early) {
+        pdl_wait();
+        KT_WAITED();
+    }
+    pdl_trigger();  // every CTA is past its copy wait (k_ffn_down reads ids / slot_of early)
+    Stager sg;
+    sg.init(bar);
+    if (s_from_r) {
+        sg.add(xs, st.r + static_cast<long long>(layer) * m.Hp, H * 4);
+        const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32),
+                                                    m.Hp / 32, H, m.eps);
+        sg.wait();
+        block_apply_norm(xs, m.moe_gain + static_cast<long long>(layer) * H, H, scale, xs);
+    } else {
+        sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
+        sg.wait();
+    }
+    // tolerance mode only (launch_gu); SMOE_FAST is constant 0 in the exact-only object
+    const float part = nc > 0 && SMOE_FAST(m) ? pipe.run_fast(tile, nc, xs + c0) : 0.0f;
+    const float acc = cs_reduce(part, red);
+    if (threadIdx.x >= 32) return;
+    const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
+    if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
+}
+
 // Single-GPU epilogue of one 32-row block of executed expert i's down
 // projection: the raw rows y_i; the last of the K arrivals on the block
 // (device-scope counter, threadfence pattern) forms the gate-weighted mixture
@@ -2011,6 +2125,55 @@ __global__ void __launch_bounds__(256) k_pred_ahead(DevModel m, TraceDev tr, int
     }
 }
 
+// ------------------------------------------------------ packed experts ----
+// Decoder of the xp12 expert block (engine.h, xpack.cpp): thread t expands
+// elements 8t..8t+7 — one 4-byte load of exponent codes, one 8-byte load of
+// sign|mantissa bytes, one 16-byte store (all coalesced); an escaped element
+// (code 15) takes its raw value from the ascending escape list (binary
+// search; ~1e-4 of Gaussian weights).  HBM-bound: 1.5 B read + 2 B written
+// per weight, ~3 us for a 9.4 MB Q30 expert, beside a ~130 us H2D.
+__global__ void __launch_bounds__(256) k_xp_unpack(const uint8_t* __restrict__ src, uint16_t* __restrict__ dst) {
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(src);
+    const uint32_t base = __ldg(hdr + 1), nesc = __ldg(hdr + 2), n8 = __ldg(hdr + 3);
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n8) return;
+    const uint8_t* codes = src + 16;
+    const uint8_t* sm = codes + static_cast<long long>(n8) * 4;
+    const uint8_t* esc = sm + static_cast<long long>(n8) * 8;
+    const uint32_t c = __ldcs(reinterpret_cast<const unsigned int*>(codes) + t);
+    const uint2 b = __ldcs(reinterpret_cast<const uint2*>(sm) + t);
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t code = (c >> (4 * j)) & 15u;
+        const uint32_t byte = ((j < 4 ? b.x : b.y) >> (8 * (j & 3))) & 0xffu;
+        uint32_t v = ((byte & 0x80u) << 8) | ((base + code) << 7) | (byte & 0x7fu);
+        if (code == 15u) {  // escape: raw value from the list (ascending indices)
+            const uint32_t idx = static_cast<uint32_t>(t * 8 + j);
+            uint32_t lo = 0, hi = nesc;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(reinterpret_cast<const uint32_t*>(esc + 8ull * mid)) < idx) lo = mid + 1;
+                else hi = mid;
+            }
+            v = __ldg(reinterpret_cast<const uint16_t*>(esc + 8ull * lo + 4));
+        }
+        if (j & 1) w[j >> 1] |= v << 16;
+        else w[j >> 1] = v;
+    }
+    reinterpret_cast<uint4*>(dst)[t] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+std::atomic<long long> g_xp_launches{0};  // copy-lane launches (outside the decode graphs)
+long long xp_unpack_launches() { return g_xp_launches.load(); }
+
+cudaError_t launch_xp_unpack(const uint8_t* src, uint16_t* dst, long long n, cudaStream_t s) {
+    const long long n8 = n / 8;
+    k_xp_unpack<<<static_cast<unsigned>((n8 + 255) / 256), 256, 0, s>>>(src, dst);
+    ++g_xp_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pred_ahead(const DevModel& m, const TraceDev& tr, int first, int n, int depth, int* out,
                               cudaStream_t s) {
     const int nb = (m.H + 31) / 32;
@@ -2128,9 +2291,16 @@ int gu_warps() {
     static const int w = std::getenv("SMOE_GU_WARPS") ? std::atoi(std::getenv("SMOE_GU_WARPS")) : kGuWarps;
     return w >= 1 && w <= 4 ? w : 1;
 }
+size_t gu_cs_smem(const DevModel& m) {
+    return 128 + kCsWarps * 32 * 4 + vec_bytes(m.H) + 128 + kCsWarps * round_up(PipeCs::kBytes, 128);
+}
 cudaError_t launch_gu(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer, int exec_src,
                       int s_from_r, cudaStream_t s) {
     const int w = gu_warps(), nt = m.Hmp / 16;
+    if (m.fast) {  // tolerance mode: column-split warps
+        PDL(k_ffn_gu_cs, dim3(nt, m.K), 32 * kCsWarps, gu_cs_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+        return cudaSuccess;
+    }
     switch (w) {
     case 2: PDL(k_ffn_gu_w<2>, dim3((nt + 1) / 2, m.K), 64, gu_w_smem(m, 2), s, m, st, ctl, layer, exec_src, s_from_r); break;
     case 3: PDL(k_ffn_gu_w<3>, dim3((nt + 2) / 3, m.K), 96, gu_w_smem(m, 3), s, m, st, ctl, layer, exec_src, s_from_r); break;
@@ -2164,6 +2334,7 @@ std::string kernel_limit_violation(const DevModel& m) {
     } v[] = {{"k_qkv", qkv_smem(m), 200 * 1024},     {"k_wo", wo_smem(m), 200 * 1024},
              {"k_router", router_smem(m, 0), 200 * 1024}, {"k_ffn_gu", gu_w_smem(m, gu_warps()), (gu_warps() > 1 ? 227u : 200u) * 1024},
              {"k_ffn_down", down_smem(m), 220 * 1024}, {"k_final", final_smem(m), 200 * 1024},
+             {"k_ffn_gu_cs", gu_cs_smem(m), 200 * 1024},
              {"k_attn", attn_smem(m), 220 * 1024}};
     for (const Need& n : v)
         if (n.bytes > n.limit)
@@ -2251,7 +2422,8 @@ cudaError_t preload_kernels() {
                          (const void*)k_trace, (const void*)k_trace_y, (const void*)k_trace_bump,
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
                          (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
-                         (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast};
+                         (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast, (const void*)k_ffn_gu_cs,
+                         (const void*)k_xp_unpack};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -2275,6 +2447,7 @@ cudaError_t preload_kernels() {
     if ((e = set_smem((const void*)k_attn, 220 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_attn_fast, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn_gu_cs, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
@@ -2374,8 +2547,9 @@ cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl&
     if (part == 0 || part == 2) {
         const cudaError_t e = launch_gu(m, st, ctl, layer, part == 2, part == 2, s);
         if (e != cudaSuccess) return e;
-    } else
+    } else {
         PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, 0);
+    }
     return counted(1);
 }
 

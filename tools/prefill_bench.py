@@ -1,5 +1,5 @@
 """Batched vs token-by-token prefill wall time (Q30 shape).  Tools only.
-    python tools/prefill_bench.py [layers] [prompt_len] [cache_fraction]"""
+    python tools/prefill_bench.py [layers] [prompt_len] [cache_fraction] [batched,tensor,token]"""
 import os
 import sys
 import time
@@ -22,15 +22,18 @@ s.set_cache_fraction(frac)
 s.set_predictor("router-pf")
 prompt = (np.arange(P) * 37 % 256).astype(np.int32)
 res = {}
-for name in ("batched", "token"):
+names = sys.argv[4].split(",") if len(sys.argv) > 4 else ["batched", "token"]
+for name in names:  # batched (exact chains), tensor (tcgen05 expert GEMMs, tolerance), token
+    s.set_prefill_mode("tensor" if name == "tensor" else "exact")
     for rep in range(2):
         s.reset(P + 4, False)
         t0 = time.perf_counter()
-        (s.prefill_batched if name == "batched" else s.prefill)(prompt)
+        (s.prefill if name == "token" else s.prefill_batched)(prompt)
         dt = time.perf_counter() - t0
     res[name] = dt
     tok = int(s.tokens(P)[P - 1])
     print(f"{name:8s} prefill of {P} tokens, {L} layers, cache {frac}: {dt * 1e3:9.1f} ms "
           f"({dt * 1e6 / P:8.1f} us/token), next token {tok}", flush=True)
-print(f"speed-up {res['token'] / res['batched']:.1f}x")
+for a in names[1:]:
+    print(f"{a} / {names[0]}: {res[a] / res[names[0]]:.2f}x")
 s.close()
