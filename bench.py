@@ -713,7 +713,13 @@ def main():
                 "all_miss_bytes_per_token": L * K * 3 * H * Hm * 2,
                 "achieved_GBps": h2d_gbps, "link_peak_GBps": link,
                 "frac": (h2d_gbps / link) if h2d_gbps else None,
-                "peak_how": "same pinned store, expert-sized cudaMemcpyAsync H2D, 128 copies"},
+                "peak_how": "same pinned store, expert-sized cudaMemcpyAsync H2D, 128 copies",
+                "store_format": ("xp12: exponent-packed bf16, lossless (12 bits per weight on the link; "
+                                 "k_xp_unpack restores the bf16 block in the HBM slot)"
+                                 if out.get("path", {}).get("store_packed_blocks") else "raw bf16"),
+                "wire_per_raw": out.get("path", {}).get("store_wire_per_raw", 1.0),
+                "bytes": "link (wire) bytes; achieved_GBps = wire bytes / copy-lane busy time, which "
+                         "includes the decode of the request's last expert"},
         "tpot_roofline": {"prefetch_ms": t_roof_pf, "on_demand_ms": t_roof_od,
                           "prefetch_frac": t_roof_pf / pf["tpot_ms"],
                           "on_demand_frac": t_roof_od / od["tpot_ms"],

@@ -337,8 +337,20 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
  * (1) or gate/up + down kernels (0); out[1] split-attention CTAs; out[2]
  * host-ordered copy waits (profiler / sanitizer attached or
  * SMOE_HOST_ORDERED=1); out[3] device-side all-hit release; out[4] NUMA node
- * the pinned expert store is bound to (-1: not bound — single-node host). */
+ * the pinned expert store is bound to (-1: not bound — single-node host);
+ * out[5] expert blocks held exponent-packed in the pinned store; out[6]
+ * link bytes per 1000 raw expert bytes. */
 int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap);
+
+/* Lossless exponent packing of one bf16 expert block ("xp12", engine.h):
+ * the pinned store's wire format (12 bits per Gaussian-like weight instead of
+ * 16; SMOE_STORE_PACK=0 keeps the store raw).  Host only, no GPU needed.
+ * smoe_xp_pack writes at most `cap` bytes and sets *packed_bytes (0: the block
+ * does not pack — n % 8 != 0 or too many escapes); smoe_xp_unpack restores the
+ * n raw values (n from the block header).  Replaces no reference function: the
+ * reference copies raw experts (executor.cpp:138-198). */
+int smoe_xp_pack(const uint16_t* raw, int64_t n, uint8_t* out, int64_t cap, int64_t* packed_bytes);
+int smoe_xp_unpack(const uint8_t* packed, uint16_t* out, int64_t n);
 
 /* Diagnostics: request counter, error flag, scheduler progress, ready[L], req_seq[L]. */
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap);

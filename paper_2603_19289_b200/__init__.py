@@ -5,8 +5,8 @@ include/smoe.h); this package only binds it.
 """
 from .engine import (EXPORTS, GATING, MODE, PRED, CopyEvent, Event, ModelConfig, Session,
                      SmoeError, breakdown, hybrid_map_json, layer_hit_rates, load_library, recall_at_k,
-                     select_hybrid_map, simulate)
+                     select_hybrid_map, simulate, xp_pack, xp_unpack)
 
 __all__ = ["EXPORTS", "GATING", "MODE", "PRED", "CopyEvent", "Event", "ModelConfig", "Session",
            "SmoeError", "breakdown", "hybrid_map_json", "layer_hit_rates", "load_library", "recall_at_k",
-           "select_hybrid_map", "simulate"]
+           "select_hybrid_map", "simulate", "xp_pack", "xp_unpack"]

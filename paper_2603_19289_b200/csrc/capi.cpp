@@ -367,6 +367,24 @@ int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->path_info(out, cap); });
 }
 
+int smoe_xp_pack(const uint16_t* raw, int64_t n, uint8_t* out, int64_t cap, int64_t* packed_bytes) {
+    return guard([&] {
+        if (!raw || !out || !packed_bytes || n < 0 || cap < 0) throw std::invalid_argument("xp_pack: bad arguments");
+        *packed_bytes = smoe::xp_pack(raw, n, out, cap);
+    });
+}
+
+int smoe_xp_unpack(const uint8_t* packed, uint16_t* out, int64_t n) {
+    return guard([&] {
+        if (!packed || !out) throw std::invalid_argument("xp_unpack: bad arguments");
+        uint32_t hdr[4];
+        std::memcpy(hdr, packed, sizeof hdr);
+        if (hdr[0] != smoe::kXpMagic) throw std::invalid_argument("xp_unpack: not a packed expert block");
+        if (static_cast<int64_t>(hdr[3]) * 8 != n) throw std::invalid_argument("xp_unpack: element count mismatch");
+        smoe::xp_unpack(packed, out);
+    });
+}
+
 int smoe_debug_state(smoe_session* s, int32_t* out, int32_t cap) {
     return guard([&] { S(s)->debug_state(out, cap); });
 }

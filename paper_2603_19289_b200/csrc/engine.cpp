@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <immintrin.h>
 
+#include <algorithm>
 #include <charconv>
 #include <chrono>
 #include <cmath>
@@ -192,7 +193,7 @@ int numa_nodes() {
 // are bound to the NUMA node of the GPU's PCIe root (mmap + mbind, then
 // cudaHostRegister pins them there), so each rank's H2D copies read local
 // DRAM; otherwise cudaHostAlloc.
-ExpertStore::ExpertStore(long long n, long long elems, int device) : n_(n), elems_(elems) {
+ExpertStore::ExpertStore(long long n, long long elems, int device) : n_(n), elems_(elems), packed_(n, 0) {
     const size_t bytes = static_cast<size_t>(n) * elems * 2;
     const int node = gpu_numa_node(device);
     if (node >= 0 && node < 64 && numa_nodes() > 1 && !std::getenv("SMOE_NO_NUMA_BIND")) {
@@ -226,6 +227,37 @@ ExpertStore::~ExpertStore() {
     } else {
         cudaFreeHost(base_);
     }
+}
+
+// Packs every raw block in place, on all host cores.  A block is packed into
+// a scratch buffer first (the packed layout overlaps the raw one) and copied
+// back over the block's head; blocks that do not pack stay raw.
+long long ExpertStore::pack_all() {
+    const int nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::atomic<long long> next{0}, done{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            std::vector<uint8_t> buf(static_cast<size_t>(max_packed_bytes()));
+            for (long long i; (i = next.fetch_add(1)) < n_;) {
+                if (packed_[i]) continue;
+                const long long b = xp_pack(expert(i), elems_, buf.data(), max_packed_bytes());
+                if (!b) continue;
+                std::memcpy(expert(i), buf.data(), static_cast<size_t>(b));
+                packed_[i] = b;
+                ++done;
+            }
+        });
+    for (auto& t : th) t.join();
+    return done.load();
+}
+
+void ExpertStore::unpack(long long i) {
+    if (!packed_[i]) return;
+    std::vector<uint8_t> buf(static_cast<size_t>(packed_[i]));
+    std::memcpy(buf.data(), expert(i), buf.size());
+    xp_unpack(buf.data(), expert(i));
+    packed_[i] = 0;
 }
 
 // -------------------------------------------------------------- SlotCache --
@@ -425,13 +457,13 @@ void CopyScheduler::handle(const MailboxEntry& e) {
         if (ev_next_ < npairs) ev = ev_next_++;
     }
     if (ev >= 0) ck(cudaEventRecord(s.ev_copy_[2 * ev], s.s_copy_), "event record");
-    const long long bytes_per = s.store_->bytes_per_expert();
     const int E = s.cfg_.E;
+    long long wire = 0;
     for (auto& [slot, expert] : copies) {
         uint16_t* dst = s.d_slots_ + (static_cast<long long>(e.layer) * s.C_ + slot) * s.dm_.expert_elems;
-        const uint16_t* src = s.store_->expert(s.store_index(e.layer, expert));
-        ck(cudaMemcpyAsync(dst, src, bytes_per, cudaMemcpyHostToDevice, s.s_copy_), "H2D expert copy");
+        wire += s.copy_expert(e.layer, expert, dst, s.s_copy_, "H2D expert copy");
     }
+    s.join_unpack(s.s_copy_);  // the slot table and the ready flag follow the decodes
     if (!copies.empty()) {
         int* stage = s.h_stage_ + static_cast<long long>(stage_idx_ % 256) * E;
         // the copy that last used this staging row is >=256 requests old and
@@ -458,8 +490,7 @@ void CopyScheduler::handle(const MailboxEntry& e) {
         if (r != CUDA_SUCCESS) throw std::runtime_error("cuStreamWriteValue32 failed");
     }
     std::lock_guard<std::mutex> g(mu_);
-    recs_.push_back({e.seq, e.layer, e.step, hits, misses,
-                     static_cast<long long>(copies.size()) * bytes_per, ev});
+    recs_.push_back({e.seq, e.layer, e.step, hits, misses, wire, ev});
 }
 
 // ---------------------------------------------------------------- Session --
@@ -479,6 +510,31 @@ void Session::d2h(void* dst, const void* src, size_t n, const char* what) {
 }
 void Session::dset(void* p, int v, size_t n, const char* what) {
     ck(cudaMemsetAsync(p, v, n, s_comp_), what);
+}
+
+long long Session::copy_expert(int layer, int expert, uint16_t* dst, cudaStream_t s, const char* what) {
+    const long long b = store_index(layer, expert);
+    const long long packed = store_->packed_bytes(b);
+    if (!packed) {
+        ck(cudaMemcpyAsync(dst, store_->expert(b), store_->bytes_per_expert(), cudaMemcpyHostToDevice, s), what);
+        return store_->bytes_per_expert();
+    }
+    const int k = static_cast<int>(xp_next_.fetch_add(1) % kXpRing);
+    unsigned char* stage = d_xp_stage_ + k * xp_stride_;
+    ck(cudaStreamWaitEvent(s, ev_xp_[k], 0), "xp ring");  // the slot's previous decode is done
+    ck(cudaMemcpyAsync(stage, store_->expert(b), static_cast<size_t>(packed), cudaMemcpyHostToDevice, s), what);
+    ck(cudaEventRecord(ev_h2d_[k], s), "xp h2d");
+    ck(cudaStreamWaitEvent(s_unpack_, ev_h2d_[k], 0), "xp h2d");
+    ck(launch_xp_unpack(stage, dst, dm_.expert_elems, s_unpack_), "expert unpack");
+    ck(cudaEventRecord(ev_xp_[k], s_unpack_), "xp decode");
+    ++xp_pending_;
+    return packed;
+}
+
+void Session::join_unpack(cudaStream_t s) {
+    if (xp_pending_.exchange(0) == 0) return;
+    ck(cudaEventRecord(ev_unp_join_, s_unpack_), "xp join");
+    ck(cudaStreamWaitEvent(s, ev_unp_join_, 0), "xp join");
 }
 
 void* Session::dalloc(size_t bytes) {
@@ -558,7 +614,18 @@ void Session::free_all() {
     if (s_copy_) cudaStreamDestroy(s_copy_);
     if (s_side_) cudaStreamDestroy(s_side_);
     if (s_log_) cudaStreamDestroy(s_log_);
-    s_comp_ = s_copy_ = s_side_ = s_log_ = nullptr;
+    if (s_unpack_) {
+        cudaStreamSynchronize(s_unpack_);
+        cudaStreamDestroy(s_unpack_);
+    }
+    for (int k = 0; k < kXpRing; ++k) {
+        if (ev_h2d_[k]) cudaEventDestroy(ev_h2d_[k]);
+        if (ev_xp_[k]) cudaEventDestroy(ev_xp_[k]);
+        ev_h2d_[k] = ev_xp_[k] = nullptr;
+    }
+    if (ev_unp_join_) cudaEventDestroy(ev_unp_join_);
+    ev_unp_join_ = nullptr;
+    s_comp_ = s_copy_ = s_side_ = s_log_ = s_unpack_ = nullptr;
 }
 
 void Session::drop_graphs() {
@@ -608,7 +675,14 @@ void Session::alloc() {
         if (std::getenv("SMOE_NO_PRIO")) lo = hi = 0;  // diagnostics
         ck(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
         ck(cudaStreamCreateWithPriority(&s_log_, cudaStreamNonBlocking, lo), "stream");
+        // expert decodes: placed before pending compute CTAs (a ready flag waits on them)
+        ck(cudaStreamCreateWithPriority(&s_unpack_, cudaStreamNonBlocking, hi), "stream");
     }
+    for (int k = 0; k < kXpRing; ++k) {
+        ck(cudaEventCreateWithFlags(&ev_h2d_[k], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&ev_xp_[k], cudaEventDisableTiming), "event");
+    }
+    ck(cudaEventCreateWithFlags(&ev_unp_join_, cudaEventDisableTiming), "event");
     ev_fork_.resize(L);
     ev_join_.resize(L);
     for (int l = 0; l < L; ++l) {
@@ -778,6 +852,8 @@ void Session::alloc() {
     ck(cudaEventCreate(&ev_origin_), "event");
 
     store_ = std::make_unique<ExpertStore>(static_cast<long long>(L) * el_max_, m.expert_elems, opts_.device);
+    xp_stride_ = (store_->max_packed_bytes() + 255) / 256 * 256;
+    d_xp_stage_ = static_cast<unsigned char*>(dalloc(static_cast<size_t>(kXpRing * xp_stride_)));
     cache_ = std::make_unique<SlotCache>(L, E, C_);
     ck(cudaDeviceSynchronize(), "alloc");
     reset(0, 0);
@@ -917,10 +993,8 @@ void Session::preload_all() {
         int h = 0, mi = 0;
         auto copies = cache_->request(l, ids.data(), static_cast<int>(ids.size()), &h, &mi);
         for (auto& [slot, expert] : copies)
-            ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * per,
-                               store_->expert(store_index(l, expert)), per * 2,
-                               cudaMemcpyHostToDevice, s_copy_),
-               "preload");
+            copy_expert(l, expert, d_slots_ + (static_cast<long long>(l) * C_ + slot) * per, s_copy_, "preload");
+        join_unpack(s_copy_);
         ck(cudaMemcpyAsync(d_slot_of_ + static_cast<long long>(l) * cfg_.E, cache_->slot_row(l).data(),
                            4ull * cfg_.E, cudaMemcpyHostToDevice, s_copy_),
            "preload table");
@@ -1010,6 +1084,7 @@ void Session::init_weights_seeded() {
     }
     ck(cudaStreamSynchronize(s), "init sync");
     cudaFree(stage);
+    if (pack_store_) store_->pack_all();  // xp12: 12 bits per weight on the link (lossless)
     cache_->invalidate();
     ctl_.resident = 0;
     drop_graphs();
@@ -1084,6 +1159,7 @@ void Session::load_tensor(const std::string& name, const float* data, long long 
     char which[32];
     if (std::sscanf(rest.c_str(), "expert%d.%31s", &e, which) == 2 && e >= 0 && e < c.E) {
         if (!is_local(e)) return;  // EP: another rank owns this expert
+        store_->unpack(store_index(l, e));  // raw bf16 again before a partial rewrite
         uint16_t* blk = store_->expert(store_index(l, e));
         const std::string w = which;
         if (w == "w_gate" || w == "w_up") {
@@ -1627,11 +1703,10 @@ void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt)
         if (!ctl_.resident) {  // load the wave's experts into this layer's slots
             int hits = 0, misses = 0;
             auto copies = cache_->request(l, wv.e, nw, &hits, &misses);
-            const long long bytes = store_->bytes_per_expert();
             for (auto& [slot, expert] : copies)
-                ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems,
-                                   store_->expert(store_index(l, expert)), bytes, cudaMemcpyHostToDevice, s_copy_),
-                   "prefill expert copy");
+                copy_expert(l, expert, d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems, s_copy_,
+                            "prefill expert copy");
+            join_unpack(s_copy_);
             ck(cudaStreamSynchronize(s_copy_), "prefill copies");
             h2d(d_slot_of_ + static_cast<long long>(l) * c.E, cache_->slot_row(l).data(), 4ull * c.E, "slot table");
         }
@@ -1846,13 +1921,11 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                         if (want[e]) first.push_back(e);
                     int hits = 0, misses = 0;
                     const auto copies = cache_->request(l + 1, first.data(), static_cast<int>(first.size()), &hits, &misses);
-                    const long long bytes = store_->bytes_per_expert();
                     for (const auto& [slot, expert] : copies)
-                        ck(cudaMemcpyAsync(d_slots_ + (static_cast<long long>(l + 1) * C_ + slot) * m.expert_elems,
-                                           store_->expert(store_index(l + 1, expert)), bytes,
-                                           cudaMemcpyHostToDevice, s_copy_),
-                           "batch prefetch copy");
-                    batch_prefetched_bytes_ += static_cast<long long>(copies.size()) * bytes;
+                        batch_prefetched_bytes_ += copy_expert(
+                            l + 1, expert, d_slots_ + (static_cast<long long>(l + 1) * C_ + slot) * m.expert_elems,
+                            s_copy_, "batch prefetch copy");
+                    join_unpack(s_copy_);
                 }
             }
         }
@@ -2142,9 +2215,18 @@ cudaGraphExec_t Session::get_graph(int mode, int stream) {
 // Kernels in one captured decode step: the teacher-forced (stream) graph if
 // it was built, else the greedy one; -1 before any graph exists.
 void Session::path_info(int* out, int cap) const {
+    // packed store: blocks packed, and the packed wire bytes per 1000 raw bytes
+    long long np = 0, wire = 0, raw = 0;
+    if (store_)
+        for (long long i = 0; i < store_->blocks(); ++i) {
+            np += store_->packed_bytes(i) != 0;
+            wire += store_->wire_bytes(i);
+            raw += store_->bytes_per_expert();
+        }
     const int v[] = {dm_.ffn_fused, dm_.attn_grid, host_ordered_ ? 1 : 0, ctl_.fast_hit,
-                     store_ ? store_->numa_node() : -1};
-    for (int i = 0; i < cap && i < 5; ++i) out[i] = v[i];
+                     store_ ? store_->numa_node() : -1, static_cast<int>(np),
+                     raw ? static_cast<int>(1000 * wire / raw) : 0};
+    for (int i = 0; i < cap && i < 7; ++i) out[i] = v[i];
 }
 
 int Session::kernels_per_step(int mode) const {

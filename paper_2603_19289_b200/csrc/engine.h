@@ -64,6 +64,27 @@ struct CopyRecord {  // one mailbox request as the copy lane saw it
     int ev;  // index into the event pool, -1 if none
 };
 
+// Exponent-packed bf16 expert blocks ("xp12", lossless): a block of n bf16
+// weights (n % 8 == 0) becomes
+//   [16 B header: magic, base, nesc, n/8][n/2 B exponent codes][n B sign|mantissa]
+//   [nesc x 8 B escapes: u32 index, u16 raw value, u16 0 — ascending index]
+// Element i: code c = 4-bit nibble i (low nibble first), byte b = sign<<7 |
+// mantissa; bf16 = (b & 0x80) << 8 | (base + c) << 7 | (b & 0x7f) for c < 15,
+// c == 15: the escape entry's raw value (exponents outside [base, base+14],
+// zeros, subnormals).  base: the 15-binade window with the most weights.  12 bits per weight
+// on the wire instead of 16 for Gaussian-like weights (the exponent of a
+// weight drawn around a fixed scale spans few binades).
+constexpr uint32_t kXpMagic = 0x32315058u;  // "XP12"
+constexpr int kXpHeader = 16;
+// packed size of a block with `nesc` escapes
+inline long long xp_bytes(long long n, long long nesc) { return kXpHeader + n / 2 + n + nesc * 8; }
+// Packs `raw` (n bf16) into `out` (capacity `cap` bytes).  Returns the packed
+// size, or 0 when the block is not worth packing (n % 8, or the escapes would
+// make it larger than 7/8 of the raw bytes, or it does not fit `cap`).
+long long xp_pack(const uint16_t* raw, long long n, uint8_t* out, long long cap);
+// Inverse of xp_pack (host side; the device side is k_xp_unpack).
+void xp_unpack(const uint8_t* in, uint16_t* out);
+
 class ExpertStore {
 public:
     ExpertStore(long long n_experts, long long elems_per_expert, int device);
@@ -71,12 +92,22 @@ public:
     uint16_t* expert(long long i) { return base_ + i * elems_; }
     long long bytes_per_expert() const { return elems_ * 2; }
     int numa_node() const { return node_; }  // -1: not NUMA-bound (single node / unknown)
+    // packed size of block i on the wire (0: stored raw)
+    long long packed_bytes(long long i) const { return packed_[i]; }
+    long long wire_bytes(long long i) const { return packed_[i] ? packed_[i] : elems_ * 2; }
+    long long max_packed_bytes() const { return elems_ * 2 * 7 / 8 + 64; }
+    // packs every raw block in place (host threads); returns blocks packed
+    long long pack_all();
+    // restores block i to raw bf16 (before a partial rewrite of its weights)
+    void unpack(long long i);
+    long long blocks() const { return n_; }
 
 private:
     uint16_t* base_ = nullptr;
     long long n_, elems_;
     size_t mapped_ = 0;  // mmap'd + cudaHostRegister'ed (NUMA-bound) when > 0
     int node_ = -1;
+    std::vector<long long> packed_;  // [n_] packed bytes, 0 = raw
 };
 
 class SlotCache {
@@ -292,6 +323,25 @@ private:
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]
     int* d_epoch_ = nullptr;               // EP combines done [L]
     std::vector<void*> ipc_opened_;
+
+    // packed expert copies (xp12): H2D of the packed block into a staging ring
+    // slot, then k_xp_unpack into the HBM slot, both on `s` (FIFO: a ring slot
+    // is reused kXpRing copies later, after its decode ran)
+    // The decodes run on their own highest-priority stream (s_unpack_), so
+    // expert i+1's H2D overlaps expert i's decode; a ring slot's next H2D waits
+    // for its previous decode (ev_xp_), and join_unpack() orders a stream
+    // after every decode issued so far (before a ready flag / slot use).
+    static constexpr int kXpRing = 8;
+    unsigned char* d_xp_stage_ = nullptr;
+    long long xp_stride_ = 0;
+    std::atomic<long long> xp_next_{0};
+    cudaStream_t s_unpack_ = nullptr;
+    cudaEvent_t ev_h2d_[kXpRing] = {}, ev_xp_[kXpRing] = {}, ev_unp_join_ = nullptr;
+    std::atomic<int> xp_pending_{0};  // decodes issued since the last join_unpack
+    void join_unpack(cudaStream_t s);
+    bool pack_store_ = std::getenv("SMOE_STORE_PACK") == nullptr || std::atoi(std::getenv("SMOE_STORE_PACK")) != 0;
+    // copies expert (layer, e) from the pinned store into `dst`; returns the bytes moved over the link
+    long long copy_expert(int layer, int expert, uint16_t* dst, cudaStream_t s, const char* what);
 
     // host
     std::unique_ptr<ExpertStore> store_;

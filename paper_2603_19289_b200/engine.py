@@ -36,7 +36,7 @@ EXPORTS = [
     "smoe_timeline", "smoe_simulate", "smoe_breakdown", "smoe_recall_at_k",
     "smoe_write_trace_bundle", "smoe_prefill_batched", "smoe_estimator_param_count", "smoe_simulate_cache", "smoe_predict_ahead", "smoe_batch_generate", "smoe_exp", "smoe_build_distill_dataset",
     "smoe_estimator_init", "smoe_train_estimator", "smoe_run_offloaded_decode_ex", "smoe_path_info", "smoe_decide", "smoe_layer_hit_rates",
-    "smoe_select_hybrid_map", "smoe_set_prefill_mode", "smoe_set_decode_mode",
+    "smoe_select_hybrid_map", "smoe_set_prefill_mode", "smoe_set_decode_mode", "smoe_xp_pack", "smoe_xp_unpack",
 ]
 
 
@@ -180,6 +180,26 @@ def layer_hit_rates(exec_ids, true_ids) -> np.ndarray:
     steps, L, k = e.shape
     out = np.zeros(L - 1, np.float64)
     _check(lib.smoe_layer_hit_rates(_p(e), _p(t), steps, L, k, _p(out)))
+    return out
+
+
+def xp_pack(raw) -> bytes | None:
+    """Exponent-packed (xp12) form of a bf16 block given as uint16 [n]; None when
+    the block does not pack (the store then keeps it raw)."""
+    lib = load_library()
+    raw = np.ascontiguousarray(raw, np.uint16)
+    out = np.zeros(raw.size * 2 + 64, np.uint8)
+    nb = C.c_int64()
+    _check(lib.smoe_xp_pack(_p(raw), C.c_int64(raw.size), _p(out), C.c_int64(out.size), C.byref(nb)))
+    return out[: nb.value].tobytes() if nb.value else None
+
+
+def xp_unpack(packed: bytes, n: int) -> np.ndarray:
+    """Inverse of xp_pack -> uint16 [n]."""
+    lib = load_library()
+    buf = np.frombuffer(packed, np.uint8).copy()
+    out = np.zeros(n, np.uint16)
+    _check(lib.smoe_xp_unpack(_p(buf), _p(out), C.c_int64(n)))
     return out
 
 
@@ -528,10 +548,11 @@ class Session:
         _check(self.lib.smoe_set_prefill_mode(self._h, {"exact": 0, "tensor": 1}[mode]))
 
     def path_info(self) -> dict:
-        out = np.zeros(5, np.int32)
-        _check(self.lib.smoe_path_info(self._h, _p(out), 5))
+        out = np.zeros(7, np.int32)
+        _check(self.lib.smoe_path_info(self._h, _p(out), 7))
         return {"ffn_fused": bool(out[0]), "attn_ctas": int(out[1]), "host_ordered": bool(out[2]),
-                "device_hit_path": bool(out[3]), "store_numa_node": int(out[4])}
+                "device_hit_path": bool(out[3]), "store_numa_node": int(out[4]),
+                "store_packed_blocks": int(out[5]), "store_wire_per_raw": float(out[6]) / 1000.0}
 
     def measure_link(self, n_copies: int = 64) -> float:
         g = C.c_double()

@@ -296,8 +296,11 @@ def test_copy_lane_invariants(lib):
     assert c["requests"] == len(ev) == 6 * TOY["layers"]
     assert sum(e.hits + e.misses for e in ev) == len(ev) * K
     assert int(c["hits"].sum()) == sum(e.hits for e in ev)
-    per = 3 * TOY["hidden"] * TOY["expert_hidden"] * 2
-    assert all(e.bytes == e.misses * per for e in ev)  # toy dims need no tile padding
+    per = 3 * TOY["hidden"] * TOY["expert_hidden"] * 2  # toy dims need no tile padding
+    # the link carries the store's wire format: raw bf16 or exponent-packed
+    # (xp12, ~0.75 of raw; per-block size varies by a few escapes)
+    ratio = s.path_info()["store_wire_per_raw"]
+    assert all(abs(e.bytes - e.misses * per * ratio) <= e.misses * per * 0.003 for e in ev)
     spans = sorted((e.start_ms, e.end_ms) for e in ev if e.misses > 0)
     for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
         assert b0 >= a1 - 1e-3

@@ -185,3 +185,27 @@ def test_decision_routine_vs_oracle(lib, E, K, gating):
         wi, wg = orc.make_decision(lg[r], K, gid)
         assert np.array_equal(ids[r], wi), (r, ids[r], wi)
         assert np.array_equal(gates[r].view(np.uint32), wg.view(np.uint32)), (r, gates[r], wg)
+
+
+@pytest.mark.parametrize("mode", ["on_demand", "prefetch"])
+def test_packed_expert_store_is_lossless_on_the_copy_path(lib, toy, mode):
+    """Experts travel exponent-packed (xp12) and k_xp_unpack restores them in
+    the slot: same trace as the raw store, bit for bit, with ~3/4 of the link
+    bytes; and both equal the oracle."""
+    orc, om, table = toy
+    prompt = [5, 77, 200, 13, 9]
+    stream = list(np.random.default_rng(4).integers(0, 256, 24))
+    raw = _session({"SMOE_STORE_PACK": "0"})
+    pk = _session({"SMOE_STORE_PACK": None})
+    assert raw.path_info()["store_packed_blocks"] == 0
+    assert pk.path_info()["store_packed_blocks"] == TOY["layers"] * TOY["experts"]
+    ra, eva = _decode(raw, table, prompt, 24, mode, stream)
+    rb, evb = _decode(pk, table, prompt, 24, mode, stream)
+    for k in ("id_exec", "id_true", "s", "m", "logits", "tokens", "hits", "misses"):
+        assert np.array_equal(ra[k], rb[k]), k
+    assert ra["bytes"] > 0 and 0.74 < rb["bytes"] / ra["bytes"] < 0.77
+    pred = orc.make_predictor("router-pf", om, table) if mode == "prefetch" else None
+    want = om.generate_trace(prompt, 25, pred, forced=np.array(stream[:24], np.int32))
+    assert np.array_equal(rb["id_exec"], want.ids)
+    raw.close()
+    pk.close()
