@@ -700,9 +700,11 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
     const int pos = __ldcg(st.pos), n = pos + 1, b = blockIdx.x;
     const int ppc = max(4 * kAttnFastChunk, (n + gridDim.x - 1) / gridDim.x);
     const int G = (n + ppc - 1) / ppc;  // CTAs with positions
-    if (b >= G) {
+    if (b >= G) {  // no positions: leave at once (an exit counts as the PDL trigger)
+#ifdef SMOE_ATTN_IDLE_WAIT
         pdl_wait();
         pdl_trigger();
+#endif
         return;
     }
     const int j0 = b * ppc, j1 = min(n, j0 + ppc), nch = (j1 - j0 + kAttnFastChunk - 1) / kAttnFastChunk;

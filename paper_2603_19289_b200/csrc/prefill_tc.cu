@@ -13,30 +13,36 @@
 //     residue of x — a stated tolerance, not bit parity; the exact path
 //     (prefill.cu, one lane per row walking the columns in order) stays the
 //     default.
-//   * Operands stream into shared memory with cp.async.bulk (the weight row
-//     tiles need no re-layout: a 32-row tile's 8-column groups are exactly
-//     UMMA's no-swizzle K-major core matrices, SBO = 128 B, LBO = 512 B); the
-//     packed activations use the same canonical layout (SBO 128 B, LBO 2 KB).
-//   * One thread issues tcgen05.mma (kind::f16, M = 128 tokens, N = 32 rows per
-//     tile, K = 16) into a TMEM accumulator per tile; tcgen05.commit frees each
-//     stage; the epilogue reads TMEM with tcgen05.ld (32x32b) — one warp per
-//     32-token lane quarter — and applies SwiGLU (gate/up) or stores the raw
-//     expert rows (down).
+//   * Operands stream into shared memory with cp.async.bulk: the packed
+//     activations in UMMA's no-swizzle K-major canonical layout (SBO 128 B,
+//     LBO 2 KB), the weights of 8 consecutive 32-row tiles gathered per
+//     8-column group into one K-major operand of N = 256 rows (SBO 128 B,
+//     LBO 4 KB) — 512-byte pieces of the stored row tiles, no re-layout pass.
+//   * A persistent, warp-specialised kernel per projection (k_tc_ffn): a TMA
+//     producer lane, an MMA lane issuing tcgen05.mma (kind::f16, M = 128
+//     tokens, N = 256 rows, K = 16) into one of two TMEM accumulators, and four
+//     epilogue warps draining the other with tcgen05.ld (32x32b) — SwiGLU for
+//     gate/up, raw expert rows for down.
 #include "kernels.h"
 #include "smoe_chain.cuh"
+
+#include <cuda.h>
+
+#include <algorithm>
 
 namespace smoe {
 
 namespace {
 
 constexpr int kTcM = 128;          // tokens per tile (UMMA M)
-constexpr int kTcTiles = 4;        // 32-row weight tiles per CTA (N = 128)
+constexpr int kTcTiles = 8;        // 32-row weight tiles per CTA (N = 256: half the activation re-reads of N = 128)
 constexpr int kTcK = 64;           // K columns per stage
-constexpr int kTcStages = 4;
+constexpr int kTcStages = 3;
 constexpr int kTcAChunk = kTcM * kTcK * 2;          // bytes of one operand half (hi or lo) per stage
 constexpr int kTcBTile = 32 * kTcK * 2;             // bytes of one tile's chunk per stage
-constexpr int kTcStage = 2 * kTcAChunk + kTcTiles * kTcBTile;  // 48 KB
-constexpr int kTcSmem = kTcStages * kTcStage + 1024;
+constexpr int kTcStage = 2 * kTcAChunk + kTcTiles * kTcBTile;  // 64 KB
+constexpr int kTcSmem = kTcStages * kTcStage + 1024;  // + barriers and the TMEM address
+constexpr int kTcCols = 32 * kTcTiles;              // TMEM columns (one 32-column accumulator per tile)
 
 __device__ __forceinline__ uint16_t bf16_rn(float x) {
     uint32_t u = __float_as_uint(x);
@@ -54,8 +60,9 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;         // base offset 0, legacy LBO mode, layout SWIZZLE_NONE
 }
 
-// bf16 x bf16 -> f32, M = 128, N = 32, both K-major.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// bf16 x bf16 -> f32, M = 128 tokens, N = 32 * kTcTiles weight rows, both K-major.
+constexpr uint32_t kIdesc =
+    (1u << 4) | (1u << 7) | (1u << 10) | (((32u * kTcTiles) >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
     asm volatile(
@@ -90,92 +97,198 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Main loop: TMEM columns [32 t, 32 t + 32) += A(128 x K) . tile_t(32 x K)^T for
-// t < nt.  a_hi / a_lo: the packed activations of this token block
-// ([K/8][128][8] bf16 each); tiles: row-tile bases (layout [K/8][32][8]).
-// Executed by thread 0 (copies and MMA issue); returns once the last MMA's
-// completion is signalled on `done`.
-__device__ void tc_mainloop(const uint16_t* a_hi, const uint16_t* a_lo, const uint16_t* const* tiles, int nt, int K,
-                            unsigned char* smem, uint64_t* full, uint64_t* empty, uint64_t* done, uint32_t tmem) {
-    const int nk = K / kTcK;
-    const uint32_t bytes = 2 * kTcAChunk + nt * kTcBTile;
-    auto issue = [&](int k) {
-        const int st = k % kTcStages;
-        unsigned char* s = smem + st * kTcStage;
-        mbar_expect_tx(&full[st], bytes);
-        bulk_g2s(s, a_hi + static_cast<long long>(k) * kTcM * kTcK, kTcAChunk, &full[st]);
-        bulk_g2s(s + kTcAChunk, a_lo + static_cast<long long>(k) * kTcM * kTcK, kTcAChunk, &full[st]);
-        for (int t = 0; t < nt; ++t)
-            bulk_g2s(s + 2 * kTcAChunk + t * kTcBTile, tiles[t] + static_cast<long long>(k) * kTcK * 32, kTcBTile,
-                     &full[st]);
-    };
-    for (int k = 0; k < kTcStages && k < nk; ++k) issue(k);
-    for (int k = 0; k < nk; ++k) {
-        const int st = k % kTcStages;
-        mbar_wait(&full[st], static_cast<uint32_t>((k / kTcStages) & 1));
-        tc_fence_after();
-        const uint32_t s = smem_u32(smem + st * kTcStage);
-#pragma unroll
-        for (int kk = 0; kk < kTcK / 16; ++kk) {
-            const uint64_t ah = umma_desc(s + kk * 4096, 2048, 128);
-            const uint64_t al = umma_desc(s + kTcAChunk + kk * 4096, 2048, 128);
-            for (int t = 0; t < nt; ++t) {
-                const uint64_t b = umma_desc(s + 2 * kTcAChunk + t * kTcBTile + kk * 1024, 512, 128);
-                tc_mma(tmem + 32 * t, ah, b, (k | kk) != 0);
-                tc_mma(tmem + 32 * t, al, b, 1);
-            }
-        }
-        tc_commit(&empty[st]);  // this stage's smem is free once these MMAs complete
-        if (k + kTcStages < nk) {
-            mbar_wait(&empty[st], static_cast<uint32_t>((k / kTcStages) & 1));
-            issue(k + kTcStages);
-        }
-    }
-    tc_commit(done);
+// Persistent, warp-specialised expert GEMM (one CTA per SM, 6 warps):
+//   warp 0 lane 0  TMA producer: for each work item of this CTA, the K/64
+//                  stages of [a_hi | a_lo | nt weight-tile chunks] into a
+//                  3-stage shared-memory ring (cp.async.bulk, mbarrier
+//                  complete_tx), refilling a stage once its MMAs completed;
+//   warp 1 lane 0  MMA issuer: per stage 2 x 4 tcgen05.mma (kind::f16,
+//                  M = 128 tokens, N = 256 rows, K = 16) into one of two TMEM
+//                  accumulators (2 x 256 columns: item i uses buffer i & 1),
+//                  tcgen05.commit to free the stage, and to hand the finished
+//                  accumulator to the epilogue;
+//   warps 2-5      epilogue: tcgen05.ld (32x32b, warp w reads TMEM lanes
+//                  32 (w % 4) ..) of tokens, SwiGLU (gate/up) or raw rows
+//                  (down), then release the accumulator buffer.
+// So the epilogue of item i overlaps the MMAs of item i + 1, and the ring
+// keeps streaming across item boundaries.  A work item is (token block it,
+// n-block nb of kTcTiles 32-row tiles).
+constexpr int kTcThreads = 192;
+constexpr int kTcBufCols = kTcCols;          // columns per accumulator buffer
+constexpr int kTcTmemCols = 2 * kTcBufCols;  // TMEM allocation (power of two, <= 512)
+
+struct TcItem {
+    int it, e, b0, cnt, c0, t0, nt, slot;
+};
+__device__ __forceinline__ TcItem tc_item(const DevModel& m, const PrefillDev& pf, const PfWave& wv, int w,
+                                          int nblk, int ntiles) {
+    TcItem r;
+    r.it = w / nblk;
+    const int nb = w % nblk;
+    const int u = __ldcg(pf.chunk_u + r.it);
+    r.e = wv.e[u];
+    r.slot = wv.slot[u];
+    r.b0 = pf.off[r.e];
+    r.cnt = pf.off[r.e + 1] - r.b0;
+    r.c0 = __ldcg(pf.chunk_c + r.it) * kTcM;
+    r.t0 = nb * kTcTiles;
+    r.nt = min(kTcTiles, ntiles - r.t0);
+    return r;
 }
 
-// Shared prologue: barriers, TMEM allocation (128 columns), item decode.
-struct TcCta {
-    unsigned char* smem;
-    uint64_t *full, *empty, *done;
-    uint32_t* tptr;
-    uint32_t tmem;
-    __device__ void setup() {
-        smem = align128(g_smem);
-        unsigned char* tail = smem + kTcStages * kTcStage;
-        full = reinterpret_cast<uint64_t*>(tail);
-        empty = full + kTcStages;
-        done = empty + kTcStages;
-        tptr = reinterpret_cast<uint32_t*>(done + 1);
-        if (threadIdx.x == 0) {
-            for (int i = 0; i < kTcStages; ++i) {
-                mbar_init(&full[i], 1);
-                mbar_init(&empty[i], 1);
+// MODE 0: gate/up (K = H, tiles of 16 SwiGLU rows, h = silu(g) * u into Hb);
+// MODE 1: down (K = Hm, tiles of 32 rows, raw expert rows into Y).
+// wmap (when use_map): 5-D TMA map of this projection's weight tiles in the
+// slot pool — dims (8 cols, 32 rows, tile, 8-col group, layer * C + slot),
+// strides (2 B, 16 B, tile, 512 B, expert block) — whose box (8, 32, 8, 8, 1)
+// lands exactly the gathered [group][tile][row][col] operand; otherwise
+// 512-byte bulk copies build the same layout.
+template <int MODE>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_ffn(DevModel m, PrefillDev pf, int layer, PfWave wv,
+                                                          const uint16_t* apk, int n_work,
+                                                          const __grid_constant__ CUtensorMap wmap, int use_map) {
+    pdl_wait();
+    pdl_trigger();
+    const int K = MODE == 0 ? m.H : m.Hm;
+    const int ntiles = MODE == 0 ? m.Hmp / 16 : m.Hp / 32;
+    const int nblk = (ntiles + kTcTiles - 1) / kTcTiles;
+    const long long tile_elems = static_cast<long long>(K) * 32;
+    const long long blk_off = MODE == 0 ? 0 : m.gu_elems;
+    unsigned char* smem = align128(g_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStage);
+    uint64_t* empty = full + kTcStages;
+    uint64_t* acc_full = empty + kTcStages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;      // [2]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTcStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tptr)),
+                     "n"(kTcTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tptr;
+    const int nk = K / kTcK;
+    if (warp == 0 && lane == 0) {  // ---- producer
+        int g = 0;
+        for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+            const TcItem r = tc_item(m, pf, wv, w, nblk, ntiles);
+            const uint16_t* blk = m.slots + (static_cast<long long>(layer) * m.C + r.slot) * m.expert_elems + blk_off;
+            const uint16_t* hi = apk + static_cast<long long>(r.it) * 2 * K * kTcM;
+            const uint16_t* lo = hi + static_cast<long long>(K) * kTcM;
+            // the tensor copy always lands its whole box (tiles past ntiles are zero-filled)
+            const uint32_t bytes = 2 * kTcAChunk + (use_map ? kTcTiles : r.nt) * kTcBTile;
+            for (int k = 0; k < nk; ++k, ++g) {
+                const int st = g % kTcStages;
+                if (g >= kTcStages) mbar_wait(&empty[st], static_cast<uint32_t>(((g / kTcStages) - 1) & 1));
+                unsigned char* sp = smem + st * kTcStage;
+                mbar_expect_tx(&full[st], bytes);
+                bulk_g2s(sp, hi + static_cast<long long>(k) * kTcM * kTcK, kTcAChunk, &full[st]);
+                bulk_g2s(sp + kTcAChunk, lo + static_cast<long long>(k) * kTcM * kTcK, kTcAChunk, &full[st]);
+                // weights as ONE K-major operand of N = 32 * kTcTiles rows: the
+                // 512-byte [32 rows][8 cols] block of tile t, column group j goes to
+                // [j][t] (rows of consecutive tiles adjacent, SBO 128 B, LBO
+                // kTcTiles * 512 B); rows of absent tiles (t >= nt) stay stale and
+                // only feed accumulator columns the epilogue never reads
+                if (use_map) {  // one 5-D tensor copy: box (8 cols, 32 rows, 8 tiles, 8 groups, 1 expert)
+                    const int slot_idx = layer * m.C + r.slot;
+                    asm volatile(
+                        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(sp + 2 * kTcAChunk)),
+                        "l"(reinterpret_cast<uint64_t>(&wmap)), "r"(0), "r"(0), "r"(r.t0), "r"(k * (kTcK / 8)),
+                        "r"(slot_idx), "r"(smem_u32(&full[st]))
+                        : "memory");
+                } else {
+                    for (int t = 0; t < r.nt; ++t) {
+                        const uint16_t* src = blk + (r.t0 + t) * tile_elems + static_cast<long long>(k) * kTcK * 32;
+                        for (int j = 0; j < kTcK / 8; ++j)
+                            bulk_g2s(sp + 2 * kTcAChunk + (j * kTcTiles + t) * 512, src + j * 256, 512, &full[st]);
+                    }
+                }
             }
-            mbar_init(done, 1);
-            fence_mbar_init();
         }
-        if (threadIdx.x < 32) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tptr))
-                         : "memory");
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
+        int g = 0, i = 0;
+        for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++i) {
+            const int b = i & 1;
+            if (i >= 2) mbar_wait(&acc_empty[b], static_cast<uint32_t>(((i >> 1) - 1) & 1));
+            tc_fence_after();
+            const uint32_t acc = tmem + b * kTcBufCols;
+            for (int k = 0; k < nk; ++k, ++g) {
+                const int st = g % kTcStages;
+                mbar_wait(&full[st], static_cast<uint32_t>((g / kTcStages) & 1));
+                tc_fence_after();
+                const uint32_t sa = smem_u32(smem + st * kTcStage);
+#pragma unroll
+                for (int kk = 0; kk < kTcK / 16; ++kk) {
+                    const uint64_t ah = umma_desc(sa + kk * 4096, 2048, 128);
+                    const uint64_t al = umma_desc(sa + kTcAChunk + kk * 4096, 2048, 128);
+                    const uint64_t bd = umma_desc(sa + 2 * kTcAChunk + kk * 2 * kTcTiles * 512, kTcTiles * 512, 128);
+                    tc_mma(acc, ah, bd, (k | kk) != 0);  // M 128 x N 256 x K 16: all tiles at once
+                    tc_mma(acc, al, bd, 1);
+                }
+                tc_commit(&empty[st]);
+            }
+            tc_commit(&acc_full[b]);
         }
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        tmem = *tptr;
+    } else if (warp >= 2) {  // ---- epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int i = 0;
+        for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++i) {
+            const TcItem r = tc_item(m, pf, wv, w, nblk, ntiles);
+            const int b = i & 1;
+            mbar_wait(&acc_full[b], static_cast<uint32_t>((i >> 1) & 1));
+            tc_fence_after();
+            const int tok = q * 32 + lane;
+            const bool valid = r.c0 + tok < r.cnt;
+            const int ent = valid ? __ldcg(pf.list + r.b0 + r.c0 + tok) : 0;
+            for (int t = 0; t < r.nt; ++t) {
+                float v[32];
+                tmem_ld32(tmem + b * kTcBufCols + (static_cast<uint32_t>(q * 32) << 16) + 32 * t, v);
+                if (!valid) continue;
+                if (MODE == 0) {
+                    float* h = pf.Hb + static_cast<long long>(ent) * m.Hmp + (r.t0 + t) * 16;
+#pragma unroll
+                    for (int rr = 0; rr < 16; rr += 4) {
+                        float o[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float gv = v[2 * (rr + j)], uv = v[2 * (rr + j) + 1];
+                            o[j] = gv / (1.0f + __expf(-gv)) * uv;  // f32 SiLU: tolerance mode
+                        }
+                        *reinterpret_cast<float4*>(h + rr) = make_float4(o[0], o[1], o[2], o[3]);
+                    }
+                } else {
+                    float* y = pf.Y + static_cast<long long>(ent) * m.Hp + (r.t0 + t) * 32;
+#pragma unroll
+                    for (int rr = 0; rr < 32; rr += 4)
+                        *reinterpret_cast<float4*>(y + rr) = make_float4(v[rr], v[rr + 1], v[rr + 2], v[rr + 3]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
     }
-    __device__ void teardown() {
-        tc_fence_before();
-        __syncthreads();
-        if (threadIdx.x < 32)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
-    }
-    __device__ void wait_done() {
-        mbar_wait(done, 0);
-        tc_fence_after();
-    }
-};
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols) : "memory");
+}
 
 }  // namespace
 
@@ -234,77 +347,6 @@ __global__ void __launch_bounds__(256) k_tc_pack(DevModel m, PrefillDev pf, int 
     }
 }
 
-// gate/up: grid (ceil((Hmp/16) / 4), items), 128 threads.  CTA x covers the
-// 16-row SwiGLU tiles 4x .. 4x+3 (virtual rows 2r = gate, 2r+1 = up); the
-// epilogue forms h = silu(g) * u (silu in f64, numerics.cpp:86-89) per token.
-__global__ void __launch_bounds__(128) k_tc_gu(DevModel m, PrefillDev pf, int layer, PfWave wv, const uint16_t* apk) {
-    pdl_wait();
-    pdl_trigger();
-    TcCta c;
-    c.setup();
-    const int it = blockIdx.y, u = __ldcg(pf.chunk_u + it), e = wv.e[u];
-    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + it) * kTcM;
-    const int ntiles = m.Hmp / 16, t0 = blockIdx.x * kTcTiles, nt = min(kTcTiles, ntiles - t0);
-    const uint16_t* blk = m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems;
-    if (threadIdx.x == 0) {
-        const uint16_t* tiles[kTcTiles];
-        for (int t = 0; t < kTcTiles; ++t) tiles[t] = blk + static_cast<long long>(t0 + min(t, nt - 1)) * m.H * 32;
-        const uint16_t* hi = apk + static_cast<long long>(it) * 2 * m.H * kTcM;
-        tc_mainloop(hi, hi + static_cast<long long>(m.H) * kTcM, tiles, nt, m.H, c.smem, c.full, c.empty, c.done,
-                    c.tmem);
-    }
-    __syncwarp();
-    c.wait_done();
-    const int w = threadIdx.x >> 5, tok = w * 32 + (threadIdx.x & 31);
-    const bool valid = c0 + tok < cnt;
-    const int ent = valid ? __ldcg(pf.list + b0 + c0 + tok) : 0;
-    for (int t = 0; t < nt; ++t) {
-        float v[32];
-        tmem_ld32(c.tmem + (static_cast<uint32_t>(w * 32) << 16) + 32 * t, v);
-        if (valid)
-#pragma unroll
-            for (int r = 0; r < 16; ++r)
-                pf.Hb[static_cast<long long>(ent) * m.Hmp + (t0 + t) * 16 + r] = silu_ref(v[2 * r]) * v[2 * r + 1];
-    }
-    c.teardown();
-}
-
-// down: grid (ceil((Hp/32) / 4), items), 128 threads: raw expert rows into Y.
-__global__ void __launch_bounds__(128) k_tc_down(DevModel m, PrefillDev pf, int layer, PfWave wv,
-                                                 const uint16_t* apk) {
-    pdl_wait();
-    pdl_trigger();
-    TcCta c;
-    c.setup();
-    const int it = blockIdx.y, u = __ldcg(pf.chunk_u + it), e = wv.e[u];
-    const int b0 = pf.off[e], cnt = pf.off[e + 1] - b0, c0 = __ldcg(pf.chunk_c + it) * kTcM;
-    const int ntiles = m.Hp / 32, t0 = blockIdx.x * kTcTiles, nt = min(kTcTiles, ntiles - t0);
-    const uint16_t* blk =
-        m.slots + (static_cast<long long>(layer) * m.C + wv.slot[u]) * m.expert_elems + m.gu_elems;
-    if (threadIdx.x == 0) {
-        const uint16_t* tiles[kTcTiles];
-        for (int t = 0; t < kTcTiles; ++t) tiles[t] = blk + static_cast<long long>(t0 + min(t, nt - 1)) * m.Hmp * 32;
-        const uint16_t* hi = apk + static_cast<long long>(it) * 2 * m.Hm * kTcM;
-        tc_mainloop(hi, hi + static_cast<long long>(m.Hm) * kTcM, tiles, nt, m.Hm, c.smem, c.full, c.empty, c.done,
-                    c.tmem);
-    }
-    __syncwarp();
-    c.wait_done();
-    const int w = threadIdx.x >> 5, tok = w * 32 + (threadIdx.x & 31);
-    const bool valid = c0 + tok < cnt;
-    const int ent = valid ? __ldcg(pf.list + b0 + c0 + tok) : 0;
-    for (int t = 0; t < nt; ++t) {
-        float v[32];
-        tmem_ld32(c.tmem + (static_cast<uint32_t>(w * 32) << 16) + 32 * t, v);
-        if (valid) {
-            float* y = pf.Y + static_cast<long long>(ent) * m.Hp + (t0 + t) * 32;
-#pragma unroll
-            for (int r = 0; r < 32; r += 4) *reinterpret_cast<float4*>(y + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
-        }
-    }
-    c.teardown();
-}
-
 bool tc_prefill_supported(const DevModel& m) {
     return m.H % kTcK == 0 && m.Hm % kTcK == 0 && m.Hmp == m.Hm && m.Hp == m.H;
 }
@@ -314,10 +356,57 @@ size_t tc_pack_bytes(const DevModel& m, int items) {
     return static_cast<size_t>(items) * 2 * K * kTcM * 2;
 }
 
+int g_tc_ctas = 148;  // persistent grid: one CTA per SM (set by tc_preload)
+
 cudaError_t tc_preload() {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_gu, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tc_down, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_tc_ffn<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tc_ffn<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+    int dev = 0, sms = 0;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess && sms > 0) g_tc_ctas = sms;
     return e;
+}
+
+// The two weight gathers of the slot pool as 5-D TMA maps (built once per
+// slot pool; SMOE_TC_NO_TMAP=1 or an encode failure selects the 512-byte
+// bulk-copy path, same smem layout).
+struct TcMaps {
+    const uint16_t* slots = nullptr;
+    long long key[5] = {0, 0, 0, 0, 0};  // H, Hmp, L, C, expert_elems of the pool the maps describe
+    CUtensorMap gu{}, dn{};
+    int ok = 0;
+};
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+const TcMaps& tc_maps(const DevModel& m) {
+    static TcMaps cache;
+    const long long key[5] = {m.H, m.Hmp, m.L, m.C, m.expert_elems};
+    if (cache.slots == m.slots && std::equal(key, key + 5, cache.key)) return cache;
+    cache = TcMaps{};
+    cache.slots = m.slots;
+    std::copy(key, key + 5, cache.key);
+    static EncodeTiledFn enc = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    if (!enc || std::getenv("SMOE_TC_NO_TMAP")) return cache;
+    const cuuint64_t nslots = static_cast<cuuint64_t>(m.L) * m.C, eb = static_cast<cuuint64_t>(m.expert_elems) * 2;
+    const cuuint32_t box[5] = {8, 32, kTcTiles, kTcK / 8, 1}, es[5] = {1, 1, 1, 1, 1};
+    auto make = [&](CUtensorMap* out, const uint16_t* base, int K, int ntiles) {
+        const cuuint64_t dims[5] = {8, 32, static_cast<cuuint64_t>(ntiles), static_cast<cuuint64_t>(K / 8), nslots};
+        const cuuint64_t strides[4] = {16, static_cast<cuuint64_t>(K) * 64, 512, eb};
+        return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, const_cast<uint16_t*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    cache.ok = make(&cache.gu, m.slots, m.H, m.Hmp / 16) && make(&cache.dn, m.slots + m.gu_elems, m.Hmp, m.Hp / 32);
+    return cache;
 }
 
 // items: (wave expert, 128-token block) pairs in pf.chunk_u / chunk_c.
@@ -325,11 +414,14 @@ cudaError_t launch_pf_experts_tc(const DevModel& m, const PrefillDev& pf, int la
                                  uint16_t* apk, cudaStream_t s) {
     if (items < 1) return cudaSuccess;
     PDL(k_tc_pack, dim3((m.H / 8 + 15) / 16, items), 256, 0, s, m, pf, layer, wv, 0, apk);
-    PDL(k_tc_gu, dim3((m.Hmp / 16 + kTcTiles - 1) / kTcTiles, items), 128, kTcSmem, s, m, pf, layer, wv,
-        static_cast<const uint16_t*>(apk));
+    const int gu_work = items * ((m.Hmp / 16 + kTcTiles - 1) / kTcTiles);
+    const int dn_work = items * ((m.Hp / 32 + kTcTiles - 1) / kTcTiles);
+    const TcMaps& tm = tc_maps(m);
+    PDL(k_tc_ffn<0>, std::min(g_tc_ctas, gu_work), kTcThreads, kTcSmem, s, m, pf, layer, wv,
+        static_cast<const uint16_t*>(apk), gu_work, tm.gu, tm.ok);
     PDL(k_tc_pack, dim3((m.Hm / 8 + 15) / 16, items), 256, 0, s, m, pf, layer, wv, 1, apk);
-    PDL(k_tc_down, dim3((m.Hp / 32 + kTcTiles - 1) / kTcTiles, items), 128, kTcSmem, s, m, pf, layer, wv,
-        static_cast<const uint16_t*>(apk));
+    PDL(k_tc_ffn<1>, std::min(g_tc_ctas, dn_work), kTcThreads, kTcSmem, s, m, pf, layer, wv,
+        static_cast<const uint16_t*>(apk), dn_work, tm.dn, tm.ok);
     return cudaGetLastError();
 }
 

@@ -15,7 +15,7 @@ from paper_2603_19289_b200 import ModelConfig, Session  # noqa: E402
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 cfg = ModelConfig(layers=L, experts=128, top_k=8, hidden=2048, expert_hidden=768, vocab=256,
                   head_dim=128, seed=1)
-s = Session(cfg, cache_fraction=1.0, max_positions=256)
+s = Session(cfg, cache_fraction=1.0, max_positions=int(os.environ.get("KB_CAP", "256")))
 s.init_weights_seeded()
 s.load_default_vectors(np.zeros((L, 128, 2048), np.float32))
 s.set_predictor("router-pf")
