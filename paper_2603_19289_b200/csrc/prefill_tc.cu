@@ -395,7 +395,7 @@ const TcMaps& tc_maps(const DevModel& m) {
             return static_cast<EncodeTiledFn>(nullptr);
         return reinterpret_cast<EncodeTiledFn>(p);
     }();
-    if (!enc || std::getenv("SMOE_TC_NO_TMAP")) return cache;
+    if (!enc) return cache;
     const cuuint64_t nslots = static_cast<cuuint64_t>(m.L) * m.C, eb = static_cast<cuuint64_t>(m.expert_elems) * 2;
     const cuuint32_t box[5] = {8, 32, kTcTiles, kTcK / 8, 1}, es[5] = {1, 1, 1, 1, 1};
     auto make = [&](CUtensorMap* out, const uint16_t* base, int K, int ntiles) {
@@ -417,11 +417,12 @@ cudaError_t launch_pf_experts_tc(const DevModel& m, const PrefillDev& pf, int la
     const int gu_work = items * ((m.Hmp / 16 + kTcTiles - 1) / kTcTiles);
     const int dn_work = items * ((m.Hp / 32 + kTcTiles - 1) / kTcTiles);
     const TcMaps& tm = tc_maps(m);
+    const int use_map = tm.ok && !std::getenv("SMOE_TC_NO_TMAP");
     PDL(k_tc_ffn<0>, std::min(g_tc_ctas, gu_work), kTcThreads, kTcSmem, s, m, pf, layer, wv,
-        static_cast<const uint16_t*>(apk), gu_work, tm.gu, tm.ok);
+        static_cast<const uint16_t*>(apk), gu_work, tm.gu, use_map);
     PDL(k_tc_pack, dim3((m.Hm / 8 + 15) / 16, items), 256, 0, s, m, pf, layer, wv, 1, apk);
     PDL(k_tc_ffn<1>, std::min(g_tc_ctas, dn_work), kTcThreads, kTcSmem, s, m, pf, layer, wv,
-        static_cast<const uint16_t*>(apk), dn_work, tm.dn, tm.ok);
+        static_cast<const uint16_t*>(apk), dn_work, tm.dn, use_map);
     return cudaGetLastError();
 }
 

@@ -43,8 +43,13 @@ def _rel(a, b):
     return float(np.max(np.linalg.norm(a - b, axis=-1) / np.maximum(np.linalg.norm(b, axis=-1), 1e-30)))
 
 
+@pytest.mark.parametrize("gather", ["tensor_map", "bulk_copies"])
 @pytest.mark.parametrize("cfg,plen,frac", [(TOY, 300, 0.5), (Q30_2, 333, 0.25)])
-def test_tensor_core_prefill_within_tolerance(lib, cfg, plen, frac):
+def test_tensor_core_prefill_within_tolerance(lib, cfg, plen, frac, gather, monkeypatch):
+    """Both weight-gather paths: the 5-D TMA tensor copy and the 512-byte bulk
+    copies (SMOE_TC_NO_TMAP=1) build the same N = 256 operand."""
+    if gather == "bulk_copies":
+        monkeypatch.setenv("SMOE_TC_NO_TMAP", "1")
     prompt = np.random.default_rng(plen).integers(0, cfg["vocab"], plen).astype(np.int32)
     a = _run(cfg, prompt, 4, "exact", frac)
     b = _run(cfg, prompt, 4, "tensor", frac)
