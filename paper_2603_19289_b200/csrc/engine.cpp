@@ -732,9 +732,12 @@ void Session::alloc() {
     // The tag (a random 128-bit value) lets a peer verify, and if need be
     // find, the region inside the block its cudaIpcOpenMemHandle mapped:
     // small cudaMallocs are sub-allocated from shared driver blocks.
+    // ... | batched counters (padded) | batched exchange [2][kEpBatchMax * K][Hp] f32],
+    // at fixed offsets from the exchange buffer (ep_batch_ptrs)
     {
         const size_t cnt_bytes = (4ull * L + 255) / 256 * 256;
-        unsigned char* reg = static_cast<unsigned char*>(dalloc(256 + cnt_bytes + 4ull * 2 * K * m.Hp));
+        unsigned char* reg = static_cast<unsigned char*>(
+            dalloc(256 + cnt_bytes + 4ull * 2 * K * m.Hp + cnt_bytes + 4ull * 2 * kEpBatchMax * K * m.Hp));
         std::random_device rd;
         ep_tag_[0] = 0x31585045454f4d53ull;  // "SMOEEPX1"
         ep_tag_[1] = (static_cast<uint64_t>(rd()) << 32 ^ rd()) ^ reinterpret_cast<uintptr_t>(reg) ^
@@ -745,6 +748,11 @@ void Session::alloc() {
         d_xbuf_ = reinterpret_cast<float*>(reg + 256 + cnt_bytes);
     }
     d_epoch_ = static_cast<int*>(dalloc(4ull * L));
+    d_bepoch_ = static_cast<int*>(dalloc(4ull * L));
+    d_bdone_ = static_cast<int*>(dalloc(4ull * L));
+    ctl_.ep.bepoch = d_bepoch_;
+    ctl_.ep.bdone = d_bdone_;
+    ep_batch_ptrs(d_xbuf_, &ctl_.ep.bcnt[0], &ctl_.ep.bxbuf[0]);
     ctl_.ep.rank = 0;
     ctl_.ep.world = 1;  // EP activates at ep_connect(); until then this rank runs everything it owns
     ctl_.ep.xbuf[0] = d_xbuf_;
@@ -869,6 +877,15 @@ int Session::slots_for(float frac) const {
     return C;
 }
 
+// The batched exchange of a rank's region sits at fixed offsets after its
+// exchange buffer (same L, K, Hp on every rank): counters, then rows.
+void Session::ep_batch_ptrs(float* xbuf, int** bcnt, float** bxbuf) const {
+    const size_t cnt_bytes = (4ull * cfg_.L + 255) / 256 * 256;
+    unsigned char* b = reinterpret_cast<unsigned char*>(xbuf) + 4ull * 2 * cfg_.K * dm_.Hp;
+    *bcnt = reinterpret_cast<int*>(b);
+    *bxbuf = reinterpret_cast<float*>(b + cnt_bytes);
+}
+
 void Session::ep_buffers(void** xbuf, void** cnt) {
     *xbuf = d_xbuf_;
     *cnt = d_cnt_;
@@ -917,13 +934,18 @@ void Session::ep_connect(void* const* xbufs, void* const* cnts) {
         }
         ctl_.ep.xbuf[p] = static_cast<float*>(xbufs[p]);
         ctl_.ep.cnt[p] = static_cast<int*>(cnts[p]);
+        ep_batch_ptrs(ctl_.ep.xbuf[p], &ctl_.ep.bcnt[p], &ctl_.ep.bxbuf[p]);
     }
     ctl_.ep.xbuf[opts_.ep_rank] = d_xbuf_;
     ctl_.ep.cnt[opts_.ep_rank] = d_cnt_;
+    ep_batch_ptrs(d_xbuf_, &ctl_.ep.bcnt[opts_.ep_rank], &ctl_.ep.bxbuf[opts_.ep_rank]);
     ctl_.ep.rank = opts_.ep_rank;
     ctl_.ep.world = W;
     dset(d_cnt_, 0, 4ull * cfg_.L, "ep reset");
     dset(d_epoch_, 0, 4ull * cfg_.L, "ep reset");
+    dset(ctl_.ep.bcnt[opts_.ep_rank], 0, 4ull * cfg_.L, "ep reset");
+    dset(d_bepoch_, 0, 4ull * cfg_.L, "ep reset");
+    dset(d_bdone_, 0, 4ull * cfg_.L, "ep reset");
     // the reset must land before any peer (released by the caller's barrier)
     // starts adding to these counters
     ck(cudaDeviceSynchronize(), "ep reset sync");
@@ -1683,7 +1705,7 @@ void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt)
     const DevModel& m = dm_;
     std::vector<int> uni;
     for (int e = 0; e < c.E; ++e)
-        if (cnt[e] > 0) uni.push_back(e);
+        if (cnt[e] > 0 && is_local(e)) uni.push_back(e);  // EP: this rank's experts
     const int W = std::min<int>(C_, kMaxWave);
     for (size_t w0 = 0; w0 < uni.size(); w0 += W) {
         const int nw = static_cast<int>(std::min<size_t>(W, uni.size() - w0));
@@ -1750,7 +1772,11 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
     if (B < 1) throw std::invalid_argument("batch_generate: batch must be >= 1");
     if (P < 1) throw std::invalid_argument("generate: empty prompt");
     if (n_new < 1) throw std::invalid_argument("generate: n_new must be >= 1");
-    if (opts_.ep_world > 1) throw std::invalid_argument("batch_generate: single GPU only");
+    if (opts_.ep_world > 1 && ctl_.ep.world != opts_.ep_world)
+        throw std::invalid_argument("batch_generate: expert-parallel ranks must be connected first (ep_connect)");
+    if (ctl_.ep.world > 1 && B > kEpBatchMax)
+        throw std::invalid_argument("batch_generate: at most " + std::to_string(kEpBatchMax) +
+                                    " sequences per step under expert parallelism");
     if (mode == 1 && pred_kind_ == kNone)
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
     if (mode == 1 && pred_kind_ == kOracle)
@@ -1867,19 +1893,28 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
             else
                 ck(launch_pf_exec_pred(m, bd, l & 1, s_comp_), "batch executed = predicted");
             if (dev_lists) {
-                PfWave wv{};
+                PfWave wv{};  // every expert (wave index = expert id); work items for this rank's only
                 wv.n = c.E;
                 const std::vector<int>& row = cache_->slot_row(l);
                 for (int e = 0; e < c.E; ++e) {
                     wv.e[e] = e;
                     wv.slot[e] = row[e];
                 }
-                ck(launch_pf_experts_dev(m, bd, l, wv, max_chunks, s_comp_), "batch experts");
+                ck(launch_pf_experts_dev(m, bd, l, wv, max_chunks, s_comp_, ctl_.ep.world > 1 ? ctl_.ep.rank : 0,
+                                         ctl_.ep.world),
+                   "batch experts");
             } else {
                 d2h(cnt.data(), bd.cnt, 4ull * E, "batch counts");  // (synchronises)
-                pf_waves(bd, l, cnt);
+                pf_waves(bd, l, cnt);  // local experts only
             }
-            ck(launch_pf_mix(m, bd, s_comp_), "batch mix");
+            if (ctl_.ep.world > 1) {  // every rank's expert rows of this layer, then the mix reads them
+                ck(launch_pf_ep_combine(m, bd, ctl_.ep, l, ctl_.error, ctl_.spin_limit, s_comp_), "batch ep combine");
+                PrefillDev bx = bd;
+                bx.Y = ctl_.ep.bxbuf[ctl_.ep.rank] + static_cast<long long>(l & 1) * kEpBatchMax * K * Hp;
+                ck(launch_pf_mix(m, bx, s_comp_), "batch mix");
+            } else {
+                ck(launch_pf_mix(m, bd, s_comp_), "batch mix");
+            }
             if (md == 1 && l + 1 < c.L) {  // prediction for l+1 (speculation.cpp:174-252)
                 const int k = kind_at(l), buf = (l + 1) & 1;
                 if (k == kBaselineS) {
@@ -1918,7 +1953,7 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                     std::vector<int> first;
                     const int W = std::min<int>(C_, kMaxWave);
                     for (int e = 0; e < c.E && static_cast<int>(first.size()) < W; ++e)
-                        if (want[e]) first.push_back(e);
+                        if (want[e] && is_local(e)) first.push_back(e);
                     int hits = 0, misses = 0;
                     const auto copies = cache_->request(l + 1, first.data(), static_cast<int>(first.size()), &hits, &misses);
                     for (const auto& [slot, expert] : copies)

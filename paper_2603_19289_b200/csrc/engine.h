@@ -322,6 +322,9 @@ private:
     int pf_cap_ = 0;
     int* d_cnt_ = nullptr;                 // EP arrival counters [L]
     int* d_epoch_ = nullptr;               // EP combines done [L]
+    int* d_bepoch_ = nullptr;              // EP batched combines done [L]
+    int* d_bdone_ = nullptr;               // EP batched publish CTAs [L] (self-resetting)
+    void ep_batch_ptrs(float* xbuf, int** bcnt, float** bxbuf) const;
     std::vector<void*> ipc_opened_;
 
     // packed expert copies (xp12): H2D of the packed block into a staging ring

@@ -161,6 +161,10 @@ cudaError_t launch_pf_layer_dense(const DevModel& m, const DevState& st, const P
 cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
                               int chunks, cudaStream_t s, int chains = 8);
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
+// batched decode under EP: publish this rank's expert rows to every rank and
+// wait for every rank's rows of this layer (mix then reads the exchange buffer)
+cudaError_t launch_pf_ep_combine(const DevModel& m, const PrefillDev& pf, const DevEP& ep, int layer, int* error,
+                                 long long spin_limit, cudaStream_t s);
 // tensor-core expert GEMMs of the batched prefill (prefill_tc.cu, tolerance
 // mode): items = (wave expert, 128-token block) pairs in pf.chunk_u / chunk_c;
 // apk: packed-activation scratch of tc_pack_bytes(m, items)
@@ -188,7 +192,7 @@ cudaError_t launch_pf_decide_pred(const DevModel& m, const PrefillDev& pf, int b
 // resident experts: the (expert, chunk) list is built on the device from the
 // counts (no host round trip); wv must map every expert u < E to its slot.
 cudaError_t launch_pf_experts_dev(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
-                                  int max_chunks, cudaStream_t s);
+                                  int max_chunks, cudaStream_t s, int ep_rank = 0, int ep_world = 1);
 cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_t s);
 cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
 

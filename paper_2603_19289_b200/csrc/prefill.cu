@@ -420,6 +420,58 @@ __global__ void __launch_bounds__(32) k_pf_mix(DevModel m, PrefillDev pf) {
     warp_ssq_partial(xv, pf.ssqx + static_cast<long long>(t) * (m.Hp / 32) + rb);
 }
 
+// ------------------------------------------- batched decode under EP ----
+// The single-token combine (kernels.cu k_ffn_down / k_ep_mix) over a step's
+// B·k expert rows: every rank computed the rows Y[t·k + i] of the entries
+// whose expert it owns; k_pf_ep_publish stores those rows into every rank's
+// batched exchange buffer (peer memory; one writer per row), fences them
+// system-wide, and the last of its CTAs makes ONE system-scope arrival on
+// every rank's per-layer counter; k_pf_ep_wait (one CTA) waits for all
+// `world` arrivals of this layer's step; k_pf_mix then reads the rows from the
+// exchange buffer — the same rows, mixed in the same decision order, so the
+// result equals the single-GPU batch bit for bit.  Layer parity double-
+// buffers the exchange (a rank arrives for layer l only after its own layer-l
+// work, so no rank can be two layers ahead of a peer).
+__global__ void __launch_bounds__(128) k_pf_ep_publish(DevModel m, PrefillDev pf, DevEP ep, int layer) {
+    pf_prologue();
+    const int ent = blockIdx.x, K = m.K;
+    const int e = __ldcg(pf.ids + ent);
+    if (e % ep.world == ep.rank) {
+        const long long o = (static_cast<long long>(layer & 1) * kEpBatchMax * K + ent) * m.Hp;
+        const float4* src = reinterpret_cast<const float4*>(pf.Y + static_cast<long long>(ent) * m.Hp);
+        for (int p = 0; p < ep.world; ++p) {
+            float4* dst = reinterpret_cast<float4*>(ep.bxbuf[p] + o);
+            for (int j = threadIdx.x; j < m.Hp / 4; j += blockDim.x) __stcg(dst + j, __ldcg(src + j));
+        }
+    }
+    __threadfence_system();
+    if (last_cta(ep.bdone + layer, gridDim.x) && threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < ep.world; ++p) atomicAdd_system(ep.bcnt[p] + layer, 1);
+    }
+}
+
+__global__ void __launch_bounds__(32) k_pf_ep_wait(DevEP ep, int layer, int* error, long long spin_limit) {
+    pf_prologue();
+    if (threadIdx.x != 0) return;
+    const int want = (ep.bepoch[layer] + 1) * ep.world;
+    const int* c = ep.bcnt[ep.rank] + layer;
+    const long long t0 = clock64();
+    for (;;) {
+        int v;
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= want) break;
+        if (*(volatile int*)error) break;
+        if (clock64() - t0 > spin_limit) {
+            atomicCAS(error, 0, 4000 + layer);  // EP batched combine: a peer never arrived
+            break;
+        }
+        __nanosleep(64);
+    }
+    ep.bepoch[layer] += 1;
+    __threadfence();
+}
+
 // hands the last token to the per-token state: x, its final-norm partials,
 // position and input token, so k_final produces the prefill's next token.
 __global__ void __launch_bounds__(32) k_pf_handoff(DevModel m, DevState st, PrefillDev pf) {
@@ -519,11 +571,13 @@ __global__ void __launch_bounds__(32) k_pf_normq(DevModel m, PrefillDev pf, cons
 }
 
 // (expert, 8-token chunk) work list from the per-expert counts, expert order
-__global__ void k_pf_chunks(DevModel m, PrefillDev pf) {
+// (wave = every expert, wave index = expert id; under EP only this rank's
+// experts e % ep_world == ep_rank get work items)
+__global__ void k_pf_chunks(DevModel m, PrefillDev pf, int ep_rank, int ep_world) {
     pf_prologue();
     if (threadIdx.x == 0) {
         int k = 0;
-        for (int e = 0; e < m.E; ++e)
+        for (int e = ep_rank; e < m.E; e += ep_world)
             for (int q = 0; q < (pf.cnt[e] + kPT - 1) / kPT; ++q) {
                 pf.chunk_u[k] = e;
                 pf.chunk_c[k] = q;
@@ -618,7 +672,8 @@ cudaError_t pf_preload() {
                          (const void*)k_pf_scales, (const void*)k_pf_gemvn<PipePF>,
                          (const void*)k_pf_gemvn<PipeDeep>, (const void*)k_pf_decide_pred,
                          (const void*)k_pf_take_pred, (const void*)k_pf_quasi, (const void*)k_pf_argmax,
-                         (const void*)k_pf_chunks, (const void*)k_pf_normq};
+                         (const void*)k_pf_chunks, (const void*)k_pf_normq, (const void*)k_pf_ep_publish,
+                         (const void*)k_pf_ep_wait};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -705,8 +760,8 @@ cudaError_t launch_pf_predict(const DevModel& m, const PrefillDev& pf, int layer
 }
 
 cudaError_t launch_pf_experts_dev(const DevModel& m, const PrefillDev& pf, int layer, const PfWave& wv,
-                                  int max_chunks, cudaStream_t s) {
-    PDL(k_pf_chunks, 1, 32, 0, s, m, pf);
+                                  int max_chunks, cudaStream_t s, int ep_rank, int ep_world) {
+    PDL(k_pf_chunks, 1, 32, 0, s, m, pf, ep_rank, ep_world);
     return launch_pf_experts(m, pf, layer, wv, max_chunks, s, 0);
 }
 
@@ -761,6 +816,13 @@ cudaError_t launch_pf_experts(const DevModel& m, const PrefillDev& pf, int layer
     // chains < 8: small batches whose chunks hold 1-8 tokens -> per-chunk dispatch
     if (chains < kPT) return launch_pf_experts_t<0>(m, pf, layer, wv, chunks, s);
     return launch_pf_experts_t<kPT>(m, pf, layer, wv, chunks, s);
+}
+
+cudaError_t launch_pf_ep_combine(const DevModel& m, const PrefillDev& pf, const DevEP& ep, int layer, int* error,
+                                 long long spin_limit, cudaStream_t s) {
+    PDL(k_pf_ep_publish, pf.P * m.K, 128, 0, s, m, pf, ep, layer);
+    PDL(k_pf_ep_wait, 1, 32, 0, s, ep, layer, error, spin_limit);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pf_mix(const DevModel& m, const PrefillDev& pf, cudaStream_t s) {

@@ -359,7 +359,9 @@ size_t tc_pack_bytes(const DevModel& m, int items) {
 int g_tc_ctas = 148;  // persistent grid: one CTA per SM (set by tc_preload)
 
 cudaError_t tc_preload() {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_ffn<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+    cudaFuncAttributes fa;  // load every kernel now (lazy loading synchronises the context)
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_tc_pack);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tc_ffn<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tc_ffn<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
     int dev = 0, sms = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);

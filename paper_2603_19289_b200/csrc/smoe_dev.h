@@ -159,11 +159,17 @@ struct DevState {
 // all k rows in decision order, so EP results equal single-GPU results bit
 // for bit.
 constexpr int kMaxEP = 8;
+constexpr int kEpBatchMax = 16;  // batched decode under EP: sequences per step (BASELINE configs 2-3: B <= 16)
 struct DevEP {
     int rank, world;
     float* xbuf[kMaxEP];  // rank p's exchange buffer [2][K][Hp] (layer parity), mapped here
     int* cnt[kMaxEP];     // rank p's arrival counters [L] (monotonic)
     int* epoch;           // this rank's combines completed per layer [L]
+    // batched decode: the same scheme over the step's B·k expert rows
+    float* bxbuf[kMaxEP];  // rank p's [2][kEpBatchMax * K][Hp] (layer parity)
+    int* bcnt[kMaxEP];     // rank p's batched arrival counters [L] (monotonic)
+    int* bepoch;           // this rank's batched combines completed per layer [L]
+    int* bdone;            // [L] this rank's publish CTAs (self-resetting)
 };
 
 // Cross-stream control block (device memory unless noted).

@@ -106,3 +106,57 @@ def test_batch_generate_mixtral_shape_batch16_est_pf():
         want_t, _ = _single(s, prompts[b], 4, "prefetch")
         assert np.array_equal(toks[b], want_t), b
     s.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["on_demand", "prefetch"])
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+def test_batch_generate_expert_parallel_two_ranks(mode, frac):
+    """Batched decode under expert parallelism (SURVEY §8e, B > 1): two ranks
+    sharing this GPU, each computing only its experts' rows of the step's B·k
+    entries and exchanging them through peer stores + one system-scope
+    arrival per rank per layer (k_pf_ep_publish / k_pf_ep_wait).  Both ranks
+    return the single-GPU batch's tokens and logits bit for bit — resident
+    experts (device-built work lists, CUDA graph) and an offloaded cache
+    (host-driven waves, Algorithm 1 copies of local experts only)."""
+    import threading
+    from paper_2603_19289_b200 import ModelConfig, Session
+    ref = Session(ModelConfig(**TOY), cache_fraction=1.0, max_positions=128)
+    ref.init_weights_seeded()
+    d, _ = ref.calibrate(64, 2, 32)
+    ref.load_default_vectors(d)
+    ref.set_predictor("router-pf")
+    B, P, n_new = 6, 4, 7
+    prompts = np.random.default_rng(31).integers(0, 256, (B, P)).astype(np.int32)
+    want_t, want_lg = ref.batch_generate(prompts, n_new, mode, logits=True)
+    ref.close()
+    ranks = [Session(ModelConfig(**TOY), cache_fraction=frac, max_positions=128, ep_rank=r, ep_world=2)
+             for r in (0, 1)]
+    for s in ranks:
+        s.init_weights_seeded()
+        s.load_default_vectors(d)
+        s.set_predictor("router-pf")
+        if frac == 1.0:
+            s.preload_all()
+    bufs = [s.ep_buffers() for s in ranks]
+    for s in ranks:
+        s.ep_connect([b[0] for b in bufs], [b[1] for b in bufs])
+    out, errs = [None, None], []
+
+    def run(i):
+        try:
+            out[i] = ranks[i].batch_generate(prompts, n_new, mode, logits=True)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for toks, lg in out:
+        assert np.array_equal(toks, want_t)
+        assert np.array_equal(lg.view(np.uint32), want_lg.view(np.uint32))
+    for s in ranks:
+        s.close()
