@@ -414,8 +414,8 @@ class Oracle(_Common):
         L.orc_quasi_hidden.argtypes = [C.c_void_p] * 3 + [C.c_int, C.c_float, C.c_void_p]
         if threads:
             L.orc_set_threads(threads)
-        else:
-            L.orc_set_threads(os.cpu_count() or 1)
+        else:  # ORC_THREADS overrides; at most 32 (fills and expert FFNs split into <= 64 jobs)
+            L.orc_set_threads(int(os.environ.get("ORC_THREADS", min(os.cpu_count() or 1, 32))))
 
     def lib_err(self):
         return self.lib.orc_last_error().decode()
@@ -526,6 +526,17 @@ class Oracle(_Common):
         return p
 
 
+class _Owned(np.ndarray):
+    """A view of C-owned memory that keeps its owning handle alive (so
+    `np.array(handle_returning_call().d)` cannot read freed memory)."""
+
+
+def _owned(arr: np.ndarray, owner) -> np.ndarray:
+    v = arr.view(_Owned)
+    v._owner = owner
+    return v
+
+
 class OracleHandle:
     def __init__(self, owner, h, free_fn, **kw):
         self.owner, self.h, self._free = owner, h, free_fn
@@ -535,19 +546,19 @@ class OracleHandle:
     def d(self):
         L, E, H = self.shape
         p = self.owner.lib.orc_table_data(self.h)
-        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (L, E, H))
+        return _owned(np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (L, E, H)), self)
 
     @property
     def counts(self):
         L, E, H = self.shape
         p = self.owner.lib.orc_table_counts(self.h)
-        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_int64)), (L, E))
+        return _owned(np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_int64)), (L, E)), self)
 
     @property
     def flat(self):
         n = C.c_int64()
         p = self.owner.lib.orc_est_flat(self.h, C.byref(n))
-        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n.value,))
+        return _owned(np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n.value,)), self)
 
     def __del__(self):
         try:
@@ -572,7 +583,7 @@ class OracleModel:
         p = self.orc.lib.orc_model_tensor(self.h, name.encode(), C.byref(n))
         if not p:
             raise KeyError(name)
-        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n.value,))
+        return _owned(np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n.value,)), self)
 
     def ensure_experts(self, layer: int, ids):
         ids = np.ascontiguousarray(ids, np.int32)

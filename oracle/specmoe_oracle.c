@@ -79,6 +79,7 @@ void orc_fill_gaussian(uint64_t seed, double stddev, float* out, uint64_t n) {
     int nt = (n < (1u << 16)) ? 1 : g_threads;
     pthread_t th[64];
     fill_job jobs[64];
+    int started[64] = {0};
     if (nt > 64) nt = 64;
     for (int t = 0; t < nt; ++t) {
         jobs[t].out = out;
@@ -86,13 +87,12 @@ void orc_fill_gaussian(uint64_t seed, double stddev, float* out, uint64_t n) {
         jobs[t].stddev = stddev;
         jobs[t].begin = n * t / nt;
         jobs[t].end = n * (t + 1) / nt;
-        if (nt > 1)
-            pthread_create(&th[t], NULL, fill_worker, &jobs[t]);
-        else
-            fill_worker(&jobs[t]);
+        /* a thread that cannot be created (process / cgroup thread limits) runs inline */
+        started[t] = nt > 1 && pthread_create(&th[t], NULL, fill_worker, &jobs[t]) == 0;
+        if (!started[t]) fill_worker(&jobs[t]);
     }
-    if (nt > 1)
-        for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+    for (int t = 0; t < nt; ++t)
+        if (started[t]) pthread_join(th[t], NULL);
 }
 
 /* Rng(seed).next_u64() stream, for random_token_stream (trace.cpp:205-211). */
@@ -431,16 +431,16 @@ static void moe_block(const orc_model* m, int l, const float* s, const int* ids,
     const int par = g_threads > 1 && (size_t)H * Hm >= (1u << 18) && K <= 64;
     pthread_t th[64];
     ffn_job jobs[64];
+    int started[64] = {0};
     for (int i = 0; i < K; ++i) {
         ffn_job jb = {m, l, ids[i], s, ys + (size_t)i * H};
         jobs[i] = jb;
-        if (par)
-            pthread_create(&th[i], NULL, ffn_worker, &jobs[i]);
-        else
-            ffn_worker(&jobs[i]);
+        /* a thread that cannot be created (process / cgroup thread limits) runs inline */
+        started[i] = par && pthread_create(&th[i], NULL, ffn_worker, &jobs[i]) == 0;
+        if (!started[i]) ffn_worker(&jobs[i]);
     }
-    if (par)
-        for (int i = 0; i < K; ++i) pthread_join(th[i], NULL);
+    for (int i = 0; i < K; ++i)
+        if (started[i]) pthread_join(th[i], NULL);
     for (int j = 0; j < H; ++j) out[j] = 0.0f;
     for (int i = 0; i < K; ++i) {
         const float g = gates[i];

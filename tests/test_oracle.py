@@ -212,3 +212,20 @@ def test_oracle_vs_reference_library_live(orc, ref, gating):
     for f in ("tokens", "s", "m", "logits", "ids", "gates", "outputs", "final_logits",
               "pred_ids", "pred_gates", "pred_logits"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+def test_handle_views_keep_their_handle_alive():
+    """`np.array(model.calibrate(...).d)` drops the table handle while its
+    view is read: the view must keep the C table alive (the bench's
+    reference arm crashed on exactly this expression)."""
+    import gc
+    from oracle.bindings import Config, Oracle
+    cfg = Config(layers=2, experts=8, top_k=2, hidden=64, expert_hidden=96, vocab=64, head_dim=16, seed=3)
+    om = Oracle().build_model(cfg, round_bf16=True)
+    held = om.calibrate(16, 2, 16)
+    want = np.array(held.d)
+    v = om.calibrate(16, 2, 16).d  # the table handle is unreachable except through the view
+    gc.collect()
+    _ = [np.zeros(1 << 16) for _ in range(8)]  # churn the allocator
+    assert np.array_equal(np.array(v), want)
+    assert np.array_equal(np.array(om.calibrate(16, 2, 16).d), want)

@@ -37,6 +37,7 @@ if frac == 1.0:
     s.preload_all()
 s.calibrate(64, 2, 256)
 s.set_predictor("router-pf")
+s.set_decode_mode(os.environ.get("SMOE_DECODE_MODE", "exact"))
 rng = np.random.default_rng(4)
 forced = rng.integers(0, 256, 64).astype(np.int32)
 for mode in ("prefetch", "on_demand"):
