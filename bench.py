@@ -647,8 +647,10 @@ def main():
     # K experts x gate+up weights.  Activation reads (K x H f32) are negligible.
     fused = bool(out.get("path", {}).get("ffn_fused"))
     if fused:
-        gu_name, gu_bytes, gu_us = "k_ffn", K * 3 * Hm * H * 2, prof["ffn"]
-        gu_desc = "k_ffn (fused expert FFN: gate/up + down GEMV, one launch per layer)"
+        gu_name = "k_ffn_cs" if args.decode_mode == "fast" else "k_ffn"
+        gu_bytes, gu_us = K * 3 * Hm * H * 2, prof["ffn"]
+        gu_desc = (f"{gu_name} (fused expert FFN: gate/up + down GEMV, one launch per layer, "
+                   f"{args.decode_mode} decode arithmetic)")
     else:
         # as the headline (prefetch) decode launches it for layers >= 1: decision
         # published a layer ahead, weight stream started before the PDL wait

@@ -664,6 +664,7 @@ void Session::alloc() {
     // gate/up pipe in two round trips, and the L2 prefetch of the down blocks
     // during the gate/up phase did not turn those reads into L2 hits)
     m.ffn_fused = std::getenv("SMOE_FUSED_FFN") ? ffn_fused_ok(m, opts_.device) : 0;
+    m.ffn_cs_fused = ffn_cs_fused_ok(m, opts_.device);
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
@@ -2258,7 +2259,8 @@ void Session::path_info(int* out, int cap) const {
             wire += store_->wire_bytes(i);
             raw += store_->bytes_per_expert();
         }
-    const int v[] = {dm_.ffn_fused, dm_.attn_grid, host_ordered_ ? 1 : 0, ctl_.fast_hit,
+    const int v[] = {dm_.ffn_fused || (dm_.fast && dm_.ffn_cs_fused), dm_.attn_grid, host_ordered_ ? 1 : 0,
+                     ctl_.fast_hit,
                      store_ ? store_->numa_node() : -1, static_cast<int>(np),
                      raw ? static_cast<int>(1000 * wire / raw) : 0};
     for (int i = 0; i < cap && i < 7; ++i) out[i] = v[i];

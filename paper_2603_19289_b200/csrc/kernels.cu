@@ -1475,10 +1475,30 @@ __device__ __forceinline__ float cs_reduce(float part, float* red) {
     return s;
 }
 
-__global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevState st, DevCtl ctl, int layer,
-                                                            int exec_src, int s_from_r) {
-    KTRACE(9, layer);
-    const int lane = threadIdx.x & 31, rb = blockIdx.x, i = blockIdx.y;
+// this warp's ring behind the red / staging areas (k_ffn_gu_cs, k_ffn_cs)
+__device__ __forceinline__ unsigned char* cs_pipe_mem(const DevModel& m) {
+    float* xs = reinterpret_cast<float*>(g_smem + 128) + kCsWarps * 32;
+    return align128(reinterpret_cast<unsigned char*>(xs + round_up(max(m.H, m.Hmp), 32))) +
+           (threadIdx.x >> 5) * round_up(PipeCs::kBytes, 128);
+}
+
+// Gate/up of one (16-row block rb, executed expert i) by the CTA's kCsWarps
+// warps.  `fused`: the down projection runs in the same grid (k_ffn_cs) and
+// waits on gu_done[layer][i], counted here on every exit path.
+__device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
+                                           int exec_src, int s_from_r, int rb, int i, bool fused, PipeCs& pipe) {
+    struct Done {  // a down CTA never waits for a gate/up CTA that left early
+        const DevState& st;
+        int idx;
+        bool on;
+        __device__ ~Done() {
+            if (on && threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(st.gu_done + idx, 1);
+            }
+        }
+    } done{st, layer * m.K + i, fused};
+    const int lane = threadIdx.x & 31;
     const bool early = exec_src != 0;  // prefetch mode: decision published a layer ahead
     if (early) {
         wait_decision(st, ctl, layer);
@@ -1495,8 +1515,6 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevStat
     uint64_t* bar = reinterpret_cast<uint64_t*>(g_smem);
     float* red = reinterpret_cast<float*>(g_smem + 128);
     float* xs = red + kCsWarps * 32;
-    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(xs + round_up(H, 32))) +
-                              (threadIdx.x >> 5) * round_up(PipeCs::kBytes, 128);
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
     if (slot < 0) {
         if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
@@ -1506,11 +1524,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevStat
     cs_range(H, c0, nc);
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems +
                            static_cast<long long>(rb) * H * 32 + static_cast<long long>(c0) * 32;
-    PipeCs pipe;
-    if (nc > 0) {
-        pipe.init(pipe_mem, kL2EvictFirst);
-        pipe.prime(tile, nc);
-    }
+    if (nc > 0) pipe.prime(tile, nc);
     if (early) {
         pdl_wait();
         KT_WAITED();
@@ -1531,9 +1545,94 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevStat
     // tolerance mode only (launch_gu); SMOE_FAST is constant 0 in the exact-only object
     const float part = nc > 0 && SMOE_FAST(m) ? pipe.run_fast(tile, nc, xs + c0) : 0.0f;
     const float acc = cs_reduce(part, red);
-    if (threadIdx.x >= 32) return;
-    const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
-    if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
+    if (threadIdx.x < 32) {
+        const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
+        if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
+    }
+    if (fused) __syncthreads();  // h rows written before the count (Done)
+}
+
+__global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                            int exec_src, int s_from_r) {
+    KTRACE(9, layer);
+    PipeCs pipe;  // one ring per warp (its mbarriers are initialised once per launch)
+    pipe.init(cs_pipe_mem(m), kL2EvictFirst);
+    gu_cs_unit(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false, pipe);
+}
+
+__device__ __forceinline__ void down_block_epilogue(const DevModel& m, const DevState& st, const float* gts,
+                                                    int layer, int rb, int i, float acc);
+
+// Tolerance-mode expert FFN in ONE launch (single GPU; every CTA co-resident,
+// checked at session creation): CTA b first computes gate/up unit
+// (b % (Hmp/16), b / (Hmp/16)) as k_ffn_gu_cs, then claims down items
+// (32-row block, expert) from an atomic counter — gate/up units are never
+// claimed, so a claimed item only waits for CTAs that are already running.
+// For each item the CTA primes the item's down weights (4 warps x a column
+// slice) BEFORE waiting for the expert's gate/up units (gu_done), so the down
+// weights stream while the last gate/up tiles finish; then h, the 4-warp
+// column-split sums, and k_ffn_down's epilogue.  One launch per layer: no
+// down-kernel launch gap, ramp or gate/up tail.
+__global__ void __launch_bounds__(32 * kCsWarps) k_ffn_cs(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                         int exec_src, int s_from_r) {
+    KTRACE(15, layer);
+    const int ngu_x = m.Hmp / 16, nrb = m.Hp / 32, items = nrb * m.K;
+    const int epoch = __ldcg(st.ffn_epoch + layer);  // before this launch's last CTA bumps it
+    // one ring per warp for the whole launch: the down items continue its
+    // chunk count (re-initialising the mbarriers between runs stalled the TMA)
+    PipeCs pipe;
+    pipe.init(cs_pipe_mem(m), kL2EvictFirst);
+    gu_cs_unit(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x % ngu_x, blockIdx.x / ngu_x, true, pipe);
+    const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * m.K;
+    const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * m.K;
+    float* red = reinterpret_cast<float*>(g_smem + 128);
+    float* hs = red + kCsWarps * 32;
+    const int target = (epoch + 1) * ngu_x;
+    __shared__ int s_it;
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous item's smem
+        if (threadIdx.x == 0) s_it = atomicAdd(st.counters + 6, 1);
+        __syncthreads();
+        const int it = s_it;
+        if (__syncthreads_or(*(volatile int*)ctl.error) || it >= items) break;
+        const int i = it / nrb, rb = it % nrb;
+        const int e = __ldcg(ids + i);
+        const int slot = __ldcg(m.slot_of + layer * m.E + e);
+        if (slot < 0) {
+            if (threadIdx.x == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+            break;
+        }
+        int c0, nc;
+        cs_range(m.Hm, c0, nc);
+        const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems +
+                               static_cast<long long>(rb) * m.Hmp * 32 + static_cast<long long>(c0) * 32;
+        if (nc > 0) pipe.prime(tile, nc);  // weights do not depend on h: stream them now
+        if (threadIdx.x == 0) {  // this expert's h rows are complete
+            const int* cnt = st.gu_done + layer * m.K + i;
+            const long long t0 = clock64();
+            for (;;) {
+                int v;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                if (v >= target || *(volatile int*)ctl.error) break;
+                if (clock64() - t0 > ctl.spin_limit) {
+                    atomicCAS(ctl.error, 0, 1000 + layer);
+                    break;
+                }
+                __nanosleep(32);
+            }
+        }
+        if (__syncthreads_or(*(volatile int*)ctl.error)) break;
+        const float4* h4 = reinterpret_cast<const float4*>(st.h + static_cast<long long>(i) * m.Hmp);
+        for (int t = threadIdx.x; t < m.Hmp / 4; t += blockDim.x) reinterpret_cast<float4*>(hs)[t] = __ldcg(h4 + t);
+        __syncthreads();
+        const float part = nc > 0 && SMOE_FAST(m) ? pipe.run_fast(tile, nc, hs + c0) : 0.0f;
+        const float acc = cs_reduce(part, red);
+        if (threadIdx.x < 32) down_block_epilogue(m, st, gts, layer, rb, i, acc);
+    }
+    if (last_cta(st.counters + 5, gridDim.x) && threadIdx.x == 0) {
+        st.counters[6] = 0;  // every CTA has left its claim loop
+        st.ffn_epoch[layer] = epoch + 1;
+    }
 }
 
 // Single-GPU epilogue of one 32-row block of executed expert i's down
@@ -2293,8 +2392,9 @@ int gu_warps() {
     static const int w = std::getenv("SMOE_GU_WARPS") ? std::atoi(std::getenv("SMOE_GU_WARPS")) : kGuWarps;
     return w >= 1 && w <= 4 ? w : 1;
 }
-size_t gu_cs_smem(const DevModel& m) {
-    return 128 + kCsWarps * 32 * 4 + vec_bytes(m.H) + 128 + kCsWarps * round_up(PipeCs::kBytes, 128);
+size_t gu_cs_smem(const DevModel& m) {  // also k_ffn_cs: the staging holds s (H) or h (Hmp)
+    return 128 + kCsWarps * 32 * 4 + vec_bytes(m.H > m.Hmp ? m.H : m.Hmp) + 128 +
+           kCsWarps * round_up(PipeCs::kBytes, 128);
 }
 cudaError_t launch_gu(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer, int exec_src,
                       int s_from_r, cudaStream_t s) {
@@ -2374,6 +2474,22 @@ int ffn_fused_ok(const DevModel& m, int device) {
     return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
 }
 
+// k_ffn_cs: every CTA co-resident (claimed down items wait on gate/up units
+// of the same grid), with room left for the side-stream predictor CTAs.
+// Opt-in (SMOE_FFN_CS_FUSED=1): measured slower than k_ffn_gu_cs + k_ffn_down
+// on Q30 (22.2 vs 18.5 us per layer, tools/kbench.py): a claimed down item
+// waits for the slowest gate/up tile of its expert, and one CTA streams a
+// 48 KB down tile that 4 one-warp k_ffn_down CTAs on 4 SMs would share.
+int ffn_cs_fused_ok(const DevModel& m, int device) {
+    if (!std::getenv("SMOE_FFN_CS_FUSED")) return 0;
+    int nb = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ffn_cs, 32 * kCsWarps, gu_cs_smem(m)) != cudaSuccess)
+        return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    const long long grid = static_cast<long long>(m.Hmp / 16) * m.K;
+    return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
+}
+
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), ffn_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
@@ -2425,7 +2541,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
                          (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
                          (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast, (const void*)k_ffn_gu_cs,
-                         (const void*)k_xp_unpack};
+                         (const void*)k_xp_unpack, (const void*)k_ffn_cs};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -2450,6 +2566,7 @@ cudaError_t preload_kernels() {
     if ((e = set_smem((const void*)k_attn_fast, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gu_cs, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn_cs, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
 
@@ -2523,6 +2640,10 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
+    if (ctl.ep.world == 1 && m.fast && m.ffn_cs_fused) {  // tolerance mode: one launch per layer
+        PDL(k_ffn_cs, (m.Hmp / 16) * m.K, 32 * kCsWarps, gu_cs_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+        return counted(1);
+    }
     if (ctl.ep.world == 1 && m.ffn_fused) {
         PDL(k_ffn, (m.Hmp / 16) * m.K, 32, ffn_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
         return counted(1);

@@ -201,6 +201,7 @@ std::string kernel_limit_violation(const DevModel& m);     // "" when every kern
 std::string estimator_limit_violation(const DevModel& m);  // after the estimator dims are set
 int attn_grid_for(const DevModel& m, int device);
 int ffn_fused_ok(const DevModel& m, int device);  // 1: launch_ffn uses the one-launch k_ffn
+int ffn_cs_fused_ok(const DevModel& m, int device);  // 1: tolerance mode uses the one-launch k_ffn_cs
 cudaError_t preload_kernels();
 // Number of kernel launches enqueued by the launchers so far (host counter).
 long long launch_counter();

@@ -97,6 +97,7 @@ struct DevModel {
     int* attn_err;
     long long attn_spin;
     int ffn_fused;      // expert FFN as one launch (k_ffn) when its grid is co-resident
+    int ffn_cs_fused;   // tolerance mode: expert FFN as one launch (k_ffn_cs) when co-resident
 };
 
 // Per-stream decode state (the main stream, and the Oracle's shadow stream).

@@ -117,3 +117,10 @@ def test_fast_mode_switch_rebuilds_graphs(lib):
         out.append(np.asarray(got))
     s.close()
     assert np.array_equal(out[0], out[2])
+
+
+def test_fast_mode_one_launch_ffn_toy(lib, monkeypatch):
+    """The opt-in one-launch tolerance FFN (k_ffn_cs, SMOE_FFN_CS_FUSED=1):
+    gate/up units then claimed down items in one grid, same tolerance."""
+    monkeypatch.setenv("SMOE_FFN_CS_FUSED", "1")
+    _run(TOY, 12, 16, 0.5, 64, "toy_ffn_cs")
