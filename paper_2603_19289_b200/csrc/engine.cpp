@@ -1727,8 +1727,8 @@ void Session::pf_waves(const PrefillDev& pf, int l, const std::vector<int>& cnt)
             int hits = 0, misses = 0;
             auto copies = cache_->request(l, wv.e, nw, &hits, &misses);
             for (auto& [slot, expert] : copies)
-                copy_expert(l, expert, d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems, s_copy_,
-                            "prefill expert copy");
+                direct_bytes_ += copy_expert(l, expert, d_slots_ + (static_cast<long long>(l) * C_ + slot) * m.expert_elems,
+                                             s_copy_, "prefill expert copy");
             join_unpack(s_copy_);
             ck(cudaStreamSynchronize(s_copy_), "prefill copies");
             h2d(d_slot_of_ + static_cast<long long>(l) * c.E, cache_->slot_row(l).data(), 4ull * c.E, "slot table");
@@ -1957,10 +1957,13 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
                         if (want[e] && is_local(e)) first.push_back(e);
                     int hits = 0, misses = 0;
                     const auto copies = cache_->request(l + 1, first.data(), static_cast<int>(first.size()), &hits, &misses);
-                    for (const auto& [slot, expert] : copies)
-                        batch_prefetched_bytes_ += copy_expert(
+                    for (const auto& [slot, expert] : copies) {
+                        const long long b = copy_expert(
                             l + 1, expert, d_slots_ + (static_cast<long long>(l + 1) * C_ + slot) * m.expert_elems,
                             s_copy_, "batch prefetch copy");
+                        batch_prefetched_bytes_ += b;
+                        direct_bytes_ += b;
+                    }
                     join_unpack(s_copy_);
                 }
             }
@@ -2279,6 +2282,7 @@ void Session::clear_stats() {
     ck(cudaStreamSynchronize(s_copy_), "copy stream");
     cache_->clear_stats();
     sched_->clear_records();
+    direct_bytes_ = 0;
     n_step_events_ = 0;
 }
 
@@ -2613,7 +2617,7 @@ void Session::counters(long long* hits, long long* misses, long long* bytes, dou
             if (cudaEventElapsedTime(&t, ev_copy_[2 * r.ev], ev_copy_[2 * r.ev + 1]) == cudaSuccess) ms += t;
         }
     }
-    if (bytes) *bytes = b;
+    if (bytes) *bytes = b + direct_bytes_.load();  // + host-driven (batched) copies
     if (copy_ms) *copy_ms = ms;
     if (requests) *requests = static_cast<int>(recs.size());
 }

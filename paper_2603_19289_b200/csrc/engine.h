@@ -310,6 +310,7 @@ private:
     PrefillDev bd_{};                      // batched-decode buffers (sized for bd_cap_ sequences)
     int bd_cap_ = 0;
     long long batch_prefetched_bytes_ = 0;  // batched decode: expert bytes copied one layer ahead
+    std::atomic<long long> direct_bytes_{0};  // link bytes of host-driven copies (batched waves / prefetch)
     int pf_tc_ = 0;                         // batched prefill expert GEMMs on tcgen05 (tolerance mode)
     uint16_t* d_tc_apk_ = nullptr;          // packed activations of the tensor-core prefill
     size_t tc_apk_cap_ = 0;
