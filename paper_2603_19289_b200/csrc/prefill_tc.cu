@@ -383,7 +383,9 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 const TcMaps& tc_maps(const DevModel& m) {
-    static TcMaps cache;
+    // per host thread (sessions driven from different threads never share an
+    // entry; one thread alternating sessions re-encodes, two driver calls)
+    thread_local TcMaps cache;
     const long long key[5] = {m.H, m.Hmp, m.L, m.C, m.expert_elems};
     if (cache.slots == m.slots && std::equal(key, key + 5, cache.key)) return cache;
     cache = TcMaps{};
