@@ -380,7 +380,8 @@ int smoe_xp_unpack(const uint8_t* packed, uint16_t* out, int64_t n) {
         uint32_t hdr[4];
         std::memcpy(hdr, packed, sizeof hdr);
         if (hdr[0] != smoe::kXpMagic) throw std::invalid_argument("xp_unpack: not a packed expert block");
-        if (static_cast<int64_t>(hdr[3]) * 8 != n) throw std::invalid_argument("xp_unpack: element count mismatch");
+        if (static_cast<int64_t>(hdr[1]) * smoe::kXpGroup != n)
+            throw std::invalid_argument("xp_unpack: element count mismatch");
         smoe::xp_unpack(packed, out);
     });
 }

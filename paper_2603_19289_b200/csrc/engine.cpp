@@ -463,7 +463,19 @@ void CopyScheduler::handle(const MailboxEntry& e) {
         uint16_t* dst = s.d_slots_ + (static_cast<long long>(e.layer) * s.C_ + slot) * s.dm_.expert_elems;
         wire += s.copy_expert(e.layer, expert, dst, s.s_copy_, "H2D expert copy");
     }
-    s.join_unpack(s.s_copy_);  // the slot table and the ready flag follow the decodes
+    if (ev >= 0) ck(cudaEventRecord(s.ev_copy_[2 * ev + 1], s.s_copy_), "event record");  // link busy
+    // The slot table and the ready flag follow every byte of the request.  A
+    // packed store decodes on s_unpack_: the tail goes there (after this
+    // request's H2Ds), so the copy stream starts the next request's H2D at
+    // once instead of waiting for this request's last decode.  One tail
+    // stream per session keeps the ready values of a layer in request order.
+    cudaStream_t tail = s.s_copy_;
+    if (s.store_packed_) {
+        ck(cudaEventRecord(s.ev_h2d_tail_, s.s_copy_), "h2d tail");
+        ck(cudaStreamWaitEvent(s.s_unpack_, s.ev_h2d_tail_, 0), "h2d tail");
+        s.xp_pending_ = 0;  // the tail is ordered after every decode issued so far
+        tail = s.s_unpack_;
+    }
     if (!copies.empty()) {
         int* stage = s.h_stage_ + static_cast<long long>(stage_idx_ % 256) * E;
         // the copy that last used this staging row is >=256 requests old and
@@ -471,19 +483,18 @@ void CopyScheduler::handle(const MailboxEntry& e) {
         // can post more than a few new ones.
         std::memcpy(stage, s.cache_->slot_row(e.layer).data(), sizeof(int) * E);
         ck(cudaMemcpyAsync(s.d_slot_of_ + static_cast<long long>(e.layer) * E, stage, sizeof(int) * E,
-                           cudaMemcpyHostToDevice, s.s_copy_),
+                           cudaMemcpyHostToDevice, tail),
            "slot table update");
         ++stage_idx_;
     }
-    if (ev >= 0) ck(cudaEventRecord(s.ev_copy_[2 * ev + 1], s.s_copy_), "event record");
     static const int ready_mode = std::getenv("SMOE_READY_MODE") ? std::atoi(std::getenv("SMOE_READY_MODE")) : 0;
     if (ready_mode == 2) {
         int* flag = s.h_stage_ + 256LL * E + (stage_idx_ % 256);
         *flag = e.seq;
         ++stage_idx_;
-        ck(cudaMemcpyAsync(s.ctl_.ready + e.layer, flag, 4, cudaMemcpyHostToDevice, s.s_copy_), "ready flag");
+        ck(cudaMemcpyAsync(s.ctl_.ready + e.layer, flag, 4, cudaMemcpyHostToDevice, tail), "ready flag");
     } else {
-        const CUresult r = write_value_fn()(reinterpret_cast<CUstream>(s.s_copy_),
+        const CUresult r = write_value_fn()(reinterpret_cast<CUstream>(tail),
                                             reinterpret_cast<CUdeviceptr>(s.ctl_.ready + e.layer),
                                             static_cast<cuuint32_t>(e.seq),
                                             ready_mode == 1 ? CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER : 0);
@@ -624,7 +635,9 @@ void Session::free_all() {
         ev_h2d_[k] = ev_xp_[k] = nullptr;
     }
     if (ev_unp_join_) cudaEventDestroy(ev_unp_join_);
-    ev_unp_join_ = nullptr;
+    if (ev_h2d_tail_) cudaEventDestroy(ev_h2d_tail_);
+    if (ev_hostord2_) cudaEventDestroy(ev_hostord2_);
+    ev_unp_join_ = ev_h2d_tail_ = ev_hostord2_ = nullptr;
     s_comp_ = s_copy_ = s_side_ = s_log_ = s_unpack_ = nullptr;
 }
 
@@ -684,6 +697,8 @@ void Session::alloc() {
         ck(cudaEventCreateWithFlags(&ev_xp_[k], cudaEventDisableTiming), "event");
     }
     ck(cudaEventCreateWithFlags(&ev_unp_join_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_h2d_tail_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_hostord2_, cudaEventDisableTiming), "event");
     ev_fork_.resize(L);
     ev_join_.resize(L);
     for (int l = 0; l < L; ++l) {
@@ -1107,7 +1122,7 @@ void Session::init_weights_seeded() {
     }
     ck(cudaStreamSynchronize(s), "init sync");
     cudaFree(stage);
-    if (pack_store_) store_->pack_all();  // xp12: 12 bits per weight on the link (lossless)
+    if (pack_store_) store_packed_ = store_->pack_all() > 0;  // xp11: ~11 bits per weight on the link (lossless)
     cache_->invalidate();
     ctl_.resident = 0;
     drop_graphs();
@@ -1566,6 +1581,8 @@ void Session::host_copy_barrier(cudaStream_t s) {
     }
     ck(cudaEventRecord(ev_hostord_, s_copy_), "event");
     ck(cudaStreamWaitEvent(s, ev_hostord_, 0), "host-ordered wait");
+    ck(cudaEventRecord(ev_hostord2_, s_unpack_), "event");  // tails of a packed store
+    ck(cudaStreamWaitEvent(s, ev_hostord2_, 0), "host-ordered wait");
 }
 
 void Session::set_token(int tok) {

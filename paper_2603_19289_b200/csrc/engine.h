@@ -64,23 +64,38 @@ struct CopyRecord {  // one mailbox request as the copy lane saw it
     int ev;  // index into the event pool, -1 if none
 };
 
-// Exponent-packed bf16 expert blocks ("xp12", lossless): a block of n bf16
-// weights (n % 8 == 0) becomes
-//   [16 B header: magic, base, nesc, n/8][n/2 B exponent codes][n B sign|mantissa]
-//   [nesc x 8 B escapes: u32 index, u16 raw value, u16 0 — ascending index]
-// Element i: code c = 4-bit nibble i (low nibble first), byte b = sign<<7 |
-// mantissa; bf16 = (b & 0x80) << 8 | (base + c) << 7 | (b & 0x7f) for c < 15,
-// c == 15: the escape entry's raw value (exponents outside [base, base+14],
-// zeros, subnormals).  base: the 15-binade window with the most weights.  12 bits per weight
-// on the wire instead of 16 for Gaussian-like weights (the exponent of a
-// weight drawn around a fixed scale spans few binades).
-constexpr uint32_t kXpMagic = 0x32315058u;  // "XP12"
-constexpr int kXpHeader = 16;
-// packed size of a block with `nesc` escapes
-inline long long xp_bytes(long long n, long long nesc) { return kXpHeader + n / 2 + n + nesc * 8; }
+// Exponent-packed bf16 expert blocks ("xp11", lossless).  Sign and mantissa
+// of bf16 weights are incompressible, but the 8-bit exponent of weights drawn
+// around a fixed scale spans a few binades (Q30 init: 3 exponents hold 75 % of
+// the weights, entropy 2.55 bits), so each exponent is coded with two levels:
+//   primary    2 bits: 0/1/2 = the block's three most frequent exponents,
+//              3 = a secondary code follows;
+//   secondary  4 bits, in element order: exponent = base + c for c < 15 (the
+//              15-binade window holding the most non-primary weights), 15 =
+//              escape (zeros, subnormals, outliers: the raw value is listed).
+// A block of n bf16 weights (n % 256 == 0) becomes
+//   [32 B header: magic, n/256 groups, n_secondary, n_escape, p0, p1, p2, base]
+//   [n/4 B primary codes: element i in bits 2(i%4) of byte i/4]
+//   [n/256 x u32: secondary codes before each 256-weight group]
+//   [ceil(n_secondary/2) B secondary codes: code k in the low nibble of byte
+//    k/2 for even k, the high nibble for odd k]  (padded to 16 B)
+//   [n B sign<<7 | mantissa]
+//   [n_escape x 8 B: u32 index, u16 raw value, u16 0 — ascending index]
+// ~11.1 bits per Q30 weight on the wire instead of 16 (0.70 of raw).
+constexpr uint32_t kXpMagic = 0x31315058u;  // "XP11"
+constexpr int kXpHeader = 32;
+constexpr int kXpGroup = 256;  // weights per group (one warp decodes a group)
+inline long long xp_pad16(long long b) { return (b + 15) / 16 * 16; }
+// byte offsets of the sections of a packed block
+inline long long xp_off_groups(long long n) { return kXpHeader + n / 4; }
+inline long long xp_off_sec(long long n) { return xp_off_groups(n) + xp_pad16(4 * (n / kXpGroup)); }
+inline long long xp_off_sm(long long n, long long nsec) { return xp_off_sec(n) + xp_pad16((nsec + 1) / 2); }
+inline long long xp_off_esc(long long n, long long nsec) { return xp_off_sm(n, nsec) + n; }
+// packed size of a block with `nsec` secondary codes and `nesc` escapes
+inline long long xp_bytes(long long n, long long nsec, long long nesc) { return xp_off_esc(n, nsec) + nesc * 8; }
 // Packs `raw` (n bf16) into `out` (capacity `cap` bytes).  Returns the packed
-// size, or 0 when the block is not worth packing (n % 8, or the escapes would
-// make it larger than 7/8 of the raw bytes, or it does not fit `cap`).
+// size, or 0 when the block is not worth packing (n % 256, or it would be
+// larger than 7/8 of the raw bytes, or it does not fit `cap`).
 long long xp_pack(const uint16_t* raw, long long n, uint8_t* out, long long cap);
 // Inverse of xp_pack (host side; the device side is k_xp_unpack).
 void xp_unpack(const uint8_t* in, uint16_t* out);
@@ -328,7 +343,7 @@ private:
     void ep_batch_ptrs(float* xbuf, int** bcnt, float** bxbuf) const;
     std::vector<void*> ipc_opened_;
 
-    // packed expert copies (xp12): H2D of the packed block into a staging ring
+    // packed expert copies (xp11): H2D of the packed block into a staging ring
     // slot, then k_xp_unpack into the HBM slot, both on `s` (FIFO: a ring slot
     // is reused kXpRing copies later, after its decode ran)
     // The decodes run on their own highest-priority stream (s_unpack_), so
@@ -342,6 +357,8 @@ private:
     cudaStream_t s_unpack_ = nullptr;
     cudaEvent_t ev_h2d_[kXpRing] = {}, ev_xp_[kXpRing] = {}, ev_unp_join_ = nullptr;
     std::atomic<int> xp_pending_{0};  // decodes issued since the last join_unpack
+    bool store_packed_ = false;       // some expert block is packed: request tails run on s_unpack_
+    cudaEvent_t ev_h2d_tail_ = nullptr, ev_hostord2_ = nullptr;
     void join_unpack(cudaStream_t s);
     bool pack_store_ = std::getenv("SMOE_STORE_PACK") == nullptr || std::atoi(std::getenv("SMOE_STORE_PACK")) != 0;
     // copies expert (layer, e) from the pinned store into `dst`; returns the bytes moved over the link

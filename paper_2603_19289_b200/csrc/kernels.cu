@@ -2227,30 +2227,56 @@ __global__ void __launch_bounds__(256) k_pred_ahead(DevModel m, TraceDev tr, int
 }
 
 // ------------------------------------------------------ packed experts ----
-// Decoder of the xp12 expert block (engine.h, xpack.cpp): thread t expands
-// elements 8t..8t+7 — one 4-byte load of exponent codes, one 8-byte load of
-// sign|mantissa bytes, one 16-byte store (all coalesced); an escaped element
-// (code 15) takes its raw value from the ascending escape list (binary
-// search; ~1e-4 of Gaussian weights).  HBM-bound: 1.5 B read + 2 B written
-// per weight, ~3 us for a 9.4 MB Q30 expert, beside a ~130 us H2D.
+// section offsets of a packed block (mirror of engine.h's xp_off_*)
+__device__ __forceinline__ long long xp_off_sec_d(long long n) { return 32 + n / 4 + (4 * (n / 256) + 15) / 16 * 16; }
+__device__ __forceinline__ long long xp_off_sm_d(long long n, long long nsec) {
+    return xp_off_sec_d(n) + ((nsec + 1) / 2 + 15) / 16 * 16;
+}
+
+// Decoder of the xp11 expert block (engine.h, xpack.cpp): one warp per
+// 256-weight group, lane l expands weights 8l..8l+7 — one 2-byte load of its
+// primary codes, a warp scan of its secondary-code count (offset into the
+// group's secondary stream, whose start the block's group table holds), its
+// secondary nibbles, one 8-byte load of sign|mantissa bytes and one 16-byte
+// store; an escaped weight takes its raw value from the ascending escape list
+// (binary search; ~1e-4 of Gaussian weights).  HBM-bound: ~1.4 B read + 2 B
+// written per weight, a few µs per 9.4 MB Q30 expert beside a ~120 µs H2D.
 __global__ void __launch_bounds__(256) k_xp_unpack(const uint8_t* __restrict__ src, uint16_t* __restrict__ dst) {
     const uint32_t* hdr = reinterpret_cast<const uint32_t*>(src);
-    const uint32_t base = __ldg(hdr + 1), nesc = __ldg(hdr + 2), n8 = __ldg(hdr + 3);
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= n8) return;
-    const uint8_t* codes = src + 16;
-    const uint8_t* sm = codes + static_cast<long long>(n8) * 4;
-    const uint8_t* esc = sm + static_cast<long long>(n8) * 8;
-    const uint32_t c = __ldcs(reinterpret_cast<const unsigned int*>(codes) + t);
-    const uint2 b = __ldcs(reinterpret_cast<const uint2*>(sm) + t);
+    const uint32_t ngroups = __ldg(hdr + 1), nsec = __ldg(hdr + 2), nesc = __ldg(hdr + 3);
+    const uint32_t g = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (g >= ngroups) return;
+    const uint32_t p0 = __ldg(hdr + 4), p1 = __ldg(hdr + 5), p2 = __ldg(hdr + 6), base = __ldg(hdr + 7);
+    const long long n = static_cast<long long>(ngroups) * 256;
+    const uint8_t* sc = src + xp_off_sec_d(n);
+    const uint8_t* sm = src + xp_off_sm_d(n, nsec);
+    const uint8_t* esc = sm + n;
+    const uint32_t c16 = __ldg(reinterpret_cast<const unsigned short*>(src + 32 + static_cast<long long>(g) * 64) + lane);
+    const int cnt = __popc(c16 & (c16 >> 1) & 0x5555u);  // codes == 3: secondary follows
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (static_cast<int>(lane) >= o) incl += t;
+    }
+    uint32_t k = __ldg(reinterpret_cast<const uint32_t*>(src + 32 + n / 4) + g) + (incl - cnt);
+    const uint2 b = __ldcs(reinterpret_cast<const uint2*>(sm + static_cast<long long>(g) * 256) + lane);
     uint32_t w[4];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const uint32_t code = (c >> (4 * j)) & 15u;
+        const uint32_t c = (c16 >> (2 * j)) & 3u;
+        uint32_t e = c == 0 ? p0 : (c == 1 ? p1 : p2);
+        bool escaped = false;
+        if (c == 3u) {
+            const uint32_t s2 = (__ldg(sc + (k >> 1)) >> (4 * (k & 1))) & 15u;
+            ++k;
+            e = base + s2;
+            escaped = s2 == 15u;
+        }
         const uint32_t byte = ((j < 4 ? b.x : b.y) >> (8 * (j & 3))) & 0xffu;
-        uint32_t v = ((byte & 0x80u) << 8) | ((base + code) << 7) | (byte & 0x7fu);
-        if (code == 15u) {  // escape: raw value from the list (ascending indices)
-            const uint32_t idx = static_cast<uint32_t>(t * 8 + j);
+        uint32_t v = ((byte & 0x80u) << 8) | ((e & 0xffu) << 7) | (byte & 0x7fu);
+        if (escaped) {  // raw value from the list (ascending indices)
+            const uint32_t idx = static_cast<uint32_t>(g * 256 + lane * 8 + j);
             uint32_t lo = 0, hi = nesc;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
@@ -2262,15 +2288,15 @@ __global__ void __launch_bounds__(256) k_xp_unpack(const uint8_t* __restrict__ s
         if (j & 1) w[j >> 1] |= v << 16;
         else w[j >> 1] = v;
     }
-    reinterpret_cast<uint4*>(dst)[t] = make_uint4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<uint4*>(dst + static_cast<long long>(g) * 256)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 std::atomic<long long> g_xp_launches{0};  // copy-lane launches (outside the decode graphs)
 long long xp_unpack_launches() { return g_xp_launches.load(); }
 
 cudaError_t launch_xp_unpack(const uint8_t* src, uint16_t* dst, long long n, cudaStream_t s) {
-    const long long n8 = n / 8;
-    k_xp_unpack<<<static_cast<unsigned>((n8 + 255) / 256), 256, 0, s>>>(src, dst);
+    const long long groups = n / 256;
+    k_xp_unpack<<<static_cast<unsigned>((groups + 7) / 8), 256, 0, s>>>(src, dst);
     ++g_xp_launches;
     return cudaGetLastError();
 }

@@ -94,7 +94,7 @@ cudaError_t launch_distill(const DevModel& m, const TraceDev& tr, int first, int
                            float* targets, cudaStream_t s);
 
 // Router-pf ids `depth` layers ahead over trace steps; out [n][L][K] (rows < depth untouched).
-// Expands one exponent-packed expert block (xp12, engine.h) from `src` (HBM
+// Expands one exponent-packed expert block (xp11, engine.h) from `src` (HBM
 // staging) into the bf16 slot `dst` (n elements); on the copy stream.
 cudaError_t launch_xp_unpack(const uint8_t* src, uint16_t* dst, long long n, cudaStream_t s);
 long long xp_unpack_launches();  // k_xp_unpack launches so far (process-wide)

@@ -184,7 +184,7 @@ def layer_hit_rates(exec_ids, true_ids) -> np.ndarray:
 
 
 def xp_pack(raw) -> bytes | None:
-    """Exponent-packed (xp12) form of a bf16 block given as uint16 [n]; None when
+    """Exponent-packed (xp11) form of a bf16 block given as uint16 [n]; None when
     the block does not pack (the store then keeps it raw)."""
     lib = load_library()
     raw = np.ascontiguousarray(raw, np.uint16)
