@@ -716,7 +716,7 @@ def main():
                 "achieved_GBps": h2d_gbps, "link_peak_GBps": link,
                 "frac": (h2d_gbps / link) if h2d_gbps else None,
                 "peak_how": "same pinned store, expert-sized cudaMemcpyAsync H2D, 128 copies",
-                "store_format": ("xp12: exponent-packed bf16, lossless (12 bits per weight on the link; "
+                "store_format": ("xp11: exponent-packed bf16, lossless (2-bit primary / 4-bit secondary exponent codes, ~11 bits per weight on the link; "
                                  "k_xp_unpack restores the bf16 block in the HBM slot)"
                                  if out.get("path", {}).get("store_packed_blocks") else "raw bf16"),
                 "wire_per_raw": out.get("path", {}).get("store_wire_per_raw", 1.0),

@@ -342,8 +342,8 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
  * link bytes per 1000 raw expert bytes. */
 int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap);
 
-/* Lossless exponent packing of one bf16 expert block ("xp12", engine.h):
- * the pinned store's wire format (12 bits per Gaussian-like weight instead of
+/* Lossless exponent packing of one bf16 expert block ("xp11", engine.h):
+ * the pinned store's wire format (~11 bits per Gaussian-like weight instead of
  * 16; SMOE_STORE_PACK=0 keeps the store raw).  Host only, no GPU needed.
  * smoe_xp_pack writes at most `cap` bytes and sets *packed_bytes (0: the block
  * does not pack — n % 8 != 0 or too many escapes); smoe_xp_unpack restores the

@@ -298,7 +298,7 @@ def test_copy_lane_invariants(lib):
     assert int(c["hits"].sum()) == sum(e.hits for e in ev)
     per = 3 * TOY["hidden"] * TOY["expert_hidden"] * 2  # toy dims need no tile padding
     # the link carries the store's wire format: raw bf16 or exponent-packed
-    # (xp12, ~0.75 of raw; per-block size varies by a few escapes)
+    # (xp11, ~0.70 of raw; per-block size varies by a few escapes)
     ratio = s.path_info()["store_wire_per_raw"]
     assert all(abs(e.bytes - e.misses * per * ratio) <= e.misses * per * 0.003 for e in ev)
     spans = sorted((e.start_ms, e.end_ms) for e in ev if e.misses > 0)

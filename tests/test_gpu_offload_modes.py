@@ -189,7 +189,7 @@ def test_decision_routine_vs_oracle(lib, E, K, gating):
 
 @pytest.mark.parametrize("mode", ["on_demand", "prefetch"])
 def test_packed_expert_store_is_lossless_on_the_copy_path(lib, toy, mode):
-    """Experts travel exponent-packed (xp12) and k_xp_unpack restores them in
+    """Experts travel exponent-packed (xp11) and k_xp_unpack restores them in
     the slot: same trace as the raw store, bit for bit, with ~3/4 of the link
     bytes; and both equal the oracle."""
     orc, om, table = toy
@@ -203,7 +203,7 @@ def test_packed_expert_store_is_lossless_on_the_copy_path(lib, toy, mode):
     rb, evb = _decode(pk, table, prompt, 24, mode, stream)
     for k in ("id_exec", "id_true", "s", "m", "logits", "tokens", "hits", "misses"):
         assert np.array_equal(ra[k], rb[k]), k
-    assert ra["bytes"] > 0 and 0.74 < rb["bytes"] / ra["bytes"] < 0.77
+    assert ra["bytes"] > 0 and 0.66 < rb["bytes"] / ra["bytes"] < 0.74
     pred = orc.make_predictor("router-pf", om, table) if mode == "prefetch" else None
     want = om.generate_trace(prompt, 25, pred, forced=np.array(stream[:24], np.int32))
     assert np.array_equal(rb["id_exec"], want.ids)
