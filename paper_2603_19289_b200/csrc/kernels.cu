@@ -676,8 +676,63 @@ __device__ __forceinline__ float* attn_fast_scratch(const DevModel& m, double* s
 }
 bool attn_fast_ok(const DevModel& m) { return SMOE_FAST(m) && m.D % 4 == 0 && m.D <= kAttnFastThreads; }
 size_t attn_fast_smem(const DevModel& m) { return 2ull * kAttnFastChunk * (2 * m.D + 4) * 4; }
+constexpr int kAttnGroup = 16;  // flash-decoding merge: partials per first-level group
+constexpr int kAttnGroups = (kAttnFastCtas + kAttnGroup - 1) / kAttnGroup;
 size_t attn_scratch_bytes(int cap) {
-    return 16ull * cap + 1024 + static_cast<size_t>(kAttnFastCtas) * (kMaxD + 2) * 4 + 64;
+    // e/p | CTA partials [kAttnFastCtas][kMaxD+2] | counters (64 B) | group partials | group counters
+    return 16ull * cap + 1024 + static_cast<size_t>(kAttnFastCtas) * (kMaxD + 2) * 4 + 64 +
+           static_cast<size_t>(kAttnGroups) * (kMaxD + 2) * 4 + 4 * (kAttnGroups + 1) + 64;
+}
+
+// Merge n online-softmax partials (m_q, l_q, acc_q[D]) at src (stride
+// kMaxD + 2): M = max m_q, f_q = exp(m_q - M), L = sum f_q l_q (fixed-order
+// block tree), acc = sum_q f_q acc_q (thread i: dim i, 32 loads in flight).
+// Every step is parallel over the partials; the order is fixed, so the
+// result is deterministic.  Whole block; returns M and L in every thread and
+// acc in threads < D.
+__device__ __forceinline__ void attn_merge(const float* src, int n, int D, float* fq, float* lq, float* red,
+                                           float& M, float& L, float& acc) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    float mx = -INFINITY;
+    for (int q = tid; q < n; q += blockDim.x) {
+        const float* pq = src + static_cast<long long>(q) * (kMaxD + 2);
+        const float mq = __ldcg(pq);
+        fq[q] = mq;
+        lq[q] = __ldcg(pq + 1);
+        mx = fmaxf(mx, mq);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[w] = mx;
+    __syncthreads();
+    M = red[0];
+    for (int q = 1; q < nw; ++q) M = fmaxf(M, red[q]);
+    __syncthreads();  // red reused below
+    float lt = 0.0f;
+    for (int q = tid; q < n; q += blockDim.x) {
+        const float f = __expf(fq[q] - M);
+        fq[q] = f;
+        lt = fmaf(f, lq[q], lt);
+    }
+    for (int o = 16; o > 0; o >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, o);
+    if (lane == 0) red[w] = lt;
+    __syncthreads();  // fq complete, red holds the warp sums
+    L = 0.0f;
+    for (int q = 0; q < nw; ++q) L += red[q];
+    float a = 0.0f;
+    if (tid < D) {
+        constexpr int kB = 32;
+        int q = 0;
+        for (; q + kB <= n; q += kB) {
+            float v[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) v[u] = __ldcg(src + static_cast<long long>(q + u) * (kMaxD + 2) + 2 + tid);
+#pragma unroll
+            for (int u = 0; u < kB; ++u) a = fmaf(fq[q + u], v[u], a);
+        }
+        for (; q < n; ++q) a = fmaf(fq[q], __ldcg(src + static_cast<long long>(q) * (kMaxD + 2) + 2 + tid), a);
+    }
+    acc = a;
+    __syncthreads();  // fq / lq / red free
 }
 
 __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevState st, double* scratch,
@@ -686,7 +741,6 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
     const int D = m.D, KS = D + 4;  // padded key rows: thread j's LDS.128 of row j is conflict-free
     __shared__ __align__(16) float qs[kAttnFastThreads];
     __shared__ float red[kAttnFastThreads / 32];
-    __shared__ float s_l;
     __shared__ int s_last;
     float* kt = reinterpret_cast<float*>(g_smem);  // [2][chunk][D+4]
     float* vt = kt + 2 * kAttnFastChunk * KS;      // [2][chunk][D]
@@ -698,7 +752,7 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
     int* cnt = reinterpret_cast<int*>(part + kAttnFastCtas * (kMaxD + 2));
     // st.pos is only advanced by k_final, which completed before this grid could launch
     const int pos = __ldcg(st.pos), n = pos + 1, b = blockIdx.x;
-    const int ppc = max(4 * kAttnFastChunk, (n + gridDim.x - 1) / gridDim.x);
+    const int ppc = max(2 * kAttnFastChunk, (n + gridDim.x - 1) / gridDim.x);  // both chunks in the ring
     const int G = (n + ppc - 1) / ppc;  // CTAs with positions
     if (b >= G) {  // no positions: leave at once (an exit counts as the PDL trigger)
 #ifdef SMOE_ATTN_IDLE_WAIT
@@ -796,53 +850,53 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
         if (tid < D) st.ctx[tid] = acc / lrun;
         return;
     }
+    // two-level merge: the last CTA of each group of kAttnGroup merges the
+    // group's partials into a group partial, the last group merges those
+    // (a single last-arriver merging every CTA serially bounded long contexts)
     float* pb = part + static_cast<long long>(b) * (kMaxD + 2);
     if (tid == 0) {
         pb[0] = mrun;
         pb[1] = lrun;
     }
     if (tid < D) pb[2 + tid] = acc;
+    float* gpart = reinterpret_cast<float*>(cnt + 16);  // [kAttnGroups][kMaxD+2]
+    int* gcnt = reinterpret_cast<int*>(gpart + kAttnGroups * (kMaxD + 2));  // [kAttnGroups + 1]
+    const int g = b / kAttnGroup, ng = (G + kAttnGroup - 1) / kAttnGroup;
+    const int gsize = min(kAttnGroup, G - g * kAttnGroup);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(cnt, 1) == G - 1;
+    if (tid == 0) {
+        s_last = atomicAdd(gcnt + g, 1) == gsize - 1;
+        if (s_last) gcnt[g] = 0;
+    }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (tid == 0) *cnt = 0;
-    // merge: the CTAs' maxima and weights in parallel (f[q] = exp(m_q - M)),
-    // then thread i sums dim i over the CTAs in CTA order, loads in flight
     __shared__ float fq[kAttnFastCtas];
-    float M = -INFINITY;
-    for (int q = tid; q < G; q += blockDim.x) M = fmaxf(M, __ldcg(part + static_cast<long long>(q) * (kMaxD + 2)));
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    if (lane == 0) red[w] = M;
-    __syncthreads();
-    M = red[0];
-    for (int q = 1; q < nw; ++q) M = fmaxf(M, red[q]);
-    for (int q = tid; q < G; q += blockDim.x) {
-        const float* pq = part + static_cast<long long>(q) * (kMaxD + 2);
-        fq[q] = __expf(__ldcg(pq) - M);
+    __shared__ float lq[kAttnFastCtas];
+    float M, Lt, a;
+    attn_merge(part + static_cast<long long>(g) * kAttnGroup * (kMaxD + 2), gsize, D, fq, lq, red, M, Lt, a);
+    if (ng == 1) {
+        if (tid < D) st.ctx[tid] = a / Lt;
+        return;
     }
+    float* gp = gpart + static_cast<long long>(g) * (kMaxD + 2);
+    if (tid == 0) {
+        gp[0] = M;
+        gp[1] = Lt;
+    }
+    if (tid < D) gp[2 + tid] = a;
+    __threadfence();
     __syncthreads();
     if (tid == 0) {
-        float Lt = 0.0f;
-        for (int q = 0; q < G; ++q) Lt = fmaf(fq[q], __ldcg(part + static_cast<long long>(q) * (kMaxD + 2) + 1), Lt);
-        s_l = Lt;
-    }
-    float a = 0.0f;
-    if (tid < D) {
-        int q = 0;
-        for (; q + 8 <= G; q += 8) {
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + static_cast<long long>(q + u) * (kMaxD + 2) + 2 + tid);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) a = fmaf(fq[q + u], v[u], a);
-        }
-        for (; q < G; ++q) a = fmaf(fq[q], __ldcg(part + static_cast<long long>(q) * (kMaxD + 2) + 2 + tid), a);
+        s_last = atomicAdd(gcnt + kAttnGroups, 1) == ng - 1;
+        if (s_last) gcnt[kAttnGroups] = 0;
     }
     __syncthreads();
-    if (tid < D) st.ctx[tid] = a / s_l;
+    if (!s_last) return;
+    __threadfence();
+    attn_merge(gpart, ng, D, fq, lq, red, M, Lt, a);
+    if (tid < D) st.ctx[tid] = a / Lt;
 }
 
 // attn_out = wo . ctx; r = x + attn_out (model.cpp:352, 380).
@@ -1498,6 +1552,7 @@ __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st
             }
         }
     } done{st, layer * m.K + i, fused};
+    KTRACE(9, layer);
     const int lane = threadIdx.x & 31;
     const bool early = exec_src != 0;  // prefetch mode: decision published a layer ahead
     if (early) {
@@ -1554,7 +1609,6 @@ __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st
 
 __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevState st, DevCtl ctl, int layer,
                                                             int exec_src, int s_from_r) {
-    KTRACE(9, layer);
     PipeCs pipe;  // one ring per warp (its mbarriers are initialised once per launch)
     pipe.init(cs_pipe_mem(m), kL2EvictFirst);
     gu_cs_unit(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false, pipe);
