@@ -676,7 +676,7 @@ __device__ __forceinline__ float* attn_fast_scratch(const DevModel& m, double* s
 }
 bool attn_fast_ok(const DevModel& m) { return SMOE_FAST(m) && m.D % 4 == 0 && m.D <= kAttnFastThreads; }
 size_t attn_fast_smem(const DevModel& m) { return 2ull * kAttnFastChunk * (2 * m.D + 4) * 4; }
-constexpr int kAttnGroup = 16;  // flash-decoding merge: partials per first-level group
+constexpr int kAttnGroup = 32;  // flash-decoding merge: partials per first-level group (one 32-load batch)
 constexpr int kAttnGroups = (kAttnFastCtas + kAttnGroup - 1) / kAttnGroup;
 size_t attn_scratch_bytes(int cap) {
     // e/p | CTA partials [kAttnFastCtas][kMaxD+2] | counters (64 B) | group partials | group counters
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
         if (tid < D) st.ctx[tid] = acc / lrun;
         return;
     }
-    // two-level merge: the last CTA of each group of kAttnGroup merges the
+    // two-level merge: the last CTA of each group of kAttnGroup (32) merges the
     // group's partials into a group partial, the last group merges those
     // (a single last-arriver merging every CTA serially bounded long contexts)
     float* pb = part + static_cast<long long>(b) * (kMaxD + 2);
