@@ -91,6 +91,12 @@ def test_fast_mode_long_context_toy(lib):
     _run(dict(TOY, layers=3), 700, 6, 0.5, 64, "toy_long")
 
 
+def test_fast_mode_two_level_attention_merge_toy(lib):
+    """2200+ positions: more than 32 attention CTAs, so the partials merge in
+    two levels (groups of 32, then the group partials)."""
+    _run(dict(TOY, layers=2), 2200, 4, 0.5, 64, "toy_2k_two_level")
+
+
 def test_fast_mode_long_context_q30_layers(lib):
     """head_dim 128 (float4 lanes) over 1100+ positions."""
     _run(dict(Q30, layers=2), 1100, 4, 0.25, 256, "q30_L2_long")
