@@ -233,7 +233,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     forced = token_stream(args.warmup + args.steps, c["vocab"], 4)
 
     def measure(mode: str, workload: str) -> dict:
-        tpots, h2d, cms, hit, miss, recall = [], [], [], [], [], []
+        tpots, h2d, cms, hit, miss, recall, xpk = [], [], [], [], [], [], []
         clk = ClockSampler(dev)  # accumulates over every timed region of this mode
         for run in range(args.runs):
             S = P + args.warmup + args.steps
@@ -243,8 +243,10 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                 if args.warmup:
                     s.decode_stream(mode, forced[: args.warmup])
                 s.clear_stats()
+                x0 = s.path_info()["copy_lane_kernels"]
                 with clk:
                     s.decode_stream(mode, forced[args.warmup:])
+                xpk.append(s.path_info()["copy_lane_kernels"] - x0)
             else:
                 if args.warmup:
                     s.decode(mode, args.warmup)
@@ -268,6 +270,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                     h2d_bytes_per_token=float(np.mean(h2d)), copy_busy_ms=float(np.mean(cms)),
                     cache_hits=hit, cache_misses=miss, clocks=clk.summary(),
                     kernels_per_step=s.kernels_per_step(mode),
+                    copy_lane_kernels=int(np.mean(xpk)) if xpk else 0,
                     online_recall=float(np.mean(recall)) if recall else None)
 
     res = {}
@@ -757,8 +760,10 @@ def main():
         "e2e": {"value": out["e2e_ms"], "unit": "ms", "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": 4 * c["vocab"] + 4,
                 "how": "smoe_step(): host token -> device, graph step, logits -> host, wall clock"},
-        "gpu_launches": ks * args.steps if ks and ks > 0 else None,
+        # graph kernels of the timed steps + the copy lane's expert decodes (k_xp_unpack, one per miss)
+        "gpu_launches": (ks * args.steps + pf.get("copy_lane_kernels", 0)) if ks and ks > 0 else None,
         "kernels_per_step": ks,
+        "copy_lane_kernels": pf.get("copy_lane_kernels", 0),
         "long_context": out.get("long_ctx"),
         "clocks": pf["clocks"],
         "setup_s": {"alloc": out["t_alloc"], "init_weights": out["t_init"],

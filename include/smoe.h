@@ -339,7 +339,8 @@ int smoe_recall_at_k(const int32_t* pred, const int32_t* truth, int32_t k, doubl
  * SMOE_HOST_ORDERED=1); out[3] device-side all-hit release; out[4] NUMA node
  * the pinned expert store is bound to (-1: not bound — single-node host);
  * out[5] expert blocks held exponent-packed in the pinned store; out[6]
- * link bytes per 1000 raw expert bytes. */
+ * link bytes per 1000 raw expert bytes; out[7] copy-lane decode kernels
+ * (k_xp_unpack) launched so far in this process. */
 int smoe_path_info(smoe_session* s, int32_t* out, int32_t cap);
 
 /* Lossless exponent packing of one bf16 expert block ("xp11", engine.h):

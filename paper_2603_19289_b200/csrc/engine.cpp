@@ -2282,8 +2282,9 @@ void Session::path_info(int* out, int cap) const {
     const int v[] = {dm_.ffn_fused || (dm_.fast && dm_.ffn_cs_fused), dm_.attn_grid, host_ordered_ ? 1 : 0,
                      ctl_.fast_hit,
                      store_ ? store_->numa_node() : -1, static_cast<int>(np),
-                     raw ? static_cast<int>(1000 * wire / raw) : 0};
-    for (int i = 0; i < cap && i < 7; ++i) out[i] = v[i];
+                     raw ? static_cast<int>(1000 * wire / raw) : 0,
+                     static_cast<int>(xp_unpack_launches() & 0x7fffffff)};
+    for (int i = 0; i < cap && i < 8; ++i) out[i] = v[i];
 }
 
 int Session::kernels_per_step(int mode) const {

@@ -548,11 +548,12 @@ class Session:
         _check(self.lib.smoe_set_prefill_mode(self._h, {"exact": 0, "tensor": 1}[mode]))
 
     def path_info(self) -> dict:
-        out = np.zeros(7, np.int32)
-        _check(self.lib.smoe_path_info(self._h, _p(out), 7))
+        out = np.zeros(8, np.int32)
+        _check(self.lib.smoe_path_info(self._h, _p(out), 8))
         return {"ffn_fused": bool(out[0]), "attn_ctas": int(out[1]), "host_ordered": bool(out[2]),
                 "device_hit_path": bool(out[3]), "store_numa_node": int(out[4]),
-                "store_packed_blocks": int(out[5]), "store_wire_per_raw": float(out[6]) / 1000.0}
+                "store_packed_blocks": int(out[5]), "store_wire_per_raw": float(out[6]) / 1000.0,
+                "copy_lane_kernels": int(out[7])}
 
     def measure_link(self, n_copies: int = 64) -> float:
         g = C.c_double()
