@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
     __shared__ int s_last;
     float* kt = reinterpret_cast<float*>(g_smem);  // [2][chunk][D+4]
     float* vt = kt + 2 * kAttnFastChunk * KS;      // [2][chunk][D]
-    __shared__ float ps[kAttnFastChunk];
+    __shared__ float ps[2 * kAttnFastChunk];
     const long long base = static_cast<long long>(layer) * m.cap * D;
     const float* K = st.kc + base;
     const float* V = st.vc + base;
@@ -761,11 +761,16 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
 #endif
         return;
     }
-    const int j0 = b * ppc, j1 = min(n, j0 + ppc), nch = (j1 - j0 + kAttnFastChunk - 1) / kAttnFastChunk;
+    // a slice of <= 2 chunks (every CTA up to ~19 k positions, and the one
+    // CTA of a short context) is one pass over both ring slots as a single
+    // 64-position chunk: one softmax round instead of two
+    const int j0 = b * ppc, j1 = min(n, j0 + ppc);
+    const int CH = j1 - j0 <= 2 * kAttnFastChunk ? 2 * kAttnFastChunk : kAttnFastChunk;
+    const int nch = (j1 - j0 + CH - 1) / CH;
     auto fetch = [&](int c, int skip) {
-        const int p0 = j0 + c * kAttnFastChunk, pn = min(kAttnFastChunk, j1 - p0);
-        float* kd = kt + (c & 1) * kAttnFastChunk * KS;
-        float* vd = vt + (c & 1) * kAttnFastChunk * D;
+        const int p0 = j0 + c * CH, pn = min(CH, j1 - p0);
+        float* kd = kt + (c & 1) * CH * KS;
+        float* vd = vt + (c & 1) * CH * D;
         const int per = D / 4;
         for (int t = threadIdx.x; t < pn * per; t += blockDim.x) {
             const int r = t / per, q4 = (t % per) * 4;
@@ -783,10 +788,10 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
     pdl_trigger();
     for (int t = threadIdx.x; t < D / 4; t += blockDim.x) {
         cp_async16(qs + 4 * t, st.q + 4 * t);
-        const int c = (pos - j0) / kAttnFastChunk, r = (pos - j0) % kAttnFastChunk;
+        const int c = (pos - j0) / CH, r = (pos - j0) % CH;
         if (pos >= j0 && pos < j1 && c < 2) {
-            cp_async16(kt + (c & 1) * kAttnFastChunk * KS + r * KS + 4 * t, K + static_cast<long long>(pos) * D + 4 * t);
-            cp_async16(vt + (c & 1) * kAttnFastChunk * D + r * D + 4 * t, V + static_cast<long long>(pos) * D + 4 * t);
+            cp_async16(kt + (c & 1) * CH * KS + r * KS + 4 * t, K + static_cast<long long>(pos) * D + 4 * t);
+            cp_async16(vt + (c & 1) * CH * D + r * D + 4 * t, V + static_cast<long long>(pos) * D + 4 * t);
         }
     }
     cp_async_commit();
@@ -798,9 +803,9 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
         else
             cp_async_wait<0>();  // (c = 0: q and row pos too)
         __syncthreads();
-        const int p0 = j0 + c * kAttnFastChunk, pn = min(kAttnFastChunk, j1 - p0);
-        const float* kc = kt + (c & 1) * kAttnFastChunk * KS;
-        const float* vc = vt + (c & 1) * kAttnFastChunk * D;
+        const int p0 = j0 + c * CH, pn = min(CH, j1 - p0);
+        const float* kc = kt + (c & 1) * CH * KS;
+        const float* vc = vt + (c & 1) * CH * D;
         float sj = -INFINITY;
         if (tid < pn) {
             const float* kj = kc + tid * KS;
@@ -825,7 +830,7 @@ __global__ void __launch_bounds__(kAttnFastThreads) k_attn_fast(DevModel m, DevS
         const float mn = fmaxf(mrun, cm);
         const float sc = __expf(mrun - mn);  // 0 on the first chunk
         const float p = tid < pn ? __expf(sj - mn) : 0.0f;
-        if (tid < kAttnFastChunk) ps[tid] = p;
+        if (tid < CH) ps[tid] = p;
         float cs = p;
         for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
         __syncthreads();  // red (max) read by all; ps complete
