@@ -1367,6 +1367,11 @@ void Session::check_device_error() {
             throw std::runtime_error("split attention stalled at layer " + std::to_string(err - 4000) +
                                      ": its CTAs were not co-resident within " +
                                      std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) + " ms");
+        if (err >= 5000 && err < 6000)
+            throw std::runtime_error("deadlock suspected: batched expert-parallel combine of layer " +
+                                     std::to_string(err - 5000) + " waited " +
+                                     std::to_string(static_cast<long long>(opts_.deadlock_s * 1000)) +
+                                     " ms for peer ranks");
         throw std::runtime_error("expert read before readiness at layer " + std::to_string(err - 2000));
     }
 }
@@ -1381,6 +1386,7 @@ void Session::reset(int max_steps, int trace_full) {
         dset(st->down_cnt, 0, 4ull * (dm_.Hp / 32), "reset");
     }
     h2d(ctl_.step, &zero, 4, "reset");
+    host_pos_ = 0;
     // trace buffers
     if (max_steps != max_steps_ || trace_full != trace_full_ || !tr_.step) {
         auto drop = [&](void* p) {
@@ -1609,6 +1615,7 @@ void Session::prefill(const int* tokens, int n) {
         }
         ++steps_;
     }
+    host_pos_ = pos + n;
     sync();
 }
 
@@ -1692,6 +1699,7 @@ void Session::prefill_batched(const int* tokens, int n) {
     ck(launch_pf_handoff(m, st_, pf_, s_comp_), "prefill handoff");
     ck(launch_final(dm_, st_, ctl_, 1, s_comp_), "final");
     steps_ += n;
+    host_pos_ = pos + n;
     sync();
 }
 
@@ -1899,7 +1907,9 @@ void Session::batch_generate(int B, const int* prompts, int P, int n_new, int mo
     // speculative_forward, model.cpp:355-398, speculation.cpp:350-399)
     // resident experts: each step mode is captured once as a CUDA graph (the
     // position and the tokens live on the device; nothing in a step needs the host)
-    const bool use_graph = dev_lists && std::getenv("SMOE_BATCH_NO_GRAPH") == nullptr;
+    // (not under EP: instantiating a graph may wait for the device, which a
+    // peer's combine is spinning on)
+    const bool use_graph = dev_lists && ctl_.ep.world == 1 && std::getenv("SMOE_BATCH_NO_GRAPH") == nullptr;
     bd.pos_dev = use_graph ? bd_pos_ : nullptr;
     auto body = [&](int md) {
         ck(launch_pf_embed(m, bd, s_comp_), "batch embed");
@@ -2046,6 +2056,8 @@ void Session::decode(int mode, int n_steps, int use_graph) {
     int pos = 0;
     d2h(&pos, st_.pos, 4, "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
+    size_attn_grid(pos + n_steps);
+    host_pos_ = pos + n_steps;
     cudaGraphExec_t exec = use_graph ? get_graph(mode) : nullptr;
     ck(cudaEventRecord(ev_origin_, s_comp_), "event");
     for (int i = 0; i < n_steps; ++i) {
@@ -2058,6 +2070,7 @@ void Session::decode(int mode, int n_steps, int use_graph) {
         if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
         ++steps_;
     }
+    dm_.attn_fast_grid = 0;
     sync();
 }
 
@@ -2161,6 +2174,8 @@ void Session::decode_stream(int mode, const int* tokens, int n_steps) {
     d2h(&pos, st_.pos, 4, "pos");
     if (pos + n_steps >= dm_.cap) throw std::invalid_argument("decode: KV capacity exceeded");
     upload_stream(tokens, n_steps);
+    size_attn_grid(pos + n_steps);
+    host_pos_ = pos + n_steps;
     cudaGraphExec_t exec = get_graph(mode, 1);
     ck(cudaEventRecord(ev_origin_, s_comp_), "event");
     for (int i = 0; i < n_steps; ++i) {
@@ -2173,6 +2188,7 @@ void Session::decode_stream(int mode, const int* tokens, int n_steps) {
         if (ev >= 0) ck(cudaEventRecord(ev_step_[2 * ev + 1], s_comp_), "event");
         ++steps_;
     }
+    dm_.attn_fast_grid = 0;
     sync();
 }
 
@@ -2180,6 +2196,10 @@ int Session::step_host(int mode, int token, float* logits_out) {
     if (token < 0 || token >= cfg_.V) throw std::invalid_argument("forward_decode: token out of vocab");
     if (mode == 1 && pred_kind_ == kNone)
         throw std::invalid_argument("offloaded decode: prefetch mode needs a predictor");
+    // host mirror of the position (no device read on this path); if it is
+    // stale the grid is only suboptimal, never wrong
+    size_attn_grid(std::min(host_pos_ + 64, dm_.cap - 1));
+    ++host_pos_;
     cudaGraphExec_t exec = get_graph(mode);
     h_token_[0] = token;
     ck(cudaMemcpyAsync(st_.token, h_token_, 4, cudaMemcpyHostToDevice, s_comp_), "token H2D");
@@ -2187,6 +2207,7 @@ int Session::step_host(int mode, int token, float* logits_out) {
         ck(cudaGraphLaunch(exec, s_comp_), "graph launch");
     else
         enqueue_step(mode, 0, 1, 0, s_comp_);
+    dm_.attn_fast_grid = 0;
     ck(cudaMemcpyAsync(h_logits_, st_.logits, 4ull * cfg_.V, cudaMemcpyDeviceToHost, s_comp_), "logits D2H");
     ck(cudaMemcpyAsync(h_token_ + 1, st_.token, 4, cudaMemcpyDeviceToHost, s_comp_), "token D2H");
     ck(cudaStreamSynchronize(s_comp_), "step");
@@ -2249,9 +2270,23 @@ void Session::calibrate(long long ntok, uint64_t seed, int seq_len, float* d_out
 
 int Session::steps_done() { return steps_; }
 
+// Tolerance-mode attention grid for decode steps that reach position
+// `pos_end`: the power of two >= the CTAs the positions need (64 per CTA), so
+// a short context does not launch (and wait for) the capacity's 296 CTAs.
+// Any grid is correct (the kernel spreads the positions over the CTAs it
+// has); graphs are cached per grid.
+void Session::size_attn_grid(int pos_end) {
+    if (!dm_.fast) return;
+    const int need = (pos_end + 1 + 63) / 64;
+    int b = 1;
+    while (b < need && b < 296) b *= 2;
+    dm_.attn_fast_grid = std::min(b, 296);
+}
+
 cudaGraphExec_t Session::get_graph(int mode, int stream) {
     if (host_ordered_) return nullptr;  // the step syncs on the host mid-pass: no graphs
-    const long long key = mode * 10 + 1 + (stream ? 100 : 0);
+    const long long base = mode * 10 + 1 + (stream ? 100 : 0);
+    const long long key = base + 1000LL * (dm_.fast ? dm_.attn_fast_grid : 0);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;
     sync();
@@ -2261,7 +2296,7 @@ cudaGraphExec_t Session::get_graph(int mode, int stream) {
     ck(cudaStreamBeginCapture(s_comp_, cudaStreamCaptureModeThreadLocal), "capture");
     enqueue_step(mode, 0, 1, 0, s_comp_, stream);
     ck(cudaStreamEndCapture(s_comp_, &g), "capture");
-    graph_kernels_[key] = static_cast<int>(launch_counter() - before);
+    graph_kernels_[base] = static_cast<int>(launch_counter() - before);
     ck(cudaGraphInstantiate(&exec, g, 0), "instantiate");
     cudaGraphDestroy(g);
     graphs_[key] = exec;

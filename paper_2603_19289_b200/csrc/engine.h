@@ -398,6 +398,8 @@ private:
     std::map<long long, cudaGraphExec_t> graphs_;
     std::map<long long, int> graph_kernels_;
     cudaGraphExec_t get_graph(int mode, int stream = 0);
+    void size_attn_grid(int pos_end);
+    int host_pos_ = 0;  // position mirror for step_host's attention grid (advisory)
     int* d_stream_ = nullptr;
     // timeline recording (decode_timeline): event pairs per (step, layer, phase)
     struct TlRec {

@@ -2663,7 +2663,8 @@ cudaError_t launch_qkv(const DevModel& m, const DevState& st, int layer, cudaStr
 cudaError_t launch_attn(const DevModel& m, const DevState& st, double* scratch, int layer,
                         cudaStream_t s) {
     if (attn_fast_ok(m)) {  // tolerance mode: flash-decoding split over positions
-        const int g = static_cast<int>(std::min<long long>(kAttnFastCtas, std::max(1, m.cap / kAttnFastChunk)));
+        const int gcap = static_cast<int>(std::min<long long>(kAttnFastCtas, std::max(1, m.cap / kAttnFastChunk)));
+        const int g = m.attn_fast_grid > 0 ? std::min(m.attn_fast_grid, gcap) : gcap;
         PDL(k_attn_fast, g, kAttnFastThreads, attn_fast_smem(m), s, m, st, scratch, layer);
         return counted(1);
     }

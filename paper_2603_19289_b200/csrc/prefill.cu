@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(32) k_pf_ep_wait(DevEP ep, int layer, int* err
         if (v >= want) break;
         if (*(volatile int*)error) break;
         if (clock64() - t0 > spin_limit) {
-            atomicCAS(error, 0, 4000 + layer);  // EP batched combine: a peer never arrived
+            atomicCAS(error, 0, 5000 + layer);  // EP batched combine: a peer never arrived
             break;
         }
         __nanosleep(64);

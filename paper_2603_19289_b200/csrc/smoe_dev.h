@@ -98,6 +98,8 @@ struct DevModel {
     long long attn_spin;
     int ffn_fused;      // expert FFN as one launch (k_ffn) when its grid is co-resident
     int ffn_cs_fused;   // tolerance mode: expert FFN as one launch (k_ffn_cs) when co-resident
+    int attn_fast_grid; // tolerance-mode attention CTAs (0: sized for the KV capacity); any value is
+                        // correct, the host sizes it for the positions a decode call reaches
 };
 
 // Per-stream decode state (the main stream, and the Oracle's shadow stream).
