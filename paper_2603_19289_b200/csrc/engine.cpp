@@ -2346,6 +2346,9 @@ void Session::profile_kernels(int reps, double* out) {
     cudaEvent_t a, b;
     ck(cudaEventCreate(&a), "event");
     ck(cudaEventCreate(&b), "event");
+    int pos = 0;
+    d2h(&pos, st_.pos, 4, "pos");
+    size_attn_grid(pos);  // the attention grid a decode step at this position launches
     for (int k = 0; k < 7; ++k) {
         // warm-up pass
         for (int pass = 0; pass < 2; ++pass) {
@@ -2414,6 +2417,7 @@ void Session::profile_kernels(int reps, double* out) {
             out[8] = 1000.0 * ms / (static_cast<double>(reps) * (L - 1));
         }
     }
+    dm_.attn_fast_grid = 0;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     sync();
