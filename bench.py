@@ -188,6 +188,32 @@ def hbm_bytes_per_token(c: dict, P: int) -> dict:
 
 # ------------------------------------------------------------------ ours -----
 
+def _launch_ceiling(achieved):
+    """What one launch of this size can stream at all: tools/stream_bench.cu
+    times the same 50 MB block per launch (distinct blocks, back-to-back PDL
+    launches) as a plain LDG.128 read and as the production TMA pipe with no
+    arithmetic; the best of those bounds a 50 MB launch (ramp + tail), below
+    the copy-kernel peak.  Static figures from profiles/r02_stream_ceiling.txt."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_stream_ceiling.txt")
+    best = {}
+    try:
+        for line in open(path):
+            parts = line.split()
+            if "GB/s" in parts:
+                gbs = float(parts[parts.index("GB/s") - 1])
+                kind = "ldg" if line.startswith("ldg") else ("tma_no_math" if " none" in line else None)
+                if kind:
+                    best[kind] = max(best.get(kind, 0.0), gbs)
+    except OSError:
+        return None
+    if not best:
+        return None
+    top = max(best.values())
+    return {"ldg_GBps": best.get("ldg"), "tma_no_math_GBps": best.get("tma_no_math"),
+            "frac_of_best": achieved / top if achieved else None,
+            "source": "profiles/r02_stream_ceiling.txt (tools/stream_bench.cu, 16 x 50 MB blocks)"}
+
+
 def run_ours(args, rank: int, world: int) -> dict | None:
     import torch
     from paper_2603_19289_b200 import ModelConfig, Session
@@ -744,7 +770,8 @@ def main():
                      "avg_launch_us_on_demand_form": prof["ffn_gate_up"],
                      "timing": "CUDA events on the compute stream around L back-to-back launches "
                                "(one per layer, distinct weights, 3 repetitions), Session::profile_kernels",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)",
+                     "launch_ceiling": _launch_ceiling(achieved)},
         "kernel_us": prof,
         "decode_modes": _modes_block(args, pf, od, prof, out.get("alt"), gu_bytes, hbm_peak),
         "path": out.get("path"),

@@ -1560,6 +1560,8 @@ __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st
     KTRACE(9, layer);
     const int lane = threadIdx.x & 31;
     const bool early = exec_src != 0;  // prefetch mode: decision published a layer ahead
+    GainRegs gr;  // the MoE norm gain is static: in registers before any wait
+    if (s_from_r) gr.load(m.moe_gain + static_cast<long long>(layer) * m.H, m.H);
     if (early) {
         wait_decision(st, ctl, layer);
     } else {
@@ -1597,7 +1599,7 @@ __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st
         const float scale = rms_scale_from_partials(st.ssq_r + static_cast<long long>(layer) * (m.Hp / 32),
                                                     m.Hp / 32, H, m.eps);
         sg.wait();
-        block_apply_norm(xs, m.moe_gain + static_cast<long long>(layer) * H, H, scale, xs);
+        block_apply_norm_regs(xs, gr, m.moe_gain + static_cast<long long>(layer) * H, H, scale, xs);
     } else {
         sg.add(xs, st.s + static_cast<long long>(layer) * m.Hp, H * 4);
         sg.wait();

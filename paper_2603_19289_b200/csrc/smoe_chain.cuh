@@ -243,6 +243,44 @@ __device__ __forceinline__ void block_apply_norm(const float* v, const float* ga
     __syncthreads();
 }
 
+// The first kGainRegs float4 of a block's share of a static norm gain, loaded
+// into registers before the kernel's dependency wait so the normalisation
+// after it costs no further global round trip (the rest, for n > 4 x 4 x
+// blockDim, is read from global as block_apply_norm does).
+struct GainRegs {
+    static constexpr int kRegs = 4;
+    float4 g[kRegs];
+    __device__ __forceinline__ void load(const float* gain, int n) {
+        const float4* g4 = reinterpret_cast<const float4*>(gain);
+#pragma unroll
+        for (int q = 0; q < kRegs; ++q) {
+            const int i = threadIdx.x + q * blockDim.x;
+            if (i < (n >> 2)) g[q] = __ldg(g4 + i);
+        }
+    }
+};
+
+// block_apply_norm with the gain's first part from registers (same arithmetic).
+__device__ __forceinline__ void block_apply_norm_regs(const float* v, const GainRegs& gr, const float* gain, int n,
+                                                      float scale, float* out) {
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(gain);
+    float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+    for (int q = 0; q < GainRegs::kRegs; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < (n >> 2)) {
+            const float4 t = v4[i], g = gr.g[q];
+            o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z, t.w * scale * g.w);
+        }
+    }
+    for (int i = threadIdx.x + GainRegs::kRegs * blockDim.x; i < (n >> 2); i += blockDim.x) {
+        const float4 t = v4[i], g = g4[i];
+        o4[i] = make_float4(t.x * scale * g.x, t.y * scale * g.y, t.z * scale * g.z, t.w * scale * g.w);
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ unsigned char* align128(unsigned char* p) {
     return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
 }
