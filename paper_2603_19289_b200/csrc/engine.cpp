@@ -678,6 +678,8 @@ void Session::alloc() {
     // during the gate/up phase did not turn those reads into L2 hits)
     m.ffn_fused = std::getenv("SMOE_FUSED_FFN") ? ffn_fused_ok(m, opts_.device) : 0;
     m.ffn_cs_fused = ffn_cs_fused_ok(m, opts_.device);
+    // opt-in (SMOE_FFN_GUD=1): measured slower than k_ffn_gu_cs + k_ffn_down
+    m.ffn_gud = std::getenv("SMOE_FFN_GUD") && std::string(std::getenv("SMOE_FFN_GUD")) == "1";
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
@@ -814,6 +816,7 @@ void Session::alloc() {
         st.quasi = static_cast<float*>(dalloc(4ull * m.Hp));
         st.h = static_cast<float*>(dalloc(4ull * K * m.Hmp));
         st.y = static_cast<float*>(dalloc(4ull * K * m.Hp));
+        st.dpart = static_cast<float*>(dalloc(4ull * K * (m.Hmp / 16) * m.Hp));
         st.logits = static_cast<float*>(dalloc(4ull * m.Vp));
         st.pos = static_cast<int*>(dalloc(4));
         st.token = static_cast<int*>(dalloc(4));

@@ -25,7 +25,7 @@
 // wait and the last CTA exit, in globaltimer ns, min/max over CTAs.
 namespace smoe {
 
-constexpr int kKtKinds = 16, kKtLayers = 128;
+constexpr int kKtKinds = 17, kKtLayers = 128;
 __device__ unsigned long long g_kt[kKtKinds * kKtLayers][4];
 __device__ __forceinline__ unsigned long long kt_now() {
     unsigned long long t;
@@ -1544,6 +1544,7 @@ __device__ __forceinline__ unsigned char* cs_pipe_mem(const DevModel& m) {
 // Gate/up of one (16-row block rb, executed expert i) by the CTA's kCsWarps
 // warps.  `fused`: the down projection runs in the same grid (k_ffn_cs) and
 // waits on gu_done[layer][i], counted here on every exit path.
+template <bool DOWN = false>
 __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                                            int exec_src, int s_from_r, int rb, int i, bool fused, PipeCs& pipe) {
     struct Done {  // a down CTA never waits for a gate/up CTA that left early
@@ -1606,12 +1607,64 @@ __device__ __forceinline__ void gu_cs_unit(const DevModel& m, const DevState& st
     }
     // tolerance mode only (launch_gu); SMOE_FAST is constant 0 in the exact-only object
     const float part = nc > 0 && SMOE_FAST(m) ? pipe.run_fast(tile, nc, xs + c0) : 0.0f;
+    // DOWN (k_ffn_gud): this warp's share of the down block's 16-column slice
+    // [16 rb, 16 rb + 16) — one 1 KB piece per 32-row tile — streams into the
+    // ring right behind the gate/up chunks, before the cross-warp reduction
+    const int nrt = m.Hp / 32, per = (nrt + kCsWarps - 1) / kCsWarps, w = threadIdx.x >> 5;
+    const int t0 = min(nrt, w * per), tn = max(0, min(nrt - t0, per));
+    constexpr int kTpc = PipeCs::kChunkElems / 512;  // 1 KB pieces per ring chunk
+    const int nchd = (tn + kTpc - 1) / kTpc;
+    const uint16_t* dsrc = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems +
+                           static_cast<long long>(t0) * m.Hmp * 32 + rb * 512;
+    if (DOWN && lane == 0)
+        for (int c = 0; c < PipeCs::kS && c < nchd; ++c)
+            pipe.issue_gather(dsrc + static_cast<long long>(c) * kTpc * m.Hmp * 32, static_cast<long long>(m.Hmp) * 32,
+                              min(kTpc, tn - c * kTpc), 512, pipe.ctr + c);
     const float acc = cs_reduce(part, red);
     if (threadIdx.x < 32) {
         const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
-        if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = silu_ref(acc) * up;
+        const float hv = silu_ref(acc) * up;
+        if ((lane & 1) == 0) st.h[static_cast<long long>(i) * m.Hmp + rb * 16 + (lane >> 1)] = hv;
+        if (DOWN && (lane & 1) == 0) xs[lane >> 1] = hv;  // xs is free: every warp is past its sums
     }
     if (fused) __syncthreads();  // h rows written before the count (Done)
+    if (!DOWN || !SMOE_FAST(m)) return;
+    __syncthreads();
+    float hr[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) hr[c] = xs[c];
+    float* out = st.dpart + (static_cast<long long>(i) * (m.Hmp / 16) + rb) * m.Hp + static_cast<long long>(t0) * 32;
+    for (int c = 0; c < nchd; ++c) {
+        const uint32_t cb = pipe.wait_chunk(pipe.ctr + c);
+        const int np = min(kTpc, tn - c * kTpc);
+        for (int p = 0; p < np; ++p) {
+            const uint4 g0 = lds128(cb + p * 1024 + lane * 16), g1 = lds128(cb + p * 1024 + 512 + lane * 16);
+            float a = lo_bf(g0.x) * hr[0];
+            a = a + hi_bf(g0.x) * hr[1];
+            a = a + lo_bf(g0.y) * hr[2];
+            a = a + hi_bf(g0.y) * hr[3];
+            a = a + lo_bf(g0.z) * hr[4];
+            a = a + hi_bf(g0.z) * hr[5];
+            a = a + lo_bf(g0.w) * hr[6];
+            a = a + hi_bf(g0.w) * hr[7];
+            a = a + lo_bf(g1.x) * hr[8];
+            a = a + hi_bf(g1.x) * hr[9];
+            a = a + lo_bf(g1.y) * hr[10];
+            a = a + hi_bf(g1.y) * hr[11];
+            a = a + lo_bf(g1.z) * hr[12];
+            a = a + hi_bf(g1.z) * hr[13];
+            a = a + lo_bf(g1.w) * hr[14];
+            a = a + hi_bf(g1.w) * hr[15];
+            __stcg(out + (c * kTpc + p) * 32 + lane, a);
+        }
+        __syncwarp();
+        if (c + PipeCs::kS < nchd && lane == 0) {
+            const int cn = c + PipeCs::kS;
+            pipe.issue_gather(dsrc + static_cast<long long>(cn) * kTpc * m.Hmp * 32, static_cast<long long>(m.Hmp) * 32,
+                              min(kTpc, tn - cn * kTpc), 512, pipe.ctr + cn);
+        }
+    }
+    pipe.ctr += nchd;
 }
 
 __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevState st, DevCtl ctl, int layer,
@@ -1619,6 +1672,73 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gu_cs(DevModel m, DevStat
     PipeCs pipe;  // one ring per warp (its mbarriers are initialised once per launch)
     pipe.init(cs_pipe_mem(m), kL2EvictFirst);
     gu_cs_unit(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false, pipe);
+}
+
+// Tolerance-mode expert FFN on one GPU as two launches without a cross-CTA
+// wait between gate/up and down: CTA (rb, i) computes the 16 h values of
+// rows [16 rb, 16 rb + 16) of expert i (as k_ffn_gu_cs) and then the down
+// projection's partial over exactly those 16 columns of h for all H rows,
+// its 16-column slice of the down block (Hp/32 pieces of 1 KB) streamed
+// through the same per-warp ring right behind the gate/up chunks.  So the
+// layer's 75 MB of expert weights stream in ONE launch with no CTA waiting
+// for another; k_down_reduce then sums the Hmp/16 partials of each row in
+// slice order (deterministic), mixes the experts in decision order
+// (model.cpp:297-301) and adds the residual, like k_ffn_down's epilogue.
+// Opt-in (SMOE_FFN_GUD=1): the fused launch streams its 75 MB in ~15 µs
+// (5.0 TB/s, vs 9.9 + 7.5 µs for the pair), but the reduction launch costs
+// ~4 µs after it (device timeline), so the layer is ~1 µs slower.
+__global__ void __launch_bounds__(32 * kCsWarps) k_ffn_gud(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                          int exec_src, int s_from_r) {
+    PipeCs pipe;
+    pipe.init(cs_pipe_mem(m), kL2EvictFirst);
+    gu_cs_unit<true>(m, st, ctl, layer, exec_src, s_from_r, blockIdx.x, blockIdx.y, false, pipe);
+}
+
+__global__ void __launch_bounds__(32 * kMaxK) k_down_reduce(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                            int exec_src) {
+    KTRACE(16, layer);
+    __shared__ float ys[kMaxK][32];
+    pdl_wait();
+    KT_WAITED();
+    pdl_trigger();
+    const int K = m.K, q = threadIdx.x >> 5, lane = threadIdx.x & 31, rb = blockIdx.x, j = rb * 32 + lane;
+    const int ncb = m.Hmp / 16;
+    if (*(volatile int*)ctl.error) return;
+    // warp 0's mixture inputs, loaded up front (independent of the partial sums)
+    const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
+    float gv[kMaxK], rv = 0.0f;
+    if (q == 0) {
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) gv[k] = k < K ? __ldcg(gts + k) : 0.0f;
+        if (j < m.H) rv = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j);
+    }
+    if (q < K) {
+        const float* p = st.dpart + static_cast<long long>(q) * ncb * m.Hp + j;
+        float y = 0.0f;
+        for (int c0 = 0; c0 < ncb; c0 += 64) {  // 64 loads in flight (one L2 round trip), then the sum in order
+            float v[64];
+#pragma unroll
+            for (int u = 0; u < 64; ++u) v[u] = c0 + u < ncb ? __ldcg(p + static_cast<long long>(c0 + u) * m.Hp) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < 64; ++u)
+                if (c0 + u < ncb) y = y + v[u];
+        }
+        ys[q][lane] = y;
+        if (j < m.H) st.y[static_cast<long long>(q) * m.Hp + j] = y;
+    }
+    __syncthreads();
+    if (q != 0) return;
+    float xv = 0.0f;
+    if (j < m.H) {
+        float out = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k)
+            if (k < K) out += gv[k] * ys[k][lane];
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        xv = rv + out;
+        st.x[j] = xv;
+    }
+    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
 }
 
 __device__ __forceinline__ void down_block_epilogue(const DevModel& m, const DevState& st, const float* gts,
@@ -2628,6 +2748,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
                          (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
                          (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast, (const void*)k_ffn_gu_cs,
+                         (const void*)k_ffn_gud, (const void*)k_down_reduce,
                          (const void*)k_xp_unpack, (const void*)k_ffn_cs};
     for (const void* f : fns) {
         cudaFuncAttributes a;
@@ -2653,6 +2774,7 @@ cudaError_t preload_kernels() {
     if ((e = set_smem((const void*)k_attn_fast, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gu_cs, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn_gud, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_cs, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
@@ -2728,6 +2850,11 @@ cudaError_t launch_estimator(const DevModel& m, const DevState& st, const DevCtl
 
 cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl, int layer,
                        cudaStream_t s, int exec_src, int s_from_r) {
+    if (ctl.ep.world == 1 && m.fast && m.ffn_gud) {  // tolerance mode, one GPU (k_ffn_gud)
+        PDL(k_ffn_gud, dim3(m.Hmp / 16, m.K), 32 * kCsWarps, gu_cs_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
+        PDL(k_down_reduce, m.Hp / 32, 32 * m.K, 0, s, m, st, ctl, layer, exec_src);
+        return counted(2);
+    }
     if (ctl.ep.world == 1 && m.fast && m.ffn_cs_fused) {  // tolerance mode: one launch per layer
         PDL(k_ffn_cs, (m.Hmp / 16) * m.K, 32 * kCsWarps, gu_cs_smem(m), s, m, st, ctl, layer, exec_src, s_from_r);
         return counted(1);

@@ -510,6 +510,26 @@ struct WarpPipe {
             bulk_g2s(buf + st * kChunkElems, tile + static_cast<long long>(c0) * 32, bytes, &full[st]);
     }
 
+    // Chunk g (absolute ring index, continuing ctr) as a gather of n pieces of
+    // `piece` elements, piece p from src + p * stride, into consecutive places
+    // of the chunk; one lane issues.
+    __device__ void issue_gather(const WT* src, long long stride, int n, int piece, int g) {
+        const int st = g % S;
+        const uint32_t pb = static_cast<uint32_t>(piece) * sizeof(WT);
+        mbar_expect_tx(&full[st], pb * static_cast<uint32_t>(n));
+        for (int p = 0; p < n; ++p) {
+            if (hinted)
+                bulk_g2s_hint(buf + st * kChunkElems + p * piece, src + p * stride, pb, &full[st], policy);
+            else
+                bulk_g2s(buf + st * kChunkElems + p * piece, src + p * stride, pb, &full[st]);
+        }
+    }
+    // Wait for chunk g; returns its shared-window address.
+    __device__ uint32_t wait_chunk(int g) {
+        mbar_wait(&full[g % S], static_cast<uint32_t>((g / S) & 1));
+        return sbuf + (g % S) * kChunkBytes;
+    }
+
     // Issue the first chunks of `tile` before the input vector exists (weights
     // are independent of the activations), so the first wait finds data.
     __device__ void prime(const WT* tile, int cols) {

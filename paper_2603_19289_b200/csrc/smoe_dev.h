@@ -98,6 +98,7 @@ struct DevModel {
     long long attn_spin;
     int ffn_fused;      // expert FFN as one launch (k_ffn) when its grid is co-resident
     int ffn_cs_fused;   // tolerance mode: expert FFN as one launch (k_ffn_cs) when co-resident
+    int ffn_gud;        // tolerance mode, one GPU: gate/up + column-split down (k_ffn_gud + k_down_reduce)
     int attn_fast_grid; // tolerance-mode attention CTAs (0: sized for the KV capacity); any value is
                         // correct, the host sizes it for the positions a decode call reaches
 };
@@ -126,6 +127,7 @@ struct DevState {
     float* est_xn;     // [dm] gain*xhat + bias
     float* h;          // [K][Hmp]
     float* y;          // [K][Hp]  raw expert outputs (decision order)
+    float* dpart;      // [K][Hmp/16][Hp] tolerance-mode down partials per 16-column slice of h
     float* logits;     // [V]
     int* pos;          // position
     int* token;        // current token

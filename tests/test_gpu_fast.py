@@ -130,3 +130,18 @@ def test_fast_mode_one_launch_ffn_toy(lib, monkeypatch):
     gate/up units then claimed down items in one grid, same tolerance."""
     monkeypatch.setenv("SMOE_FFN_CS_FUSED", "1")
     _run(TOY, 12, 16, 0.5, 64, "toy_ffn_cs")
+
+
+def test_fast_mode_column_split_down_toy(lib, monkeypatch):
+    """The opt-in gate/up + column-split down path (k_ffn_gud + k_down_reduce,
+    SMOE_FFN_GUD=1): each gate/up CTA also computes the down partial over its
+    16 columns of h; the partials are summed in slice order. Same tolerance."""
+    monkeypatch.setenv("SMOE_FFN_GUD", "1")
+    _run(TOY, 12, 16, 0.5, 64, "toy_ffn_gud")
+
+
+def test_fast_mode_column_split_down_q30_layers(lib, monkeypatch):
+    """The same at the Q30 layer shape (Hm 768: 48 column slices, the 64-wide
+    in-flight batches of the reduction), two layers, offloaded prefetch."""
+    monkeypatch.setenv("SMOE_FFN_GUD", "1")
+    _run(dict(Q30, layers=2), 10, 8, 0.25, 64, "q30_L2_ffn_gud")

@@ -21,7 +21,7 @@ from paper_2603_19289_b200 import ModelConfig, Session  # noqa: E402
 
 KINDS = {14: "l2_pf", 0: "embed", 1: "qkv", 2: "attn", 3: "wo", 4: "router", 5: "est0", 6: "est1", 7: "est2",
          8: "est3", 9: "ffn_gu", 10: "ffn_down", 11: "ep_mix", 12: "final", 13: "predictor",
-         15: "ffn_fused"}
+         15: "ffn_fused", 16: "down_reduce"}
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 wl = sys.argv[3] if len(sys.argv) > 3 else "greedy"
@@ -52,7 +52,7 @@ for mode in ("prefetch", "on_demand"):
         s.decode_stream(mode, forced[8:9])
     else:
         s.decode(mode, 1, use_graph=use_graph)
-    buf = np.zeros((16 * 128, 4), np.uint64)
+    buf = np.zeros((17 * 128, 4), np.uint64)
     lib.smoe_ktrace_read(buf.ctypes.data)
     t0 = min(int(r[0]) for r in buf if r[0] != np.uint64(~np.uint64(0)) and r[2] > 0)
     print(f"== {mode} ({wl}, cache {frac}, L={L}) step {float(s.token_ms()[-1]):.3f} ms ==")
