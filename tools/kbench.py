@@ -22,12 +22,12 @@ s.set_predictor("router-pf")
 s.preload_all()
 if os.environ.get("SMOE_DECODE_MODE"):
     s.set_decode_mode(os.environ["SMOE_DECODE_MODE"])
-s.reset(64, False)
-s.prefill(list(range(32)))
+s.reset(max(64, int(os.environ.get("KB_PROMPT", "32")) + 16), False)
+s.prefill([t % 256 for t in range(int(os.environ.get("KB_PROMPT", "32")))])
 s.decode("prefetch", 2)  # predicted decisions of every layer in place (prefetch-form timing)
 for _ in range(2):
     p = s.profile_kernels(reps=5)
-s.reset(64, False)
+s.reset(max(64, int(os.environ.get("KB_PROMPT", "32")) + 16), False)
 s.prefill(list(range(32)))
 s.decode("prefetch", 4)
 s.decode("prefetch", 16)
