@@ -910,7 +910,13 @@ using PipeB = WarpPipe<uint16_t, kS, kCCb>;
 using PipeGU = WarpPipe<uint16_t, SMOE_GU_STAGES, SMOE_GU_CC>;  // expert gate/up: deeper HBM stream per warp
 using PipeBL = WarpPipe<uint16_t, kS, 256>;  // 16 KB chunks: few-CTA kernels (qkv, router, final)
 using PipeF = WarpPipe<float, kS, kCCf>;
-using PipeD = WarpPipe<uint16_t, kS, kCCd>;
+#ifndef SMOE_D_STAGES
+#define SMOE_D_STAGES kS
+#endif
+#ifndef SMOE_D_CC
+#define SMOE_D_CC kCCd
+#endif
+using PipeD = WarpPipe<uint16_t, SMOE_D_STAGES, SMOE_D_CC>;
 using PipeR = WarpPipe<uint16_t, 3, 256>;  // router: 48 KB, fits beside three k_ffn_gu CTAs
 
 // -------------------------------------------------------------- decision --
