@@ -680,6 +680,8 @@ void Session::alloc() {
     m.ffn_cs_fused = ffn_cs_fused_ok(m, opts_.device);
     // opt-in (SMOE_FFN_GUD=1): measured slower than k_ffn_gu_cs + k_ffn_down
     m.ffn_gud = std::getenv("SMOE_FFN_GUD") && std::string(std::getenv("SMOE_FFN_GUD")) == "1";
+    // tolerance-mode down as one CTA per row block (k_ffn_down_rb; SMOE_DOWN_RB=0: k_ffn_down)
+    m.down_rb = down_rb_ok(m) && !(std::getenv("SMOE_DOWN_RB") && std::string(std::getenv("SMOE_DOWN_RB")) == "0");
 
     ck(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");

@@ -1976,6 +1976,79 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
 #endif
 }
 
+// Tolerance-mode down projection, one GPU (the default when its shared memory
+// fits: Q30 152 KB): CTA rb owns the 32-row block rb of
+// ALL k executed experts (warp q: expert q's 48 KB tile through its own 2 x 8
+// KB ring, primed before the PDL wait), so the mixture in decision order
+// (model.cpp:297-301), the residual and the rms partial of x are formed in
+// shared memory — no y round trip through global memory, no device-scope
+// fence / arrival counter as k_ffn_down's last-of-k CTA needs.
+__global__ void __launch_bounds__(32 * kMaxK) k_ffn_down_rb(DevModel m, DevState st, DevCtl ctl, int layer,
+                                                           int exec_src) {
+    KTRACE(10, layer);
+    const int K = m.K, Hmp = m.Hmp, q = threadIdx.x >> 5, lane = threadIdx.x & 31, rb = blockIdx.x;
+    const int j = rb * 32 + lane;
+    __shared__ float ys[kMaxK][32];
+    float* hs = reinterpret_cast<float*>(g_smem) + static_cast<long long>(q) * Hmp;  // [K][Hmp]
+    unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(reinterpret_cast<float*>(g_smem) + K * Hmp)) +
+                              q * round_up(PipeCs::kBytes, 128);
+    const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
+    const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
+    // ids / slot_of are final once every gate/up CTA passed its copy wait (its PDL trigger)
+    const int e = __ldcg(ids + q);
+    const int slot = __ldcg(m.slot_of + layer * m.E + e);
+    PipeCs pipe;
+    pipe.init(pipe_mem, kL2EvictFirst);
+    const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems +
+                           static_cast<long long>(rb) * Hmp * 32;
+    if (slot >= 0) pipe.prime(tile, m.Hm);
+    pdl_wait();
+    KT_WAITED();
+    pdl_trigger();
+    if (__syncthreads_or(*(volatile int*)ctl.error)) return;
+    if (slot < 0) {  // (per warp) report; the warp contributes 0 and the CTA finishes together
+        if (lane == 0) atomicCAS(ctl.error, 0, 2000 + layer);
+    }
+    float gv = 0.0f, rv = 0.0f;
+    if (q == 0) {
+        if (lane < K) gv = __ldcg(gts + lane);
+        if (j < m.H) rv = __ldcg(st.r + static_cast<long long>(layer) * m.Hp + j);
+    }
+    float y = 0.0f;
+    if (slot >= 0) {
+        // h (k_ffn_gu_cs's rows of expert q, L2-resident): 16-byte loads, all in flight
+        const float4* h4 = reinterpret_cast<const float4*>(st.h + static_cast<long long>(q) * Hmp);
+        for (int t0 = 0; t0 < Hmp / 4; t0 += 8 * 32) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * 32 + lane;
+                if (t < Hmp / 4) v[u] = __ldcg(h4 + t);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * 32 + lane;
+                if (t < Hmp / 4) reinterpret_cast<float4*>(hs)[t] = v[u];
+            }
+        }
+        __syncwarp();
+        y = SMOE_FAST(m) ? pipe.run_fast(tile, m.Hm, hs) : 0.0f;
+        if (j < m.H) st.y[static_cast<long long>(q) * m.Hp + j] = y;
+    }
+    ys[q][lane] = y;
+    __syncthreads();
+    if (q != 0) return;
+    float out = 0.0f;
+    for (int k = 0; k < K; ++k) out += __shfl_sync(0xffffffffu, gv, k) * ys[k][lane];
+    float xv = 0.0f;
+    if (j < m.H) {
+        st.m[static_cast<long long>(layer) * m.Hp + j] = out;
+        xv = rv + out;
+        st.x[j] = xv;
+    }
+    warp_ssq_partial(xv, st.ssq_x + static_cast<long long>(layer + 1) * (m.Hp / 32) + rb);
+}
+
 __global__ void __launch_bounds__(32) k_ffn_down(DevModel m, DevState st, DevCtl ctl, int layer,
                                                  int exec_src) {
     ffn_down_body(m, st, ctl, layer, exec_src, blockIdx.x, blockIdx.y, false, 0);
@@ -2620,6 +2693,9 @@ cudaError_t launch_gu(const DevModel& m, const DevState& st, const DevCtl& ctl, 
 }
 size_t ffn_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeGU::kBytes; }
 size_t down_smem(const DevModel& m) { return 128 + static_cast<size_t>(m.Hmp) * 4 + 128 + PipeD::kBytes; }
+size_t down_rb_smem(const DevModel& m) {
+    return static_cast<size_t>(m.K) * m.Hmp * 4 + 128 + static_cast<size_t>(m.K) * round_up(PipeCs::kBytes, 128);
+}
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
     size_t b = 256 + kMaxD * 4 + 2ull * kAttnChunk * (2 * m.D + 4) * 4;
@@ -2697,6 +2773,8 @@ int ffn_cs_fused_ok(const DevModel& m, int device) {
     return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
 }
 
+int down_rb_ok(const DevModel& m) { return m.K <= kMaxK && down_rb_smem(m) <= 200 * 1024 ? 1 : 0; }
+
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), ffn_smem(m), down_smem(m),
                   final_smem(m), attn_smem(m)};
@@ -2748,7 +2826,7 @@ cudaError_t preload_kernels() {
                          (const void*)k_ep_mix, (const void*)k_quasi_rd, (const void*)k_l2_prefetch,
                          (const void*)k_ffn, (const void*)k_ffn_gu_w<2>, (const void*)k_ffn_gu_w<3>,
                          (const void*)k_ffn_gu_w<4>, (const void*)k_attn_fast, (const void*)k_ffn_gu_cs,
-                         (const void*)k_ffn_gud, (const void*)k_down_reduce,
+                         (const void*)k_ffn_gud, (const void*)k_down_reduce, (const void*)k_ffn_down_rb,
                          (const void*)k_xp_unpack, (const void*)k_ffn_cs};
     for (const void* f : fns) {
         cudaFuncAttributes a;
@@ -2775,6 +2853,7 @@ cudaError_t preload_kernels() {
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gu_cs, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gud, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn_down_rb, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_cs, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
@@ -2867,6 +2946,10 @@ cudaError_t launch_ffn(const DevModel& m, const DevState& st, const DevCtl& ctl,
         const cudaError_t e = launch_gu(m, st, ctl, layer, exec_src, s_from_r, s);
         if (e != cudaSuccess) return e;
     }
+    if (ctl.ep.world == 1 && m.fast && m.down_rb) {
+        PDL(k_ffn_down_rb, m.Hp / 32, 32 * m.K, down_rb_smem(m), s, m, st, ctl, layer, exec_src);
+        return counted(2);
+    }
     PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, exec_src);
     if (ctl.ep.world > 1) {
         PDL(k_ep_mix, m.Hp / 32, 32, 0, s, m, st, ctl, layer, exec_src);
@@ -2885,6 +2968,8 @@ cudaError_t launch_ffn_part(const DevModel& m, const DevState& st, const DevCtl&
     if (part == 0 || part == 2) {
         const cudaError_t e = launch_gu(m, st, ctl, layer, part == 2, part == 2, s);
         if (e != cudaSuccess) return e;
+    } else if (ctl.ep.world == 1 && m.fast && m.down_rb) {
+        PDL(k_ffn_down_rb, m.Hp / 32, 32 * m.K, down_rb_smem(m), s, m, st, ctl, layer, 0);
     } else {
         PDL(k_ffn_down, dim3(m.Hp / 32, m.K), 32, down_smem(m), s, m, st, ctl, layer, 0);
     }

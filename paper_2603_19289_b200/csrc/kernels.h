@@ -197,6 +197,8 @@ cudaError_t launch_pf_final(const DevModel& m, const PrefillDev& pf, cudaStream_
 cudaError_t launch_pf_handoff(const DevModel& m, const DevState& st, const PrefillDev& pf, cudaStream_t s);
 
 int max_dynamic_smem_needed(const DevModel& m);
+// k_ffn_down_rb's shared memory (K rings + K staged h vectors) fits one CTA
+int down_rb_ok(const DevModel& m);
 std::string kernel_limit_violation(const DevModel& m);     // "" when every kernel fits
 std::string estimator_limit_violation(const DevModel& m);  // after the estimator dims are set
 int attn_grid_for(const DevModel& m, int device);

@@ -99,6 +99,7 @@ struct DevModel {
     int ffn_fused;      // expert FFN as one launch (k_ffn) when its grid is co-resident
     int ffn_cs_fused;   // tolerance mode: expert FFN as one launch (k_ffn_cs) when co-resident
     int ffn_gud;        // tolerance mode, one GPU: gate/up + column-split down (k_ffn_gud + k_down_reduce)
+    int down_rb;        // tolerance mode, one GPU: down as one CTA per row block, K warps (k_ffn_down_rb)
     int attn_fast_grid; // tolerance-mode attention CTAs (0: sized for the KV capacity); any value is
                         // correct, the host sizes it for the positions a decode call reaches
 };

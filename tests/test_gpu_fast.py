@@ -145,3 +145,17 @@ def test_fast_mode_column_split_down_q30_layers(lib, monkeypatch):
     in-flight batches of the reduction), two layers, offloaded prefetch."""
     monkeypatch.setenv("SMOE_FFN_GUD", "1")
     _run(dict(Q30, layers=2), 10, 8, 0.25, 64, "q30_L2_ffn_gud")
+
+
+def test_fast_mode_per_expert_down_toy(lib, monkeypatch):
+    """The previous down projection (k_ffn_down: one warp per (row block,
+    expert), last-of-k CTA mixes; SMOE_DOWN_RB=0) next to the default
+    row-block kernel (k_ffn_down_rb) the other tests run. Same tolerance."""
+    monkeypatch.setenv("SMOE_DOWN_RB", "0")
+    _run(TOY, 12, 16, 0.5, 64, "toy_down_per_expert")
+
+
+def test_fast_mode_per_expert_down_q30_layers(lib, monkeypatch):
+    """The same at the Q30 layer shape, two layers, offloaded prefetch."""
+    monkeypatch.setenv("SMOE_DOWN_RB", "0")
+    _run(dict(Q30, layers=2), 10, 8, 0.25, 64, "q30_L2_down_per_expert")
