@@ -1976,6 +1976,14 @@ __device__ __forceinline__ void ffn_down_body(const DevModel& m, const DevState&
 #endif
 }
 
+#ifndef SMOE_DR_S
+#define SMOE_DR_S 2
+#endif
+#ifndef SMOE_DR_CC
+#define SMOE_DR_CC 128
+#endif
+using PipeDR = WarpPipe<uint16_t, SMOE_DR_S, SMOE_DR_CC>;  // k_ffn_down_rb: per-warp ring (2 x 8 KB)
+
 // Tolerance-mode down projection, one GPU (the default when its shared memory
 // fits: Q30 152 KB): CTA rb owns the 32-row block rb of
 // ALL k executed experts (warp q: expert q's 48 KB tile through its own 2 x 8
@@ -1991,13 +1999,13 @@ __global__ void __launch_bounds__(32 * kMaxK) k_ffn_down_rb(DevModel m, DevState
     __shared__ float ys[kMaxK][32];
     float* hs = reinterpret_cast<float*>(g_smem) + static_cast<long long>(q) * Hmp;  // [K][Hmp]
     unsigned char* pipe_mem = align128(reinterpret_cast<unsigned char*>(reinterpret_cast<float*>(g_smem) + K * Hmp)) +
-                              q * round_up(PipeCs::kBytes, 128);
+                              q * round_up(PipeDR::kBytes, 128);
     const int* ids = (exec_src ? st.id_pred : st.id_exec) + layer * K;
     const float* gts = (exec_src ? st.g_pred : st.g_exec) + layer * K;
     // ids / slot_of are final once every gate/up CTA passed its copy wait (its PDL trigger)
     const int e = __ldcg(ids + q);
     const int slot = __ldcg(m.slot_of + layer * m.E + e);
-    PipeCs pipe;
+    PipeDR pipe;
     pipe.init(pipe_mem, kL2EvictFirst);
     const uint16_t* tile = m.slots + (static_cast<long long>(layer) * m.C + slot) * m.expert_elems + m.gu_elems +
                            static_cast<long long>(rb) * Hmp * 32;
@@ -2694,7 +2702,7 @@ cudaError_t launch_gu(const DevModel& m, const DevState& st, const DevCtl& ctl, 
 size_t ffn_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeGU::kBytes; }
 size_t down_smem(const DevModel& m) { return 128 + static_cast<size_t>(m.Hmp) * 4 + 128 + PipeD::kBytes; }
 size_t down_rb_smem(const DevModel& m) {
-    return static_cast<size_t>(m.K) * m.Hmp * 4 + 128 + static_cast<size_t>(m.K) * round_up(PipeCs::kBytes, 128);
+    return static_cast<size_t>(m.K) * m.Hmp * 4 + 128 + static_cast<size_t>(m.K) * round_up(PipeDR::kBytes, 128);
 }
 size_t final_smem(const DevModel& m) { return 128 + 2 * vec_bytes(m.H) + 128 + PipeBL::kBytes; }
 size_t attn_smem(const DevModel& m) {
@@ -2773,7 +2781,7 @@ int ffn_cs_fused_ok(const DevModel& m, int device) {
     return grid + 16 <= static_cast<long long>(nb) * sms ? 1 : 0;
 }
 
-int down_rb_ok(const DevModel& m) { return m.K <= kMaxK && down_rb_smem(m) <= 200 * 1024 ? 1 : 0; }
+int down_rb_ok(const DevModel& m) { return m.K <= kMaxK && down_rb_smem(m) <= 224 * 1024 ? 1 : 0; }
 
 int max_dynamic_smem_needed(const DevModel& m) {
     size_t v[] = {qkv_smem(m), wo_smem(m), router_smem(m, 0), est_smem(m), ffn_smem(m), down_smem(m),
@@ -2853,7 +2861,7 @@ cudaError_t preload_kernels() {
     if ((e = set_smem((const void*)k_ffn, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gu_cs, 200 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_gud, 200 * 1024)) != cudaSuccess) return e;
-    if ((e = set_smem((const void*)k_ffn_down_rb, 200 * 1024)) != cudaSuccess) return e;
+    if ((e = set_smem((const void*)k_ffn_down_rb, 224 * 1024)) != cudaSuccess) return e;
     if ((e = set_smem((const void*)k_ffn_cs, 200 * 1024)) != cudaSuccess) return e;
     return set_smem((const void*)k_ffn_down, 220 * 1024);
 }
